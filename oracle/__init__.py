@@ -1,0 +1,142 @@
+"""oracle -- TEST INFRASTRUCTURE ONLY.
+
+ctypes wrapper over oracle/oracle.c, the plain fp64 CPU oracle of the J2 /
+distance-row hot path (see oracle.c for the citations of every function).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline and
+``--impl reference`` legs may import this package.  It shares no code with
+paper_1708_02645_b200/ and never imports it.
+
+Parity status: pinned (tests/test_oracle_pins.py); nothing is
+"parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+GCC_FLAGS = ["-O2", "-fno-fast-math", "-ffp-contract=off", "-fPIC", "-shared",
+             "-std=c11", "-pthread"]
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (no SIMD pragmas, no fast-math, no FMA
+    contraction so every product/sum rounds once as written)."""
+    if (not force and os.path.exists(_LIB)
+            and os.path.getmtime(_LIB) >= os.path.getmtime(_SRC)):
+        return _LIB
+    tmp = _LIB + f".tmp{os.getpid()}"
+    subprocess.check_call(["gcc", *GCC_FLAGS, "-o", tmp, _SRC, "-lm"])
+    os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        dp = ctypes.POINTER(ctypes.c_double)
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        i64 = ctypes.c_int64
+        _lib.orc_eval.restype = i64
+        _lib.orc_eval.argtypes = [dp, ctypes.c_double, ctypes.c_int, dp,
+                                  i64, i64, i64, i64, i64, i64,
+                                  dp, i32p, ctypes.c_int32, dp,
+                                  dp, dp, dp, ctypes.c_int]
+        _lib.orc_j2_total.restype = ctypes.c_double
+        _lib.orc_j2_total.argtypes = [dp, ctypes.c_double, ctypes.c_int, dp,
+                                      i64, i64, i64, dp]
+        _lib.orc_bspline_batch.restype = None
+        _lib.orc_bspline_batch.argtypes = [dp, ctypes.c_int, ctypes.c_double, i64, dp, dp]
+        _lib.orc_min_image_batch.restype = None
+        _lib.orc_min_image_batch.argtypes = [dp, i64, dp, dp, dp]
+    return _lib
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+class CoincidentError(ValueError):
+    """r == 0 inside the cutoff (reading R9: undefined; the oracle refuses)."""
+
+
+def eval_j2(R, k, r_trial, fn, n_total: int, n_up: int, i_offset: int = 0,
+            row: bool = False, threads: int = 1, n_local: int | None = None):
+    """Oracle of qj2_eval.
+
+    R: [W][3][Np] (fp32 or fp64; promoted exactly), k: [W] global indices,
+    r_trial: [W][P][3], fn: qmcgen.Functor-like (L, r_cut, m, coef[2][m+3]).
+    Returns (out[W][P][5], abs[W][P][5], row[W][P][4][Np] or None), fp64.
+    """
+    R = _f64(R)
+    W, three, Np = R.shape
+    assert three == 3
+    N_local = min(Np, n_total - i_offset) if n_local is None else int(n_local)
+    rt = _f64(r_trial)
+    P = rt.shape[1]
+    k = np.ascontiguousarray(np.asarray(k, dtype=np.int32))
+    L = _f64(fn.L)
+    coef = _f64(fn.coef)
+    out = np.zeros((W, P, 5))
+    absout = np.zeros((W, P, 5))
+    rowout = np.full((W, P, 4, Np), np.nan) if row else None
+    st = lib().orc_eval(_dp(L), float(fn.r_cut), int(fn.m), _dp(coef),
+                        W, n_total, n_up, i_offset, N_local, Np,
+                        _dp(R), k.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                        P, _dp(rt), _dp(out), _dp(absout),
+                        _dp(rowout) if row else ctypes.POINTER(ctypes.c_double)(),
+                        int(threads))
+    if st:
+        raise CoincidentError(f"coincident source at (w*P+p) = {st - 1}")
+    return out, absout, rowout
+
+
+def j2_total(R1, n: int, n_up: int, fn) -> float:
+    """Brute-force J2 = sum_{i<j} U(r_ij) of one configuration R1[3][Np]."""
+    R1 = _f64(R1)
+    return lib().orc_j2_total(_dp(_f64(fn.L)), float(fn.r_cut), int(fn.m),
+                              _dp(_f64(fn.coef)), n, n_up, R1.shape[1], _dp(R1))
+
+
+def bspline(coef_channel, m: int, r_cut: float, r) -> np.ndarray:
+    """[n][3] = (U, U', U'') of one channel at distances r."""
+    r = _f64(np.atleast_1d(r))
+    c = _f64(coef_channel)
+    out = np.zeros((r.size, 3))
+    lib().orc_bspline_batch(_dp(c), int(m), float(r_cut), r.size, _dp(r), _dp(out))
+    return out
+
+
+def min_image(L, a, b) -> np.ndarray:
+    """[n][4] = (dist, dx, dy, dz) of b - a wrapped (a, b: [n][3])."""
+    a = _f64(np.atleast_2d(a))
+    b = _f64(np.atleast_2d(b))
+    out = np.zeros((a.shape[0], 4))
+    lib().orc_min_image_batch(_dp(_f64(L)), a.shape[0], _dp(a), _dp(b), _dp(out))
+    return out
+
+
+def normalized_error(gpu, orc, absout, fn) -> np.ndarray:
+    """Parity metric (reading R14): per component
+    |s_gpu - s_orc| / max(A_s, F_s), F = max|c| (V), max|c|/delta (G),
+    max|c|/delta^2 (L)."""
+    cmax = float(np.max(np.abs(fn.coef)))
+    delta = fn.r_cut / fn.m
+    F = np.array([cmax, cmax / delta, cmax / delta, cmax / delta, cmax / delta ** 2])
+    denom = np.maximum(absout, F)
+    return np.abs(np.asarray(gpu, dtype=np.float64) - orc) / denom

@@ -1,0 +1,277 @@
+/*
+ * oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct CPU oracle for the hot path of
+ * Mathuriya et al., "Embracing a new era of highly efficient and productive
+ * quantum Monte Carlo simulations" (SC'17, arXiv 1708.02645): the on-the-fly
+ * electron-electron distance row and the two-body Jastrow (J2) value,
+ * gradient and Laplacian of a particle-by-particle move.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference leg may load this library.  The product path
+ * (paper_1708_02645_b200/) shares no code with it and never calls it.
+ *
+ * Citations: PAPER:n is a line of /root/reference/PAPER.md, SPEC:n a line of
+ * /root/reference/SPEC.md (a spec written from the paper; used for
+ * interfaces and test ideas only).  Readings of the paper where it is silent
+ * are numbered R1..R15 as in DESIGN.md.
+ *
+ * Everything is scalar fp64, IEEE round-to-nearest, no SIMD pragmas, sums are
+ * Neumaier-compensated.  Positions given in fp32 are promoted to fp64 exactly
+ * by the caller.
+ *
+ * Parity status: every function here is pinned by tests/test_oracle_pins.py
+ * (closed forms, brute force, finite differences, library B-spline, worked
+ * examples).  Nothing is "parity unpinned".
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <pthread.h>
+
+/* ------------------------------------------------------------------------ */
+/* Compensated (Neumaier) summation.                                         */
+/* ------------------------------------------------------------------------ */
+typedef struct { double s, c; } nsum;
+
+static void nsum_add(nsum *a, double x)
+{
+    double t = a->s + x;
+    if (fabs(a->s) >= fabs(x)) a->c += (a->s - t) + x;
+    else                       a->c += (x - t) + a->s;
+    a->s = t;
+}
+static double nsum_get(const nsum *a) { return a->s + a->c; }
+
+/* ------------------------------------------------------------------------ */
+/* Minimum-image displacement b - a on an orthorhombic, fully periodic cell.  */
+/* SPEC:113-121 (min_image_disp: "displacement = b - a wrapped to nearest     */
+/* image"), SPEC:138 ("disp_d in (-L_d/2, L_d/2]").  Reading R7.              */
+/* The paper's row is d(k,i) = |r_i - r_k|, dr(k,i) = r_i - r_k (PAPER:1300-  */
+/* 1301), so the oracle is called with a = trial position, b = source i.      */
+/* ------------------------------------------------------------------------ */
+void orc_min_image(const double L[3], const double a[3], const double b[3],
+                   double d[3], double *dist)
+{
+    double s = 0.0;
+    for (int c = 0; c < 3; ++c) {
+        double t = b[c] - a[c];
+        if (t > 0.5 * L[c])        t -= L[c];
+        else if (t <= -0.5 * L[c]) t += L[c];
+        d[c] = t;
+        s += t * t;
+    }
+    *dist = sqrt(s);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Uniform cubic B-spline radial functor U(r), U'(r), U''(r).                 */
+/* PAPER:817-819 ("The one-dimensional cubic B-spline is extensively used"),  */
+/* SPEC:256-258 (CubicBspline1D: r_cut, m intervals, delta = r_cut/m, m+3     */
+/* coefficients, zero for r >= r_cut), SPEC:279-287 (functor_eval_vgl).       */
+/* Readings R3 (index/basis convention) and R5 (contribute iff r < r_cut).    */
+/*   t = r/delta, j = min(floor(t), m-1), f = t - j,                          */
+/*   U = sum_a c[j+a] B_a(f),  U' = sum c[j+a] B_a'(f)/delta,                 */
+/*   U'' = sum c[j+a] B_a''(f)/delta^2.                                       */
+/* The tail c[m..m+2] is NOT forced to zero here (closed-form pins use        */
+/* polynomial coefficient sequences); the cutoff test is explicit.            */
+/* ------------------------------------------------------------------------ */
+void orc_bspline(const double *c, int m, double r_cut, double r, double out[3])
+{
+    if (!(r < r_cut)) { out[0] = out[1] = out[2] = 0.0; return; }
+    double delta = r_cut / (double)m;
+    double t = r / delta;
+    int j = (int)floor(t);
+    if (j > m - 1) j = m - 1;
+    if (j < 0) j = 0;
+    double f = t - (double)j;
+    double g = 1.0 - f;
+
+    double B0 = g * g * g / 6.0;
+    double B1 = (3.0 * f * f * f - 6.0 * f * f + 4.0) / 6.0;
+    double B2 = (-3.0 * f * f * f + 3.0 * f * f + 3.0 * f + 1.0) / 6.0;
+    double B3 = f * f * f / 6.0;
+
+    double D0 = -0.5 * g * g;
+    double D1 = 0.5 * (3.0 * f * f - 4.0 * f);
+    double D2 = 0.5 * (-3.0 * f * f + 2.0 * f + 1.0);
+    double D3 = 0.5 * f * f;
+
+    double S0 = 1.0 - f;
+    double S1 = 3.0 * f - 2.0;
+    double S2 = 1.0 - 3.0 * f;
+    double S3 = f;
+
+    out[0] = c[j] * B0 + c[j + 1] * B1 + c[j + 2] * B2 + c[j + 3] * B3;
+    out[1] = (c[j] * D0 + c[j + 1] * D1 + c[j + 2] * D2 + c[j + 3] * D3) / delta;
+    out[2] = (c[j] * S0 + c[j + 1] * S1 + c[j + 2] * S2 + c[j + 3] * S3) / (delta * delta);
+}
+
+/* Spin channel of the pair (i, k): 0 = same spin, 1 = opposite spin.
+ * PAPER:800-801 (N^u = N^d = N/2), SPEC:431 (indices [0,N/2) up, like/unlike
+ * channels).  Reading R6. */
+static int spin_channel(int64_t i, int64_t k, int64_t n_up)
+{
+    return ((i < n_up) == (k < n_up)) ? 0 : 1;
+}
+
+/* ------------------------------------------------------------------------ */
+/* The hot path: for each walker w and trial p, with r = r_trial[w][p],       */
+/*   V  = sum_{i != k, i in slice}  U_s(|d_i|)                                */
+/*   G  = -sum U_s'(|d_i|) d_i / |d_i|                                        */
+/*   L  = sum [U_s''(|d_i|) + 2 U_s'(|d_i|)/|d_i|]                            */
+/* with d_i = minimg(r_i - r).  This is U^2_k of PAPER:1382 ("Two-body        */
+/* Jastrow takes the similar form as Delta J2 = U^2_k(R') - U^2_k(R)"),       */
+/* i.e. one term of Eq. (5), and its gradient and Laplacian   */
+/* with respect to the moved electron (Alg. 1 L8).  Readings R1,   */
+/* R2, R8, R11, R12.  abs_out receives the absolute-term sums                 */
+/* (sum|U|, sum|U' d_c/r|, sum|U''| + 2|U'|/r) used by the parity tolerance.  */
+/*                                                                            */
+/* Sharding: the slice holds global sources [i_offset, i_offset + N_local);   */
+/* R is [W][3][Np] over the slice.  Spin and self-exclusion use global        */
+/* indices.                                                                   */
+/*                                                                            */
+/* row_out (optional) is Fig. 6's temporary row v:          */
+/* [W][P][4][Np] = (r, dx, dy, dz); slot k and padding are left untouched.    */
+/*                                                                            */
+/* Returns 0, or 1 + (flat index w*P+p) of the first coincident pair          */
+/* (r == 0 inside the cutoff: reading R9, undefined, the oracle refuses).     */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    const double *L; double r_cut; int m; const double *coef; /* [2][m+3] */
+    int64_t W, N_total, N_up, i_offset, N_local, Np;
+    const double *R; const int32_t *k; int32_t P; const double *r_trial;
+    double *out; double *abs_out; double *row_out;
+    int64_t w_begin, w_end;
+    int64_t status;
+} orc_job;
+
+static int64_t eval_walkers(orc_job *J)
+{
+    const int mc = J->m + 3;
+    for (int64_t w = J->w_begin; w < J->w_end; ++w) {
+        const double *Rw = J->R + w * 3 * J->Np;
+        int64_t kw = J->k[w];
+        for (int32_t p = 0; p < J->P; ++p) {
+            const double *rt = J->r_trial + (w * J->P + p) * 3;
+            nsum V = {0, 0}, G[3] = {{0, 0}, {0, 0}, {0, 0}}, Lp = {0, 0};
+            nsum AV = {0, 0}, AG[3] = {{0, 0}, {0, 0}, {0, 0}}, AL = {0, 0};
+            double *row = J->row_out ? J->row_out + ((w * J->P + p) * 4) * J->Np : NULL;
+            for (int64_t il = 0; il < J->N_local; ++il) {
+                int64_t i = J->i_offset + il;          /* global index */
+                if (i == kw) continue;                 /* i != k, Eq. (5) */
+                double src[3] = { Rw[il], Rw[J->Np + il], Rw[2 * J->Np + il] };
+                double d[3], rho;
+                orc_min_image(J->L, rt, src, d, &rho);
+                if (row) {
+                    row[il] = rho;
+                    row[J->Np + il] = d[0];
+                    row[2 * J->Np + il] = d[1];
+                    row[3 * J->Np + il] = d[2];
+                }
+                if (!(rho < J->r_cut)) continue;       /* finite cutoff */
+                if (rho == 0.0) return 1 + w * J->P + p;
+                int s = spin_channel(i, kw, J->N_up);
+                double u[3];
+                orc_bspline(J->coef + s * mc, J->m, J->r_cut, rho, u);
+                nsum_add(&V, u[0]);
+                nsum_add(&AV, fabs(u[0]));
+                for (int c = 0; c < 3; ++c) {
+                    double g = u[1] * d[c] / rho;
+                    nsum_add(&G[c], -g);
+                    nsum_add(&AG[c], fabs(g));
+                }
+                nsum_add(&Lp, u[2] + 2.0 * u[1] / rho);
+                nsum_add(&AL, fabs(u[2]) + 2.0 * fabs(u[1]) / rho);
+            }
+            double *o = J->out + (w * J->P + p) * 5;
+            o[0] = nsum_get(&V);
+            o[1] = nsum_get(&G[0]); o[2] = nsum_get(&G[1]); o[3] = nsum_get(&G[2]);
+            o[4] = nsum_get(&Lp);
+            if (J->abs_out) {
+                double *a = J->abs_out + (w * J->P + p) * 5;
+                a[0] = nsum_get(&AV);
+                a[1] = nsum_get(&AG[0]); a[2] = nsum_get(&AG[1]); a[3] = nsum_get(&AG[2]);
+                a[4] = nsum_get(&AL);
+            }
+        }
+    }
+    return 0;
+}
+
+static void *eval_thread(void *arg)
+{
+    orc_job *J = (orc_job *)arg;
+    J->status = eval_walkers(J);
+    return NULL;
+}
+
+int64_t orc_eval(const double L[3], double r_cut, int m, const double *coef,
+                 int64_t W, int64_t N_total, int64_t N_up,
+                 int64_t i_offset, int64_t N_local, int64_t Np,
+                 const double *R, const int32_t *k, int32_t P, const double *r_trial,
+                 double *out, double *abs_out, double *row_out, int nthreads)
+{
+    (void)N_total;
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > W) nthreads = (int)(W > 0 ? W : 1);
+    orc_job *jobs = (orc_job *)calloc((size_t)nthreads, sizeof(orc_job));
+    pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+    int64_t per = (W + nthreads - 1) / nthreads;
+    for (int t = 0; t < nthreads; ++t) {
+        orc_job J = { L, r_cut, m, coef, W, N_total, N_up, i_offset, N_local, Np,
+                      R, k, P, r_trial, out, abs_out, row_out,
+                      t * per, (t + 1) * per < W ? (t + 1) * per : W, 0 };
+        if (J.w_begin > W) J.w_begin = W;
+        jobs[t] = J;
+    }
+    for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, eval_thread, &jobs[t]);
+    eval_thread(&jobs[0]);
+    for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+    int64_t st = 0;
+    for (int t = 0; t < nthreads && !st; ++t) st = jobs[t].status;
+    free(jobs); free(th);
+    return st;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Brute-force two-body Jastrow of one configuration, Eq. (3) second term     */
+/* under reading R1: J2 = sum_{i<j} U_s(|r_i - r_j|) over     */
+/* unordered pairs, so that Delta J2 = J2(R') - J2(R) reproduces Eq. (5).     */
+/* O(N^2); used only by the pins on tiny N.                                   */
+/* ------------------------------------------------------------------------ */
+double orc_j2_total(const double L[3], double r_cut, int m, const double *coef,
+                    int64_t N, int64_t N_up, int64_t Np, const double *R)
+{
+    const int mc = m + 3;
+    nsum J = {0, 0};
+    for (int64_t i = 0; i < N; ++i)
+        for (int64_t j = i + 1; j < N; ++j) {
+            double a[3] = { R[i], R[Np + i], R[2 * Np + i] };
+            double b[3] = { R[j], R[Np + j], R[2 * Np + j] };
+            double d[3], rho, u[3];
+            orc_min_image(L, a, b, d, &rho);
+            orc_bspline(coef + spin_channel(i, j, N_up) * mc, m, r_cut, rho, u);
+            nsum_add(&J, u[0]);
+        }
+    return nsum_get(&J);
+}
+
+/* Batched functor evaluation (SPEC:279 functor_eval_vgl) for the pins. */
+void orc_bspline_batch(const double *c, int m, double r_cut, int64_t n,
+                       const double *r, double *out /* [n][3] */)
+{
+    for (int64_t i = 0; i < n; ++i) orc_bspline(c, m, r_cut, r[i], out + 3 * i);
+}
+
+/* Batched minimum image for the pins: out[n][4] = (dist, d). */
+void orc_min_image_batch(const double L[3], int64_t n, const double *a,
+                         const double *b, double *out)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        double d[3], rho;
+        orc_min_image(L, a + 3 * i, b + 3 * i, d, &rho);
+        out[4 * i] = rho; out[4 * i + 1] = d[0]; out[4 * i + 2] = d[1]; out[4 * i + 3] = d[2];
+    }
+}

@@ -1,0 +1,234 @@
+"""qmcgen -- seeded synthetic inputs shared by the oracle side and the CUDA side.
+
+This module holds NO arithmetic of the method (no minimum image, no spline,
+no reduction).  It only draws numbers.  Both the tests/oracle and the product
+path may import it; it imports neither.
+
+Input recipe:
+
+* Cell: cubic, periodic, density 1: L = fl32(N ** (1/3)) (chosen exactly
+  representable in fp32 so fp32 and fp64 paths share the same cell), r_cut = L/2
+  (reading R4).
+* Positions R[w][d][i]: counter-based hash (splitmix64 finaliser) of
+  (seed, walker, coordinate, electron) -> u in [0,1) -> x = fl_T(L * u), kept
+  below L.  The device generator in the CUDA library implements the same integer
+  recipe independently (a test checks bit equality on samples).
+* Active electron k_w ~ U{0..N-1}; trial r' = wrap(r_k + delta),
+  delta ~ N(0, 0.01 I) (reading R13); NumPy default_rng.
+* Functor: m = 8 intervals, per spin channel c[0..m-1] ~ U[0,1), c[m..m+2] = 0
+  (C2 cutoff, reading R3).
+* N_up = N / 2.
+
+The paper's workloads (Table 1) need QMCPACK orbital,
+pseudopotential and Jastrow files that are not available; these synthetic
+inputs stand in for them with the paper's shape parameters (N, W).
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+MASK64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+GOLDEN = 0x9E3779B97F4A7C15
+_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_M2 = np.uint64(0x94D049BB133111EB)
+
+
+def mix64(z: np.ndarray) -> np.ndarray:
+    """splitmix64 finaliser on uint64 arrays (wrapping arithmetic)."""
+    z = np.asarray(z, dtype=np.uint64).copy()
+    with np.errstate(over="ignore"):
+        z ^= z >> np.uint64(30)
+        z *= _M1
+        z ^= z >> np.uint64(27)
+        z *= _M2
+        z ^= z >> np.uint64(31)
+    return z
+
+
+def seed_key(seed: int) -> np.uint64:
+    """Per-instance key: mix64(seed * GOLDEN + GOLDEN) (mod 2^64)."""
+    s = (int(seed) * GOLDEN + GOLDEN) & 0xFFFFFFFFFFFFFFFF
+    return mix64(np.array([s], dtype=np.uint64))[0]
+
+
+def hash_u64(seed: int, w, d, i) -> np.ndarray:
+    """h = mix64(key ^ ((w*3 + d) << 32 | i)) for broadcastable int arrays."""
+    key = seed_key(seed)
+    w = np.asarray(w, dtype=np.uint64)
+    d = np.asarray(d, dtype=np.uint64)
+    i = np.asarray(i, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        ctr = ((w * np.uint64(3) + d) << np.uint64(32)) | i
+    return mix64(ctr ^ key)
+
+
+def _scale(h: np.ndarray, L: float, dtype) -> np.ndarray:
+    if np.dtype(dtype) == np.float32:
+        u = (h >> np.uint64(40)).astype(np.float32) * np.float32(2.0 ** -24)
+        Lf = np.float32(L)
+        x = (Lf * u).astype(np.float32)
+        below = np.nextafter(Lf, np.float32(0))
+        return np.where(x >= Lf, below, x).astype(np.float32)
+    u = (h >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+    x = np.float64(L) * u
+    below = np.nextafter(np.float64(L), 0.0)
+    return np.where(x >= L, below, x)
+
+
+def cell_length(N: int) -> float:
+    """L = fl32(N^(1/3)): density 1, exactly representable in fp32."""
+    return float(np.float32(float(N) ** (1.0 / 3.0)))
+
+
+def positions(seed: int, walkers, N: int, Np: int, L: float, dtype) -> np.ndarray:
+    """R[len(walkers)][3][Np] (dtype); walkers are GLOBAL walker ids; padding 0."""
+    walkers = np.asarray(walkers, dtype=np.int64).reshape(-1)
+    out = np.zeros((walkers.size, 3, Np), dtype=dtype)
+    i = np.arange(N, dtype=np.uint64)
+    for a, w in enumerate(walkers):
+        for d in range(3):
+            out[a, d, :N] = _scale(hash_u64(seed, w, d, i), L, dtype)
+    return out
+
+
+def position_at(seed: int, w, d, i, L: float, dtype) -> np.ndarray:
+    """Single coordinates R[w][d][i] for broadcastable index arrays."""
+    return _scale(hash_u64(seed, w, d, i), L, dtype)
+
+
+def padded_size(n: int, block: int) -> int:
+    """Smallest multiple of block >= max(n, 1)."""
+    if block < 1:
+        raise ValueError("block must be >= 1")
+    n = max(int(n), 1)
+    return ((n + block - 1) // block) * block
+
+
+@dataclasses.dataclass(frozen=True)
+class Functor:
+    """J2 radial functor data: cell, cutoff and two channels of m+3 B-spline
+    coefficients ([0] same spin, [1] opposite spin)."""
+    L: tuple
+    r_cut: float
+    m: int
+    coef: np.ndarray  # [2][m+3] float64
+
+    @property
+    def delta(self) -> float:
+        return self.r_cut / self.m
+
+
+def make_functor(seed: int, L: float, m: int = 8, r_cut: float | None = None,
+                 zero_tail: bool = True) -> Functor:
+    rng = np.random.default_rng([int(seed), 2])
+    coef = np.zeros((2, m + 3), dtype=np.float64)
+    coef[:, :m] = rng.random((2, m))
+    if not zero_tail:
+        coef[:, m:] = rng.random((2, 3))
+    rc = L / 2.0 if r_cut is None else float(r_cut)
+    return Functor(L=(float(L),) * 3, r_cut=rc, m=int(m), coef=coef)
+
+
+def make_k(seed: int, W: int, N: int, w_offset: int = 0) -> np.ndarray:
+    """Active electron per walker, uniform on [0, N)."""
+    rng = np.random.default_rng([int(seed), 1])
+    k = rng.integers(0, N, size=w_offset + W, dtype=np.int64)[w_offset:]
+    return k.astype(np.int32)
+
+
+def make_trials(seed: int, walkers, k: np.ndarray, N: int, L: float, dtype,
+                P: int = 1, mode: str = "move") -> np.ndarray:
+    """r_trial[W][P][3] (dtype).
+
+    mode="move":  every p is r'_k = wrap(r_k + delta_p), delta ~ N(0, 0.01 I).
+    mode="drift": p = 0 is r_k itself (current position), p >= 1 are moves
+                  (the P = 2 variant: value at R and at R' in one pass).
+    mode="noop":  every p is r_k (no-op move).
+    """
+    walkers = np.asarray(walkers, dtype=np.int64).reshape(-1)
+    W = walkers.size
+    rng = np.random.default_rng([int(seed), 3])
+    # draw for the whole walker range up to max id so draws do not depend on
+    # which subset is requested
+    nmax = int(walkers.max()) + 1 if W else 0
+    delta = rng.normal(0.0, 0.1, size=(nmax, P, 3))[walkers] if W else np.zeros((0, P, 3))
+    rk = np.stack([position_at(seed, walkers, d, k.astype(np.int64), L, dtype)
+                   for d in range(3)], axis=-1).astype(np.float64)  # [W][3]
+    out = np.empty((W, P, 3), dtype=dtype)
+    for p in range(P):
+        if mode == "noop" or (mode == "drift" and p == 0):
+            out[:, p, :] = rk.astype(dtype)
+            continue
+        t = np.mod(rk + delta[:, p, :], L)
+        t = t.astype(dtype)
+        below = np.nextafter(np.asarray(L, dtype=dtype), np.asarray(0, dtype=dtype))
+        t = np.where(t >= np.asarray(L, dtype=dtype), below, t)
+        out[:, p, :] = t
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Configurations (BASELINE.json configs; concrete instances SURVEY.md 8(d)).
+# ---------------------------------------------------------------------------
+@dataclasses.dataclass(frozen=True)
+class Config:
+    name: str
+    N: int
+    W: int
+    dtype: str          # "f32" | "f64"
+    seed: int
+    instances: int = 1  # C4: independent instances with seeds seed..seed+instances-1
+    m: int = 8
+
+    @property
+    def np_dtype(self):
+        return np.float32 if self.dtype == "f32" else np.float64
+
+    @property
+    def Np(self) -> int:
+        # 128-byte padded lanes: 32 fp32 or 16 fp64 elements
+        return padded_size(self.N, 32 if self.dtype == "f32" else 16)
+
+    @property
+    def L(self) -> float:
+        return cell_length(self.N)
+
+    @property
+    def n_up(self) -> int:
+        return self.N // 2
+
+    @property
+    def items(self) -> int:
+        """(walker, trial, source i != k) terms per instance at P = 1."""
+        return self.W * (self.N - 1)
+
+    def functor(self, seed: int | None = None) -> Functor:
+        return make_functor(self.seed if seed is None else seed, self.L, self.m)
+
+
+CONFIGS = {
+    "C1": Config("C1", N=14, W=1024, dtype="f64", seed=0),
+    "C2": Config("C2", N=1400, W=1024, dtype="f32", seed=1),
+    "C2f64": Config("C2f64", N=1400, W=1024, dtype="f64", seed=1),
+    "C3": Config("C3", N=614400, W=1024, dtype="f32", seed=2),
+    "C4": Config("C4", N=6144, W=1024, dtype="f32", seed=3, instances=4096),
+    "C5": Config("C5", N=4915200, W=1024, dtype="f32", seed=5),
+}
+
+
+def host_instance(cfg: Config, seed: int | None = None, walkers=None, P: int = 1,
+                  mode: str = "move"):
+    """Generate (R, k, r_trial, functor) on the host for the given walkers
+    (default all).  Used for small configs and for sampled checks of large
+    ones."""
+    seed = cfg.seed if seed is None else seed
+    walkers = np.arange(cfg.W) if walkers is None else np.asarray(walkers)
+    L = cfg.L
+    k_all = make_k(seed, cfg.W, cfg.N)
+    k = k_all[walkers]
+    R = positions(seed, walkers, cfg.N, cfg.Np, L, cfg.np_dtype)
+    rt = make_trials(seed, walkers, k, cfg.N, L, cfg.np_dtype, P=P, mode=mode)
+    return R, k, rt, make_functor(seed, L, cfg.m)

@@ -1,0 +1,60 @@
+"""Host-side checks of the seeded input generator (qmcgen) -- no GPU."""
+import numpy as np
+
+import qmcgen
+
+
+def test_positions_in_cell_and_deterministic():
+    for dtype in (np.float32, np.float64):
+        N = 1000
+        L = qmcgen.cell_length(N)
+        R = qmcgen.positions(7, [0, 5, 9], N, qmcgen.padded_size(N, 32), L, dtype)
+        assert R.dtype == dtype
+        assert np.all(R[:, :, :N] >= 0) and np.all(R[:, :, :N] < dtype(L))
+        assert np.all(R[:, :, N:] == 0)
+        R2 = qmcgen.positions(7, [5], N, qmcgen.padded_size(N, 32), L, dtype)
+        assert np.array_equal(R[1], R2[0])          # walker subset independent
+        assert not np.array_equal(R[0], R[1])
+
+
+def test_position_at_matches_positions():
+    N, L = 500, qmcgen.cell_length(500)
+    R = qmcgen.positions(3, [4], N, 512, L, np.float32)
+    i = np.array([0, 17, 499])
+    for d in range(3):
+        assert np.array_equal(qmcgen.position_at(3, 4, d, i, L, np.float32), R[0, d, i])
+
+
+def test_cell_is_fp32_exact():
+    for N in (14, 1400, 614400, 6144, 4915200):
+        L = qmcgen.cell_length(N)
+        assert float(np.float32(L)) == L
+        assert abs(L ** 3 / N - 1) < 1e-5
+
+
+def test_uniformity_rough():
+    N = 200000
+    L = qmcgen.cell_length(N)
+    R = qmcgen.positions(1, [0], N, N, L, np.float32)[0] / np.float32(L)
+    h, _ = np.histogram(R.ravel(), bins=10, range=(0, 1))
+    assert np.all(np.abs(h / h.mean() - 1) < 0.02)
+
+
+def test_trials_and_k():
+    cfg = qmcgen.CONFIGS["C2"]
+    R, k, rt, fn = qmcgen.host_instance(cfg, walkers=np.arange(64), P=2, mode="drift")
+    assert k.dtype == np.int32 and np.all((k >= 0) & (k < cfg.N))
+    assert rt.shape == (64, 2, 3) and rt.dtype == np.float32
+    for w in range(64):
+        assert np.array_equal(rt[w, 0], R[w, :, k[w]])     # drift mode p=0 is r_k
+    assert np.all(rt >= 0) and np.all(rt < np.float32(cfg.L))
+    assert fn.coef.shape == (2, 11) and np.all(fn.coef[:, 8:] == 0)
+    assert fn.r_cut == cfg.L / 2
+
+
+def test_config_sizes():
+    c3 = qmcgen.CONFIGS["C3"]
+    assert c3.W * 3 * c3.Np * 4 == 7549747200           # ~7.55 GB of R
+    assert c3.items == 1024 * 614399
+    c5 = qmcgen.CONFIGS["C5"]
+    assert c5.W * 3 * c5.Np * 4 == 60397977600
