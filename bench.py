@@ -1,0 +1,458 @@
+#!/usr/bin/env python
+"""bench.py -- hot-path items/s and HBM-roofline fraction on B200, next to the
+CPU oracle (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C3|C4|C5]
+
+One step = one pass of the whole hot path (staged
+SoA rows -> on-the-fly distance row -> functor -> fp64 reduction -> out and
+e^{dJ2}) over one batch: a single qj2_eval launch for all W walkers.
+
+Workload (N=1 default): C3 = one instance of N = 614,400 electrons x W = 1024
+walkers, P = 1, fp32 (7.55 GB of positions: larger than the 126 MB L2, so no
+L2 flush is needed between steps).  BASELINE.json names C3 the "single-GPU
+roofline measurement"; C2 (17 MB) is L2-resident and is a parity case.
+N>1 (torchrun): --config C3 (default) runs one distinct C3 instance per rank
+(weak scaling, no collective on the data path); C4 shards 4096 independent
+instances by rank; C5 splits one N = 4,915,200 instance along the electron
+axis and combines the partial sums with an NCCL all-reduce.
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "hot-path items/sec and fraction of roofline at 1/2/4/8 B200 vs CPU oracle"
+UNIT = "items/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-walkers", type=int, default=0, help="0 = auto")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def dist_init(world, local, backend="nccl"):
+    import torch
+    import torch.distributed as dist
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return dist if world > 1 else None
+
+
+def allreduce_max(x: float, dist_mod) -> float:
+    if dist_mod is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist_mod.all_reduce(t, op=dist_mod.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    BAD = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "hw_power_brake")
+
+    def __init__(self, device_index: int, period_s: float = 0.02):
+        self.period = period_s
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            log(f"[bench] NVML unavailable: {e}")
+            self.max_mhz = None
+
+    def _names(self, mask):
+        nv = self.nv
+        table = {
+            "gpu_idle": nv.nvmlClocksEventReasonGpuIdle,
+            "applications_clocks_setting": nv.nvmlClocksEventReasonApplicationsClocksSetting,
+            "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap,
+            "hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+            "sync_boost": nv.nvmlClocksEventReasonSyncBoost,
+            "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+            "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+            "hw_power_brake": nv.nvmlClocksEventReasonHwPowerBrakeSlowdown,
+        }
+        return {n for n, b in table.items() if mask & b}
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self._names(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+    def rejected(self):
+        s = self.summary()
+        if any(r in s["reasons"] for r in self.BAD):
+            return True
+        if s["sm_mhz"] and s["sm_max_mhz"] and s["sm_mhz"] < 0.6 * s["sm_max_mhz"] and not s["reasons"]:
+            return True
+        return False
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy_ of 1 Gi bf16)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def committed_traffic(config_name: str):
+    """dram read+write bytes per launch of the dominant kernel from the committed
+    ncu --set full capture (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        e = d.get(config_name)
+        if e:
+            return e.get("dram_bytes_per_launch")
+    return None
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (cpu_baseline leg and --impl reference)
+# ---------------------------------------------------------------------------
+def oracle_rate(cfg, walkers, threads):
+    """Time the oracle (as it stands) on `walkers` of cfg; return (items/s, seconds)."""
+    import oracle
+    import qmcgen
+    seed = cfg.seed
+    L = cfg.L
+    k_all = qmcgen.make_k(seed, cfg.W, cfg.N)
+    w = np.asarray(walkers)
+    R = qmcgen.positions(seed, w, cfg.N, cfg.Np, L, cfg.np_dtype)
+    rt = qmcgen.make_trials(seed, np.arange(cfg.W), k_all, cfg.N, L, cfg.np_dtype)[w]
+    fn = qmcgen.make_functor(seed, L, cfg.m)
+    Rf = np.ascontiguousarray(R, dtype=np.float64)          # promotion outside the timed region
+    t0 = time.perf_counter()
+    oracle.eval_j2(Rf, k_all[w], rt, fn, cfg.N, cfg.n_up, threads=threads)
+    dt = time.perf_counter() - t0
+    return w.size * (cfg.N - 1) / dt, dt
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    import qmcgen
+    cfg = qmcgen.CONFIGS[args.config]
+    cores = cpu_cores()
+    # calibrate: one walker per core, then size each step to the time budget
+    budget_total = 150.0
+    per_step = max(0.5, min(10.0, budget_total / max(1, args.steps + args.warmup)))
+    n0 = min(cfg.W, cores)
+    rate0, dt0 = oracle_rate(cfg, np.arange(n0), cores)
+    per_walker = dt0 / n0 * min(cores, n0)   # seconds per walker per core
+    ws = int(max(1, min(cfg.W, per_step * cores / max(per_walker, 1e-9))))
+    ws = max(1, (ws // cores) * cores) if ws >= cores else ws
+    log(f"[reference] oracle {rate0:.3e} items/s on {n0} walkers; {ws} walkers per step")
+    for i in range(args.warmup):
+        oracle_rate(cfg, (np.arange(ws) + i * ws) % cfg.W, cores)
+    times = []
+    for i in range(args.steps):
+        r, dt = oracle_rate(cfg, (np.arange(ws) + i * ws) % cfg.W, cores)
+        times.append(dt)
+    t = float(np.mean(times))
+    value = ws * (cfg.N - 1) / t
+    sample = (f"{ws} of {cfg.W} walkers of {cfg.name} (N={cfg.N}, P=1) per step, fp32 inputs promoted to "
+              f"fp64, plain C oracle, {cores} threads ({cpu_model()})")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(cfg, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(cfg, world):
+    name = cfg.name
+    desc = {
+        "C3": f"C3: one instance per rank, N={cfg.N} electrons x W={cfg.W} walkers, P=1, fp32, seed 2(+rank)",
+        "C4": f"C4: 4096 instances of N={cfg.N} x W={cfg.W}, P=1, fp32, seeds 3..4098, sharded by instance",
+        "C5": f"C5: one instance N={cfg.N} x W={cfg.W}, P=1, fp32, seed 5, split along N + NCCL all-reduce",
+    }[name]
+    return {"workload": desc, "N": cfg.N, "W": cfg.W, "P": 1, "m": cfg.m, "Np": cfg.Np,
+            "parallelism": f"{'walker-instance' if name != 'C5' else 'source-axis'} x{world}",
+            "l2": "inputs > 126 MB L2 (no flush needed)"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+class C3Plan:
+    """One C3-shaped instance per rank (weak scaling; no collective on the data path)."""
+    mode = "C3"
+    launches_per_step = 1
+
+    def __init__(self, cfg, rank, world):
+        self.cfg = cfg
+        self.seed = cfg.seed + rank
+        self.items_per_step = cfg.W * (cfg.N - 1)
+        sz = 4
+        # algorithmic bytes: x, y, z of every source i != k once per walker,
+        # plus per walker k (4 B), r_trial (12 B), V_cur (8 B), out (40 B), ratio (16 B)
+        self.alg_bytes_per_launch = cfg.W * (cfg.N - 1) * 3 * sz + cfg.W * (4 + 12 + 8 + 40 + 16)
+
+    def prepare(self, q):
+        import torch
+        import qmcgen
+        cfg = self.cfg
+        self.fn = q.Functor.of(qmcgen.make_functor(cfg.seed, cfg.L, cfg.m))
+        self.R = q.gen_positions(self.seed, cfg.W, cfg.N, cfg.Np, cfg.L, torch.float32)
+        k = qmcgen.make_k(self.seed, cfg.W, cfg.N)
+        rt = qmcgen.make_trials(self.seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32)
+        rk = qmcgen.make_trials(self.seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32, mode="noop")
+        self.k = torch.from_numpy(k).cuda()
+        self.rt = torch.from_numpy(rt).cuda()
+        self.ws = q.Workspace(q.workspace_size(cfg.W, 1, cfg.N, torch.float32))
+        # the caller's 5N state: U^2_k(R) at the current positions (untimed)
+        v0 = q.eval(self.R, self.k, torch.from_numpy(rk).cuda(), self.fn, cfg.N, cfg.n_up, workspace=self.ws)
+        self.V_cur = v0[:, 0, 0].contiguous()
+        self.out = torch.empty((cfg.W, 1, 5), dtype=torch.float64, device="cuda")
+        self.ratio = torch.empty((cfg.W, 1, 2), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+
+    def step(self, q, dist_mod):
+        cfg = self.cfg
+        q.eval(self.R, self.k, self.rt, self.fn, cfg.N, cfg.n_up, V_cur=self.V_cur, ratio=True,
+               out=self.out, ratio_out=self.ratio, workspace=self.ws)
+
+    def kernel_ms(self, q, stream, reps):
+        import torch
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(reps):
+            self.step(q, None)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    def e2e(self, q, steps, dist_mod):
+        """Same metric through the public host-buffer API (qj2_eval_host): every step copies the
+        step's inputs from pinned host memory and reads the result back."""
+        import torch
+        cfg = self.cfg
+        Rh = torch.empty(self.R.shape, dtype=self.R.dtype, pin_memory=True)
+        Rh.copy_(self.R)
+        kh = self.k.cpu().pin_memory()
+        th = self.rt.cpu().pin_memory()
+        vh = self.V_cur.cpu().pin_memory()
+        outh = torch.empty((cfg.W, 1, 5), dtype=torch.float64, pin_memory=True)
+        rath = torch.empty((cfg.W, 1, 2), dtype=torch.float64, pin_memory=True)
+        chunk = 32
+        ws = q.Workspace(q.host_workspace_size(cfg.W, 1, cfg.Np, torch.float32, chunk))
+        run = lambda: q.eval_host(Rh, kh, th, self.fn, cfg.N, cfg.n_up, V_cur=vh, ratio=True,  # noqa: E731
+                                  chunk_walkers=chunk, out=outh, ratio_out=rath, workspace=ws)
+        run()
+        torch.cuda.synchronize()
+        if dist_mod:
+            dist_mod.barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            run()
+        dt = (time.perf_counter() - t0) / steps
+        dt = allreduce_max(dt, dist_mod)
+        same = bool(torch.equal(outh, self.out.cpu()))
+        world = dist_mod.get_world_size() if dist_mod else 1
+        h2d = Rh.numel() * 4 + kh.numel() * 4 + th.numel() * 4 + vh.numel() * 8
+        d2h = outh.numel() * 8 + rath.numel() * 8
+        del Rh
+        return {"value": self.items_per_step * world / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3, "steps": steps,
+                "api": "qj2_eval_host (pinned host buffers, 2-stage H2D/compute pipeline)",
+                "matches_device_path": same}
+
+
+def make_plan(cfg, rank, world):
+    if cfg.name == "C3":
+        return C3Plan(cfg, rank, world)
+    from paper_1708_02645_b200 import parallel  # noqa: F401
+    raise NotImplementedError(cfg.name)
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        log(f"[bench] warning: --gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    dist_mod = dist_init(world, local)
+    import qmcgen
+    import paper_1708_02645_b200 as q
+    q.device_check()
+    cfg = qmcgen.CONFIGS[args.config]
+
+    plan = make_plan(cfg, rank, world)
+    plan.prepare(q)                                   # device-resident inputs (generation untimed)
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        plan.step(q, dist_mod)
+    torch.cuda.synchronize()
+
+    def timed(K):
+        if dist_mod:
+            dist_mod.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            e0.record(stream)
+            for _ in range(K):
+                plan.step(q, dist_mod)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        if dist_mod:
+            dist_mod.barrier()
+        return e0.elapsed_time(e1) / K, clk
+
+    ms, clk = timed(args.steps)
+    if clk.rejected():
+        log(f"[bench] clocks rejected ({clk.summary()}); re-measuring once")
+        ms, clk = timed(args.steps)
+    ms_max = allreduce_max(ms, dist_mod)
+    items_total = plan.items_per_step * world
+    value = items_total / (ms_max / 1e3)
+
+    # roofline of the dominant kernel (j2_eval_kernel), timed on its launching stream
+    kms = plan.kernel_ms(q, stream, reps=max(5, min(args.steps, 50)))
+    alg_bytes = plan.alg_bytes_per_launch
+    peak, peak_src = measured_peaks()
+    achieved = alg_bytes / (kms / 1e3) / 1e9
+    traffic = committed_traffic(cfg.name)
+
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        e2e = plan.e2e(q, args.e2e_steps, dist_mod)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = cpu_cores()
+        nw = args.cpu_sample_walkers or min(cfg.W, max(cores, 16))
+        rate, dt = oracle_rate(cfg, np.arange(nw), cores)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{nw} of {cfg.W} walkers of {cfg.name} (N={cfg.N}, P=1) once, fp32 inputs promoted "
+                         f"to fp64, plain C oracle, {cores} threads ({cpu_model()}), {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "weak" if plan.mode == "C3" else "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(cfg, world),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "j2_eval_kernel<float,1,false>", "kernel_ms": kms,
+                         "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": plan.launches_per_step * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist_mod:
+        dist_mod.barrier()
+        dist_mod.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

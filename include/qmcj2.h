@@ -1,0 +1,235 @@
+/*
+ * qmcj2.h -- C ABI of the B200 (sm_100a) hot path of arXiv 1708.02645
+ * (Mathuriya et al., SC'17): the batched on-the-fly electron-electron distance
+ * row and two-body Jastrow (J2) value, gradient and Laplacian of a
+ * particle-by-particle move.
+ *
+ * Citations: PAPER:n = line n of the paper's LaTeX,
+ * SPEC:n = line n of the CPU-miniapp spec written from it (interfaces only).
+ *
+ * Conventions common to every entry point
+ * ---------------------------------------
+ * - Plain pointers and sizes only.  "device" pointers are CUDA device
+ *   (or managed) memory owned by the caller; "host" pointers are host memory
+ *   owned by the caller.  The library never frees caller memory and
+ *   allocates no device memory (scratch comes from the caller's workspace).
+ * - stream is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   Device-pointer entry points are asynchronous on that stream; asynchronous
+ *   device faults surface at the caller's next synchronisation.
+ * - Every entry point validates its arguments on the host before any launch
+ *   and returns a qj2_status; no exception crosses the ABI.  On failure,
+ *   qj2_last_error() returns a thread-local detail string.
+ * - The library holds no global mutable state: calls on different streams with
+ *   different workspaces are independent and may run concurrently.
+ * - Device entry points require an sm_100 device (else QJ2_ENOTSUP).
+ * - All sizes are int64; all flat offsets inside kernels are 64-bit.
+ */
+#ifndef QMCJ2_H
+#define QMCJ2_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QJ2_VERSION 10000 /* major*10000 + minor*100 + patch */
+
+typedef enum {
+    QJ2_OK = 0,
+    QJ2_EINVAL = 1,   /* invalid argument ("invalid-argument") */
+    QJ2_ERANGE = 2,   /* out-of-range index/slice ("out-of-range") */
+    QJ2_ENOTSUP = 3,  /* current device is not sm_100 (B200) */
+    QJ2_ECUDA = 4     /* CUDA launch / runtime failure */
+} qj2_status;
+
+typedef enum { QJ2_FP32 = 0, QJ2_FP64 = 1 } qj2_dtype;
+
+enum { QJ2_MAX_M = 64, QJ2_MAX_P = 64 };
+
+/*
+ * Two-body Jastrow functor U_s(r) and the simulation cell.
+ * PAPER:812-819 (Eq. 3, "one-dimensional cubic B-spline")
+ * ("finite cutoff"), SPEC:256-258 (uniform B-spline: delta = r_cut/m, m+3
+ * coefficients, zero for r >= r_cut).  Basis convention (R3):
+ *   t = r/delta, j = min(floor(t), m-1), f = t - j,
+ *   U(r) = sum_{a=0..3} coef[s][j+a] B_a(f), uniform cubic B-spline basis.
+ * Channel s = 0 same spin, 1 opposite spin.
+ * Requirements (else QJ2_EINVAL): L[d] > 0, 0 < r_cut <= min(L)/2 (so the
+ * minimum image is exact), 4 <= m <= QJ2_MAX_M, coef[s][m..m+2] == 0 (the
+ * functor and its first two derivatives vanish at r_cut), finite values.
+ * Passed by pointer to host memory; copied into kernel parameters per call.
+ */
+typedef struct {
+    double  L[3];                      /* orthorhombic periodic cell lengths */
+    double  r_cut;                     /* functor cutoff radius */
+    int32_t m;                         /* number of B-spline intervals */
+    int32_t reserved;                  /* must be 0 */
+    double  coef[2][QJ2_MAX_M + 3];    /* [0] same-spin, [1] opposite-spin */
+} qj2_functor;
+
+/* ------------------------------------------------------------------------ */
+/* Library information                                                       */
+/* ------------------------------------------------------------------------ */
+int32_t     qj2_version(void);
+const char *qj2_status_string(qj2_status s);     /* static string, never NULL */
+const char *qj2_last_error(void);                /* thread-local detail, never NULL */
+
+/* QJ2_OK if the current CUDA device is sm_100 (compute capability 10.0),
+ * QJ2_ENOTSUP otherwise, QJ2_ECUDA if there is no usable device. */
+qj2_status  qj2_device_check(void);
+
+/* ------------------------------------------------------------------------ */
+/* padded_size ("Np includes the padding for     */
+/* alignment"): *out = smallest multiple of block >= max(n, 1).              */
+/* Errors: n < 0 or block < 1 -> QJ2_EINVAL; out == NULL -> QJ2_EINVAL.      */
+/* ------------------------------------------------------------------------ */
+qj2_status qj2_padded_size(int64_t n, int64_t block, int64_t *out);
+
+/* ------------------------------------------------------------------------ */
+/* Scratch needed by qj2_eval for (W, P, N_local, dtype): per-tile fp64      */
+/* partial sums plus per-(walker, trial-group) completion counters.          */
+/* ------------------------------------------------------------------------ */
+qj2_status qj2_eval_workspace_size(int64_t W, int32_t P, int64_t N_local,
+                                   qj2_dtype dtype, size_t *bytes);
+
+/* ------------------------------------------------------------------------ */
+/* qj2_eval -- THE HOT PATH.             */
+/*                                                                           */
+/* For every walker w < W and trial p < P, with r = r_trial[w][p]:           */
+/*   d_i = minimg(r_i - r)  (1-by-N relations d(k,i),       */
+/*         dr(k,i); Fig. 6's temporary row v, computed on   */
+/*         the fly)                                         */
+/*   V  = sum_{i != k, |d_i| < r_cut} U_s(|d_i|)                             */
+/*   G  = -sum U_s'(|d_i|) d_i/|d_i|           (= grad_r V)                  */
+/*   L  = sum U_s''(|d_i|) + 2 U_s'(|d_i|)/|d_i|   (= lap_r V)               */
+/* over the source slice i in [i_offset, i_offset + N_local).  With the full */
+/* range and r = r'_k these are U^2_k(R') of PAPER:1382 (one term of Eq. 5,  */
+/* PAPER:885-887) and the J2 shares of grad_k, lap_k at R' (Alg. 1 L8,       */
+/* PAPER:849).  Arithmetic: dtype positions and per-term math, fp64          */
+/* accumulation and outputs ("quantities per walker ... in double           */
+/* precision").                                               */
+/*                                                                           */
+/* Arguments                                                                 */
+/*   fn        host, functor + cell (see qj2_functor).                       */
+/*   dtype     QJ2_FP32 or QJ2_FP64: type of R, r_trial and row_out.         */
+/*   W         walkers (>= 0; W == 0 is a no-op).                            */
+/*   N_total   electrons per walker (>= 2).  N_up: spin-up electrons are     */
+/*             global indices [0, N_up) (0 <= N_up <= N_total).              */
+/*   i_offset, N_local: this call's source slice (sharding along the        */
+/*             electron axis; 0 <= i_offset, 1 <= N_local,                   */
+/*             i_offset + N_local <= N_total else QJ2_ERANGE).  Spin channel */
+/*             and self-exclusion use GLOBAL indices, so the slices' partial */
+/*             sums add up to the unsplit result.                            */
+/*   Np        padded lane length, Np >= N_local, Np % 4 == 0 (fp32) or      */
+/*             Np % 2 == 0 (fp64).                                           */
+/*   R         device [W][3][Np] dtype, SoA lanes x|y|z (PAPER:1290-1296,    */
+/*             Rsoa[3][Np]); coordinates in [0, L_d); 16-byte aligned.       */
+/*   k         device [W] int32, active electron, global index < N_total.    */
+/*   P         trial positions per walker, 1 <= P <= QJ2_MAX_P.             */
+/*   r_trial   device [W][P][3] dtype, coordinates in [0, L_d).              */
+/*   out       device [W][P][5] fp64: (V, Gx, Gy, Gz, L) over the slice.     */
+/*   row_out   device [W][P][4][Np] dtype (r, dx, dy, dz) or NULL: the       */
+/*             candidate distance row v;     */
+/*             slot k and padding slots are unspecified.  16-byte aligned.   */
+/*   V_cur     device [W] fp64 or NULL: U^2_k(R) from the caller's 5N state  */
+/*              for the ratio below.                        */
+/*   ratio_out device [W][P][2] fp64 or NULL: (dJ2, exp(dJ2)) with           */
+/*             dJ2 = V_p - V_cur[w] (or V_p - V_0 when V_cur == NULL and     */
+/*             P <= 4): the e^{dJ2} factor of Eq. 4.   */
+/*             Only for unsharded calls (i_offset == 0, N_local == N_total); */
+/*             sharded callers reduce `out` first and call qj2_ratio.        */
+/*   workspace device scratch >= qj2_eval_workspace_size(); must be          */
+/*             zero-filled before its FIRST use; every completed call leaves */
+/*             its counters zero again.  One workspace per concurrent call.  */
+/*   stream    cudaStream_t.                                                 */
+/* Preconditions not checked on the hot path (see qj2_check_inputs):         */
+/* coordinates in range, k < N_total, no coincident source inside the        */
+/* cutoff (r = 0 is undefined: the result may be non-finite).                */
+/* ------------------------------------------------------------------------ */
+qj2_status qj2_eval(const qj2_functor *fn, qj2_dtype dtype,
+                    int64_t W, int64_t N_total, int64_t N_up,
+                    int64_t i_offset, int64_t N_local, int64_t Np,
+                    const void *R, const int32_t *k,
+                    int32_t P, const void *r_trial,
+                    double *out, void *row_out,
+                    const double *V_cur, double *ratio_out,
+                    void *workspace, size_t workspace_bytes,
+                    void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* qj2_ratio: ratio_out[w][p] = (dJ2, exp(dJ2)), dJ2 = out[w][p][0] - ref,   */
+/* ref = V_cur[w] or out[w][0][0] when V_cur == NULL (Eq. 4-5, PAPER:875-887,*/
+/* PAPER:1382).  For sharded evaluation after the partial sums are reduced.  */
+/* out, V_cur, ratio_out: device fp64.  W >= 0, 1 <= P <= QJ2_MAX_P.         */
+/* ------------------------------------------------------------------------ */
+qj2_status qj2_ratio(int64_t W, int32_t P, const double *out, const double *V_cur,
+                     double *ratio_out, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Host-buffer variant of qj2_eval (the end-to-end path): R, k, r_trial are  */
+/* HOST arrays (pinned for full PCIe rate), out (and ratio_out if non-NULL)  */
+/* HOST arrays, same shapes as qj2_eval.  Walkers are streamed in chunks of  */
+/* chunk_walkers through two device staging buffers carved from workspace:  */
+/* the host->device copy of chunk c+1 overlaps the kernel of chunk c.        */
+/* Blocking: returns after out is written (synchronises `stream`).           */
+/* workspace: device, >= qj2_eval_host_workspace_size(), zero-filled before  */
+/* its first use.                                                            */
+/* ------------------------------------------------------------------------ */
+qj2_status qj2_eval_host_workspace_size(int64_t W, int32_t P, int64_t Np,
+                                        qj2_dtype dtype, int64_t chunk_walkers,
+                                        size_t *bytes);
+qj2_status qj2_eval_host(const qj2_functor *fn, qj2_dtype dtype,
+                         int64_t W, int64_t N_total, int64_t N_up,
+                         int64_t i_offset, int64_t N_local, int64_t Np,
+                         const void *R_host, const int32_t *k_host,
+                         int32_t P, const void *r_trial_host,
+                         double *out_host, const double *V_cur_host,
+                         double *ratio_out_host,
+                         int64_t chunk_walkers,
+                         void *workspace, size_t workspace_bytes,
+                         void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Building blocks, batched on the device (for tests and callers):           */
+/* qj2_functor_eval_vgl: out[n][3] fp64 = (U_s, U_s', U_s'')  */
+/*   at r[n] (device, dtype), channel s in {0, 1}; zero for r >= r_cut.      */
+/* qj2_min_image_disp: out[n][4] dtype =                 */
+/*   (|d|, dx, dy, dz), d = minimg(b - a), a/b device [n][3] dtype in        */
+/*   [0, L_d); components in (-L_d/2, L_d/2] (+-1 ulp at exact ties).        */
+/* ------------------------------------------------------------------------ */
+qj2_status qj2_functor_eval_vgl(const qj2_functor *fn, qj2_dtype dtype, int32_t channel,
+                                int64_t n, const void *r, double *out, void *stream);
+qj2_status qj2_min_image_disp(const double L[3], qj2_dtype dtype, int64_t n,
+                              const void *a, const void *b, void *out, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Optional device-side precondition scan for qj2_eval's data.  ORs into     */
+/* *d_flag (device int32, caller zeroes it): 1 = coordinate outside [0,L_d)  */
+/* or non-finite in R[:, :, :N_local], 2 = k outside [0, N_total),           */
+/* 4 = r_trial coordinate outside [0, L_d) or non-finite.                    */
+/* ------------------------------------------------------------------------ */
+qj2_status qj2_check_inputs(const qj2_functor *fn, qj2_dtype dtype,
+                            int64_t W, int64_t N_total, int64_t N_local, int64_t Np,
+                            const void *R, const int32_t *k,
+                            int32_t P, const void *r_trial,
+                            int32_t *d_flag, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Synthetic-input generator (test/bench harness, NOT part of the method):   */
+/* writes R[w][d][i] for w in [0, W), i in [0, Np) as the counter-based      */
+/* hash recipe of qmcgen/ (DESIGN.md "Input recipe"):                        */
+/*   key = mix64(seed*G + G), h = mix64(key ^ (((w_offset+w)*3 + d) << 32   */
+/*         | (i_offset+i))), u = top 24 (fp32) / 53 (fp64) bits of h,        */
+/*   x = fl(L*u) kept below L; padding slots i >= N_local are 0.             */
+/* R: device [W][3][Np] dtype.                                               */
+/* ------------------------------------------------------------------------ */
+qj2_status qj2gen_positions(qj2_dtype dtype, uint64_t seed, int64_t W, int64_t w_offset,
+                            int64_t i_offset, int64_t N_local, int64_t Np,
+                            double L, void *R, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QMCJ2_H */

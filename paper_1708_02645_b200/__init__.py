@@ -1,0 +1,331 @@
+"""paper_1708_02645_b200 -- B200-native hot path of arXiv 1708.02645.
+
+Thin Python binding over the C ABI in include/qmcj2.h (libqmcj2.so, built
+in-tree by _build.py).  This module only marshals arguments: every step of the
+hot path runs in the CUDA kernels of csrc/.  PyTorch provides device memory and
+streams.  There is no CPU fallback: importing this package without the built
+library raises, and every call goes to the GPU library.
+
+Public API (names follow include/qmcj2.h):
+    eval(R, k, r_trial, fn, n_total, n_up, ...)   -> out [W][P][5] fp64 (and row, ratio)
+    eval_host(R, k, r_trial, fn, ...)             -> host-buffer end-to-end path
+    ratio(out, V_cur=None)                        -> [W][P][2] (dJ2, exp(dJ2))
+    functor_eval_vgl(fn, channel, r)              -> [n][3] (U, U', U'')
+    min_image_disp(L, a, b)                       -> [n][4] (|d|, dx, dy, dz)
+    check_inputs(...), padded_size(n, block), gen_positions(...)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+from . import _build
+
+__all__ = ["QJ2Error", "Functor", "Workspace", "eval", "eval_host", "ratio", "functor_eval_vgl",
+           "min_image_disp", "check_inputs", "padded_size", "gen_positions", "lib_path",
+           "workspace_size", "host_workspace_size", "version", "device_check"]
+
+QJ2_FP32, QJ2_FP64 = 0, 1
+QJ2_MAX_M = 64
+QJ2_MAX_P = 64
+
+
+class QJ2Error(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        super().__init__(f"{where}: status {status} ({detail})")
+        self.status = status
+
+
+class _Functor(ctypes.Structure):
+    _fields_ = [("L", ctypes.c_double * 3),
+                ("r_cut", ctypes.c_double),
+                ("m", ctypes.c_int32),
+                ("reserved", ctypes.c_int32),
+                ("coef", (ctypes.c_double * (QJ2_MAX_M + 3)) * 2)]
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def _load():
+    if not os.path.exists(_build.LIB):
+        raise ImportError(f"{_build.LIB} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(no CPU fallback exists)")
+    lib = ctypes.CDLL(_build.LIB)
+    i64, i32, vp, dp = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)
+    F = ctypes.POINTER(_Functor)
+    sz = ctypes.c_size_t
+    sigs = {
+        "qj2_version": (i32, []),
+        "qj2_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+        "qj2_last_error": (ctypes.c_char_p, []),
+        "qj2_device_check": (ctypes.c_int, []),
+        "qj2_padded_size": (ctypes.c_int, [i64, i64, ctypes.POINTER(i64)]),
+        "qj2_eval_workspace_size": (ctypes.c_int, [i64, i32, i64, ctypes.c_int, ctypes.POINTER(sz)]),
+        "qj2_eval": (ctypes.c_int, [F, ctypes.c_int, i64, i64, i64, i64, i64, i64, vp, vp, i32, vp,
+                                    vp, vp, vp, vp, vp, sz, vp]),
+        "qj2_ratio": (ctypes.c_int, [i64, i32, vp, vp, vp, vp]),
+        "qj2_eval_host_workspace_size": (ctypes.c_int, [i64, i32, i64, ctypes.c_int, i64, ctypes.POINTER(sz)]),
+        "qj2_eval_host": (ctypes.c_int, [F, ctypes.c_int, i64, i64, i64, i64, i64, i64, vp, vp, i32, vp,
+                                         vp, vp, vp, i64, vp, sz, vp]),
+        "qj2_functor_eval_vgl": (ctypes.c_int, [F, ctypes.c_int, i32, i64, vp, vp, vp]),
+        "qj2_min_image_disp": (ctypes.c_int, [dp, ctypes.c_int, i64, vp, vp, vp, vp]),
+        "qj2_check_inputs": (ctypes.c_int, [F, ctypes.c_int, i64, i64, i64, i64, vp, vp, i32, vp, vp, vp]),
+        "qj2gen_positions": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, i64, i64, i64, i64, i64,
+                                            ctypes.c_double, vp, vp]),
+    }
+    for name, (res, args) in sigs.items():
+        fnc = getattr(lib, name)
+        fnc.restype = res
+        fnc.argtypes = args
+    return lib
+
+
+_lib = _load()
+EXPORTS = ("qj2_version", "qj2_status_string", "qj2_last_error", "qj2_device_check", "qj2_padded_size",
+           "qj2_eval_workspace_size", "qj2_eval", "qj2_ratio", "qj2_eval_host_workspace_size",
+           "qj2_eval_host", "qj2_functor_eval_vgl", "qj2_min_image_disp", "qj2_check_inputs",
+           "qj2gen_positions")
+
+
+def _check(st: int, where: str):
+    if st != 0:
+        detail = _lib.qj2_last_error().decode() or _lib.qj2_status_string(st).decode()
+        raise QJ2Error(st, where, detail)
+
+
+def version() -> int:
+    return _lib.qj2_version()
+
+
+def device_check():
+    _check(_lib.qj2_device_check(), "qj2_device_check")
+
+
+class Functor:
+    """Functor + cell in the C layout (qj2_functor)."""
+
+    def __init__(self, L, r_cut: float, m: int, coef):
+        coef = np.asarray(coef, dtype=np.float64)
+        if coef.shape != (2, m + 3):
+            raise ValueError(f"coef must be [2][m+3], got {coef.shape}")
+        self.L = tuple(float(x) for x in (L if np.ndim(L) else (L, L, L)))
+        self.r_cut, self.m, self.coef = float(r_cut), int(m), coef
+        c = _Functor()
+        for d in range(3):
+            c.L[d] = self.L[d]
+        c.r_cut, c.m, c.reserved = self.r_cut, self.m, 0
+        for s in range(2):
+            for j in range(m + 3):
+                c.coef[s][j] = float(coef[s, j])
+        self._c = c
+
+    @classmethod
+    def of(cls, fn) -> "Functor":
+        return fn if isinstance(fn, Functor) else cls(fn.L, fn.r_cut, fn.m, fn.coef)
+
+    @property
+    def ptr(self):
+        return ctypes.byref(self._c)
+
+
+def _dtype_code(t: torch.dtype) -> int:
+    if t == torch.float32:
+        return QJ2_FP32
+    if t == torch.float64:
+        return QJ2_FP64
+    raise TypeError(f"positions must be float32 or float64, got {t}")
+
+
+def _stream_ptr(stream) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _req(t: torch.Tensor, name: str, dtype=None, ndim=None):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if ndim is not None and t.dim() != ndim:
+        raise ValueError(f"{name} must have {ndim} dims, got {t.dim()}")
+
+
+def padded_size(n: int, block: int) -> int:
+    out = ctypes.c_int64()
+    _check(_lib.qj2_padded_size(int(n), int(block), ctypes.byref(out)), "qj2_padded_size")
+    return out.value
+
+
+def workspace_size(W: int, P: int, n_local: int, dtype: torch.dtype) -> int:
+    b = ctypes.c_size_t()
+    _check(_lib.qj2_eval_workspace_size(W, P, n_local, _dtype_code(dtype), ctypes.byref(b)),
+           "qj2_eval_workspace_size")
+    return b.value
+
+
+class Workspace:
+    """Reusable zero-initialised device scratch for qj2_eval (the library
+    leaves its counters zero after each completed call)."""
+
+    def __init__(self, nbytes: int = 0, device=None):
+        self.device = device
+        self.buf = None
+        self.reserve(nbytes)
+
+    def reserve(self, nbytes: int):
+        if nbytes > 0 and (self.buf is None or self.buf.numel() < nbytes):
+            self.buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8,
+                                   device=self.device or torch.cuda.current_device())
+        return self
+
+    @property
+    def nbytes(self) -> int:
+        return 0 if self.buf is None else self.buf.numel()
+
+
+def eval(R, k, r_trial, fn, n_total: int, n_up: int, *, i_offset: int = 0, n_local: int | None = None,
+         row: bool = False, V_cur=None, ratio: bool = False, out=None, row_out=None, ratio_out=None,
+         workspace: Workspace | None = None, stream=None):
+    """qj2_eval on torch tensors (see include/qmcj2.h).
+
+    R [W][3][Np] f32/f64, k [W] int32, r_trial [W][P][3] (same dtype as R).
+    Returns out [W][P][5] fp64, plus row [W][P][4][Np] if row=True and
+    ratio [W][P][2] if ratio=True.
+    """
+    _req(R, "R", ndim=3)
+    W, three, Np = R.shape
+    if three != 3:
+        raise ValueError("R must be [W][3][Np]")
+    _req(k, "k", torch.int32, 1)
+    _req(r_trial, "r_trial", R.dtype, 3)
+    P = r_trial.shape[1]
+    if k.shape[0] != W or r_trial.shape[0] != W or r_trial.shape[2] != 3:
+        raise ValueError("shape mismatch between R, k and r_trial")
+    n_local = min(Np, n_total - i_offset) if n_local is None else int(n_local)
+    f = Functor.of(fn)
+    dev = R.device
+    if out is None:
+        out = torch.empty((W, P, 5), dtype=torch.float64, device=dev)
+    _req(out, "out", torch.float64)
+    if row and row_out is None:
+        row_out = torch.empty((W, P, 4, Np), dtype=R.dtype, device=dev)
+    if ratio and ratio_out is None:
+        ratio_out = torch.empty((W, P, 2), dtype=torch.float64, device=dev)
+    if V_cur is not None:
+        _req(V_cur, "V_cur", torch.float64, 1)
+    need = workspace_size(max(W, 0), P, max(n_local, 1), R.dtype) if W > 0 and n_local >= 1 else 0
+    ws = workspace if workspace is not None else Workspace(device=dev)
+    ws.reserve(need)
+    st = _lib.qj2_eval(f.ptr, _dtype_code(R.dtype), W, n_total, n_up, i_offset, n_local, Np,
+                       _ptr(R), _ptr(k), P, _ptr(r_trial), _ptr(out),
+                       _ptr(row_out) if row else None, _ptr(V_cur), _ptr(ratio_out) if ratio else None,
+                       _ptr(ws.buf), ws.nbytes, ctypes.c_void_p(_stream_ptr(stream)))
+    _check(st, "qj2_eval")
+    res = [out]
+    if row:
+        res.append(row_out)
+    if ratio:
+        res.append(ratio_out)
+    return res[0] if len(res) == 1 else tuple(res)
+
+
+def ratio(out, V_cur=None, ratio_out=None, stream=None):
+    """qj2_ratio: (dJ2, exp(dJ2)) per (w, p) from (reduced) `out`."""
+    _req(out, "out", torch.float64, 3)
+    W, P, _ = out.shape
+    if ratio_out is None:
+        ratio_out = torch.empty((W, P, 2), dtype=torch.float64, device=out.device)
+    if V_cur is not None:
+        _req(V_cur, "V_cur", torch.float64, 1)
+    _check(_lib.qj2_ratio(W, P, _ptr(out), _ptr(V_cur), _ptr(ratio_out), ctypes.c_void_p(_stream_ptr(stream))),
+           "qj2_ratio")
+    return ratio_out
+
+
+def host_workspace_size(W, P, Np, dtype, chunk_walkers) -> int:
+    b = ctypes.c_size_t()
+    _check(_lib.qj2_eval_host_workspace_size(W, P, Np, _dtype_code(dtype), chunk_walkers, ctypes.byref(b)),
+           "qj2_eval_host_workspace_size")
+    return b.value
+
+
+def eval_host(R, k, r_trial, fn, n_total: int, n_up: int, *, i_offset: int = 0, n_local: int | None = None,
+              V_cur=None, ratio: bool = False, chunk_walkers: int = 16, out=None, ratio_out=None,
+              workspace: Workspace | None = None, stream=None):
+    """qj2_eval_host: HOST tensors in (pinned for full PCIe rate), host out.
+
+    R [W][3][Np] (CPU torch tensor), k [W] int32, r_trial [W][P][3]; returns
+    out [W][P][5] fp64 CPU tensor (and ratio [W][P][2])."""
+    for t, nm in ((R, "R"), (k, "k"), (r_trial, "r_trial")):
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"{nm} must be a contiguous host tensor")
+    W, _, Np = R.shape
+    P = r_trial.shape[1]
+    n_local = min(Np, n_total - i_offset) if n_local is None else int(n_local)
+    if out is None:
+        out = torch.empty((W, P, 5), dtype=torch.float64, pin_memory=R.is_pinned())
+    if ratio and ratio_out is None:
+        ratio_out = torch.empty((W, P, 2), dtype=torch.float64, pin_memory=R.is_pinned())
+    f = Functor.of(fn)
+    need = host_workspace_size(W, P, Np, R.dtype, chunk_walkers)
+    ws = workspace if workspace is not None else Workspace(device=torch.cuda.current_device())
+    ws.reserve(need)
+    st = _lib.qj2_eval_host(f.ptr, _dtype_code(R.dtype), W, n_total, n_up, i_offset, n_local, Np,
+                            _ptr(R), _ptr(k), P, _ptr(r_trial), _ptr(out), _ptr(V_cur),
+                            _ptr(ratio_out) if ratio else None, chunk_walkers,
+                            _ptr(ws.buf), ws.nbytes, ctypes.c_void_p(_stream_ptr(stream)))
+    _check(st, "qj2_eval_host")
+    return (out, ratio_out) if ratio else out
+
+
+def functor_eval_vgl(fn, channel: int, r, stream=None):
+    _req(r, "r", ndim=1)
+    f = Functor.of(fn)
+    out = torch.empty((r.shape[0], 3), dtype=torch.float64, device=r.device)
+    _check(_lib.qj2_functor_eval_vgl(f.ptr, _dtype_code(r.dtype), channel, r.shape[0], _ptr(r), _ptr(out),
+                                     ctypes.c_void_p(_stream_ptr(stream))), "qj2_functor_eval_vgl")
+    return out
+
+
+def min_image_disp(L, a, b, stream=None):
+    _req(a, "a", ndim=2)
+    _req(b, "b", a.dtype, 2)
+    Ls = (ctypes.c_double * 3)(*[float(x) for x in (L if np.ndim(L) else (L, L, L))])
+    out = torch.empty((a.shape[0], 4), dtype=a.dtype, device=a.device)
+    _check(_lib.qj2_min_image_disp(Ls, _dtype_code(a.dtype), a.shape[0], _ptr(a), _ptr(b), _ptr(out),
+                                   ctypes.c_void_p(_stream_ptr(stream))), "qj2_min_image_disp")
+    return out
+
+
+def check_inputs(R, k, r_trial, fn, n_total: int, n_local: int | None = None, stream=None) -> int:
+    """Device precondition scan; returns the flag bits (0 = clean)."""
+    W, _, Np = R.shape
+    n_local = min(Np, n_total) if n_local is None else n_local
+    flag = torch.zeros(1, dtype=torch.int32, device=R.device)
+    f = Functor.of(fn)
+    _check(_lib.qj2_check_inputs(f.ptr, _dtype_code(R.dtype), W, n_total, n_local, Np, _ptr(R), _ptr(k),
+                                 r_trial.shape[1], _ptr(r_trial), _ptr(flag),
+                                 ctypes.c_void_p(_stream_ptr(stream))), "qj2_check_inputs")
+    return int(flag.item())
+
+
+def gen_positions(seed: int, W: int, N_local: int, Np: int, L: float, dtype=torch.float32, *,
+                  w_offset: int = 0, i_offset: int = 0, out=None, stream=None, device=None):
+    """Device synthetic-input generator (harness; same recipe as qmcgen)."""
+    if out is None:
+        out = torch.empty((W, 3, Np), dtype=dtype, device=device or torch.cuda.current_device())
+    _check(_lib.qj2gen_positions(_dtype_code(out.dtype), int(seed) & 0xFFFFFFFFFFFFFFFF, W, w_offset,
+                                 i_offset, N_local, Np, float(L), _ptr(out),
+                                 ctypes.c_void_p(_stream_ptr(stream))), "qj2gen_positions")
+    return out

@@ -1,0 +1,164 @@
+// j2_device.cuh -- device building blocks of the J2 / distance-row hot path
+// (arXiv 1708.02645), written for sm_100a.  Product code: shares nothing with
+// oracle/.
+//
+// Layout/precision decisions are in DESIGN.md ("Kernels").  In short:
+//  * minimum image with a single rounding (case split on the trial coordinate,
+//    exact shifts by Sterbenz's lemma) -- PAPER:1298-1304, SPEC:113-121, 138;
+//  * functor as a per-interval power basis in shared memory, evaluated by
+//    Horner with branch-free cutoff (index clamped onto an all-zero interval)
+//    -- PAPER:817-819, 1473-1475 ("branch conditions originated from the
+//    finite cutoff");
+//  * 1/r from MUFU rsqrt (fp32) / accurate rsqrt (fp64).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace qj2 {
+
+// ---------------------------------------------------------------------------
+// Type traits
+// ---------------------------------------------------------------------------
+template <typename T> struct Traits;
+
+template <> struct Traits<float> {
+    using V = float4;                       // 16-byte vector of sources
+    static constexpr int VW = 4;
+    using U = unsigned int;
+    static constexpr float MAGIC = 12582912.0f;          // 1.5 * 2^23
+    static constexpr unsigned MAGIC_BITS = 0x4B400000u;  // bits of MAGIC
+    static __device__ __forceinline__ float add_rd(float a, float b) { return __fadd_rd(a, b); }
+    static __device__ __forceinline__ unsigned bits(float a) { return __float_as_uint(a); }
+    static __device__ __forceinline__ float rsqrt(float x) {
+        float y;
+        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+        return y;
+    }
+    static __device__ __forceinline__ float4 ld_stream(const float4 *p) {
+        float4 v;
+        asm("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+            : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+        return v;
+    }
+    static __device__ __forceinline__ float comp(const float4 &v, int e) {
+        return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+    }
+    static __device__ __forceinline__ void set(float4 &v, int e, float x) {
+        if (e == 0) v.x = x; else if (e == 1) v.y = x; else if (e == 2) v.z = x; else v.w = x;
+    }
+    static __device__ __forceinline__ float below(float L) {   // largest float < L (L > 0)
+        return __uint_as_float(__float_as_uint(L) - 1u);
+    }
+};
+
+template <> struct Traits<double> {
+    using V = double2;
+    static constexpr int VW = 2;
+    using U = unsigned long long;
+    static constexpr double MAGIC = 6755399441055744.0;                  // 1.5 * 2^52
+    static constexpr unsigned long long MAGIC_BITS = 0x4338000000000000ull;
+    static __device__ __forceinline__ double add_rd(double a, double b) { return __dadd_rd(a, b); }
+    static __device__ __forceinline__ unsigned long long bits(double a) {
+        return (unsigned long long)__double_as_longlong(a);
+    }
+    static __device__ __forceinline__ double rsqrt(double x) { return ::rsqrt(x); }
+    static __device__ __forceinline__ double2 ld_stream(const double2 *p) {
+        double2 v;
+        asm("ld.global.nc.L1::no_allocate.L2::256B.v2.f64 {%0,%1}, [%2];"
+            : "=d"(v.x), "=d"(v.y) : "l"(p));
+        return v;
+    }
+    static __device__ __forceinline__ double comp(const double2 &v, int e) { return e == 0 ? v.x : v.y; }
+    static __device__ __forceinline__ void set(double2 &v, int e, double x) {
+        if (e == 0) v.x = x; else v.y = x;
+    }
+    static __device__ __forceinline__ double below(double L) {
+        return __longlong_as_double(__double_as_longlong(L) - 1ll);
+    }
+};
+
+// One interval of the functor in power basis: U(f) = a0 + a1 f + a2 f^2 + a3 f^3,
+// f in [0,1) the fractional position inside the interval.  Interval m (and
+// every clamped index beyond) is all zeros: U = U' = U'' = 0 at r >= r_cut.
+template <typename T> struct alignas(4 * sizeof(T)) Coef4 { T a0, a1, a2, a3; };
+
+// ---------------------------------------------------------------------------
+// Minimum image with one rounding.
+// For a trial coordinate c in [0, L) only one wrap direction is possible:
+//   case A (c <  L/2): wrap iff x > c + L/2, then d = (x - L) - c, where x - L
+//                      is exact (x in [L/2, L): Sterbenz);
+//   case B (c >= L/2): wrap iff x <= c - L/2, then d = x - (c - L), where
+//                      c - L is exact.
+// Unified per trial coordinate with 4 constants so the inner loop has no
+// data-dependent branch:  hit = x > thr;  xs = hit ? x - a1 : x;
+//                         d = xs - (hit ? b1 : b0).
+// ---------------------------------------------------------------------------
+template <typename T> struct Axis { T thr, a1, b1, b0; };
+
+template <typename T>
+__device__ __forceinline__ Axis<T> make_axis(T c, T L) {
+    Axis<T> a;
+    const T half = L * T(0.5);
+    if (c < half) {               // case A
+        a.thr = c + half;         // rounding here only matters at |d| = L/2 (+-1 ulp)
+        a.a1 = L;
+        a.b1 = c;
+        a.b0 = c;
+    } else {                      // case B: "hit" means no wrap
+        a.thr = c - half;         // exact (Sterbenz)
+        a.a1 = T(0);
+        a.b1 = c;
+        a.b0 = c - L;             // exact (Sterbenz)
+    }
+    return a;
+}
+
+template <typename T>
+__device__ __forceinline__ T min_image(T x, const Axis<T> &a) {
+    const bool hit = x > a.thr;
+    const T xs = hit ? x - a.a1 : x;
+    return xs - (hit ? a.b1 : a.b0);
+}
+
+// ---------------------------------------------------------------------------
+// Functor evaluation from t = r/delta (power basis, Horner).
+//   returns u = U, du = U' * delta, h = U'' * delta^2 / 2.
+// The interval index j = floor(t) is obtained with the round-down magic-number
+// add (no F2I), clamped to m (the zero interval).
+// tab_base: shared-memory byte address of interval 0 of the channel, minus
+// MAGIC_BITS * sizeof(Coef4) (so bits * sizeof(Coef4) + tab_base addresses j).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void ld_shared_c4(uint32_t addr, float &a0, float &a1, float &a2, float &a3) {
+    asm("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3) : "r"(addr));
+}
+__device__ __forceinline__ void ld_shared_c4(uint32_t addr, double &a0, double &a1, double &a2, double &a3) {
+    asm("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(a0), "=d"(a1) : "r"(addr));
+    asm("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(a2), "=d"(a3) : "r"(addr + 16));
+}
+
+template <typename T>
+struct FunctorEval {
+    T u, du, h;
+};
+
+template <typename T>
+__device__ __forceinline__ FunctorEval<T> functor_from_t(T t, uint32_t tab_base, typename Traits<T>::U clamp_bits) {
+    using Tr = Traits<T>;
+    const T tf = Tr::add_rd(t, Tr::MAGIC);                // MAGIC + floor(t)
+    typename Tr::U jb = Tr::bits(tf);
+    jb = jb < clamp_bits ? jb : clamp_bits;              // j = min(floor(t), m)
+    const T f = t - (tf - Tr::MAGIC);
+    T a0, a1, a2, a3;
+    ld_shared_c4(tab_base + (uint32_t)jb * (uint32_t)sizeof(Coef4<T>), a0, a1, a2, a3);
+    FunctorEval<T> e;
+    const T p = fma(a3, f, a2);       // a2 + a3 f
+    const T q = fma(p, f, a1);        // a1 + a2 f + a3 f^2
+    e.u = fma(q, f, a0);              // U
+    const T r1 = fma(a3, f, p);       // a2 + 2 a3 f
+    e.du = fma(r1, f, q);             // a1 + 2 a2 f + 3 a3 f^2   = U' delta
+    e.h = fma(a3, f, r1);             // a2 + 3 a3 f              = U'' delta^2 / 2
+    return e;
+}
+
+}  // namespace qj2

@@ -231,4 +231,6 @@ def host_instance(cfg: Config, seed: int | None = None, walkers=None, P: int = 1
     k = k_all[walkers]
     R = positions(seed, walkers, cfg.N, cfg.Np, L, cfg.np_dtype)
     rt = make_trials(seed, walkers, k, cfg.N, L, cfg.np_dtype, P=P, mode=mode)
-    return R, k, rt, make_functor(seed, L, cfg.m)
+    # the functor is a property of the system: one per config (C4's 4096
+    # instances share it; their seeds only change positions and moves)
+    return R, k, rt, make_functor(cfg.seed, L, cfg.m)

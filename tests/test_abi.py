@@ -1,0 +1,122 @@
+"""C-ABI library: loads on CPU and exports every symbol include/qmcj2.h
+declares; host-side validation paths that return before any CUDA call.
+No compute calls (no GPU here)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "qmcj2.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"\b(qj2\w*)\s*\(", src)
+    return sorted(set(names))
+
+
+@pytest.fixture(scope="module")
+def q():
+    from paper_1708_02645_b200 import _build
+    _build.build()
+    import paper_1708_02645_b200 as q
+    return q
+
+
+def test_header_symbols_exported(q):
+    lib = ctypes.CDLL(q.lib_path())
+    names = _declared_symbols()
+    assert len(names) >= 14, names
+    for n in names:
+        assert hasattr(lib, n), f"{n} declared in qmcj2.h but not exported"
+    assert set(names) == set(q.EXPORTS)
+
+
+def test_version_and_status_strings(q):
+    assert q.version() == 10000
+    lib = q._lib
+    assert lib.qj2_status_string(0) == b"ok"
+    assert lib.qj2_status_string(1) == b"invalid-argument"
+    assert lib.qj2_status_string(2) == b"out-of-range"
+
+
+def test_padded_size_examples(q):
+    # SPEC:38-40
+    assert q.padded_size(5, 8) == 8
+    assert q.padded_size(16, 8) == 16
+    assert q.padded_size(768, 16) == 768
+    assert q.padded_size(0, 32) == 32
+    with pytest.raises(q.QJ2Error) as ei:
+        q.padded_size(5, 0)
+    assert ei.value.status == 1
+
+
+def _functor(q, **kw):
+    import qmcgen
+    fn = qmcgen.make_functor(0, 10.0)
+    f = q.Functor(fn.L, fn.r_cut, fn.m, fn.coef)
+    for a, v in kw.items():
+        setattr(f._c, a, v)
+    return f
+
+
+def _call_eval(q, f, **over):
+    args = dict(dtype=0, W=4, N_total=100, N_up=50, i_offset=0, N_local=100, Np=128,
+                R=ctypes.c_void_p(4096), k=ctypes.c_void_p(4096), P=1, rt=ctypes.c_void_p(4096),
+                out=ctypes.c_void_p(4096), row=None, vcur=None, ratio=None, ws=ctypes.c_void_p(4096),
+                wsb=1 << 30)
+    args.update(over)
+    st = q._lib.qj2_eval(f.ptr, args["dtype"], args["W"], args["N_total"], args["N_up"], args["i_offset"],
+                         args["N_local"], args["Np"], args["R"], args["k"], args["P"], args["rt"],
+                         args["out"], args["row"], args["vcur"], args["ratio"], args["ws"], args["wsb"], None)
+    return st, q._lib.qj2_last_error().decode()
+
+
+def test_eval_host_validation(q):
+    f = _functor(q)
+    assert _call_eval(q, f, N_total=1)[0] == 1
+    assert _call_eval(q, f, N_up=101)[0] == 2
+    assert _call_eval(q, f, i_offset=50, N_local=60)[0] == 2
+    assert _call_eval(q, f, Np=99)[0] == 1           # not a multiple of 4
+    assert _call_eval(q, f, Np=64)[0] == 1           # Np < N_local
+    assert _call_eval(q, f, P=0)[0] == 1
+    assert _call_eval(q, f, dtype=7)[0] == 1
+    assert _call_eval(q, f, R=None)[0] == 1
+    assert _call_eval(q, f, R=ctypes.c_void_p(4100))[0] == 1     # misaligned
+    assert _call_eval(q, f, i_offset=10, N_local=20, ratio=ctypes.c_void_p(4096))[0] == 1
+    assert _call_eval(q, f, P=8, ratio=ctypes.c_void_p(4096))[0] == 1   # needs V_cur
+    assert _call_eval(q, f, W=0) == (0, _call_eval(q, f, W=0)[1])      # no-op
+    st, msg = _call_eval(q, f, N_local=1 << 20, Np=1 << 20, N_total=1 << 20, wsb=16)
+    assert st == 1 and "workspace" in msg
+
+
+def test_functor_validation(q):
+    assert _call_eval(q, _functor(q, m=3))[0] == 1
+    assert _call_eval(q, _functor(q, m=65))[0] == 1
+    assert _call_eval(q, _functor(q, r_cut=5.01))[0] == 1       # > L/2
+    f = _functor(q)
+    f._c.coef[0][f.m] = 0.5                                     # tail must be zero
+    assert _call_eval(q, f)[0] == 1
+    assert _call_eval(q, _functor(q, reserved=1))[0] == 1
+
+
+def test_workspace_size(q):
+    import torch
+    assert q.workspace_size(1024, 1, 1400, torch.float32) == 0            # one tile per walker
+    b = q.workspace_size(1024, 1, 614400, torch.float32)
+    assert b >= 1024 * 75 * 6 * 8 + 1024 * 4
+    assert q.workspace_size(8, 3, 20000, torch.float64) > 0
+
+
+def test_package_has_no_cpu_fallback():
+    """The product package must not import the oracle (no CPU path)."""
+    pkg = os.path.join(ROOT, "paper_1708_02645_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, fn)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, fn
+                assert "liboracle" not in txt, fn

@@ -1,0 +1,318 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by
+element on the same seeded inputs (-m gpu; needs a B200).
+
+Tolerance: per output component
+|s_gpu - s_orc| / max(A_s, F_s) <= 1e-5 (fp32 path) or 1e-12 (fp64 path),
+A_s the oracle's absolute-term sum, F_s the functor scale.  Row output:
+dx, dy, dz bit-exact in fp32 (except exact |d| = L/2 ties), r within 3 ulp.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import qmcgen
+
+pytestmark = pytest.mark.gpu
+
+TOL = {np.float32: 1e-5, np.float64: 1e-12}
+THREADS = os.cpu_count() or 1
+
+
+@pytest.fixture(scope="module")
+def q():
+    import paper_1708_02645_b200 as q
+    assert torch.cuda.is_available()
+    q.device_check()
+    return q
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def instance(N, W, seed, dtype, P=1, mode="move", Np=None, m=8, n_up=None):
+    L = qmcgen.cell_length(N)
+    vw = 4 if dtype == np.float32 else 2
+    Np = Np or qmcgen.padded_size(N, vw)
+    walkers = np.arange(W)
+    R = qmcgen.positions(seed, walkers, N, Np, L, dtype)
+    k = qmcgen.make_k(seed, W, N) if W else np.zeros(0, np.int32)
+    rt = (qmcgen.make_trials(seed, walkers, k, N, L, dtype, P=P, mode=mode) if W
+          else np.zeros((0, P, 3), dtype))
+    fn = qmcgen.make_functor(seed, L, m)
+    return R, k, rt, fn, (N // 2 if n_up is None else n_up)
+
+
+def check(q, R, k, rt, fn, N, n_up, dtype, i_offset=0, n_local=None, row=False):
+    res = q.eval(dev(R), dev(k), dev(rt), fn, N, n_up, i_offset=i_offset, n_local=n_local, row=row)
+    torch.cuda.synchronize()
+    out = (res[0] if row else res).cpu().numpy()
+    orc, absout, orow = oracle.eval_j2(R, k, rt, fn, N, n_up, i_offset=i_offset, n_local=n_local,
+                                       row=row, threads=THREADS)
+    err = oracle.normalized_error(out, orc, absout, fn)
+    assert np.all(np.isfinite(out))
+    assert err.max() <= TOL[dtype], f"max normalized error {err.max():.3e}"
+    if row:
+        return out, orc, res[1].cpu().numpy(), orow
+    return out, orc
+
+
+# ---------------------------------------------------------------------------
+# Configs C1, C2 (fp32 and fp64) in full
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["C1", "C2", "C2f64"])
+def test_config_full(q, name):
+    cfg = qmcgen.CONFIGS[name]
+    R, k, rt, fn = qmcgen.host_instance(cfg)
+    check(q, R, k, rt, fn, cfg.N, cfg.n_up, cfg.np_dtype)
+
+
+# ---------------------------------------------------------------------------
+# Edge cases: tiny / ragged / tile boundaries / spin boundary / P groups
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("N", [2, 3, 5, 17, 1023, 8191, 8192, 8193, 20001])
+def test_ragged_sizes(q, dtype, N):
+    R, k, rt, fn, n_up = instance(N, 37, seed=100 + N, dtype=dtype)
+    check(q, R, k, rt, fn, N, n_up, dtype)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_k_at_tile_and_spin_boundaries(q, dtype):
+    N = 3 * 8192 + 77
+    R, k, rt, fn, _ = instance(N, 12, seed=7, dtype=dtype)
+    ks = np.array([0, 1, 4095, 4096, 8191, 8192, 8193, 12288, 16383, N - 2, N - 1, N // 2], np.int32)
+    L = qmcgen.cell_length(N)
+    rt = qmcgen.make_trials(7, np.arange(12), ks, N, L, dtype)
+    for n_up in (N // 2, 8192, 8190, 0, N, 1):   # spin boundary inside / on a tile edge / degenerate
+        check(q, R, ks, rt, fn, N, n_up, dtype)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("P", [2, 3, 4, 5, 9])
+def test_multi_trial(q, dtype, P):
+    R, k, rt, fn, n_up = instance(9000, 9, seed=200 + P, dtype=dtype, P=P)
+    check(q, R, k, rt, fn, 9000, n_up, dtype)
+
+
+def test_empty_batch(q):
+    R, k, rt, fn, n_up = instance(100, 0, seed=1, dtype=np.float32)
+    out = q.eval(dev(R), dev(k), dev(rt), fn, 100, n_up)
+    assert out.shape == (0, 1, 5)
+
+
+def test_single_walker_and_larger_m(q):
+    for m in (4, 13, 64):
+        R, k, rt, fn, n_up = instance(4000, 1, seed=300 + m, dtype=np.float32, m=m)
+        check(q, R, k, rt, fn, 4000, n_up, np.float32)
+
+
+def test_noop_move_ratio_exactly_one(q):
+    """P = 2 with r_trial[0] == r_trial[1] (no-op move): dJ2 = 0 bitwise,
+    ratio 1."""
+    for dtype in (np.float32, np.float64):
+        R, k, rt, fn, n_up = instance(30000, 16, seed=11, dtype=dtype, P=2, mode="noop")
+        out, ratio = q.eval(dev(R), dev(k), dev(rt), fn, 30000, n_up, ratio=True)
+        ratio = ratio.cpu().numpy()
+        assert np.all(ratio[:, :, 0] == 0.0) and np.all(ratio[:, :, 1] == 1.0)
+
+
+def test_ratio_against_oracle_delta_j2(q):
+    """P = 2 drift variant: dJ2 = V(r'_k) - V(r_k) (Eq. 5) and exp(dJ2) (Eq. 4)."""
+    R, k, rt, fn, n_up = instance(20000, 32, seed=12, dtype=np.float64, P=2, mode="drift")
+    out, ratio = q.eval(dev(R), dev(k), dev(rt), fn, 20000, n_up, ratio=True)
+    orc, absout, _ = oracle.eval_j2(R, k, rt, fn, 20000, n_up, threads=THREADS)
+    dj = orc[:, 1, 0] - orc[:, 0, 0]
+    r = ratio.cpu().numpy()
+    scale = np.maximum(absout[:, :, 0].max(1), 1.0)
+    assert np.max(np.abs(r[:, 1, 0] - dj) / scale) < 1e-12
+    np.testing.assert_allclose(r[:, 1, 1], np.exp(dj), rtol=1e-11)
+    # V_cur variant and the standalone qj2_ratio kernel agree
+    vcur = dev(out[:, 0, 0].cpu().numpy().copy())
+    _, r2 = q.eval(dev(R), dev(k), dev(rt), fn, 20000, n_up, V_cur=vcur, ratio=True)
+    r3 = q.ratio(out, V_cur=vcur)
+    assert torch.equal(r2, r3)
+
+
+def test_determinism(q):
+    R, k, rt, fn, n_up = instance(50000, 64, seed=13, dtype=np.float32)
+    a = q.eval(dev(R), dev(k), dev(rt), fn, 50000, n_up)
+    b = q.eval(dev(R), dev(k), dev(rt), fn, 50000, n_up)
+    assert torch.equal(a, b)
+
+
+# ---------------------------------------------------------------------------
+# Row output (Fig. 6's v)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_row_output(q, dtype):
+    N = 9001
+    R, k, rt, fn, n_up = instance(N, 8, seed=21, dtype=dtype, P=2)
+    out, orc, row, orow = check(q, R, k, rt, fn, N, n_up, dtype, row=True)
+    L = np.float64(fn.L[0])
+    for w in range(8):
+        for p in range(2):
+            i = np.array([j for j in range(N) if j != k[w]])
+            d_gpu = row[w, p, 1:, i].astype(np.float64)
+            d_orc = orow[w, p, 1:, i]
+            tie = np.abs(np.abs(d_orc) - L / 2) <= 4 * np.spacing(np.float32(L))
+            if dtype == np.float32:
+                ok = (d_gpu == d_orc.astype(np.float32)) | tie
+                assert ok.all()
+                rg, ro = row[w, p, 0, i], orow[w, p, 0, i].astype(np.float32)
+                assert np.all(np.abs(rg - ro) <= 3 * np.spacing(ro))
+            else:
+                assert np.all((np.abs(d_gpu - d_orc) <= 2 * np.spacing(L)) | tie)
+                np.testing.assert_allclose(row[w, p, 0, i], orow[w, p, 0, i], rtol=4e-16)
+
+
+# ---------------------------------------------------------------------------
+# Sharding along the electron axis (the per-rank path of C5)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_fake_shard_partial_sums(q, dtype):
+    N, W = 40000, 24
+    R, k, rt, fn, n_up = instance(N, W, seed=31, dtype=dtype)
+    full = q.eval(dev(R), dev(k), dev(rt), fn, N, n_up).cpu().numpy()
+    orc, absout, _ = oracle.eval_j2(R, k, rt, fn, N, n_up, threads=THREADS)
+    for G in (2, 3, 8):
+        tot = np.zeros_like(full)
+        bounds = [N * g // G for g in range(G + 1)]
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            vw = 4 if dtype == np.float32 else 2
+            Np = qmcgen.padded_size(b - a, vw)
+            Rs = np.zeros((W, 3, Np), dtype)
+            Rs[:, :, :b - a] = R[:, :, a:b]
+            part = q.eval(dev(Rs), dev(k), dev(rt), fn, N, n_up, i_offset=a, n_local=b - a)
+            tot += part.cpu().numpy()
+        assert oracle.normalized_error(tot, orc, absout, fn).max() <= TOL[dtype]
+        assert oracle.normalized_error(tot, full, absout, fn).max() <= TOL[dtype]
+
+
+# ---------------------------------------------------------------------------
+# Building blocks
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_functor_eval_vgl(q, dtype):
+    fn = qmcgen.make_functor(5, 20.0, m=8)
+    r = (np.random.default_rng(0).random(100000) * 12.0).astype(dtype)
+    for ch in (0, 1):
+        g = q.functor_eval_vgl(fn, ch, dev(r)).cpu().numpy()
+        o = oracle.bspline(fn.coef[ch], fn.m, fn.r_cut, r.astype(np.float64))
+        cmax, delta = np.abs(fn.coef).max(), fn.r_cut / fn.m
+        tol = 4e-6 if dtype == np.float32 else 1e-13
+        # compare away from the cutoff (fp32 r/delta may round across r_cut)
+        inside = r.astype(np.float64) < fn.r_cut * (1 - 1e-6)
+        for nu in range(3):
+            assert np.max(np.abs(g[inside, nu] - o[inside, nu])) <= tol * cmax / delta ** nu
+        assert np.all(g[r.astype(np.float64) >= fn.r_cut] == 0.0)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_min_image_disp(q, dtype):
+    rng = np.random.default_rng(1)
+    L = np.float32(17.5)
+    a = (rng.random((50000, 3)) * L).astype(dtype)
+    b = (rng.random((50000, 3)) * L).astype(dtype)
+    g = q.min_image_disp([float(L)] * 3, dev(a), dev(b)).cpu().numpy()
+    o = oracle.min_image([float(L)] * 3, a, b)
+    if dtype == np.float32:
+        assert np.array_equal(g[:, 1:], o[:, 1:].astype(np.float32))   # single rounding
+        assert np.all(np.abs(g[:, 0] - o[:, 0]) <= 3 * np.spacing(o[:, 0].astype(np.float32)))
+    else:
+        np.testing.assert_allclose(g[:, 1:], o[:, 1:], atol=4 * np.spacing(17.5))
+        np.testing.assert_allclose(g[:, 0], o[:, 0], rtol=4e-16)
+
+
+def test_check_inputs_flags(q):
+    R, k, rt, fn, n_up = instance(1000, 4, seed=3, dtype=np.float32)
+    assert q.check_inputs(dev(R), dev(k), dev(rt), fn, 1000) == 0
+    R2 = R.copy(); R2[1, 2, 5] = np.float32(fn.L[0])
+    k2 = k.copy(); k2[3] = 1000
+    rt2 = rt.copy(); rt2[0, 0, 1] = -1.0
+    assert q.check_inputs(dev(R2), dev(k), dev(rt), fn, 1000) == 1
+    assert q.check_inputs(dev(R), dev(k2), dev(rt), fn, 1000) == 2
+    assert q.check_inputs(dev(R), dev(k), dev(rt2), fn, 1000) == 4
+
+
+def test_device_generator_matches_host_generator(q):
+    for dtype, tdt in ((np.float32, torch.float32), (np.float64, torch.float64)):
+        N, Np, L = 5000, 5008, qmcgen.cell_length(5000)
+        g = q.gen_positions(42, 6, N, Np, L, tdt, w_offset=100).cpu().numpy()
+        h = qmcgen.positions(42, np.arange(100, 106), N, Np, L, dtype)
+        assert np.array_equal(g, h)
+        # a slice of the source axis (C5 per-rank generation)
+        g2 = q.gen_positions(42, 2, 1000, 1000, L, tdt, w_offset=100, i_offset=3000).cpu().numpy()
+        assert np.array_equal(g2, h[:2, :, 3000:4000])
+
+
+def test_eval_host_matches_device_path(q):
+    R, k, rt, fn, n_up = instance(30000, 40, seed=41, dtype=np.float32)
+    d = q.eval(dev(R), dev(k), dev(rt), fn, 30000, n_up).cpu()
+    Rh = torch.from_numpy(R).pin_memory()
+    kh = torch.from_numpy(k).pin_memory()
+    th = torch.from_numpy(rt).pin_memory()
+    h = q.eval_host(Rh, kh, th, fn, 30000, n_up, chunk_walkers=7)
+    assert torch.equal(d, h)
+    vcur = torch.from_numpy(d[:, 0, 0].numpy().copy())
+    h2, rat = q.eval_host(Rh, kh, th, fn, 30000, n_up, V_cur=vcur, ratio=True, chunk_walkers=16)
+    assert torch.equal(h2, d)
+    assert torch.all(rat[:, 0, 0] == 0) and torch.all(rat[:, 0, 1] == 1)
+
+
+# ---------------------------------------------------------------------------
+# Full-size configs in the launch configuration bench.py times (sampled)
+# ---------------------------------------------------------------------------
+def _sampled_check(q, cfg, seed, Rdev, walkers_sample, n_local=None, i_offset=0, out=None):
+    L = cfg.L
+    k = qmcgen.make_k(seed, cfg.W, cfg.N)
+    rt = qmcgen.make_trials(seed, np.arange(cfg.W), k, cfg.N, L, cfg.np_dtype)
+    fn = qmcgen.make_functor(cfg.seed, L, cfg.m)
+    if out is None:
+        out = q.eval(Rdev, dev(k), dev(rt), fn, cfg.N, cfg.n_up).cpu().numpy()
+    assert np.all(np.isfinite(out))
+    Rs = qmcgen.positions(seed, walkers_sample, cfg.N, cfg.Np, L, cfg.np_dtype)
+    orc, absout, _ = oracle.eval_j2(Rs, k[walkers_sample], rt[walkers_sample], fn, cfg.N, cfg.n_up,
+                                    threads=THREADS)
+    err = oracle.normalized_error(out[walkers_sample], orc, absout, fn)
+    assert err.max() <= TOL[cfg.np_dtype], err.max()
+    return out
+
+
+def test_C3_full_size_sampled(q):
+    cfg = qmcgen.CONFIGS["C3"]
+    R = q.gen_positions(cfg.seed, cfg.W, cfg.N, cfg.Np, cfg.L, torch.float32)
+    sample = np.array([0, 1, 77, 511, 512, 1000, 1023])
+    _sampled_check(q, cfg, cfg.seed, R, sample)
+    del R
+    torch.cuda.empty_cache()
+
+
+def test_C4_instances_sampled(q):
+    cfg = qmcgen.CONFIGS["C4"]
+    for inst in (0, 1, 4095):
+        seed = cfg.seed + inst
+        R = q.gen_positions(seed, cfg.W, cfg.N, cfg.Np, cfg.L, torch.float32)
+        _sampled_check(q, cfg, seed, R, np.array([0, 5, 1023]))
+
+
+def test_C5_sliced_single_gpu_sampled(q):
+    """C5 (N = 4,915,200) as 8 source slices evaluated in turn on one GPU with
+    i_offset (exactly the per-rank kernel calls), partials summed on the host."""
+    cfg = qmcgen.CONFIGS["C5"]
+    G = 8
+    k = qmcgen.make_k(cfg.seed, cfg.W, cfg.N)
+    rt = qmcgen.make_trials(cfg.seed, np.arange(cfg.W), k, cfg.N, cfg.L, cfg.np_dtype)
+    fn = qmcgen.make_functor(cfg.seed, cfg.L, cfg.m)
+    tot = np.zeros((cfg.W, 1, 5))
+    kd, td = dev(k), dev(rt)
+    for g in range(G):
+        a, b = cfg.N * g // G, cfg.N * (g + 1) // G
+        R = q.gen_positions(cfg.seed, cfg.W, b - a, b - a, cfg.L, torch.float32, i_offset=a)
+        tot += q.eval(R, kd, td, fn, cfg.N, cfg.n_up, i_offset=a, n_local=b - a).cpu().numpy()
+        del R
+    torch.cuda.empty_cache()
+    _sampled_check(q, cfg, cfg.seed, None, np.array([0, 333, 1023]), out=tot)
