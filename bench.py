@@ -183,22 +183,36 @@ def committed_traffic(config_name: str):
 # ---------------------------------------------------------------------------
 # CPU oracle (cpu_baseline leg and --impl reference)
 # ---------------------------------------------------------------------------
-def oracle_rate(cfg, walkers, threads):
-    """Time the oracle (as it stands) on `walkers` of cfg; return (items/s, seconds)."""
-    import oracle
-    import qmcgen
-    seed = cfg.seed
-    L = cfg.L
-    k_all = qmcgen.make_k(seed, cfg.W, cfg.N)
-    w = np.asarray(walkers)
-    R = qmcgen.positions(seed, w, cfg.N, cfg.Np, L, cfg.np_dtype)
-    rt = qmcgen.make_trials(seed, np.arange(cfg.W), k_all, cfg.N, L, cfg.np_dtype)[w]
-    fn = qmcgen.make_functor(seed, L, cfg.m)
-    Rf = np.ascontiguousarray(R, dtype=np.float64)          # promotion outside the timed region
-    t0 = time.perf_counter()
-    oracle.eval_j2(Rf, k_all[w], rt, fn, cfg.N, cfg.n_up, threads=threads)
-    dt = time.perf_counter() - t0
-    return w.size * (cfg.N - 1) / dt, dt
+class OracleSample:
+    """The CPU oracle (as it stands) on walkers [0, n) of cfg.  Inputs are drawn
+    by the oracle side's own C generator (untimed); run() times one evaluation."""
+
+    def __init__(self, cfg, n_walkers, threads):
+        import oracle
+        import qmcgen
+        self.cfg, self.n, self.threads = cfg, int(n_walkers), threads
+        k_all = qmcgen.make_k(cfg.seed, cfg.W, cfg.N)
+        self.k = k_all[:self.n]
+        self.rt = qmcgen.make_trials(cfg.seed, np.arange(cfg.W), k_all, cfg.N, cfg.L, cfg.np_dtype)[:self.n]
+        self.fn = qmcgen.make_functor(cfg.seed, cfg.L, cfg.m)
+        self.R = oracle.gen_positions(cfg.seed, 0, self.n, cfg.N, cfg.Np, cfg.L, cfg.np_dtype, threads)
+        self.items = self.n * (cfg.N - 1)
+
+    def run(self):
+        import oracle
+        t0 = time.perf_counter()
+        oracle.eval_j2(self.R, self.k, self.rt, self.fn, self.cfg.N, self.cfg.n_up, threads=self.threads)
+        return time.perf_counter() - t0
+
+
+def oracle_sample_size(cfg, cores, budget_s):
+    """Walkers such that one oracle pass takes about budget_s on `cores` threads
+    (calibrated on one walker per core), capped at the whole workload."""
+    n0 = min(cfg.W, cores)
+    dt0 = OracleSample(cfg, n0, cores).run()
+    per_round = max(dt0, 1e-6)              # one walker per core
+    n = int(budget_s / per_round) * cores
+    return max(n0, min(cfg.W, n)), n0 * (cfg.N - 1) / dt0
 
 
 def cpu_cores():
@@ -225,25 +239,18 @@ def run_reference(args):
     import qmcgen
     cfg = qmcgen.CONFIGS[args.config]
     cores = cpu_cores()
-    # calibrate: one walker per core, then size each step to the time budget
-    budget_total = 150.0
-    per_step = max(0.5, min(10.0, budget_total / max(1, args.steps + args.warmup)))
-    n0 = min(cfg.W, cores)
-    rate0, dt0 = oracle_rate(cfg, np.arange(n0), cores)
-    per_walker = dt0 / n0 * min(cores, n0)   # seconds per walker per core
-    ws = int(max(1, min(cfg.W, per_step * cores / max(per_walker, 1e-9))))
-    ws = max(1, (ws // cores) * cores) if ws >= cores else ws
-    log(f"[reference] oracle {rate0:.3e} items/s on {n0} walkers; {ws} walkers per step")
-    for i in range(args.warmup):
-        oracle_rate(cfg, (np.arange(ws) + i * ws) % cfg.W, cores)
-    times = []
-    for i in range(args.steps):
-        r, dt = oracle_rate(cfg, (np.arange(ws) + i * ws) % cfg.W, cores)
-        times.append(dt)
+    budget_total = 120.0
+    per_step = max(0.2, min(10.0, budget_total / max(1, args.steps + args.warmup)))
+    ws, rate0 = oracle_sample_size(cfg, cores, per_step)
+    log(f"[reference] oracle {rate0:.3e} items/s (calibration); {ws} walkers per step")
+    smp = OracleSample(cfg, ws, cores)
+    for _ in range(args.warmup):
+        smp.run()
+    times = [smp.run() for _ in range(args.steps)]
     t = float(np.mean(times))
-    value = ws * (cfg.N - 1) / t
-    sample = (f"{ws} of {cfg.W} walkers of {cfg.name} (N={cfg.N}, P=1) per step, fp32 inputs promoted to "
-              f"fp64, plain C oracle, {cores} threads ({cpu_model()})")
+    value = smp.items / t
+    sample = (f"{ws} of {cfg.W} walkers of {cfg.name} (N={cfg.N}, P=1) per step, fp32 inputs promoted "
+              f"exactly to fp64, plain C oracle, {cores} threads ({cpu_model()})")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -418,11 +425,13 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = cpu_cores()
-        nw = args.cpu_sample_walkers or min(cfg.W, max(cores, 16))
-        rate, dt = oracle_rate(cfg, np.arange(nw), cores)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{nw} of {cfg.W} walkers of {cfg.name} (N={cfg.N}, P=1) once, fp32 inputs promoted "
-                         f"to fp64, plain C oracle, {cores} threads ({cpu_model()}), {dt:.1f} s"}
+        nw = args.cpu_sample_walkers or oracle_sample_size(cfg, cores, 15.0)[0]
+        smp = OracleSample(cfg, nw, cores)
+        dt = smp.run()
+        cpu = {"value": smp.items / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{nw} of {cfg.W} walkers of {cfg.name} (N={cfg.N}, P=1), one pass, fp32 inputs "
+                         f"promoted exactly to fp64, plain C oracle, {cores} threads ({cpu_model()}), "
+                         f"{dt:.1f} s wall"}
 
     if rank == 0:
         line = {

@@ -53,6 +53,14 @@ def lib():
                                   i64, i64, i64, i64, i64, i64,
                                   dp, i32p, ctypes.c_int32, dp,
                                   dp, dp, dp, ctypes.c_int]
+        _lib.orc_eval_f32.restype = i64
+        _lib.orc_eval_f32.argtypes = [dp, ctypes.c_double, ctypes.c_int, dp,
+                                      i64, i64, i64, i64, i64, i64,
+                                      ctypes.c_void_p, i32p, ctypes.c_int32, ctypes.c_void_p,
+                                      dp, dp, dp, ctypes.c_int]
+        _lib.orc_gen_positions.restype = None
+        _lib.orc_gen_positions.argtypes = [ctypes.c_uint64, i64, i64, i64, i64, ctypes.c_double,
+                                           ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
         _lib.orc_j2_total.restype = ctypes.c_double
         _lib.orc_j2_total.argtypes = [dp, ctypes.c_double, ctypes.c_int, dp,
                                       i64, i64, i64, dp]
@@ -83,11 +91,16 @@ def eval_j2(R, k, r_trial, fn, n_total: int, n_up: int, i_offset: int = 0,
     r_trial: [W][P][3], fn: qmcgen.Functor-like (L, r_cut, m, coef[2][m+3]).
     Returns (out[W][P][5], abs[W][P][5], row[W][P][4][Np] or None), fp64.
     """
-    R = _f64(R)
+    f32 = (np.asarray(R).dtype == np.float32 and np.asarray(r_trial).dtype == np.float32)
+    if f32:   # promoted element by element inside the oracle (exact)
+        R = np.ascontiguousarray(R)
+        rt = np.ascontiguousarray(r_trial)
+    else:
+        R = _f64(R)
+        rt = _f64(r_trial)
     W, three, Np = R.shape
     assert three == 3
     N_local = min(Np, n_total - i_offset) if n_local is None else int(n_local)
-    rt = _f64(r_trial)
     P = rt.shape[1]
     k = np.ascontiguousarray(np.asarray(k, dtype=np.int32))
     L = _f64(fn.L)
@@ -95,15 +108,28 @@ def eval_j2(R, k, r_trial, fn, n_total: int, n_up: int, i_offset: int = 0,
     out = np.zeros((W, P, 5))
     absout = np.zeros((W, P, 5))
     rowout = np.full((W, P, 4, Np), np.nan) if row else None
-    st = lib().orc_eval(_dp(L), float(fn.r_cut), int(fn.m), _dp(coef),
-                        W, n_total, n_up, i_offset, N_local, Np,
-                        _dp(R), k.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-                        P, _dp(rt), _dp(out), _dp(absout),
-                        _dp(rowout) if row else ctypes.POINTER(ctypes.c_double)(),
-                        int(threads))
+    entry = lib().orc_eval_f32 if f32 else lib().orc_eval
+    st = entry(_dp(L), float(fn.r_cut), int(fn.m), _dp(coef),
+               W, n_total, n_up, i_offset, N_local, Np,
+               R.ctypes.data_as(ctypes.c_void_p) if f32 else _dp(R),
+               k.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+               P, rt.ctypes.data_as(ctypes.c_void_p) if f32 else _dp(rt), _dp(out), _dp(absout),
+               _dp(rowout) if row else ctypes.POINTER(ctypes.c_double)(),
+               int(threads))
     if st:
         raise CoincidentError(f"coincident source at (w*P+p) = {st - 1}")
     return out, absout, rowout
+
+
+def gen_positions(seed: int, walkers_begin: int, n_walkers: int, N: int, Np: int, L: float,
+                  dtype, threads: int = 1) -> np.ndarray:
+    """Oracle-side C twin of qmcgen.positions for contiguous global walker ids
+    [walkers_begin, walkers_begin + n_walkers) (input generation only)."""
+    f32 = np.dtype(dtype) == np.float32
+    out = np.empty((n_walkers, 3, Np), dtype=np.float32 if f32 else np.float64)
+    lib().orc_gen_positions(int(seed) & 0xFFFFFFFFFFFFFFFF, walkers_begin, n_walkers, N, Np, float(L),
+                            1 if f32 else 0, out.ctypes.data_as(ctypes.c_void_p), int(threads))
+    return out
 
 
 def j2_total(R1, n: int, n_up: int, fn) -> float:

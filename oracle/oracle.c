@@ -142,6 +142,7 @@ typedef struct {
     const double *L; double r_cut; int m; const double *coef; /* [2][m+3] */
     int64_t W, N_total, N_up, i_offset, N_local, Np;
     const double *R; const int32_t *k; int32_t P; const double *r_trial;
+    const float *Rf; const float *r_trial_f;   /* fp32 inputs, promoted exactly (or NULL) */
     double *out; double *abs_out; double *row_out;
     int64_t w_begin, w_end;
     int64_t status;
@@ -151,17 +152,22 @@ static int64_t eval_walkers(orc_job *J)
 {
     const int mc = J->m + 3;
     for (int64_t w = J->w_begin; w < J->w_end; ++w) {
-        const double *Rw = J->R + w * 3 * J->Np;
+        const double *Rw = J->R ? J->R + w * 3 * J->Np : NULL;
         int64_t kw = J->k[w];
         for (int32_t p = 0; p < J->P; ++p) {
-            const double *rt = J->r_trial + (w * J->P + p) * 3;
+            double rt[3];
+            for (int c = 0; c < 3; ++c)
+                rt[c] = J->r_trial_f ? (double)J->r_trial_f[(w * J->P + p) * 3 + c]
+                                     : J->r_trial[(w * J->P + p) * 3 + c];
             nsum V = {0, 0}, G[3] = {{0, 0}, {0, 0}, {0, 0}}, Lp = {0, 0};
             nsum AV = {0, 0}, AG[3] = {{0, 0}, {0, 0}, {0, 0}}, AL = {0, 0};
             double *row = J->row_out ? J->row_out + ((w * J->P + p) * 4) * J->Np : NULL;
             for (int64_t il = 0; il < J->N_local; ++il) {
                 int64_t i = J->i_offset + il;          /* global index */
                 if (i == kw) continue;                 /* i != k, Eq. (5) */
-                double src[3] = { Rw[il], Rw[J->Np + il], Rw[2 * J->Np + il] };
+                double src[3];
+                for (int c = 0; c < 3; ++c)
+                    src[c] = J->Rf ? (double)J->Rf[(w * 3 + c) * J->Np + il] : Rw[c * J->Np + il];
                 double d[3], rho;
                 orc_min_image(J->L, rt, src, d, &rho);
                 if (row) {
@@ -207,23 +213,19 @@ static void *eval_thread(void *arg)
     return NULL;
 }
 
-int64_t orc_eval(const double L[3], double r_cut, int m, const double *coef,
-                 int64_t W, int64_t N_total, int64_t N_up,
-                 int64_t i_offset, int64_t N_local, int64_t Np,
-                 const double *R, const int32_t *k, int32_t P, const double *r_trial,
-                 double *out, double *abs_out, double *row_out, int nthreads)
+static int64_t run_eval(orc_job proto, int nthreads)
 {
-    (void)N_total;
+    int64_t W = proto.W;
     if (nthreads < 1) nthreads = 1;
     if (nthreads > W) nthreads = (int)(W > 0 ? W : 1);
     orc_job *jobs = (orc_job *)calloc((size_t)nthreads, sizeof(orc_job));
     pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
     int64_t per = (W + nthreads - 1) / nthreads;
     for (int t = 0; t < nthreads; ++t) {
-        orc_job J = { L, r_cut, m, coef, W, N_total, N_up, i_offset, N_local, Np,
-                      R, k, P, r_trial, out, abs_out, row_out,
-                      t * per, (t + 1) * per < W ? (t + 1) * per : W, 0 };
-        if (J.w_begin > W) J.w_begin = W;
+        orc_job J = proto;
+        J.w_begin = t * per < W ? t * per : W;
+        J.w_end = (t + 1) * per < W ? (t + 1) * per : W;
+        J.status = 0;
         jobs[t] = J;
     }
     for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, eval_thread, &jobs[t]);
@@ -233,6 +235,29 @@ int64_t orc_eval(const double L[3], double r_cut, int m, const double *coef,
     for (int t = 0; t < nthreads && !st; ++t) st = jobs[t].status;
     free(jobs); free(th);
     return st;
+}
+
+int64_t orc_eval(const double L[3], double r_cut, int m, const double *coef,
+                 int64_t W, int64_t N_total, int64_t N_up,
+                 int64_t i_offset, int64_t N_local, int64_t Np,
+                 const double *R, const int32_t *k, int32_t P, const double *r_trial,
+                 double *out, double *abs_out, double *row_out, int nthreads)
+{
+    orc_job J = { L, r_cut, m, coef, W, N_total, N_up, i_offset, N_local, Np,
+                  R, k, P, r_trial, NULL, NULL, out, abs_out, row_out, 0, 0, 0 };
+    return run_eval(J, nthreads);
+}
+
+/* Same computation on fp32 inputs (each coordinate promoted exactly to fp64). */
+int64_t orc_eval_f32(const double L[3], double r_cut, int m, const double *coef,
+                     int64_t W, int64_t N_total, int64_t N_up,
+                     int64_t i_offset, int64_t N_local, int64_t Np,
+                     const float *R, const int32_t *k, int32_t P, const float *r_trial,
+                     double *out, double *abs_out, double *row_out, int nthreads)
+{
+    orc_job J = { L, r_cut, m, coef, W, N_total, N_up, i_offset, N_local, Np,
+                  NULL, k, P, NULL, R, r_trial, out, abs_out, row_out, 0, 0, 0 };
+    return run_eval(J, nthreads);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -274,4 +299,72 @@ void orc_min_image_batch(const double L[3], int64_t n, const double *a,
         orc_min_image(L, a + 3 * i, b + 3 * i, d, &rho);
         out[4 * i] = rho; out[4 * i + 1] = d[0]; out[4 * i + 2] = d[1]; out[4 * i + 3] = d[2];
     }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Host twin of the seeded input generator (qmcgen.positions), written       */
+/* independently in plain C so the oracle side can draw large samples        */
+/* quickly.  Not part of the method.  Pinned bitwise against qmcgen by       */
+/* tests/test_inputs.py.                                                      */
+/* ------------------------------------------------------------------------ */
+static uint64_t orc_mix64(uint64_t z)
+{
+    z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27; z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+
+typedef struct { uint64_t key; int64_t w0, w1, N, Np; double L; int f32; void *R; int64_t wbase; } gen_job;
+
+static void *gen_thread(void *arg)
+{
+    gen_job *J = (gen_job *)arg;
+    for (int64_t a = J->w0; a < J->w1; ++a)
+        for (int d = 0; d < 3; ++d)
+            for (int64_t i = 0; i < J->Np; ++i) {
+                size_t o = ((size_t)a * 3 + (size_t)d) * (size_t)J->Np + (size_t)i;
+                if (i >= J->N) {
+                    if (J->f32) ((float *)J->R)[o] = 0.0f; else ((double *)J->R)[o] = 0.0;
+                    continue;
+                }
+                uint64_t ctr = ((uint64_t)((J->wbase + a) * 3 + d) << 32) | (uint64_t)i;
+                uint64_t h = orc_mix64(J->key ^ ctr);
+                if (J->f32) {
+                    float Lf = (float)J->L;
+                    float u = (float)(uint32_t)(h >> 40) * 5.9604644775390625e-08f;
+                    float x = Lf * u;
+                    if (x >= Lf) x = nextafterf(Lf, 0.0f);
+                    ((float *)J->R)[o] = x;
+                } else {
+                    double u = (double)(h >> 11) * 1.1102230246251565e-16;
+                    double x = J->L * u;
+                    if (x >= J->L) x = nextafter(J->L, 0.0);
+                    ((double *)J->R)[o] = x;
+                }
+            }
+    return NULL;
+}
+
+/* R[n_walkers][3][Np] for global walker ids wbase .. wbase+n_walkers-1. */
+void orc_gen_positions(uint64_t seed, int64_t wbase, int64_t n_walkers, int64_t N, int64_t Np,
+                       double L, int f32, void *R, int nthreads)
+{
+    uint64_t key = orc_mix64(seed * 0x9E3779B97F4A7C15ull + 0x9E3779B97F4A7C15ull);
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > n_walkers) nthreads = (int)(n_walkers > 0 ? n_walkers : 1);
+    gen_job *jobs = (gen_job *)calloc((size_t)nthreads, sizeof(gen_job));
+    pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+    int64_t per = (n_walkers + nthreads - 1) / nthreads;
+    for (int t = 0; t < nthreads; ++t) {
+        int64_t a = t * per, b = (t + 1) * per;
+        if (a > n_walkers) a = n_walkers;
+        if (b > n_walkers) b = n_walkers;
+        gen_job J = { key, a, b, N, Np, L, f32, R, wbase };
+        jobs[t] = J;
+    }
+    for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, gen_thread, &jobs[t]);
+    gen_thread(&jobs[0]);
+    for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+    free(jobs); free(th);
 }

@@ -58,3 +58,13 @@ def test_config_sizes():
     assert c3.items == 1024 * 614399
     c5 = qmcgen.CONFIGS["C5"]
     assert c5.W * 3 * c5.Np * 4 == 60397977600
+
+
+def test_oracle_side_generator_matches_qmcgen():
+    import oracle
+    for dtype in (np.float32, np.float64):
+        N, Np = 3001, 3008
+        L = qmcgen.cell_length(N)
+        a = oracle.gen_positions(9, 40, 5, N, Np, L, dtype, threads=3)
+        b = qmcgen.positions(9, np.arange(40, 45), N, Np, L, dtype)
+        assert a.dtype == b.dtype and np.array_equal(a, b)
