@@ -140,9 +140,10 @@ qj2_status qj2_eval_workspace_size(int64_t W, int32_t P, int64_t N_local,
 /*             P <= 4): the e^{dJ2} factor of Eq. 4.   */
 /*             Only for unsharded calls (i_offset == 0, N_local == N_total); */
 /*             sharded callers reduce `out` first and call qj2_ratio.        */
-/*   workspace device scratch >= qj2_eval_workspace_size(); must be          */
-/*             zero-filled before its FIRST use; every completed call leaves */
-/*             its counters zero again.  One workspace per concurrent call.  */
+/*   workspace device scratch >= qj2_eval_workspace_size() (per-tile fp64   */
+/*             partials + completion counters, which the call zeroes itself  */
+/*             with one cudaMemsetAsync when the slice spans > 1 tile).  No  */
+/*             initialisation needed.  One workspace per concurrent call.    */
 /*   stream    cudaStream_t.                                                 */
 /* Preconditions not checked on the hot path (see qj2_check_inputs):         */
 /* coordinates in range, k < N_total, no coincident source inside the        */
@@ -174,8 +175,7 @@ qj2_status qj2_ratio(int64_t W, int32_t P, const double *out, const double *V_cu
 /* chunk_walkers through two device staging buffers carved from workspace:  */
 /* the host->device copy of chunk c+1 overlaps the kernel of chunk c.        */
 /* Blocking: returns after out is written (synchronises `stream`).           */
-/* workspace: device, >= qj2_eval_host_workspace_size(), zero-filled before  */
-/* its first use.                                                            */
+/* workspace: device, >= qj2_eval_host_workspace_size() (no initialisation). */
 /* ------------------------------------------------------------------------ */
 qj2_status qj2_eval_host_workspace_size(int64_t W, int32_t P, int64_t Np,
                                         qj2_dtype dtype, int64_t chunk_walkers,

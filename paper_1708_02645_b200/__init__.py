@@ -175,8 +175,8 @@ def workspace_size(W: int, P: int, n_local: int, dtype: torch.dtype) -> int:
 
 
 class Workspace:
-    """Reusable zero-initialised device scratch for qj2_eval (the library
-    leaves its counters zero after each completed call)."""
+    """Reusable device scratch for qj2_eval / qj2_eval_host (grown on demand;
+    the library initialises what it needs on every call)."""
 
     def __init__(self, nbytes: int = 0, device=None):
         self.device = device

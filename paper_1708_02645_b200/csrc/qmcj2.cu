@@ -45,6 +45,7 @@ struct EvalParams {
     unsigned int *counters;       // [W][n_groups]
     double L[3];
     double inv_delta;
+    float inv_delta_f;
     double pcoef[2][QJ2_MAX_M + 1][4];   // power basis per interval; row m = 0
 };
 
@@ -74,24 +75,16 @@ __device__ __forceinline__ void load_table(const EvalParams &p, Coef4<T> *tab) {
 // Per-trial constants: the three axes' minimum-image constants.
 template <typename T> struct Trial { Axis<T> ax, ay, az; };
 
-// One source term for one trial.  acc: V, Gx, Gy, Gz (sum du/r * d), H (sum h),
-// S (sum du/r).  Final scaling to U', U'' happens once, in fp64.
-// If MASK, `dead` sources (self, padding) get r^2 = BIG, which lands on the
-// all-zero interval: every accumulated quantity is exactly 0.
-template <typename T, bool MASK>
-__device__ __forceinline__ void term(T x, T y, T z, const Trial<T> &tr, T inv_delta,
-                                     uint32_t tab_base, typename Traits<T>::U clamp_bits,
-                                     bool dead, T *acc, T &r_out, T &dx_out, T &dy_out, T &dz_out) {
+// Functor + accumulation for one source at squared distance r2 (and
+// displacement d).  acc: V, Gx, Gy, Gz (sum du/r * d), H (sum h), S (sum du/r).
+// Final scaling to U', U'' happens once, in fp64, per tile.
+template <typename T>
+__device__ __forceinline__ T accumulate(T dx, T dy, T dz, T r2, T inv_delta, uint32_t tab_base,
+                                        typename Traits<T>::U clamp_bits, T *acc) {
     using Tr = Traits<T>;
-    const T dx = min_image(x, tr.ax);
-    const T dy = min_image(y, tr.ay);
-    const T dz = min_image(z, tr.az);
-    T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-    if (MASK) r2 = dead ? T(1e30) : r2;
     const T ir = Tr::rsqrt(r2);
     const T r = r2 * ir;
-    const T t = r * inv_delta;
-    const FunctorEval<T> e = functor_from_t<T>(t, tab_base, clamp_bits);
+    const FunctorEval<T> e = functor_from_t<T>(r * inv_delta, tab_base, clamp_bits);
     const T g = e.du * ir;
     acc[0] += e.u;
     acc[1] = fma(g, dx, acc[1]);
@@ -99,73 +92,106 @@ __device__ __forceinline__ void term(T x, T y, T z, const Trial<T> &tr, T inv_de
     acc[3] = fma(g, dz, acc[3]);
     acc[4] += e.h;
     acc[5] += g;
-    r_out = r; dx_out = dx; dy_out = dy; dz_out = dz;
+    return r;
 }
 
-// Process one tile [start, end) of sources for PB trials.
-template <typename T, int PB, bool MASK, bool ROW>
-__device__ __forceinline__ void tile_loop(const EvalParams &p, int64_t w, int32_t p0, int np,
-                                          int64_t start, int64_t end,
-                                          const Trial<T> (&tr)[PB], T inv_delta,
-                                          uint32_t base_same, uint32_t base_opp, bool k_up,
-                                          int64_t k_local, typename Traits<T>::U clamp_bits,
-                                          T (&acc)[PB][NACC]) {
+// Fast path: a full tile (CH sources), no self source, one spin channel.
+// Every thread walks ITERS vectors at a constant stride of TPB vectors, so
+// every load address is base + immediate; the next vector group is loaded
+// before the current one is consumed (software pipelining).
+template <typename T, int PB, bool ROW>
+__device__ __forceinline__ void tile_fast(const typename Traits<T>::V *__restrict__ px,
+                                          const typename Traits<T>::V *__restrict__ py,
+                                          const typename Traits<T>::V *__restrict__ pz,
+                                          const Trial<T> (&tr)[PB], int np, T inv_delta, uint32_t base,
+                                          typename Traits<T>::U clamp_bits, T (&acc)[PB][NACC],
+                                          typename Traits<T>::V *const (&rowp)[PB], int64_t row_stride) {
     using Tr = Traits<T>;
     using V = typename Tr::V;
-    constexpr int VW = Tr::VW;
-    const V *Rx = reinterpret_cast<const V *>(static_cast<const T *>(p.R) + (w * 3 + 0) * p.Np);
-    const V *Ry = reinterpret_cast<const V *>(static_cast<const T *>(p.R) + (w * 3 + 1) * p.Np);
-    const V *Rz = reinterpret_cast<const V *>(static_cast<const T *>(p.R) + (w * 3 + 2) * p.Np);
-    const int64_t nup_local = p.N_up - p.i_offset;   // first local index of the spin-down half
-    // fast-path channel (tile entirely on one side of the spin boundary)
-    const bool tile_up = start < nup_local;
-    const uint32_t base_fast = (tile_up == k_up) ? base_same : base_opp;
-
-    // software pipeline: prefetch the next vector group while computing this one
-    int64_t idx = start + (int64_t)threadIdx.x * VW;
-    bool valid = idx < end;
-    V cx, cy, cz;
-    if (valid) { cx = Tr::ld_stream(Rx + idx / VW); cy = Tr::ld_stream(Ry + idx / VW); cz = Tr::ld_stream(Rz + idx / VW); }
+    V cx = Tr::ld_stream(px), cy = Tr::ld_stream(py), cz = Tr::ld_stream(pz);
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
-        const int64_t nidx = idx + (int64_t)TPB * VW;
-        const bool nvalid = (it + 1 < ITERS) && nidx < end;
         V nx, ny, nz;
-        if (nvalid) { nx = Tr::ld_stream(Rx + nidx / VW); ny = Tr::ld_stream(Ry + nidx / VW); nz = Tr::ld_stream(Rz + nidx / VW); }
-        if (valid) {
-            V ro[PB][4];
+        if (it + 1 < ITERS) {
+            nx = Tr::ld_stream(px + (it + 1) * TPB);
+            ny = Tr::ld_stream(py + (it + 1) * TPB);
+            nz = Tr::ld_stream(pz + (it + 1) * TPB);
+        }
+        V ro[PB][4];
 #pragma unroll
-            for (int e = 0; e < VW; ++e) {
-                const int64_t li = idx + e;
-                bool dead = false;
-                uint32_t base = base_fast;
-                if (MASK) {
-                    dead = (li >= end) || (li == k_local);
-                    base = ((li < nup_local) == k_up) ? base_same : base_opp;
-                }
-                const T x = Tr::comp(cx, e), y = Tr::comp(cy, e), z = Tr::comp(cz, e);
+        for (int e = 0; e < Tr::VW; ++e) {
+            const T x = Tr::comp(cx, e), y = Tr::comp(cy, e), z = Tr::comp(cz, e);
 #pragma unroll
-                for (int q = 0; q < PB; ++q) {
-                    if (q < np) {
-                        T r, dx, dy, dz;
-                        term<T, MASK>(x, y, z, tr[q], inv_delta, base, clamp_bits, dead, acc[q], r, dx, dy, dz);
-                        if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
-                    }
-                }
-            }
-            if (ROW) {
-#pragma unroll
-                for (int q = 0; q < PB; ++q) {
-                    if (q < np) {
-                        V *row = reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + p0 + q) * 4) * p.Np);
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) __stcs(row + (c * p.Np + idx) / VW, ro[q][c]);
-                    }
+            for (int q = 0; q < PB; ++q) {
+                if (PB == 1 || q < np) {
+                    const T dx = min_image(x, tr[q].ax);
+                    const T dy = min_image(y, tr[q].ay);
+                    const T dz = min_image(z, tr[q].az);
+                    const T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                    const T r = accumulate<T>(dx, dy, dz, r2, inv_delta, base, clamp_bits, acc[q]);
+                    if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
                 }
             }
         }
-        idx = nidx; valid = nvalid;
-        cx = nx; cy = ny; cz = nz;
+        if (ROW) {
+#pragma unroll
+            for (int q = 0; q < PB; ++q)
+                if (PB == 1 || q < np)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) __stcs(rowp[q] + c * row_stride + it * TPB, ro[q][c]);
+        }
+        if (it + 1 < ITERS) { cx = nx; cy = ny; cz = nz; }
+    }
+}
+
+// General path: ragged tile, the tile holding the self source k, or the
+// tile straddling the spin boundary.  Per-source masks; dead sources (self,
+// padding) get r^2 = BIG, which lands on the all-zero interval, so every
+// accumulated quantity is exactly 0 for them.
+template <typename T, int PB, bool ROW>
+__device__ __forceinline__ void tile_general(const typename Traits<T>::V *__restrict__ px,
+                                          const typename Traits<T>::V *__restrict__ py,
+                                          const typename Traits<T>::V *__restrict__ pz,
+                                          const Trial<T> (&tr)[PB], int np, T inv_delta,
+                                          uint32_t base_same, uint32_t base_opp, bool k_up,
+                                          typename Traits<T>::U clamp_bits, int len, int k_rel, int up_rel,
+                                          T (&acc)[PB][NACC],
+                                          typename Traits<T>::V *const (&rowp)[PB], int64_t row_stride) {
+    using Tr = Traits<T>;
+    using V = typename Tr::V;
+    constexpr int VW = Tr::VW;
+    const int tid = threadIdx.x;
+    for (int it = 0; it < ITERS; ++it) {
+        const int rel = (it * TPB + tid) * VW;          // offset of this vector inside the tile
+        if (rel >= len) break;
+        const V cx = Tr::ld_stream(px + it * TPB), cy = Tr::ld_stream(py + it * TPB), cz = Tr::ld_stream(pz + it * TPB);
+        V ro[PB][4];
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+            const int li = rel + e;
+            const bool dead = (li >= len) || (li == k_rel);
+            const uint32_t base = ((li < up_rel) == k_up) ? base_same : base_opp;
+            const T x = Tr::comp(cx, e), y = Tr::comp(cy, e), z = Tr::comp(cz, e);
+#pragma unroll
+            for (int q = 0; q < PB; ++q) {
+                if (PB == 1 || q < np) {
+                    const T dx = min_image(x, tr[q].ax);
+                    const T dy = min_image(y, tr[q].ay);
+                    const T dz = min_image(z, tr[q].az);
+                    T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                    r2 = dead ? T(1e30) : r2;
+                    const T r = accumulate<T>(dx, dy, dz, r2, inv_delta, base, clamp_bits, acc[q]);
+                    if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
+                }
+            }
+        }
+        if (ROW) {
+#pragma unroll
+            for (int q = 0; q < PB; ++q)
+                if (PB == 1 || q < np)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) __stcs(rowp[q] + c * row_stride + it * TPB, ro[q][c]);
+        }
     }
 }
 
@@ -173,7 +199,9 @@ template <typename T, int PB, bool ROW>
 __global__ void __launch_bounds__(TPB, (sizeof(T) == 4 && PB == 1) ? 4 : 2)
 j2_eval_kernel(const __grid_constant__ EvalParams p) {
     using Tr = Traits<T>;
-    constexpr int CH = TPB * Tr::VW * ITERS;
+    using V = typename Tr::V;
+    constexpr int VW = Tr::VW;
+    constexpr int CH = TPB * VW * ITERS;
     __shared__ Coef4<T> tab[2 * (QJ2_MAX_M + 1)];
     __shared__ double red[TPB / 32][PB * NACC];
     __shared__ int last_flag;
@@ -192,7 +220,6 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
 
     const int64_t kw = p.k[w];
     const bool k_up = kw < p.N_up;
-    const int64_t k_local = kw - p.i_offset;
     const T L0 = T(p.L[0]), L1 = T(p.L[1]), L2 = T(p.L[2]);
     Trial<T> tr[PB];
 #pragma unroll
@@ -203,7 +230,7 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
         tr[q].ay = make_axis<T>(rt[1], L1);
         tr[q].az = make_axis<T>(rt[2], L2);
     }
-    const T inv_delta = T(p.inv_delta);
+    const T inv_delta = sizeof(T) == 4 ? T(p.inv_delta_f) : T(p.inv_delta);
     const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tab);
     const uint32_t magic_off = (uint32_t)(Tr::MAGIC_BITS * (typename Tr::U)sizeof(Coef4<T>));
     const uint32_t base_same = tab_addr - magic_off;
@@ -212,10 +239,23 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
 
     const int64_t start = c * CH;
     const int64_t end = min(start + (int64_t)CH, p.N_local);
-    const int64_t nup_local = p.N_up - p.i_offset;
-    const bool masked = (k_local >= start && k_local < end) ||
-                        ((end - start) % Tr::VW != 0) ||
+    const int64_t k_local = kw - p.i_offset;
+    const int64_t nup_local = p.N_up - p.i_offset;   // first local index of the spin-down half
+    const bool masked = (end - start != CH) ||
+                        (k_local >= start && k_local < end) ||
                         (nup_local > start && nup_local < end);
+
+    const T *Rw = static_cast<const T *>(p.R) + w * 3 * p.Np;
+    const int64_t voff = (start >> (VW == 4 ? 2 : 1)) + threadIdx.x;   // this thread's first vector
+    const V *px = reinterpret_cast<const V *>(Rw) + voff;
+    const V *py = reinterpret_cast<const V *>(Rw + p.Np) + voff;
+    const V *pz = reinterpret_cast<const V *>(Rw + 2 * p.Np) + voff;
+    V *rowp[PB];
+#pragma unroll
+    for (int q = 0; q < PB; ++q)
+        rowp[q] = ROW ? reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + p0 + (q < np ? q : 0)) * 4) * p.Np) + voff
+                      : nullptr;
+    const int64_t row_stride = p.Np / VW;
     __syncthreads();
 
     T acc[PB][NACC];
@@ -224,10 +264,17 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
 #pragma unroll
         for (int a = 0; a < NACC; ++a) acc[q][a] = T(0);
 
-    if (masked)
-        tile_loop<T, PB, true, ROW>(p, w, p0, np, start, end, tr, inv_delta, base_same, base_opp, k_up, k_local, clamp_bits, acc);
-    else
-        tile_loop<T, PB, false, ROW>(p, w, p0, np, start, end, tr, inv_delta, base_same, base_opp, k_up, k_local, clamp_bits, acc);
+    if (masked) {
+        const int len = (int)(end - start);
+        const int k_rel = (k_local >= start && k_local < end) ? (int)(k_local - start) : -1;
+        const int up_rel = (int)max((int64_t)0, min(nup_local - start, (int64_t)CH));
+        tile_general<T, PB, ROW>(px, py, pz, tr, np, inv_delta, base_same, base_opp, k_up, clamp_bits,
+                                 len, k_rel, up_rel, acc, rowp, row_stride);
+    } else {
+        const bool tile_up = start < nup_local;
+        const uint32_t base = (tile_up == k_up) ? base_same : base_opp;
+        tile_fast<T, PB, ROW>(px, py, pz, tr, np, inv_delta, base, clamp_bits, acc, rowp, row_stride);
+    }
 
     // ---- CTA reduction in fp64 (fixed order: deterministic) ----
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -269,7 +316,6 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
                 s = warp_sum(s);
                 if (lane == v) tot = s;      // lane v keeps value v (PB*NACC <= 24 < 32)
             }
-            if (lane == 0) p.counters[wg] = 0u;   // ready for the next call
         }
     }
 
@@ -517,11 +563,16 @@ qj2_status eval_impl(const qj2_functor *fn, qj2_dtype dtype,
     p.counters = cnt_b ? reinterpret_cast<unsigned *>(static_cast<char *>(workspace) + part_b) : nullptr;
     for (int d = 0; d < 3; ++d) p.L[d] = fn->L[d];
     p.inv_delta = (double)fn->m / fn->r_cut;
+    p.inv_delta_f = (float)p.inv_delta;
     power_basis(fn->coef[0], fn->m, p.pcoef[0]);
     power_basis(fn->coef[1], fn->m, p.pcoef[1]);
 
     const bool row = row_out != nullptr;
     cudaError_t e;
+    if (cnt_b) {   // completion counters start at zero every call (no caller-side init needed)
+        e = cudaMemsetAsync(p.counters, 0, (size_t)W * ng * sizeof(unsigned), stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counters)");
+    }
     if (dtype == QJ2_FP32) {
         e = pb == 1 ? launch_eval<float, 1>(p, nblocks, row, stream)
           : pb == 2 ? launch_eval<float, 2>(p, nblocks, row, stream)
