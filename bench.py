@@ -279,7 +279,7 @@ def workload_config(cfg, world):
 class C3Plan:
     """One C3-shaped instance per rank (weak scaling; no collective on the data path)."""
     mode = "C3"
-    launches_per_step = 1
+    launches_per_step = 2      # j2_eval_kernel + the 4 KB counter memset issued by qj2_eval
 
     def __init__(self, cfg, rank, world):
         self.cfg = cfg
