@@ -22,7 +22,8 @@
 namespace qj2 {
 
 constexpr int TPB = 256;          // threads per CTA
-constexpr int ITERS = 8;          // vector iterations per tile: 32 fp32 terms per thread per trial
+constexpr int ITERS = 8;          // vector iterations per sub-tile: 32 fp32 terms per thread per trial
+constexpr int SUB = 2;            // sub-tiles per CTA tile
 constexpr int NACC = 6;           // V, Gx, Gy, Gz, sum h, sum du/r  (per trial)
 constexpr int MAXPB = 4;
 
@@ -201,18 +202,22 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
     using Tr = Traits<T>;
     using V = typename Tr::V;
     constexpr int VW = Tr::VW;
-    constexpr int CH = TPB * VW * ITERS;
+    constexpr int SCH = TPB * VW * ITERS;         // sub-tile: 32 terms per thread
+    constexpr int CH = SCH * SUB;                 // tile handled by one CTA
     __shared__ Coef4<T> tab[2 * (QJ2_MAX_M + 1)];
     __shared__ double red[TPB / 32][PB * NACC];
     __shared__ int last_flag;
 
     // tile decode: chunk fastest so consecutive CTAs stream consecutive memory
-    const int64_t b = blockIdx.x;
+    // (32-bit arithmetic: the host guarantees W * n_groups * tiles < 2^31)
+    const uint32_t b = blockIdx.x;
+    const uint32_t tpw32 = (uint32_t)p.tiles_per_walker;
+    const uint32_t per_w = tpw32 * (uint32_t)p.n_groups;
+    const uint32_t w32 = b / per_w;
+    const uint32_t rem = b - w32 * per_w;
+    const uint32_t g32 = rem / tpw32;
     const int64_t tpw = p.tiles_per_walker;
-    const int64_t w = b / (tpw * p.n_groups);
-    const int64_t rem = b - w * tpw * p.n_groups;
-    const int64_t g = rem / tpw;
-    const int64_t c = rem - g * tpw;
+    const int64_t w = w32, g = g32, c = rem - g32 * tpw32;
     const int32_t p0 = (int32_t)g * PB;
     const int np = min(PB, p.P - p0);
 
@@ -241,9 +246,6 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
     const int64_t end = min(start + (int64_t)CH, p.N_local);
     const int64_t k_local = kw - p.i_offset;
     const int64_t nup_local = p.N_up - p.i_offset;   // first local index of the spin-down half
-    const bool masked = (end - start != CH) ||
-                        (k_local >= start && k_local < end) ||
-                        (nup_local > start && nup_local < end);
 
     const T *Rw = static_cast<const T *>(p.R) + w * 3 * p.Np;
     const int64_t voff = (start >> (VW == 4 ? 2 : 1)) + threadIdx.x;   // this thread's first vector
@@ -258,22 +260,46 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
     const int64_t row_stride = p.Np / VW;
     __syncthreads();
 
-    T acc[PB][NACC];
+    // The tile is SUB sub-tiles of SCH sources.  Per sub-tile, each thread
+    // accumulates <= ITERS*VW = 32 terms in T, then flushes to fp64
+    // ("quantities per walker ... in double precision").
+    double dacc[PB][NACC];
 #pragma unroll
     for (int q = 0; q < PB; ++q)
 #pragma unroll
-        for (int a = 0; a < NACC; ++a) acc[q][a] = T(0);
+        for (int a = 0; a < NACC; ++a) dacc[q][a] = 0.0;
 
-    if (masked) {
-        const int len = (int)(end - start);
-        const int k_rel = (k_local >= start && k_local < end) ? (int)(k_local - start) : -1;
-        const int up_rel = (int)max((int64_t)0, min(nup_local - start, (int64_t)CH));
-        tile_general<T, PB, ROW>(px, py, pz, tr, np, inv_delta, base_same, base_opp, k_up, clamp_bits,
-                                 len, k_rel, up_rel, acc, rowp, row_stride);
-    } else {
-        const bool tile_up = start < nup_local;
-        const uint32_t base = (tile_up == k_up) ? base_same : base_opp;
-        tile_fast<T, PB, ROW>(px, py, pz, tr, np, inv_delta, base, clamp_bits, acc, rowp, row_stride);
+#pragma unroll 1
+    for (int sidx = 0; sidx < SUB; ++sidx) {
+        const int64_t sstart = start + (int64_t)sidx * SCH;
+        if (sstart >= end) break;
+        const int64_t send = min(sstart + (int64_t)SCH, end);
+        const int64_t vs = (int64_t)sidx * (SCH / VW);
+        T acc[PB][NACC];
+#pragma unroll
+        for (int q = 0; q < PB; ++q)
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) acc[q][a] = T(0);
+        const bool k_in = k_local >= sstart && k_local < send;
+        const bool masked = (send - sstart != SCH) || k_in || (nup_local > sstart && nup_local < send);
+        V *rp[PB];
+#pragma unroll
+        for (int q = 0; q < PB; ++q) rp[q] = ROW ? rowp[q] + vs : nullptr;
+        if (masked) {
+            const int len = (int)(send - sstart);
+            const int k_rel = k_in ? (int)(k_local - sstart) : -1;
+            const int up_rel = (int)max((int64_t)0, min(nup_local - sstart, (int64_t)SCH));
+            tile_general<T, PB, ROW>(px + vs, py + vs, pz + vs, tr, np, inv_delta, base_same, base_opp, k_up,
+                                     clamp_bits, len, k_rel, up_rel, acc, rp, row_stride);
+        } else {
+            const bool tile_up = sstart < nup_local;
+            const uint32_t base = (tile_up == k_up) ? base_same : base_opp;
+            tile_fast<T, PB, ROW>(px + vs, py + vs, pz + vs, tr, np, inv_delta, base, clamp_bits, acc, rp, row_stride);
+        }
+#pragma unroll
+        for (int q = 0; q < PB; ++q)
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) dacc[q][a] += (double)acc[q][a];
     }
 
     // ---- CTA reduction in fp64 (fixed order: deterministic) ----
@@ -282,7 +308,7 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
     for (int q = 0; q < PB; ++q)
 #pragma unroll
         for (int a = 0; a < NACC; ++a) {
-            const double v = warp_sum((double)acc[q][a]);
+            const double v = warp_sum(dacc[q][a]);
             if (lane == 0) red[warp][q * NACC + a] = v;
         }
     __syncthreads();
@@ -496,7 +522,7 @@ void power_basis(const double *c, int m, double (*pc)[4]) {
 }
 
 inline int vw_of(qj2_dtype d) { return d == QJ2_FP32 ? 4 : 2; }
-inline int64_t ch_of(qj2_dtype d) { return (int64_t)TPB * vw_of(d) * ITERS; }
+inline int64_t ch_of(qj2_dtype d) { return (int64_t)TPB * vw_of(d) * ITERS * SUB; }
 inline int pb_of(int32_t P) { return P == 1 ? 1 : P == 2 ? 2 : MAXPB; }
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
