@@ -18,6 +18,8 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdarg>
+#include <cstdlib>
+#include <algorithm>
 
 namespace qj2 {
 
@@ -374,6 +376,8 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
 
 }  // namespace qj2
 
+#include "j2_tma.cuh"
+
 // ===========================================================================
 // Small kernels
 // ===========================================================================
@@ -535,10 +539,39 @@ void ws_layout(int64_t W, int32_t P, int64_t N_local, qj2_dtype dtype,
     *cnt_bytes = tpw > 1 ? align256((size_t)W * ng * sizeof(unsigned)) : 0;
 }
 
+// Kernel choice: the TMA-pipelined persistent kernel for the no-row path
+// (default), the LDG kernel for row output.  QJ2_KERNEL=ldg forces the LDG
+// kernel (A/B measurements).
+bool use_tma() {
+    const char *e = getenv("QJ2_KERNEL");
+    return !(e && strcmp(e, "ldg") == 0);
+}
+
 template <typename T, int PB>
 cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStream_t s) {
-    if (row) j2_eval_kernel<T, PB, true><<<(unsigned)nblocks, TPB, 0, s>>>(p);
-    else     j2_eval_kernel<T, PB, false><<<(unsigned)nblocks, TPB, 0, s>>>(p);
+    if (row) {
+        j2_eval_kernel<T, PB, true><<<(unsigned)nblocks, TPB, 0, s>>>(p);
+    } else if (use_tma()) {
+        const size_t smem = tma_smem_bytes<T>(PB);
+        static int configured = 0;          // benign race: idempotent attribute set
+        static int blocks_per_sm = 0, sms = 0;
+        if (!configured) {
+            cudaError_t e = cudaFuncSetAttribute(j2_eval_tma_kernel<T, PB>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, j2_eval_tma_kernel<T, PB>,
+                                                              TMA_THREADS, smem);
+            if (e != cudaSuccess) return e;
+            configured = 1;
+        }
+        const int64_t grid = std::min<int64_t>(nblocks, (int64_t)sms * std::max(blocks_per_sm, 1));
+        j2_eval_tma_kernel<T, PB><<<(unsigned)grid, TMA_THREADS, smem, s>>>(p, (uint32_t)nblocks);
+    } else {
+        j2_eval_kernel<T, PB, false><<<(unsigned)nblocks, TPB, 0, s>>>(p);
+    }
     return cudaGetLastError();
 }
 
