@@ -16,7 +16,6 @@ namespace qj2 {
 
 constexpr int TMA_NCW = 8;                    // consumer warps
 constexpr int TMA_THREADS = (TMA_NCW + 1) * 32;
-constexpr int TMA_NST = 4;                    // ring stages
 
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(count) : "memory");
@@ -61,19 +60,21 @@ __device__ __forceinline__ TileInfo decode_tile(const EvalParams &p, uint32_t t,
     return ti;
 }
 
-template <typename T, int PB>
-__global__ void __launch_bounds__(TMA_THREADS, 2)
+// MINB: resident CTAs per SM (register budget), VPT: vectors per consumer
+// lane per stage, TMA_NST: ring stages.
+template <typename T, int PB, int MINB, int VPT, int TMA_NST>
+__global__ void __launch_bounds__(TMA_THREADS, MINB)
 j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
     using Tr = Traits<T>;
     using V = typename Tr::V;
     constexpr int VW = Tr::VW;
-    constexpr int SRC_STAGE = TPB * VW;                 // sources per stage (one vector per lane)
+    constexpr int SRC_STAGE = TPB * VW * VPT;           // sources per stage (VPT vectors per lane)
     constexpr uint32_t LANE_BYTES = SRC_STAGE * sizeof(T);
-    constexpr int STAGES_PER_TILE = ITERS * SUB;        // same tile as j2_eval_kernel
+    constexpr int STAGES_PER_TILE = ITERS * SUB / VPT;  // same tile as j2_eval_kernel
     constexpr int64_t CH = (int64_t)SRC_STAGE * STAGES_PER_TILE;
 
     extern __shared__ __align__(128) unsigned char smem[];
-    V *ring = reinterpret_cast<V *>(smem);                                   // [NST][3][TPB]
+    V *ring = reinterpret_cast<V *>(smem);                                   // [NST][3][VPT*TPB]
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + TMA_NST * 3 * LANE_BYTES);  // full[NST], empty[NST]
     Coef4<T> *tab = reinterpret_cast<Coef4<T> *>(bars + 2 * TMA_NST);       // [2][m+1]
     double *red = reinterpret_cast<double *>(tab + 2 * (QJ2_MAX_M + 1));    // [2][NCW][PB*NACC]
@@ -155,20 +156,28 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
         for (int64_t s0 = ti.start; s0 < ti.end; s0 += SRC_STAGE, ++n, ++sc) {
             const uint32_t slot = n % TMA_NST, round = n / TMA_NST;
             mbar_wait(bar_base + 8 * slot, round & 1);
-            const V *st = ring + slot * 3 * TPB;
-            const V cx = st[tid], cy = st[TPB + tid], cz = st[2 * TPB + tid];
+            const V *st = ring + slot * 3 * (VPT * TPB);
+            V cx[VPT], cy[VPT], cz[VPT];
+#pragma unroll
+            for (int u = 0; u < VPT; ++u) {
+                cx[u] = st[u * TPB + tid];
+                cy[u] = st[VPT * TPB + u * TPB + tid];
+                cz[u] = st[2 * VPT * TPB + u * TPB + tid];
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_base + 8 * (TMA_NST + slot));   // data is in registers
 
             const int64_t len = min((int64_t)SRC_STAGE, ti.end - s0);
-            const int rel = tid * VW;
             const bool k_in = k_local >= s0 && k_local < s0 + len;
             const bool clean = (len == SRC_STAGE) && !k_in && !(nup_local > s0 && nup_local < s0 + len);
+#pragma unroll
+            for (int u = 0; u < VPT; ++u) {
+            const int rel = (u * TPB + tid) * VW;
             if (clean) {
                 const uint32_t base = ((s0 < nup_local) == k_up) ? base_same : base_opp;
 #pragma unroll
                 for (int e = 0; e < VW; ++e) {
-                    const T x = Tr::comp(cx, e), y = Tr::comp(cy, e), z = Tr::comp(cz, e);
+                    const T x = Tr::comp(cx[u], e), y = Tr::comp(cy[u], e), z = Tr::comp(cz[u], e);
 #pragma unroll
                     for (int q = 0; q < PB; ++q) {
                         if (PB == 1 || q < np) {
@@ -188,7 +197,7 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
                     const int li = rel + e;
                     const bool dead = (li >= len) || (li == k_rel);
                     const uint32_t base = ((li < up_rel) == k_up) ? base_same : base_opp;
-                    const T x = Tr::comp(cx, e), y = Tr::comp(cy, e), z = Tr::comp(cz, e);
+                    const T x = Tr::comp(cx[u], e), y = Tr::comp(cy[u], e), z = Tr::comp(cz[u], e);
 #pragma unroll
                     for (int q = 0; q < PB; ++q) {
                         if (PB == 1 || q < np) {
@@ -202,7 +211,8 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
                     }
                 }
             }
-            if ((sc & (ITERS - 1)) == ITERS - 1) {      // <= ITERS*VW = 32 terms per fp32 partial
+            }
+            if ((sc & (ITERS / VPT - 1)) == ITERS / VPT - 1) {   // <= ITERS*VW = 32 terms per fp32 partial
 #pragma unroll
                 for (int q = 0; q < PB; ++q)
 #pragma unroll
@@ -276,8 +286,8 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
 }
 
 template <typename T>
-constexpr size_t tma_smem_bytes(int PB) {
-    return (size_t)TMA_NST * 3 * TPB * Traits<T>::VW * sizeof(T) + 2 * TMA_NST * sizeof(uint64_t) +
+constexpr size_t tma_smem_bytes(int PB, int VPT, int TMA_NST) {
+    return (size_t)TMA_NST * 3 * VPT * TPB * Traits<T>::VW * sizeof(T) + 2 * TMA_NST * sizeof(uint64_t) +
            2 * (QJ2_MAX_M + 1) * sizeof(Coef4<T>) + 2 * TMA_NCW * PB * NACC * sizeof(double);
 }
 

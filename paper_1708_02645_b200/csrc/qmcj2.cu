@@ -539,39 +539,57 @@ void ws_layout(int64_t W, int32_t P, int64_t N_local, qj2_dtype dtype,
     *cnt_bytes = tpw > 1 ? align256((size_t)W * ng * sizeof(unsigned)) : 0;
 }
 
-// Kernel choice: the TMA-pipelined persistent kernel for the no-row path
-// (default), the LDG kernel for row output.  QJ2_KERNEL=ldg forces the LDG
-// kernel (A/B measurements).
-bool use_tma() {
+// Kernel choice: QJ2_KERNEL=ldg | tma<minb><vpt><nst> (A/B measurements);
+// default below.
+struct TmaCfg { int minb, vpt, nst; };
+constexpr TmaCfg kTmaCfgs[] = {{2, 1, 4}, {3, 1, 4}, {4, 1, 3}, {3, 2, 3}, {4, 2, 2}, {2, 2, 4}};
+int kernel_choice() {   // -1 = LDG kernel, else index into kTmaCfgs
     const char *e = getenv("QJ2_KERNEL");
-    return !(e && strcmp(e, "ldg") == 0);
+    if (!e) return -1;
+    if (strcmp(e, "ldg") == 0) return -1;
+    if (strncmp(e, "tma", 3) == 0 && strlen(e) == 6) {
+        for (int i = 0; i < (int)(sizeof(kTmaCfgs) / sizeof(kTmaCfgs[0])); ++i)
+            if (e[3] - '0' == kTmaCfgs[i].minb && e[4] - '0' == kTmaCfgs[i].vpt && e[5] - '0' == kTmaCfgs[i].nst)
+                return i;
+    }
+    return -1;
+}
+
+template <typename T, int PB, int MINB, int VPT, int NST>
+cudaError_t launch_tma(const EvalParams &p, int64_t nblocks, cudaStream_t s) {
+    auto kern = j2_eval_tma_kernel<T, PB, MINB, VPT, NST>;
+    const size_t smem = tma_smem_bytes<T>(PB, VPT, NST);
+    static int configured = 0;          // benign race: idempotent attribute set
+    static int blocks_per_sm = 0, sms = 0;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, TMA_THREADS, smem);
+        if (e != cudaSuccess) return e;
+        configured = 1;
+    }
+    const int64_t grid = std::min<int64_t>(nblocks, (int64_t)sms * std::max(blocks_per_sm, 1));
+    kern<<<(unsigned)grid, TMA_THREADS, smem, s>>>(p, (uint32_t)nblocks);
+    return cudaGetLastError();
 }
 
 template <typename T, int PB>
 cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStream_t s) {
-    if (row) {
-        j2_eval_kernel<T, PB, true><<<(unsigned)nblocks, TPB, 0, s>>>(p);
-    } else if (use_tma()) {
-        const size_t smem = tma_smem_bytes<T>(PB);
-        static int configured = 0;          // benign race: idempotent attribute set
-        static int blocks_per_sm = 0, sms = 0;
-        if (!configured) {
-            cudaError_t e = cudaFuncSetAttribute(j2_eval_tma_kernel<T, PB>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, j2_eval_tma_kernel<T, PB>,
-                                                              TMA_THREADS, smem);
-            if (e != cudaSuccess) return e;
-            configured = 1;
-        }
-        const int64_t grid = std::min<int64_t>(nblocks, (int64_t)sms * std::max(blocks_per_sm, 1));
-        j2_eval_tma_kernel<T, PB><<<(unsigned)grid, TMA_THREADS, smem, s>>>(p, (uint32_t)nblocks);
-    } else {
-        j2_eval_kernel<T, PB, false><<<(unsigned)nblocks, TPB, 0, s>>>(p);
+    const int kc = row ? -1 : kernel_choice();
+    switch (kc) {
+        case 0: return launch_tma<T, PB, 2, 1, 4>(p, nblocks, s);
+        case 1: return launch_tma<T, PB, 3, 1, 4>(p, nblocks, s);
+        case 2: return launch_tma<T, PB, 4, 1, 3>(p, nblocks, s);
+        case 3: return launch_tma<T, PB, 3, 2, 3>(p, nblocks, s);
+        case 4: return launch_tma<T, PB, 4, 2, 2>(p, nblocks, s);
+        case 5: return launch_tma<T, PB, 2, 2, 4>(p, nblocks, s);
+        default: break;
     }
+    if (row) j2_eval_kernel<T, PB, true><<<(unsigned)nblocks, TPB, 0, s>>>(p);
+    else     j2_eval_kernel<T, PB, false><<<(unsigned)nblocks, TPB, 0, s>>>(p);
     return cudaGetLastError();
 }
 
