@@ -25,7 +25,7 @@ namespace qj2 {
 
 constexpr int TPB = 256;          // threads per CTA
 constexpr int ITERS = 8;          // vector iterations per sub-tile: 32 fp32 terms per thread per trial
-constexpr int SUB = 2;            // sub-tiles per CTA tile
+constexpr int SUB = 4;            // sub-tiles per CTA tile
 constexpr int NACC = 6;           // V, Gx, Gy, Gz, sum h, sum du/r  (per trial)
 constexpr int MAXPB = 4;
 

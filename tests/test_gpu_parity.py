@@ -74,7 +74,7 @@ def test_config_full(q, name):
 # Edge cases: tiny / ragged / tile boundaries / spin boundary / P groups
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-@pytest.mark.parametrize("N", [2, 3, 5, 17, 1023, 8191, 8192, 8193, 20001])
+@pytest.mark.parametrize("N", [2, 3, 5, 17, 1023, 8191, 8192, 8193, 20001, 32769, 70001])
 def test_ragged_sizes(q, dtype, N):
     R, k, rt, fn, n_up = instance(N, 37, seed=100 + N, dtype=dtype)
     check(q, R, k, rt, fn, N, n_up, dtype)
@@ -82,12 +82,15 @@ def test_ragged_sizes(q, dtype, N):
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 def test_k_at_tile_and_spin_boundaries(q, dtype):
-    N = 3 * 8192 + 77
-    R, k, rt, fn, _ = instance(N, 12, seed=7, dtype=dtype)
-    ks = np.array([0, 1, 4095, 4096, 8191, 8192, 8193, 12288, 16383, N - 2, N - 1, N // 2], np.int32)
+    # sub-tiles of 8192 (fp32) / 4096 (fp64) sources, CTA tiles of 4 sub-tiles
+    N = 2 * 32768 + 77
+    ks = np.array([0, 1, 4095, 4096, 8191, 8192, 8193, 16383, 32767, 32768, 32769, 65535, 65536,
+                   N - 2, N - 1, N // 2], np.int32)
+    W = ks.size
+    R, k, rt, fn, _ = instance(N, W, seed=7, dtype=dtype)
     L = qmcgen.cell_length(N)
-    rt = qmcgen.make_trials(7, np.arange(12), ks, N, L, dtype)
-    for n_up in (N // 2, 8192, 8190, 0, N, 1):   # spin boundary inside / on a tile edge / degenerate
+    rt = qmcgen.make_trials(7, np.arange(W), ks, N, L, dtype)
+    for n_up in (N // 2, 32768, 8192, 8190, 0, N, 1):   # spin boundary inside / on a tile edge / degenerate
         check(q, R, ks, rt, fn, N, n_up, dtype)
 
 
