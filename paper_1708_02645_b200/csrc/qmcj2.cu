@@ -98,11 +98,26 @@ __device__ __forceinline__ T accumulate(T dx, T dy, T dz, T r2, T inv_delta, uin
     return r;
 }
 
-// Fast path: a full tile (CH sources), no self source, one spin channel.
+// Minimum image for one axis, optionally specialised on the trial
+// coordinate's case (SPEC = 1: case A, c < L/2; 0: case B; -1: unified,
+// see make_axis).  Specialised forms take 3 instructions instead of 4.
+template <typename T, int SPEC>
+__device__ __forceinline__ T min_image_k(T x, const Axis<T> &a) {
+    if constexpr (SPEC < 0) {
+        return min_image(x, a);
+    } else if constexpr (SPEC == 1) {           // case A: wrap shifts the source (x - L exact)
+        const T xs = x > a.thr ? x - a.a1 : x;
+        return xs - a.b0;
+    } else {                                    // case B: wrap shifts the trial (c - L exact)
+        return x - (x > a.thr ? a.b1 : a.b0);
+    }
+}
+
+// Fast path: a full sub-tile, no self source, one spin channel.
 // Every thread walks ITERS vectors at a constant stride of TPB vectors, so
-// every load address is base + immediate; the next vector group is loaded
-// before the current one is consumed (software pipelining).
-template <typename T, int PB, bool ROW>
+// every load address is base + immediate; PF vector groups are in flight
+// ahead of the one being consumed (software pipelining).
+template <typename T, int PB, bool ROW, int PF, int SX, int SY, int SZ>
 __device__ __forceinline__ void tile_fast(const typename Traits<T>::V *__restrict__ px,
                                           const typename Traits<T>::V *__restrict__ py,
                                           const typename Traits<T>::V *__restrict__ pz,
@@ -111,25 +126,30 @@ __device__ __forceinline__ void tile_fast(const typename Traits<T>::V *__restric
                                           typename Traits<T>::V *const (&rowp)[PB], int64_t row_stride) {
     using Tr = Traits<T>;
     using V = typename Tr::V;
-    V cx = Tr::ld_stream(px), cy = Tr::ld_stream(py), cz = Tr::ld_stream(pz);
+    V bx[ITERS], by[ITERS], bz[ITERS];      // fully unrolled: only PF+1 groups are live
+#pragma unroll
+    for (int j = 0; j < PF && j < ITERS; ++j) {
+        bx[j] = Tr::ld_stream(px + j * TPB);
+        by[j] = Tr::ld_stream(py + j * TPB);
+        bz[j] = Tr::ld_stream(pz + j * TPB);
+    }
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
-        V nx, ny, nz;
-        if (it + 1 < ITERS) {
-            nx = Tr::ld_stream(px + (it + 1) * TPB);
-            ny = Tr::ld_stream(py + (it + 1) * TPB);
-            nz = Tr::ld_stream(pz + (it + 1) * TPB);
+        if (it + PF < ITERS) {
+            bx[it + PF] = Tr::ld_stream(px + (it + PF) * TPB);
+            by[it + PF] = Tr::ld_stream(py + (it + PF) * TPB);
+            bz[it + PF] = Tr::ld_stream(pz + (it + PF) * TPB);
         }
         V ro[PB][4];
 #pragma unroll
         for (int e = 0; e < Tr::VW; ++e) {
-            const T x = Tr::comp(cx, e), y = Tr::comp(cy, e), z = Tr::comp(cz, e);
+            const T x = Tr::comp(bx[it], e), y = Tr::comp(by[it], e), z = Tr::comp(bz[it], e);
 #pragma unroll
             for (int q = 0; q < PB; ++q) {
                 if (PB == 1 || q < np) {
-                    const T dx = min_image(x, tr[q].ax);
-                    const T dy = min_image(y, tr[q].ay);
-                    const T dz = min_image(z, tr[q].az);
+                    const T dx = min_image_k<T, SX>(x, tr[q].ax);
+                    const T dy = min_image_k<T, SY>(y, tr[q].ay);
+                    const T dz = min_image_k<T, SZ>(z, tr[q].az);
                     const T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
                     const T r = accumulate<T>(dx, dy, dz, r2, inv_delta, base, clamp_bits, acc[q]);
                     if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
@@ -143,7 +163,28 @@ __device__ __forceinline__ void tile_fast(const typename Traits<T>::V *__restric
 #pragma unroll
                     for (int c = 0; c < 4; ++c) __stcs(rowp[q] + c * row_stride + it * TPB, ro[q][c]);
         }
-        if (it + 1 < ITERS) { cx = nx; cy = ny; cz = nz; }
+    }
+}
+
+// Dispatch of the fast path: with SPEC the per-walker trial coordinate cases
+// select one of 8 specialised bodies (PB == 1 only).
+template <typename T, int PB, bool ROW, int PF, bool SPEC>
+__device__ __forceinline__ void tile_fast_dispatch(const typename Traits<T>::V *__restrict__ px,
+                                                   const typename Traits<T>::V *__restrict__ py,
+                                                   const typename Traits<T>::V *__restrict__ pz,
+                                                   const Trial<T> (&tr)[PB], int np, T inv_delta, uint32_t base,
+                                                   typename Traits<T>::U clamp_bits, T (&acc)[PB][NACC],
+                                                   typename Traits<T>::V *const (&rowp)[PB], int64_t row_stride) {
+    if constexpr (SPEC && PB == 1) {
+        const int cs = (tr[0].ax.a1 != T(0) ? 1 : 0) | (tr[0].ay.a1 != T(0) ? 2 : 0) | (tr[0].az.a1 != T(0) ? 4 : 0);
+        switch (cs) {
+#define QJ2_CASE(C) case C: tile_fast<T, PB, ROW, PF, (C & 1) ? 1 : 0, (C & 2) ? 1 : 0, (C & 4) ? 1 : 0>( \
+            px, py, pz, tr, np, inv_delta, base, clamp_bits, acc, rowp, row_stride); break;
+            QJ2_CASE(0) QJ2_CASE(1) QJ2_CASE(2) QJ2_CASE(3) QJ2_CASE(4) QJ2_CASE(5) QJ2_CASE(6) QJ2_CASE(7)
+#undef QJ2_CASE
+        }
+    } else {
+        tile_fast<T, PB, ROW, PF, -1, -1, -1>(px, py, pz, tr, np, inv_delta, base, clamp_bits, acc, rowp, row_stride);
     }
 }
 
@@ -198,8 +239,10 @@ __device__ __forceinline__ void tile_general(const typename Traits<T>::V *__rest
     }
 }
 
-template <typename T, int PB, bool ROW>
-__global__ void __launch_bounds__(TPB, (sizeof(T) == 4 && PB == 1) ? 4 : 2)
+// PF: prefetch distance (vector groups in flight), MINB: resident CTAs per SM
+// (register budget), SPEC: per-walker min-image specialisation.
+template <typename T, int PB, bool ROW, int PF = 1, int MINB = ((sizeof(T) == 4 && PB == 1) ? 4 : 2), bool SPEC = false>
+__global__ void __launch_bounds__(TPB, MINB)
 j2_eval_kernel(const __grid_constant__ EvalParams p) {
     using Tr = Traits<T>;
     using V = typename Tr::V;
@@ -296,7 +339,8 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
         } else {
             const bool tile_up = sstart < nup_local;
             const uint32_t base = (tile_up == k_up) ? base_same : base_opp;
-            tile_fast<T, PB, ROW>(px + vs, py + vs, pz + vs, tr, np, inv_delta, base, clamp_bits, acc, rp, row_stride);
+            tile_fast_dispatch<T, PB, ROW, PF, SPEC>(px + vs, py + vs, pz + vs, tr, np, inv_delta, base, clamp_bits,
+                                                     acc, rp, row_stride);
         }
 #pragma unroll
         for (int q = 0; q < PB; ++q)
@@ -588,8 +632,21 @@ cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStre
         case 5: return launch_tma<T, PB, 2, 2, 4>(p, nblocks, s);
         default: break;
     }
-    if (row) j2_eval_kernel<T, PB, true><<<(unsigned)nblocks, TPB, 0, s>>>(p);
-    else     j2_eval_kernel<T, PB, false><<<(unsigned)nblocks, TPB, 0, s>>>(p);
+    const char *e = getenv("QJ2_KERNEL");
+    const unsigned nb = (unsigned)nblocks;
+    if (row) {
+        j2_eval_kernel<T, PB, true><<<nb, TPB, 0, s>>>(p);
+    } else if (PB == 1 && e && strcmp(e, "ldg2") == 0) {
+        j2_eval_kernel<T, PB, false, 2, 3, false><<<nb, TPB, 0, s>>>(p);
+    } else if (PB == 1 && e && strcmp(e, "ldgs") == 0) {
+        j2_eval_kernel<T, PB, false, 1, 4, true><<<nb, TPB, 0, s>>>(p);
+    } else if (PB == 1 && e && strcmp(e, "ldg2s") == 0) {
+        j2_eval_kernel<T, PB, false, 2, 3, true><<<nb, TPB, 0, s>>>(p);
+    } else if (PB == 1 && e && strcmp(e, "ldg3") == 0) {
+        j2_eval_kernel<T, PB, false, 3, 3, false><<<nb, TPB, 0, s>>>(p);
+    } else {
+        j2_eval_kernel<T, PB, false><<<nb, TPB, 0, s>>>(p);
+    }
     return cudaGetLastError();
 }
 
