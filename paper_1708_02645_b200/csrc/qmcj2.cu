@@ -100,7 +100,9 @@ __device__ __forceinline__ T accumulate(T dx, T dy, T dz, T r2, T inv_delta, uin
 
 // Minimum image for one axis, optionally specialised on the trial
 // coordinate's case (SPEC = 1: case A, c < L/2; 0: case B; -1: unified,
-// see make_axis).  Specialised forms take 3 instructions instead of 4.
+// see make_axis).  Specialised forms take 3 instructions instead of 4, but the
+// 8 per-walker bodies measured slower on B200 (instruction-cache pressure,
+// DESIGN.md section 9); the kernel uses the unified form.
 template <typename T, int SPEC>
 __device__ __forceinline__ T min_image_k(T x, const Axis<T> &a) {
     if constexpr (SPEC < 0) {
@@ -166,28 +168,6 @@ __device__ __forceinline__ void tile_fast(const typename Traits<T>::V *__restric
     }
 }
 
-// Dispatch of the fast path: with SPEC the per-walker trial coordinate cases
-// select one of 8 specialised bodies (PB == 1 only).
-template <typename T, int PB, bool ROW, int PF, bool SPEC>
-__device__ __forceinline__ void tile_fast_dispatch(const typename Traits<T>::V *__restrict__ px,
-                                                   const typename Traits<T>::V *__restrict__ py,
-                                                   const typename Traits<T>::V *__restrict__ pz,
-                                                   const Trial<T> (&tr)[PB], int np, T inv_delta, uint32_t base,
-                                                   typename Traits<T>::U clamp_bits, T (&acc)[PB][NACC],
-                                                   typename Traits<T>::V *const (&rowp)[PB], int64_t row_stride) {
-    if constexpr (SPEC && PB == 1) {
-        const int cs = (tr[0].ax.a1 != T(0) ? 1 : 0) | (tr[0].ay.a1 != T(0) ? 2 : 0) | (tr[0].az.a1 != T(0) ? 4 : 0);
-        switch (cs) {
-#define QJ2_CASE(C) case C: tile_fast<T, PB, ROW, PF, (C & 1) ? 1 : 0, (C & 2) ? 1 : 0, (C & 4) ? 1 : 0>( \
-            px, py, pz, tr, np, inv_delta, base, clamp_bits, acc, rowp, row_stride); break;
-            QJ2_CASE(0) QJ2_CASE(1) QJ2_CASE(2) QJ2_CASE(3) QJ2_CASE(4) QJ2_CASE(5) QJ2_CASE(6) QJ2_CASE(7)
-#undef QJ2_CASE
-        }
-    } else {
-        tile_fast<T, PB, ROW, PF, -1, -1, -1>(px, py, pz, tr, np, inv_delta, base, clamp_bits, acc, rowp, row_stride);
-    }
-}
-
 // General path: ragged tile, the tile holding the self source k, or the
 // tile straddling the spin boundary.  Per-source masks; dead sources (self,
 // padding) get r^2 = BIG, which lands on the all-zero interval, so every
@@ -240,8 +220,8 @@ __device__ __forceinline__ void tile_general(const typename Traits<T>::V *__rest
 }
 
 // PF: prefetch distance (vector groups in flight), MINB: resident CTAs per SM
-// (register budget), SPEC: per-walker min-image specialisation.
-template <typename T, int PB, bool ROW, int PF = 1, int MINB = ((sizeof(T) == 4 && PB == 1) ? 4 : 2), bool SPEC = false>
+// (register budget).
+template <typename T, int PB, bool ROW, int PF = 1, int MINB = ((sizeof(T) == 4 && PB == 1) ? 4 : 2)>
 __global__ void __launch_bounds__(TPB, MINB)
 j2_eval_kernel(const __grid_constant__ EvalParams p) {
     using Tr = Traits<T>;
@@ -339,8 +319,8 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
         } else {
             const bool tile_up = sstart < nup_local;
             const uint32_t base = (tile_up == k_up) ? base_same : base_opp;
-            tile_fast_dispatch<T, PB, ROW, PF, SPEC>(px + vs, py + vs, pz + vs, tr, np, inv_delta, base, clamp_bits,
-                                                     acc, rp, row_stride);
+            tile_fast<T, PB, ROW, PF, -1, -1, -1>(px + vs, py + vs, pz + vs, tr, np, inv_delta, base, clamp_bits,
+                                                  acc, rp, row_stride);
         }
 #pragma unroll
         for (int q = 0; q < PB; ++q)
@@ -583,10 +563,11 @@ void ws_layout(int64_t W, int32_t P, int64_t N_local, qj2_dtype dtype,
     *cnt_bytes = tpw > 1 ? align256((size_t)W * ng * sizeof(unsigned)) : 0;
 }
 
-// Kernel choice: QJ2_KERNEL=ldg | tma<minb><vpt><nst> (A/B measurements);
-// default below.
+// Kernel choice (A/B measurements only): QJ2_KERNEL=ldg1 (prefetch distance
+// 1, 4 CTAs/SM) or tma323 (TMA-pipelined persistent kernel, 3 CTAs/SM, 2
+// vectors per lane per stage, 3 stages); default: LDG kernel, prefetch 2.
 struct TmaCfg { int minb, vpt, nst; };
-constexpr TmaCfg kTmaCfgs[] = {{2, 1, 4}, {3, 1, 4}, {4, 1, 3}, {3, 2, 3}, {4, 2, 2}, {2, 2, 4}};
+constexpr TmaCfg kTmaCfgs[] = {{3, 2, 3}};
 int kernel_choice() {   // -1 = LDG kernel, else index into kTmaCfgs
     const char *e = getenv("QJ2_KERNEL");
     if (!e) return -1;
@@ -624,26 +605,19 @@ template <typename T, int PB>
 cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStream_t s) {
     const int kc = row ? -1 : kernel_choice();
     switch (kc) {
-        case 0: return launch_tma<T, PB, 2, 1, 4>(p, nblocks, s);
-        case 1: return launch_tma<T, PB, 3, 1, 4>(p, nblocks, s);
-        case 2: return launch_tma<T, PB, 4, 1, 3>(p, nblocks, s);
-        case 3: return launch_tma<T, PB, 3, 2, 3>(p, nblocks, s);
-        case 4: return launch_tma<T, PB, 4, 2, 2>(p, nblocks, s);
-        case 5: return launch_tma<T, PB, 2, 2, 4>(p, nblocks, s);
+        case 0: return launch_tma<T, PB, 3, 2, 3>(p, nblocks, s);
         default: break;
     }
     const char *e = getenv("QJ2_KERNEL");
     const unsigned nb = (unsigned)nblocks;
     if (row) {
         j2_eval_kernel<T, PB, true><<<nb, TPB, 0, s>>>(p);
-    } else if (PB == 1 && e && strcmp(e, "ldg2") == 0) {
-        j2_eval_kernel<T, PB, false, 2, 3, false><<<nb, TPB, 0, s>>>(p);
-    } else if (PB == 1 && e && strcmp(e, "ldgs") == 0) {
-        j2_eval_kernel<T, PB, false, 1, 4, true><<<nb, TPB, 0, s>>>(p);
-    } else if (PB == 1 && e && strcmp(e, "ldg2s") == 0) {
-        j2_eval_kernel<T, PB, false, 2, 3, true><<<nb, TPB, 0, s>>>(p);
-    } else if (PB == 1 && e && strcmp(e, "ldg3") == 0) {
-        j2_eval_kernel<T, PB, false, 3, 3, false><<<nb, TPB, 0, s>>>(p);
+    } else if constexpr (PB == 1) {
+        if (e && strcmp(e, "ldg1") == 0)       // A/B: prefetch distance 1, 4 CTAs/SM
+            j2_eval_kernel<T, PB, false, 1, 4><<<nb, TPB, 0, s>>>(p);
+        else    // default: two vector groups in flight per thread, 3 CTAs/SM (80 registers);
+                // measured best on B200
+            j2_eval_kernel<T, PB, false, 2, 3><<<nb, TPB, 0, s>>>(p);
     } else {
         j2_eval_kernel<T, PB, false><<<nb, TPB, 0, s>>>(p);
     }
