@@ -285,10 +285,20 @@ class C3Plan:
         self.cfg = cfg
         self.seed = cfg.seed + rank
         self.items_per_step = cfg.W * (cfg.N - 1)
+
+    def items_total(self, world):
+        return self.items_per_step * world
+
+    def _alg(self):
+        cfg = self.cfg
         sz = 4
         # algorithmic bytes: x, y, z of every source i != k once per walker,
         # plus per walker k (4 B), r_trial (12 B), V_cur (8 B), out (40 B), ratio (16 B)
-        self.alg_bytes_per_launch = cfg.W * (cfg.N - 1) * 3 * sz + cfg.W * (4 + 12 + 8 + 40 + 16)
+        return cfg.W * (cfg.N - 1) * 3 * sz + cfg.W * (4 + 12 + 8 + 40 + 16)
+
+    @property
+    def alg_bytes_per_launch(self):
+        return self._alg()
 
     def prepare(self, q):
         import torch
@@ -361,10 +371,185 @@ class C3Plan:
                 "matches_device_path": same}
 
 
+def _event_ms(fn, stream, reps=1):
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+class C5Plan:
+    """One instance N = 4,915,200 x W = 1024 split along the electron axis: rank g
+    evaluates sources [g*N/G, (g+1)*N/G) (qj2_eval with i_offset), then one NCCL
+    all_reduce(SUM) of the 40 KB fp64 partials and qj2_ratio (strong scaling)."""
+    mode = "C5"
+    launches_per_step = 3      # j2_eval_kernel + counter memset + ratio_kernel (+ NCCL all-reduce if G > 1)
+
+    def __init__(self, cfg, rank, world):
+        from paper_1708_02645_b200 import parallel
+        self.cfg, self.rank, self.world = cfg, rank, world
+        self.a, self.b = parallel.shard_bounds(cfg.N, rank, world)
+        self.n_local = self.b - self.a
+        self.Np = ((self.n_local + 31) // 32) * 32
+        self.items_per_step = cfg.W * (cfg.N - 1)      # global: every rank reports the whole job
+        self.alg_bytes_per_launch = cfg.W * self.n_local * 12 + cfg.W * (4 + 12 + 40)
+
+    def items_total(self, world):
+        return self.items_per_step
+
+    def prepare(self, q):
+        import torch
+        import qmcgen
+        from paper_1708_02645_b200 import parallel
+        self.parallel = parallel
+        cfg = self.cfg
+        self.fn = q.Functor.of(qmcgen.make_functor(cfg.seed, cfg.L, cfg.m))
+        self.R = q.gen_positions(cfg.seed, cfg.W, self.n_local, self.Np, cfg.L, torch.float32, i_offset=self.a)
+        k = qmcgen.make_k(cfg.seed, cfg.W, cfg.N)
+        rt = qmcgen.make_trials(cfg.seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32)
+        rk = qmcgen.make_trials(cfg.seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32, mode="noop")
+        self.k = torch.from_numpy(k).cuda()
+        self.rt = torch.from_numpy(rt).cuda()
+        self.ws = q.Workspace(q.workspace_size(cfg.W, 1, self.n_local, torch.float32))
+        v0 = parallel.eval_sharded(self.R, self.k, torch.from_numpy(rk).cuda(), self.fn, cfg.N, cfg.n_up,
+                                   self.a, self.n_local, workspace=self.ws)
+        self.V_cur = v0[:, 0, 0].contiguous()
+        self.out = torch.empty((cfg.W, 1, 5), dtype=torch.float64, device="cuda")
+        self.ratio = torch.empty((cfg.W, 1, 2), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+
+    def step(self, q, dist_mod):
+        cfg = self.cfg
+        self.parallel.eval_sharded(self.R, self.k, self.rt, self.fn, cfg.N, cfg.n_up, self.a, self.n_local,
+                                   V_cur=self.V_cur, ratio=True, out=self.out, ratio_out=self.ratio,
+                                   workspace=self.ws)
+
+    def kernel_ms(self, q, stream, reps):
+        cfg = self.cfg
+        return _event_ms(lambda: q.eval(self.R, self.k, self.rt, self.fn, cfg.N, cfg.n_up, i_offset=self.a,
+                                        n_local=self.n_local, out=self.out, workspace=self.ws), stream, reps)
+
+    def e2e(self, q, steps, dist_mod):
+        return None   # see DESIGN.md: the host-buffer path is measured on C3
+
+
+class C4Plan:
+    """4096 independent instances (N = 6144, W = 1024, seeds 3..4098, one functor)
+    sharded by instance; each rank evaluates its instances as one batch of
+    n_inst * 1024 walkers per launch, in waves that fit HBM (generation of a
+    wave is outside the timed spans; the step time is the sum of the waves'
+    kernel spans).  No collective on the data path."""
+    mode = "C4"
+    launches_per_step = 2      # per wave: j2_eval_kernel (+ no memset: one tile per walker)
+    MAX_RESIDENT = 1024        # instances per wave (77 GB)
+
+    def __init__(self, cfg, rank, world):
+        from paper_1708_02645_b200 import parallel
+        self.cfg, self.rank, self.world = cfg, rank, world
+        self.i0, self.i1 = parallel.instance_range(cfg.instances, rank, world)
+        self.n_inst = self.i1 - self.i0
+        self.waves = parallel.waves(self.i0, self.n_inst, self.MAX_RESIDENT)
+        self.launches_per_step = len(self.waves)
+        self.items_per_step = self.n_inst * cfg.W * (cfg.N - 1)
+        n_first = self.waves[0][1] if self.waves else 0
+        self.alg_bytes_per_launch = n_first * cfg.W * ((cfg.N - 1) * 12 + 4 + 12 + 8 + 40 + 16)
+
+    def items_total(self, world):
+        return self.cfg.instances * self.cfg.W * (self.cfg.N - 1)
+
+    def _gen_wave(self, q, first, count):
+        import torch
+        cfg = self.cfg
+        for j in range(count):
+            q.gen_positions(cfg.seed + first + j, cfg.W, cfg.N, cfg.Np, cfg.L, torch.float32,
+                            out=self.R[j * cfg.W:(j + 1) * cfg.W])
+
+    def prepare(self, q):
+        import torch
+        import qmcgen
+        cfg = self.cfg
+        self.fn = q.Functor.of(qmcgen.make_functor(cfg.seed, cfg.L, cfg.m))
+        nmax = max((c for _, c in self.waves), default=0)
+        self.R = torch.empty((nmax * cfg.W, 3, cfg.Np), dtype=torch.float32, device="cuda")
+        ks, rts, rks = [], [], []
+        for inst in range(self.i0, self.i1):
+            seed = cfg.seed + inst
+            k = qmcgen.make_k(seed, cfg.W, cfg.N)
+            ks.append(k)
+            rts.append(qmcgen.make_trials(seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32))
+            rks.append(qmcgen.make_trials(seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32, mode="noop"))
+        self.k = torch.from_numpy(np.concatenate(ks)).cuda()
+        self.rt = torch.from_numpy(np.concatenate(rts)).cuda()
+        rk = torch.from_numpy(np.concatenate(rks)).cuda()
+        self.ws = q.Workspace(0)
+        self.out = torch.empty((self.n_inst * cfg.W, 1, 5), dtype=torch.float64, device="cuda")
+        self.ratio = torch.empty((self.n_inst * cfg.W, 1, 2), dtype=torch.float64, device="cuda")
+        self.V_cur = torch.empty((self.n_inst * cfg.W,), dtype=torch.float64, device="cuda")
+        for first, count in self.waves:
+            self._gen_wave(q, first, count)
+            sl = self._slice(first, count)
+            v0 = q.eval(self.R[:count * cfg.W], self.k[sl], rk[sl], self.fn, cfg.N, cfg.n_up, workspace=self.ws)
+            self.V_cur[sl] = v0[:, 0, 0]
+        self.resident = self.waves[-1] if self.waves else None
+        torch.cuda.synchronize()
+
+    def _slice(self, first, count):
+        W = self.cfg.W
+        return slice((first - self.i0) * W, (first - self.i0 + count) * W)
+
+    def _eval_wave(self, q, first, count):
+        cfg = self.cfg
+        sl = self._slice(first, count)
+        q.eval(self.R[:count * cfg.W], self.k[sl], self.rt[sl], self.fn, cfg.N, cfg.n_up, V_cur=self.V_cur[sl],
+               ratio=True, out=self.out[sl], ratio_out=self.ratio[sl], workspace=self.ws)
+
+    def step(self, q, dist_mod):
+        # warm-up form: evaluate the resident wave(s) only
+        if len(self.waves) == 1:
+            self._eval_wave(q, *self.waves[0])
+        else:
+            self._eval_wave(q, *self.resident)
+
+    def timed(self, K, stream, local, dist_mod):
+        """Sum over waves of the kernel spans (generation between waves untimed)."""
+        import torch
+        if dist_mod:
+            dist_mod.barrier()
+        torch.cuda.synchronize()
+        total = 0.0
+        with ClockSampler(local) as clk:
+            if len(self.waves) == 1:
+                total = _event_ms(lambda: self._eval_wave(q, *self.waves[0]), stream, K) * K
+            else:
+                for _ in range(K):
+                    for first, count in self.waves:
+                        if (first, count) != self.resident:
+                            self._gen_wave(q, first, count)
+                            self.resident = (first, count)
+                            torch.cuda.synchronize()
+                        total += _event_ms(lambda: self._eval_wave(q, first, count), stream, 1)
+        if dist_mod:
+            dist_mod.barrier()
+        return total / K, clk
+
+    def kernel_ms(self, q, stream, reps):
+        return _event_ms(lambda: self._eval_wave(q, *self.resident), stream, reps)
+
+    def e2e(self, q, steps, dist_mod):
+        return None   # see DESIGN.md: the host-buffer path is measured on C3
+
+
 def make_plan(cfg, rank, world):
     if cfg.name == "C3":
         return C3Plan(cfg, rank, world)
-    from paper_1708_02645_b200 import parallel  # noqa: F401
+    if cfg.name == "C4":
+        return C4Plan(cfg, rank, world)
+    if cfg.name == "C5":
+        return C5Plan(cfg, rank, world)
     raise NotImplementedError(cfg.name)
 
 
@@ -403,12 +588,13 @@ def run_ours(args):
             dist_mod.barrier()
         return e0.elapsed_time(e1) / K, clk
 
-    ms, clk = timed(args.steps)
+    run_timed = (lambda K: plan.timed(K, stream, local, dist_mod)) if hasattr(plan, "timed") else timed
+    ms, clk = run_timed(args.steps)
     if clk.rejected():
         log(f"[bench] clocks rejected ({clk.summary()}); re-measuring once")
-        ms, clk = timed(args.steps)
+        ms, clk = run_timed(args.steps)
     ms_max = allreduce_max(ms, dist_mod)
-    items_total = plan.items_per_step * world
+    items_total = plan.items_total(world)
     value = items_total / (ms_max / 1e3)
 
     # roofline of the dominant kernel (j2_eval_kernel), timed on its launching stream

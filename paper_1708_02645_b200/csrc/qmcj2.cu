@@ -115,36 +115,67 @@ __device__ __forceinline__ T min_image_k(T x, const Axis<T> &a) {
     }
 }
 
-// Fast path: a full sub-tile, no self source, one spin channel.
-// Every thread walks ITERS vectors at a constant stride of TPB vectors, so
-// every load address is base + immediate; PF vector groups are in flight
-// ahead of the one being consumed (software pipelining).
-template <typename T, int PB, bool ROW, int PF, int SX, int SY, int SZ>
-__device__ __forceinline__ void tile_fast(const typename Traits<T>::V *__restrict__ px,
-                                          const typename Traits<T>::V *__restrict__ py,
-                                          const typename Traits<T>::V *__restrict__ pz,
-                                          const Trial<T> (&tr)[PB], int np, T inv_delta, uint32_t base,
-                                          typename Traits<T>::U clamp_bits, T (&acc)[PB][NACC],
-                                          typename Traits<T>::V *const (&rowp)[PB], int64_t row_stride) {
+// Masks of a sub-tile that is not "clean" (ragged length, holds the self
+// source k, or straddles the spin boundary N_up).  All offsets are relative to
+// the sub-tile start.
+struct SubMask {
+    int len;          // valid sources in the sub-tile
+    int k_rel;        // self source, or -1
+    int up_rel;       // first spin-down source (clamped to [0, SCH])
+    bool k_up;        // spin of k
+};
+
+// One sub-tile.  Every thread walks ITERS vectors at a constant stride of TPB
+// vectors, so every load address is base + immediate; PF vector groups are in
+// flight ahead of the one being consumed (software pipelining).
+// GEN = false: full sub-tile, no self source, one spin channel (`base`).
+// GEN = true: loads predicated on the sub-tile length; per source, dead
+// sources (self, padding) get r^2 = BIG, which lands on the all-zero interval
+// (every accumulated quantity exactly 0), and the channel is chosen per source.
+template <typename T, int PB, bool ROW, int PF, bool GEN, int NT = TPB, int SX = -1, int SY = -1, int SZ = -1>
+__device__ __forceinline__ void tile_run(int tid,const typename Traits<T>::V *__restrict__ px,
+                                         const typename Traits<T>::V *__restrict__ py,
+                                         const typename Traits<T>::V *__restrict__ pz,
+                                         const Trial<T> (&tr)[PB], int np, T inv_delta, uint32_t base,
+                                         uint32_t base_opp, const SubMask &mk,
+                                         typename Traits<T>::U clamp_bits, T (&acc)[PB][NACC],
+                                         typename Traits<T>::V *const (&rowp)[PB], int64_t row_stride) {
     using Tr = Traits<T>;
     using V = typename Tr::V;
+    constexpr int VW = Tr::VW;
+    // GEN: vector index clamped into the sub-tile (vectors past the end reload
+    // the last valid vector; their sources are all dead), so loads need no
+    // predicate and the pipeline has the same shape as the fast path.
+    const int vmax = GEN ? (mk.len - 1) / VW : 0;
+    auto voff = [&](int j) -> int {
+        return GEN ? min(j * NT + tid, vmax) - tid : j * NT;   // relative to this thread's vector
+    };
     V bx[ITERS], by[ITERS], bz[ITERS];      // fully unrolled: only PF+1 groups are live
 #pragma unroll
     for (int j = 0; j < PF && j < ITERS; ++j) {
-        bx[j] = Tr::ld_stream(px + j * TPB);
-        by[j] = Tr::ld_stream(py + j * TPB);
-        bz[j] = Tr::ld_stream(pz + j * TPB);
+        bx[j] = Tr::ld_stream(px + voff(j));
+        by[j] = Tr::ld_stream(py + voff(j));
+        bz[j] = Tr::ld_stream(pz + voff(j));
     }
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
         if (it + PF < ITERS) {
-            bx[it + PF] = Tr::ld_stream(px + (it + PF) * TPB);
-            by[it + PF] = Tr::ld_stream(py + (it + PF) * TPB);
-            bz[it + PF] = Tr::ld_stream(pz + (it + PF) * TPB);
+            bx[it + PF] = Tr::ld_stream(px + voff(it + PF));
+            by[it + PF] = Tr::ld_stream(py + voff(it + PF));
+            bz[it + PF] = Tr::ld_stream(pz + voff(it + PF));
         }
+        const int rel = (it * NT + tid) * VW;
+        if (!GEN || rel < mk.len) {
         V ro[PB][4];
 #pragma unroll
-        for (int e = 0; e < Tr::VW; ++e) {
+        for (int e = 0; e < VW; ++e) {
+            bool dead = false;
+            uint32_t b = base;
+            if (GEN) {
+                const int li = rel + e;
+                dead = (li >= mk.len) || (li == mk.k_rel);
+                b = ((li < mk.up_rel) == mk.k_up) ? base : base_opp;
+            }
             const T x = Tr::comp(bx[it], e), y = Tr::comp(by[it], e), z = Tr::comp(bz[it], e);
 #pragma unroll
             for (int q = 0; q < PB; ++q) {
@@ -152,59 +183,9 @@ __device__ __forceinline__ void tile_fast(const typename Traits<T>::V *__restric
                     const T dx = min_image_k<T, SX>(x, tr[q].ax);
                     const T dy = min_image_k<T, SY>(y, tr[q].ay);
                     const T dz = min_image_k<T, SZ>(z, tr[q].az);
-                    const T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-                    const T r = accumulate<T>(dx, dy, dz, r2, inv_delta, base, clamp_bits, acc[q]);
-                    if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
-                }
-            }
-        }
-        if (ROW) {
-#pragma unroll
-            for (int q = 0; q < PB; ++q)
-                if (PB == 1 || q < np)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) __stcs(rowp[q] + c * row_stride + it * TPB, ro[q][c]);
-        }
-    }
-}
-
-// General path: ragged tile, the tile holding the self source k, or the
-// tile straddling the spin boundary.  Per-source masks; dead sources (self,
-// padding) get r^2 = BIG, which lands on the all-zero interval, so every
-// accumulated quantity is exactly 0 for them.
-template <typename T, int PB, bool ROW>
-__device__ __forceinline__ void tile_general(const typename Traits<T>::V *__restrict__ px,
-                                          const typename Traits<T>::V *__restrict__ py,
-                                          const typename Traits<T>::V *__restrict__ pz,
-                                          const Trial<T> (&tr)[PB], int np, T inv_delta,
-                                          uint32_t base_same, uint32_t base_opp, bool k_up,
-                                          typename Traits<T>::U clamp_bits, int len, int k_rel, int up_rel,
-                                          T (&acc)[PB][NACC],
-                                          typename Traits<T>::V *const (&rowp)[PB], int64_t row_stride) {
-    using Tr = Traits<T>;
-    using V = typename Tr::V;
-    constexpr int VW = Tr::VW;
-    const int tid = threadIdx.x;
-    for (int it = 0; it < ITERS; ++it) {
-        const int rel = (it * TPB + tid) * VW;          // offset of this vector inside the tile
-        if (rel >= len) break;
-        const V cx = Tr::ld_stream(px + it * TPB), cy = Tr::ld_stream(py + it * TPB), cz = Tr::ld_stream(pz + it * TPB);
-        V ro[PB][4];
-#pragma unroll
-        for (int e = 0; e < VW; ++e) {
-            const int li = rel + e;
-            const bool dead = (li >= len) || (li == k_rel);
-            const uint32_t base = ((li < up_rel) == k_up) ? base_same : base_opp;
-            const T x = Tr::comp(cx, e), y = Tr::comp(cy, e), z = Tr::comp(cz, e);
-#pragma unroll
-            for (int q = 0; q < PB; ++q) {
-                if (PB == 1 || q < np) {
-                    const T dx = min_image(x, tr[q].ax);
-                    const T dy = min_image(y, tr[q].ay);
-                    const T dz = min_image(z, tr[q].az);
                     T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-                    r2 = dead ? T(1e30) : r2;
-                    const T r = accumulate<T>(dx, dy, dz, r2, inv_delta, base, clamp_bits, acc[q]);
+                    if (GEN) r2 = dead ? T(1e30) : r2;
+                    const T r = accumulate<T>(dx, dy, dz, r2, inv_delta, b, clamp_bits, acc[q]);
                     if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
                 }
             }
@@ -214,7 +195,8 @@ __device__ __forceinline__ void tile_general(const typename Traits<T>::V *__rest
             for (int q = 0; q < PB; ++q)
                 if (PB == 1 || q < np)
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) __stcs(rowp[q] + c * row_stride + it * TPB, ro[q][c]);
+                    for (int c = 0; c < 4; ++c) __stcs(rowp[q] + c * row_stride + it * NT, ro[q][c]);
+        }
         }
     }
 }
@@ -311,16 +293,21 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
 #pragma unroll
         for (int q = 0; q < PB; ++q) rp[q] = ROW ? rowp[q] + vs : nullptr;
         if (masked) {
-            const int len = (int)(send - sstart);
-            const int k_rel = k_in ? (int)(k_local - sstart) : -1;
-            const int up_rel = (int)max((int64_t)0, min(nup_local - sstart, (int64_t)SCH));
-            tile_general<T, PB, ROW>(px + vs, py + vs, pz + vs, tr, np, inv_delta, base_same, base_opp, k_up,
-                                     clamp_bits, len, k_rel, up_rel, acc, rp, row_stride);
+            SubMask mk;
+            mk.len = (int)(send - sstart);
+            mk.k_rel = k_in ? (int)(k_local - sstart) : -1;
+            mk.up_rel = (int)max((int64_t)0, min(nup_local - sstart, (int64_t)SCH));
+            mk.k_up = true;   // base_same is "channel of sources below up_rel" iff k is up
+            const uint32_t b_lo = k_up ? base_same : base_opp;   // channel of sources i < N_up
+            const uint32_t b_hi = k_up ? base_opp : base_same;   // channel of sources i >= N_up
+            tile_run<T, PB, ROW, PF, true>(threadIdx.x, px + vs, py + vs, pz + vs, tr, np, inv_delta, b_lo, b_hi, mk,
+                                           clamp_bits, acc, rp, row_stride);
         } else {
             const bool tile_up = sstart < nup_local;
             const uint32_t base = (tile_up == k_up) ? base_same : base_opp;
-            tile_fast<T, PB, ROW, PF, -1, -1, -1>(px + vs, py + vs, pz + vs, tr, np, inv_delta, base, clamp_bits,
-                                                  acc, rp, row_stride);
+            SubMask mk{SCH, -1, 0, true};
+            tile_run<T, PB, ROW, PF, false>(threadIdx.x, px + vs, py + vs, pz + vs, tr, np, inv_delta, base, base, mk,
+                                            clamp_bits, acc, rp, row_stride);
         }
 #pragma unroll
         for (int q = 0; q < PB; ++q)
@@ -393,6 +380,122 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
                     p.ratio_out[o * 2 + 0] = dj;
                     p.ratio_out[o * 2 + 1] = exp(dj);
                 }
+            }
+        }
+    }
+}
+
+// Small-N mapping (one tile per walker and many walkers, e.g. C1, C2, C4):
+// one warp per (walker, trial group) walks all of the walker's sources in
+// per-warp sub-tiles of 32*VW*ITERS sources (<= 32 fp32 terms per lane, then
+// an fp64 flush), so there is no shared-memory reduction, no cross-CTA
+// partials and no counters; the warp's fp64 shuffle tree is the whole
+// (deterministic) reduction.
+template <typename T, int PB, bool ROW, int PF, int MINB = (sizeof(T) == 4 && PB == 1 && !ROW) ? 3 : 2>
+__global__ void __launch_bounds__(TPB, MINB)
+j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
+    using Tr = Traits<T>;
+    using V = typename Tr::V;
+    constexpr int VW = Tr::VW;
+    constexpr int SCH = 32 * VW * ITERS;
+    __shared__ Coef4<T> tab[2 * (QJ2_MAX_M + 1)];
+    load_table<T>(p, tab);
+    __syncthreads();
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t unit = (int64_t)blockIdx.x * (TPB / 32) + warp;
+    if (unit >= n_units) return;
+    const int64_t w = unit / p.n_groups, g = unit - w * p.n_groups;
+    const int32_t p0 = (int32_t)g * PB;
+    const int np = min(PB, p.P - p0);
+    const int64_t kw = p.k[w];
+    const bool k_up = kw < p.N_up;
+    const T L0 = T(p.L[0]), L1 = T(p.L[1]), L2 = T(p.L[2]);
+    Trial<T> tr[PB];
+#pragma unroll
+    for (int q = 0; q < PB; ++q) {
+        const int qq = q < np ? q : 0;
+        const T *rt = static_cast<const T *>(p.r_trial) + ((w * p.P + p0 + qq) * 3);
+        tr[q].ax = make_axis<T>(rt[0], L0);
+        tr[q].ay = make_axis<T>(rt[1], L1);
+        tr[q].az = make_axis<T>(rt[2], L2);
+    }
+    const T inv_delta = sizeof(T) == 4 ? T(p.inv_delta_f) : T(p.inv_delta);
+    const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tab);
+    const uint32_t magic_off = (uint32_t)(Tr::MAGIC_BITS * (typename Tr::U)sizeof(Coef4<T>));
+    const uint32_t base_same = tab_addr - magic_off;
+    const uint32_t base_opp = tab_addr + (uint32_t)((p.m + 1) * sizeof(Coef4<T>)) - magic_off;
+    const typename Tr::U clamp_bits = Tr::MAGIC_BITS + (typename Tr::U)p.m;
+    const int64_t k_local = kw - p.i_offset;
+    const int64_t nup_local = p.N_up - p.i_offset;
+    const T *Rw = static_cast<const T *>(p.R) + w * 3 * p.Np;
+    const int64_t row_stride = p.Np / VW;
+
+    double dacc[PB][NACC];
+#pragma unroll
+    for (int q = 0; q < PB; ++q)
+#pragma unroll
+        for (int a = 0; a < NACC; ++a) dacc[q][a] = 0.0;
+
+    for (int64_t sstart = 0; sstart < p.N_local; sstart += SCH) {
+        const int64_t send = min(sstart + (int64_t)SCH, p.N_local);
+        const int64_t voff = (sstart / VW) + lane;
+        const V *px = reinterpret_cast<const V *>(Rw) + voff;
+        const V *py = reinterpret_cast<const V *>(Rw + p.Np) + voff;
+        const V *pz = reinterpret_cast<const V *>(Rw + 2 * p.Np) + voff;
+        V *rp[PB];
+#pragma unroll
+        for (int q = 0; q < PB; ++q)
+            rp[q] = ROW ? reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + p0 + (q < np ? q : 0)) * 4) * p.Np) + voff
+                        : nullptr;
+        T acc[PB][NACC];
+#pragma unroll
+        for (int q = 0; q < PB; ++q)
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) acc[q][a] = T(0);
+        const bool k_in = k_local >= sstart && k_local < send;
+        const bool masked = (send - sstart != SCH) || k_in || (nup_local > sstart && nup_local < send);
+        if (masked) {
+            SubMask mk;
+            mk.len = (int)(send - sstart);
+            mk.k_rel = k_in ? (int)(k_local - sstart) : -1;
+            mk.up_rel = (int)max((int64_t)0, min(nup_local - sstart, (int64_t)SCH));
+            mk.k_up = true;
+            const uint32_t b_lo = k_up ? base_same : base_opp;
+            const uint32_t b_hi = k_up ? base_opp : base_same;
+            tile_run<T, PB, ROW, PF, true, 32>(lane, px, py, pz, tr, np, inv_delta, b_lo, b_hi, mk, clamp_bits,
+                                               acc, rp, row_stride);
+        } else {
+            const uint32_t base = ((sstart < nup_local) == k_up) ? base_same : base_opp;
+            SubMask mk{SCH, -1, 0, true};
+            tile_run<T, PB, ROW, PF, false, 32>(lane, px, py, pz, tr, np, inv_delta, base, base, mk, clamp_bits,
+                                                acc, rp, row_stride);
+        }
+#pragma unroll
+        for (int q = 0; q < PB; ++q)
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) dacc[q][a] += (double)acc[q][a];
+    }
+
+    const double id = p.inv_delta;
+    double V0 = 0.0;
+#pragma unroll
+    for (int q = 0; q < PB; ++q) {
+        double s[NACC];
+#pragma unroll
+        for (int a = 0; a < NACC; ++a) s[a] = warp_sum(dacc[q][a]);
+        if (q == 0) V0 = s[0];
+        if (lane == 0 && q < np) {
+            const int64_t o = w * p.P + p0 + q;
+            p.out[o * 5 + 0] = s[0];
+            p.out[o * 5 + 1] = -id * s[1];
+            p.out[o * 5 + 2] = -id * s[2];
+            p.out[o * 5 + 3] = -id * s[3];
+            p.out[o * 5 + 4] = 2.0 * id * id * s[4] + 2.0 * id * s[5];
+            if (p.ratio_out) {
+                const double dj = s[0] - (p.V_cur ? p.V_cur[w] : V0);
+                p.ratio_out[o * 2 + 0] = dj;
+                p.ratio_out[o * 2 + 1] = exp(dj);
             }
         }
     }
@@ -601,8 +704,21 @@ cudaError_t launch_tma(const EvalParams &p, int64_t nblocks, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// Warp-per-walker mapping when a walker's slice is one CTA tile and there
+// are enough (walker, group) units to fill the GPU (or the slice is tiny).
+bool use_warp_mapping(const EvalParams &p) {
+    return p.tiles_per_walker == 1 && (p.W * p.n_groups >= 4096 || p.N_local <= 2048);
+}
+
 template <typename T, int PB>
 cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStream_t s) {
+    if (use_warp_mapping(p)) {
+        const int64_t units = p.W * p.n_groups;
+        const unsigned nbw = (unsigned)((units + TPB / 32 - 1) / (TPB / 32));
+        if (row) j2_eval_warp_kernel<T, PB, true, 1><<<nbw, TPB, 0, s>>>(p, units);
+        else     j2_eval_warp_kernel<T, PB, false, 2><<<nbw, TPB, 0, s>>>(p, units);
+        return cudaGetLastError();
+    }
     const int kc = row ? -1 : kernel_choice();
     switch (kc) {
         case 0: return launch_tma<T, PB, 3, 2, 3>(p, nblocks, s);
@@ -612,12 +728,14 @@ cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStre
     const unsigned nb = (unsigned)nblocks;
     if (row) {
         j2_eval_kernel<T, PB, true><<<nb, TPB, 0, s>>>(p);
-    } else if constexpr (PB == 1) {
+    } else if constexpr (PB == 1 && sizeof(T) == 4) {
         if (e && strcmp(e, "ldg1") == 0)       // A/B: prefetch distance 1, 4 CTAs/SM
             j2_eval_kernel<T, PB, false, 1, 4><<<nb, TPB, 0, s>>>(p);
         else    // default: two vector groups in flight per thread, 3 CTAs/SM (80 registers);
                 // measured best on B200
             j2_eval_kernel<T, PB, false, 2, 3><<<nb, TPB, 0, s>>>(p);
+    } else if constexpr (PB == 1) {             // fp64: two groups in flight, 2 CTAs/SM
+        j2_eval_kernel<T, PB, false, 2, 2><<<nb, TPB, 0, s>>>(p);
     } else {
         j2_eval_kernel<T, PB, false><<<nb, TPB, 0, s>>>(p);
     }
