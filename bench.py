@@ -472,6 +472,7 @@ class C4Plan:
         import torch
         import qmcgen
         cfg = self.cfg
+        self.q = q
         self.fn = q.Functor.of(qmcgen.make_functor(cfg.seed, cfg.L, cfg.m))
         nmax = max((c for _, c in self.waves), default=0)
         self.R = torch.empty((nmax * cfg.W, 3, cfg.Np), dtype=torch.float32, device="cuda")
@@ -517,6 +518,7 @@ class C4Plan:
     def timed(self, K, stream, local, dist_mod):
         """Sum over waves of the kernel spans (generation between waves untimed)."""
         import torch
+        q = self.q
         if dist_mod:
             dist_mod.barrier()
         torch.cuda.synchronize()
