@@ -320,3 +320,71 @@ def test_C5_sliced_single_gpu_sampled(q):
         del R
     torch.cuda.empty_cache()
     _sampled_check(q, cfg, cfg.seed, None, np.array([0, 333, 1023]), out=tot)
+
+
+# ---------------------------------------------------------------------------
+# Warp-per-walker mapping (>= 4096 walker units, one tile per walker): the
+# kernel C4's bench waves run.  Positions generated on the device; the oracle
+# side regenerates sampled walkers with its own C generator.
+# ---------------------------------------------------------------------------
+def _warp_case(q, N, W, seed, dtype, row=False, P=1, sample=(0, 1, 97, 2048, 4095)):
+    tdt = torch.float32 if dtype == np.float32 else torch.float64
+    L = qmcgen.cell_length(N)
+    Np = qmcgen.padded_size(N, 32 if dtype == np.float32 else 16)
+    R = q.gen_positions(seed, W, N, Np, L, tdt)
+    k = qmcgen.make_k(seed, W, N)
+    rt = qmcgen.make_trials(seed, np.arange(W), k, N, L, dtype, P=P)
+    fn = qmcgen.make_functor(seed, L)
+    res = q.eval(R, dev(k), dev(rt), fn, N, N // 2, row=row)
+    out = (res[0] if row else res).cpu().numpy()
+    w = np.array(sample)
+    Rs = np.concatenate([oracle.gen_positions(seed, int(i), 1, N, Np, L, dtype) for i in w])
+    orc, absout, orow = oracle.eval_j2(Rs, k[w], rt[w], fn, N, N // 2, row=row, threads=THREADS)
+    assert oracle.normalized_error(out[w], orc, absout, fn).max() <= TOL[dtype]
+    assert np.all(np.isfinite(out))
+    if row:
+        rowg = res[1].cpu().numpy()[w]
+        for a in range(w.size):
+            i = np.array([j for j in range(N) if j != k[w[a]]])
+            if dtype == np.float32:
+                tie = np.abs(np.abs(orow[a, 0, 1:, i]) - L / 2) <= 4 * np.spacing(np.float32(L))
+                assert np.all((rowg[a, 0, 1:, i] == orow[a, 0, 1:, i].astype(np.float32)) | tie)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("N", [1000, 5003, 6144, 10001])
+def test_warp_mapping_parity(q, dtype, N):
+    _warp_case(q, N, 4096, seed=400 + N, dtype=dtype)
+
+
+def test_warp_mapping_row_and_multi_trial(q):
+    _warp_case(q, 3001, 4096, seed=77, dtype=np.float32, row=True)
+    _warp_case(q, 2500, 4096, seed=78, dtype=np.float32, P=2)
+    _warp_case(q, 2500, 2048, seed=79, dtype=np.float64, P=3)
+
+
+def test_C4_batched_waves_as_benched(q):
+    """C4 exactly as bench.py runs it: instances concatenated into one launch
+    (here 5 instances = 5120 walkers, warp mapping), shared functor (R16)."""
+    cfg = qmcgen.CONFIGS["C4"]
+    insts = [0, 1, 2, 3, 4095]
+    W = cfg.W
+    R = torch.empty((len(insts) * W, 3, cfg.Np), dtype=torch.float32, device="cuda")
+    ks, rts = [], []
+    for j, inst in enumerate(insts):
+        seed = cfg.seed + inst
+        q.gen_positions(seed, W, cfg.N, cfg.Np, cfg.L, torch.float32, out=R[j * W:(j + 1) * W])
+        k = qmcgen.make_k(seed, W, cfg.N)
+        ks.append(k)
+        rts.append(qmcgen.make_trials(seed, np.arange(W), k, cfg.N, cfg.L, np.float32))
+    k = np.concatenate(ks)
+    rt = np.concatenate(rts)
+    fn = qmcgen.make_functor(cfg.seed, cfg.L, cfg.m)
+    out = q.eval(R, dev(k), dev(rt), fn, cfg.N, cfg.n_up).cpu().numpy()
+    for j, inst in enumerate(insts):
+        seed = cfg.seed + inst
+        for wl in (0, 511, 1023):
+            Rs = oracle.gen_positions(seed, wl, 1, cfg.N, cfg.Np, cfg.L, np.float32)
+            g = j * W + wl
+            orc, absout, _ = oracle.eval_j2(Rs, k[g:g + 1], rt[g:g + 1], fn, cfg.N, cfg.n_up)
+            assert oracle.normalized_error(out[g:g + 1], orc, absout, fn).max() <= TOL[np.float32]
