@@ -360,7 +360,7 @@ def test_warp_mapping_parity(q, dtype, N):
 def test_warp_mapping_row_and_multi_trial(q):
     _warp_case(q, 3001, 4096, seed=77, dtype=np.float32, row=True)
     _warp_case(q, 2500, 4096, seed=78, dtype=np.float32, P=2)
-    _warp_case(q, 2500, 2048, seed=79, dtype=np.float64, P=3)
+    _warp_case(q, 2500, 2048, seed=79, dtype=np.float64, P=3, sample=(0, 1, 97, 2047))
 
 
 def test_C4_batched_waves_as_benched(q):
