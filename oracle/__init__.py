@@ -61,6 +61,10 @@ def lib():
         _lib.orc_gen_positions.restype = None
         _lib.orc_gen_positions.argtypes = [ctypes.c_uint64, i64, i64, i64, i64, ctypes.c_double,
                                            ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
+        _lib.orc_eval_j1.restype = i64
+        _lib.orc_eval_j1.argtypes = [dp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), dp,
+                                     ctypes.POINTER(ctypes.c_int), dp, ctypes.c_int,
+                                     i64, i64, i64, dp, ctypes.c_int32, dp, dp, dp]
         _lib.orc_j2_total.restype = ctypes.c_double
         _lib.orc_j2_total.argtypes = [dp, ctypes.c_double, ctypes.c_int, dp,
                                       i64, i64, i64, dp]
@@ -119,6 +123,37 @@ def eval_j2(R, k, r_trial, fn, n_total: int, n_up: int, i_offset: int = 0,
     if st:
         raise CoincidentError(f"coincident source at (w*P+p) = {st - 1}")
     return out, absout, rowout
+
+
+def eval_j1(ions, species_start, r_trial, fn1):
+    """Oracle of qj2_eval_j1 (NEXT-1).  ions: [3][Np] sorted by species,
+    species_start: [S+1], r_trial [W][P][3], fn1: qmcgen.J1Functor-like
+    (L, r_cut[S], m[S], coef[S][max_m+3]).  Returns (out, abs) [W][P][5]."""
+    ions = _f64(ions)
+    rt = _f64(r_trial)
+    W, P = rt.shape[0], rt.shape[1]
+    S = len(fn1.m)
+    st = np.ascontiguousarray(np.asarray(species_start, dtype=np.int64))
+    rc = _f64(fn1.r_cut)
+    mm = np.ascontiguousarray(np.asarray(fn1.m, dtype=np.int32))
+    coef = _f64(fn1.coef)
+    out = np.zeros((W, P, 5))
+    absout = np.zeros((W, P, 5))
+    r = lib().orc_eval_j1(_dp(_f64(fn1.L)), S, st.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _dp(rc),
+                          mm.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), _dp(coef), coef.shape[1],
+                          W, int(st[-1]), ions.shape[1], _dp(ions), P, _dp(rt), _dp(out), _dp(absout))
+    if r:
+        raise CoincidentError(f"ion coincides with trial (w*P+p) = {r - 1}")
+    return out, absout
+
+
+def normalized_error_j1(gpu, orc, absout, fn1) -> np.ndarray:
+    """Parity metric for J1: as normalized_error with the functor scale taken
+    over all species (max|c|, max|c|/delta_s, max|c|/delta_s^2)."""
+    cmax = float(np.max(np.abs(fn1.coef)))
+    dmin = min(rc / m for rc, m in zip(fn1.r_cut, fn1.m))
+    F = np.array([cmax, cmax / dmin, cmax / dmin, cmax / dmin, cmax / dmin ** 2])
+    return np.abs(np.asarray(gpu, dtype=np.float64) - orc) / np.maximum(absout, F)
 
 
 def gen_positions(seed: int, walkers_begin: int, n_walkers: int, N: int, Np: int, L: float,

@@ -368,3 +368,60 @@ void orc_gen_positions(uint64_t seed, int64_t wbase, int64_t n_walkers, int64_t 
     for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
     free(jobs); free(th);
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-1: one-body Jastrow over the electron-ion (AB) row.                   */
+/* "Delta J1 = U^1_k(R') - U^1_k(R), U^1_k = sum_I^{N_ion}   */
+/* U_I(|r_I - r_k|)"; Eq. (3) first term; ions fixed and      */
+/* shared by all walkers; per-species functors U_I          */
+/* (Fig. 3 caption).  Ions are given sorted by   */
+/* species: species s owns ions [sp_start[s], sp_start[s+1]).  Species s has  */
+/* its own cutoff r_cut[s], m[s] intervals and m[s]+3 coefficients at         */
+/* coef + s*coef_stride.  For each walker w and trial p, r = r_trial[w][p]:   */
+/*   V = sum_I U_s(I)(|d_I|), G = -sum U' d/|d|, L = sum U'' + 2U'/|d|,       */
+/*   d_I = minimg(r_I - r)  (no self term: electrons and ions differ).        */
+/* Returns 0 or 1 + (w*P+p) if an ion coincides with the trial position      */
+/* inside its cutoff (undefined, refused).                                   */
+/* ------------------------------------------------------------------------ */
+int64_t orc_eval_j1(const double L[3], int n_species, const int64_t *sp_start,
+                    const double *r_cut, const int *m, const double *coef, int coef_stride,
+                    int64_t W, int64_t n_ions, int64_t Np, const double *ions /* [3][Np] */,
+                    int32_t P, const double *r_trial, double *out, double *abs_out)
+{
+    (void)n_ions;
+    for (int64_t w = 0; w < W; ++w)
+        for (int32_t p = 0; p < P; ++p) {
+            const double *rt = r_trial + (w * P + p) * 3;
+            nsum V = {0, 0}, G[3] = {{0, 0}, {0, 0}, {0, 0}}, Lp = {0, 0};
+            nsum AV = {0, 0}, AG[3] = {{0, 0}, {0, 0}, {0, 0}}, AL = {0, 0};
+            for (int s = 0; s < n_species; ++s)
+                for (int64_t I = sp_start[s]; I < sp_start[s + 1]; ++I) {
+                    double src[3] = { ions[I], ions[Np + I], ions[2 * Np + I] };
+                    double d[3], rho, u[3];
+                    orc_min_image(L, rt, src, d, &rho);
+                    if (!(rho < r_cut[s])) continue;
+                    if (rho == 0.0) return 1 + w * P + p;
+                    orc_bspline(coef + s * coef_stride, m[s], r_cut[s], rho, u);
+                    nsum_add(&V, u[0]);
+                    nsum_add(&AV, fabs(u[0]));
+                    for (int c = 0; c < 3; ++c) {
+                        double g = u[1] * d[c] / rho;
+                        nsum_add(&G[c], -g);
+                        nsum_add(&AG[c], fabs(g));
+                    }
+                    nsum_add(&Lp, u[2] + 2.0 * u[1] / rho);
+                    nsum_add(&AL, fabs(u[2]) + 2.0 * fabs(u[1]) / rho);
+                }
+            double *o = out + (w * P + p) * 5;
+            o[0] = nsum_get(&V);
+            o[1] = nsum_get(&G[0]); o[2] = nsum_get(&G[1]); o[3] = nsum_get(&G[2]);
+            o[4] = nsum_get(&Lp);
+            if (abs_out) {
+                double *a = abs_out + (w * P + p) * 5;
+                a[0] = nsum_get(&AV);
+                a[1] = nsum_get(&AG[0]); a[2] = nsum_get(&AG[1]); a[3] = nsum_get(&AG[2]);
+                a[4] = nsum_get(&AL);
+            }
+        }
+    return 0;
+}

@@ -171,6 +171,42 @@ def make_trials(seed: int, walkers, k: np.ndarray, N: int, L: float, dtype,
 
 
 # ---------------------------------------------------------------------------
+# NEXT-1 inputs: ions and per-species one-body functors.
+# Table 1: N / N_ion = 12 for NiO (2 species, Ni and O, 1:1),
+# 4 for graphite (1 species).  Ions are a fixed set shared by all walkers
+# (PAPER:1306-1308), drawn from the same hash with a walker id no walker uses.
+# ---------------------------------------------------------------------------
+ION_WALKER_ID = (1 << 31) - 1
+
+
+@dataclasses.dataclass(frozen=True)
+class J1Functor:
+    """Per-species one-body functors: r_cut[s], m[s], coef[s][max_m+3] (tail 0)."""
+    L: tuple
+    r_cut: tuple
+    m: tuple
+    coef: np.ndarray
+
+
+def make_j1_functor(seed: int, L: float, n_species: int = 2, m=(8, 10), rcut_frac=(0.5, 0.4)) -> J1Functor:
+    rng = np.random.default_rng([int(seed), 4])
+    ms = tuple(int(m[s % len(m)]) for s in range(n_species))
+    rcs = tuple(float(L) * float(rcut_frac[s % len(rcut_frac)]) for s in range(n_species))
+    coef = np.zeros((n_species, max(ms) + 3))
+    for s in range(n_species):
+        coef[s, :ms[s]] = rng.random(ms[s])
+    return J1Functor(L=(float(L),) * 3, r_cut=rcs, m=ms, coef=coef)
+
+
+def make_ions(seed: int, n_ions: int, Np: int, L: float, dtype, n_species: int = 2):
+    """ions [3][Np] (dtype, padding 0) sorted by species, and species_start [S+1]
+    (species as equal as possible, NiO-like 1:1 for S = 2)."""
+    R = positions(seed, [ION_WALKER_ID], n_ions, Np, L, dtype)[0]
+    start = np.array([n_ions * s // n_species for s in range(n_species + 1)], dtype=np.int64)
+    return R, start
+
+
+# ---------------------------------------------------------------------------
 # Configurations (BASELINE.json configs; concrete instances SURVEY.md 8(d)).
 # ---------------------------------------------------------------------------
 @dataclasses.dataclass(frozen=True)

@@ -68,3 +68,13 @@ def test_oracle_side_generator_matches_qmcgen():
         a = oracle.gen_positions(9, 40, 5, N, Np, L, dtype, threads=3)
         b = qmcgen.positions(9, np.arange(40, 45), N, Np, L, dtype)
         assert a.dtype == b.dtype and np.array_equal(a, b)
+
+
+def test_j1_inputs():
+    L = qmcgen.cell_length(614400)
+    ions, start = qmcgen.make_ions(2, 51200, 51200, L, np.float32)
+    assert ions.shape == (3, 51200) and list(start) == [0, 25600, 51200]
+    assert np.all(ions >= 0) and np.all(ions < np.float32(L))
+    fn1 = qmcgen.make_j1_functor(2, L)
+    assert fn1.m == (8, 10) and fn1.r_cut[0] == L / 2 and fn1.r_cut[1] < L / 2
+    assert np.all(fn1.coef[0, 8:] == 0) and np.all(fn1.coef[1, 10:] == 0)

@@ -412,3 +412,86 @@ def test_min_image_tie_range_is_half_open():
     L = [10.0, 10.0, 10.0]
     out = oracle.min_image(L, [[5.0, 0.0, 0.0], [0.0, 0.0, 0.0]], [[0.0, 0.0, 0.0], [5.0, 0.0, 0.0]])
     assert out[0, 1] == 5.0 and out[1, 1] == 5.0
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1: one-body Jastrow over the AB row
+# ---------------------------------------------------------------------------
+def _j1_instance(n_ions, W, seed, P=1, mode="move", N=40):
+    L = qmcgen.cell_length(max(N, 12 * n_ions))
+    fn1 = qmcgen.make_j1_functor(seed, L)
+    ions, start = qmcgen.make_ions(seed, n_ions, qmcgen.padded_size(n_ions, 16), L, np.float64)
+    R = qmcgen.positions(seed, np.arange(W), N, qmcgen.padded_size(N, 16), L, np.float64)
+    k = qmcgen.make_k(seed, W, N)
+    rt = qmcgen.make_trials(seed, np.arange(W), k, N, L, np.float64, P=P, mode=mode)
+    return L, fn1, ions, start, R, k, rt
+
+
+def _ref_j1_point(fn1, ions, start, r):
+    """sum_I U_s(|r_I - r|) with scipy B-splines and 27-image distances."""
+    tot = 0.0
+    for s in range(len(fn1.m)):
+        idx = np.arange(start[s], start[s + 1])
+        if idx.size == 0:
+            continue
+        rr, _ = ref_minimg_27(fn1.L, np.repeat(np.asarray(r, float)[None], idx.size, 0), ions[:, idx].T)
+        tot += ref_functor(fn1.coef[s, :fn1.m[s] + 3], fn1.m[s], fn1.r_cut[s], rr).sum()
+    return tot
+
+
+def test_j1_single_ion_is_the_functor():
+    L, fn1, _, _, _, _, _ = _j1_instance(4, 1, seed=3)
+    rng = np.random.default_rng(0)
+    for s in range(2):
+        ion = np.zeros((3, 16))
+        ion[:, 0] = [L / 2, L / 2, L / 2]
+        start = np.array([0, 1, 1]) if s == 0 else np.array([0, 0, 1])
+        for _ in range(20):
+            r = ion[:, 0] + (rng.random(3) - 0.5) * fn1.r_cut[s]
+            out, _ = oracle.eval_j1(ion, start, r.reshape(1, 1, 3), fn1)
+            d = ion[:, 0] - r
+            rho = np.linalg.norm(d)
+            c = fn1.coef[s, :fn1.m[s] + 3]
+            u = [ref_functor(c, fn1.m[s], fn1.r_cut[s], rho, nu) for nu in range(3)]
+            exp = [u[0], *(-u[1] * d / rho), u[2] + 2 * u[1] / rho]
+            np.testing.assert_allclose(out[0, 0], exp, rtol=1e-11, atol=1e-12)
+            # G points along +-(r - r_I) (radial symmetry, SPEC:422)
+            assert np.linalg.norm(np.cross(out[0, 0, 1:4], r - ion[:, 0])) <= 1e-9 * max(1, np.abs(out[0, 0, 1:4]).max())
+
+
+def test_j1_per_species_cutoff():
+    L, fn1, _, _, _, _, _ = _j1_instance(4, 1, seed=3)
+    assert fn1.r_cut[1] < fn1.r_cut[0]
+    ion = np.zeros((3, 16))
+    ion[:, 0] = [L / 2] * 3
+    r = ion[:, 0] + np.array([0.5 * (fn1.r_cut[0] + fn1.r_cut[1]), 0, 0])   # inside U_0, beyond U_1
+    out0, _ = oracle.eval_j1(ion, np.array([0, 1, 1]), r.reshape(1, 1, 3), fn1)
+    out1, _ = oracle.eval_j1(ion, np.array([0, 0, 1]), r.reshape(1, 1, 3), fn1)
+    assert out0[0, 0, 0] != 0.0 and np.all(out1 == 0.0)
+
+
+@pytest.mark.parametrize("n_ions", [1, 5, 32])
+def test_delta_j1_equals_brute_force(n_ions):
+    """Delta J1 = J1(R') - J1(R) with J1 = sum_i sum_I U_I(|r_I - r_i|)
+    (Eq. 3 first term) equals U^1_k(R') - U^1_k(R)."""
+    N, W = 30, 4
+    L, fn1, ions, start, R, k, rt = _j1_instance(n_ions, W, seed=10 + n_ions, P=2, mode="drift", N=N)
+    out, _ = oracle.eval_j1(ions, start, rt, fn1)
+    for w in range(W):
+        J = lambda Rw: sum(_ref_j1_point(fn1, ions, start, Rw[:, i]) for i in range(N))  # noqa: E731
+        Rp = R[w].copy()
+        Rp[:, k[w]] = rt[w, 1]
+        dj = J(Rp) - J(R[w])
+        assert abs((out[w, 1, 0] - out[w, 0, 0]) - dj) <= 1e-12 * max(1.0, abs(J(R[w])))
+
+
+def test_j1_gradient_laplacian_fd():
+    L, fn1, ions, start, _, _, rt = _j1_instance(24, 4, seed=21, N=288)
+    out, absout = oracle.eval_j1(ions, start, rt, fn1)
+    h1, h2 = 1e-5 * L, 1e-4 * L
+    for w in range(4):
+        V = lambda sh: oracle.eval_j1(ions, start, (rt[w, 0] + sh).reshape(1, 1, 3), fn1)[0][0, 0, 0]  # noqa: E731
+        g = np.array([(V(h1 * e) - V(-h1 * e)) / (2 * h1) for e in np.eye(3)])
+        lap = sum((V(h2 * e) - 2 * V(0 * e) + V(-h2 * e)) / h2 ** 2 for e in np.eye(3))
+        assert np.max(np.abs(g - out[w, 0, 1:4])) <= 1e-6 * max(absout[w, 0, 1:4].max(), 1)
+        assert abs(lap - out[w, 0, 4]) <= 1e-5 * max(absout[w, 0, 4], 1)
