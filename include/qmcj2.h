@@ -46,7 +46,7 @@ typedef enum {
 
 typedef enum { QJ2_FP32 = 0, QJ2_FP64 = 1 } qj2_dtype;
 
-enum { QJ2_MAX_M = 64, QJ2_MAX_P = 64 };
+enum { QJ2_MAX_M = 64, QJ2_MAX_P = 64, QJ2_MAX_SPECIES = 4 };
 
 /*
  * Two-body Jastrow functor U_s(r) and the simulation cell.
@@ -158,6 +158,39 @@ qj2_status qj2_eval(const qj2_functor *fn, qj2_dtype dtype,
                     const double *V_cur, double *ratio_out,
                     void *workspace, size_t workspace_bytes,
                     void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-1: one-body Jastrow over the electron-ion (AB) row.                  */
+/* PAPER:1376-1381 ("Delta J1 = U^1_k(R') - U^1_k(R), U^1_k = sum_I U_I(     */
+/* |r_I - r_k|)"), Eq. (3) first term; per-species functors  */
+/* (Fig. 3); ions fixed and shared by every walker            */
+/* (PAPER:1306-1308).  Species s: cutoff r_cut[s], m[s] intervals, m[s]+3    */
+/* uniform cubic B-spline coefficients (same convention as qj2_functor; tail */
+/* coef[s][m[s]..m[s]+2] must be 0).                                         */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    double  L[3];                                   /* cell */
+    int32_t n_species;                              /* 1 <= n_species <= QJ2_MAX_SPECIES */
+    int32_t reserved;                               /* must be 0 */
+    double  r_cut[QJ2_MAX_SPECIES];                 /* 0 < r_cut[s] <= min(L)/2 */
+    int32_t m[QJ2_MAX_SPECIES];                     /* 4 <= m[s] <= QJ2_MAX_M */
+    double  coef[QJ2_MAX_SPECIES][QJ2_MAX_M + 3];
+} qj2_j1_functor;
+
+/* For every walker w and trial p (r = r_trial[w][p]), over all ions I:        */
+/*   V = sum_I U_{s(I)}(|d_I|), G = -sum U' d/|d|, L = sum U'' + 2U'/|d|,      */
+/*   d_I = minimg(r_I - r); no self term.  Same output layout, precision,      */
+/*   row output ([W][P][4][Np]: the AB row), fused ratio and workspace rules   */
+/*   as qj2_eval (workspace size: qj2_eval_workspace_size(W, P, n_ions, dtype)).*/
+/*   species_start: host [n_species+1], species_start[0] = 0, nondecreasing;   */
+/*   ions are sorted by species: species s owns [species_start[s], [s+1]).     */
+/*   ions: device [3][Np] dtype (SoA x|y|z, the ions' Rsoa), coordinates in    */
+/*   [0, L_d), padding 0, 16-byte aligned; Np >= n_ions, Np % 4 (fp32) / 2.    */
+qj2_status qj2_eval_j1(const qj2_j1_functor *fn, qj2_dtype dtype, int64_t W,
+                       const int64_t *species_start, int64_t Np, const void *ions,
+                       int32_t P, const void *r_trial, double *out, void *row_out,
+                       const double *V_cur, double *ratio_out,
+                       void *workspace, size_t workspace_bytes, void *stream);
 
 /* ------------------------------------------------------------------------ */
 /* qj2_ratio: ratio_out[w][p] = (dJ2, exp(dJ2)), dJ2 = out[w][p][0] - ref,   */

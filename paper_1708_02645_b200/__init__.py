@@ -8,6 +8,7 @@ library raises, and every call goes to the GPU library.
 
 Public API (names follow include/qmcj2.h):
     eval(R, k, r_trial, fn, n_total, n_up, ...)   -> out [W][P][5] fp64 (and row, ratio)
+    eval_j1(ions, species_start, r_trial, fn1)    -> NEXT-1: J1 over the AB row
     eval_host(R, k, r_trial, fn, ...)             -> host-buffer end-to-end path
     ratio(out, V_cur=None)                        -> [W][P][2] (dJ2, exp(dJ2))
     functor_eval_vgl(fn, channel, r)              -> [n][3] (U, U', U'')
@@ -24,13 +25,14 @@ import torch
 
 from . import _build
 
-__all__ = ["QJ2Error", "Functor", "Workspace", "eval", "eval_host", "ratio", "functor_eval_vgl",
+__all__ = ["QJ2Error", "Functor", "J1Functor", "Workspace", "eval", "eval_j1", "eval_host", "ratio", "functor_eval_vgl",
            "min_image_disp", "check_inputs", "padded_size", "gen_positions", "lib_path",
            "workspace_size", "host_workspace_size", "version", "device_check"]
 
 QJ2_FP32, QJ2_FP64 = 0, 1
 QJ2_MAX_M = 64
 QJ2_MAX_P = 64
+QJ2_MAX_SPECIES = 4
 
 
 class QJ2Error(RuntimeError):
@@ -45,6 +47,15 @@ class _Functor(ctypes.Structure):
                 ("m", ctypes.c_int32),
                 ("reserved", ctypes.c_int32),
                 ("coef", (ctypes.c_double * (QJ2_MAX_M + 3)) * 2)]
+
+
+class _J1Functor(ctypes.Structure):
+    _fields_ = [("L", ctypes.c_double * 3),
+                ("n_species", ctypes.c_int32),
+                ("reserved", ctypes.c_int32),
+                ("r_cut", ctypes.c_double * QJ2_MAX_SPECIES),
+                ("m", ctypes.c_int32 * QJ2_MAX_SPECIES),
+                ("coef", (ctypes.c_double * (QJ2_MAX_M + 3)) * QJ2_MAX_SPECIES)]
 
 
 def lib_path() -> str:
@@ -69,6 +80,8 @@ def _load():
         "qj2_eval": (ctypes.c_int, [F, ctypes.c_int, i64, i64, i64, i64, i64, i64, vp, vp, i32, vp,
                                     vp, vp, vp, vp, vp, sz, vp]),
         "qj2_ratio": (ctypes.c_int, [i64, i32, vp, vp, vp, vp]),
+        "qj2_eval_j1": (ctypes.c_int, [ctypes.POINTER(_J1Functor), ctypes.c_int, i64, ctypes.POINTER(i64), i64,
+                                       vp, i32, vp, vp, vp, vp, vp, vp, sz, vp]),
         "qj2_eval_host_workspace_size": (ctypes.c_int, [i64, i32, i64, ctypes.c_int, i64, ctypes.POINTER(sz)]),
         "qj2_eval_host": (ctypes.c_int, [F, ctypes.c_int, i64, i64, i64, i64, i64, i64, vp, vp, i32, vp,
                                          vp, vp, vp, i64, vp, sz, vp]),
@@ -87,7 +100,7 @@ def _load():
 
 _lib = _load()
 EXPORTS = ("qj2_version", "qj2_status_string", "qj2_last_error", "qj2_device_check", "qj2_padded_size",
-           "qj2_eval_workspace_size", "qj2_eval", "qj2_ratio", "qj2_eval_host_workspace_size",
+           "qj2_eval_workspace_size", "qj2_eval", "qj2_ratio", "qj2_eval_j1", "qj2_eval_host_workspace_size",
            "qj2_eval_host", "qj2_functor_eval_vgl", "qj2_min_image_disp", "qj2_check_inputs",
            "qj2gen_positions")
 
@@ -232,6 +245,73 @@ def eval(R, k, r_trial, fn, n_total: int, n_up: int, *, i_offset: int = 0, n_loc
                        _ptr(row_out) if row else None, _ptr(V_cur), _ptr(ratio_out) if ratio else None,
                        _ptr(ws.buf), ws.nbytes, ctypes.c_void_p(_stream_ptr(stream)))
     _check(st, "qj2_eval")
+    res = [out]
+    if row:
+        res.append(row_out)
+    if ratio:
+        res.append(ratio_out)
+    return res[0] if len(res) == 1 else tuple(res)
+
+
+class J1Functor:
+    """Per-species one-body functors in the C layout (qj2_j1_functor)."""
+
+    def __init__(self, L, r_cut, m, coef):
+        r_cut = [float(x) for x in r_cut]
+        m = [int(x) for x in m]
+        coef = np.asarray(coef, dtype=np.float64)
+        S = len(m)
+        if not (1 <= S <= QJ2_MAX_SPECIES) or len(r_cut) != S or coef.shape[0] != S:
+            raise ValueError("need 1..4 species with matching r_cut, m, coef")
+        self.L = tuple(float(x) for x in (L if np.ndim(L) else (L, L, L)))
+        self.r_cut, self.m, self.coef = tuple(r_cut), tuple(m), coef
+        c = _J1Functor()
+        for d in range(3):
+            c.L[d] = self.L[d]
+        c.n_species, c.reserved = S, 0
+        for s in range(S):
+            c.r_cut[s] = r_cut[s]
+            c.m[s] = m[s]
+            for j in range(min(coef.shape[1], QJ2_MAX_M + 3)):
+                c.coef[s][j] = float(coef[s, j])
+        self._c = c
+
+    @classmethod
+    def of(cls, fn) -> "J1Functor":
+        return fn if isinstance(fn, J1Functor) else cls(fn.L, fn.r_cut, fn.m, fn.coef)
+
+    @property
+    def ptr(self):
+        return ctypes.byref(self._c)
+
+
+def eval_j1(ions, species_start, r_trial, fn1, *, row: bool = False, V_cur=None, ratio: bool = False,
+            out=None, row_out=None, ratio_out=None, workspace: Workspace | None = None, stream=None):
+    """qj2_eval_j1 (NEXT-1): one-body Jastrow over the AB row.
+
+    ions [3][Np] (f32/f64, sorted by species), species_start [S+1] (host ints),
+    r_trial [W][P][3] (same dtype).  Returns out [W][P][5] fp64 (and row
+    [W][P][4][Np], ratio [W][P][2])."""
+    _req(ions, "ions", ndim=2)
+    _req(r_trial, "r_trial", ions.dtype, 3)
+    W, P = r_trial.shape[0], r_trial.shape[1]
+    Np = ions.shape[1]
+    f = J1Functor.of(fn1)
+    st = (ctypes.c_int64 * (len(f.m) + 1))(*[int(x) for x in species_start])
+    n_ions = int(species_start[-1])
+    dev = ions.device
+    if out is None:
+        out = torch.empty((W, P, 5), dtype=torch.float64, device=dev)
+    if row and row_out is None:
+        row_out = torch.empty((W, P, 4, Np), dtype=ions.dtype, device=dev)
+    if ratio and ratio_out is None:
+        ratio_out = torch.empty((W, P, 2), dtype=torch.float64, device=dev)
+    need = workspace_size(W, P, max(n_ions, 1), ions.dtype) if W > 0 else 0
+    ws = workspace if workspace is not None else Workspace(device=dev)
+    ws.reserve(need)
+    _check(_lib.qj2_eval_j1(f.ptr, _dtype_code(ions.dtype), W, st, Np, _ptr(ions), P, _ptr(r_trial), _ptr(out),
+                            _ptr(row_out) if row else None, _ptr(V_cur), _ptr(ratio_out) if ratio else None,
+                            _ptr(ws.buf), ws.nbytes, ctypes.c_void_p(_stream_ptr(stream))), "qj2_eval_j1")
     res = [out]
     if row:
         res.append(row_out)

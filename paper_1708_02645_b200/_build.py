@@ -1,7 +1,11 @@
 """Build libqmcj2.so in-tree with nvcc for sm_100a (no JIT cache, no torch
-extension machinery: the library is plain CUDA C++ with a C ABI)."""
+extension machinery: the library is plain CUDA C++ with a C ABI).
+
+Translation units are compiled to objects in parallel (the kernel
+instantiations are split by dtype / trial-batch size), then linked."""
 from __future__ import annotations
 
+import concurrent.futures as cf
 import os
 import subprocess
 
@@ -9,38 +13,61 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libqmcj2.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("qmcj2.cu", "gen.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "j2_device.cuh"), os.path.join(ROOT, "include", "qmcj2.h")]
+OBJDIR = os.path.join(PKG, "build_obj")
+SOURCES = [os.path.join(CSRC, f) for f in ("qmcj2.cu", "gen.cu", "launch_f32_pb1.cu", "launch_f32_pbn.cu",
+                                           "launch_f64_pb1.cu", "launch_f64_pbn.cu")]
+HEADERS = [os.path.join(CSRC, f) for f in ("j2_device.cuh", "j2_kernels.cuh", "j2_tma.cuh", "launch.cuh")] + \
+          [os.path.join(ROOT, "include", "qmcj2.h")]
 
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
-    "-I", os.path.join(ROOT, "include"),
-]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
 
 
 def nvcc() -> str:
-    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
-        if cand and (os.path.isabs(cand) and os.path.exists(cand) or not os.path.isabs(cand)):
-            return cand
-    return "nvcc"
+    cand = os.environ.get("NVCC")
+    if cand:
+        return cand
+    return "/usr/local/cuda/bin/nvcc" if os.path.exists("/usr/local/cuda/bin/nvcc") else "nvcc"
 
 
 def up_to_date() -> bool:
     if not os.path.exists(LIB):
         return False
     t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(d) <= t for d in DEPS)
+    return all(os.path.getmtime(d) <= t for d in SOURCES + HEADERS)
+
+
+def _obj(src: str) -> str:
+    return os.path.join(OBJDIR, os.path.basename(src).replace(".cu", ".o"))
+
+
+def _compile(src: str, verbose: bool) -> str:
+    obj = _obj(src)
+    hdr_t = max(os.path.getmtime(h) for h in HEADERS)
+    if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_t):
+        return obj
+    cmd = [nvcc(), *NVCC_FLAGS, "-c", "-o", obj + f".tmp{os.getpid()}", src]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.check_call(cmd)
+    os.replace(obj + f".tmp{os.getpid()}", obj)
+    return obj
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
+    os.makedirs(OBJDIR, exist_ok=True)
+    if force:
+        for s in SOURCES:
+            if os.path.exists(_obj(s)):
+                os.remove(_obj(s))
+    with cf.ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, *SOURCES]
+    cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs]
     if verbose:
-        print(" ".join(cmd))
+        print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
     return LIB

@@ -1,0 +1,539 @@
+// j2_kernels.cuh -- the hot-path kernels (included by qmcj2.cu).
+//
+// One kernel core serves two rows of SURVEY.md section 8:
+//   * J2 (section 8(a), the hot path): sources = the walker's own electrons,
+//     self-exclusion i != k, two source groups (spin halves);
+//     a group's functor is the same-spin or opposite-spin channel relative to
+//     k's spin.
+//   * J1 (NEXT-1): sources = the ions, shared by all walkers (walker stride 0,
+//     PAPER:1306-1308), no self term, one source group per species, each with
+//     its own functor, cutoff and interval count.
+// Sources are contiguous groups [grp_start[g], grp_start[g+1]); a sub-tile
+// inside one group is "clean" and runs with uniform functor constants.
+//
+// Accumulation: per sub-tile each thread sums <= 32 terms in T (raw Horner
+// outputs), then flushes to fp64 with the sub-tile's group scale factors, so
+// the fp64 accumulators hold physical (V, Gx, Gy, Gz, L)
+// ("quantities per walker ... in double precision").
+#pragma once
+
+namespace qj2 {
+
+constexpr int TPB = 256;          // threads per CTA
+constexpr int ITERS = 8;          // vector iterations per sub-tile: 32 fp32 terms per thread per trial
+constexpr int SUB = 4;            // sub-tiles per CTA tile
+constexpr int NACC = 6;           // fp32 accumulators per trial: V, Gx, Gy, Gz, sum h, sum du/r
+constexpr int NOUT = 5;           // fp64 physical outputs per trial: V, Gx, Gy, Gz, L
+constexpr int MAXPB = 4;
+constexpr int MAXG = 4;           // source groups (J2: 2 spin halves; J1: up to 4 species)
+constexpr int MAXTAB = MAXG * (QJ2_MAX_M + 1);
+
+enum { MODE_J2 = 0, MODE_J1 = 1 };
+
+// ---------------------------------------------------------------------------
+// Kernel parameters (by value, __grid_constant__).
+// ---------------------------------------------------------------------------
+struct EvalParams {
+    int64_t W, N_total, N_up, i_offset, N_local, Np;
+    int64_t tiles_per_walker;     // ceil(N_local / CH)
+    int64_t n_groups;             // trial groups: ceil(P / PB)
+    int32_t P, m;                 // m: J2 interval count
+    int32_t mode;                 // MODE_J2 | MODE_J1
+    int32_t n_src_groups;         // J2: 2; J1: species
+    int32_t n_tab;                // table rows to stage in shared memory
+    int64_t src_stride;           // elements between walkers' source blocks (J2 3*Np, J1 0)
+    int64_t grp_start[MAXG + 1];  // global source index boundaries of the groups
+    int32_t grp_tab[MAXG];        // J1: first table row of species g
+    int32_t grp_m[MAXG];          // J1: interval count of species g
+    double grp_invd[MAXG];        // J1: 1/delta of species g
+    const void *R;
+    const int32_t *k;             // J2 only
+    const void *r_trial;
+    double *out;
+    void *row_out;
+    const double *V_cur;
+    double *ratio_out;
+    double *partials;             // [W][n_groups][tiles][PB][NOUT]
+    unsigned int *counters;       // [W][n_groups]
+    double L[3];
+    double inv_delta;             // J2: 1/delta
+    double pcoef[MAXTAB][4];      // power basis per interval (J2: [0,m] same spin, [m+1,2m+1] opposite)
+};
+
+// ---------------------------------------------------------------------------
+// Helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ void load_table(const EvalParams &p, Coef4<T> *tab) {
+    for (int e = threadIdx.x; e < p.n_tab; e += blockDim.x) {
+        Coef4<T> c;
+        c.a0 = T(p.pcoef[e][0]);
+        c.a1 = T(p.pcoef[e][1]);
+        c.a2 = T(p.pcoef[e][2]);
+        c.a3 = T(p.pcoef[e][3]);
+        tab[e] = c;
+    }
+}
+
+// Functor constants of one source group for the current walker.
+template <typename T>
+struct GroupC {
+    uint32_t base;                    // shared address of row 0, minus MAGIC_BITS * sizeof(Coef4)
+    T invd;                           // 1/delta
+    typename Traits<T>::U clamp;      // MAGIC_BITS + m (the zero row)
+    double sg, sh, ss;                // fp64 flush scales: G = sg*acc, L = sh*acc_h + ss*acc_s
+};
+
+__device__ __forceinline__ int src_group(const EvalParams &p, int64_t gi) {
+    int g = 0;
+    for (int b = 1; b < p.n_src_groups; ++b) g += (gi >= p.grp_start[b]) ? 1 : 0;
+    return g;
+}
+
+// kg: group (spin half) of the walker's active electron (J2).
+template <typename T>
+__device__ __forceinline__ GroupC<T> group_consts(const EvalParams &p, int g, int kg, uint32_t tab_addr) {
+    using Tr = Traits<T>;
+    const uint32_t magic_off = (uint32_t)(Tr::MAGIC_BITS * (typename Tr::U)sizeof(Coef4<T>));
+    GroupC<T> c;
+    int row, m;
+    double invd;
+    if (p.mode == MODE_J2) {
+        row = (g == kg) ? 0 : (p.m + 1);
+        m = p.m;
+        invd = p.inv_delta;
+    } else {
+        row = p.grp_tab[g];
+        m = p.grp_m[g];
+        invd = p.grp_invd[g];
+    }
+    c.base = tab_addr + (uint32_t)(row * (int)sizeof(Coef4<T>)) - magic_off;
+    c.invd = T(invd);
+    c.clamp = Tr::MAGIC_BITS + (typename Tr::U)m;
+    c.sg = -invd;
+    c.sh = 2.0 * invd * invd;
+    c.ss = 2.0 * invd;
+    return c;
+}
+
+// Per-trial constants: the three axes' minimum-image constants.
+template <typename T> struct Trial { Axis<T> ax, ay, az; };
+
+// Functor + accumulation for one source at squared distance r2 (and
+// displacement d).  acc: V, Gx, Gy, Gz (sum du/r * d), H (sum h), S (sum du/r)
+// in raw units (scaled at the flush), or, with PHYS, already scaled by this
+// source's 1/delta (per-source groups in a masked J1 sub-tile).
+template <typename T, bool PHYS = false>
+__device__ __forceinline__ T accumulate(T dx, T dy, T dz, T r2, T inv_delta, uint32_t tab_base,
+                                        typename Traits<T>::U clamp_bits, T *acc) {
+    using Tr = Traits<T>;
+    const T ir = Tr::rsqrt(r2);
+    const T r = r2 * ir;
+    const FunctorEval<T> e = functor_from_t<T>(r * inv_delta, tab_base, clamp_bits);
+    T g = e.du * ir;
+    T h = e.h;
+    if (PHYS) {
+        g *= inv_delta;                        // U'/r
+        h *= T(2) * inv_delta * inv_delta;     // U''
+    }
+    acc[0] += e.u;
+    acc[1] = fma(g, dx, acc[1]);
+    acc[2] = fma(g, dy, acc[2]);
+    acc[3] = fma(g, dz, acc[3]);
+    acc[4] += h;
+    acc[5] += g;
+    return r;
+}
+
+// Minimum image for one axis, optionally specialised on the trial
+// coordinate's case (SPEC = 1: case A, c < L/2; 0: case B; -1: unified,
+// see make_axis).  Specialised forms take 3 instructions instead of 4, but the
+// 8 per-walker bodies measured slower on B200 (instruction-cache pressure,
+// DESIGN.md section 7); the kernels use the unified form.
+template <typename T, int SPEC>
+__device__ __forceinline__ T min_image_k(T x, const Axis<T> &a) {
+    if constexpr (SPEC < 0) {
+        return min_image(x, a);
+    } else if constexpr (SPEC == 1) {           // case A: wrap shifts the source (x - L exact)
+        const T xs = x > a.thr ? x - a.a1 : x;
+        return xs - a.b0;
+    } else {                                    // case B: wrap shifts the trial (c - L exact)
+        return x - (x > a.thr ? a.b1 : a.b0);
+    }
+}
+
+// A sub-tile that is not "clean": ragged length, holds the self source k, or
+// straddles a group boundary.  Offsets relative to the sub-tile start.
+struct SubMask {
+    int len;          // valid sources in the sub-tile
+    int k_rel;        // self source, or -1
+    int64_t g0;       // global index of the sub-tile's first source
+};
+
+// One sub-tile.  Every thread walks ITERS vectors at a constant stride of NT
+// vectors, so every load address is base + immediate; PF vector groups are in
+// flight ahead of the one being consumed (software pipelining).
+// GEN = false: full sub-tile, no self source, one group (constants gc).
+// GEN = true: vector indices clamped into the sub-tile (vectors past the end
+// reload the last valid vector; their sources are dead) so loads stay
+// unpredicated; per source, dead sources (self, padding) get r^2 = BIG, which
+// lands on the all-zero interval (every accumulated quantity exactly 0), and
+// the source's group picks the functor.  J2 groups share delta, so only the
+// table row changes (raw accumulation); J1 groups differ in delta, so GEN
+// sub-tiles accumulate physical units (PHYS).
+template <typename T, int PB, bool ROW, int PF, bool GEN, int NT = TPB, bool MULTI = false, bool PHYS = false>
+__device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, uint32_t tab_addr,
+                                         const typename Traits<T>::V *__restrict__ px,
+                                         const typename Traits<T>::V *__restrict__ py,
+                                         const typename Traits<T>::V *__restrict__ pz,
+                                         const Trial<T> (&tr)[PB], int np, const GroupC<T> &gc,
+                                         const SubMask &mk, T (&acc)[PB][NACC],
+                                         typename Traits<T>::V *const (&rowp)[PB], int64_t row_stride) {
+    using Tr = Traits<T>;
+    using V = typename Tr::V;
+    constexpr int VW = Tr::VW;
+    const int vmax = GEN ? (mk.len - 1) / VW : 0;
+    auto voff = [&](int j) -> int {
+        return GEN ? min(j * NT + tid, vmax) - tid : j * NT;   // relative to this thread's vector
+    };
+    V bx[ITERS], by[ITERS], bz[ITERS];      // fully unrolled: only PF+1 groups are live
+#pragma unroll
+    for (int j = 0; j < PF && j < ITERS; ++j) {
+        bx[j] = Tr::ld_stream(px + voff(j));
+        by[j] = Tr::ld_stream(py + voff(j));
+        bz[j] = Tr::ld_stream(pz + voff(j));
+    }
+#pragma unroll
+    for (int it = 0; it < ITERS; ++it) {
+        if (it + PF < ITERS) {
+            bx[it + PF] = Tr::ld_stream(px + voff(it + PF));
+            by[it + PF] = Tr::ld_stream(py + voff(it + PF));
+            bz[it + PF] = Tr::ld_stream(pz + voff(it + PF));
+        }
+        const int rel = (it * NT + tid) * VW;
+        if (!GEN || rel < mk.len) {
+            V ro[PB][4];
+#pragma unroll
+            for (int e = 0; e < VW; ++e) {
+                bool dead = false;
+                uint32_t b = gc.base;
+                T invd = gc.invd;
+                typename Tr::U clamp = gc.clamp;
+                if (GEN) {
+                    const int li = rel + e;
+                    dead = (li >= mk.len) || (li == mk.k_rel);
+                    if (MULTI) {       // sub-tile straddles a group boundary
+                        const GroupC<T> ge = group_consts<T>(p, src_group(p, mk.g0 + li), kg, tab_addr);
+                        b = ge.base;
+                        invd = ge.invd;
+                        clamp = ge.clamp;
+                    }
+                }
+                const T x = Tr::comp(bx[it], e), y = Tr::comp(by[it], e), z = Tr::comp(bz[it], e);
+#pragma unroll
+                for (int q = 0; q < PB; ++q) {
+                    if (PB == 1 || q < np) {
+                        const T dx = min_image_k<T, -1>(x, tr[q].ax);
+                        const T dy = min_image_k<T, -1>(y, tr[q].ay);
+                        const T dz = min_image_k<T, -1>(z, tr[q].az);
+                        T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                        if (GEN) r2 = dead ? T(1e30) : r2;
+                        const T r = accumulate<T, PHYS>(dx, dy, dz, r2, invd, b, clamp, acc[q]);
+                        if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
+                    }
+                }
+            }
+            if (ROW) {
+#pragma unroll
+                for (int q = 0; q < PB; ++q)
+                    if (PB == 1 || q < np)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) __stcs(rowp[q] + c * row_stride + it * NT, ro[q][c]);
+            }
+        }
+    }
+}
+
+// Flush a sub-tile's T partials into the fp64 physical accumulators.
+template <typename T, int PB>
+__device__ __forceinline__ void flush(T (&acc)[PB][NACC], double (&dacc)[PB][NOUT], double sg, double sh, double ss) {
+#pragma unroll
+    for (int q = 0; q < PB; ++q) {
+        dacc[q][0] += (double)acc[q][0];
+        dacc[q][1] += sg * (double)acc[q][1];
+        dacc[q][2] += sg * (double)acc[q][2];
+        dacc[q][3] += sg * (double)acc[q][3];
+        dacc[q][4] += sh * (double)acc[q][4] + ss * (double)acc[q][5];
+    }
+}
+
+// Process the sub-tile [sstart, send) (local indices) of one walker for a team
+// of NT threads: classify, run the clean or the masked loop, flush to fp64.
+template <typename T, int PB, bool ROW, int PF, int NT>
+__device__ __forceinline__ void sub_tile(int tid, const EvalParams &p, int kg, uint32_t tab_addr,
+                                         int64_t sstart, int64_t send, int64_t k_local,
+                                         const typename Traits<T>::V *px, const typename Traits<T>::V *py,
+                                         const typename Traits<T>::V *pz, const Trial<T> (&tr)[PB], int np,
+                                         double (&dacc)[PB][NOUT],
+                                         typename Traits<T>::V *const (&rp)[PB], int64_t row_stride) {
+    constexpr int SCH = NT * Traits<T>::VW * ITERS;
+    T acc[PB][NACC];
+#pragma unroll
+    for (int q = 0; q < PB; ++q)
+#pragma unroll
+        for (int a = 0; a < NACC; ++a) acc[q][a] = T(0);
+    const int64_t g0 = sstart + p.i_offset;                 // global index of the first source
+    const int grp = src_group(p, g0);
+    const bool one_group = src_group(p, send - 1 + p.i_offset) == grp;
+    const bool k_in = k_local >= sstart && k_local < send;
+    SubMask mk;
+    mk.len = (int)(send - sstart);
+    mk.k_rel = k_in ? (int)(k_local - sstart) : -1;
+    mk.g0 = g0;
+    const GroupC<T> gc = group_consts<T>(p, grp, kg, tab_addr);
+    if (mk.len == SCH && !k_in && one_group) {                 // clean
+        tile_run<T, PB, ROW, PF, false, NT>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp, row_stride);
+        flush<T, PB>(acc, dacc, gc.sg, gc.sh, gc.ss);
+    } else if (one_group) {                                    // ragged and/or holds k
+        tile_run<T, PB, ROW, PF, true, NT>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp, row_stride);
+        flush<T, PB>(acc, dacc, gc.sg, gc.sh, gc.ss);
+    } else if (p.mode == MODE_J2) {                            // spin halves share delta
+        tile_run<T, PB, ROW, PF, true, NT, true>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp, row_stride);
+        flush<T, PB>(acc, dacc, gc.sg, gc.sh, gc.ss);
+    } else {                                                   // species differ in delta
+        tile_run<T, PB, ROW, PF, true, NT, true, true>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp,
+                                                       row_stride);
+        flush<T, PB>(acc, dacc, -1.0, 1.0, 2.0);
+    }
+}
+
+// Per-walker setup shared by the CTA and warp kernels.
+template <typename T, int PB>
+__device__ __forceinline__ void walker_setup(const EvalParams &p, int64_t w, int32_t p0, int np,
+                                             Trial<T> (&tr)[PB], int &kg, int64_t &k_local) {
+    const int64_t kw = p.mode == MODE_J2 ? (int64_t)p.k[w] : -1;
+    kg = (p.mode == MODE_J2 && kw >= p.N_up) ? 1 : 0;
+    k_local = p.mode == MODE_J2 ? kw - p.i_offset : -1;
+    const T L0 = T(p.L[0]), L1 = T(p.L[1]), L2 = T(p.L[2]);
+#pragma unroll
+    for (int q = 0; q < PB; ++q) {
+        const int qq = q < np ? q : 0;
+        const T *rt = static_cast<const T *>(p.r_trial) + ((w * p.P + p0 + qq) * 3);
+        tr[q].ax = make_axis<T>(rt[0], L0);
+        tr[q].ay = make_axis<T>(rt[1], L1);
+        tr[q].az = make_axis<T>(rt[2], L2);
+    }
+}
+
+// Write the physical totals (lane 0 holds them) and the fused ratio.
+template <int PB>
+__device__ __forceinline__ void write_out(const EvalParams &p, int64_t w, int32_t p0, int np, int q,
+                                          const double (&s)[NOUT], double V0) {
+    if (q >= np) return;
+    const int64_t o = w * p.P + p0 + q;
+#pragma unroll
+    for (int a = 0; a < NOUT; ++a) p.out[o * 5 + a] = s[a];
+    if (p.ratio_out) {   // e^{dJ} factor of Eq. 4 (host guarantees a valid reference)
+        const double dj = s[0] - (p.V_cur ? p.V_cur[w] : V0);
+        p.ratio_out[o * 2 + 0] = dj;
+        p.ratio_out[o * 2 + 1] = exp(dj);
+    }
+}
+
+// ===========================================================================
+// Long rows: one CTA per (walker, trial group, tile of SUB sub-tiles).
+// PF: prefetch distance (vector groups in flight), MINB: resident CTAs per SM.
+// ===========================================================================
+template <typename T, int PB, bool ROW, int PF = 1, int MINB = ((sizeof(T) == 4 && PB == 1) ? 4 : 2)>
+__global__ void __launch_bounds__(TPB, MINB)
+j2_eval_kernel(const __grid_constant__ EvalParams p) {
+    using Tr = Traits<T>;
+    using V = typename Tr::V;
+    constexpr int VW = Tr::VW;
+    constexpr int SCH = TPB * VW * ITERS;         // sub-tile: 32 terms per thread
+    constexpr int CH = SCH * SUB;                 // tile handled by one CTA
+    __shared__ Coef4<T> tab[MAXTAB];
+    __shared__ double red[TPB / 32][PB * NOUT];
+    __shared__ int last_flag;
+
+    // tile decode: chunk fastest so consecutive CTAs stream consecutive memory
+    // (32-bit arithmetic: the host guarantees W * n_groups * tiles < 2^31)
+    const uint32_t b = blockIdx.x;
+    const uint32_t tpw32 = (uint32_t)p.tiles_per_walker;
+    const uint32_t per_w = tpw32 * (uint32_t)p.n_groups;
+    const uint32_t w32 = b / per_w;
+    const uint32_t rem = b - w32 * per_w;
+    const uint32_t g32 = rem / tpw32;
+    const int64_t tpw = p.tiles_per_walker;
+    const int64_t w = w32, g = g32, c = rem - g32 * tpw32;
+    const int32_t p0 = (int32_t)g * PB;
+    const int np = min(PB, p.P - p0);
+
+    load_table<T>(p, tab);
+    Trial<T> tr[PB];
+    int kg;
+    int64_t k_local;
+    walker_setup<T, PB>(p, w, p0, np, tr, kg, k_local);
+    const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tab);
+
+    const int64_t start = c * CH;
+    const int64_t end = min(start + (int64_t)CH, p.N_local);
+    const T *Rw = static_cast<const T *>(p.R) + w * p.src_stride;
+    const int64_t voff = (start >> (VW == 4 ? 2 : 1)) + threadIdx.x;   // this thread's first vector
+    const V *px = reinterpret_cast<const V *>(Rw) + voff;
+    const V *py = reinterpret_cast<const V *>(Rw + p.Np) + voff;
+    const V *pz = reinterpret_cast<const V *>(Rw + 2 * p.Np) + voff;
+    V *rowp[PB];
+#pragma unroll
+    for (int q = 0; q < PB; ++q)
+        rowp[q] = ROW ? reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + p0 + (q < np ? q : 0)) * 4) * p.Np) + voff
+                      : nullptr;
+    const int64_t row_stride = p.Np / VW;
+    __syncthreads();
+
+    double dacc[PB][NOUT];
+#pragma unroll
+    for (int q = 0; q < PB; ++q)
+#pragma unroll
+        for (int a = 0; a < NOUT; ++a) dacc[q][a] = 0.0;
+
+#pragma unroll 1
+    for (int sidx = 0; sidx < SUB; ++sidx) {
+        const int64_t sstart = start + (int64_t)sidx * SCH;
+        if (sstart >= end) break;
+        const int64_t send = min(sstart + (int64_t)SCH, end);
+        const int64_t vs = (int64_t)sidx * (SCH / VW);
+        V *rp[PB];
+#pragma unroll
+        for (int q = 0; q < PB; ++q) rp[q] = ROW ? rowp[q] + vs : nullptr;
+        sub_tile<T, PB, ROW, PF, TPB>(threadIdx.x, p, kg, tab_addr, sstart, send, k_local, px + vs, py + vs,
+                                      pz + vs, tr, np, dacc, rp, row_stride);
+    }
+
+    // ---- CTA reduction in fp64 (fixed order: deterministic) ----
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < PB; ++q)
+#pragma unroll
+        for (int a = 0; a < NOUT; ++a) {
+            const double v = warp_sum(dacc[q][a]);
+            if (lane == 0) red[warp][q * NOUT + a] = v;
+        }
+    __syncthreads();
+
+    double tot = 0.0;   // thread t < PB*NOUT holds value t of this tile
+    if (threadIdx.x < PB * NOUT) {
+#pragma unroll
+        for (int wi = 0; wi < TPB / 32; ++wi) tot += red[wi][threadIdx.x];
+    }
+
+    const int64_t wg = w * p.n_groups + g;
+    if (tpw > 1) {
+        // publish this tile's partials; the last CTA of (w, g) reduces them
+        double *part = p.partials + (wg * tpw + c) * (PB * NOUT);
+        if (threadIdx.x < PB * NOUT) part[threadIdx.x] = tot;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned prev = atomicAdd(p.counters + wg, 1u);
+            last_flag = (prev == (unsigned)(tpw - 1));
+        }
+        __syncthreads();
+        if (!last_flag) return;
+        __threadfence();
+        // warp 0: value v summed over tiles, lane-strided then shuffle tree
+        if (warp == 0) {
+            const double *base = p.partials + wg * tpw * (PB * NOUT);
+            for (int v = 0; v < PB * NOUT; ++v) {
+                double s = 0.0;
+                for (int64_t t = lane; t < tpw; t += 32) s += __ldcg(base + t * (PB * NOUT) + v);
+                s = warp_sum(s);
+                if (lane == v) tot = s;      // lane v keeps value v (PB*NOUT <= 20 < 32)
+            }
+        }
+    }
+
+    // ---- finalize: lane t < PB*NOUT of warp 0 holds value (q = t / NOUT, a = t % NOUT) ----
+    if (warp == 0) {
+        const double V0 = __shfl_sync(0xffffffffu, tot, 0);   // V of this group's first trial
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+            double s[NOUT];
+#pragma unroll
+            for (int a = 0; a < NOUT; ++a) s[a] = __shfl_sync(0xffffffffu, tot, q * NOUT + a);
+            if (lane == 0) write_out<PB>(p, w, p0, np, q, s, V0);
+        }
+    }
+}
+
+// ===========================================================================
+// Short rows with many walkers (C1, C2, C4 waves): one warp per (walker,
+// trial group) walks all of the walker's sources in per-warp sub-tiles of
+// 32*VW*ITERS sources; the warp's fp64 shuffle tree is the whole
+// (deterministic) reduction: no shared-memory reduction, no cross-CTA
+// partials, no counters.
+// ===========================================================================
+template <typename T, int PB, bool ROW, int PF, int MINB = (sizeof(T) == 4 && PB == 1 && !ROW) ? 3 : 2>
+__global__ void __launch_bounds__(TPB, MINB)
+j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
+    using Tr = Traits<T>;
+    using V = typename Tr::V;
+    constexpr int VW = Tr::VW;
+    constexpr int SCH = 32 * VW * ITERS;
+    __shared__ Coef4<T> tab[MAXTAB];
+    load_table<T>(p, tab);
+    __syncthreads();
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t unit = (int64_t)blockIdx.x * (TPB / 32) + warp;
+    if (unit >= n_units) return;
+    const int64_t w = unit / p.n_groups, g = unit - w * p.n_groups;
+    const int32_t p0 = (int32_t)g * PB;
+    const int np = min(PB, p.P - p0);
+    Trial<T> tr[PB];
+    int kg;
+    int64_t k_local;
+    walker_setup<T, PB>(p, w, p0, np, tr, kg, k_local);
+    const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tab);
+    const T *Rw = static_cast<const T *>(p.R) + w * p.src_stride;
+    const int64_t row_stride = p.Np / VW;
+
+    double dacc[PB][NOUT];
+#pragma unroll
+    for (int q = 0; q < PB; ++q)
+#pragma unroll
+        for (int a = 0; a < NOUT; ++a) dacc[q][a] = 0.0;
+
+    for (int64_t sstart = 0; sstart < p.N_local; sstart += SCH) {
+        const int64_t send = min(sstart + (int64_t)SCH, p.N_local);
+        const int64_t voff = (sstart / VW) + lane;
+        const V *px = reinterpret_cast<const V *>(Rw) + voff;
+        const V *py = reinterpret_cast<const V *>(Rw + p.Np) + voff;
+        const V *pz = reinterpret_cast<const V *>(Rw + 2 * p.Np) + voff;
+        V *rp[PB];
+#pragma unroll
+        for (int q = 0; q < PB; ++q)
+            rp[q] = ROW ? reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + p0 + (q < np ? q : 0)) * 4) * p.Np) + voff
+                        : nullptr;
+        sub_tile<T, PB, ROW, PF, 32>(lane, p, kg, tab_addr, sstart, send, k_local, px, py, pz, tr, np, dacc, rp,
+                                     row_stride);
+    }
+
+    double V0 = 0.0;
+#pragma unroll
+    for (int q = 0; q < PB; ++q) {
+        double s[NOUT];
+#pragma unroll
+        for (int a = 0; a < NOUT; ++a) s[a] = warp_sum(dacc[q][a]);
+        if (q == 0) V0 = s[0];
+        if (lane == 0) write_out<PB>(p, w, p0, np, q, s, V0);
+    }
+}
+
+}  // namespace qj2

@@ -76,8 +76,8 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
     extern __shared__ __align__(128) unsigned char smem[];
     V *ring = reinterpret_cast<V *>(smem);                                   // [NST][3][VPT*TPB]
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + TMA_NST * 3 * LANE_BYTES);  // full[NST], empty[NST]
-    Coef4<T> *tab = reinterpret_cast<Coef4<T> *>(bars + 2 * TMA_NST);       // [2][m+1]
-    double *red = reinterpret_cast<double *>(tab + 2 * (QJ2_MAX_M + 1));    // [2][NCW][PB*NACC]
+    Coef4<T> *tab = reinterpret_cast<Coef4<T> *>(bars + 2 * TMA_NST);       // [MAXTAB]
+    double *red = reinterpret_cast<double *>(tab + MAXTAB);                 // [2][NCW][PB*NOUT]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t bar_base = (uint32_t)__cvta_generic_to_shared(bars);
@@ -98,7 +98,7 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
             uint32_t n = 0;   // global stage counter
             for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
                 const TileInfo ti = decode_tile(p, t, CH);
-                const T *Rw = static_cast<const T *>(p.R) + ti.w * 3 * p.Np;
+                const T *Rw = static_cast<const T *>(p.R) + ti.w * p.src_stride;
                 for (int64_t s0 = ti.start; s0 < ti.end; s0 += SRC_STAGE, ++n) {
                     const uint32_t slot = n % TMA_NST, round = n / TMA_NST;
                     mbar_wait(bar_base + 8 * (TMA_NST + slot), (round & 1) ^ 1);
@@ -117,12 +117,6 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
 
     // =====================  consumer warps  =====================
     const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tab);
-    const uint32_t magic_off = (uint32_t)(Tr::MAGIC_BITS * (typename Tr::U)sizeof(Coef4<T>));
-    const uint32_t base_same = tab_addr - magic_off;
-    const uint32_t base_opp = tab_addr + (uint32_t)((p.m + 1) * sizeof(Coef4<T>)) - magic_off;
-    const typename Tr::U clamp_bits = Tr::MAGIC_BITS + (typename Tr::U)p.m;
-    const T inv_delta = sizeof(T) == 4 ? T(p.inv_delta_f) : T(p.inv_delta);
-    const T L0 = T(p.L[0]), L1 = T(p.L[1]), L2 = T(p.L[2]);
     const int tid = threadIdx.x;
     const int64_t tpw = p.tiles_per_walker;
 
@@ -132,28 +126,18 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
         const TileInfo ti = decode_tile(p, t, CH);
         const int32_t p0 = (int32_t)ti.g * PB;
         const int np = min(PB, p.P - p0);
-        const int64_t kw = p.k[ti.w];
-        const bool k_up = kw < p.N_up;
-        const int64_t k_local = kw - p.i_offset;
-        const int64_t nup_local = p.N_up - p.i_offset;
         Trial<T> tr[PB];
-#pragma unroll
-        for (int q = 0; q < PB; ++q) {
-            const int qq = q < np ? q : 0;
-            const T *rt = static_cast<const T *>(p.r_trial) + ((ti.w * p.P + p0 + qq) * 3);
-            tr[q].ax = make_axis<T>(rt[0], L0);
-            tr[q].ay = make_axis<T>(rt[1], L1);
-            tr[q].az = make_axis<T>(rt[2], L2);
-        }
-        double dacc[PB][NACC];
+        int kg;
+        int64_t k_local;
+        walker_setup<T, PB>(p, ti.w, p0, np, tr, kg, k_local);
+        double dacc[PB][NOUT];
         T acc[PB][NACC];
 #pragma unroll
         for (int q = 0; q < PB; ++q)
 #pragma unroll
-            for (int a = 0; a < NACC; ++a) { dacc[q][a] = 0.0; acc[q][a] = T(0); }
+            for (int a = 0; a < NOUT; ++a) dacc[q][a] = 0.0;
 
-        int sc = 0;
-        for (int64_t s0 = ti.start; s0 < ti.end; s0 += SRC_STAGE, ++n, ++sc) {
+        for (int64_t s0 = ti.start; s0 < ti.end; s0 += SRC_STAGE, ++n) {
             const uint32_t slot = n % TMA_NST, round = n / TMA_NST;
             mbar_wait(bar_base + 8 * slot, round & 1);
             const V *st = ring + slot * 3 * (VPT * TPB);
@@ -168,35 +152,25 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
             if (lane == 0) mbar_arrive(bar_base + 8 * (TMA_NST + slot));   // data is in registers
 
             const int64_t len = min((int64_t)SRC_STAGE, ti.end - s0);
+            const int64_t g0 = s0 + p.i_offset;
+            const int grp = src_group(p, g0);
+            const bool one_group = src_group(p, s0 + len - 1 + p.i_offset) == grp;
             const bool k_in = k_local >= s0 && k_local < s0 + len;
-            const bool clean = (len == SRC_STAGE) && !k_in && !(nup_local > s0 && nup_local < s0 + len);
+            const GroupC<T> gc = group_consts<T>(p, grp, kg, tab_addr);
+#pragma unroll
+            for (int q = 0; q < PB; ++q)
+#pragma unroll
+                for (int a = 0; a < NACC; ++a) acc[q][a] = T(0);
 #pragma unroll
             for (int u = 0; u < VPT; ++u) {
-            const int rel = (u * TPB + tid) * VW;
-            if (clean) {
-                const uint32_t base = ((s0 < nup_local) == k_up) ? base_same : base_opp;
-#pragma unroll
-                for (int e = 0; e < VW; ++e) {
-                    const T x = Tr::comp(cx[u], e), y = Tr::comp(cy[u], e), z = Tr::comp(cz[u], e);
-#pragma unroll
-                    for (int q = 0; q < PB; ++q) {
-                        if (PB == 1 || q < np) {
-                            const T dx = min_image(x, tr[q].ax);
-                            const T dy = min_image(y, tr[q].ay);
-                            const T dz = min_image(z, tr[q].az);
-                            const T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-                            accumulate<T>(dx, dy, dz, r2, inv_delta, base, clamp_bits, acc[q]);
-                        }
-                    }
-                }
-            } else if (rel < len) {
-                const int k_rel = k_in ? (int)(k_local - s0) : -1;
-                const int64_t up_rel = nup_local - s0;
+                const int rel = (u * TPB + tid) * VW;
+                if (rel >= len) continue;
 #pragma unroll
                 for (int e = 0; e < VW; ++e) {
                     const int li = rel + e;
-                    const bool dead = (li >= len) || (li == k_rel);
-                    const uint32_t base = ((li < up_rel) == k_up) ? base_same : base_opp;
+                    const bool dead = (li >= len) || (k_in && li == (int)(k_local - s0));
+                    uint32_t base = gc.base;
+                    if (!one_group) base = group_consts<T>(p, src_group(p, g0 + li), kg, tab_addr).base;
                     const T x = Tr::comp(cx[u], e), y = Tr::comp(cy[u], e), z = Tr::comp(cz[u], e);
 #pragma unroll
                     for (int q = 0; q < PB; ++q) {
@@ -206,46 +180,36 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
                             const T dz = min_image(z, tr[q].az);
                             T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
                             r2 = dead ? T(1e30) : r2;
-                            accumulate<T>(dx, dy, dz, r2, inv_delta, base, clamp_bits, acc[q]);
+                            accumulate<T>(dx, dy, dz, r2, gc.invd, base, gc.clamp, acc[q]);
                         }
                     }
                 }
             }
-            }
-            if ((sc & (ITERS / VPT - 1)) == ITERS / VPT - 1) {   // <= ITERS*VW = 32 terms per fp32 partial
-#pragma unroll
-                for (int q = 0; q < PB; ++q)
-#pragma unroll
-                    for (int a = 0; a < NACC; ++a) { dacc[q][a] += (double)acc[q][a]; acc[q][a] = T(0); }
-            }
+            flush<T, PB>(acc, dacc, gc.sg, gc.sh, gc.ss);   // J2 only: groups share delta
         }
-#pragma unroll
-        for (int q = 0; q < PB; ++q)
-#pragma unroll
-            for (int a = 0; a < NACC; ++a) dacc[q][a] += (double)acc[q][a];
 
         // ---- CTA (consumer) reduction, double-buffered scratch ----
-        double *rb = red + parity_tile * (TMA_NCW * PB * NACC);
+        double *rb = red + parity_tile * (TMA_NCW * PB * NOUT);
 #pragma unroll
         for (int q = 0; q < PB; ++q)
 #pragma unroll
-            for (int a = 0; a < NACC; ++a) {
+            for (int a = 0; a < NOUT; ++a) {
                 const double v = warp_sum(dacc[q][a]);
-                if (lane == 0) rb[warp * (PB * NACC) + q * NACC + a] = v;
+                if (lane == 0) rb[warp * (PB * NOUT) + q * NOUT + a] = v;
             }
         named_bar(1, TPB);
         if (warp != 0) continue;
 
         // warp 0: tile total, publish, and (last CTA of the walker) finalize
         double tot = 0.0;
-        if (lane < PB * NACC) {
+        if (lane < PB * NOUT) {
 #pragma unroll
-            for (int wi = 0; wi < TMA_NCW; ++wi) tot += rb[wi * (PB * NACC) + lane];
+            for (int wi = 0; wi < TMA_NCW; ++wi) tot += rb[wi * (PB * NOUT) + lane];
         }
         const int64_t wg = ti.w * p.n_groups + ti.g;
         if (tpw > 1) {
-            double *part = p.partials + (wg * tpw + ti.c) * (PB * NACC);
-            if (lane < PB * NACC) part[lane] = tot;
+            double *part = p.partials + (wg * tpw + ti.c) * (PB * NOUT);
+            if (lane < PB * NOUT) part[lane] = tot;
             __threadfence();
             __syncwarp();
             unsigned last = 0;
@@ -253,34 +217,21 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
             last = __shfl_sync(0xffffffffu, last, 0);
             if (!last) continue;
             __threadfence();
-            const double *pb = p.partials + wg * tpw * (PB * NACC);
-            for (int v = 0; v < PB * NACC; ++v) {
+            const double *pb = p.partials + wg * tpw * (PB * NOUT);
+            for (int v = 0; v < PB * NOUT; ++v) {
                 double s = 0.0;
-                for (int64_t c = lane; c < tpw; c += 32) s += __ldcg(pb + c * (PB * NACC) + v);
+                for (int64_t c = lane; c < tpw; c += 32) s += __ldcg(pb + c * (PB * NOUT) + v);
                 s = warp_sum(s);
                 if (lane == v) tot = s;
             }
         }
-        const double id = p.inv_delta;
         const double V0 = __shfl_sync(0xffffffffu, tot, 0);
 #pragma unroll
         for (int q = 0; q < PB; ++q) {
-            double s[NACC];
+            double s[NOUT];
 #pragma unroll
-            for (int a = 0; a < NACC; ++a) s[a] = __shfl_sync(0xffffffffu, tot, q * NACC + a);
-            if (lane == 0 && q < np) {
-                const int64_t o = ti.w * p.P + p0 + q;
-                p.out[o * 5 + 0] = s[0];
-                p.out[o * 5 + 1] = -id * s[1];
-                p.out[o * 5 + 2] = -id * s[2];
-                p.out[o * 5 + 3] = -id * s[3];
-                p.out[o * 5 + 4] = 2.0 * id * id * s[4] + 2.0 * id * s[5];
-                if (p.ratio_out) {
-                    const double dj = s[0] - (p.V_cur ? p.V_cur[ti.w] : V0);
-                    p.ratio_out[o * 2 + 0] = dj;
-                    p.ratio_out[o * 2 + 1] = exp(dj);
-                }
-            }
+            for (int a = 0; a < NOUT; ++a) s[a] = __shfl_sync(0xffffffffu, tot, q * NOUT + a);
+            if (lane == 0) write_out<PB>(p, ti.w, p0, np, q, s, V0);
         }
     }
 }
@@ -288,7 +239,7 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
 template <typename T>
 constexpr size_t tma_smem_bytes(int PB, int VPT, int TMA_NST) {
     return (size_t)TMA_NST * 3 * VPT * TPB * Traits<T>::VW * sizeof(T) + 2 * TMA_NST * sizeof(uint64_t) +
-           2 * (QJ2_MAX_M + 1) * sizeof(Coef4<T>) + 2 * TMA_NCW * PB * NACC * sizeof(double);
+           MAXTAB * sizeof(Coef4<T>) + 2 * TMA_NCW * PB * NOUT * sizeof(double);
 }
 
 }  // namespace qj2

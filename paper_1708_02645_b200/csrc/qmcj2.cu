@@ -21,489 +21,7 @@
 #include <cstdlib>
 #include <algorithm>
 
-namespace qj2 {
-
-constexpr int TPB = 256;          // threads per CTA
-constexpr int ITERS = 8;          // vector iterations per sub-tile: 32 fp32 terms per thread per trial
-constexpr int SUB = 4;            // sub-tiles per CTA tile
-constexpr int NACC = 6;           // V, Gx, Gy, Gz, sum h, sum du/r  (per trial)
-constexpr int MAXPB = 4;
-
-// ---------------------------------------------------------------------------
-// Kernel parameters (by value, __grid_constant__).
-// ---------------------------------------------------------------------------
-struct EvalParams {
-    int64_t W, N_total, N_up, i_offset, N_local, Np;
-    int64_t tiles_per_walker;     // ceil(N_local / CH)
-    int64_t n_groups;             // ceil(P / PB)
-    int32_t P, m;
-    const void *R;
-    const int32_t *k;
-    const void *r_trial;
-    double *out;
-    void *row_out;
-    const double *V_cur;
-    double *ratio_out;
-    double *partials;             // [W][n_groups][tiles][PB][NACC]
-    unsigned int *counters;       // [W][n_groups]
-    double L[3];
-    double inv_delta;
-    float inv_delta_f;
-    double pcoef[2][QJ2_MAX_M + 1][4];   // power basis per interval; row m = 0
-};
-
-// ---------------------------------------------------------------------------
-// Helpers
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-template <typename T>
-__device__ __forceinline__ void load_table(const EvalParams &p, Coef4<T> *tab) {
-    const int n = 2 * (p.m + 1);
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const int s = e / (p.m + 1), j = e % (p.m + 1);
-        Coef4<T> c;
-        c.a0 = T(p.pcoef[s][j][0]);
-        c.a1 = T(p.pcoef[s][j][1]);
-        c.a2 = T(p.pcoef[s][j][2]);
-        c.a3 = T(p.pcoef[s][j][3]);
-        tab[e] = c;
-    }
-}
-
-// Per-trial constants: the three axes' minimum-image constants.
-template <typename T> struct Trial { Axis<T> ax, ay, az; };
-
-// Functor + accumulation for one source at squared distance r2 (and
-// displacement d).  acc: V, Gx, Gy, Gz (sum du/r * d), H (sum h), S (sum du/r).
-// Final scaling to U', U'' happens once, in fp64, per tile.
-template <typename T>
-__device__ __forceinline__ T accumulate(T dx, T dy, T dz, T r2, T inv_delta, uint32_t tab_base,
-                                        typename Traits<T>::U clamp_bits, T *acc) {
-    using Tr = Traits<T>;
-    const T ir = Tr::rsqrt(r2);
-    const T r = r2 * ir;
-    const FunctorEval<T> e = functor_from_t<T>(r * inv_delta, tab_base, clamp_bits);
-    const T g = e.du * ir;
-    acc[0] += e.u;
-    acc[1] = fma(g, dx, acc[1]);
-    acc[2] = fma(g, dy, acc[2]);
-    acc[3] = fma(g, dz, acc[3]);
-    acc[4] += e.h;
-    acc[5] += g;
-    return r;
-}
-
-// Minimum image for one axis, optionally specialised on the trial
-// coordinate's case (SPEC = 1: case A, c < L/2; 0: case B; -1: unified,
-// see make_axis).  Specialised forms take 3 instructions instead of 4, but the
-// 8 per-walker bodies measured slower on B200 (instruction-cache pressure,
-// DESIGN.md section 9); the kernel uses the unified form.
-template <typename T, int SPEC>
-__device__ __forceinline__ T min_image_k(T x, const Axis<T> &a) {
-    if constexpr (SPEC < 0) {
-        return min_image(x, a);
-    } else if constexpr (SPEC == 1) {           // case A: wrap shifts the source (x - L exact)
-        const T xs = x > a.thr ? x - a.a1 : x;
-        return xs - a.b0;
-    } else {                                    // case B: wrap shifts the trial (c - L exact)
-        return x - (x > a.thr ? a.b1 : a.b0);
-    }
-}
-
-// Masks of a sub-tile that is not "clean" (ragged length, holds the self
-// source k, or straddles the spin boundary N_up).  All offsets are relative to
-// the sub-tile start.
-struct SubMask {
-    int len;          // valid sources in the sub-tile
-    int k_rel;        // self source, or -1
-    int up_rel;       // first spin-down source (clamped to [0, SCH])
-    bool k_up;        // spin of k
-};
-
-// One sub-tile.  Every thread walks ITERS vectors at a constant stride of TPB
-// vectors, so every load address is base + immediate; PF vector groups are in
-// flight ahead of the one being consumed (software pipelining).
-// GEN = false: full sub-tile, no self source, one spin channel (`base`).
-// GEN = true: loads predicated on the sub-tile length; per source, dead
-// sources (self, padding) get r^2 = BIG, which lands on the all-zero interval
-// (every accumulated quantity exactly 0), and the channel is chosen per source.
-template <typename T, int PB, bool ROW, int PF, bool GEN, int NT = TPB, int SX = -1, int SY = -1, int SZ = -1>
-__device__ __forceinline__ void tile_run(int tid,const typename Traits<T>::V *__restrict__ px,
-                                         const typename Traits<T>::V *__restrict__ py,
-                                         const typename Traits<T>::V *__restrict__ pz,
-                                         const Trial<T> (&tr)[PB], int np, T inv_delta, uint32_t base,
-                                         uint32_t base_opp, const SubMask &mk,
-                                         typename Traits<T>::U clamp_bits, T (&acc)[PB][NACC],
-                                         typename Traits<T>::V *const (&rowp)[PB], int64_t row_stride) {
-    using Tr = Traits<T>;
-    using V = typename Tr::V;
-    constexpr int VW = Tr::VW;
-    // GEN: vector index clamped into the sub-tile (vectors past the end reload
-    // the last valid vector; their sources are all dead), so loads need no
-    // predicate and the pipeline has the same shape as the fast path.
-    const int vmax = GEN ? (mk.len - 1) / VW : 0;
-    auto voff = [&](int j) -> int {
-        return GEN ? min(j * NT + tid, vmax) - tid : j * NT;   // relative to this thread's vector
-    };
-    V bx[ITERS], by[ITERS], bz[ITERS];      // fully unrolled: only PF+1 groups are live
-#pragma unroll
-    for (int j = 0; j < PF && j < ITERS; ++j) {
-        bx[j] = Tr::ld_stream(px + voff(j));
-        by[j] = Tr::ld_stream(py + voff(j));
-        bz[j] = Tr::ld_stream(pz + voff(j));
-    }
-#pragma unroll
-    for (int it = 0; it < ITERS; ++it) {
-        if (it + PF < ITERS) {
-            bx[it + PF] = Tr::ld_stream(px + voff(it + PF));
-            by[it + PF] = Tr::ld_stream(py + voff(it + PF));
-            bz[it + PF] = Tr::ld_stream(pz + voff(it + PF));
-        }
-        const int rel = (it * NT + tid) * VW;
-        if (!GEN || rel < mk.len) {
-        V ro[PB][4];
-#pragma unroll
-        for (int e = 0; e < VW; ++e) {
-            bool dead = false;
-            uint32_t b = base;
-            if (GEN) {
-                const int li = rel + e;
-                dead = (li >= mk.len) || (li == mk.k_rel);
-                b = ((li < mk.up_rel) == mk.k_up) ? base : base_opp;
-            }
-            const T x = Tr::comp(bx[it], e), y = Tr::comp(by[it], e), z = Tr::comp(bz[it], e);
-#pragma unroll
-            for (int q = 0; q < PB; ++q) {
-                if (PB == 1 || q < np) {
-                    const T dx = min_image_k<T, SX>(x, tr[q].ax);
-                    const T dy = min_image_k<T, SY>(y, tr[q].ay);
-                    const T dz = min_image_k<T, SZ>(z, tr[q].az);
-                    T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-                    if (GEN) r2 = dead ? T(1e30) : r2;
-                    const T r = accumulate<T>(dx, dy, dz, r2, inv_delta, b, clamp_bits, acc[q]);
-                    if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
-                }
-            }
-        }
-        if (ROW) {
-#pragma unroll
-            for (int q = 0; q < PB; ++q)
-                if (PB == 1 || q < np)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) __stcs(rowp[q] + c * row_stride + it * NT, ro[q][c]);
-        }
-        }
-    }
-}
-
-// PF: prefetch distance (vector groups in flight), MINB: resident CTAs per SM
-// (register budget).
-template <typename T, int PB, bool ROW, int PF = 1, int MINB = ((sizeof(T) == 4 && PB == 1) ? 4 : 2)>
-__global__ void __launch_bounds__(TPB, MINB)
-j2_eval_kernel(const __grid_constant__ EvalParams p) {
-    using Tr = Traits<T>;
-    using V = typename Tr::V;
-    constexpr int VW = Tr::VW;
-    constexpr int SCH = TPB * VW * ITERS;         // sub-tile: 32 terms per thread
-    constexpr int CH = SCH * SUB;                 // tile handled by one CTA
-    __shared__ Coef4<T> tab[2 * (QJ2_MAX_M + 1)];
-    __shared__ double red[TPB / 32][PB * NACC];
-    __shared__ int last_flag;
-
-    // tile decode: chunk fastest so consecutive CTAs stream consecutive memory
-    // (32-bit arithmetic: the host guarantees W * n_groups * tiles < 2^31)
-    const uint32_t b = blockIdx.x;
-    const uint32_t tpw32 = (uint32_t)p.tiles_per_walker;
-    const uint32_t per_w = tpw32 * (uint32_t)p.n_groups;
-    const uint32_t w32 = b / per_w;
-    const uint32_t rem = b - w32 * per_w;
-    const uint32_t g32 = rem / tpw32;
-    const int64_t tpw = p.tiles_per_walker;
-    const int64_t w = w32, g = g32, c = rem - g32 * tpw32;
-    const int32_t p0 = (int32_t)g * PB;
-    const int np = min(PB, p.P - p0);
-
-    load_table<T>(p, tab);
-
-    const int64_t kw = p.k[w];
-    const bool k_up = kw < p.N_up;
-    const T L0 = T(p.L[0]), L1 = T(p.L[1]), L2 = T(p.L[2]);
-    Trial<T> tr[PB];
-#pragma unroll
-    for (int q = 0; q < PB; ++q) {
-        const int qq = q < np ? q : 0;
-        const T *rt = static_cast<const T *>(p.r_trial) + ((w * p.P + p0 + qq) * 3);
-        tr[q].ax = make_axis<T>(rt[0], L0);
-        tr[q].ay = make_axis<T>(rt[1], L1);
-        tr[q].az = make_axis<T>(rt[2], L2);
-    }
-    const T inv_delta = sizeof(T) == 4 ? T(p.inv_delta_f) : T(p.inv_delta);
-    const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tab);
-    const uint32_t magic_off = (uint32_t)(Tr::MAGIC_BITS * (typename Tr::U)sizeof(Coef4<T>));
-    const uint32_t base_same = tab_addr - magic_off;
-    const uint32_t base_opp = tab_addr + (uint32_t)((p.m + 1) * sizeof(Coef4<T>)) - magic_off;
-    const typename Tr::U clamp_bits = Tr::MAGIC_BITS + (typename Tr::U)p.m;
-
-    const int64_t start = c * CH;
-    const int64_t end = min(start + (int64_t)CH, p.N_local);
-    const int64_t k_local = kw - p.i_offset;
-    const int64_t nup_local = p.N_up - p.i_offset;   // first local index of the spin-down half
-
-    const T *Rw = static_cast<const T *>(p.R) + w * 3 * p.Np;
-    const int64_t voff = (start >> (VW == 4 ? 2 : 1)) + threadIdx.x;   // this thread's first vector
-    const V *px = reinterpret_cast<const V *>(Rw) + voff;
-    const V *py = reinterpret_cast<const V *>(Rw + p.Np) + voff;
-    const V *pz = reinterpret_cast<const V *>(Rw + 2 * p.Np) + voff;
-    V *rowp[PB];
-#pragma unroll
-    for (int q = 0; q < PB; ++q)
-        rowp[q] = ROW ? reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + p0 + (q < np ? q : 0)) * 4) * p.Np) + voff
-                      : nullptr;
-    const int64_t row_stride = p.Np / VW;
-    __syncthreads();
-
-    // The tile is SUB sub-tiles of SCH sources.  Per sub-tile, each thread
-    // accumulates <= ITERS*VW = 32 terms in T, then flushes to fp64
-    // ("quantities per walker ... in double precision").
-    double dacc[PB][NACC];
-#pragma unroll
-    for (int q = 0; q < PB; ++q)
-#pragma unroll
-        for (int a = 0; a < NACC; ++a) dacc[q][a] = 0.0;
-
-#pragma unroll 1
-    for (int sidx = 0; sidx < SUB; ++sidx) {
-        const int64_t sstart = start + (int64_t)sidx * SCH;
-        if (sstart >= end) break;
-        const int64_t send = min(sstart + (int64_t)SCH, end);
-        const int64_t vs = (int64_t)sidx * (SCH / VW);
-        T acc[PB][NACC];
-#pragma unroll
-        for (int q = 0; q < PB; ++q)
-#pragma unroll
-            for (int a = 0; a < NACC; ++a) acc[q][a] = T(0);
-        const bool k_in = k_local >= sstart && k_local < send;
-        const bool masked = (send - sstart != SCH) || k_in || (nup_local > sstart && nup_local < send);
-        V *rp[PB];
-#pragma unroll
-        for (int q = 0; q < PB; ++q) rp[q] = ROW ? rowp[q] + vs : nullptr;
-        if (masked) {
-            SubMask mk;
-            mk.len = (int)(send - sstart);
-            mk.k_rel = k_in ? (int)(k_local - sstart) : -1;
-            mk.up_rel = (int)max((int64_t)0, min(nup_local - sstart, (int64_t)SCH));
-            mk.k_up = true;   // base_same is "channel of sources below up_rel" iff k is up
-            const uint32_t b_lo = k_up ? base_same : base_opp;   // channel of sources i < N_up
-            const uint32_t b_hi = k_up ? base_opp : base_same;   // channel of sources i >= N_up
-            tile_run<T, PB, ROW, PF, true>(threadIdx.x, px + vs, py + vs, pz + vs, tr, np, inv_delta, b_lo, b_hi, mk,
-                                           clamp_bits, acc, rp, row_stride);
-        } else {
-            const bool tile_up = sstart < nup_local;
-            const uint32_t base = (tile_up == k_up) ? base_same : base_opp;
-            SubMask mk{SCH, -1, 0, true};
-            tile_run<T, PB, ROW, PF, false>(threadIdx.x, px + vs, py + vs, pz + vs, tr, np, inv_delta, base, base, mk,
-                                            clamp_bits, acc, rp, row_stride);
-        }
-#pragma unroll
-        for (int q = 0; q < PB; ++q)
-#pragma unroll
-            for (int a = 0; a < NACC; ++a) dacc[q][a] += (double)acc[q][a];
-    }
-
-    // ---- CTA reduction in fp64 (fixed order: deterministic) ----
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int q = 0; q < PB; ++q)
-#pragma unroll
-        for (int a = 0; a < NACC; ++a) {
-            const double v = warp_sum(dacc[q][a]);
-            if (lane == 0) red[warp][q * NACC + a] = v;
-        }
-    __syncthreads();
-
-    double tot = 0.0;   // thread t < PB*NACC holds value t of this tile
-    if (threadIdx.x < PB * NACC) {
-#pragma unroll
-        for (int wi = 0; wi < TPB / 32; ++wi) tot += red[wi][threadIdx.x];
-    }
-
-    const int64_t wg = w * p.n_groups + g;
-    if (tpw > 1) {
-        // publish this tile's partials; the last CTA of (w, g) reduces them
-        double *part = p.partials + (wg * tpw + c) * (PB * NACC);
-        if (threadIdx.x < PB * NACC) part[threadIdx.x] = tot;
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const unsigned prev = atomicAdd(p.counters + wg, 1u);
-            last_flag = (prev == (unsigned)(tpw - 1));
-        }
-        __syncthreads();
-        if (!last_flag) return;
-        __threadfence();
-        // warp 0: value v summed over tiles, lane-strided then shuffle tree
-        if (warp == 0) {
-            const double *base = p.partials + wg * tpw * (PB * NACC);
-            for (int v = 0; v < PB * NACC; ++v) {
-                double s = 0.0;
-                for (int64_t t = lane; t < tpw; t += 32) s += __ldcg(base + t * (PB * NACC) + v);
-                s = warp_sum(s);
-                if (lane == v) tot = s;      // lane v keeps value v (PB*NACC <= 24 < 32)
-            }
-        }
-    }
-
-    // ---- finalize: lane t < PB*NACC of warp 0 holds value (q = t / NACC, a = t % NACC) ----
-    if (warp == 0) {
-        const double id = p.inv_delta;
-        const double V0 = __shfl_sync(0xffffffffu, tot, 0);   // V of this group's first trial
-#pragma unroll
-        for (int q = 0; q < PB; ++q) {
-            double s[NACC];
-#pragma unroll
-            for (int a = 0; a < NACC; ++a) s[a] = __shfl_sync(0xffffffffu, tot, q * NACC + a);
-            if (lane == 0 && q < np) {
-                const int64_t o = w * p.P + p0 + q;
-                const double V = s[0];
-                p.out[o * 5 + 0] = V;
-                p.out[o * 5 + 1] = -id * s[1];
-                p.out[o * 5 + 2] = -id * s[2];
-                p.out[o * 5 + 3] = -id * s[3];
-                p.out[o * 5 + 4] = 2.0 * id * id * s[4] + 2.0 * id * s[5];
-                if (p.ratio_out) {   // e^{dJ2} factor of Eq. 4 (host guarantees a valid reference)
-                    const double dj = V - (p.V_cur ? p.V_cur[w] : V0);
-                    p.ratio_out[o * 2 + 0] = dj;
-                    p.ratio_out[o * 2 + 1] = exp(dj);
-                }
-            }
-        }
-    }
-}
-
-// Small-N mapping (one tile per walker and many walkers, e.g. C1, C2, C4):
-// one warp per (walker, trial group) walks all of the walker's sources in
-// per-warp sub-tiles of 32*VW*ITERS sources (<= 32 fp32 terms per lane, then
-// an fp64 flush), so there is no shared-memory reduction, no cross-CTA
-// partials and no counters; the warp's fp64 shuffle tree is the whole
-// (deterministic) reduction.
-template <typename T, int PB, bool ROW, int PF, int MINB = (sizeof(T) == 4 && PB == 1 && !ROW) ? 3 : 2>
-__global__ void __launch_bounds__(TPB, MINB)
-j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
-    using Tr = Traits<T>;
-    using V = typename Tr::V;
-    constexpr int VW = Tr::VW;
-    constexpr int SCH = 32 * VW * ITERS;
-    __shared__ Coef4<T> tab[2 * (QJ2_MAX_M + 1)];
-    load_table<T>(p, tab);
-    __syncthreads();
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t unit = (int64_t)blockIdx.x * (TPB / 32) + warp;
-    if (unit >= n_units) return;
-    const int64_t w = unit / p.n_groups, g = unit - w * p.n_groups;
-    const int32_t p0 = (int32_t)g * PB;
-    const int np = min(PB, p.P - p0);
-    const int64_t kw = p.k[w];
-    const bool k_up = kw < p.N_up;
-    const T L0 = T(p.L[0]), L1 = T(p.L[1]), L2 = T(p.L[2]);
-    Trial<T> tr[PB];
-#pragma unroll
-    for (int q = 0; q < PB; ++q) {
-        const int qq = q < np ? q : 0;
-        const T *rt = static_cast<const T *>(p.r_trial) + ((w * p.P + p0 + qq) * 3);
-        tr[q].ax = make_axis<T>(rt[0], L0);
-        tr[q].ay = make_axis<T>(rt[1], L1);
-        tr[q].az = make_axis<T>(rt[2], L2);
-    }
-    const T inv_delta = sizeof(T) == 4 ? T(p.inv_delta_f) : T(p.inv_delta);
-    const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tab);
-    const uint32_t magic_off = (uint32_t)(Tr::MAGIC_BITS * (typename Tr::U)sizeof(Coef4<T>));
-    const uint32_t base_same = tab_addr - magic_off;
-    const uint32_t base_opp = tab_addr + (uint32_t)((p.m + 1) * sizeof(Coef4<T>)) - magic_off;
-    const typename Tr::U clamp_bits = Tr::MAGIC_BITS + (typename Tr::U)p.m;
-    const int64_t k_local = kw - p.i_offset;
-    const int64_t nup_local = p.N_up - p.i_offset;
-    const T *Rw = static_cast<const T *>(p.R) + w * 3 * p.Np;
-    const int64_t row_stride = p.Np / VW;
-
-    double dacc[PB][NACC];
-#pragma unroll
-    for (int q = 0; q < PB; ++q)
-#pragma unroll
-        for (int a = 0; a < NACC; ++a) dacc[q][a] = 0.0;
-
-    for (int64_t sstart = 0; sstart < p.N_local; sstart += SCH) {
-        const int64_t send = min(sstart + (int64_t)SCH, p.N_local);
-        const int64_t voff = (sstart / VW) + lane;
-        const V *px = reinterpret_cast<const V *>(Rw) + voff;
-        const V *py = reinterpret_cast<const V *>(Rw + p.Np) + voff;
-        const V *pz = reinterpret_cast<const V *>(Rw + 2 * p.Np) + voff;
-        V *rp[PB];
-#pragma unroll
-        for (int q = 0; q < PB; ++q)
-            rp[q] = ROW ? reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + p0 + (q < np ? q : 0)) * 4) * p.Np) + voff
-                        : nullptr;
-        T acc[PB][NACC];
-#pragma unroll
-        for (int q = 0; q < PB; ++q)
-#pragma unroll
-            for (int a = 0; a < NACC; ++a) acc[q][a] = T(0);
-        const bool k_in = k_local >= sstart && k_local < send;
-        const bool masked = (send - sstart != SCH) || k_in || (nup_local > sstart && nup_local < send);
-        if (masked) {
-            SubMask mk;
-            mk.len = (int)(send - sstart);
-            mk.k_rel = k_in ? (int)(k_local - sstart) : -1;
-            mk.up_rel = (int)max((int64_t)0, min(nup_local - sstart, (int64_t)SCH));
-            mk.k_up = true;
-            const uint32_t b_lo = k_up ? base_same : base_opp;
-            const uint32_t b_hi = k_up ? base_opp : base_same;
-            tile_run<T, PB, ROW, PF, true, 32>(lane, px, py, pz, tr, np, inv_delta, b_lo, b_hi, mk, clamp_bits,
-                                               acc, rp, row_stride);
-        } else {
-            const uint32_t base = ((sstart < nup_local) == k_up) ? base_same : base_opp;
-            SubMask mk{SCH, -1, 0, true};
-            tile_run<T, PB, ROW, PF, false, 32>(lane, px, py, pz, tr, np, inv_delta, base, base, mk, clamp_bits,
-                                                acc, rp, row_stride);
-        }
-#pragma unroll
-        for (int q = 0; q < PB; ++q)
-#pragma unroll
-            for (int a = 0; a < NACC; ++a) dacc[q][a] += (double)acc[q][a];
-    }
-
-    const double id = p.inv_delta;
-    double V0 = 0.0;
-#pragma unroll
-    for (int q = 0; q < PB; ++q) {
-        double s[NACC];
-#pragma unroll
-        for (int a = 0; a < NACC; ++a) s[a] = warp_sum(dacc[q][a]);
-        if (q == 0) V0 = s[0];
-        if (lane == 0 && q < np) {
-            const int64_t o = w * p.P + p0 + q;
-            p.out[o * 5 + 0] = s[0];
-            p.out[o * 5 + 1] = -id * s[1];
-            p.out[o * 5 + 2] = -id * s[2];
-            p.out[o * 5 + 3] = -id * s[3];
-            p.out[o * 5 + 4] = 2.0 * id * id * s[4] + 2.0 * id * s[5];
-            if (p.ratio_out) {
-                const double dj = s[0] - (p.V_cur ? p.V_cur[w] : V0);
-                p.ratio_out[o * 2 + 0] = dj;
-                p.ratio_out[o * 2 + 1] = exp(dj);
-            }
-        }
-    }
-}
-
-}  // namespace qj2
-
-#include "j2_tma.cuh"
+#include "launch.cuh"
 
 // ===========================================================================
 // Small kernels
@@ -662,84 +180,41 @@ void ws_layout(int64_t W, int32_t P, int64_t N_local, qj2_dtype dtype,
     const int64_t tpw = (N_local + ch_of(dtype) - 1) / ch_of(dtype);
     const int pb = pb_of(P);
     const int64_t ng = (P + pb - 1) / pb;
-    *part_bytes = tpw > 1 ? align256((size_t)W * ng * tpw * pb * NACC * sizeof(double)) : 0;
+    *part_bytes = tpw > 1 ? align256((size_t)W * ng * tpw * pb * NOUT * sizeof(double)) : 0;
     *cnt_bytes = tpw > 1 ? align256((size_t)W * ng * sizeof(unsigned)) : 0;
 }
 
-// Kernel choice (A/B measurements only): QJ2_KERNEL=ldg1 (prefetch distance
-// 1, 4 CTAs/SM) or tma323 (TMA-pipelined persistent kernel, 3 CTAs/SM, 2
-// vectors per lane per stage, 3 stages); default: LDG kernel, prefetch 2.
-struct TmaCfg { int minb, vpt, nst; };
-constexpr TmaCfg kTmaCfgs[] = {{3, 2, 3}};
-int kernel_choice() {   // -1 = LDG kernel, else index into kTmaCfgs
-    const char *e = getenv("QJ2_KERNEL");
-    if (!e) return -1;
-    if (strcmp(e, "ldg") == 0) return -1;
-    if (strncmp(e, "tma", 3) == 0 && strlen(e) == 6) {
-        for (int i = 0; i < (int)(sizeof(kTmaCfgs) / sizeof(kTmaCfgs[0])); ++i)
-            if (e[3] - '0' == kTmaCfgs[i].minb && e[4] - '0' == kTmaCfgs[i].vpt && e[5] - '0' == kTmaCfgs[i].nst)
-                return i;
+// Kernel launches live in launch_*.cu (one translation unit per dtype / trial
+// batch, compiled in parallel); see launch.cuh.
+// Shared tail of qj2_eval / qj2_eval_j1: workspace, counters, dispatch.
+qj2_status launch_common(EvalParams &p, qj2_dtype dtype, int pb, int64_t ng, void *workspace,
+                         size_t workspace_bytes, cudaStream_t stream, bool check_dev) {
+    if (((uintptr_t)p.R & 15) || (p.row_out && ((uintptr_t)p.row_out & 15)))
+        return fail(QJ2_EINVAL, "source positions and row_out must be 16-byte aligned");
+    size_t part_b, cnt_b;
+    ws_layout(p.W, p.P, p.N_local, dtype, &part_b, &cnt_b);
+    if (part_b + cnt_b > 0 && (!workspace || workspace_bytes < part_b + cnt_b))
+        return fail(QJ2_EINVAL, "workspace too small: need %zu bytes", part_b + cnt_b);
+    const int64_t tpw = (p.N_local + ch_of(dtype) - 1) / ch_of(dtype);
+    const int64_t nblocks = p.W * ng * tpw;
+    if (nblocks > 0x7fffffffLL) return fail(QJ2_EINVAL, "problem too large for one launch (%lld CTAs)", (long long)nblocks);
+    if (check_dev) { qj2_status st = check_device(); if (st) return st; }
+    p.tiles_per_walker = tpw;
+    p.n_groups = ng;
+    p.partials = part_b ? static_cast<double *>(workspace) : nullptr;
+    p.counters = cnt_b ? reinterpret_cast<unsigned *>(static_cast<char *>(workspace) + part_b) : nullptr;
+    const bool row = p.row_out != nullptr;
+    cudaError_t e;
+    if (cnt_b) {   // completion counters start at zero every call (no caller-side init needed)
+        e = cudaMemsetAsync(p.counters, 0, (size_t)p.W * ng * sizeof(unsigned), stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counters)");
     }
-    return -1;
-}
-
-template <typename T, int PB, int MINB, int VPT, int NST>
-cudaError_t launch_tma(const EvalParams &p, int64_t nblocks, cudaStream_t s) {
-    auto kern = j2_eval_tma_kernel<T, PB, MINB, VPT, NST>;
-    const size_t smem = tma_smem_bytes<T>(PB, VPT, NST);
-    static int configured = 0;          // benign race: idempotent attribute set
-    static int blocks_per_sm = 0, sms = 0;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, TMA_THREADS, smem);
-        if (e != cudaSuccess) return e;
-        configured = 1;
-    }
-    const int64_t grid = std::min<int64_t>(nblocks, (int64_t)sms * std::max(blocks_per_sm, 1));
-    kern<<<(unsigned)grid, TMA_THREADS, smem, s>>>(p, (uint32_t)nblocks);
-    return cudaGetLastError();
-}
-
-// Warp-per-walker mapping when a walker's slice is one CTA tile and there
-// are enough (walker, group) units to fill the GPU (or the slice is tiny).
-bool use_warp_mapping(const EvalParams &p) {
-    return p.tiles_per_walker == 1 && (p.W * p.n_groups >= 4096 || p.N_local <= 2048);
-}
-
-template <typename T, int PB>
-cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStream_t s) {
-    if (use_warp_mapping(p)) {
-        const int64_t units = p.W * p.n_groups;
-        const unsigned nbw = (unsigned)((units + TPB / 32 - 1) / (TPB / 32));
-        if (row) j2_eval_warp_kernel<T, PB, true, 1><<<nbw, TPB, 0, s>>>(p, units);
-        else     j2_eval_warp_kernel<T, PB, false, 2><<<nbw, TPB, 0, s>>>(p, units);
-        return cudaGetLastError();
-    }
-    const int kc = row ? -1 : kernel_choice();
-    switch (kc) {
-        case 0: return launch_tma<T, PB, 3, 2, 3>(p, nblocks, s);
-        default: break;
-    }
-    const char *e = getenv("QJ2_KERNEL");
-    const unsigned nb = (unsigned)nblocks;
-    if (row) {
-        j2_eval_kernel<T, PB, true><<<nb, TPB, 0, s>>>(p);
-    } else if constexpr (PB == 1 && sizeof(T) == 4) {
-        if (e && strcmp(e, "ldg1") == 0)       // A/B: prefetch distance 1, 4 CTAs/SM
-            j2_eval_kernel<T, PB, false, 1, 4><<<nb, TPB, 0, s>>>(p);
-        else    // default: two vector groups in flight per thread, 3 CTAs/SM (80 registers);
-                // measured best on B200
-            j2_eval_kernel<T, PB, false, 2, 3><<<nb, TPB, 0, s>>>(p);
-    } else if constexpr (PB == 1) {             // fp64: two groups in flight, 2 CTAs/SM
-        j2_eval_kernel<T, PB, false, 2, 2><<<nb, TPB, 0, s>>>(p);
-    } else {
-        j2_eval_kernel<T, PB, false><<<nb, TPB, 0, s>>>(p);
-    }
-    return cudaGetLastError();
+    if (dtype == QJ2_FP32)
+        e = pb == 1 ? launch_f32_pb1(p, nblocks, row, stream) : launch_f32_pbn(p, pb, nblocks, row, stream);
+    else
+        e = pb == 1 ? launch_f64_pb1(p, nblocks, row, stream) : launch_f64_pbn(p, pb, nblocks, row, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "j2_eval_kernel launch");
+    return QJ2_OK;
 }
 
 qj2_status eval_impl(const qj2_functor *fn, qj2_dtype dtype,
@@ -768,48 +243,90 @@ qj2_status eval_impl(const qj2_functor *fn, qj2_dtype dtype,
     }
     if (W == 0) return QJ2_OK;
     if (!R || !k || !r_trial || !out) return fail(QJ2_EINVAL, "R, k, r_trial and out must be non-NULL");
-    if (((uintptr_t)R & 15) || (row_out && ((uintptr_t)row_out & 15)))
-        return fail(QJ2_EINVAL, "R and row_out must be 16-byte aligned");
-    size_t part_b, cnt_b;
-    ws_layout(W, P, N_local, dtype, &part_b, &cnt_b);
-    if (part_b + cnt_b > 0 && (!workspace || workspace_bytes < part_b + cnt_b))
-        return fail(QJ2_EINVAL, "workspace too small: need %zu bytes", part_b + cnt_b);
-    const int64_t tpw = (N_local + ch_of(dtype) - 1) / ch_of(dtype);
-    const int64_t nblocks = W * ng * tpw;
-    if (nblocks > 0x7fffffffLL) return fail(QJ2_EINVAL, "problem too large for one launch (%lld CTAs)", (long long)nblocks);
-    if (check_dev) { st = check_device(); if (st) return st; }
 
     EvalParams p;
     memset(&p, 0, sizeof p);
     p.W = W; p.N_total = N_total; p.N_up = N_up; p.i_offset = i_offset; p.N_local = N_local; p.Np = Np;
-    p.tiles_per_walker = tpw; p.n_groups = ng; p.P = P; p.m = fn->m;
+    p.P = P; p.m = fn->m;
+    p.mode = MODE_J2;
+    p.src_stride = 3 * Np;
+    p.n_src_groups = 2;                       // spin halves [0, N_up), [N_up, N_total)
+    p.grp_start[0] = 0; p.grp_start[1] = N_up; p.grp_start[2] = N_total;
+    for (int g = 3; g <= MAXG; ++g) p.grp_start[g] = N_total;
     p.R = R; p.k = k; p.r_trial = r_trial; p.out = out; p.row_out = row_out;
     p.V_cur = V_cur; p.ratio_out = ratio_out;
-    p.partials = part_b ? static_cast<double *>(workspace) : nullptr;
-    p.counters = cnt_b ? reinterpret_cast<unsigned *>(static_cast<char *>(workspace) + part_b) : nullptr;
     for (int d = 0; d < 3; ++d) p.L[d] = fn->L[d];
     p.inv_delta = (double)fn->m / fn->r_cut;
-    p.inv_delta_f = (float)p.inv_delta;
-    power_basis(fn->coef[0], fn->m, p.pcoef[0]);
-    power_basis(fn->coef[1], fn->m, p.pcoef[1]);
+    power_basis(fn->coef[0], fn->m, p.pcoef);                  // rows [0, m]: same spin
+    power_basis(fn->coef[1], fn->m, p.pcoef + (fn->m + 1));    // rows [m+1, 2m+1]: opposite spin
+    p.n_tab = 2 * (fn->m + 1);
+    return launch_common(p, dtype, pb, ng, workspace, workspace_bytes, stream, check_dev);
+}
 
-    const bool row = row_out != nullptr;
-    cudaError_t e;
-    if (cnt_b) {   // completion counters start at zero every call (no caller-side init needed)
-        e = cudaMemsetAsync(p.counters, 0, (size_t)W * ng * sizeof(unsigned), stream);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counters)");
+qj2_status validate_j1_functor(const qj2_j1_functor *fn) {
+    if (!fn) return fail(QJ2_EINVAL, "fn is NULL");
+    if (fn->reserved != 0) return fail(QJ2_EINVAL, "fn->reserved must be 0");
+    if (fn->n_species < 1 || fn->n_species > QJ2_MAX_SPECIES)
+        return fail(QJ2_EINVAL, "n_species must be in [1, %d]", QJ2_MAX_SPECIES);
+    for (int d = 0; d < 3; ++d)
+        if (!(fn->L[d] > 0) || !std::isfinite(fn->L[d])) return fail(QJ2_EINVAL, "L[%d] must be finite and > 0", d);
+    const double Lmin = std::fmin(fn->L[0], std::fmin(fn->L[1], fn->L[2]));
+    for (int s = 0; s < fn->n_species; ++s) {
+        if (!(fn->r_cut[s] > 0) || !(fn->r_cut[s] <= 0.5 * Lmin))
+            return fail(QJ2_EINVAL, "r_cut[%d] must satisfy 0 < r_cut <= min(L)/2", s);
+        if (fn->m[s] < 4 || fn->m[s] > QJ2_MAX_M) return fail(QJ2_EINVAL, "m[%d] must be in [4, %d]", s, QJ2_MAX_M);
+        for (int j = 0; j < fn->m[s] + 3; ++j)
+            if (!std::isfinite(fn->coef[s][j])) return fail(QJ2_EINVAL, "coef[%d][%d] not finite", s, j);
+        for (int j = fn->m[s]; j < fn->m[s] + 3; ++j)
+            if (fn->coef[s][j] != 0.0) return fail(QJ2_EINVAL, "coef[%d][%d] must be 0 (C2 cutoff)", s, j);
     }
-    if (dtype == QJ2_FP32) {
-        e = pb == 1 ? launch_eval<float, 1>(p, nblocks, row, stream)
-          : pb == 2 ? launch_eval<float, 2>(p, nblocks, row, stream)
-                    : launch_eval<float, MAXPB>(p, nblocks, row, stream);
-    } else {
-        e = pb == 1 ? launch_eval<double, 1>(p, nblocks, row, stream)
-          : pb == 2 ? launch_eval<double, 2>(p, nblocks, row, stream)
-                    : launch_eval<double, MAXPB>(p, nblocks, row, stream);
-    }
-    if (e != cudaSuccess) return cuda_fail(e, "j2_eval_kernel launch");
     return QJ2_OK;
+}
+
+qj2_status eval_j1_impl(const qj2_j1_functor *fn, qj2_dtype dtype, int64_t W, const int64_t *species_start,
+                        int64_t Np, const void *ions, int32_t P, const void *r_trial, double *out, void *row_out,
+                        const double *V_cur, double *ratio_out, void *workspace, size_t workspace_bytes,
+                        cudaStream_t stream) {
+    qj2_status st = validate_j1_functor(fn);
+    if (st) return st;
+    if (dtype != QJ2_FP32 && dtype != QJ2_FP64) return fail(QJ2_EINVAL, "bad dtype %d", (int)dtype);
+    if (W < 0) return fail(QJ2_EINVAL, "W < 0");
+    if (!species_start) return fail(QJ2_EINVAL, "species_start is NULL");
+    if (species_start[0] != 0) return fail(QJ2_EINVAL, "species_start[0] must be 0");
+    for (int s = 0; s < fn->n_species; ++s)
+        if (species_start[s + 1] < species_start[s]) return fail(QJ2_EINVAL, "species_start must be nondecreasing");
+    const int64_t n_ions = species_start[fn->n_species];
+    if (n_ions < 1) return fail(QJ2_EINVAL, "need at least one ion");
+    if (Np < n_ions || Np % vw_of(dtype) != 0)
+        return fail(QJ2_EINVAL, "Np must be >= n_ions and a multiple of %d", vw_of(dtype));
+    if (P < 1 || P > QJ2_MAX_P) return fail(QJ2_EINVAL, "P must be in [1, %d]", QJ2_MAX_P);
+    const int pb = pb_of(P);
+    const int64_t ng = (P + pb - 1) / pb;
+    if (ratio_out && !V_cur && ng != 1) return fail(QJ2_EINVAL, "ratio_out with V_cur == NULL needs P <= %d", MAXPB);
+    if (W == 0) return QJ2_OK;
+    if (!ions || !r_trial || !out) return fail(QJ2_EINVAL, "ions, r_trial and out must be non-NULL");
+
+    EvalParams p;
+    memset(&p, 0, sizeof p);
+    p.W = W; p.N_total = n_ions; p.N_up = 0; p.i_offset = 0; p.N_local = n_ions; p.Np = Np;
+    p.P = P; p.m = 0;
+    p.mode = MODE_J1;
+    p.src_stride = 0;                          // one ion set shared by all walkers
+    p.n_src_groups = fn->n_species;
+    int row = 0;
+    for (int g = 0; g <= MAXG; ++g) p.grp_start[g] = g <= fn->n_species ? species_start[g] : n_ions;
+    for (int s = 0; s < fn->n_species; ++s) {
+        p.grp_tab[s] = row;
+        p.grp_m[s] = fn->m[s];
+        p.grp_invd[s] = (double)fn->m[s] / fn->r_cut[s];
+        power_basis(fn->coef[s], fn->m[s], p.pcoef + row);
+        row += fn->m[s] + 1;
+    }
+    p.n_tab = row;
+    p.R = ions; p.k = nullptr; p.r_trial = r_trial; p.out = out; p.row_out = row_out;
+    p.V_cur = V_cur; p.ratio_out = ratio_out;
+    for (int d = 0; d < 3; ++d) p.L[d] = fn->L[d];
+    return launch_common(p, dtype, pb, ng, workspace, workspace_bytes, stream, true);
 }
 
 }  // namespace
@@ -860,6 +377,14 @@ qj2_status qj2_eval(const qj2_functor *fn, qj2_dtype dtype,
                     void *workspace, size_t workspace_bytes, void *stream) {
     return eval_impl(fn, dtype, W, N_total, N_up, i_offset, N_local, Np, R, k, P, r_trial, out, row_out,
                      V_cur, ratio_out, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), true);
+}
+
+qj2_status qj2_eval_j1(const qj2_j1_functor *fn, qj2_dtype dtype, int64_t W, const int64_t *species_start,
+                       int64_t Np, const void *ions, int32_t P, const void *r_trial, double *out, void *row_out,
+                       const double *V_cur, double *ratio_out, void *workspace, size_t workspace_bytes,
+                       void *stream) {
+    return eval_j1_impl(fn, dtype, W, species_start, Np, ions, P, r_trial, out, row_out, V_cur, ratio_out,
+                        workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
 }
 
 qj2_status qj2_ratio(int64_t W, int32_t P, const double *out, const double *V_cur, double *ratio_out, void *stream) {
