@@ -81,6 +81,14 @@ __device__ __forceinline__ void load_table(const EvalParams &p, Coef4<T> *tab) {
     }
 }
 
+// Opaque copy: keeps a precomputed table base in one register (otherwise the
+// compiler re-associates base + j*16 into 4 instructions per term).
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+    uint32_t y;
+    asm("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+
 // Functor constants of one source group for the current walker.
 template <typename T>
 struct GroupC {
@@ -113,7 +121,7 @@ __device__ __forceinline__ GroupC<T> group_consts(const EvalParams &p, int g, in
         m = p.grp_m[g];
         invd = p.grp_invd[g];
     }
-    c.base = tab_addr + (uint32_t)(row * (int)sizeof(Coef4<T>)) - magic_off;
+    c.base = opaque(tab_addr + (uint32_t)(row * (int)sizeof(Coef4<T>)) - magic_off);
     c.invd = T(invd);
     c.clamp = Tr::MAGIC_BITS + (typename Tr::U)m;
     c.sg = -invd;
