@@ -126,7 +126,7 @@ __device__ __forceinline__ T min_image(T x, const Axis<T> &a) {
 //   returns u = U, du = U' * delta, h = U'' * delta^2 / 2.
 // The interval index j = floor(t) is obtained with the round-down magic-number
 // add (no F2I), clamped to m (the zero interval).
-// tab_base: shared-memory byte address of interval 0 of the channel, minus
+// tab_base: shared-memory byte address of table row 0, minus
 // MAGIC_BITS * sizeof(Coef4) (so bits * sizeof(Coef4) + tab_base addresses j).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void ld_shared_c4(uint32_t addr, float &a0, float &a1, float &a2, float &a3) {
@@ -142,12 +142,18 @@ struct FunctorEval {
     T u, du, h;
 };
 
+// tab_base: shared-memory byte address of table row 0 (CTA-uniform).
+// row: first table row of the functor MINUS MAGIC_BITS (mod 2^bits), so
+// bits(MAGIC + floor(t)) + row = row0 + floor(t); clamp_bits = row0 + m (the
+// functor's all-zero row).  min(bits + row, clamp) is one VIADDMNMX and the
+// address one LEA off the uniform base: two instructions per term.
 template <typename T>
-__device__ __forceinline__ FunctorEval<T> functor_from_t(T t, uint32_t tab_base, typename Traits<T>::U clamp_bits) {
+__device__ __forceinline__ FunctorEval<T> functor_from_t(T t, uint32_t tab_base, typename Traits<T>::U row,
+                                                         typename Traits<T>::U clamp_bits) {
     using Tr = Traits<T>;
     const T tf = Tr::add_rd(t, Tr::MAGIC);                // MAGIC + floor(t)
-    typename Tr::U jb = Tr::bits(tf);
-    jb = jb < clamp_bits ? jb : clamp_bits;              // j = min(floor(t), m)
+    typename Tr::U jb = Tr::bits(tf) + row;               // row0 + floor(t)
+    jb = jb < clamp_bits ? jb : clamp_bits;              // row0 + min(floor(t), m)
     const T f = t - (tf - Tr::MAGIC);
     T a0, a1, a2, a3;
     ld_shared_c4(tab_base + (uint32_t)jb * (uint32_t)sizeof(Coef4<T>), a0, a1, a2, a3);

@@ -81,20 +81,12 @@ __device__ __forceinline__ void load_table(const EvalParams &p, Coef4<T> *tab) {
     }
 }
 
-// Opaque copy: keeps a precomputed table base in one register (otherwise the
-// compiler re-associates base + j*16 into 4 instructions per term).
-__device__ __forceinline__ uint32_t opaque(uint32_t x) {
-    uint32_t y;
-    asm("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
-    return y;
-}
-
 // Functor constants of one source group for the current walker.
 template <typename T>
 struct GroupC {
-    uint32_t base;                    // shared address of row 0, minus MAGIC_BITS * sizeof(Coef4)
+    typename Traits<T>::U row;        // first table row of the group's functor - MAGIC_BITS
     T invd;                           // 1/delta
-    typename Traits<T>::U clamp;      // MAGIC_BITS + m (the zero row)
+    typename Traits<T>::U clamp;      // first row + m (the group's zero row)
     double sg, sh, ss;                // fp64 flush scales: G = sg*acc, L = sh*acc_h + ss*acc_s
 };
 
@@ -106,9 +98,8 @@ __device__ __forceinline__ int src_group(const EvalParams &p, int64_t gi) {
 
 // kg: group (spin half) of the walker's active electron (J2).
 template <typename T>
-__device__ __forceinline__ GroupC<T> group_consts(const EvalParams &p, int g, int kg, uint32_t tab_addr) {
+__device__ __forceinline__ GroupC<T> group_consts(const EvalParams &p, int g, int kg, uint32_t /*tab_addr*/) {
     using Tr = Traits<T>;
-    const uint32_t magic_off = (uint32_t)(Tr::MAGIC_BITS * (typename Tr::U)sizeof(Coef4<T>));
     GroupC<T> c;
     int row, m;
     double invd;
@@ -121,9 +112,9 @@ __device__ __forceinline__ GroupC<T> group_consts(const EvalParams &p, int g, in
         m = p.grp_m[g];
         invd = p.grp_invd[g];
     }
-    c.base = opaque(tab_addr + (uint32_t)(row * (int)sizeof(Coef4<T>)) - magic_off);
+    c.row = (typename Tr::U)row - Tr::MAGIC_BITS;       // see functor_from_t
     c.invd = T(invd);
-    c.clamp = Tr::MAGIC_BITS + (typename Tr::U)m;
+    c.clamp = (typename Tr::U)(row + m);
     c.sg = -invd;
     c.sh = 2.0 * invd * invd;
     c.ss = 2.0 * invd;
@@ -139,11 +130,11 @@ template <typename T> struct Trial { Axis<T> ax, ay, az; };
 // source's 1/delta (per-source groups in a masked J1 sub-tile).
 template <typename T, bool PHYS = false>
 __device__ __forceinline__ T accumulate(T dx, T dy, T dz, T r2, T inv_delta, uint32_t tab_base,
-                                        typename Traits<T>::U clamp_bits, T *acc) {
+                                        typename Traits<T>::U row, typename Traits<T>::U clamp_bits, T *acc) {
     using Tr = Traits<T>;
     const T ir = Tr::rsqrt(r2);
     const T r = r2 * ir;
-    const FunctorEval<T> e = functor_from_t<T>(r * inv_delta, tab_base, clamp_bits);
+    const FunctorEval<T> e = functor_from_t<T>(r * inv_delta, tab_base, row, clamp_bits);
     T g = e.du * ir;
     T h = e.h;
     if (PHYS) {
@@ -206,6 +197,7 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
     using Tr = Traits<T>;
     using V = typename Tr::V;
     constexpr int VW = Tr::VW;
+    const uint32_t tab_base = tab_addr;
     const int vmax = GEN ? (mk.len - 1) / VW : 0;
     auto voff = [&](int j) -> int {
         return GEN ? min(j * NT + tid, vmax) - tid : j * NT;   // relative to this thread's vector
@@ -230,7 +222,7 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
 #pragma unroll
             for (int e = 0; e < VW; ++e) {
                 bool dead = false;
-                uint32_t b = gc.base;
+                typename Tr::U row = gc.row;
                 T invd = gc.invd;
                 typename Tr::U clamp = gc.clamp;
                 if (GEN) {
@@ -238,7 +230,7 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
                     dead = (li >= mk.len) || (li == mk.k_rel);
                     if (MULTI) {       // sub-tile straddles a group boundary
                         const GroupC<T> ge = group_consts<T>(p, src_group(p, mk.g0 + li), kg, tab_addr);
-                        b = ge.base;
+                        row = ge.row;
                         invd = ge.invd;
                         clamp = ge.clamp;
                     }
@@ -252,7 +244,7 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
                         const T dz = min_image_k<T, -1>(z, tr[q].az);
                         T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
                         if (GEN) r2 = dead ? T(1e30) : r2;
-                        const T r = accumulate<T, PHYS>(dx, dy, dz, r2, invd, b, clamp, acc[q]);
+                        const T r = accumulate<T, PHYS>(dx, dy, dz, r2, invd, tab_base, row, clamp, acc[q]);
                         if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
                     }
                 }

@@ -169,8 +169,7 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
                 for (int e = 0; e < VW; ++e) {
                     const int li = rel + e;
                     const bool dead = (li >= len) || (k_in && li == (int)(k_local - s0));
-                    uint32_t base = gc.base;
-                    if (!one_group) base = group_consts<T>(p, src_group(p, g0 + li), kg, tab_addr).base;
+                    const GroupC<T> ge = one_group ? gc : group_consts<T>(p, src_group(p, g0 + li), kg, tab_addr);
                     const T x = Tr::comp(cx[u], e), y = Tr::comp(cy[u], e), z = Tr::comp(cz[u], e);
 #pragma unroll
                     for (int q = 0; q < PB; ++q) {
@@ -180,7 +179,7 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
                             const T dz = min_image(z, tr[q].az);
                             T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
                             r2 = dead ? T(1e30) : r2;
-                            accumulate<T>(dx, dy, dz, r2, gc.invd, base, gc.clamp, acc[q]);
+                            accumulate<T>(dx, dy, dz, r2, gc.invd, tab_addr, ge.row, ge.clamp, acc[q]);
                         }
                     }
                 }
