@@ -186,7 +186,7 @@ struct SubMask {
 // the source's group picks the functor.  J2 groups share delta, so only the
 // table row changes (raw accumulation); J1 groups differ in delta, so GEN
 // sub-tiles accumulate physical units (PHYS).
-template <typename T, int PB, bool ROW, int PF, bool GEN, int NT = TPB, bool MULTI = false, bool PHYS = false>
+template <typename T, int PB, bool ROW, int PF, bool GEN, int NT = TPB>
 __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, uint32_t tab_addr,
                                          const typename Traits<T>::V *__restrict__ px,
                                          const typename Traits<T>::V *__restrict__ py,
@@ -228,12 +228,6 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
                 if (GEN) {
                     const int li = rel + e;
                     dead = (li >= mk.len) || (li == mk.k_rel);
-                    if (MULTI) {       // sub-tile straddles a group boundary
-                        const GroupC<T> ge = group_consts<T>(p, src_group(p, mk.g0 + li), kg, tab_addr);
-                        row = ge.row;
-                        invd = ge.invd;
-                        clamp = ge.clamp;
-                    }
                 }
                 const T x = Tr::comp(bx[it], e), y = Tr::comp(by[it], e), z = Tr::comp(bz[it], e);
 #pragma unroll
@@ -244,7 +238,7 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
                         const T dz = min_image_k<T, -1>(z, tr[q].az);
                         T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
                         if (GEN) r2 = dead ? T(1e30) : r2;
-                        const T r = accumulate<T, PHYS>(dx, dy, dz, r2, invd, tab_base, row, clamp, acc[q]);
+                        const T r = accumulate<T>(dx, dy, dz, r2, invd, tab_base, row, clamp, acc[q]);
                         if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
                     }
                 }
@@ -256,6 +250,56 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
 #pragma unroll
                         for (int c = 0; c < 4; ++c) __stcs(rowp[q] + c * row_stride + it * NT, ro[q][c]);
             }
+        }
+    }
+}
+
+// A sub-tile straddling a group boundary (spin halves in J2, species in J1):
+// rare, so a compact rolled loop (one vector per iteration, no prefetch) keeps
+// the instruction footprint of the hot loop small.  The group is looked up
+// per source and the terms are accumulated in physical units (PHYS) because
+// J1 species differ in delta.
+template <typename T, int PB, bool ROW, int NT>
+__device__ __noinline__ void tile_multi(int tid, const EvalParams &p, int kg, uint32_t tab_addr,
+                                        const typename Traits<T>::V *__restrict__ px,
+                                        const typename Traits<T>::V *__restrict__ py,
+                                        const typename Traits<T>::V *__restrict__ pz,
+                                        const Trial<T> *tr, int np, const SubMask &mk, T *acc /* [PB][NACC] */,
+                                        typename Traits<T>::V *const *rowp, int64_t row_stride) {
+    using Tr = Traits<T>;
+    using V = typename Tr::V;
+    constexpr int VW = Tr::VW;
+#pragma unroll 1
+    for (int it = 0; it < ITERS; ++it) {
+        const int rel = (it * NT + tid) * VW;
+        if (rel >= mk.len) break;
+        const V vx = Tr::ld_stream(px + it * NT), vy = Tr::ld_stream(py + it * NT), vz = Tr::ld_stream(pz + it * NT);
+        V ro[PB][4];
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+            const int li = rel + e;
+            const bool dead = (li >= mk.len) || (li == mk.k_rel);
+            const GroupC<T> ge = group_consts<T>(p, src_group(p, mk.g0 + li), kg, tab_addr);
+            const T x = Tr::comp(vx, e), y = Tr::comp(vy, e), z = Tr::comp(vz, e);
+#pragma unroll
+            for (int q = 0; q < PB; ++q) {
+                if (PB == 1 || q < np) {
+                    const T dx = min_image(x, tr[q].ax);
+                    const T dy = min_image(y, tr[q].ay);
+                    const T dz = min_image(z, tr[q].az);
+                    T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                    r2 = dead ? T(1e30) : r2;
+                    const T r = accumulate<T, true>(dx, dy, dz, r2, ge.invd, tab_addr, ge.row, ge.clamp, acc + q * NACC);
+                    if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
+                }
+            }
+        }
+        if (ROW) {
+#pragma unroll
+            for (int q = 0; q < PB; ++q)
+                if (PB == 1 || q < np)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) __stcs(rowp[q] + c * row_stride + it * NT, ro[q][c]);
         }
     }
 }
@@ -303,12 +347,8 @@ __device__ __forceinline__ void sub_tile(int tid, const EvalParams &p, int kg, u
     } else if (one_group) {                                    // ragged and/or holds k
         tile_run<T, PB, ROW, PF, true, NT>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp, row_stride);
         flush<T, PB>(acc, dacc, gc.sg, gc.sh, gc.ss);
-    } else if (p.mode == MODE_J2) {                            // spin halves share delta
-        tile_run<T, PB, ROW, PF, true, NT, true>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp, row_stride);
-        flush<T, PB>(acc, dacc, gc.sg, gc.sh, gc.ss);
-    } else {                                                   // species differ in delta
-        tile_run<T, PB, ROW, PF, true, NT, true, true>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp,
-                                                       row_stride);
+    } else {                                                   // straddles a group boundary
+        tile_multi<T, PB, ROW, NT>(tid, p, kg, tab_addr, px, py, pz, tr, np, mk, &acc[0][0], rp, row_stride);
         flush<T, PB>(acc, dacc, -1.0, 1.0, 2.0);
     }
 }
