@@ -14,8 +14,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libqmcj2.so")
 OBJDIR = os.path.join(PKG, "build_obj")
-SOURCES = [os.path.join(CSRC, f) for f in ("qmcj2.cu", "gen.cu", "launch_f32_pb1.cu", "launch_f32_pbn.cu",
-                                           "launch_f64_pb1.cu", "launch_f64_pbn.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in
+           ["qmcj2.cu", "gen.cu"] + [f"launch_{d}_{b}_{m}.cu" for d in ("f32", "f64") for b in ("pb1", "pbn")
+                                     for m in ("j2", "j1")]]
 HEADERS = [os.path.join(CSRC, f) for f in ("j2_device.cuh", "j2_kernels.cuh", "j2_tma.cuh", "launch.cuh")] + \
           [os.path.join(ROOT, "include", "qmcj2.h")]
 

@@ -142,18 +142,17 @@ struct FunctorEval {
     T u, du, h;
 };
 
-// tab_base: shared-memory byte address of table row 0 (CTA-uniform).
-// row: first table row of the functor MINUS MAGIC_BITS (mod 2^bits), so
-// bits(MAGIC + floor(t)) + row = row0 + floor(t); clamp_bits = row0 + m (the
-// functor's all-zero row).  min(bits + row, clamp) is one VIADDMNMX and the
-// address one LEA off the uniform base: two instructions per term.
+// tab_base: shared-memory byte address of the functor's row 0 minus
+// MAGIC_BITS * sizeof(Coef4) (so bits * sizeof(Coef4) + tab_base addresses
+// row j); clamp_bits = MAGIC_BITS + m (the all-zero row).  min(bits, clamp) is
+// one VIADDMNMX and the address one LEA.
 template <typename T>
-__device__ __forceinline__ FunctorEval<T> functor_from_t(T t, uint32_t tab_base, typename Traits<T>::U row,
+__device__ __forceinline__ FunctorEval<T> functor_from_t(T t, uint32_t tab_base,
                                                          typename Traits<T>::U clamp_bits) {
     using Tr = Traits<T>;
     const T tf = Tr::add_rd(t, Tr::MAGIC);                // MAGIC + floor(t)
-    typename Tr::U jb = Tr::bits(tf) + row;               // row0 + floor(t)
-    jb = jb < clamp_bits ? jb : clamp_bits;              // row0 + min(floor(t), m)
+    typename Tr::U jb = Tr::bits(tf);
+    jb = jb < clamp_bits ? jb : clamp_bits;              // MAGIC + min(floor(t), m)
     const T f = t - (tf - Tr::MAGIC);
     T a0, a1, a2, a3;
     ld_shared_c4(tab_base + (uint32_t)jb * (uint32_t)sizeof(Coef4<T>), a0, a1, a2, a3);

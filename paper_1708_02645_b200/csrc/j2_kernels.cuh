@@ -38,7 +38,7 @@ struct EvalParams {
     int64_t tiles_per_walker;     // ceil(N_local / CH)
     int64_t n_groups;             // trial groups: ceil(P / PB)
     int32_t P, m;                 // m: J2 interval count
-    int32_t mode;                 // MODE_J2 | MODE_J1
+    int32_t mode;                 // MODE_J2 | MODE_J1 (the kernels are also templated on it)
     int32_t n_src_groups;         // J2: 2; J1: species
     int32_t n_tab;                // table rows to stage in shared memory
     int64_t src_stride;           // elements between walkers' source blocks (J2 3*Np, J1 0)
@@ -57,6 +57,7 @@ struct EvalParams {
     unsigned int *counters;       // [W][n_groups]
     double L[3];
     double inv_delta;             // J2: 1/delta
+    float inv_delta_f;            // J2: 1/delta rounded to fp32
     double pcoef[MAXTAB][4];      // power basis per interval (J2: [0,m] same spin, [m+1,2m+1] opposite)
 };
 
@@ -84,9 +85,9 @@ __device__ __forceinline__ void load_table(const EvalParams &p, Coef4<T> *tab) {
 // Functor constants of one source group for the current walker.
 template <typename T>
 struct GroupC {
-    typename Traits<T>::U row;        // first table row of the group's functor - MAGIC_BITS
+    uint32_t base;                    // shared address of the group's row 0 minus MAGIC_BITS*sizeof(Coef4)
     T invd;                           // 1/delta
-    typename Traits<T>::U clamp;      // first row + m (the group's zero row)
+    typename Traits<T>::U clamp;      // MAGIC_BITS + m (the group's zero row)
     double sg, sh, ss;                // fp64 flush scales: G = sg*acc, L = sh*acc_h + ss*acc_s
 };
 
@@ -96,25 +97,30 @@ __device__ __forceinline__ int src_group(const EvalParams &p, int64_t gi) {
     return g;
 }
 
-// kg: group (spin half) of the walker's active electron (J2).
-template <typename T>
-__device__ __forceinline__ GroupC<T> group_consts(const EvalParams &p, int g, int kg, uint32_t /*tab_addr*/) {
+// kg: group (spin half) of the walker's active electron (J2).  MODE is a
+// template parameter so that, for J2, 1/delta and m are kernel-parameter
+// constants and the base a select between two precomputed values: all
+// warp-uniform, so they live in uniform registers and the hot loop keeps its
+// regular registers for data.
+template <typename T, int MODE>
+__device__ __forceinline__ GroupC<T> group_consts(const EvalParams &p, int g, int kg, uint32_t tab_addr) {
     using Tr = Traits<T>;
+    const uint32_t magic_off = (uint32_t)(Tr::MAGIC_BITS * (typename Tr::U)sizeof(Coef4<T>));
     GroupC<T> c;
-    int row, m;
     double invd;
-    if (p.mode == MODE_J2) {
-        row = (g == kg) ? 0 : (p.m + 1);
-        m = p.m;
+    if constexpr (MODE == MODE_J2) {
+        const uint32_t base_same = tab_addr - magic_off;
+        const uint32_t base_opp = tab_addr + (uint32_t)((p.m + 1) * (int)sizeof(Coef4<T>)) - magic_off;
+        c.base = (g == kg) ? base_same : base_opp;
+        c.invd = sizeof(T) == 4 ? T(p.inv_delta_f) : T(p.inv_delta);
+        c.clamp = Tr::MAGIC_BITS + (typename Tr::U)p.m;
         invd = p.inv_delta;
     } else {
-        row = p.grp_tab[g];
-        m = p.grp_m[g];
+        c.base = tab_addr + (uint32_t)(p.grp_tab[g] * (int)sizeof(Coef4<T>)) - magic_off;
+        c.invd = T(p.grp_invd[g]);
+        c.clamp = Tr::MAGIC_BITS + (typename Tr::U)p.grp_m[g];
         invd = p.grp_invd[g];
     }
-    c.row = (typename Tr::U)row - Tr::MAGIC_BITS;       // see functor_from_t
-    c.invd = T(invd);
-    c.clamp = (typename Tr::U)(row + m);
     c.sg = -invd;
     c.sh = 2.0 * invd * invd;
     c.ss = 2.0 * invd;
@@ -130,11 +136,11 @@ template <typename T> struct Trial { Axis<T> ax, ay, az; };
 // source's 1/delta (per-source groups in a masked J1 sub-tile).
 template <typename T, bool PHYS = false>
 __device__ __forceinline__ T accumulate(T dx, T dy, T dz, T r2, T inv_delta, uint32_t tab_base,
-                                        typename Traits<T>::U row, typename Traits<T>::U clamp_bits, T *acc) {
+                                        typename Traits<T>::U clamp_bits, T *acc) {
     using Tr = Traits<T>;
     const T ir = Tr::rsqrt(r2);
     const T r = r2 * ir;
-    const FunctorEval<T> e = functor_from_t<T>(r * inv_delta, tab_base, row, clamp_bits);
+    const FunctorEval<T> e = functor_from_t<T>(r * inv_delta, tab_base, clamp_bits);
     T g = e.du * ir;
     T h = e.h;
     if (PHYS) {
@@ -186,7 +192,7 @@ struct SubMask {
 // the source's group picks the functor.  J2 groups share delta, so only the
 // table row changes (raw accumulation); J1 groups differ in delta, so GEN
 // sub-tiles accumulate physical units (PHYS).
-template <typename T, int PB, bool ROW, int PF, bool GEN, int NT = TPB>
+template <typename T, int PB, bool ROW, int PF, bool GEN, int NT, int MODE>
 __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, uint32_t tab_addr,
                                          const typename Traits<T>::V *__restrict__ px,
                                          const typename Traits<T>::V *__restrict__ py,
@@ -197,7 +203,6 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
     using Tr = Traits<T>;
     using V = typename Tr::V;
     constexpr int VW = Tr::VW;
-    const uint32_t tab_base = tab_addr;
     const int vmax = GEN ? (mk.len - 1) / VW : 0;
     auto voff = [&](int j) -> int {
         return GEN ? min(j * NT + tid, vmax) - tid : j * NT;   // relative to this thread's vector
@@ -222,9 +227,6 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
 #pragma unroll
             for (int e = 0; e < VW; ++e) {
                 bool dead = false;
-                typename Tr::U row = gc.row;
-                T invd = gc.invd;
-                typename Tr::U clamp = gc.clamp;
                 if (GEN) {
                     const int li = rel + e;
                     dead = (li >= mk.len) || (li == mk.k_rel);
@@ -238,7 +240,7 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
                         const T dz = min_image_k<T, -1>(z, tr[q].az);
                         T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
                         if (GEN) r2 = dead ? T(1e30) : r2;
-                        const T r = accumulate<T>(dx, dy, dz, r2, invd, tab_base, row, clamp, acc[q]);
+                        const T r = accumulate<T>(dx, dy, dz, r2, gc.invd, gc.base, gc.clamp, acc[q]);
                         if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
                     }
                 }
@@ -259,7 +261,7 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
 // the instruction footprint of the hot loop small.  The group is looked up
 // per source and the terms are accumulated in physical units (PHYS) because
 // J1 species differ in delta.
-template <typename T, int PB, bool ROW, int NT>
+template <typename T, int PB, bool ROW, int NT, int MODE>
 __device__ __noinline__ void tile_multi(int tid, const EvalParams &p, int kg, uint32_t tab_addr,
                                         const typename Traits<T>::V *__restrict__ px,
                                         const typename Traits<T>::V *__restrict__ py,
@@ -279,7 +281,7 @@ __device__ __noinline__ void tile_multi(int tid, const EvalParams &p, int kg, ui
         for (int e = 0; e < VW; ++e) {
             const int li = rel + e;
             const bool dead = (li >= mk.len) || (li == mk.k_rel);
-            const GroupC<T> ge = group_consts<T>(p, src_group(p, mk.g0 + li), kg, tab_addr);
+            const GroupC<T> ge = group_consts<T, MODE>(p, src_group(p, mk.g0 + li), kg, tab_addr);
             const T x = Tr::comp(vx, e), y = Tr::comp(vy, e), z = Tr::comp(vz, e);
 #pragma unroll
             for (int q = 0; q < PB; ++q) {
@@ -289,7 +291,7 @@ __device__ __noinline__ void tile_multi(int tid, const EvalParams &p, int kg, ui
                     const T dz = min_image(z, tr[q].az);
                     T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
                     r2 = dead ? T(1e30) : r2;
-                    const T r = accumulate<T, true>(dx, dy, dz, r2, ge.invd, tab_addr, ge.row, ge.clamp, acc + q * NACC);
+                    const T r = accumulate<T, true>(dx, dy, dz, r2, ge.invd, ge.base, ge.clamp, acc + q * NACC);
                     if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
                 }
             }
@@ -319,7 +321,7 @@ __device__ __forceinline__ void flush(T (&acc)[PB][NACC], double (&dacc)[PB][NOU
 
 // Process the sub-tile [sstart, send) (local indices) of one walker for a team
 // of NT threads: classify, run the clean or the masked loop, flush to fp64.
-template <typename T, int PB, bool ROW, int PF, int NT>
+template <typename T, int PB, bool ROW, int PF, int NT, int MODE>
 __device__ __forceinline__ void sub_tile(int tid, const EvalParams &p, int kg, uint32_t tab_addr,
                                          int64_t sstart, int64_t send, int64_t k_local,
                                          const typename Traits<T>::V *px, const typename Traits<T>::V *py,
@@ -340,26 +342,28 @@ __device__ __forceinline__ void sub_tile(int tid, const EvalParams &p, int kg, u
     mk.len = (int)(send - sstart);
     mk.k_rel = k_in ? (int)(k_local - sstart) : -1;
     mk.g0 = g0;
-    const GroupC<T> gc = group_consts<T>(p, grp, kg, tab_addr);
+    const GroupC<T> gc = group_consts<T, MODE>(p, grp, kg, tab_addr);
     if (mk.len == SCH && !k_in && one_group) {                 // clean
-        tile_run<T, PB, ROW, PF, false, NT>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp, row_stride);
+        tile_run<T, PB, ROW, PF, false, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp,
+                                                  row_stride);
         flush<T, PB>(acc, dacc, gc.sg, gc.sh, gc.ss);
     } else if (one_group) {                                    // ragged and/or holds k
-        tile_run<T, PB, ROW, PF, true, NT>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp, row_stride);
+        tile_run<T, PB, ROW, PF, true, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp,
+                                                 row_stride);
         flush<T, PB>(acc, dacc, gc.sg, gc.sh, gc.ss);
     } else {                                                   // straddles a group boundary
-        tile_multi<T, PB, ROW, NT>(tid, p, kg, tab_addr, px, py, pz, tr, np, mk, &acc[0][0], rp, row_stride);
+        tile_multi<T, PB, ROW, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, np, mk, &acc[0][0], rp, row_stride);
         flush<T, PB>(acc, dacc, -1.0, 1.0, 2.0);
     }
 }
 
 // Per-walker setup shared by the CTA and warp kernels.
-template <typename T, int PB>
+template <typename T, int PB, int MODE>
 __device__ __forceinline__ void walker_setup(const EvalParams &p, int64_t w, int32_t p0, int np,
                                              Trial<T> (&tr)[PB], int &kg, int64_t &k_local) {
-    const int64_t kw = p.mode == MODE_J2 ? (int64_t)p.k[w] : -1;
-    kg = (p.mode == MODE_J2 && kw >= p.N_up) ? 1 : 0;
-    k_local = p.mode == MODE_J2 ? kw - p.i_offset : -1;
+    const int64_t kw = MODE == MODE_J2 ? (int64_t)p.k[w] : -1;
+    kg = (MODE == MODE_J2 && kw >= p.N_up) ? 1 : 0;
+    k_local = MODE == MODE_J2 ? kw - p.i_offset : -1;
     const T L0 = T(p.L[0]), L1 = T(p.L[1]), L2 = T(p.L[2]);
 #pragma unroll
     for (int q = 0; q < PB; ++q) {
@@ -390,7 +394,8 @@ __device__ __forceinline__ void write_out(const EvalParams &p, int64_t w, int32_
 // Long rows: one CTA per (walker, trial group, tile of SUB sub-tiles).
 // PF: prefetch distance (vector groups in flight), MINB: resident CTAs per SM.
 // ===========================================================================
-template <typename T, int PB, bool ROW, int PF = 1, int MINB = ((sizeof(T) == 4 && PB == 1) ? 4 : 2)>
+template <typename T, int PB, bool ROW, int PF = 1, int MINB = ((sizeof(T) == 4 && PB == 1) ? 4 : 2),
+          int MODE = MODE_J2>
 __global__ void __launch_bounds__(TPB, MINB)
 j2_eval_kernel(const __grid_constant__ EvalParams p) {
     using Tr = Traits<T>;
@@ -419,7 +424,7 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
     Trial<T> tr[PB];
     int kg;
     int64_t k_local;
-    walker_setup<T, PB>(p, w, p0, np, tr, kg, k_local);
+    walker_setup<T, PB, MODE>(p, w, p0, np, tr, kg, k_local);
     const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tab);
 
     const int64_t start = c * CH;
@@ -452,8 +457,8 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
         V *rp[PB];
 #pragma unroll
         for (int q = 0; q < PB; ++q) rp[q] = ROW ? rowp[q] + vs : nullptr;
-        sub_tile<T, PB, ROW, PF, TPB>(threadIdx.x, p, kg, tab_addr, sstart, send, k_local, px + vs, py + vs,
-                                      pz + vs, tr, np, dacc, rp, row_stride);
+        sub_tile<T, PB, ROW, PF, TPB, MODE>(threadIdx.x, p, kg, tab_addr, sstart, send, k_local, px + vs, py + vs,
+                                            pz + vs, tr, np, dacc, rp, row_stride);
     }
 
     // ---- CTA reduction in fp64 (fixed order: deterministic) ----
@@ -519,7 +524,8 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
 // (deterministic) reduction: no shared-memory reduction, no cross-CTA
 // partials, no counters.
 // ===========================================================================
-template <typename T, int PB, bool ROW, int PF, int MINB = (sizeof(T) == 4 && PB == 1 && !ROW) ? 3 : 2>
+template <typename T, int PB, bool ROW, int PF, int MINB = (sizeof(T) == 4 && PB == 1 && !ROW) ? 3 : 2,
+          int MODE = MODE_J2>
 __global__ void __launch_bounds__(TPB, MINB)
 j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
     using Tr = Traits<T>;
@@ -539,7 +545,7 @@ j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
     Trial<T> tr[PB];
     int kg;
     int64_t k_local;
-    walker_setup<T, PB>(p, w, p0, np, tr, kg, k_local);
+    walker_setup<T, PB, MODE>(p, w, p0, np, tr, kg, k_local);
     const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tab);
     const T *Rw = static_cast<const T *>(p.R) + w * p.src_stride;
     const int64_t row_stride = p.Np / VW;
@@ -561,8 +567,8 @@ j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
         for (int q = 0; q < PB; ++q)
             rp[q] = ROW ? reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + p0 + (q < np ? q : 0)) * 4) * p.Np) + voff
                         : nullptr;
-        sub_tile<T, PB, ROW, PF, 32>(lane, p, kg, tab_addr, sstart, send, k_local, px, py, pz, tr, np, dacc, rp,
-                                     row_stride);
+        sub_tile<T, PB, ROW, PF, 32, MODE>(lane, p, kg, tab_addr, sstart, send, k_local, px, py, pz, tr, np, dacc, rp,
+                                           row_stride);
     }
 
     double V0 = 0.0;

@@ -129,7 +129,7 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
         Trial<T> tr[PB];
         int kg;
         int64_t k_local;
-        walker_setup<T, PB>(p, ti.w, p0, np, tr, kg, k_local);
+        walker_setup<T, PB, MODE_J2>(p, ti.w, p0, np, tr, kg, k_local);
         double dacc[PB][NOUT];
         T acc[PB][NACC];
 #pragma unroll
@@ -156,7 +156,7 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
             const int grp = src_group(p, g0);
             const bool one_group = src_group(p, s0 + len - 1 + p.i_offset) == grp;
             const bool k_in = k_local >= s0 && k_local < s0 + len;
-            const GroupC<T> gc = group_consts<T>(p, grp, kg, tab_addr);
+            const GroupC<T> gc = group_consts<T, MODE_J2>(p, grp, kg, tab_addr);
 #pragma unroll
             for (int q = 0; q < PB; ++q)
 #pragma unroll
@@ -169,7 +169,7 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
                 for (int e = 0; e < VW; ++e) {
                     const int li = rel + e;
                     const bool dead = (li >= len) || (k_in && li == (int)(k_local - s0));
-                    const GroupC<T> ge = one_group ? gc : group_consts<T>(p, src_group(p, g0 + li), kg, tab_addr);
+                    const GroupC<T> ge = one_group ? gc : group_consts<T, MODE_J2>(p, src_group(p, g0 + li), kg, tab_addr);
                     const T x = Tr::comp(cx[u], e), y = Tr::comp(cy[u], e), z = Tr::comp(cz[u], e);
 #pragma unroll
                     for (int q = 0; q < PB; ++q) {
@@ -179,7 +179,7 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
                             const T dz = min_image(z, tr[q].az);
                             T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
                             r2 = dead ? T(1e30) : r2;
-                            accumulate<T>(dx, dy, dz, r2, gc.invd, tab_addr, ge.row, ge.clamp, acc[q]);
+                            accumulate<T>(dx, dy, dz, r2, gc.invd, ge.base, ge.clamp, acc[q]);
                         }
                     }
                 }

@@ -57,42 +57,43 @@ inline bool use_warp_mapping(const EvalParams &p) {
     return p.tiles_per_walker == 1 && (p.W * p.n_groups >= 4096 || p.N_local <= 2048);
 }
 
-template <typename T, int PB>
+template <typename T, int PB, int MODE>
 cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStream_t s) {
     if (use_warp_mapping(p)) {
         const int64_t units = p.W * p.n_groups;
         const unsigned nbw = (unsigned)((units + TPB / 32 - 1) / (TPB / 32));
-        if (row) j2_eval_warp_kernel<T, PB, true, 1><<<nbw, TPB, 0, s>>>(p, units);
-        else     j2_eval_warp_kernel<T, PB, false, 2><<<nbw, TPB, 0, s>>>(p, units);
+        constexpr int MB = (sizeof(T) == 4 && PB == 1) ? 3 : 2;
+        if (row) j2_eval_warp_kernel<T, PB, true, 1, 2, MODE><<<nbw, TPB, 0, s>>>(p, units);
+        else     j2_eval_warp_kernel<T, PB, false, 2, MB, MODE><<<nbw, TPB, 0, s>>>(p, units);
         return cudaGetLastError();
     }
-    const int kc = (row || p.mode != MODE_J2) ? -1 : kernel_choice();
-    if constexpr (PB == 1) {
-        if (kc == 0) return launch_tma<T, PB, 3, 2, 3>(p, nblocks, s);
-    }
-    const char *e = getenv("QJ2_KERNEL");
     const unsigned nb = (unsigned)nblocks;
+    if constexpr (MODE == MODE_J2 && PB == 1) {
+        if (!row && kernel_choice() == 0) return launch_tma<T, PB, 3, 2, 3>(p, nblocks, s);
+    }
+    constexpr int MB0 = (sizeof(T) == 4 && PB == 1) ? 4 : 2;
     if (row) {
-        j2_eval_kernel<T, PB, true><<<nb, TPB, 0, s>>>(p);
+        j2_eval_kernel<T, PB, true, 1, MB0, MODE><<<nb, TPB, 0, s>>>(p);
     } else if constexpr (PB == 1 && sizeof(T) == 4) {
-        if (e && strcmp(e, "ldg1") == 0)       // A/B: prefetch distance 1, 4 CTAs/SM
-            j2_eval_kernel<T, PB, false, 1, 4><<<nb, TPB, 0, s>>>(p);
+        const char *e = getenv("QJ2_KERNEL");
+        if (MODE == MODE_J2 && e && strcmp(e, "ldg1") == 0)   // A/B: prefetch distance 1, 4 CTAs/SM
+            j2_eval_kernel<T, PB, false, 1, 4, MODE><<<nb, TPB, 0, s>>>(p);
         else    // default: two vector groups in flight per thread, 3 CTAs/SM (80 registers);
-                // measured best on B200 (DESIGN.md section 9)
-            j2_eval_kernel<T, PB, false, 2, 3><<<nb, TPB, 0, s>>>(p);
+                // measured best on B200 (DESIGN.md section 7)
+            j2_eval_kernel<T, PB, false, 2, 3, MODE><<<nb, TPB, 0, s>>>(p);
     } else if constexpr (PB == 1) {             // fp64: two groups in flight, 2 CTAs/SM
-        j2_eval_kernel<T, PB, false, 2, 2><<<nb, TPB, 0, s>>>(p);
+        j2_eval_kernel<T, PB, false, 2, 2, MODE><<<nb, TPB, 0, s>>>(p);
     } else {
-        j2_eval_kernel<T, PB, false><<<nb, TPB, 0, s>>>(p);
+        j2_eval_kernel<T, PB, false, 1, MB0, MODE><<<nb, TPB, 0, s>>>(p);
     }
     return cudaGetLastError();
 }
 
-
-// Per translation unit entry points (see launch_*.cu).
-cudaError_t launch_f32_pb1(const EvalParams &p, int64_t nblocks, bool row, cudaStream_t s);
-cudaError_t launch_f32_pbn(const EvalParams &p, int pb, int64_t nblocks, bool row, cudaStream_t s);
-cudaError_t launch_f64_pb1(const EvalParams &p, int64_t nblocks, bool row, cudaStream_t s);
-cudaError_t launch_f64_pbn(const EvalParams &p, int pb, int64_t nblocks, bool row, cudaStream_t s);
+// Per translation unit entry points (see launch_*.cu): <dtype>_<trial batch>_<mode>.
+#define QJ2_DECL(NAME) \
+    cudaError_t NAME(const EvalParams &p, int pb, int64_t nblocks, bool row, cudaStream_t s);
+QJ2_DECL(launch_f32_pb1_j2) QJ2_DECL(launch_f32_pbn_j2) QJ2_DECL(launch_f64_pb1_j2) QJ2_DECL(launch_f64_pbn_j2)
+QJ2_DECL(launch_f32_pb1_j1) QJ2_DECL(launch_f32_pbn_j1) QJ2_DECL(launch_f64_pb1_j1) QJ2_DECL(launch_f64_pbn_j1)
+#undef QJ2_DECL
 
 }  // namespace qj2

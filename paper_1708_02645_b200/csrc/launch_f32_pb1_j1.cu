@@ -1,0 +1,12 @@
+// launch_f32_pb1_j1.cu -- kernel instantiations for one dtype / trial-batch size /
+// mode (separate translation unit so the build compiles them in parallel).
+#include "launch.cuh"
+
+namespace qj2 {
+
+cudaError_t launch_f32_pb1_j1(const EvalParams &p, int pb, int64_t nblocks, bool row, cudaStream_t s) {
+    (void)pb;
+    return launch_eval<float, 1, MODE_J1>(p, nblocks, row, s);
+}
+
+}  // namespace qj2

@@ -58,10 +58,10 @@ __global__ void vgl_kernel(const __grid_constant__ VglParams p, const T *__restr
     __syncthreads();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= p.n) return;
-    const uint32_t base = (uint32_t)__cvta_generic_to_shared(tab);
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(tab) -
+                          (uint32_t)(Tr::MAGIC_BITS * (typename Tr::U)sizeof(Coef4<T>));
     const T id = T(p.inv_delta);
-    const FunctorEval<T> e = functor_from_t<T>(r[i] * id, base, (typename Tr::U)0 - Tr::MAGIC_BITS,
-                                               (typename Tr::U)p.m);
+    const FunctorEval<T> e = functor_from_t<T>(r[i] * id, base, Tr::MAGIC_BITS + (typename Tr::U)p.m);
     out[i * 3 + 0] = (double)e.u;
     out[i * 3 + 1] = (double)e.du * p.inv_delta;
     out[i * 3 + 2] = 2.0 * (double)e.h * p.inv_delta * p.inv_delta;
@@ -209,10 +209,14 @@ qj2_status launch_common(EvalParams &p, qj2_dtype dtype, int pb, int64_t ng, voi
         e = cudaMemsetAsync(p.counters, 0, (size_t)p.W * ng * sizeof(unsigned), stream);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counters)");
     }
-    if (dtype == QJ2_FP32)
-        e = pb == 1 ? launch_f32_pb1(p, nblocks, row, stream) : launch_f32_pbn(p, pb, nblocks, row, stream);
-    else
-        e = pb == 1 ? launch_f64_pb1(p, nblocks, row, stream) : launch_f64_pbn(p, pb, nblocks, row, stream);
+    const bool j1 = p.mode == MODE_J1;
+    if (dtype == QJ2_FP32) {
+        if (pb == 1) e = j1 ? launch_f32_pb1_j1(p, pb, nblocks, row, stream) : launch_f32_pb1_j2(p, pb, nblocks, row, stream);
+        else         e = j1 ? launch_f32_pbn_j1(p, pb, nblocks, row, stream) : launch_f32_pbn_j2(p, pb, nblocks, row, stream);
+    } else {
+        if (pb == 1) e = j1 ? launch_f64_pb1_j1(p, pb, nblocks, row, stream) : launch_f64_pb1_j2(p, pb, nblocks, row, stream);
+        else         e = j1 ? launch_f64_pbn_j1(p, pb, nblocks, row, stream) : launch_f64_pbn_j2(p, pb, nblocks, row, stream);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "j2_eval_kernel launch");
     return QJ2_OK;
 }
@@ -257,6 +261,7 @@ qj2_status eval_impl(const qj2_functor *fn, qj2_dtype dtype,
     p.V_cur = V_cur; p.ratio_out = ratio_out;
     for (int d = 0; d < 3; ++d) p.L[d] = fn->L[d];
     p.inv_delta = (double)fn->m / fn->r_cut;
+    p.inv_delta_f = (float)p.inv_delta;
     power_basis(fn->coef[0], fn->m, p.pcoef);                  // rows [0, m]: same spin
     power_basis(fn->coef[1], fn->m, p.pcoef + (fn->m + 1));    // rows [m+1, 2m+1]: opposite spin
     p.n_tab = 2 * (fn->m + 1);
