@@ -59,14 +59,15 @@ class _J1Functor(ctypes.Structure):
 
 
 def lib_path() -> str:
-    return _build.LIB
+    return os.environ.get("QJ2_LIB") or _build.LIB
 
 
 def _load():
-    if not os.path.exists(_build.LIB):
-        raise ImportError(f"{_build.LIB} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+    path = lib_path()   # QJ2_LIB: load another build of the library (A/B measurements)
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
                           "(no CPU fallback exists)")
-    lib = ctypes.CDLL(_build.LIB)
+    lib = ctypes.CDLL(path)
     i64, i32, vp, dp = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)
     F = ctypes.POINTER(_Functor)
     sz = ctypes.c_size_t
@@ -92,6 +93,8 @@ def _load():
                                             ctypes.c_double, vp, vp]),
     }
     for name, (res, args) in sigs.items():
+        if not hasattr(lib, name) and os.environ.get("QJ2_LIB"):
+            continue          # an older A/B build may lack newer entry points
         fnc = getattr(lib, name)
         fnc.restype = res
         fnc.argtypes = args
