@@ -262,12 +262,13 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
 // per source and the terms are accumulated in physical units (PHYS) because
 // J1 species differ in delta.
 template <typename T, int PB, bool ROW, int NT, int MODE>
-__device__ __noinline__ void tile_multi(int tid, const EvalParams &p, int kg, uint32_t tab_addr,
-                                        const typename Traits<T>::V *__restrict__ px,
-                                        const typename Traits<T>::V *__restrict__ py,
-                                        const typename Traits<T>::V *__restrict__ pz,
-                                        const Trial<T> *tr, int np, const SubMask &mk, T *acc /* [PB][NACC] */,
-                                        typename Traits<T>::V *const *rowp, int64_t row_stride) {
+__device__ __forceinline__ void tile_multi(int tid, const EvalParams &p, int kg, uint32_t tab_addr,
+                                           const typename Traits<T>::V *__restrict__ px,
+                                           const typename Traits<T>::V *__restrict__ py,
+                                           const typename Traits<T>::V *__restrict__ pz,
+                                           const Trial<T> (&tr)[PB], int np, const SubMask &mk,
+                                           T (&acc)[PB][NACC],
+                                           typename Traits<T>::V *const (&rowp)[PB], int64_t row_stride) {
     using Tr = Traits<T>;
     using V = typename Tr::V;
     constexpr int VW = Tr::VW;
@@ -281,7 +282,8 @@ __device__ __noinline__ void tile_multi(int tid, const EvalParams &p, int kg, ui
         for (int e = 0; e < VW; ++e) {
             const int li = rel + e;
             const bool dead = (li >= mk.len) || (li == mk.k_rel);
-            const GroupC<T> ge = group_consts<T, MODE>(p, src_group(p, mk.g0 + li), kg, tab_addr);
+            const int gsrc = MODE == MODE_J2 ? (mk.g0 + li >= p.N_up ? 1 : 0) : src_group(p, mk.g0 + li);
+            const GroupC<T> ge = group_consts<T, MODE>(p, gsrc, kg, tab_addr);
             const T x = Tr::comp(vx, e), y = Tr::comp(vy, e), z = Tr::comp(vz, e);
 #pragma unroll
             for (int q = 0; q < PB; ++q) {
@@ -291,7 +293,7 @@ __device__ __noinline__ void tile_multi(int tid, const EvalParams &p, int kg, ui
                     const T dz = min_image(z, tr[q].az);
                     T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
                     r2 = dead ? T(1e30) : r2;
-                    const T r = accumulate<T, true>(dx, dy, dz, r2, ge.invd, ge.base, ge.clamp, acc + q * NACC);
+                    const T r = accumulate<T, true>(dx, dy, dz, r2, ge.invd, ge.base, ge.clamp, acc[q]);
                     if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
                 }
             }
@@ -335,8 +337,15 @@ __device__ __forceinline__ void sub_tile(int tid, const EvalParams &p, int kg, u
 #pragma unroll
         for (int a = 0; a < NACC; ++a) acc[q][a] = T(0);
     const int64_t g0 = sstart + p.i_offset;                 // global index of the first source
-    const int grp = src_group(p, g0);
-    const bool one_group = src_group(p, send - 1 + p.i_offset) == grp;
+    int grp;
+    bool one_group;
+    if constexpr (MODE == MODE_J2) {                        // two spin halves: one compare each
+        grp = g0 >= p.N_up ? 1 : 0;
+        one_group = (send - 1 + p.i_offset >= p.N_up ? 1 : 0) == grp;
+    } else {
+        grp = src_group(p, g0);
+        one_group = src_group(p, send - 1 + p.i_offset) == grp;
+    }
     const bool k_in = k_local >= sstart && k_local < send;
     SubMask mk;
     mk.len = (int)(send - sstart);
@@ -352,7 +361,7 @@ __device__ __forceinline__ void sub_tile(int tid, const EvalParams &p, int kg, u
                                                  row_stride);
         flush<T, PB>(acc, dacc, gc.sg, gc.sh, gc.ss);
     } else {                                                   // straddles a group boundary
-        tile_multi<T, PB, ROW, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, np, mk, &acc[0][0], rp, row_stride);
+        tile_multi<T, PB, ROW, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, np, mk, acc, rp, row_stride);
         flush<T, PB>(acc, dacc, -1.0, 1.0, 2.0);
     }
 }
