@@ -30,6 +30,11 @@ constexpr int MAXTAB = MAXG * (QJ2_MAX_M + 1);
 
 enum { MODE_J2 = 0, MODE_J1 = 1 };
 
+// fp64 accumulators per trial: J2 keeps the 6 raw sums (one delta for every
+// group: scaled once at the end); J1 keeps 5 physical values (species differ
+// in delta: scaled at every sub-tile flush).
+template <int MODE> __host__ __device__ constexpr int ndacc() { return MODE == MODE_J2 ? NACC : NOUT; }
+
 // ---------------------------------------------------------------------------
 // Kernel parameters (by value, __grid_constant__).
 // ---------------------------------------------------------------------------
@@ -53,7 +58,7 @@ struct EvalParams {
     void *row_out;
     const double *V_cur;
     double *ratio_out;
-    double *partials;             // [W][n_groups][tiles][PB][NOUT]
+    double *partials;             // [W][n_groups][tiles][PB][ndacc]
     unsigned int *counters;       // [W][n_groups]
     double L[3];
     double inv_delta;             // J2: 1/delta
@@ -293,7 +298,7 @@ __device__ __forceinline__ void tile_multi(int tid, const EvalParams &p, int kg,
                     const T dz = min_image(z, tr[q].az);
                     T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
                     r2 = dead ? T(1e30) : r2;
-                    const T r = accumulate<T, true>(dx, dy, dz, r2, ge.invd, ge.base, ge.clamp, acc[q]);
+                    const T r = accumulate<T, MODE == MODE_J1>(dx, dy, dz, r2, ge.invd, ge.base, ge.clamp, acc[q]);
                     if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
                 }
             }
@@ -308,16 +313,39 @@ __device__ __forceinline__ void tile_multi(int tid, const EvalParams &p, int kg,
     }
 }
 
-// Flush a sub-tile's T partials into the fp64 physical accumulators.
-template <typename T, int PB>
-__device__ __forceinline__ void flush(T (&acc)[PB][NACC], double (&dacc)[PB][NOUT], double sg, double sh, double ss) {
+// Flush a sub-tile's T partials into the fp64 accumulators: raw for J2,
+// physical (scaled by the sub-tile group's delta factors) for J1.
+template <typename T, int PB, int MODE>
+__device__ __forceinline__ void flush(T (&acc)[PB][NACC], double (&dacc)[PB][ndacc<MODE>()], double sg, double sh,
+                                      double ss) {
 #pragma unroll
     for (int q = 0; q < PB; ++q) {
-        dacc[q][0] += (double)acc[q][0];
-        dacc[q][1] += sg * (double)acc[q][1];
-        dacc[q][2] += sg * (double)acc[q][2];
-        dacc[q][3] += sg * (double)acc[q][3];
-        dacc[q][4] += sh * (double)acc[q][4] + ss * (double)acc[q][5];
+        if constexpr (MODE == MODE_J2) {
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) dacc[q][a] += (double)acc[q][a];
+        } else {
+            dacc[q][0] += (double)acc[q][0];
+            dacc[q][1] += sg * (double)acc[q][1];
+            dacc[q][2] += sg * (double)acc[q][2];
+            dacc[q][3] += sg * (double)acc[q][3];
+            dacc[q][4] += sh * (double)acc[q][4] + ss * (double)acc[q][5];
+        }
+    }
+}
+
+// Physical (V, G, L) of one trial from the reduced fp64 accumulators.
+template <int MODE>
+__device__ __forceinline__ void to_physical(const EvalParams &p, const double *s, double (&o)[NOUT]) {
+    if constexpr (MODE == MODE_J2) {
+        const double id = p.inv_delta;
+        o[0] = s[0];
+        o[1] = -id * s[1];
+        o[2] = -id * s[2];
+        o[3] = -id * s[3];
+        o[4] = 2.0 * id * id * s[4] + 2.0 * id * s[5];
+    } else {
+#pragma unroll
+        for (int a = 0; a < NOUT; ++a) o[a] = s[a];
     }
 }
 
@@ -328,7 +356,7 @@ __device__ __forceinline__ void sub_tile(int tid, const EvalParams &p, int kg, u
                                          int64_t sstart, int64_t send, int64_t k_local,
                                          const typename Traits<T>::V *px, const typename Traits<T>::V *py,
                                          const typename Traits<T>::V *pz, const Trial<T> (&tr)[PB], int np,
-                                         double (&dacc)[PB][NOUT],
+                                         double (&dacc)[PB][ndacc<MODE>()],
                                          typename Traits<T>::V *const (&rp)[PB], int64_t row_stride) {
     constexpr int SCH = NT * Traits<T>::VW * ITERS;
     T acc[PB][NACC];
@@ -355,14 +383,15 @@ __device__ __forceinline__ void sub_tile(int tid, const EvalParams &p, int kg, u
     if (mk.len == SCH && !k_in && one_group) {                 // clean
         tile_run<T, PB, ROW, PF, false, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp,
                                                   row_stride);
-        flush<T, PB>(acc, dacc, gc.sg, gc.sh, gc.ss);
+        flush<T, PB, MODE>(acc, dacc, gc.sg, gc.sh, gc.ss);
     } else if (one_group) {                                    // ragged and/or holds k
         tile_run<T, PB, ROW, PF, true, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp,
                                                  row_stride);
-        flush<T, PB>(acc, dacc, gc.sg, gc.sh, gc.ss);
+        flush<T, PB, MODE>(acc, dacc, gc.sg, gc.sh, gc.ss);
     } else {                                                   // straddles a group boundary
         tile_multi<T, PB, ROW, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, np, mk, acc, rp, row_stride);
-        flush<T, PB>(acc, dacc, -1.0, 1.0, 2.0);
+        if constexpr (MODE == MODE_J2) flush<T, PB, MODE>(acc, dacc, gc.sg, gc.sh, gc.ss);   // shared delta: raw
+        else flush<T, PB, MODE>(acc, dacc, -1.0, 1.0, 2.0);                                  // already physical
     }
 }
 
@@ -385,10 +414,12 @@ __device__ __forceinline__ void walker_setup(const EvalParams &p, int64_t w, int
 }
 
 // Write the physical totals (lane 0 holds them) and the fused ratio.
-template <int PB>
+template <int PB, int MODE>
 __device__ __forceinline__ void write_out(const EvalParams &p, int64_t w, int32_t p0, int np, int q,
-                                          const double (&s)[NOUT], double V0) {
+                                          const double *sraw, double V0) {
     if (q >= np) return;
+    double s[NOUT];
+    to_physical<MODE>(p, sraw, s);
     const int64_t o = w * p.P + p0 + q;
 #pragma unroll
     for (int a = 0; a < NOUT; ++a) p.out[o * 5 + a] = s[a];
@@ -412,8 +443,9 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
     constexpr int VW = Tr::VW;
     constexpr int SCH = TPB * VW * ITERS;         // sub-tile: 32 terms per thread
     constexpr int CH = SCH * SUB;                 // tile handled by one CTA
+    constexpr int ND = ndacc<MODE>();
     __shared__ Coef4<T> tab[MAXTAB];
-    __shared__ double red[TPB / 32][PB * NOUT];
+    __shared__ double red[TPB / 32][PB * ND];
     __shared__ int last_flag;
 
     // tile decode: chunk fastest so consecutive CTAs stream consecutive memory
@@ -451,11 +483,11 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
     const int64_t row_stride = p.Np / VW;
     __syncthreads();
 
-    double dacc[PB][NOUT];
+    double dacc[PB][ND];
 #pragma unroll
     for (int q = 0; q < PB; ++q)
 #pragma unroll
-        for (int a = 0; a < NOUT; ++a) dacc[q][a] = 0.0;
+        for (int a = 0; a < ND; ++a) dacc[q][a] = 0.0;
 
 #pragma unroll 1
     for (int sidx = 0; sidx < SUB; ++sidx) {
@@ -475,14 +507,14 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
 #pragma unroll
     for (int q = 0; q < PB; ++q)
 #pragma unroll
-        for (int a = 0; a < NOUT; ++a) {
+        for (int a = 0; a < ND; ++a) {
             const double v = warp_sum(dacc[q][a]);
-            if (lane == 0) red[warp][q * NOUT + a] = v;
+            if (lane == 0) red[warp][q * ND + a] = v;
         }
     __syncthreads();
 
-    double tot = 0.0;   // thread t < PB*NOUT holds value t of this tile
-    if (threadIdx.x < PB * NOUT) {
+    double tot = 0.0;   // thread t < PB*ND holds value t of this tile
+    if (threadIdx.x < PB * ND) {
 #pragma unroll
         for (int wi = 0; wi < TPB / 32; ++wi) tot += red[wi][threadIdx.x];
     }
@@ -490,8 +522,8 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
     const int64_t wg = w * p.n_groups + g;
     if (tpw > 1) {
         // publish this tile's partials; the last CTA of (w, g) reduces them
-        double *part = p.partials + (wg * tpw + c) * (PB * NOUT);
-        if (threadIdx.x < PB * NOUT) part[threadIdx.x] = tot;
+        double *part = p.partials + (wg * tpw + c) * (PB * ND);
+        if (threadIdx.x < PB * ND) part[threadIdx.x] = tot;
         __threadfence();
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -503,25 +535,25 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
         __threadfence();
         // warp 0: value v summed over tiles, lane-strided then shuffle tree
         if (warp == 0) {
-            const double *base = p.partials + wg * tpw * (PB * NOUT);
-            for (int v = 0; v < PB * NOUT; ++v) {
+            const double *base = p.partials + wg * tpw * (PB * ND);
+            for (int v = 0; v < PB * ND; ++v) {
                 double s = 0.0;
-                for (int64_t t = lane; t < tpw; t += 32) s += __ldcg(base + t * (PB * NOUT) + v);
+                for (int64_t t = lane; t < tpw; t += 32) s += __ldcg(base + t * (PB * ND) + v);
                 s = warp_sum(s);
-                if (lane == v) tot = s;      // lane v keeps value v (PB*NOUT <= 20 < 32)
+                if (lane == v) tot = s;      // lane v keeps value v (PB*ND <= 24 < 32)
             }
         }
     }
 
-    // ---- finalize: lane t < PB*NOUT of warp 0 holds value (q = t / NOUT, a = t % NOUT) ----
+    // ---- finalize: lane t < PB*ND of warp 0 holds value (q = t / ND, a = t % ND) ----
     if (warp == 0) {
         const double V0 = __shfl_sync(0xffffffffu, tot, 0);   // V of this group's first trial
 #pragma unroll
         for (int q = 0; q < PB; ++q) {
-            double s[NOUT];
+            double s[ND];
 #pragma unroll
-            for (int a = 0; a < NOUT; ++a) s[a] = __shfl_sync(0xffffffffu, tot, q * NOUT + a);
-            if (lane == 0) write_out<PB>(p, w, p0, np, q, s, V0);
+            for (int a = 0; a < ND; ++a) s[a] = __shfl_sync(0xffffffffu, tot, q * ND + a);
+            if (lane == 0) write_out<PB, MODE>(p, w, p0, np, q, s, V0);
         }
     }
 }
@@ -559,11 +591,12 @@ j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
     const T *Rw = static_cast<const T *>(p.R) + w * p.src_stride;
     const int64_t row_stride = p.Np / VW;
 
-    double dacc[PB][NOUT];
+    constexpr int ND = ndacc<MODE>();
+    double dacc[PB][ND];
 #pragma unroll
     for (int q = 0; q < PB; ++q)
 #pragma unroll
-        for (int a = 0; a < NOUT; ++a) dacc[q][a] = 0.0;
+        for (int a = 0; a < ND; ++a) dacc[q][a] = 0.0;
 
     for (int64_t sstart = 0; sstart < p.N_local; sstart += SCH) {
         const int64_t send = min(sstart + (int64_t)SCH, p.N_local);
@@ -583,11 +616,11 @@ j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
     double V0 = 0.0;
 #pragma unroll
     for (int q = 0; q < PB; ++q) {
-        double s[NOUT];
+        double s[ND];
 #pragma unroll
-        for (int a = 0; a < NOUT; ++a) s[a] = warp_sum(dacc[q][a]);
+        for (int a = 0; a < ND; ++a) s[a] = warp_sum(dacc[q][a]);
         if (q == 0) V0 = s[0];
-        if (lane == 0) write_out<PB>(p, w, p0, np, q, s, V0);
+        if (lane == 0) write_out<PB, MODE>(p, w, p0, np, q, s, V0);
     }
 }
 

@@ -77,7 +77,7 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
     V *ring = reinterpret_cast<V *>(smem);                                   // [NST][3][VPT*TPB]
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + TMA_NST * 3 * LANE_BYTES);  // full[NST], empty[NST]
     Coef4<T> *tab = reinterpret_cast<Coef4<T> *>(bars + 2 * TMA_NST);       // [MAXTAB]
-    double *red = reinterpret_cast<double *>(tab + MAXTAB);                 // [2][NCW][PB*NOUT]
+    double *red = reinterpret_cast<double *>(tab + MAXTAB);                 // [2][NCW][PB*NACC]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t bar_base = (uint32_t)__cvta_generic_to_shared(bars);
@@ -130,12 +130,12 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
         int kg;
         int64_t k_local;
         walker_setup<T, PB, MODE_J2>(p, ti.w, p0, np, tr, kg, k_local);
-        double dacc[PB][NOUT];
+        double dacc[PB][NACC];
         T acc[PB][NACC];
 #pragma unroll
         for (int q = 0; q < PB; ++q)
 #pragma unroll
-            for (int a = 0; a < NOUT; ++a) dacc[q][a] = 0.0;
+            for (int a = 0; a < NACC; ++a) dacc[q][a] = 0.0;
 
         for (int64_t s0 = ti.start; s0 < ti.end; s0 += SRC_STAGE, ++n) {
             const uint32_t slot = n % TMA_NST, round = n / TMA_NST;
@@ -184,31 +184,31 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
                     }
                 }
             }
-            flush<T, PB>(acc, dacc, gc.sg, gc.sh, gc.ss);   // J2 only: groups share delta
+            flush<T, PB, MODE_J2>(acc, dacc, gc.sg, gc.sh, gc.ss);   // J2 only: raw sums
         }
 
         // ---- CTA (consumer) reduction, double-buffered scratch ----
-        double *rb = red + parity_tile * (TMA_NCW * PB * NOUT);
+        double *rb = red + parity_tile * (TMA_NCW * PB * NACC);
 #pragma unroll
         for (int q = 0; q < PB; ++q)
 #pragma unroll
-            for (int a = 0; a < NOUT; ++a) {
+            for (int a = 0; a < NACC; ++a) {
                 const double v = warp_sum(dacc[q][a]);
-                if (lane == 0) rb[warp * (PB * NOUT) + q * NOUT + a] = v;
+                if (lane == 0) rb[warp * (PB * NACC) + q * NACC + a] = v;
             }
         named_bar(1, TPB);
         if (warp != 0) continue;
 
         // warp 0: tile total, publish, and (last CTA of the walker) finalize
         double tot = 0.0;
-        if (lane < PB * NOUT) {
+        if (lane < PB * NACC) {
 #pragma unroll
-            for (int wi = 0; wi < TMA_NCW; ++wi) tot += rb[wi * (PB * NOUT) + lane];
+            for (int wi = 0; wi < TMA_NCW; ++wi) tot += rb[wi * (PB * NACC) + lane];
         }
         const int64_t wg = ti.w * p.n_groups + ti.g;
         if (tpw > 1) {
-            double *part = p.partials + (wg * tpw + ti.c) * (PB * NOUT);
-            if (lane < PB * NOUT) part[lane] = tot;
+            double *part = p.partials + (wg * tpw + ti.c) * (PB * NACC);
+            if (lane < PB * NACC) part[lane] = tot;
             __threadfence();
             __syncwarp();
             unsigned last = 0;
@@ -216,10 +216,10 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
             last = __shfl_sync(0xffffffffu, last, 0);
             if (!last) continue;
             __threadfence();
-            const double *pb = p.partials + wg * tpw * (PB * NOUT);
-            for (int v = 0; v < PB * NOUT; ++v) {
+            const double *pb = p.partials + wg * tpw * (PB * NACC);
+            for (int v = 0; v < PB * NACC; ++v) {
                 double s = 0.0;
-                for (int64_t c = lane; c < tpw; c += 32) s += __ldcg(pb + c * (PB * NOUT) + v);
+                for (int64_t c = lane; c < tpw; c += 32) s += __ldcg(pb + c * (PB * NACC) + v);
                 s = warp_sum(s);
                 if (lane == v) tot = s;
             }
@@ -227,10 +227,10 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
         const double V0 = __shfl_sync(0xffffffffu, tot, 0);
 #pragma unroll
         for (int q = 0; q < PB; ++q) {
-            double s[NOUT];
+            double s[NACC];
 #pragma unroll
-            for (int a = 0; a < NOUT; ++a) s[a] = __shfl_sync(0xffffffffu, tot, q * NOUT + a);
-            if (lane == 0) write_out<PB>(p, ti.w, p0, np, q, s, V0);
+            for (int a = 0; a < NACC; ++a) s[a] = __shfl_sync(0xffffffffu, tot, q * NACC + a);
+            if (lane == 0) write_out<PB, MODE_J2>(p, ti.w, p0, np, q, s, V0);
         }
     }
 }
@@ -238,7 +238,7 @@ j2_eval_tma_kernel(const __grid_constant__ EvalParams p, uint32_t n_tiles) {
 template <typename T>
 constexpr size_t tma_smem_bytes(int PB, int VPT, int TMA_NST) {
     return (size_t)TMA_NST * 3 * VPT * TPB * Traits<T>::VW * sizeof(T) + 2 * TMA_NST * sizeof(uint64_t) +
-           MAXTAB * sizeof(Coef4<T>) + 2 * TMA_NCW * PB * NOUT * sizeof(double);
+           MAXTAB * sizeof(Coef4<T>) + 2 * TMA_NCW * PB * NACC * sizeof(double);
 }
 
 }  // namespace qj2

@@ -180,7 +180,7 @@ void ws_layout(int64_t W, int32_t P, int64_t N_local, qj2_dtype dtype,
     const int64_t tpw = (N_local + ch_of(dtype) - 1) / ch_of(dtype);
     const int pb = pb_of(P);
     const int64_t ng = (P + pb - 1) / pb;
-    *part_bytes = tpw > 1 ? align256((size_t)W * ng * tpw * pb * NOUT * sizeof(double)) : 0;
+    *part_bytes = tpw > 1 ? align256((size_t)W * ng * tpw * pb * NACC * sizeof(double)) : 0;
     *cnt_bytes = tpw > 1 ? align256((size_t)W * ng * sizeof(unsigned)) : 0;
 }
 
