@@ -142,17 +142,17 @@ struct FunctorEval {
     T u, du, h;
 };
 
-// tab_base: shared-memory byte address of the functor's row 0 minus
-// MAGIC_BITS * sizeof(Coef4) (so bits * sizeof(Coef4) + tab_base addresses
-// row j); clamp_bits = MAGIC_BITS + m (the all-zero row).  min(bits, clamp) is
-// one VIADDMNMX and the address one LEA.
+// tab_base: shared-memory byte address of the functor's row 0; m_clamp = m
+// (the functor's all-zero row).  j = min(bits(MAGIC + floor(t)) - MAGIC_BITS, m)
+// is one VIADDMNMX (immediate -MAGIC_BITS) and the address one LEA; keeping the
+// magic bias out of the base stops ptxas from re-adding it per term.
 template <typename T>
 __device__ __forceinline__ FunctorEval<T> functor_from_t(T t, uint32_t tab_base,
-                                                         typename Traits<T>::U clamp_bits) {
+                                                         typename Traits<T>::U m_clamp) {
     using Tr = Traits<T>;
-    const T tf = Tr::add_rd(t, Tr::MAGIC);                // MAGIC + floor(t)
-    typename Tr::U jb = Tr::bits(tf);
-    jb = jb < clamp_bits ? jb : clamp_bits;              // MAGIC + min(floor(t), m)
+    const T tf = Tr::add_rd(t, Tr::MAGIC);                // MAGIC + floor(t), t >= 0
+    typename Tr::U jb = Tr::bits(tf) - Tr::MAGIC_BITS;    // floor(t) (huge for t = BIG or NaN)
+    jb = jb < m_clamp ? jb : m_clamp;                    // min(floor(t), m)
     const T f = t - (tf - Tr::MAGIC);
     T a0, a1, a2, a3;
     ld_shared_c4(tab_base + (uint32_t)jb * (uint32_t)sizeof(Coef4<T>), a0, a1, a2, a3);

@@ -90,9 +90,9 @@ __device__ __forceinline__ void load_table(const EvalParams &p, Coef4<T> *tab) {
 // Functor constants of one source group for the current walker.
 template <typename T>
 struct GroupC {
-    uint32_t base;                    // shared address of the group's row 0 minus MAGIC_BITS*sizeof(Coef4)
+    uint32_t base;                    // shared address of the group's row 0
     T invd;                           // 1/delta
-    typename Traits<T>::U clamp;      // MAGIC_BITS + m (the group's zero row)
+    typename Traits<T>::U clamp;      // m (the group's zero row)
     double sg, sh, ss;                // fp64 flush scales: G = sg*acc, L = sh*acc_h + ss*acc_s
 };
 
@@ -110,20 +110,17 @@ __device__ __forceinline__ int src_group(const EvalParams &p, int64_t gi) {
 template <typename T, int MODE>
 __device__ __forceinline__ GroupC<T> group_consts(const EvalParams &p, int g, int kg, uint32_t tab_addr) {
     using Tr = Traits<T>;
-    const uint32_t magic_off = (uint32_t)(Tr::MAGIC_BITS * (typename Tr::U)sizeof(Coef4<T>));
     GroupC<T> c;
     double invd;
     if constexpr (MODE == MODE_J2) {
-        const uint32_t base_same = tab_addr - magic_off;
-        const uint32_t base_opp = tab_addr + (uint32_t)((p.m + 1) * (int)sizeof(Coef4<T>)) - magic_off;
-        c.base = (g == kg) ? base_same : base_opp;
+        c.base = tab_addr + ((g == kg) ? 0u : (uint32_t)((p.m + 1) * (int)sizeof(Coef4<T>)));
         c.invd = sizeof(T) == 4 ? T(p.inv_delta_f) : T(p.inv_delta);
-        c.clamp = Tr::MAGIC_BITS + (typename Tr::U)p.m;
+        c.clamp = (typename Tr::U)p.m;
         invd = p.inv_delta;
     } else {
-        c.base = tab_addr + (uint32_t)(p.grp_tab[g] * (int)sizeof(Coef4<T>)) - magic_off;
+        c.base = tab_addr + (uint32_t)(p.grp_tab[g] * (int)sizeof(Coef4<T>));
         c.invd = T(p.grp_invd[g]);
-        c.clamp = Tr::MAGIC_BITS + (typename Tr::U)p.grp_m[g];
+        c.clamp = (typename Tr::U)p.grp_m[g];
         invd = p.grp_invd[g];
     }
     c.sg = -invd;

@@ -58,10 +58,9 @@ __global__ void vgl_kernel(const __grid_constant__ VglParams p, const T *__restr
     __syncthreads();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= p.n) return;
-    const uint32_t base = (uint32_t)__cvta_generic_to_shared(tab) -
-                          (uint32_t)(Tr::MAGIC_BITS * (typename Tr::U)sizeof(Coef4<T>));
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(tab);
     const T id = T(p.inv_delta);
-    const FunctorEval<T> e = functor_from_t<T>(r[i] * id, base, Tr::MAGIC_BITS + (typename Tr::U)p.m);
+    const FunctorEval<T> e = functor_from_t<T>(r[i] * id, base, (typename Tr::U)p.m);
     out[i * 3 + 0] = (double)e.u;
     out[i * 3 + 1] = (double)e.du * p.inv_delta;
     out[i * 3 + 2] = 2.0 * (double)e.h * p.inv_delta * p.inv_delta;
