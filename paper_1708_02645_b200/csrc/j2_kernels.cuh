@@ -181,6 +181,8 @@ struct SubMask {
     int len;          // valid sources in the sub-tile
     int k_rel;        // self source, or -1
     int64_t g0;       // global index of the sub-tile's first source
+    int up_rel;       // J2: first spin-down source of the sub-tile (len if none)
+    uint32_t base_hi; // J2: table base of the spin-down sources
 };
 
 // One sub-tile.  Every thread walks ITERS vectors at a constant stride of NT
@@ -229,9 +231,11 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
 #pragma unroll
             for (int e = 0; e < VW; ++e) {
                 bool dead = false;
+                uint32_t base = gc.base;
                 if (GEN) {
                     const int li = rel + e;
                     dead = (li >= mk.len) || (li == mk.k_rel);
+                    if (MODE == MODE_J2) base = li < mk.up_rel ? gc.base : mk.base_hi;   // spin halves
                 }
                 const T x = Tr::comp(bx[it], e), y = Tr::comp(by[it], e), z = Tr::comp(bz[it], e);
 #pragma unroll
@@ -242,7 +246,7 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
                         const T dz = min_image_k<T, -1>(z, tr[q].az);
                         T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
                         if (GEN) r2 = dead ? T(1e30) : r2;
-                        const T r = accumulate<T>(dx, dy, dz, r2, gc.invd, gc.base, gc.clamp, acc[q]);
+                        const T r = accumulate<T>(dx, dy, dz, r2, gc.invd, base, gc.clamp, acc[q]);
                         if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
                     }
                 }
@@ -258,11 +262,11 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
     }
 }
 
-// A sub-tile straddling a group boundary (spin halves in J2, species in J1):
-// rare, so a compact rolled loop (one vector per iteration, no prefetch) keeps
-// the instruction footprint of the hot loop small.  The group is looked up
-// per source and the terms are accumulated in physical units (PHYS) because
-// J1 species differ in delta.
+// A J1 sub-tile straddling a species boundary: rare, so a compact rolled
+// loop (one vector per iteration, no prefetch) keeps the instruction
+// footprint small.  The species is looked up per source and the terms are
+// accumulated in physical units because species differ in delta.  (J2's spin
+// straddle stays in the pipelined loop: both halves share delta.)
 template <typename T, int PB, bool ROW, int NT, int MODE>
 __device__ __forceinline__ void tile_multi(int tid, const EvalParams &p, int kg, uint32_t tab_addr,
                                            const typename Traits<T>::V *__restrict__ px,
@@ -376,16 +380,24 @@ __device__ __forceinline__ void sub_tile(int tid, const EvalParams &p, int kg, u
     mk.len = (int)(send - sstart);
     mk.k_rel = k_in ? (int)(k_local - sstart) : -1;
     mk.g0 = g0;
+    mk.up_rel = mk.len;
     const GroupC<T> gc = group_consts<T, MODE>(p, grp, kg, tab_addr);
+    mk.base_hi = gc.base;
+    if constexpr (MODE == MODE_J2) {
+        if (!one_group) {           // straddles N_up: both halves share delta, select the table per source
+            mk.up_rel = (int)(p.N_up - g0);
+            mk.base_hi = group_consts<T, MODE>(p, 1, kg, tab_addr).base;
+        }
+    }
     if (mk.len == SCH && !k_in && one_group) {                 // clean
         tile_run<T, PB, ROW, PF, false, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp,
                                                   row_stride);
         flush<T, PB, MODE>(acc, dacc, gc.sg, gc.sh, gc.ss);
-    } else if (one_group) {                                    // ragged and/or holds k
+    } else if (one_group || MODE == MODE_J2) {                // ragged, holds k, or straddles N_up (J2)
         tile_run<T, PB, ROW, PF, true, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp,
                                                  row_stride);
         flush<T, PB, MODE>(acc, dacc, gc.sg, gc.sh, gc.ss);
-    } else {                                                   // straddles a group boundary
+    } else {                                                   // J1: straddles a species boundary
         tile_multi<T, PB, ROW, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, np, mk, acc, rp, row_stride);
         if constexpr (MODE == MODE_J2) flush<T, PB, MODE>(acc, dacc, gc.sg, gc.sh, gc.ss);   // shared delta: raw
         else flush<T, PB, MODE>(acc, dacc, -1.0, 1.0, 2.0);                                  // already physical
