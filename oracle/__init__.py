@@ -201,3 +201,64 @@ def normalized_error(gpu, orc, absout, fn) -> np.ndarray:
     F = np.array([cmax, cmax / delta, cmax / delta, cmax / delta, cmax / delta ** 2])
     denom = np.maximum(absout, F)
     return np.abs(np.asarray(gpu, dtype=np.float64) - orc) / denom
+
+
+def _lib_next2():
+    L = lib()
+    if not getattr(L, "_next2", False):
+        dp = ctypes.POINTER(ctypes.c_double)
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        i64 = ctypes.c_int64
+        L.orc_j2_state.restype = i64
+        L.orc_j2_state.argtypes = [dp, ctypes.c_double, ctypes.c_int, dp, i64, i64, i64, dp, dp, dp]
+        L.orc_accept.restype = i64
+        L.orc_accept.argtypes = [dp, ctypes.c_double, ctypes.c_int, dp, i64, i64, i64, i64,
+                                 dp, dp, i32p, dp, i32p, dp]
+        L._next2 = True
+    return L
+
+
+def j2_state(R1, n: int, n_up: int, fn):
+    """NEXT-2: per-electron J2 state of one configuration R1[3][Np] from
+    scratch: (state[5][Np], abs[5][Np]) with rows V, Gx, Gy, Gz, L (see
+    orc_j2_state).  Slots >= n are 0."""
+    R1 = _f64(R1)
+    Np = R1.shape[1]
+    st = np.zeros((5, Np))
+    ab = np.zeros((5, Np))
+    r = _lib_next2().orc_j2_state(_dp(_f64(fn.L)), float(fn.r_cut), int(fn.m), _dp(_f64(fn.coef)),
+                                  n, n_up, Np, _dp(R1), _dp(st), _dp(ab))
+    if r:
+        raise CoincidentError(f"electron {r - 1} has a coincident partner")
+    return st, ab
+
+
+def accept(R, state, k, r_new, acc, fn, n: int, n_up: int):
+    """NEXT-2 oracle of qj2_accept (orc_accept): returns (R', state', abs)
+    as fp64 copies; inputs (fp32 or fp64) are promoted exactly.
+    R [W][3][Np], state [W][5][Np], k [W], r_new [W][3], acc [W] (nonzero =
+    accepted).  abs is NaN for rejected walkers."""
+    R2 = _f64(R).copy()
+    S2 = _f64(state).copy()
+    W, _, Np = R2.shape
+    ab = np.full((W, 5, Np), np.nan)
+    k = np.ascontiguousarray(np.asarray(k, dtype=np.int32))
+    a = np.ascontiguousarray(np.asarray(acc, dtype=np.int32))
+    rn = _f64(np.asarray(r_new).reshape(W, 3))
+    r = _lib_next2().orc_accept(_dp(_f64(fn.L)), float(fn.r_cut), int(fn.m), _dp(_f64(fn.coef)),
+                                W, n, n_up, Np, _dp(R2), _dp(S2),
+                                k.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), _dp(rn),
+                                a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), _dp(ab))
+    if r:
+        raise CoincidentError(f"walker {r - 1} has a coincident pair")
+    return R2, S2, ab
+
+
+def normalized_error_state(gpu, orc, absst, fn) -> np.ndarray:
+    """Parity metric for the 5N state (NEXT-2): per entry
+    |s_gpu - s_orc| / max(A, F) with A the oracle's absolute-term bound and F
+    the functor scale of normalized_error (rows V, Gx, Gy, Gz, L)."""
+    cmax = float(np.max(np.abs(fn.coef)))
+    delta = fn.r_cut / fn.m
+    F = np.array([cmax, cmax / delta, cmax / delta, cmax / delta, cmax / delta ** 2])[:, None]
+    return np.abs(np.asarray(gpu, dtype=np.float64) - orc) / np.maximum(np.nan_to_num(absst, nan=0.0), F)

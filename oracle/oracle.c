@@ -425,3 +425,130 @@ int64_t orc_eval_j1(const double L[3], int n_species, const int64_t *sp_start,
         }
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-2: the per-electron J2 state ("5N") and the accept-side update.       */
+/*                                                                            */
+/* State of electron e ("we can afford to eliminate the      */
+/* intermediate data all together and keep the memory use of J2 at 5N"; the   */
+/* values, gradients (D=3) and Laplacians of PAPER:1384-1386 summed over the  */
+/* partner index):                                                            */
+/*   V_e = sum_{j != e} U_s(r_ej)                                             */
+/*   G_e = grad_e J2 = sum_{j != e} U_s'(r_ej) (r_e - r_j)/r_ej               */
+/*   L_e = lap_e J2  = sum_{j != e} U_s''(r_ej) + 2 U_s'(r_ej)/r_ej           */
+/* with r_e - r_j the minimum-image displacement (reading R7) and s the spin  */
+/* channel of the pair (R6).  Stored SoA as state[5][Np] per walker (the      */
+/* Rsoa layout).  Since U_s(r) depends on the pair only,     */
+/* J2 = (1/2) sum_e V_e (reading R1) and G_e, L_e are the exact gradient and  */
+/* Laplacian of J2 with respect to r_e.                                       */
+/*                                                                            */
+/* orc_j2_state: the state of one configuration from scratch, a direct        */
+/* O(N^2) loop (the state "periodically computed from scratch"). */
+/* abs_state (optional) receives the absolute-term sums.                      */
+/* Returns 0, or 1 + e for the first electron with a coincident partner.      */
+/* ------------------------------------------------------------------------ */
+static int pair_terms(const double L[3], double r_cut, int m, const double *cs,
+                      const double re[3], const double rj[3], double t[5], double a[5])
+{
+    /* t = (U, U' dx/r, U' dy/r, U' dz/r, U'' + 2U'/r) with d = re - rj,
+     * a = their absolute values (|U''| + 2|U'|/r for the last). */
+    double d[3], rho, u[3];
+    orc_min_image(L, rj, re, d, &rho);          /* d = minimg(re - rj) */
+    for (int c = 0; c < 5; ++c) t[c] = a[c] = 0.0;
+    if (!(rho < r_cut)) return 0;
+    if (rho == 0.0) return 1;
+    orc_bspline(cs, m, r_cut, rho, u);
+    t[0] = u[0];
+    for (int c = 0; c < 3; ++c) t[1 + c] = u[1] * d[c] / rho;
+    t[4] = u[2] + 2.0 * u[1] / rho;
+    a[0] = fabs(u[0]);
+    for (int c = 0; c < 3; ++c) a[1 + c] = fabs(t[1 + c]);
+    a[4] = fabs(u[2]) + 2.0 * fabs(u[1]) / rho;
+    return 0;
+}
+
+int64_t orc_j2_state(const double L[3], double r_cut, int m, const double *coef,
+                     int64_t N, int64_t N_up, int64_t Np, const double *R1,
+                     double *state, double *abs_state)
+{
+    const int mc = m + 3;
+    for (int64_t e = 0; e < N; ++e) {
+        nsum S[5], A[5];
+        for (int c = 0; c < 5; ++c) { S[c].s = S[c].c = 0.0; A[c].s = A[c].c = 0.0; }
+        double re[3] = { R1[e], R1[Np + e], R1[2 * Np + e] };
+        for (int64_t j = 0; j < N; ++j) {
+            if (j == e) continue;
+            double rj[3] = { R1[j], R1[Np + j], R1[2 * Np + j] };
+            double t[5], a[5];
+            if (pair_terms(L, r_cut, m, coef + spin_channel(e, j, N_up) * mc, re, rj, t, a))
+                return 1 + e;
+            for (int c = 0; c < 5; ++c) { nsum_add(&S[c], t[c]); nsum_add(&A[c], a[c]); }
+        }
+        for (int c = 0; c < 5; ++c) {
+            state[c * Np + e] = nsum_get(&S[c]);
+            if (abs_state) abs_state[c * Np + e] = nsum_get(&A[c]);
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* orc_accept: Alg. 1 L9 "Accept r_k <- r'_k" for the J2 share of the state   */
+/* (PAPER:850), batched over walkers.  For every walker w with accept[w] != 0 */
+/* (rejected walkers are left untouched, "or reject"), with k = k[w],         */
+/* r_k = R[w][:, k] (before the update) and r'_k = r_new[w]:                  */
+/*   for i != k:  state_i += T_i(r'_k) - T_i(r_k),   T_i(r) = the pair terms  */
+/*                of pair_terms(r_i, r) -- electron i's partner k moved       */
+/*                (Delta J2 = U^2_k(R') - U^2_k(R); the Ref's     */
+/*                "column and row are updated for each accepted move",        */
+/*                PAPER:1386-1387, here on the 5N accumulators);              */
+/*   state_k = sum_{i != k} T_k(r'_k) with d = r'_k - r_i (the from-scratch   */
+/*                values at R', equal to qj2_eval's output at r'_k: V, and    */
+/*                G = -sum U' (r_i - r'_k)/r);                                */
+/*   R[w][:, k] = r'_k  ("both R and Rsoa (6 floats) are updated with the new */
+/*                position").                                */
+/* Everything fp64 (inputs promoted exactly by the caller).  abs_state        */
+/* (optional, [W][5][Np]) receives |state_old| + |T(r')| + |T(r)| per entry   */
+/* (sum of |T(r')| for k; untouched for rejected walkers) for the tolerance.  */
+/* Returns 0, or 1 + w for the first walker with a coincident pair.          */
+/* ------------------------------------------------------------------------ */
+int64_t orc_accept(const double L[3], double r_cut, int m, const double *coef,
+                   int64_t W, int64_t N, int64_t N_up, int64_t Np,
+                   double *R, double *state, const int32_t *k, const double *r_new,
+                   const int32_t *accept, double *abs_state)
+{
+    const int mc = m + 3;
+    for (int64_t w = 0; w < W; ++w) {
+        if (!accept[w]) continue;
+        double *Rw = R + w * 3 * Np;
+        double *Sw = state + w * 5 * Np;
+        double *Aw = abs_state ? abs_state + w * 5 * Np : NULL;
+        const int64_t kw = k[w];
+        const double rk[3] = { Rw[kw], Rw[Np + kw], Rw[2 * Np + kw] };
+        const double rn[3] = { r_new[3 * w], r_new[3 * w + 1], r_new[3 * w + 2] };
+        nsum Sk[5], Ak[5];
+        for (int c = 0; c < 5; ++c) { Sk[c].s = Sk[c].c = 0.0; Ak[c].s = Ak[c].c = 0.0; }
+        for (int64_t i = 0; i < N; ++i) {
+            if (i == kw) continue;
+            const double *cs = coef + spin_channel(i, kw, N_up) * mc;
+            double ri[3] = { Rw[i], Rw[Np + i], Rw[2 * Np + i] };
+            double tn[5], an[5], to[5], ao[5], tk[5], ak[5];
+            if (pair_terms(L, r_cut, m, cs, ri, rn, tn, an)) return 1 + w;   /* d = r_i - r'_k */
+            if (pair_terms(L, r_cut, m, cs, ri, rk, to, ao)) return 1 + w;   /* d = r_i - r_k  */
+            if (pair_terms(L, r_cut, m, cs, rn, ri, tk, ak)) return 1 + w;   /* d = r'_k - r_i */
+            for (int c = 0; c < 5; ++c) {
+                double old = Sw[c * Np + i];
+                Sw[c * Np + i] = old + (tn[c] - to[c]);
+                if (Aw) Aw[c * Np + i] = fabs(old) + an[c] + ao[c];
+                nsum_add(&Sk[c], tk[c]);
+                nsum_add(&Ak[c], ak[c]);
+            }
+        }
+        for (int c = 0; c < 5; ++c) {
+            Sw[c * Np + kw] = nsum_get(&Sk[c]);
+            if (Aw) Aw[c * Np + kw] = nsum_get(&Ak[c]);
+        }
+        for (int c = 0; c < 3; ++c) Rw[c * Np + kw] = rn[c];
+    }
+    return 0;
+}
