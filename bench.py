@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5"])
+    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C3S"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -185,15 +185,26 @@ def committed_traffic(config_name: str):
 # ---------------------------------------------------------------------------
 class OracleSample:
     """The CPU oracle (as it stands) on walkers [0, n) of cfg.  Inputs are drawn
-    by the oracle side's own C generator (untimed); run() times one evaluation."""
+    by the oracle side's own C generator (untimed); run() times one evaluation
+    (C3S: one sweep step -- eval at (r_k, r'_k), the Metropolis test and the
+    accept-side update of R and the fp64 state)."""
+
+    MAX_SWEEP_WALKERS = 48     # the oracle's fp64 state is 5 * 8 * N bytes per walker
 
     def __init__(self, cfg, n_walkers, threads):
         import oracle
         import qmcgen
         self.cfg, self.n, self.threads = cfg, int(n_walkers), threads
-        k_all = qmcgen.make_k(cfg.seed, cfg.W, cfg.N)
-        self.k = k_all[:self.n]
-        self.rt = qmcgen.make_trials(cfg.seed, np.arange(cfg.W), k_all, cfg.N, cfg.L, cfg.np_dtype)[:self.n]
+        self.sweep = cfg.name == "C3S"
+        if self.sweep:
+            self.n = min(self.n, self.MAX_SWEEP_WALKERS)
+            ks, tr, u = qmcgen.make_sweep(cfg.seed, cfg.W, cfg.N, cfg.L, cfg.np_dtype, 1)
+            self.k, self.rt, self.u = ks[0][:self.n], tr[0][:self.n], u[0][:self.n]
+            self.S = np.zeros((self.n, 5, cfg.Np))
+        else:
+            k_all = qmcgen.make_k(cfg.seed, cfg.W, cfg.N)
+            self.k = k_all[:self.n]
+            self.rt = qmcgen.make_trials(cfg.seed, np.arange(cfg.W), k_all, cfg.N, cfg.L, cfg.np_dtype)[:self.n]
         self.fn = qmcgen.make_functor(cfg.seed, cfg.L, cfg.m)
         self.R = oracle.gen_positions(cfg.seed, 0, self.n, cfg.N, cfg.Np, cfg.L, cfg.np_dtype, threads)
         self.items = self.n * (cfg.N - 1)
@@ -201,8 +212,16 @@ class OracleSample:
     def run(self):
         import oracle
         t0 = time.perf_counter()
-        oracle.eval_j2(self.R, self.k, self.rt, self.fn, self.cfg.N, self.cfg.n_up, threads=self.threads)
+        out, _, _ = oracle.eval_j2(self.R, self.k, self.rt, self.fn, self.cfg.N, self.cfg.n_up,
+                                   threads=self.threads)
+        if self.sweep:
+            acc = (self.u < np.exp(out[:, 1, 0] - out[:, 0, 0]) ** 2).astype(np.int32)
+            oracle.accept(self.R, self.S, self.k, self.rt[:, 1], acc, self.fn, self.cfg.N, self.cfg.n_up)
         return time.perf_counter() - t0
+
+
+def _what(cfg):
+    return "eval P=2 + Metropolis + accept update" if cfg.name == "C3S" else "P=1"
 
 
 def oracle_sample_size(cfg, cores, budget_s):
@@ -237,7 +256,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     import qmcgen
-    cfg = qmcgen.CONFIGS[args.config]
+    cfg = qmcgen.config(args.config)
     cores = cpu_cores()
     budget_total = 120.0
     per_step = max(0.2, min(10.0, budget_total / max(1, args.steps + args.warmup)))
@@ -249,7 +268,7 @@ def run_reference(args):
     times = [smp.run() for _ in range(args.steps)]
     t = float(np.mean(times))
     value = smp.items / t
-    sample = (f"{ws} of {cfg.W} walkers of {cfg.name} (N={cfg.N}, P=1) per step, fp32 inputs promoted "
+    sample = (f"{smp.n} of {cfg.W} walkers of {cfg.name} (N={cfg.N}, {_what(cfg)}) per step, fp32 inputs promoted "
               f"exactly to fp64, plain C oracle, {cores} threads ({cpu_model()})")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
@@ -267,8 +286,11 @@ def workload_config(cfg, world):
         "C3": f"C3: one instance per rank, N={cfg.N} electrons x W={cfg.W} walkers, P=1, fp32, seed 2(+rank)",
         "C4": f"C4: 4096 instances of N={cfg.N} x W={cfg.W}, P=1, fp32, seeds 3..4098, sharded by instance",
         "C5": f"C5: one instance N={cfg.N} x W={cfg.W}, P=1, fp32, seed 5, split along N + NCCL all-reduce",
+        "C3S": f"C3S (NEXT-2 sweep step): C3 instance per rank (N={cfg.N} x W={cfg.W}, fp32, seed 2(+rank)), "
+               f"one PbyP move per walker: eval at (r_k, r'_k) -> Metropolis -> accept-side update of R and "
+               f"the 5N fp32 J2 state",
     }[name]
-    return {"workload": desc, "N": cfg.N, "W": cfg.W, "P": 1, "m": cfg.m, "Np": cfg.Np,
+    return {"workload": desc, "N": cfg.N, "W": cfg.W, "P": 2 if name == "C3S" else 1, "m": cfg.m, "Np": cfg.Np,
             "parallelism": f"{'walker-instance' if name != 'C5' else 'source-axis'} x{world}",
             "l2": "inputs > 126 MB L2 (no flush needed)"}
 
@@ -545,7 +567,81 @@ class C4Plan:
         return None   # see DESIGN.md: the host-buffer path is measured on C3
 
 
+class SweepPlan:
+    """NEXT-2: one particle-by-particle move per walker and step on a C3 instance
+    (Alg. 1 L5-L9 for the J2 factor): qj2_eval with P = 2 (U^2_k at r_k and
+    r'_k in one pass, ratio e^{dJ2} fused) -> qj2_metropolis (u < rho^2) ->
+    qj2_accept (R[:, k] and the 5N fp32 state of every partner).  Electron
+    k = (k0 + s) mod N at step s (ordered sweep), inputs pre-drawn by qmcgen."""
+    mode = "C3S"
+    launches_per_step = 5      # eval kernel + counter memset + metropolis + r_k gather + accept kernel
+
+    def __init__(self, cfg, rank, world):
+        self.cfg = cfg
+        self.seed = cfg.seed + rank
+        self.items_per_step = cfg.W * (cfg.N - 1)
+        self.s = 0
+
+    def items_total(self, world):
+        return self.items_per_step * world
+
+    def prepare(self, q, n_steps):
+        import torch
+        import qmcgen
+        cfg = self.cfg
+        self.fn = q.Functor.of(qmcgen.make_functor(cfg.seed, cfg.L, cfg.m))
+        self.R = q.gen_positions(self.seed, cfg.W, cfg.N, cfg.Np, cfg.L, torch.float32)
+        self.S = torch.zeros((cfg.W, 5, cfg.Np), dtype=torch.float32, device="cuda")   # 5N state
+        ks, tr, u = qmcgen.make_sweep(self.seed, cfg.W, cfg.N, cfg.L, np.float32, n_steps)
+        self.ks, self.tr, self.u = (torch.from_numpy(ks).cuda(), torch.from_numpy(tr).cuda(),
+                                    torch.from_numpy(u).cuda())
+        self.n = n_steps
+        self.ws = q.Workspace(q.workspace_size(cfg.W, 2, cfg.N, torch.float32))
+        self.wsa = q.Workspace(4096 * 16)
+        self.out = torch.empty((cfg.W, 2, 5), dtype=torch.float64, device="cuda")
+        self.ratio = torch.empty((cfg.W, 2, 2), dtype=torch.float64, device="cuda")
+        self.acc = torch.empty((cfg.W,), dtype=torch.int32, device="cuda")
+        torch.cuda.synchronize()
+
+    def step(self, q, dist_mod):
+        cfg = self.cfg
+        s = self.s % self.n
+        self.s += 1
+        k = self.ks[s]
+        q.eval(self.R, k, self.tr[s], self.fn, cfg.N, cfg.n_up, ratio=True, out=self.out,
+               ratio_out=self.ratio, workspace=self.ws)
+        q.metropolis(self.ratio, self.u[s], self.acc, trial=1)
+        q.accept(self.R, self.S, k, self.tr[s], self.acc, self.out, self.fn, cfg.N, cfg.n_up, trial=1,
+                 workspace=self.wsa)
+
+    def kernel_ms(self, q, stream, reps):
+        """The dominant kernel: qj2_accept on the last step's decisions (one
+        launch per call with the caller's r_old)."""
+        import torch
+        cfg = self.cfg
+        s = (self.s - 1) % self.n
+        k = self.ks[s]
+        r_old = self.tr[s][:, 0, :].contiguous()
+        self.n_acc = int(self.acc.sum().item())
+        torch.cuda.synchronize()
+        return _event_ms(lambda: q.accept(self.R, self.S, k, self.tr[s], self.acc, self.out, self.fn, cfg.N,
+                                          cfg.n_up, trial=1, r_old=r_old), stream, reps)
+
+    @property
+    def alg_bytes_per_launch(self):
+        # per accepted walker: x, y, z of every partner (12 B) + 5 fp32 state lanes read and written
+        # (40 B) per partner, + k, accept, r_new, r_old, out_new row (4+4+12+12+40 B); 4 B accept flag
+        # per rejected walker
+        cfg = self.cfg
+        return self.n_acc * ((cfg.N - 1) * 52 + 72) + (cfg.W - self.n_acc) * 4
+
+    def e2e(self, q, steps, dist_mod):
+        return None   # see DESIGN.md: the host-buffer path is measured on C3
+
+
 def make_plan(cfg, rank, world):
+    if cfg.name == "C3S":
+        return SweepPlan(cfg, rank, world)
     if cfg.name == "C3":
         return C3Plan(cfg, rank, world)
     if cfg.name == "C4":
@@ -553,6 +649,10 @@ def make_plan(cfg, rank, world):
     if cfg.name == "C5":
         return C5Plan(cfg, rank, world)
     raise NotImplementedError(cfg.name)
+
+
+def plan_kernel_name(plan):
+    return "j2_accept_kernel<float>" if plan.mode == "C3S" else "j2_eval_kernel<float,1,false>"
 
 
 def run_ours(args):
@@ -565,10 +665,13 @@ def run_ours(args):
     import qmcgen
     import paper_1708_02645_b200 as q
     q.device_check()
-    cfg = qmcgen.CONFIGS[args.config]
+    cfg = qmcgen.config(args.config)
 
     plan = make_plan(cfg, rank, world)
-    plan.prepare(q)                                   # device-resident inputs (generation untimed)
+    if plan.mode == "C3S":                            # pre-drawn sweep inputs for every step
+        plan.prepare(q, args.warmup + 2 * args.steps + 2)
+    else:
+        plan.prepare(q)                               # device-resident inputs (generation untimed)
 
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -617,7 +720,7 @@ def run_ours(args):
         smp = OracleSample(cfg, nw, cores)
         dt = smp.run()
         cpu = {"value": smp.items / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{nw} of {cfg.W} walkers of {cfg.name} (N={cfg.N}, P=1), one pass, fp32 inputs "
+               "sample": f"{smp.n} of {cfg.W} walkers of {cfg.name} (N={cfg.N}, {_what(cfg)}), one pass, fp32 inputs "
                          f"promoted exactly to fp64, plain C oracle, {cores} threads ({cpu_model()}), "
                          f"{dt:.1f} s wall"}
 
@@ -630,7 +733,7 @@ def run_ours(args):
             "config": workload_config(cfg, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "j2_eval_kernel<float,1,false>", "kernel_ms": kms,
+                         "kernel": plan_kernel_name(plan), "kernel_ms": kms,
                          "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -202,6 +202,64 @@ qj2_status qj2_ratio(int64_t W, int32_t P, const double *out, const double *V_cu
                      double *ratio_out, void *stream);
 
 /* ------------------------------------------------------------------------ */
+/* NEXT-2: accept-side update (Alg. 1 L9 "Accept r_k <- r'_k or reject",     */
+/* PAPER:850) of the positions and the per-electron J2 state.                */
+/*                                                                           */
+/* The state is the paper's compute-on-the-fly J2 storage, "5N sizeof(T)"    */
+/* per walker: for electron e,                             */
+/*   V_e = sum_{j != e} U_s(r_ej),  G_e = sum_{j != e} U_s'(r_ej) d_ej/r_ej, */
+/*   L_e = sum_{j != e} U_s''(r_ej) + 2 U_s'(r_ej)/r_ej,  d_ej = minimg(r_e - r_j), */
+/* i.e. electron e's share of J2 and the gradient/Laplacian of J2 with      */
+/* respect to r_e, stored SoA as state[w][5][Np] (rows V, Gx, Gy, Gz, L; the */
+/* Rsoa layout), type dtype.                                */
+/*                                                                           */
+/* For every walker w with accept[w] != 0 (others are not touched), k = k[w]:*/
+/*   partners i != k in the slice:                                           */
+/*     state_i += T_i(r'_k) - T_i(r_k), T_i(r) = (U, U' d/|d|, U''+2U'/|d|), */
+/*     d = minimg(r_i - r), per-term arithmetic in dtype (one rounding of   */
+/*     the stored sum per update);                                           */
+/*   if k is in the slice: state_k = out_new row w (qj2_eval's V, G, L at    */
+/*     r'_k over ALL sources -- after the all-reduce when sharded -- rounded */
+/*     to dtype: "reuse the computed values"), and R[:, k] = r'_k */
+/*     ("both R and Rsoa (6 floats) are updated").          */
+/*                                                                           */
+/* Arguments (sizes, slice, N_up, Np, alignment: as qj2_eval)                */
+/*   R         device [W][3][Np] dtype, in/out.                              */
+/*   state     device [W][5][Np] dtype, in/out, 16-byte aligned; padding     */
+/*             slots [N_local, Np) are not modified.                         */
+/*   k         device [W] int32, global index of the moved electron.         */
+/*   r_new     device dtype, row w at r_new + w*r_stride = r'_k in [0, L_d); */
+/*             r_stride >= 3 (3*P for qj2_eval's r_trial[W][P][3]).         */
+/*   r_old     device [W][3] dtype, r_k before the move, or NULL: then it is */
+/*             gathered from R (every accepted walker's k must lie in the    */
+/*             slice; sharded callers whose slice may not hold k pass r_old).*/
+/*   accept    device [W] int32, nonzero = accepted.                          */
+/*   out_new   device fp64, row w at out_new + w*out_stride = (V, Gx, Gy, Gz,*/
+/*             L) at r'_k; out_stride >= 5 (e.g. 5*P for qj2_eval's out).    */
+/*   workspace device, >= qj2_accept_workspace_size() (r_old gather; 0 bytes */
+/*             needed when r_old != NULL).                                   */
+/* Two launches when r_old == NULL (gather, update), else one.  Errors as    */
+/* qj2_eval; out-of-range k or coordinates are preconditions.                */
+/* ------------------------------------------------------------------------ */
+qj2_status qj2_accept_workspace_size(int64_t W, qj2_dtype dtype, size_t *bytes);
+qj2_status qj2_accept(const qj2_functor *fn, qj2_dtype dtype,
+                      int64_t W, int64_t N_total, int64_t N_up,
+                      int64_t i_offset, int64_t N_local, int64_t Np,
+                      void *R, void *state, const int32_t *k,
+                      const void *r_new, int64_t r_stride, const void *r_old,
+                      const int32_t *accept, const double *out_new, int64_t out_stride,
+                      void *workspace, size_t workspace_bytes, void *stream);
+
+/* Metropolis decision of Alg. 1 L9 for a J2-only trial function and a       */
+/* symmetric proposal: accept[w] = (u[w] < rho_w^2), rho_w = ratio[w*stride  */
+/* + 1] = e^{dJ2} (qj2_eval / qj2_ratio's ratio_out; Eq. 4).  */
+/* u: device [W] fp64 uniform deviates in [0, 1) drawn by the caller (the    */
+/* method's random numbers are inputs).  ratio_stride >= 2 (2*P for          */
+/* ratio_out[W][P][2] at trial 0).  accept: device [W] int32 (0/1).          */
+qj2_status qj2_metropolis(int64_t W, const double *ratio, int64_t ratio_stride,
+                          const double *u, int32_t *accept, void *stream);
+
+/* ------------------------------------------------------------------------ */
 /* Host-buffer variant of qj2_eval (the end-to-end path): R, k, r_trial are  */
 /* HOST arrays (pinned for full PCIe rate), out (and ratio_out if non-NULL)  */
 /* HOST arrays, same shapes as qj2_eval.  Walkers are streamed in chunks of  */

@@ -9,6 +9,8 @@ library raises, and every call goes to the GPU library.
 Public API (names follow include/qmcj2.h):
     eval(R, k, r_trial, fn, n_total, n_up, ...)   -> out [W][P][5] fp64 (and row, ratio)
     eval_j1(ions, species_start, r_trial, fn1)    -> NEXT-1: J1 over the AB row
+    accept(R, state, k, r_new, acc, out_new, fn, ...) -> NEXT-2: accept-side update of R and the 5N J2 state
+    metropolis(ratio, u)                          -> NEXT-2: accept flags (u < rho^2)
     eval_host(R, k, r_trial, fn, ...)             -> host-buffer end-to-end path
     ratio(out, V_cur=None)                        -> [W][P][2] (dJ2, exp(dJ2))
     functor_eval_vgl(fn, channel, r)              -> [n][3] (U, U', U'')
@@ -25,7 +27,7 @@ import torch
 
 from . import _build
 
-__all__ = ["QJ2Error", "Functor", "J1Functor", "Workspace", "eval", "eval_j1", "eval_host", "ratio", "functor_eval_vgl",
+__all__ = ["QJ2Error", "Functor", "J1Functor", "Workspace", "eval", "eval_j1", "accept", "metropolis", "eval_host", "ratio", "functor_eval_vgl",
            "min_image_disp", "check_inputs", "padded_size", "gen_positions", "lib_path",
            "workspace_size", "host_workspace_size", "version", "device_check"]
 
@@ -81,6 +83,10 @@ def _load():
         "qj2_eval": (ctypes.c_int, [F, ctypes.c_int, i64, i64, i64, i64, i64, i64, vp, vp, i32, vp,
                                     vp, vp, vp, vp, vp, sz, vp]),
         "qj2_ratio": (ctypes.c_int, [i64, i32, vp, vp, vp, vp]),
+        "qj2_accept_workspace_size": (ctypes.c_int, [i64, ctypes.c_int, ctypes.POINTER(sz)]),
+        "qj2_accept": (ctypes.c_int, [F, ctypes.c_int, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp, i64, vp,
+                                      vp, vp, i64, vp, sz, vp]),
+        "qj2_metropolis": (ctypes.c_int, [i64, vp, i64, vp, vp, vp]),
         "qj2_eval_j1": (ctypes.c_int, [ctypes.POINTER(_J1Functor), ctypes.c_int, i64, ctypes.POINTER(i64), i64,
                                        vp, i32, vp, vp, vp, vp, vp, vp, sz, vp]),
         "qj2_eval_host_workspace_size": (ctypes.c_int, [i64, i32, i64, ctypes.c_int, i64, ctypes.POINTER(sz)]),
@@ -103,7 +109,8 @@ def _load():
 
 _lib = _load()
 EXPORTS = ("qj2_version", "qj2_status_string", "qj2_last_error", "qj2_device_check", "qj2_padded_size",
-           "qj2_eval_workspace_size", "qj2_eval", "qj2_ratio", "qj2_eval_j1", "qj2_eval_host_workspace_size",
+           "qj2_eval_workspace_size", "qj2_eval", "qj2_ratio", "qj2_eval_j1", "qj2_accept_workspace_size",
+           "qj2_accept", "qj2_metropolis", "qj2_eval_host_workspace_size",
            "qj2_eval_host", "qj2_functor_eval_vgl", "qj2_min_image_disp", "qj2_check_inputs",
            "qj2gen_positions")
 
@@ -334,6 +341,66 @@ def ratio(out, V_cur=None, ratio_out=None, stream=None):
     _check(_lib.qj2_ratio(W, P, _ptr(out), _ptr(V_cur), _ptr(ratio_out), ctypes.c_void_p(_stream_ptr(stream))),
            "qj2_ratio")
     return ratio_out
+
+
+def _row_ptr(t: torch.Tensor, trial: int, width: int):
+    """(pointer, stride in elements) of trial `trial` of a [W][P][width]
+    (or [W][width]) contiguous tensor."""
+    if t.dim() == 2:
+        if trial != 0:
+            raise ValueError("trial index on a [W][width] tensor")
+        return ctypes.c_void_p(t.data_ptr()), width
+    P = t.shape[1]
+    if not 0 <= trial < P:
+        raise ValueError(f"trial {trial} out of range [0, {P})")
+    return ctypes.c_void_p(t.data_ptr() + trial * width * t.element_size()), width * P
+
+
+def accept(R, state, k, r_new, acc, out_new, fn, n_total: int, n_up: int, *, trial: int = 0, i_offset: int = 0,
+           n_local: int | None = None, r_old=None, workspace: Workspace | None = None, stream=None):
+    """qj2_accept (NEXT-2): in place on R [W][3][Np] and state [W][5][Np]
+    (same dtype).  k [W] int32, acc [W] int32 (nonzero = accepted); r_new
+    [W][P][3] (or [W][3]) and out_new (qj2_eval's out [W][P][5] fp64, or
+    [W][5]): trial `trial` is the accepted move.  Returns (R, state)."""
+    _req(R, "R", ndim=3)
+    W, _, Np = R.shape
+    _req(state, "state", R.dtype, 3)
+    if tuple(state.shape) != (W, 5, Np):
+        raise ValueError("state must be [W][5][Np]")
+    _req(k, "k", torch.int32, 1)
+    _req(acc, "acc", torch.int32, 1)
+    _req(r_new, "r_new", R.dtype)
+    if r_old is not None:
+        _req(r_old, "r_old", R.dtype, 2)
+    _req(out_new, "out_new", torch.float64)
+    rp, rs = _row_ptr(r_new, trial, 3)
+    op, os_ = _row_ptr(out_new, trial, 5)
+    n_local = min(Np, n_total - i_offset) if n_local is None else int(n_local)
+    f = Functor.of(fn)
+    b = ctypes.c_size_t()
+    _check(_lib.qj2_accept_workspace_size(W, _dtype_code(R.dtype), ctypes.byref(b)), "qj2_accept_workspace_size")
+    ws = workspace if workspace is not None else Workspace(device=R.device)
+    if r_old is None:
+        ws.reserve(b.value)
+    _check(_lib.qj2_accept(f.ptr, _dtype_code(R.dtype), W, n_total, n_up, i_offset, n_local, Np,
+                           _ptr(R), _ptr(state), _ptr(k), rp, rs, _ptr(r_old), _ptr(acc),
+                           op, os_, _ptr(ws.buf), ws.nbytes,
+                           ctypes.c_void_p(_stream_ptr(stream))), "qj2_accept")
+    return R, state
+
+
+def metropolis(ratio_out, u, acc=None, *, trial: int = 0, stream=None):
+    """qj2_metropolis: acc[w] = u[w] < rho^2 with rho = ratio_out[w][trial][1]
+    (ratio_out [W][P][2] or [W][2] fp64; u [W] fp64 uniforms in [0, 1))."""
+    _req(ratio_out, "ratio_out", torch.float64)
+    _req(u, "u", torch.float64, 1)
+    W = u.shape[0]
+    rp, rs = _row_ptr(ratio_out, trial, 2)
+    if acc is None:
+        acc = torch.empty(W, dtype=torch.int32, device=u.device)
+    _check(_lib.qj2_metropolis(W, rp, rs, _ptr(u), _ptr(acc), ctypes.c_void_p(_stream_ptr(stream))),
+           "qj2_metropolis")
+    return acc
 
 
 def host_workspace_size(W, P, Np, dtype, chunk_walkers) -> int:

@@ -22,6 +22,7 @@
 #include <algorithm>
 
 #include "launch.cuh"
+#include "accept.cuh"
 
 // ===========================================================================
 // Small kernels
@@ -37,6 +38,16 @@ __global__ void ratio_kernel(int64_t W, int32_t P, const double *__restrict__ ou
     const double dj = out[i * 5] - ref;
     ratio_out[i * 2 + 0] = dj;
     ratio_out[i * 2 + 1] = exp(dj);
+}
+
+// Metropolis decision (Alg. 1 L9) for a J2-only trial function, symmetric
+// proposal: accept iff u < rho^2.
+__global__ void metropolis_kernel(int64_t W, const double *__restrict__ ratio, int64_t stride,
+                                  const double *__restrict__ u, int32_t *__restrict__ accept) {
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= W) return;
+    const double rho = ratio[w * stride + 1];
+    accept[w] = u[w] < rho * rho ? 1 : 0;
 }
 
 struct VglParams {
@@ -470,6 +481,79 @@ qj2_status qj2_check_inputs(const qj2_functor *fn, qj2_dtype dtype,
                                                   static_cast<const double *>(R), k, P, static_cast<const double *>(r_trial), d_flag);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? QJ2_OK : cuda_fail(e, "check_kernel launch");
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-2: accept-side update (include/qmcj2.h).
+// ---------------------------------------------------------------------------
+qj2_status qj2_accept_workspace_size(int64_t W, qj2_dtype dtype, size_t *bytes) {
+    if (!bytes) return fail(QJ2_EINVAL, "bytes is NULL");
+    if (W < 0) return fail(QJ2_EINVAL, "W < 0");
+    if (dtype != QJ2_FP32 && dtype != QJ2_FP64) return fail(QJ2_EINVAL, "bad dtype");
+    *bytes = align256((size_t)W * 3 * (dtype == QJ2_FP32 ? 4 : 8));
+    return QJ2_OK;
+}
+
+qj2_status qj2_accept(const qj2_functor *fn, qj2_dtype dtype,
+                      int64_t W, int64_t N_total, int64_t N_up,
+                      int64_t i_offset, int64_t N_local, int64_t Np,
+                      void *R, void *state, const int32_t *k,
+                      const void *r_new, int64_t r_stride, const void *r_old,
+                      const int32_t *accept, const double *out_new, int64_t out_stride,
+                      void *workspace, size_t workspace_bytes, void *stream) {
+    qj2_status st = validate_functor(fn);
+    if (st) return st;
+    if (dtype != QJ2_FP32 && dtype != QJ2_FP64) return fail(QJ2_EINVAL, "bad dtype %d", (int)dtype);
+    if (W < 0) return fail(QJ2_EINVAL, "W < 0");
+    if (N_total < 2) return fail(QJ2_EINVAL, "N_total must be >= 2");
+    if (N_up < 0 || N_up > N_total) return fail(QJ2_ERANGE, "N_up out of [0, N_total]");
+    if (i_offset < 0 || N_local < 1) return fail(QJ2_EINVAL, "need i_offset >= 0 and N_local >= 1");
+    if (i_offset + N_local > N_total) return fail(QJ2_ERANGE, "i_offset + N_local > N_total");
+    if (Np < N_local || Np % vw_of(dtype) != 0)
+        return fail(QJ2_EINVAL, "Np must be >= N_local and a multiple of %d", vw_of(dtype));
+    if (out_stride < 5) return fail(QJ2_EINVAL, "out_stride must be >= 5");
+    if (r_stride < 3) return fail(QJ2_EINVAL, "r_stride must be >= 3");
+    if (W == 0) return QJ2_OK;
+    if (!R || !state || !k || !r_new || !accept || !out_new)
+        return fail(QJ2_EINVAL, "R, state, k, r_new, accept and out_new must be non-NULL");
+    if (((uintptr_t)R & 15) || ((uintptr_t)state & 15)) return fail(QJ2_EINVAL, "R and state must be 16-byte aligned");
+    size_t need = 0;
+    qj2_accept_workspace_size(W, dtype, &need);
+    if (!r_old && (!workspace || workspace_bytes < need))
+        return fail(QJ2_EINVAL, "workspace too small: need %zu bytes (or pass r_old)", need);
+    const int64_t tile = dtype == QJ2_FP32 ? accept_tile<float>() : accept_tile<double>();
+    const int64_t tpw = (N_local + tile - 1) / tile;
+    if (W * tpw > 0x7fffffffLL) return fail(QJ2_EINVAL, "problem too large for one launch");
+    st = check_device();
+    if (st) return st;
+    AcceptParams p;
+    memset(&p, 0, sizeof p);
+    p.W = W; p.N_total = N_total; p.N_up = N_up; p.i_offset = i_offset; p.N_local = N_local; p.Np = Np;
+    p.tiles_per_walker = tpw;
+    p.m = fn->m;
+    p.inv_delta = (double)fn->m / fn->r_cut;
+    p.R = R; p.state = state; p.k = k; p.r_new = r_new; p.r_stride = r_stride; p.r_old = r_old; p.accept = accept;
+    p.out_new = out_new; p.out_stride = out_stride;
+    for (int d = 0; d < 3; ++d) p.L[d] = fn->L[d];
+    power_basis(fn->coef[0], fn->m, p.pcoef);
+    power_basis(fn->coef[1], fn->m, p.pcoef + (fn->m + 1));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = dtype == QJ2_FP32 ? launch_accept_f32(p, workspace, s) : launch_accept_f64(p, workspace, s);
+    return e == cudaSuccess ? QJ2_OK : cuda_fail(e, "j2_accept_kernel launch");
+}
+
+qj2_status qj2_metropolis(int64_t W, const double *ratio, int64_t ratio_stride,
+                          const double *u, int32_t *accept, void *stream) {
+    if (W < 0) return fail(QJ2_EINVAL, "W < 0");
+    if (ratio_stride < 2) return fail(QJ2_EINVAL, "ratio_stride must be >= 2");
+    if (W == 0) return QJ2_OK;
+    if (!ratio || !u || !accept) return fail(QJ2_EINVAL, "ratio, u and accept must be non-NULL");
+    qj2_status st = check_device();
+    if (st) return st;
+    metropolis_kernel<<<(unsigned)((W + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        W, ratio, ratio_stride, u, accept);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QJ2_OK : cuda_fail(e, "metropolis_kernel launch");
 }
 
 // ---------------------------------------------------------------------------

@@ -170,6 +170,29 @@ def make_trials(seed: int, walkers, k: np.ndarray, N: int, L: float, dtype,
     return out
 
 
+def make_sweep(seed: int, W: int, N: int, L: float, dtype, steps: int):
+    """NEXT-2 sweep inputs (harness draws, no method arithmetic): for sweep step
+    s < steps, walker w moves electron k[s][w] = (k0_w + s) mod N (an ordered
+    particle-by-particle sweep, Alg. 1 L4; every electron moves at most once
+    while steps <= N, so its current position is still the generated one).
+    Returns ks [S][W] int32, trials [S][W][2][3] dtype (trial 0 = r_k, trial 1
+    = r'_k = wrap(r_k + delta), delta ~ N(0, 0.01 I)), u [S][W] fp64 uniforms
+    in [0, 1) for the Metropolis test."""
+    k0 = make_k(seed, W, N).astype(np.int64)
+    s = np.arange(steps, dtype=np.int64)[:, None]
+    ks = ((k0[None, :] + s) % N).astype(np.int32)
+    rng = np.random.default_rng([int(seed), 5])
+    delta = rng.normal(0.0, 0.1, size=(steps, W, 3))
+    u = rng.random((steps, W))
+    w = np.broadcast_to(np.arange(W, dtype=np.int64)[None, :], ks.shape)
+    rk = np.stack([position_at(seed, w, d, ks.astype(np.int64), L, dtype) for d in range(3)], axis=-1)
+    t = np.mod(rk.astype(np.float64) + delta, L).astype(dtype)
+    below = np.nextafter(np.asarray(L, dtype=dtype), np.asarray(0, dtype=dtype))
+    t = np.where(t >= np.asarray(L, dtype=dtype), below, t)
+    trials = np.stack([rk.astype(dtype), t], axis=2)
+    return ks, np.ascontiguousarray(trials), u
+
+
 # ---------------------------------------------------------------------------
 # NEXT-1 inputs: ions and per-species one-body functors.
 # Table 1 (PAPER:934-961): N / N_ion = 12 for NiO (2 species, Ni and O, 1:1),
@@ -253,6 +276,13 @@ CONFIGS = {
     "C4": Config("C4", N=6144, W=1024, dtype="f32", seed=3, instances=4096),
     "C5": Config("C5", N=4915200, W=1024, dtype="f32", seed=5),
 }
+
+
+def config(name: str) -> Config:
+    """CONFIGS[name]; "C3S" (the NEXT-2 sweep-step bench) runs on C3's instance."""
+    if name == "C3S":
+        return dataclasses.replace(CONFIGS["C3"], name="C3S")
+    return CONFIGS[name]
 
 
 def host_instance(cfg: Config, seed: int | None = None, walkers=None, P: int = 1,

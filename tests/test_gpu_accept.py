@@ -1,0 +1,222 @@
+"""GPU parity of NEXT-2 (accept-side update of R and the 5N J2 state,
+qj2_accept; Metropolis decision, qj2_metropolis) against the CPU oracle
+(oracle.accept / oracle.j2_state), through the C ABI (-m gpu; needs a B200).
+
+Tolerance: per state entry |s_gpu - s_orc| / max(A, F) <= 1e-5 (fp32 state)
+or 1e-12 (fp64), A = |s_old| + |T(r')| + |T(r)| (the oracle's bound), F the
+functor scale.  Positions: bit-exact.  Rejected walkers and padding slots:
+bitwise untouched.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import qmcgen
+
+pytestmark = pytest.mark.gpu
+
+TOL = {np.float32: 1e-5, np.float64: 1e-12}
+THREADS = os.cpu_count() or 1
+
+
+@pytest.fixture(scope="module")
+def q():
+    import paper_1708_02645_b200 as q
+    assert torch.cuda.is_available()
+    q.device_check()
+    return q
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def setup(N, W, seed, dtype, n_up=None, pad_fill=7.0):
+    L = qmcgen.cell_length(N)
+    vw = 4 if dtype == np.float32 else 2
+    Np = qmcgen.padded_size(N, vw)
+    R = qmcgen.positions(seed, np.arange(W), N, Np, L, dtype)
+    k = qmcgen.make_k(seed, W, N)
+    rt = qmcgen.make_trials(seed, np.arange(W), k, N, L, dtype)
+    fn = qmcgen.make_functor(seed, L)
+    rng = np.random.default_rng(seed)
+    state = rng.normal(size=(W, 5, Np)).astype(dtype)        # the update is additive: any state works
+    state[:, :, N:] = pad_fill
+    acc = (rng.random(W) < 0.75).astype(np.int32)
+    return R, k, rt, fn, state, acc, (N // 2 if n_up is None else n_up)
+
+
+def run_gpu(q, R, k, rt, fn, state, acc, N, n_up, **kw):
+    Rd, Sd = dev(R), dev(state)
+    out = q.eval(Rd, dev(k), dev(rt), fn, N, n_up)
+    q.accept(Rd, Sd, dev(k), dev(rt), dev(acc), out, fn, N, n_up, **kw)
+    torch.cuda.synchronize()
+    return Rd.cpu().numpy(), Sd.cpu().numpy(), out.cpu().numpy()
+
+
+def compare(R, state, acc, N, fn, dtype, Rg, Sg, R2, S2, ab):
+    assert np.array_equal(Rg.astype(np.float64), R2), "positions must be bit-exact"
+    rej = acc == 0
+    assert np.array_equal(Sg[rej], state[rej]), "rejected walkers must be untouched"
+    assert np.array_equal(Sg[:, :, N:], state[:, :, N:]), "padding must be untouched"
+    a = ~rej
+    err = oracle.normalized_error_state(Sg[a][:, :, :N], S2[a][:, :, :N], ab[a][:, :, :N], fn)
+    assert np.all(np.isfinite(Sg[a][:, :, :N]))
+    assert err.max() <= TOL[dtype], f"max normalized error {err.max():.3e}"
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("N", [2, 3, 14, 17, 1400, 4095, 8192, 8193, 20001])
+def test_accept_parity(q, dtype, N):
+    W = 33
+    R, k, rt, fn, state, acc, n_up = setup(N, W, 400 + N, dtype)
+    Rg, Sg, _ = run_gpu(q, R, k, rt, fn, state, acc, N, n_up)
+    R2, S2, ab = oracle.accept(R, state, k, rt[:, 0], acc, fn, N, n_up)
+    compare(R, state, acc, N, fn, dtype, Rg, Sg, R2, S2, ab)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_accept_k_at_tile_and_spin_boundaries(q, dtype):
+    N = 3 * 8192 + 5
+    ks = np.array([0, 1, 4095, 4096, 8191, 8192, 8193, 16384, N // 2 - 1, N // 2, N - 1], np.int32)
+    W = ks.size
+    R, _, _, fn, state, _, _ = setup(N, W, 17, dtype)
+    L = qmcgen.cell_length(N)
+    rt = qmcgen.make_trials(17, np.arange(W), ks, N, L, dtype)
+    acc = np.ones(W, np.int32)
+    for n_up in (N // 2, 8192, 0, N):
+        Rg, Sg, _ = run_gpu(q, R, ks, rt, fn, state, acc, N, n_up)
+        R2, S2, ab = oracle.accept(R, state, ks, rt[:, 0], acc, fn, N, n_up)
+        compare(R, state, acc, N, fn, dtype, Rg, Sg, R2, S2, ab)
+
+
+def test_accept_with_caller_r_old_and_empty(q):
+    N, W, dtype = 5000, 12, np.float32
+    R, k, rt, fn, state, acc, n_up = setup(N, W, 23, dtype)
+    r_old = np.ascontiguousarray(R[np.arange(W), :, k])
+    Rg, Sg, _ = run_gpu(q, R, k, rt, fn, state, acc, N, n_up, r_old=dev(r_old))
+    R2, S2, ab = oracle.accept(R, state, k, rt[:, 0], acc, fn, N, n_up)
+    compare(R, state, acc, N, fn, dtype, Rg, Sg, R2, S2, ab)
+    # W = 0 is a no-op
+    e = torch.zeros((0, 3, 16), dtype=torch.float32, device="cuda")
+    q.accept(e, torch.zeros((0, 5, 16), dtype=torch.float32, device="cuda"),
+             torch.zeros(0, dtype=torch.int32, device="cuda"), torch.zeros((0, 3), device="cuda"),
+             torch.zeros(0, dtype=torch.int32, device="cuda"), torch.zeros((0, 5), dtype=torch.float64,
+                                                                           device="cuda"), fn, 16, 8)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_accept_sharded_slices(q, dtype):
+    """Per-rank calls of a source-axis split: every slice updates its partners;
+    only the slice holding k commits r'_k and state_k (r_old from the caller)."""
+    N, W = 30000, 16
+    R, k, rt, fn, state, acc, n_up = setup(N, W, 29, dtype)
+    out = q.eval(dev(R), dev(k), dev(rt), fn, N, n_up)          # V, G, L at r'_k over all sources
+    r_old = dev(np.ascontiguousarray(R[np.arange(W), :, k]))
+    R2, S2, ab = oracle.accept(R, state, k, rt[:, 0], acc, fn, N, n_up)
+    vw = 4 if dtype == np.float32 else 2
+    for G in (2, 3):
+        bounds = [N * g // G for g in range(G + 1)]
+        Rg = np.zeros_like(R)
+        Sg = np.zeros_like(state)
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            Np = qmcgen.padded_size(b - a, vw)
+            Rs = np.zeros((W, 3, Np), dtype)
+            Rs[:, :, :b - a] = R[:, :, a:b]
+            Ss = np.zeros((W, 5, Np), dtype)
+            Ss[:, :, :b - a] = state[:, :, a:b]
+            Rd, Sd = dev(Rs), dev(Ss)
+            q.accept(Rd, Sd, dev(k), dev(rt), dev(acc), out, fn, N, n_up, i_offset=a, n_local=b - a, r_old=r_old)
+            Rg[:, :, a:b] = Rd.cpu().numpy()[:, :, :b - a]
+            Sg[:, :, a:b] = Sd.cpu().numpy()[:, :, :b - a]
+        Rg[:, :, N:] = R[:, :, N:]
+        Sg[:, :, N:] = state[:, :, N:]
+        compare(R, state, acc, N, fn, dtype, Rg, Sg, R2, S2, ab)
+
+
+def test_metropolis_decisions(q):
+    """accept = u < rho^2 (Alg. 1 L9, symmetric proposal, J2-only Psi): equal
+    to the oracle-side decision wherever u is not within 1e-9 of rho^2."""
+    N, W = 3000, 4096
+    R, k, rt, fn, _, _, n_up = setup(N, 256, 31, np.float64)
+    k = qmcgen.make_k(31, W, N)
+    R = qmcgen.positions(31, np.arange(W), N, R.shape[2], fn.L[0], np.float64)
+    rt = qmcgen.make_trials(31, np.arange(W), k, N, fn.L[0], np.float64, P=2, mode="drift")
+    u = np.random.default_rng(3).random(W)
+    out, ratio = q.eval(dev(R), dev(k), dev(rt), fn, N, n_up, ratio=True)
+    # ratio of trial 1 relative to trial 0 (V(r'_k) - V(r_k))
+    acc = q.metropolis(ratio, dev(u), trial=1).cpu().numpy()
+    orc, _, _ = oracle.eval_j2(R, k, rt, fn, N, n_up, threads=THREADS)
+    rho2 = np.exp(orc[:, 1, 0] - orc[:, 0, 0]) ** 2
+    clear = np.abs(u - rho2) > 1e-9 * np.maximum(rho2, 1e-300)
+    assert clear.mean() > 0.99
+    assert np.array_equal(acc[clear], (u < rho2)[clear].astype(np.int32))
+    assert 0 < acc.sum() < W
+
+
+def test_sweep_matches_state_from_scratch(q):
+    """20 rounds of eval -> metropolis -> accept on the GPU (fp64, N = 64),
+    started from the oracle's from-scratch state: the decisions equal the
+    oracle's own, the final state equals the from-scratch state of the final
+    configuration, and R is the oracle's sequence of accepted moves."""
+    N, W, dtype = 64, 8, np.float64
+    L = qmcgen.cell_length(N)
+    Np = qmcgen.padded_size(N, 2)
+    R = qmcgen.positions(41, np.arange(W), N, Np, L, dtype)
+    fn = qmcgen.make_functor(41, L)
+    state = np.stack([oracle.j2_state(R[w], N, N // 2, fn)[0] for w in range(W)])
+    Rd, Sd = dev(R), dev(state)
+    Rh, Sh = R.copy(), state.copy()
+    for it in range(20):
+        k = qmcgen.make_k(1000 + it, W, N)
+        rng = np.random.default_rng(2000 + it)
+        rk = Rh[np.arange(W), :, k]
+        rn = np.mod(rk + rng.normal(0, 0.4, size=(W, 3)), L)
+        rn = np.where(rn >= L, 0.0, rn)[:, None, :]
+        u = rng.random(W)
+        out, ratio = q.eval(Rd, dev(k), dev(rn), fn, N, N // 2, V_cur=Sd[torch.arange(W), 0, dev(k).long()].contiguous(),
+                            ratio=True)
+        acc = q.metropolis(ratio, dev(u))
+        q.accept(Rd, Sd, dev(k), dev(rn), acc, out, fn, N, N // 2)
+        # the oracle side takes its own decision from its own values
+        orc, _, _ = oracle.eval_j2(Rh, k, rn, fn, N, N // 2)
+        rho2 = np.exp(orc[:, 0, 0] - Sh[np.arange(W), 0, k]) ** 2
+        a = (u < rho2).astype(np.int32)
+        clear = np.abs(u - rho2) > 1e-9 * rho2
+        assert np.array_equal(acc.cpu().numpy()[clear], a[clear])
+        Rh, Sh, _ = oracle.accept(Rh, Sh, k, rn[:, 0], a, fn, N, N // 2)
+    torch.cuda.synchronize()
+    assert np.array_equal(Rd.cpu().numpy(), Rh)
+    Sg = Sd.cpu().numpy()
+    for w in range(W):
+        fresh, ab = oracle.j2_state(Rh[w], N, N // 2, fn)
+        assert oracle.normalized_error_state(Sg[w][:, :N], fresh[:, :N], ab[:, :N], fn).max() <= 1e-11
+
+
+def test_accept_C3_full_size_sampled(q):
+    """The bench's sweep step at full C3 size (N = 614,400, W = 1024, fp32):
+    eval -> accept with every walker accepted, zero initial state; sampled
+    walkers checked in full against the oracle (which regenerates their
+    positions with its own C generator)."""
+    cfg = qmcgen.CONFIGS["C3"]
+    R = q.gen_positions(cfg.seed, cfg.W, cfg.N, cfg.Np, cfg.L, torch.float32)
+    k = qmcgen.make_k(cfg.seed, cfg.W, cfg.N)
+    rt = qmcgen.make_trials(cfg.seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32)
+    fn = qmcgen.make_functor(cfg.seed, cfg.L, cfg.m)
+    S = torch.zeros((cfg.W, 5, cfg.Np), dtype=torch.float32, device="cuda")
+    acc = np.ones(cfg.W, np.int32)
+    acc[1::7] = 0
+    out = q.eval(R, dev(k), dev(rt), fn, cfg.N, cfg.n_up)
+    q.accept(R, S, dev(k), dev(rt), dev(acc), out, fn, cfg.N, cfg.n_up)
+    torch.cuda.synchronize()
+    for w in (0, 1, 511, 1023):
+        Rw = oracle.gen_positions(cfg.seed, w, 1, cfg.N, cfg.Np, cfg.L, np.float32)
+        Sw = np.zeros((1, 5, cfg.Np), np.float32)
+        R2, S2, ab = oracle.accept(Rw, Sw, k[w:w + 1], rt[w:w + 1, 0], acc[w:w + 1], fn, cfg.N, cfg.n_up)
+        compare(Rw, Sw, acc[w:w + 1], cfg.N, fn, np.float32, R[w:w + 1].cpu().numpy(),
+                S[w:w + 1].cpu().numpy(), R2, S2, ab)
+    del R, S
+    torch.cuda.empty_cache()
