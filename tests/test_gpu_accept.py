@@ -63,6 +63,8 @@ def compare(R, state, acc, N, fn, dtype, Rg, Sg, R2, S2, ab):
     assert np.array_equal(Sg[rej], state[rej]), "rejected walkers must be untouched"
     assert np.array_equal(Sg[:, :, N:], state[:, :, N:]), "padding must be untouched"
     a = ~rej
+    if not a.any():
+        return
     err = oracle.normalized_error_state(Sg[a][:, :, :N], S2[a][:, :, :N], ab[a][:, :, :N], fn)
     assert np.all(np.isfinite(Sg[a][:, :, :N]))
     assert err.max() <= TOL[dtype], f"max normalized error {err.max():.3e}"
