@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C3S"])
+    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C3S", "C3P2", "C3P12"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -202,12 +202,15 @@ class OracleSample:
             self.k, self.rt, self.u = ks[0][:self.n], tr[0][:self.n], u[0][:self.n]
             self.S = np.zeros((self.n, 5, cfg.Np))
         else:
+            P, mode = qmcgen.trial_spec(cfg.name)
             k_all = qmcgen.make_k(cfg.seed, cfg.W, cfg.N)
             self.k = k_all[:self.n]
-            self.rt = qmcgen.make_trials(cfg.seed, np.arange(cfg.W), k_all, cfg.N, cfg.L, cfg.np_dtype)[:self.n]
+            self.rt = qmcgen.make_trials(cfg.seed, np.arange(self.n), self.k, cfg.N, cfg.L, cfg.np_dtype, P=P,
+                                         mode=mode)
+        self.P = self.rt.shape[1]
         self.fn = qmcgen.make_functor(cfg.seed, cfg.L, cfg.m)
         self.R = oracle.gen_positions(cfg.seed, 0, self.n, cfg.N, cfg.Np, cfg.L, cfg.np_dtype, threads)
-        self.items = self.n * (cfg.N - 1)
+        self.items = self.n * self.P * (cfg.N - 1)
 
     def run(self):
         import oracle
@@ -221,7 +224,11 @@ class OracleSample:
 
 
 def _what(cfg):
-    return "eval P=2 + Metropolis + accept update" if cfg.name == "C3S" else "P=1"
+    import qmcgen
+    if cfg.name == "C3S":
+        return "eval P=2 + Metropolis + accept update"
+    P, mode = qmcgen.trial_spec(cfg.name)
+    return f"P={P} {mode}" if P > 1 else "P=1"
 
 
 def oracle_sample_size(cfg, cores, budget_s):
@@ -286,11 +293,15 @@ def workload_config(cfg, world):
         "C3": f"C3: one instance per rank, N={cfg.N} electrons x W={cfg.W} walkers, P=1, fp32, seed 2(+rank)",
         "C4": f"C4: 4096 instances of N={cfg.N} x W={cfg.W}, P=1, fp32, seeds 3..4098, sharded by instance",
         "C5": f"C5: one instance N={cfg.N} x W={cfg.W}, P=1, fp32, seed 5, split along N + NCCL all-reduce",
+        "C3P2": f"C3P2 (NEXT-3): C3 instance per rank (N={cfg.N} x W={cfg.W}, fp32, seed 2(+rank)), P=2 drift "
+                f"variant (U^2_k at r_k and r'_k in one step, ratio fused)",
+        "C3P12": f"C3P12 (NEXT-3): C3 instance per rank (N={cfg.N} x W={cfg.W}, fp32, seed 2(+rank)), P=12 NLPP "
+                 f"virtual moves (icosahedral quadrature sphere about a nearby ion point), ratios vs V_cur",
         "C3S": f"C3S (NEXT-2 sweep step): C3 instance per rank (N={cfg.N} x W={cfg.W}, fp32, seed 2(+rank)), "
                f"one PbyP move per walker: eval at (r_k, r'_k) -> Metropolis -> accept-side update of R and "
                f"the 5N fp32 J2 state",
     }[name]
-    return {"workload": desc, "N": cfg.N, "W": cfg.W, "P": 2 if name == "C3S" else 1, "m": cfg.m, "Np": cfg.Np,
+    return {"workload": desc, "N": cfg.N, "W": cfg.W, "P": {"C3S": 2, "C3P2": 2, "C3P12": 12}.get(name, 1), "m": cfg.m, "Np": cfg.Np,
             "parallelism": f"{'walker-instance' if name != 'C5' else 'source-axis'} x{world}",
             "l2": "inputs > 126 MB L2 (no flush needed)"}
 
@@ -567,6 +578,68 @@ class C4Plan:
         return None   # see DESIGN.md: the host-buffer path is measured on C3
 
 
+class MultiTrialPlan(C3Plan):
+    """NEXT-3: the hot path with P trial positions per walker (P = 2 drift
+    variant, P = 12 NLPP quadrature), one eval launch per step; the P trials
+    of a tile run on consecutive CTAs (one HBM read, L2 hits for the rest).
+    Issue-bound (FP32 ALU) rather than HBM-bound."""
+    launches_per_step = 2      # j2_eval_kernel + counter memset (+ ratio kernel when V_cur is not given)
+
+    def __init__(self, cfg, rank, world):
+        import qmcgen
+        super().__init__(cfg, rank, world)
+        self.mode = cfg.name
+        self.P, self.tmode = qmcgen.trial_spec(cfg.name)
+        self.items_per_step = cfg.W * self.P * (cfg.N - 1)
+        if self.tmode == "drift":
+            self.launches_per_step = 3
+
+    def _alg(self):
+        cfg = self.cfg
+        return cfg.W * (cfg.N - 1) * 12 + cfg.W * (4 + 12 * self.P + 8 + 56 * self.P)
+
+    def prepare(self, q):
+        import torch
+        import qmcgen
+        cfg = self.cfg
+        self.fn = q.Functor.of(qmcgen.make_functor(cfg.seed, cfg.L, cfg.m))
+        self.R = q.gen_positions(self.seed, cfg.W, cfg.N, cfg.Np, cfg.L, torch.float32)
+        k = qmcgen.make_k(self.seed, cfg.W, cfg.N)
+        rt = qmcgen.make_trials(self.seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32, P=self.P, mode=self.tmode)
+        rk = qmcgen.make_trials(self.seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32, mode="noop")
+        self.k = torch.from_numpy(k).cuda()
+        self.rt = torch.from_numpy(rt).cuda()
+        self.ws = q.Workspace(q.workspace_size(cfg.W, self.P, cfg.N, torch.float32))
+        self.V_cur = None
+        if self.tmode != "drift":       # NLPP ratios are relative to the current U^2_k (the caller's 5N state)
+            v0 = q.eval(self.R, self.k, torch.from_numpy(rk).cuda(), self.fn, cfg.N, cfg.n_up, workspace=self.ws)
+            self.V_cur = v0[:, 0, 0].contiguous()
+        self.out = torch.empty((cfg.W, self.P, 5), dtype=torch.float64, device="cuda")
+        self.ratio = torch.empty((cfg.W, self.P, 2), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+
+    def e2e(self, q, steps, dist_mod):
+        return None   # see DESIGN.md: the host-buffer path is measured on C3
+
+    OPS_PER_PAIR = 36          # algorithmic operations per (walker, trial, source) pair (DESIGN.md section 7)
+
+    def roofline(self, kms, peak_hbm):
+        cfg = self.cfg
+        pairs = cfg.W * self.P * (cfg.N - 1)
+        ops = pairs * self.OPS_PER_PAIR
+        clk = 1.965e9
+        peak = 148 * 128 * clk / 1e12           # one FP32/ALU op per lane per clock (the issue ceiling), T/s
+        achieved = ops / (kms / 1e3) / 1e12
+        hbm = self._alg() / (kms / 1e3) / 1e9
+        return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": committed_traffic(self.mode), "kernel": "j2_eval_kernel<float,1,false>", "kernel_ms": kms,
+                "alg_ops_per_launch": ops, "ops_per_pair": self.OPS_PER_PAIR,
+                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1.965 GHz, one op per lane per clock "
+                               "(B200_PROFILING.md unit counts; DESIGN.md section 7)",
+                "hbm": {"achieved": hbm, "peak": peak_hbm, "unit": "GB/s", "frac": hbm / peak_hbm,
+                        "alg_bytes_per_launch": self._alg()}}
+
+
 class SweepPlan:
     """NEXT-2: one particle-by-particle move per walker and step on a C3 instance
     (Alg. 1 L5-L9 for the J2 factor): qj2_eval with P = 2 (U^2_k at r_k and
@@ -640,6 +713,8 @@ class SweepPlan:
 
 
 def make_plan(cfg, rank, world):
+    if cfg.name in ("C3P2", "C3P12"):
+        return MultiTrialPlan(cfg, rank, world)
     if cfg.name == "C3S":
         return SweepPlan(cfg, rank, world)
     if cfg.name == "C3":
@@ -728,13 +803,14 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "weak" if plan.mode in ("C3", "C3S") else "strong",
+            "scaling": "weak" if plan.mode in ("C3", "C3S", "C3P2", "C3P12") else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(cfg, world),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": plan_kernel_name(plan), "kernel_ms": kms,
-                         "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src},
+            "roofline": (plan.roofline(kms, peak) if hasattr(plan, "roofline") else
+                         {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                          "frac": achieved / peak, "traffic": traffic,
+                          "kernel": plan_kernel_name(plan), "kernel_ms": kms,
+                          "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src}),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": plan.launches_per_step * args.steps,

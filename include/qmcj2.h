@@ -136,8 +136,9 @@ qj2_status qj2_eval_workspace_size(int64_t W, int32_t P, int64_t N_local,
 /*   V_cur     device [W] fp64 or NULL: U^2_k(R) from the caller's 5N state  */
 /*              for the ratio below.                        */
 /*   ratio_out device [W][P][2] fp64 or NULL: (dJ2, exp(dJ2)) with           */
-/*             dJ2 = V_p - V_cur[w] (or V_p - V_0 when V_cur == NULL and     */
-/*             P <= 4): the e^{dJ2} factor of Eq. 4.   */
+/*             dJ2 = V_p - V_cur[w] (or V_p - V_0 when V_cur == NULL; for    */
+/*             P > 1 that is a second, tiny launch after the reduction):     */
+/*             the e^{dJ2} factor of Eq. 4.            */
 /*             Only for unsharded calls (i_offset == 0, N_local == N_total); */
 /*             sharded callers reduce `out` first and call qj2_ratio.        */
 /*   workspace device scratch >= qj2_eval_workspace_size() (per-tile fp64   */

@@ -457,16 +457,18 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
     __shared__ double red[TPB / 32][PB * ND];
     __shared__ int last_flag;
 
-    // tile decode: chunk fastest so consecutive CTAs stream consecutive memory
-    // (32-bit arithmetic: the host guarantees W * n_groups * tiles < 2^31)
+    // tile decode: trial group fastest, then tile, then walker, so the CTAs of
+    // one tile's trial groups run together (one HBM read, L2 hits for the
+    // others) and consecutive tiles stream consecutive memory (32-bit
+    // arithmetic: the host guarantees W * n_groups * tiles < 2^31)
     const uint32_t b = blockIdx.x;
-    const uint32_t tpw32 = (uint32_t)p.tiles_per_walker;
-    const uint32_t per_w = tpw32 * (uint32_t)p.n_groups;
+    const uint32_t ng32 = (uint32_t)p.n_groups;
+    const uint32_t per_w = (uint32_t)p.tiles_per_walker * ng32;
     const uint32_t w32 = b / per_w;
     const uint32_t rem = b - w32 * per_w;
-    const uint32_t g32 = rem / tpw32;
+    const uint32_t c32 = rem / ng32;
     const int64_t tpw = p.tiles_per_walker;
-    const int64_t w = w32, g = g32, c = rem - g32 * tpw32;
+    const int64_t w = w32, c = c32, g = rem - c32 * ng32;
     const int32_t p0 = (int32_t)g * PB;
     const int np = min(PB, p.P - p0);
 

@@ -92,8 +92,7 @@ cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStre
 // Per translation unit entry points (see launch_*.cu): <dtype>_<trial batch>_<mode>.
 #define QJ2_DECL(NAME) \
     cudaError_t NAME(const EvalParams &p, int pb, int64_t nblocks, bool row, cudaStream_t s);
-QJ2_DECL(launch_f32_pb1_j2) QJ2_DECL(launch_f32_pbn_j2) QJ2_DECL(launch_f64_pb1_j2) QJ2_DECL(launch_f64_pbn_j2)
-QJ2_DECL(launch_f32_pb1_j1) QJ2_DECL(launch_f32_pbn_j1) QJ2_DECL(launch_f64_pb1_j1) QJ2_DECL(launch_f64_pbn_j1)
+QJ2_DECL(launch_f32_pb1_j2) QJ2_DECL(launch_f64_pb1_j2) QJ2_DECL(launch_f32_pb1_j1) QJ2_DECL(launch_f64_pb1_j1)
 #undef QJ2_DECL
 
 }  // namespace qj2

@@ -182,7 +182,12 @@ void power_basis(const double *c, int m, double (*pc)[4]) {
 
 inline int vw_of(qj2_dtype d) { return d == QJ2_FP32 ? 4 : 2; }
 inline int64_t ch_of(qj2_dtype d) { return (int64_t)TPB * vw_of(d) * ITERS * SUB; }
-inline int pb_of(int32_t P) { return P == 1 ? 1 : P == 2 ? 2 : MAXPB; }
+// Trials per CTA (or warp): always 1.  The P trials of a walker's tile run on
+// P consecutive CTAs, so the tile is read from HBM once and from L2 by the
+// other P - 1 (measured on B200 against 2 and 4 trials per thread, which
+// need 124-127 registers and run at 2 CTAs/SM: P = 2 1.84 vs 2.79 ms,
+// P = 12 10.3 vs 20.8 ms on C3).
+inline int pb_of(int32_t) { return 1; }
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 void ws_layout(int64_t W, int32_t P, int64_t N_local, qj2_dtype dtype,
@@ -221,14 +226,27 @@ qj2_status launch_common(EvalParams &p, qj2_dtype dtype, int pb, int64_t ng, voi
     }
     const bool j1 = p.mode == MODE_J1;
     if (dtype == QJ2_FP32) {
-        if (pb == 1) e = j1 ? launch_f32_pb1_j1(p, pb, nblocks, row, stream) : launch_f32_pb1_j2(p, pb, nblocks, row, stream);
-        else         e = j1 ? launch_f32_pbn_j1(p, pb, nblocks, row, stream) : launch_f32_pbn_j2(p, pb, nblocks, row, stream);
+        e = j1 ? launch_f32_pb1_j1(p, pb, nblocks, row, stream) : launch_f32_pb1_j2(p, pb, nblocks, row, stream);
     } else {
-        if (pb == 1) e = j1 ? launch_f64_pb1_j1(p, pb, nblocks, row, stream) : launch_f64_pb1_j2(p, pb, nblocks, row, stream);
-        else         e = j1 ? launch_f64_pbn_j1(p, pb, nblocks, row, stream) : launch_f64_pbn_j2(p, pb, nblocks, row, stream);
+        e = j1 ? launch_f64_pb1_j1(p, pb, nblocks, row, stream) : launch_f64_pb1_j2(p, pb, nblocks, row, stream);
     }
     if (e != cudaSuccess) return cuda_fail(e, "j2_eval_kernel launch");
     return QJ2_OK;
+}
+
+// The fused ratio relative to trial 0 (V_cur == NULL) needs trial 0 in the
+// same trial group; otherwise the ratio is a second (tiny) launch.
+qj2_status launch_with_ratio(EvalParams &p, qj2_dtype dtype, int pb, int64_t ng, void *workspace,
+                             size_t workspace_bytes, cudaStream_t stream, bool check_dev) {
+    double *ratio_out = p.ratio_out;
+    const bool after = ratio_out && !p.V_cur && ng > 1;
+    if (after) p.ratio_out = nullptr;
+    qj2_status st = launch_common(p, dtype, pb, ng, workspace, workspace_bytes, stream, check_dev);
+    if (st || !after) return st;
+    const int64_t n = p.W * p.P;
+    ratio_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(p.W, p.P, p.out, nullptr, ratio_out);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QJ2_OK : cuda_fail(e, "ratio_kernel launch");
 }
 
 qj2_status eval_impl(const qj2_functor *fn, qj2_dtype dtype,
@@ -253,7 +271,6 @@ qj2_status eval_impl(const qj2_functor *fn, qj2_dtype dtype,
     if (ratio_out) {
         if (i_offset != 0 || N_local != N_total)
             return fail(QJ2_EINVAL, "ratio_out needs an unsharded call; use qj2_ratio after reducing");
-        if (!V_cur && ng != 1) return fail(QJ2_EINVAL, "ratio_out with V_cur == NULL needs P <= %d", MAXPB);
     }
     if (W == 0) return QJ2_OK;
     if (!R || !k || !r_trial || !out) return fail(QJ2_EINVAL, "R, k, r_trial and out must be non-NULL");
@@ -275,7 +292,7 @@ qj2_status eval_impl(const qj2_functor *fn, qj2_dtype dtype,
     power_basis(fn->coef[0], fn->m, p.pcoef);                  // rows [0, m]: same spin
     power_basis(fn->coef[1], fn->m, p.pcoef + (fn->m + 1));    // rows [m+1, 2m+1]: opposite spin
     p.n_tab = 2 * (fn->m + 1);
-    return launch_common(p, dtype, pb, ng, workspace, workspace_bytes, stream, check_dev);
+    return launch_with_ratio(p, dtype, pb, ng, workspace, workspace_bytes, stream, check_dev);
 }
 
 qj2_status validate_j1_functor(const qj2_j1_functor *fn) {
@@ -317,7 +334,6 @@ qj2_status eval_j1_impl(const qj2_j1_functor *fn, qj2_dtype dtype, int64_t W, co
     if (P < 1 || P > QJ2_MAX_P) return fail(QJ2_EINVAL, "P must be in [1, %d]", QJ2_MAX_P);
     const int pb = pb_of(P);
     const int64_t ng = (P + pb - 1) / pb;
-    if (ratio_out && !V_cur && ng != 1) return fail(QJ2_EINVAL, "ratio_out with V_cur == NULL needs P <= %d", MAXPB);
     if (W == 0) return QJ2_OK;
     if (!ions || !r_trial || !out) return fail(QJ2_EINVAL, "ions, r_trial and out must be non-NULL");
 
@@ -341,7 +357,7 @@ qj2_status eval_j1_impl(const qj2_j1_functor *fn, qj2_dtype dtype, int64_t W, co
     p.R = ions; p.k = nullptr; p.r_trial = r_trial; p.out = out; p.row_out = row_out;
     p.V_cur = V_cur; p.ratio_out = ratio_out;
     for (int d = 0; d < 3; ++d) p.L[d] = fn->L[d];
-    return launch_common(p, dtype, pb, ng, workspace, workspace_bytes, stream, true);
+    return launch_with_ratio(p, dtype, pb, ng, workspace, workspace_bytes, stream, true);
 }
 
 }  // namespace

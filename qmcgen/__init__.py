@@ -147,7 +147,15 @@ def make_trials(seed: int, walkers, k: np.ndarray, N: int, L: float, dtype,
     mode="drift": p = 0 is r_k itself (current position), p >= 1 are moves
                   (the P = 2 variant: value at R and at R' in one pass).
     mode="noop":  every p is r_k (no-op move).
+    mode="nlpp":  P = 12 virtual moves of electron k onto the 12-point
+                  icosahedral quadrature sphere about a nearby "ion" point
+                  r_I ("quadrature on a spherical
+                  shell"): r_q = wrap(r_I + |r_k - r_I| R v_q), v_q the unit
+                  icosahedron vertices, R a random rotation per walker,
+                  |r_k - r_I| ~ U[0.3, 1.0) (density-1 units).
     """
+    if mode == "nlpp":
+        return _nlpp_trials(seed, walkers, k, N, L, dtype, P)
     walkers = np.asarray(walkers, dtype=np.int64).reshape(-1)
     W = walkers.size
     rng = np.random.default_rng([int(seed), 3])
@@ -168,6 +176,46 @@ def make_trials(seed: int, walkers, k: np.ndarray, N: int, L: float, dtype,
         t = np.where(t >= np.asarray(L, dtype=dtype), below, t)
         out[:, p, :] = t
     return out
+
+
+def _icosahedron() -> np.ndarray:
+    g = (1.0 + 5.0 ** 0.5) / 2.0
+    v = []
+    for a in (-1.0, 1.0):
+        for b in (-g, g):
+            v += [(0.0, a, b), (a, b, 0.0), (b, 0.0, a)]
+    v = np.array(v)
+    return v / np.linalg.norm(v, axis=1, keepdims=True)
+
+
+def _nlpp_trials(seed, walkers, k, N, L, dtype, P):
+    if P != 12:
+        raise ValueError("mode='nlpp' is the 12-point icosahedral rule (P = 12)")
+    walkers = np.asarray(walkers, dtype=np.int64).reshape(-1)
+    W = walkers.size
+    rng = np.random.default_rng([int(seed), 6])
+    nmax = int(walkers.max()) + 1 if W else 0
+    q = rng.normal(size=(nmax, 4))[walkers] if W else np.zeros((0, 4))          # random rotations
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    u_dir = rng.normal(size=(nmax, 3))[walkers] if W else np.zeros((0, 3))       # ion direction
+    u_dir /= np.linalg.norm(u_dir, axis=1, keepdims=True)
+    rad = rng.uniform(0.3, 1.0, size=nmax)[walkers] if W else np.zeros(0)
+    rk = np.stack([position_at(seed, walkers, d, k.astype(np.int64), L, dtype) for d in range(3)],
+                  axis=-1).astype(np.float64)
+    rI = rk + rad[:, None] * u_dir
+    a, b, c, d = q.T
+    Rm = np.stack([np.stack([1 - 2 * (c * c + d * d), 2 * (b * c - a * d), 2 * (b * d + a * c)], -1),
+                   np.stack([2 * (b * c + a * d), 1 - 2 * (b * b + d * d), 2 * (c * d - a * b)], -1),
+                   np.stack([2 * (b * d - a * c), 2 * (c * d + a * b), 1 - 2 * (b * b + c * c)], -1)], 1)
+    v = np.einsum("wij,qj->wqi", Rm, _icosahedron())
+    t = np.mod(rI[:, None, :] + rad[:, None, None] * v, L).astype(dtype)
+    below = np.nextafter(np.asarray(L, dtype=dtype), np.asarray(0, dtype=dtype))
+    return np.where(t >= np.asarray(L, dtype=dtype), below, t)
+
+
+def trial_spec(name: str):
+    """(P, make_trials mode) of a bench configuration."""
+    return {"C3P2": (2, "drift"), "C3P12": (12, "nlpp")}.get(name, (1, "move"))
 
 
 def make_sweep(seed: int, W: int, N: int, L: float, dtype, steps: int):
@@ -279,9 +327,11 @@ CONFIGS = {
 
 
 def config(name: str) -> Config:
-    """CONFIGS[name]; "C3S" (the NEXT-2 sweep-step bench) runs on C3's instance."""
-    if name == "C3S":
-        return dataclasses.replace(CONFIGS["C3"], name="C3S")
+    """CONFIGS[name]; "C3S" (the NEXT-2 sweep-step bench) and "C3P2" / "C3P12"
+    (NEXT-3 multi-trial benches: P = 2 drift variant, P = 12 NLPP quadrature)
+    run on C3's instance."""
+    if name in ("C3S", "C3P2", "C3P12"):
+        return dataclasses.replace(CONFIGS["C3"], name=name)
     return CONFIGS[name]
 
 

@@ -87,7 +87,8 @@ def test_eval_host_validation(q):
     assert _call_eval(q, f, R=None)[0] == 1
     assert _call_eval(q, f, R=ctypes.c_void_p(4100))[0] == 1     # misaligned
     assert _call_eval(q, f, i_offset=10, N_local=20, ratio=ctypes.c_void_p(4096))[0] == 1
-    assert _call_eval(q, f, P=8, ratio=ctypes.c_void_p(4096))[0] == 1   # needs V_cur
+    # any P may fuse the ratio relative to trial 0 (a second launch when P > 1): passes validation
+    assert _call_eval(q, f, P=8, ratio=ctypes.c_void_p(4096))[0] != 1
     assert _call_eval(q, f, W=0) == (0, _call_eval(q, f, W=0)[1])      # no-op
     st, msg = _call_eval(q, f, N_local=1 << 20, Np=1 << 20, N_total=1 << 20, wsb=16)
     assert st == 1 and "workspace" in msg

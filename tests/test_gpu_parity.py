@@ -388,3 +388,46 @@ def test_C4_batched_waves_as_benched(q):
             g = j * W + wl
             orc, absout, _ = oracle.eval_j2(Rs, k[g:g + 1], rt[g:g + 1], fn, cfg.N, cfg.n_up)
             assert oracle.normalized_error(out[g:g + 1], orc, absout, fn).max() <= TOL[np.float32]
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3: multi-trial batches (one trial per CTA, the P trials of a tile on
+# consecutive CTAs): P = 12 NLPP quadrature virtual moves, P = 2 drift, ratios
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_nlpp_P12(q, dtype):
+    N, W = 20001, 16
+    L = qmcgen.cell_length(N)
+    R, k, _, fn, n_up = instance(N, W, seed=61, dtype=dtype)
+    rt = qmcgen.make_trials(61, np.arange(W), k, N, L, dtype, P=12, mode="nlpp")
+    out, orc = check(q, R, k, rt, fn, N, n_up, dtype)
+    # ratios relative to the caller's V_cur and relative to trial 0 (second launch)
+    vcur = dev(orc[:, 0, 0].copy())
+    _, r1 = q.eval(dev(R), dev(k), dev(rt), fn, N, n_up, V_cur=vcur, ratio=True)
+    _, r0 = q.eval(dev(R), dev(k), dev(rt), fn, N, n_up, ratio=True)
+    r1, r0 = r1.cpu().numpy(), r0.cpu().numpy()
+    np.testing.assert_allclose(r1[:, :, 0], out[:, :, 0] - orc[:, :1, 0], rtol=0, atol=1e-9 * np.abs(out).max())
+    assert np.all(r0[:, 0, 0] == 0.0) and np.all(r0[:, 0, 1] == 1.0)
+    np.testing.assert_allclose(r0[:, :, 1], np.exp(out[:, :, 0] - out[:, :1, 0]), rtol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["C3P2", "C3P12"])
+def test_multi_trial_full_size_sampled(q, name):
+    """The NEXT-3 bench workloads at full C3 size (N = 614,400, W = 1024, fp32)
+    in the bench launch configuration; sampled walkers vs the oracle."""
+    cfg = qmcgen.config(name)
+    P, mode = qmcgen.trial_spec(name)
+    R = q.gen_positions(cfg.seed, cfg.W, cfg.N, cfg.Np, cfg.L, torch.float32)
+    k = qmcgen.make_k(cfg.seed, cfg.W, cfg.N)
+    rt = qmcgen.make_trials(cfg.seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32, P=P, mode=mode)
+    fn = qmcgen.make_functor(cfg.seed, cfg.L, cfg.m)
+    out = q.eval(R, dev(k), dev(rt), fn, cfg.N, cfg.n_up).cpu().numpy()
+    del R
+    torch.cuda.empty_cache()
+    ws = np.array([0, 600, 1023])
+    Rs = oracle.gen_positions(cfg.seed, 0, 1, cfg.N, cfg.Np, cfg.L, np.float32)
+    for w in ws:
+        Rs = oracle.gen_positions(cfg.seed, int(w), 1, cfg.N, cfg.Np, cfg.L, np.float32)
+        orc, absout, _ = oracle.eval_j2(Rs, k[w:w + 1], rt[w:w + 1], fn, cfg.N, cfg.n_up, threads=THREADS)
+        err = oracle.normalized_error(out[w:w + 1], orc, absout, fn)
+        assert err.max() <= TOL[np.float32], err.max()
