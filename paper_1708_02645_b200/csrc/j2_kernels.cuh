@@ -21,7 +21,10 @@ namespace qj2 {
 
 constexpr int TPB = 256;          // threads per CTA
 constexpr int ITERS = 8;          // vector iterations per sub-tile: 32 fp32 terms per thread per trial
-constexpr int SUB = 4;            // sub-tiles per CTA tile
+#ifndef QJ2_SUB
+#define QJ2_SUB 4
+#endif
+constexpr int SUB = QJ2_SUB;      // sub-tiles per CTA tile (A/B builds: -DQJ2_SUB=n)
 constexpr int NACC = 6;           // fp32 accumulators per trial: V, Gx, Gy, Gz, sum h, sum du/r
 constexpr int NOUT = 5;           // fp64 physical outputs per trial: V, Gx, Gy, Gz, L
 constexpr int MAXPB = 4;
