@@ -262,3 +262,50 @@ def normalized_error_state(gpu, orc, absst, fn) -> np.ndarray:
     delta = fn.r_cut / fn.m
     F = np.array([cmax, cmax / delta, cmax / delta, cmax / delta, cmax / delta ** 2])[:, None]
     return np.abs(np.asarray(gpu, dtype=np.float64) - orc) / np.maximum(np.nan_to_num(absst, nan=0.0), F)
+
+
+def _lib_next4():
+    L = lib()
+    if not getattr(L, "_next4", False):
+        dp = ctypes.POINTER(ctypes.c_double)
+        i64 = ctypes.c_int64
+        L.orc_spo_vgh.restype = None
+        L.orc_spo_vgh.argtypes = [i64, i64, i64, i64, i64, ctypes.c_void_p, dp, dp, dp, dp, dp, dp]
+        L.orc_det_ratio.restype = None
+        L.orc_det_ratio.argtypes = [i64, dp, dp, dp, dp, dp, dp]
+        L._next4 = True
+    return L
+
+
+def spo_vgh(table, n_orb: int, L, pos):
+    """NEXT-4 oracle of the tricubic B-spline SPOs (orc_spo_vgh).
+    table: fp32 [nx][ny][nz][ld]; pos [M][3].  Returns v [M][n_orb],
+    g [M][3][n_orb], h [M][6][n_orb] (xx, xy, xz, yy, yz, zz) and abs
+    [M][10][n_orb], fp64."""
+    T = np.ascontiguousarray(np.asarray(table, dtype=np.float32))
+    nx, ny, nz, ld = T.shape
+    pos = _f64(np.atleast_2d(pos))
+    M = pos.shape[0]
+    v = np.zeros((M, n_orb)); g = np.zeros((M, 3, n_orb)); h = np.zeros((M, 6, n_orb))
+    ab = np.zeros((M, 10, n_orb))
+    Lv = _f64(np.broadcast_to(np.asarray(L, dtype=np.float64), (3,)))
+    lb = _lib_next4()
+    for m in range(M):
+        vm, gm, hm, am = v[m], g[m], h[m], ab[m]
+        lb.orc_spo_vgh(nx, ny, nz, n_orb, ld, T.ctypes.data_as(ctypes.c_void_p), _dp(Lv),
+                       _dp(np.ascontiguousarray(pos[m])), _dp(vm), _dp(gm), _dp(hm), _dp(am))
+    return v, g, h, ab
+
+
+def det_ratio(Ainv_rows, v, g, h):
+    """NEXT-4 oracle of the determinant ratio (orc_det_ratio): per row m,
+    (rho, G, L) = (sum a.phi, sum a.grad phi / rho, sum a.lap phi / rho) and the
+    absolute-term sums.  Ainv_rows [M][n], v [M][n], g [M][3][n], h [M][6][n]."""
+    A = _f64(np.atleast_2d(Ainv_rows))
+    M, n = A.shape
+    out = np.zeros((M, 5)); ab = np.zeros((M, 5))
+    lb = _lib_next4()
+    for m in range(M):
+        lb.orc_det_ratio(n, _dp(np.ascontiguousarray(A[m])), _dp(_f64(v[m])), _dp(_f64(g[m])),
+                         _dp(_f64(h[m])), _dp(out[m]), _dp(ab[m]))
+    return out, ab

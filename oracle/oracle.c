@@ -552,3 +552,133 @@ int64_t orc_accept(const double L[3], double r_cut, int m, const double *coef,
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-4: tricubic B-spline single-particle orbitals and the determinant     */
+/* ratio.                                                                     */
+/*                                                                            */
+/* SPOs phi_o(r), o < n_orb, from a read-only 3D B-spline table shared by all */
+/* walkers ("the read-only 3D B-spline table which is shared  */
+/* by all the threads"; Table 1 "FFT grid", "# of unique SPOs", PAPER:936-    */
+/* 958; kernels "Bspline-v" and "Bspline-vgh").   */
+/* Reading R22: uniform periodic tricubic B-spline on an          */
+/* nx x ny x nz grid over the cell, coefficients P[ix][iy][iz][o] (orbital    */
+/* fastest, stride ld >= n_orb), for coordinate u = x/L_x * nx (x wrapped     */
+/* into [0, L_x)): i = floor(u), t = u - i, basis B_a(t) as in orc_bspline,   */
+/* control points (i - 1 + a) mod nx, a = 0..3; likewise y, z:                */
+/*   phi_o = sum_{a,b,c} B_a(tx) B_b(ty) B_c(tz) P[(ix-1+a)%nx][..][..][o],   */
+/* gradient and Hessian from the analytic basis derivatives scaled by nx/L_x  */
+/* etc.  Outputs v[o], g[3][o], h[6][o] (xx, xy, xz, yy, yz, zz), fp64.       */
+/* abs_out (optional, [10][n_orb]) receives the same sums over |weights*P|.   */
+/* ------------------------------------------------------------------------ */
+static void basis3(double t, double B[4], double D[4], double S[4])
+{
+    double g = 1.0 - t;
+    B[0] = g * g * g / 6.0;
+    B[1] = (3.0 * t * t * t - 6.0 * t * t + 4.0) / 6.0;
+    B[2] = (-3.0 * t * t * t + 3.0 * t * t + 3.0 * t + 1.0) / 6.0;
+    B[3] = t * t * t / 6.0;
+    D[0] = -0.5 * g * g;
+    D[1] = 0.5 * (3.0 * t * t - 4.0 * t);
+    D[2] = 0.5 * (-3.0 * t * t + 2.0 * t + 1.0);
+    D[3] = 0.5 * t * t;
+    S[0] = 1.0 - t;
+    S[1] = 3.0 * t - 2.0;
+    S[2] = 1.0 - 3.0 * t;
+    S[3] = t;
+}
+
+static void axis_setup(double x, double L, int64_t n, int64_t idx[4], double B[4], double D[4],
+                       double S[4], double *scale)
+{
+    double xw = fmod(x, L);
+    if (xw < 0) xw += L;
+    double u = xw / L * (double)n;
+    double fi = floor(u);
+    double t = u - fi;
+    int64_t i = (int64_t)fi;
+    if (i >= n) { i -= n; }          /* u == n after rounding */
+    for (int a = 0; a < 4; ++a) idx[a] = ((i - 1 + a) % n + n) % n;
+    basis3(t, B, D, S);
+    *scale = (double)n / L;
+}
+
+void orc_spo_vgh(int64_t nx, int64_t ny, int64_t nz, int64_t n_orb, int64_t ld,
+                 const float *P, const double L[3], const double pos[3],
+                 double *v, double *g, double *h, double *abs_out)
+{
+    int64_t ix[4], iy[4], iz[4];
+    double Bx[4], Dx[4], Sx[4], By[4], Dy[4], Sy[4], Bz[4], Dz[4], Sz[4], sx, sy, sz;
+    axis_setup(pos[0], L[0], nx, ix, Bx, Dx, Sx, &sx);
+    axis_setup(pos[1], L[1], ny, iy, By, Dy, Sy, &sy);
+    axis_setup(pos[2], L[2], nz, iz, Bz, Dz, Sz, &sz);
+    for (int64_t o = 0; o < n_orb; ++o) {
+        nsum acc[10], aab[10];
+        for (int c = 0; c < 10; ++c) { acc[c].s = acc[c].c = 0.0; aab[c].s = aab[c].c = 0.0; }
+        for (int a = 0; a < 4; ++a)
+            for (int b = 0; b < 4; ++b)
+                for (int c = 0; c < 4; ++c) {
+                    double p = (double)P[((ix[a] * ny + iy[b]) * nz + iz[c]) * ld + o];
+                    double w[10] = {
+                        Bx[a] * By[b] * Bz[c],                       /* v   */
+                        Dx[a] * By[b] * Bz[c] * sx,                  /* gx  */
+                        Bx[a] * Dy[b] * Bz[c] * sy,                  /* gy  */
+                        Bx[a] * By[b] * Dz[c] * sz,                  /* gz  */
+                        Sx[a] * By[b] * Bz[c] * sx * sx,             /* hxx */
+                        Dx[a] * Dy[b] * Bz[c] * sx * sy,             /* hxy */
+                        Dx[a] * By[b] * Dz[c] * sx * sz,             /* hxz */
+                        Bx[a] * Sy[b] * Bz[c] * sy * sy,             /* hyy */
+                        Bx[a] * Dy[b] * Dz[c] * sy * sz,             /* hyz */
+                        Bx[a] * By[b] * Sz[c] * sz * sz };           /* hzz */
+                    for (int q = 0; q < 10; ++q) {
+                        nsum_add(&acc[q], w[q] * p);
+                        nsum_add(&aab[q], fabs(w[q] * p));
+                    }
+                }
+        v[o] = nsum_get(&acc[0]);
+        for (int d = 0; d < 3; ++d) g[d * n_orb + o] = nsum_get(&acc[1 + d]);
+        for (int q = 0; q < 6; ++q) h[q * n_orb + o] = nsum_get(&acc[4 + q]);
+        if (abs_out)
+            for (int q = 0; q < 10; ++q) abs_out[q * n_orb + o] = nsum_get(&aab[q]);
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Determinant ratio of a move of electron k (Eq. 6: "a dot    */
+/* product of the k-th row of A^{-1} and v(phi_1(r'_k), ..., phi_{N/2}(r'_k))"*/
+/* via det(A + u e_k') = (1 + e_k' A^{-1} u) det(A)), with A(i,j) = phi_i(r_j)*/
+/* (PAPER:821-823), and the same lemma for the derivatives:   */
+/*   rho = sum_i Ainv[k][i] phi_i(r'),                                        */
+/*   G   = sum_i Ainv[k][i] grad phi_i(r') / rho     (= grad_k ln D at R'),   */
+/*   L   = sum_i Ainv[k][i] lap phi_i(r') / rho      (= lap_k D / D at R').   */
+/* Here "row k of A^{-1}" is A^{-1}[k][:] with A^{-1} A = I, so that          */
+/* sum_i Ainv[k][i] A(i,j) = delta_kj (reading R23).  out = (rho, Gx, Gy, Gz, */
+/* L); abs_out = the sums of |terms| (for rho) used by the tolerance.         */
+/* ------------------------------------------------------------------------ */
+void orc_det_ratio(int64_t n, const double *Ainv_row, const double *v, const double *g,
+                   const double *h, double out[5], double abs_out[5])
+{
+    nsum r = {0, 0}, G[3] = {{0, 0}, {0, 0}, {0, 0}}, Lp = {0, 0};
+    nsum ar = {0, 0}, aG[3] = {{0, 0}, {0, 0}, {0, 0}}, aL = {0, 0};
+    for (int64_t i = 0; i < n; ++i) {
+        double a = Ainv_row[i];
+        nsum_add(&r, a * v[i]);
+        nsum_add(&ar, fabs(a * v[i]));
+        for (int d = 0; d < 3; ++d) {
+            nsum_add(&G[d], a * g[d * n + i]);
+            nsum_add(&aG[d], fabs(a * g[d * n + i]));
+        }
+        double lap = h[0 * n + i] + h[3 * n + i] + h[5 * n + i];
+        nsum_add(&Lp, a * lap);
+        nsum_add(&aL, fabs(a * h[0 * n + i]) + fabs(a * h[3 * n + i]) + fabs(a * h[5 * n + i]));
+    }
+    double rho = nsum_get(&r);
+    out[0] = rho;
+    for (int d = 0; d < 3; ++d) out[1 + d] = nsum_get(&G[d]) / rho;
+    out[4] = nsum_get(&Lp) / rho;
+    if (abs_out) {
+        abs_out[0] = nsum_get(&ar);
+        for (int d = 0; d < 3; ++d) abs_out[1 + d] = nsum_get(&aG[d]);
+        abs_out[4] = nsum_get(&aL);
+    }
+}

@@ -242,6 +242,49 @@ def make_sweep(seed: int, W: int, N: int, L: float, dtype, steps: int):
 
 
 # ---------------------------------------------------------------------------
+# NEXT-4 inputs: a synthetic 3D B-spline SPO coefficient table (Table 1 grid
+# and orbital counts; the real DFT orbitals are not available)
+# and A^{-1} rows.  Coefficient (ix, iy, iz, o) = u*2 - 1 with u the top 24
+# bits of mix64(key' ^ flat index) times 2^-24 (exact in fp32); lanes
+# [n_orb, ld) are 0.  The device twin is qj2gen_spo_table.
+# ---------------------------------------------------------------------------
+SPO_SALT = 0x5A0C0EFF1C1E17A5
+
+
+def spo_key(seed: int) -> np.uint64:
+    return mix64(np.array([int(seed_key(seed)) ^ SPO_SALT], dtype=np.uint64))[0]
+
+
+def spo_table(seed: int, nx: int, ny: int, nz: int, n_orb: int, ld: int | None = None) -> np.ndarray:
+    """fp32 [nx][ny][nz][ld] coefficient table (small grids: host generation)."""
+    ld = n_orb if ld is None else ld
+    key = spo_key(seed)
+    idx = np.arange(nx * ny * nz * ld, dtype=np.uint64)
+    h = mix64(idx ^ key)
+    u = (h >> np.uint64(40)).astype(np.float32) * np.float32(2.0 ** -23) - np.float32(1.0)
+    t = u.reshape(nx, ny, nz, ld)
+    t[..., n_orb:] = 0.0
+    return t
+
+
+def spo_table_rows(seed: int, nx: int, ny: int, nz: int, ld: int, n_orb: int, rows) -> np.ndarray:
+    """Rows (ix, iy, iz) of the table, [len(rows)][ld] fp32, for sampled checks of big tables."""
+    rows = np.asarray(rows, dtype=np.int64).reshape(-1, 3)
+    flat = ((rows[:, 0] * ny + rows[:, 1]) * nz + rows[:, 2]).astype(np.uint64)
+    idx = flat[:, None] * np.uint64(ld) + np.arange(ld, dtype=np.uint64)[None, :]
+    h = mix64(idx ^ spo_key(seed))
+    u = (h >> np.uint64(40)).astype(np.float32) * np.float32(2.0 ** -23) - np.float32(1.0)
+    u[:, n_orb:] = 0.0
+    return u
+
+
+def make_ainv_rows(seed: int, W: int, n: int) -> np.ndarray:
+    """Synthetic rows k of A^{-1} per walker, fp32 [W][n], U[-1, 1)/sqrt(n)."""
+    rng = np.random.default_rng([int(seed), 7])
+    return ((rng.random((W, n)) * 2 - 1) / np.sqrt(n)).astype(np.float32)
+
+
+# ---------------------------------------------------------------------------
 # NEXT-1 inputs: ions and per-species one-body functors.
 # Table 1 (PAPER:934-961): N / N_ion = 12 for NiO (2 species, Ni and O, 1:1),
 # 4 for graphite (1 species).  Ions are a fixed set shared by all walkers
