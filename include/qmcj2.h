@@ -261,6 +261,64 @@ qj2_status qj2_metropolis(int64_t W, const double *ratio, int64_t ratio_stride,
                           const double *u, int32_t *accept, void *stream);
 
 /* ------------------------------------------------------------------------ */
+/* NEXT-4: tricubic B-spline single-particle orbitals (SPOs) and the         */
+/* determinant ratio.                                                        */
+/*                                                                           */
+/* The SPO set is a read-only 3D B-spline table shared by all walkers        */
+/* (Table 1 "FFT grid" and "# of unique SPOs", PAPER:936-   */
+/* 958), single precision as in the paper ("all the quantities are in double */
+/* precision ... except for the Bspline-SPO").  Convention  */
+/* (R22): uniform periodic tricubic B-spline on an nx x ny x nz    */
+/* grid over the orthorhombic cell; for u = (x mod L_x) / L_x * nx, i =      */
+/* floor(u), t = u - i, control points (i - 1 + a) mod nx, a = 0..3, with   */
+/* the uniform cubic basis B_a(t) (the same basis as qj2_functor); likewise */
+/* y, z:  phi_o(r) = sum_{a,b,c} B_a(t_x) B_b(t_y) B_c(t_z) P[ix][iy][iz][o].*/
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    double  L[3];               /* cell */
+    int64_t nx, ny, nz;         /* grid, each >= 4 */
+    int64_t n_orb;              /* orbitals, >= 1 */
+    int64_t ld;                 /* lane stride of a row, >= n_orb, ld % 4 == 0 */
+    const float *coef;          /* device [nx][ny][nz][ld] fp32, 16-byte aligned; */
+                                /* nx*ny*nz*ld < 2^31; lanes [n_orb, ld) ignored  */
+} qj2_spo_table;
+
+enum { QJ2_SPO_V = 0, QJ2_SPO_VGH = 1 };
+
+/* qj2_spo_eval -- "Bspline-v" (what = QJ2_SPO_V) or "Bspline-vgh"          */
+/* (QJ2_SPO_VGH) at one position per walker, fused with the determinant     */
+/* ratio of Eq. 6: with A(i,j) = phi_i(r_j) */
+/* and a = row k of A^{-1} (reading R23),                                    */
+/*   rho = sum_o a_o phi_o(r'),  G = sum_o a_o grad phi_o(r') / rho,         */
+/*   L = sum_o a_o lap phi_o(r') / rho   (the determinant's ratio, grad ln D */
+/*   and lap D / D at R'; same lemma).                        */
+/* Arguments                                                                 */
+/*   tab        host struct (the table itself is device memory).             */
+/*   pos_dtype  QJ2_FP32 / QJ2_FP64 of pos.                                  */
+/*   W          evaluations (>= 0).                                          */
+/*   pos        device, row w at pos + w*pos_stride elements (x, y, z), any  */
+/*              real value (wrapped into the cell); pos_stride >= 3.         */
+/*   Ainv       device fp32 or NULL (no ratio): row of walker w at           */
+/*              Ainv + w*ainv_stride + krow[w]*ainv_ld (krow == NULL: row 0),*/
+/*              n_orb entries.                                               */
+/*   out        device fp64 [W][5] (rho, Gx, Gy, Gz, L) or NULL; with        */
+/*              QJ2_SPO_V only rho is computed (G, L written as 0).          */
+/*   spo_out    device fp32 [W][10][ld] (v, gx, gy, gz, hxx, hxy, hxz, hyy,  */
+/*              hyz, hzz; QJ2_SPO_VGH) or [W][1][ld] (QJ2_SPO_V), or NULL.   */
+/* Errors: EINVAL for bad sizes / NULL table / misalignment.                 */
+qj2_status qj2_spo_eval(const qj2_spo_table *tab, int32_t what, qj2_dtype pos_dtype, int64_t W,
+                        const void *pos, int64_t pos_stride,
+                        const float *Ainv, int64_t ainv_stride, int64_t ainv_ld, const int32_t *krow,
+                        double *out, float *spo_out, void *stream);
+
+/* Synthetic SPO coefficient table (test/bench harness, NOT the method):     */
+/* coef[ix][iy][iz][o] = 2u - 1, u = top 24 bits of mix64(key' ^ flat index) */
+/* * 2^-24 with key' = mix64(mix64(seed*G + G) ^ 0x5A0C0EFF1C1E17A5), flat   */
+/* index = ((ix*ny + iy)*nz + iz)*ld + o; lanes o >= n_orb are 0 (qmcgen).   */
+qj2_status qj2gen_spo_table(uint64_t seed, int64_t nx, int64_t ny, int64_t nz, int64_t n_orb,
+                            int64_t ld, float *coef, void *stream);
+
+/* ------------------------------------------------------------------------ */
 /* Host-buffer variant of qj2_eval (the end-to-end path): R, k, r_trial are  */
 /* HOST arrays (pinned for full PCIe rate), out (and ratio_out if non-NULL)  */
 /* HOST arrays, same shapes as qj2_eval.  Walkers are streamed in chunks of  */

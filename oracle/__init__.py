@@ -309,3 +309,17 @@ def det_ratio(Ainv_rows, v, g, h):
         lb.orc_det_ratio(n, _dp(np.ascontiguousarray(A[m])), _dp(_f64(v[m])), _dp(_f64(g[m])),
                          _dp(_f64(h[m])), _dp(out[m]), _dp(ab[m]))
     return out, ab
+
+
+def gen_spo_table(seed: int, nx: int, ny: int, nz: int, n_orb: int, ld: int | None = None,
+                  threads: int = 1) -> np.ndarray:
+    """Oracle-side C twin of qmcgen.spo_table (input generation only)."""
+    ld = n_orb if ld is None else ld
+    L = lib()
+    L.orc_gen_spo_table.restype = None
+    L.orc_gen_spo_table.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                    ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int]
+    out = np.empty((nx, ny, nz, ld), dtype=np.float32)
+    L.orc_gen_spo_table(int(seed) & 0xFFFFFFFFFFFFFFFF, nx, ny, nz, n_orb, ld,
+                        out.ctypes.data_as(ctypes.c_void_p), int(threads))
+    return out

@@ -682,3 +682,46 @@ void orc_det_ratio(int64_t n, const double *Ainv_row, const double *v, const dou
         abs_out[4] = nsum_get(&aL);
     }
 }
+
+/* Host twin of the synthetic SPO table generator (qmcgen.spo_table), in     */
+/* plain C for large tables.  Not part of the method.  Pinned bitwise        */
+/* against qmcgen by tests/test_inputs.py.                                   */
+typedef struct { uint64_t key; int64_t e0, e1, ld, n_orb; float *coef; } spo_gen_job;
+
+static void *spo_gen_thread(void *arg)
+{
+    spo_gen_job *J = (spo_gen_job *)arg;
+    for (int64_t e = J->e0; e < J->e1; ++e) {
+        int64_t o = e % J->ld;
+        float x = 0.0f;
+        if (o < J->n_orb) {
+            uint64_t h = orc_mix64(J->key ^ (uint64_t)e);
+            x = (float)(uint32_t)(h >> 40) * 1.1920928955078125e-07f - 1.0f;
+        }
+        J->coef[e] = x;
+    }
+    return NULL;
+}
+
+void orc_gen_spo_table(uint64_t seed, int64_t nx, int64_t ny, int64_t nz, int64_t n_orb, int64_t ld,
+                       float *coef, int nthreads)
+{
+    uint64_t k0 = orc_mix64(seed * 0x9E3779B97F4A7C15ull + 0x9E3779B97F4A7C15ull);
+    uint64_t key = orc_mix64(k0 ^ 0x5A0C0EFF1C1E17A5ull);
+    int64_t total = nx * ny * nz * ld;
+    if (nthreads < 1) nthreads = 1;
+    spo_gen_job *jobs = (spo_gen_job *)calloc((size_t)nthreads, sizeof(spo_gen_job));
+    pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+    int64_t per = (total + nthreads - 1) / nthreads;
+    for (int t = 0; t < nthreads; ++t) {
+        int64_t a = t * per, b = (t + 1) * per;
+        if (a > total) a = total;
+        if (b > total) b = total;
+        spo_gen_job J = { key, a, b, ld, n_orb, coef };
+        jobs[t] = J;
+    }
+    for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, spo_gen_thread, &jobs[t]);
+    spo_gen_thread(&jobs[0]);
+    for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+    free(jobs); free(th);
+}

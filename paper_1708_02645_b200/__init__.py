@@ -11,6 +11,7 @@ Public API (names follow include/qmcj2.h):
     eval_j1(ions, species_start, r_trial, fn1)    -> NEXT-1: J1 over the AB row
     accept(R, state, k, r_new, acc, out_new, fn, ...) -> NEXT-2: accept-side update of R and the 5N J2 state
     metropolis(ratio, u)                          -> NEXT-2: accept flags (u < rho^2)
+    SpoTable, spo_eval(tab, pos, ...)             -> NEXT-4: Bspline-v/vgh + determinant ratio
     eval_host(R, k, r_trial, fn, ...)             -> host-buffer end-to-end path
     ratio(out, V_cur=None)                        -> [W][P][2] (dJ2, exp(dJ2))
     functor_eval_vgl(fn, channel, r)              -> [n][3] (U, U', U'')
@@ -27,7 +28,8 @@ import torch
 
 from . import _build
 
-__all__ = ["QJ2Error", "Functor", "J1Functor", "Workspace", "eval", "eval_j1", "accept", "metropolis", "eval_host", "ratio", "functor_eval_vgl",
+__all__ = ["QJ2Error", "Functor", "J1Functor", "Workspace", "eval", "eval_j1", "accept", "metropolis", "SpoTable",
+           "spo_eval", "gen_spo_table", "eval_host", "ratio", "functor_eval_vgl",
            "min_image_disp", "check_inputs", "padded_size", "gen_positions", "lib_path",
            "workspace_size", "host_workspace_size", "version", "device_check"]
 
@@ -49,6 +51,13 @@ class _Functor(ctypes.Structure):
                 ("m", ctypes.c_int32),
                 ("reserved", ctypes.c_int32),
                 ("coef", (ctypes.c_double * (QJ2_MAX_M + 3)) * 2)]
+
+
+class _SpoTable(ctypes.Structure):
+    _fields_ = [("L", ctypes.c_double * 3),
+                ("nx", ctypes.c_int64), ("ny", ctypes.c_int64), ("nz", ctypes.c_int64),
+                ("n_orb", ctypes.c_int64), ("ld", ctypes.c_int64),
+                ("coef", ctypes.c_void_p)]
 
 
 class _J1Functor(ctypes.Structure):
@@ -87,6 +96,9 @@ def _load():
         "qj2_accept": (ctypes.c_int, [F, ctypes.c_int, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp, i64, vp,
                                       vp, vp, i64, vp, sz, vp]),
         "qj2_metropolis": (ctypes.c_int, [i64, vp, i64, vp, vp, vp]),
+        "qj2_spo_eval": (ctypes.c_int, [ctypes.POINTER(_SpoTable), i32, ctypes.c_int, i64, vp, i64, vp, i64, i64,
+                                        vp, vp, vp, vp]),
+        "qj2gen_spo_table": (ctypes.c_int, [ctypes.c_uint64, i64, i64, i64, i64, i64, vp, vp]),
         "qj2_eval_j1": (ctypes.c_int, [ctypes.POINTER(_J1Functor), ctypes.c_int, i64, ctypes.POINTER(i64), i64,
                                        vp, i32, vp, vp, vp, vp, vp, vp, sz, vp]),
         "qj2_eval_host_workspace_size": (ctypes.c_int, [i64, i32, i64, ctypes.c_int, i64, ctypes.POINTER(sz)]),
@@ -110,7 +122,7 @@ def _load():
 _lib = _load()
 EXPORTS = ("qj2_version", "qj2_status_string", "qj2_last_error", "qj2_device_check", "qj2_padded_size",
            "qj2_eval_workspace_size", "qj2_eval", "qj2_ratio", "qj2_eval_j1", "qj2_accept_workspace_size",
-           "qj2_accept", "qj2_metropolis", "qj2_eval_host_workspace_size",
+           "qj2_accept", "qj2_metropolis", "qj2_spo_eval", "qj2gen_spo_table", "qj2_eval_host_workspace_size",
            "qj2_eval_host", "qj2_functor_eval_vgl", "qj2_min_image_disp", "qj2_check_inputs",
            "qj2gen_positions")
 
@@ -401,6 +413,77 @@ def metropolis(ratio_out, u, acc=None, *, trial: int = 0, stream=None):
     _check(_lib.qj2_metropolis(W, rp, rs, _ptr(u), _ptr(acc), ctypes.c_void_p(_stream_ptr(stream))),
            "qj2_metropolis")
     return acc
+
+
+QJ2_SPO_V, QJ2_SPO_VGH = 0, 1
+
+
+class SpoTable:
+    """A read-only 3D B-spline SPO table (qj2_spo_table): coef is a CUDA fp32
+    tensor [nx][ny][nz][ld] (ld % 4 == 0) holding n_orb orbitals per row."""
+
+    def __init__(self, coef: torch.Tensor, n_orb: int, L):
+        _req(coef, "coef", torch.float32, 4)
+        self.coef = coef
+        self.n_orb = int(n_orb)
+        self.L = tuple(float(x) for x in (L if np.ndim(L) else (L, L, L)))
+        nx, ny, nz, ld = coef.shape
+        c = _SpoTable()
+        for d in range(3):
+            c.L[d] = self.L[d]
+        c.nx, c.ny, c.nz, c.n_orb, c.ld = nx, ny, nz, self.n_orb, ld
+        c.coef = coef.data_ptr()
+        self._c = c
+
+    @property
+    def ptr(self):
+        return ctypes.byref(self._c)
+
+
+def spo_eval(tab: SpoTable, pos, *, vgh: bool = True, Ainv=None, krow=None, trial: int = 0, out=None,
+             spo_out=None, want_spo: bool = False, stream=None):
+    """qj2_spo_eval (NEXT-4): Bspline-vgh (vgh=True) or Bspline-v at pos
+    ([W][3] or [W][P][3], trial `trial`, f32/f64) fused with the determinant
+    ratio against Ainv (fp32, [W][n][lda] with krow [W] int32, or [W][lda]
+    rows).  Returns out [W][5] fp64 (rho, G, L) (None without Ainv) and, if
+    want_spo, spo [W][10 or 1][ld] fp32."""
+    _req(pos, "pos")
+    W = pos.shape[0]
+    pp, ps = _row_ptr(pos, trial, 3)
+    ldv = tab.coef.shape[3]
+    dev = pos.device
+    a_ptr, a_stride, a_ld = None, 0, 0
+    if Ainv is not None:
+        _req(Ainv, "Ainv", torch.float32)
+        if Ainv.dim() == 3:
+            if krow is None:
+                raise ValueError("krow is required with a [W][n][lda] Ainv")
+            _req(krow, "krow", torch.int32, 1)
+            a_stride, a_ld = Ainv.shape[1] * Ainv.shape[2], Ainv.shape[2]
+        else:
+            a_stride, a_ld = Ainv.shape[1], Ainv.shape[1]
+            krow = None
+        a_ptr = _ptr(Ainv)
+        if out is None:
+            out = torch.empty((W, 5), dtype=torch.float64, device=dev)
+    if want_spo and spo_out is None:
+        spo_out = torch.empty((W, 10 if vgh else 1, ldv), dtype=torch.float32, device=dev)
+    _check(_lib.qj2_spo_eval(tab.ptr, QJ2_SPO_VGH if vgh else QJ2_SPO_V, _dtype_code(pos.dtype), W, pp, ps,
+                             a_ptr, a_stride, a_ld, _ptr(krow), _ptr(out) if Ainv is not None else None,
+                             _ptr(spo_out), ctypes.c_void_p(_stream_ptr(stream))), "qj2_spo_eval")
+    if want_spo:
+        return out, spo_out
+    return out
+
+
+def gen_spo_table(seed: int, nx: int, ny: int, nz: int, n_orb: int, ld: int | None = None, stream=None,
+                  device=None) -> torch.Tensor:
+    """Device synthetic SPO table (harness; same recipe as qmcgen.spo_table)."""
+    ld = n_orb if ld is None else ld
+    coef = torch.empty((nx, ny, nz, ld), dtype=torch.float32, device=device or torch.cuda.current_device())
+    _check(_lib.qj2gen_spo_table(int(seed) & 0xFFFFFFFFFFFFFFFF, nx, ny, nz, n_orb, ld, _ptr(coef),
+                                 ctypes.c_void_p(_stream_ptr(stream))), "qj2gen_spo_table")
+    return coef
 
 
 def host_workspace_size(W, P, Np, dtype, chunk_walkers) -> int:

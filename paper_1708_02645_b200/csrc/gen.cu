@@ -77,3 +77,29 @@ extern "C" qj2_status qj2gen_positions(qj2_dtype dtype, uint64_t seed, int64_t W
         return QJ2_EINVAL;
     return cudaGetLastError() == cudaSuccess ? QJ2_OK : QJ2_ECUDA;
 }
+
+namespace {
+__global__ void gen_spo_kernel(unsigned long long key, int64_t total, int64_t ld, int64_t n_orb,
+                               float *__restrict__ coef) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+        const int64_t o = e % ld;
+        float x = 0.f;
+        if (o < n_orb) {
+            const unsigned long long h = mix64(key ^ (unsigned long long)e);
+            x = (float)(unsigned)(h >> 40) * 1.1920928955078125e-07f - 1.0f;   // 2^-23: 2u - 1, exact
+        }
+        coef[e] = x;
+    }
+}
+}  // namespace
+
+extern "C" qj2_status qj2gen_spo_table(uint64_t seed, int64_t nx, int64_t ny, int64_t nz, int64_t n_orb,
+                                       int64_t ld, float *coef, void *stream) {
+    if (nx < 1 || ny < 1 || nz < 1 || n_orb < 1 || ld < n_orb) return QJ2_EINVAL;
+    if (!coef) return QJ2_EINVAL;
+    const unsigned long long k0 = mix64_host(seed * 0x9E3779B97F4A7C15ull + 0x9E3779B97F4A7C15ull);
+    const unsigned long long key = mix64_host(k0 ^ 0x5A0C0EFF1C1E17A5ull);
+    gen_spo_kernel<<<148 * 16, 256, 0, static_cast<cudaStream_t>(stream)>>>(key, nx * ny * nz * ld, ld, n_orb, coef);
+    return cudaGetLastError() == cudaSuccess ? QJ2_OK : QJ2_ECUDA;
+}

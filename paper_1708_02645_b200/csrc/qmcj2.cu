@@ -23,6 +23,7 @@
 
 #include "launch.cuh"
 #include "accept.cuh"
+#include "spo.cuh"
 
 // ===========================================================================
 // Small kernels
@@ -570,6 +571,49 @@ qj2_status qj2_metropolis(int64_t W, const double *ratio, int64_t ratio_stride,
         W, ratio, ratio_stride, u, accept);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? QJ2_OK : cuda_fail(e, "metropolis_kernel launch");
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-4: tricubic B-spline SPOs + determinant ratio (include/qmcj2.h).
+// ---------------------------------------------------------------------------
+qj2_status qj2_spo_eval(const qj2_spo_table *tab, int32_t what, qj2_dtype pos_dtype, int64_t W,
+                        const void *pos, int64_t pos_stride,
+                        const float *Ainv, int64_t ainv_stride, int64_t ainv_ld, const int32_t *krow,
+                        double *out, float *spo_out, void *stream) {
+    if (!tab) return fail(QJ2_EINVAL, "tab is NULL");
+    if (what != QJ2_SPO_V && what != QJ2_SPO_VGH) return fail(QJ2_EINVAL, "what must be QJ2_SPO_V or QJ2_SPO_VGH");
+    if (pos_dtype != QJ2_FP32 && pos_dtype != QJ2_FP64) return fail(QJ2_EINVAL, "bad pos_dtype");
+    for (int d = 0; d < 3; ++d)
+        if (!(tab->L[d] > 0) || !std::isfinite(tab->L[d])) return fail(QJ2_EINVAL, "L[%d] must be finite and > 0", d);
+    if (tab->nx < 4 || tab->ny < 4 || tab->nz < 4) return fail(QJ2_EINVAL, "grid dimensions must be >= 4");
+    if (tab->n_orb < 1 || tab->ld < tab->n_orb || tab->ld % 4 != 0)
+        return fail(QJ2_EINVAL, "need 1 <= n_orb <= ld and ld %% 4 == 0");
+    if (tab->nx * tab->ny * tab->nz * tab->ld >= (1ll << 31)) return fail(QJ2_EINVAL, "table too large (>= 2^31 floats)");
+    if (W < 0 || pos_stride < 3) return fail(QJ2_EINVAL, "need W >= 0 and pos_stride >= 3");
+    if (Ainv && (ainv_stride < 0 || (krow && ainv_ld < tab->n_orb)))
+        return fail(QJ2_EINVAL, "bad Ainv strides");
+    if (W == 0) return QJ2_OK;
+    if (!tab->coef || !pos) return fail(QJ2_EINVAL, "coef and pos must be non-NULL");
+    if (((uintptr_t)tab->coef & 15) || (spo_out && ((uintptr_t)spo_out & 15)))
+        return fail(QJ2_EINVAL, "coef and spo_out must be 16-byte aligned");
+    qj2_status st = check_device();
+    if (st) return st;
+    const bool vgh = what == QJ2_SPO_VGH;
+    const int nv = vgh ? 2 : 4;                   // orbitals per thread (spo.cuh)
+    SpoParams p;
+    memset(&p, 0, sizeof p);
+    p.W = W; p.nx = tab->nx; p.ny = tab->ny; p.nz = tab->nz; p.n_orb = tab->n_orb; p.ld = tab->ld;
+    p.nvec = tab->ld / nv;
+    p.coef = tab->coef;
+    for (int d = 0; d < 3; ++d) p.L[d] = tab->L[d];
+    p.pos_f64 = pos_dtype == QJ2_FP64; p.pos = pos; p.pos_stride = pos_stride;
+    p.Ainv = Ainv; p.ainv_stride = ainv_stride; p.ainv_ld = ainv_ld; p.krow = krow;
+    p.out = out; p.spo_out = spo_out;
+    const int64_t lanes = ((p.nvec + 31) / 32) * 32;
+    p.tpw = (int32_t)(lanes < 256 ? lanes : 256);
+    p.wpc = 256 / p.tpw;
+    cudaError_t e = launch_spo(p, vgh, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? QJ2_OK : cuda_fail(e, "spo_kernel launch");
 }
 
 // ---------------------------------------------------------------------------

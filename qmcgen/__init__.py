@@ -278,6 +278,42 @@ def spo_table_rows(seed: int, nx: int, ny: int, nz: int, ld: int, n_orb: int, ro
     return u
 
 
+@dataclasses.dataclass(frozen=True)
+class SpoConfig:
+    """NEXT-4 workload: a Table-1-shaped SPO set and W walker
+    positions (one Bspline-vgh + determinant ratio each)."""
+    name: str
+    nx: int
+    ny: int
+    nz: int
+    n_orb: int
+    ld: int
+    W: int
+    N: int            # electrons of the system (cell: density 1)
+    seed: int
+
+    @property
+    def L(self) -> float:
+        return cell_length(self.N)
+
+    @property
+    def table_bytes(self) -> int:
+        return self.nx * self.ny * self.nz * self.ld * 4
+
+
+SPO_CONFIGS = {
+    # NiO-64 (Table 1): N = 768, FFT grid 80^3; the determinant needs N/2 = 384 orbitals per spin
+    "S1": SpoConfig("S1", 80, 80, 80, 384, 384, 65536, 768, seed=11),
+}
+
+
+def spo_positions(seed: int, W: int, L: float) -> np.ndarray:
+    """W positions uniform in the cell (fp32), the r'_k of one move per walker."""
+    rng = np.random.default_rng([int(seed), 8])
+    p = (rng.random((W, 3)) * L).astype(np.float32)
+    return np.where(p >= np.float32(L), np.float32(0), p)
+
+
 def make_ainv_rows(seed: int, W: int, n: int) -> np.ndarray:
     """Synthetic rows k of A^{-1} per walker, fp32 [W][n], U[-1, 1)/sqrt(n)."""
     rng = np.random.default_rng([int(seed), 7])

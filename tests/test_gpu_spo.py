@@ -1,0 +1,129 @@
+"""GPU parity of NEXT-4 (qj2_spo_eval: Bspline-v / Bspline-vgh fused with the
+determinant ratio of Eq. 6) against the CPU oracle (oracle.spo_vgh,
+oracle.det_ratio), through the C ABI (-m gpu; needs a B200).
+
+Tolerance (fp32 table, fp32 per-term arithmetic): per output
+|x_gpu - x_orc| / max(A, F) <= 1e-5, A the oracle's sum of |weight * coef|
+(or |a_o phi_o| for the ratio), F the table scale (max|P| times n/L per
+derivative order).  The ratio's G and L are compared as rho*G and rho*L (the
+lemma's numerators) so that a small rho does not amplify the comparison.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import qmcgen
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def q():
+    import paper_1708_02645_b200 as q
+    assert torch.cuda.is_available()
+    q.device_check()
+    return q
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _F(L, n):
+    s = np.array(n, dtype=np.float64) / np.array(L, dtype=np.float64)
+    # v, gx, gy, gz, hxx, hxy, hxz, hyy, hyz, hzz
+    return np.array([1, s[0], s[1], s[2], s[0] ** 2, s[0] * s[1], s[0] * s[2], s[1] ** 2, s[1] * s[2], s[2] ** 2])
+
+
+def check_spo(q, nx, ny, nz, n_orb, ld, W, seed, pos_dtype=np.float32, L=(3.0, 3.5, 4.0), krow_mode=False,
+              shift=0.0):
+    T = qmcgen.spo_table(seed, nx, ny, nz, n_orb, ld)
+    tab = q.SpoTable(dev(T), n_orb, L)
+    rng = np.random.default_rng(seed)
+    pos = (rng.random((W, 3)) * np.asarray(L) + shift).astype(pos_dtype)
+    A = qmcgen.make_ainv_rows(seed, W, n_orb)
+    if krow_mode:                        # full [W][n][lda] inverse, row krow[w]
+        lda = n_orb + 3
+        full = np.random.default_rng(seed + 1).random((W, n_orb, lda)).astype(np.float32)
+        krow = rng.integers(0, n_orb, W).astype(np.int32)
+        full[np.arange(W), krow, :n_orb] = A
+        out, spo = q.spo_eval(tab, dev(pos), Ainv=dev(full), krow=dev(krow), want_spo=True)
+    else:
+        out, spo = q.spo_eval(tab, dev(pos), Ainv=dev(A), want_spo=True)
+    out, spo = out.cpu().numpy(), spo.cpu().numpy()
+    v, g, h, ab = oracle.spo_vgh(T, n_orb, L, pos.astype(np.float64))
+    ref = np.concatenate([v[:, None, :], g, h], axis=1)               # [W][10][n_orb]
+    F = np.abs(T).max() * _F(L, (nx, ny, nz))[None, :, None]
+    err = np.abs(spo[:, :, :n_orb] - ref) / np.maximum(ab, F)
+    assert np.all(np.isfinite(spo[:, :, :n_orb]))
+    assert err.max() <= TOL, f"spo max normalized error {err.max():.3e}"
+    orc, aab = oracle.det_ratio(A, v, g, h)
+    rho_g, rho_o = out[:, 0], orc[:, 0]
+    assert np.max(np.abs(rho_g - rho_o) / aab[:, 0]) <= TOL
+    num_g = out[:, 1:] * rho_g[:, None]
+    num_o = orc[:, 1:] * rho_o[:, None]
+    assert np.max(np.abs(num_g - num_o) / aab[:, 1:]) <= TOL
+    return T, tab, pos, out, spo
+
+
+@pytest.mark.parametrize("n_orb,ld", [(1, 4), (3, 4), (10, 12), (64, 64), (130, 132), (384, 384), (600, 600)])
+def test_spo_vgh_and_ratio(q, n_orb, ld):
+    check_spo(q, 6, 7, 8, n_orb, ld, 37, seed=10 + n_orb)
+
+
+def test_spo_fp64_positions_krow_and_wrapping(q):
+    check_spo(q, 5, 9, 4, 48, 48, 29, seed=3, pos_dtype=np.float64, krow_mode=True)
+    # positions outside [0, L): wrapped into the cell (periodic table)
+    check_spo(q, 5, 9, 4, 48, 48, 29, seed=4, shift=-7.25)
+    check_spo(q, 5, 9, 4, 48, 48, 29, seed=5, shift=11.5)
+
+
+def test_spo_v_equals_vgh_values_bitwise(q):
+    """Bspline-v and the value lanes of Bspline-vgh: the same sums in the same
+    order (SPEC: 'vs spo_eval_vgh value lanes: identical')."""
+    T, tab, pos, out, spo = check_spo(q, 8, 8, 8, 96, 96, 64, seed=21)
+    A = qmcgen.make_ainv_rows(21, 64, 96)
+    out_v, spo_v = q.spo_eval(tab, dev(pos), vgh=False, Ainv=dev(A), want_spo=True)
+    assert torch.equal(spo_v[:, 0].cpu(), torch.from_numpy(spo[:, 0]))
+    assert np.array_equal(out_v.cpu().numpy()[:, 0], out[:, 0])
+    assert np.all(out_v.cpu().numpy()[:, 1:] == 0)
+
+
+def test_spo_no_ratio_and_empty(q):
+    T = qmcgen.spo_table(1, 4, 4, 4, 8, 8)
+    tab = q.SpoTable(dev(T), 8, 2.0)
+    pos = torch.rand((5, 3), device="cuda") * 2
+    out, spo = q.spo_eval(tab, pos, want_spo=True)
+    assert out is None and spo.shape == (5, 10, 8)
+    e = q.spo_eval(tab, torch.zeros((0, 3), device="cuda"), Ainv=torch.zeros((0, 8), device="cuda"))
+    assert e.shape == (0, 5)
+
+
+def test_spo_device_generator_matches_host(q):
+    g = q.gen_spo_table(77, 6, 5, 7, 30, 32).cpu().numpy()
+    assert np.array_equal(g, qmcgen.spo_table(77, 6, 5, 7, 30, 32))
+
+
+def test_spo_nio64_full_size_sampled(q):
+    """The bench workload: NiO-64-shaped table (80^3 grid, 384 orbitals = N/2
+    for N = 768, fp32, 786 MB) generated on the device, 65,536 walkers'
+    Bspline-vgh + ratio in the bench launch configuration; sampled walkers vs
+    the oracle on the oracle side's own copy of the table."""
+    cfg = qmcgen.SPO_CONFIGS["S1"]
+    coef = q.gen_spo_table(cfg.seed, cfg.nx, cfg.ny, cfg.nz, cfg.n_orb, cfg.ld)
+    tab = q.SpoTable(coef, cfg.n_orb, cfg.L)
+    pos = qmcgen.spo_positions(cfg.seed, cfg.W, cfg.L)
+    A = qmcgen.make_ainv_rows(cfg.seed, cfg.W, cfg.n_orb)
+    out = q.spo_eval(tab, dev(pos), Ainv=dev(A)).cpu().numpy()
+    del coef
+    torch.cuda.empty_cache()
+    T = oracle.gen_spo_table(cfg.seed, cfg.nx, cfg.ny, cfg.nz, cfg.n_orb, cfg.ld, threads=os.cpu_count() or 1)
+    ws = np.array([0, 1, 4097, 65535])
+    v, g, h, ab = oracle.spo_vgh(T, cfg.n_orb, cfg.L, pos[ws].astype(np.float64))
+    orc, aab = oracle.det_ratio(A[ws], v, g, h)
+    assert np.max(np.abs(out[ws, 0] - orc[:, 0]) / aab[:, 0]) <= TOL
+    assert np.max(np.abs(out[ws, 1:] * out[ws, :1] - orc[:, 1:] * orc[:, :1]) / aab[:, 1:]) <= TOL

@@ -78,3 +78,15 @@ def test_j1_inputs():
     fn1 = qmcgen.make_j1_functor(2, L)
     assert fn1.m == (8, 10) and fn1.r_cut[0] == L / 2 and fn1.r_cut[1] < L / 2
     assert np.all(fn1.coef[0, 8:] == 0) and np.all(fn1.coef[1, 10:] == 0)
+
+
+def test_spo_table_generators_agree():
+    """qmcgen.spo_table (numpy) and the oracle's C twin are bitwise equal; the
+    row sampler returns the same rows."""
+    import oracle
+    a = qmcgen.spo_table(9, 5, 6, 7, 10, 12)
+    b = oracle.gen_spo_table(9, 5, 6, 7, 10, 12, threads=3)
+    assert np.array_equal(a, b)
+    r = qmcgen.spo_table_rows(9, 5, 6, 7, 12, 10, [[4, 5, 6], [0, 0, 0]])
+    assert np.array_equal(r[0], a[4, 5, 6]) and np.array_equal(r[1], a[0, 0, 0])
+    assert np.all(a[..., 10:] == 0) and a.min() >= -1 and a.max() < 1
