@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C3S", "C3P2", "C3P12"])
+    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C3S", "C3P2", "C3P12", "S1"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -223,8 +223,43 @@ class OracleSample:
         return time.perf_counter() - t0
 
 
+_SPO_TABLE_CACHE = {}
+
+
+class OracleSampleSpo:
+    """NEXT-4 CPU oracle sample: Bspline-vgh of every orbital at the first n
+    walkers' positions and the determinant ratio (oracle.spo_vgh + det_ratio,
+    single-threaded as the oracle stands).  The table is generated once by the
+    oracle side's own C generator (untimed)."""
+
+    def __init__(self, cfg, n_walkers, threads):
+        import oracle
+        import qmcgen
+        self.cfg, self.n = cfg, int(max(1, min(n_walkers, cfg.W)))
+        if cfg.name not in _SPO_TABLE_CACHE:
+            _SPO_TABLE_CACHE[cfg.name] = oracle.gen_spo_table(cfg.seed, cfg.nx, cfg.ny, cfg.nz, cfg.n_orb, cfg.ld,
+                                                              threads=threads)
+        self.T = _SPO_TABLE_CACHE[cfg.name]
+        self.pos = qmcgen.spo_positions(cfg.seed, cfg.W, cfg.L)[:self.n].astype(np.float64)
+        self.A = qmcgen.make_ainv_rows(cfg.seed, cfg.W, cfg.n_orb)[:self.n]
+        self.items = self.n * cfg.n_orb
+
+    def run(self):
+        import oracle
+        t0 = time.perf_counter()
+        v, g, h, _ = oracle.spo_vgh(self.T, self.cfg.n_orb, self.cfg.L, self.pos)
+        oracle.det_ratio(self.A, v, g, h)
+        return time.perf_counter() - t0
+
+
+def make_oracle_sample(cfg, n, threads):
+    return OracleSampleSpo(cfg, n, threads) if cfg.name.startswith("S") else OracleSample(cfg, n, threads)
+
+
 def _what(cfg):
     import qmcgen
+    if cfg.name.startswith("S"):
+        return f"Bspline-vgh of {cfg.n_orb} orbitals + determinant ratio, {cfg.nx}x{cfg.ny}x{cfg.nz} grid"
     if cfg.name == "C3S":
         return "eval P=2 + Metropolis + accept update"
     P, mode = qmcgen.trial_spec(cfg.name)
@@ -235,10 +270,13 @@ def oracle_sample_size(cfg, cores, budget_s):
     """Walkers such that one oracle pass takes about budget_s on `cores` threads
     (calibrated on one walker per core), capped at the whole workload."""
     n0 = min(cfg.W, cores)
-    dt0 = OracleSample(cfg, n0, cores).run()
+    s0 = make_oracle_sample(cfg, n0, cores)
+    dt0 = s0.run()
     per_round = max(dt0, 1e-6)              # one walker per core
     n = int(budget_s / per_round) * cores
-    return max(n0, min(cfg.W, n)), n0 * (cfg.N - 1) / dt0
+    if cfg.name.startswith("S"):            # the SPO oracle runs on one thread
+        n = int(budget_s / per_round * n0)
+    return max(n0, min(cfg.W, n)), s0.items / dt0
 
 
 def cpu_cores():
@@ -269,19 +307,20 @@ def run_reference(args):
     per_step = max(0.2, min(10.0, budget_total / max(1, args.steps + args.warmup)))
     ws, rate0 = oracle_sample_size(cfg, cores, per_step)
     log(f"[reference] oracle {rate0:.3e} items/s (calibration); {ws} walkers per step")
-    smp = OracleSample(cfg, ws, cores)
+    smp = make_oracle_sample(cfg, ws, cores)
     for _ in range(args.warmup):
         smp.run()
     times = [smp.run() for _ in range(args.steps)]
     t = float(np.mean(times))
     value = smp.items / t
+    used = 1 if cfg.name.startswith("S") else cores
     sample = (f"{smp.n} of {cfg.W} walkers of {cfg.name} (N={cfg.N}, {_what(cfg)}) per step, fp32 inputs promoted "
-              f"exactly to fp64, plain C oracle, {cores} threads ({cpu_model()})")
+              f"exactly to fp64, plain C oracle, {used} threads ({cpu_model()})")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(cfg, world),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -289,6 +328,13 @@ def run_reference(args):
 
 def workload_config(cfg, world):
     name = cfg.name
+    if name.startswith("S"):
+        return {"workload": f"{name} (NEXT-4): NiO-64-shaped SPO set (Table 1: {cfg.nx}x{cfg.ny}x{cfg.nz} grid, "
+                            f"{cfg.n_orb} orbitals = N/2 for N={cfg.N}, fp32 table {cfg.table_bytes / 1e6:.0f} MB), "
+                            f"W={cfg.W} walkers per rank, one Bspline-vgh + determinant ratio each",
+                "nx": cfg.nx, "n_orb": cfg.n_orb, "ld": cfg.ld, "W": cfg.W, "N": cfg.N,
+                "parallelism": f"walker-batch x{world}",
+                "l2": "table 786 MB > 126 MB L2; random gathers (no flush needed)"}
     desc = {
         "C3": f"C3: one instance per rank, N={cfg.N} electrons x W={cfg.W} walkers, P=1, fp32, seed 2(+rank)",
         "C4": f"C4: 4096 instances of N={cfg.N} x W={cfg.W}, P=1, fp32, seeds 3..4098, sharded by instance",
@@ -712,7 +758,79 @@ class SweepPlan:
         return None   # see DESIGN.md: the host-buffer path is measured on C3
 
 
+class SpoPlan:
+    """NEXT-4: one Bspline-vgh + determinant ratio per walker (qj2_spo_eval) over a
+    NiO-64-shaped shared table; item = one (walker, orbital) pair."""
+    mode = "S1"
+    launches_per_step = 1
+
+    def __init__(self, cfg, rank, world):
+        self.cfg = cfg
+        self.seed = cfg.seed + rank
+        self.items_per_step = cfg.W * cfg.n_orb
+
+    def items_total(self, world):
+        return self.items_per_step * world
+
+    @property
+    def alg_bytes_per_launch(self):
+        cfg = self.cfg
+        # per walker: 64 coefficient rows of n_orb fp32 (the method's gather), the A^{-1} row,
+        # the position and the 5 fp64 outputs
+        return cfg.W * (64 * cfg.n_orb * 4 + cfg.n_orb * 4 + 12 + 40)
+
+    def prepare(self, q):
+        import torch
+        import qmcgen
+        cfg = self.cfg
+        self.coef = q.gen_spo_table(cfg.seed, cfg.nx, cfg.ny, cfg.nz, cfg.n_orb, cfg.ld)
+        self.tab = q.SpoTable(self.coef, cfg.n_orb, cfg.L)
+        self.pos = torch.from_numpy(qmcgen.spo_positions(self.seed, cfg.W, cfg.L)).cuda()
+        self.A = torch.from_numpy(qmcgen.make_ainv_rows(self.seed, cfg.W, cfg.n_orb)).cuda()
+        self.out = torch.empty((cfg.W, 5), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+
+    def step(self, q, dist_mod):
+        q.spo_eval(self.tab, self.pos, Ainv=self.A, out=self.out)
+
+    def kernel_ms(self, q, stream, reps):
+        return _event_ms(lambda: self.step(q, None), stream, reps)
+
+    def e2e(self, q, steps, dist_mod):
+        """Through the public API with host buffers: each step uploads the walkers'
+        positions and A^{-1} rows from pinned memory and reads the ratios back (the
+        shared table is model data, resident on the device)."""
+        import torch
+        cfg = self.cfg
+        ph = self.pos.cpu().pin_memory()
+        ah = self.A.cpu().pin_memory()
+        oh = torch.empty((cfg.W, 5), dtype=torch.float64, pin_memory=True)
+        pd, ad = torch.empty_like(self.pos), torch.empty_like(self.A)
+
+        def run():
+            pd.copy_(ph, non_blocking=True)
+            ad.copy_(ah, non_blocking=True)
+            q.spo_eval(self.tab, pd, Ainv=ad, out=self.out)
+            oh.copy_(self.out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        run()
+        if dist_mod:
+            dist_mod.barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            run()
+        dt = allreduce_max((time.perf_counter() - t0) / steps, dist_mod)
+        world = dist_mod.get_world_size() if dist_mod else 1
+        return {"value": self.items_per_step * world / dt, "unit": UNIT,
+                "h2d_bytes_per_step": ph.numel() * 4 + ah.numel() * 4, "d2h_bytes_per_step": oh.numel() * 8,
+                "ms_per_step": dt * 1e3, "steps": steps,
+                "api": "qj2_spo_eval with positions and A^-1 rows copied from pinned host memory every step "
+                       "(the shared table stays resident)"}
+
+
 def make_plan(cfg, rank, world):
+    if cfg.name.startswith("S"):
+        return SpoPlan(cfg, rank, world)
     if cfg.name in ("C3P2", "C3P12"):
         return MultiTrialPlan(cfg, rank, world)
     if cfg.name == "C3S":
@@ -727,7 +845,7 @@ def make_plan(cfg, rank, world):
 
 
 def plan_kernel_name(plan):
-    return "j2_accept_kernel<float>" if plan.mode == "C3S" else "j2_eval_kernel<float,1,false>"
+    return {"C3S": "j2_accept_kernel<float>", "S1": "spo_kernel<vgh>"}.get(plan.mode, "j2_eval_kernel<float,1,false>")
 
 
 def run_ours(args):
@@ -792,18 +910,19 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = cpu_cores()
         nw = args.cpu_sample_walkers or oracle_sample_size(cfg, cores, 15.0)[0]
-        smp = OracleSample(cfg, nw, cores)
+        smp = make_oracle_sample(cfg, nw, cores)
         dt = smp.run()
-        cpu = {"value": smp.items / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+        used = 1 if cfg.name.startswith("S") else cores
+        cpu = {"value": smp.items / dt, "unit": UNIT, "cores": used, "kind": "oracle",
                "sample": f"{smp.n} of {cfg.W} walkers of {cfg.name} (N={cfg.N}, {_what(cfg)}), one pass, fp32 inputs "
-                         f"promoted exactly to fp64, plain C oracle, {cores} threads ({cpu_model()}), "
+                         f"promoted exactly to fp64, plain C oracle, {used} threads ({cpu_model()}), "
                          f"{dt:.1f} s wall"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "weak" if plan.mode in ("C3", "C3S", "C3P2", "C3P12") else "strong",
+            "scaling": "weak" if plan.mode in ("C3", "C3S", "C3P2", "C3P12", "S1") else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(cfg, world),
             "roofline": (plan.roofline(kms, peak) if hasattr(plan, "roofline") else

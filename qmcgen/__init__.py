@@ -405,12 +405,14 @@ CONFIGS = {
 }
 
 
-def config(name: str) -> Config:
+def config(name: str):
     """CONFIGS[name]; "C3S" (the NEXT-2 sweep-step bench) and "C3P2" / "C3P12"
     (NEXT-3 multi-trial benches: P = 2 drift variant, P = 12 NLPP quadrature)
     run on C3's instance."""
     if name in ("C3S", "C3P2", "C3P12"):
         return dataclasses.replace(CONFIGS["C3"], name=name)
+    if name in SPO_CONFIGS:
+        return SPO_CONFIGS[name]
     return CONFIGS[name]
 
 
