@@ -1,9 +1,46 @@
 // spo.cu -- NEXT-4 SPO evaluation launches (own translation unit).
 #include "spo.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
 namespace qj2 {
 
+template <bool VGH>
+static cudaError_t launch_tma(const SpoParams &p, int nc, cudaStream_t s, bool *done) {
+    *done = false;
+    const size_t stage = (size_t)16 * p.ld * 4;
+    const size_t per_stage = stage + SPO_HDR * 4 + 16;
+    const size_t fixed = 2 * 8 * 5 * sizeof(double) + 128;
+    const size_t budget = 220 * 1024;
+    int nst = (int)std::min<size_t>(16, (budget - fixed) / per_stage);
+    if (nst < 4) return cudaSuccess;                 // rows too long for a deep ring: LDG kernel
+    const size_t smem = (size_t)nst * per_stage + fixed;
+    auto kern = spo_tma_kernel<VGH>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int threads = (nc + 1) * 32;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    if (e != cudaSuccess) return e;
+    const int64_t grid = std::min<int64_t>(p.W, (int64_t)sms * std::max(per_sm, 1));
+    kern<<<(unsigned)grid, threads, smem, s>>>(p, nst);
+    *done = true;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_spo(const SpoParams &p, bool vgh, cudaStream_t s) {
+    const char *env = getenv("QJ2_SPO");                    // A/B: "ldg" forces the LDG kernel
+    const bool force_ldg = env && strcmp(env, "ldg") == 0;
+    const int64_t nc = (p.nvec + 31) / 32;
+    if (!force_ldg && nc <= 8) {
+        bool done = false;
+        cudaError_t e = vgh ? launch_tma<true>(p, (int)nc, s, &done) : launch_tma<false>(p, (int)nc, s, &done);
+        if (e != cudaSuccess || done) return e;
+    }
     const unsigned threads = (unsigned)(p.tpw * p.wpc);
     const unsigned grid = (unsigned)((p.W + p.wpc - 1) / p.wpc);
     if (vgh) spo_kernel<true><<<grid, threads, 0, s>>>(p);

@@ -15,6 +15,7 @@
 #pragma once
 
 #include "qmcj2.h"
+#include "bulk.cuh"
 #include <cstdint>
 
 namespace qj2 {
@@ -231,6 +232,230 @@ __global__ void __launch_bounds__(256, 2) spo_kernel(const __grid_constant__ Spo
             o[1] = s[1] * inv; o[2] = s[2] * inv; o[3] = s[3] * inv; o[4] = s[4] * inv;
         } else {
             o[1] = o[2] = o[3] = o[4] = 0.0;
+        }
+    }
+}
+
+// ===========================================================================
+// TMA-pipelined variant (the default when a walker's orbitals fit one pass of
+// the consumer warps): persistent CTAs, one producer warp gathers each
+// walker's coefficient block plane by plane (x plane a = 0..3: 16 rows of
+// ld floats; the 4 z rows of an (a, b) column are one contiguous bulk copy
+// unless z wraps) into a ring of NST shared-memory stages with
+// cp.async.bulk + mbarrier complete_tx; NC consumer warps (one vector of NV
+// orbitals per thread) read the rows from shared memory.  The producer also
+// computes the walker's basis weights (fp64 -> fp32) into the stage header,
+// loading 32 walkers' positions per warp-wide load.  Per SM up to NST stages
+// (~190 KB) of gathers are in flight instead of ~50 KB of LDGs.
+// ===========================================================================
+constexpr int SPO_HDR = 48;                   // floats per stage header (36 weights, padded to 192 B)
+
+template <bool VGH>
+__global__ void spo_tma_kernel(const __grid_constant__ SpoParams p, int nst) {
+    constexpr int NV = VGH ? 2 : 4;
+    using Vt = FV<NV>;
+    constexpr int NQ = VGH ? 10 : 1;
+    constexpr int NR = VGH ? 5 : 1;
+    const int NC = blockDim.x / 32 - 1;       // consumer warps
+    const int64_t ld = p.ld;
+    const uint32_t stage_bytes = (uint32_t)(16 * ld * 4);
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    float *ring = reinterpret_cast<float *>(smem);                                        // [nst][16][ld]
+    float *hdr = reinterpret_cast<float *>(smem + (size_t)nst * stage_bytes);             // [nst][SPO_HDR]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(hdr + (size_t)nst * SPO_HDR);          // full[nst], empty[nst]
+    double *red = reinterpret_cast<double *>(bars + 2 * nst);                             // [2][8][NR]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(bars);
+    const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(ring);
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < nst; ++st) {
+            mbar_init(bar0 + 8 * st, 1);                  // full: the producer's expect_tx arrival
+            mbar_init(bar0 + 8 * (nst + st), NC);         // empty: one arrival per consumer warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t G = gridDim.x;
+
+    // =====================  producer warp  =====================
+    if (warp == NC) {
+        uint32_t n = 0;
+        const int32_t sx = (int32_t)(p.ny * p.nz * ld), sy = (int32_t)(p.nz * ld);
+        for (int64_t base = blockIdx.x; base < p.W; base += 32 * G) {
+            // lane l prepares walker base + l*G (one warp-wide position load per 32 walkers)
+            const int64_t wl = base + lane * G;
+            float wts[36];
+            int32_t i0[3] = {0, 0, 0};
+            if (wl < p.W) {
+                double x[3];
+                if (p.pos_f64) {
+                    const double *ps = static_cast<const double *>(p.pos) + wl * p.pos_stride;
+                    x[0] = ps[0]; x[1] = ps[1]; x[2] = ps[2];
+                } else {
+                    const float *ps = static_cast<const float *>(p.pos) + wl * p.pos_stride;
+                    x[0] = ps[0]; x[1] = ps[1]; x[2] = ps[2];
+                }
+                const int64_t nn[3] = {p.nx, p.ny, p.nz};
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    AxisW a;
+                    axis_weights(x[d], p.L[d], nn[d], 1, a);
+                    i0[d] = a.off[1];                      // control point of a = 1 is the cell index i
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        wts[d * 12 + c] = a.B[c];
+                        wts[d * 12 + 4 + c] = a.D[c];
+                        wts[d * 12 + 8 + c] = a.S[c];
+                    }
+                }
+            }
+            for (int qw = 0; qw < 32; ++qw) {
+                const int64_t w = base + qw * G;
+                if (w >= p.W) break;
+                const int32_t ix = __shfl_sync(0xffffffffu, i0[0], qw);
+                const int32_t iy = __shfl_sync(0xffffffffu, i0[1], qw);
+                const int32_t iz = __shfl_sync(0xffffffffu, i0[2], qw);
+                const bool zc = iz >= 1 && iz + 2 < p.nz;        // the 4 z rows are contiguous
+                for (int a = 0; a < 4; ++a, ++n) {
+                    const uint32_t slot = n % (uint32_t)nst, round = n / (uint32_t)nst;
+                    mbar_wait(bar0 + 8 * (nst + slot), (round & 1) ^ 1);
+                    if (lane == qw) {
+                        float *h = hdr + slot * SPO_HDR;
+#pragma unroll
+                        for (int e = 0; e < 36; ++e) h[e] = wts[e];
+                    }
+                    __syncwarp();
+                    const uint32_t full = bar0 + 8 * slot;
+                    if (lane == 0) mbar_expect_tx(full, stage_bytes);   // also the producer's arrival
+                    __syncwarp();
+                    int32_t xa = ix - 1 + a;
+                    xa = xa < 0 ? xa + (int32_t)p.nx : (xa >= p.nx ? xa - (int32_t)p.nx : xa);
+                    if (lane < 16) {                          // lane = b*4 + c: row (b, c) of plane a
+                        const int b = lane >> 2, c = lane & 3;
+                        int32_t yb = iy - 1 + b;
+                        yb = yb < 0 ? yb + (int32_t)p.ny : (yb >= p.ny ? yb - (int32_t)p.ny : yb);
+                        int32_t zc0 = iz - 1 + c;
+                        zc0 = zc0 < 0 ? zc0 + (int32_t)p.nz : (zc0 >= p.nz ? zc0 - (int32_t)p.nz : zc0);
+                        const uint32_t dst = ring0 + slot * stage_bytes + (uint32_t)(lane * ld * 4);
+                        if (zc) {
+                            if (c == 0)
+                                bulk_g2s(dst, p.coef + ((int64_t)xa * sx + (int64_t)yb * sy + (int64_t)zc0 * ld),
+                                         (uint32_t)(4 * ld * 4), full);
+                        } else {
+                            bulk_g2s(dst, p.coef + ((int64_t)xa * sx + (int64_t)yb * sy + (int64_t)zc0 * ld),
+                                     (uint32_t)(ld * 4), full);
+                        }
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // =====================  consumer warps  =====================
+    const int t = threadIdx.x;                  // consumer thread: orbital vector j = t
+    const int NCT = NC * 32;
+    const bool has = t < p.nvec;
+    uint32_t n = 0;
+    int par = 0;
+    for (int64_t w = blockIdx.x; w < p.W; w += G, par ^= 1) {
+        // A^{-1} row entries of this thread's orbitals (used after the gather)
+        float av[NV];
+        const float *arow = p.Ainv ? p.Ainv + w * p.ainv_stride + (p.krow ? (int64_t)p.krow[w] * p.ainv_ld : 0)
+                                   : nullptr;
+#pragma unroll
+        for (int e = 0; e < NV; ++e) {
+            const int64_t o = (int64_t)t * NV + e;
+            av[e] = (arow && has && o < p.n_orb) ? __ldg(arow + o) : 0.f;
+        }
+        Vt acc[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q] = zero4<NV>();
+        for (int a = 0; a < 4; ++a, ++n) {
+            const uint32_t slot = n % (uint32_t)nst, round = n / (uint32_t)nst;
+            mbar_wait(bar0 + 8 * slot, round & 1);
+            const float *h = hdr + slot * SPO_HDR;
+            const float bx = h[a], dx = h[4 + a], sxx = h[8 + a];
+            float By[4], Dy[4], Sy[4], Bz[4], Dz[4], Sz[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                By[c] = h[12 + c]; Dy[c] = h[16 + c]; Sy[c] = h[20 + c];
+                Bz[c] = h[24 + c]; Dz[c] = h[28 + c]; Sz[c] = h[32 + c];
+            }
+            if (has) {
+                const Vt *st = reinterpret_cast<const Vt *>(ring + (size_t)slot * 16 * ld) + t;
+                const int64_t rs = ld / NV;           // row stride in vectors
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    Vt r[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) r[c] = st[(b * 4 + c) * rs];
+                    Vt s0 = zero4<NV>();
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) fma4(s0, Bz[c], r[c]);
+                    const float wv = bx * By[b];
+                    fma4(acc[0], wv, s0);
+                    if constexpr (VGH) {
+                        Vt s1 = zero4<NV>(), s2 = zero4<NV>();
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) { fma4(s1, Dz[c], r[c]); fma4(s2, Sz[c], r[c]); }
+                        const float wgx = dx * By[b], wgy = bx * Dy[b];
+                        fma4(acc[1], wgx, s0);
+                        fma4(acc[2], wgy, s0);
+                        fma4(acc[3], wv, s1);
+                        fma4(acc[4], sxx * By[b], s0);
+                        fma4(acc[5], dx * Dy[b], s0);
+                        fma4(acc[6], wgx, s1);
+                        fma4(acc[7], bx * Sy[b], s0);
+                        fma4(acc[8], wgy, s1);
+                        fma4(acc[9], wv, s2);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar0 + 8 * (nst + slot));
+        }
+        if (has && p.spo_out) {
+            Vt *o = reinterpret_cast<Vt *>(p.spo_out + w * NQ * ld) + t;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) o[q * p.nvec] = acc[q];
+        }
+        if (!p.out || !p.Ainv) continue;
+        double part[NR];
+        auto dot = [&](const Vt &v) {
+            double d = 0.0;
+#pragma unroll
+            for (int e = 0; e < NV; ++e) d += (double)av[e] * v.v[e];
+            return d;
+        };
+        part[0] = dot(acc[0]);
+        if constexpr (VGH) {
+            part[1] = dot(acc[1]); part[2] = dot(acc[2]); part[3] = dot(acc[3]);
+            part[4] = dot(acc[4]) + dot(acc[7]) + dot(acc[9]);
+        }
+        double *rb = red + par * 8 * NR;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const double v = warp_sum_d(part[r]);
+            if (lane == 0) rb[warp * NR + r] = v;
+        }
+        named_bar(1, NCT);                          // consumers only (red is double-buffered by walker parity)
+        if (t == 0) {
+            double s[NR];
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+                s[r] = 0.0;
+                for (int k = 0; k < NC; ++k) s[r] += rb[k * NR + r];
+            }
+            double *o = p.out + w * 5;
+            o[0] = s[0];
+            if constexpr (VGH) {
+                const double inv = 1.0 / s[0];
+                o[1] = s[1] * inv; o[2] = s[2] * inv; o[3] = s[3] * inv; o[4] = s[4] * inv;
+            } else {
+                o[1] = o[2] = o[3] = o[4] = 0.0;
+            }
         }
     }
 }

@@ -39,6 +39,18 @@ def _F(L, n):
     return np.array([1, s[0], s[1], s[2], s[0] ** 2, s[0] * s[1], s[0] * s[2], s[1] ** 2, s[1] * s[2], s[2] ** 2])
 
 
+@pytest.fixture(params=["tma", "ldg"])
+def kernel(request):
+    """Both SPO kernels: the TMA-pipelined default and the LDG kernel (QJ2_SPO=ldg)."""
+    old = os.environ.pop("QJ2_SPO", None)
+    if request.param == "ldg":
+        os.environ["QJ2_SPO"] = "ldg"
+    yield request.param
+    os.environ.pop("QJ2_SPO", None)
+    if old is not None:
+        os.environ["QJ2_SPO"] = old
+
+
 def check_spo(q, nx, ny, nz, n_orb, ld, W, seed, pos_dtype=np.float32, L=(3.0, 3.5, 4.0), krow_mode=False,
               shift=0.0):
     T = qmcgen.spo_table(seed, nx, ny, nz, n_orb, ld)
@@ -71,25 +83,32 @@ def check_spo(q, nx, ny, nz, n_orb, ld, W, seed, pos_dtype=np.float32, L=(3.0, 3
 
 
 @pytest.mark.parametrize("n_orb,ld", [(1, 4), (3, 4), (10, 12), (64, 64), (130, 132), (384, 384), (600, 600)])
-def test_spo_vgh_and_ratio(q, n_orb, ld):
+def test_spo_vgh_and_ratio(q, kernel, n_orb, ld):
     check_spo(q, 6, 7, 8, n_orb, ld, 37, seed=10 + n_orb)
 
 
-def test_spo_fp64_positions_krow_and_wrapping(q):
+def test_spo_z_wrap_and_many_walkers(q, kernel):
+    """nz = 4: every walker's z rows wrap (split bulk copies); W > 32 * SMs
+    exercises several producer batches per CTA."""
+    check_spo(q, 5, 6, 4, 40, 40, 10000, seed=8)
+
+
+def test_spo_fp64_positions_krow_and_wrapping(q, kernel):
     check_spo(q, 5, 9, 4, 48, 48, 29, seed=3, pos_dtype=np.float64, krow_mode=True)
     # positions outside [0, L): wrapped into the cell (periodic table)
     check_spo(q, 5, 9, 4, 48, 48, 29, seed=4, shift=-7.25)
     check_spo(q, 5, 9, 4, 48, 48, 29, seed=5, shift=11.5)
 
 
-def test_spo_v_equals_vgh_values_bitwise(q):
+def test_spo_v_equals_vgh_values_bitwise(q, kernel):
     """Bspline-v and the value lanes of Bspline-vgh: the same sums in the same
-    order (SPEC: 'vs spo_eval_vgh value lanes: identical')."""
+    order (SPEC: 'vs spo_eval_vgh value lanes: identical'); the ratio rho is
+    the same dot product reduced over a different thread grouping (1e-12)."""
     T, tab, pos, out, spo = check_spo(q, 8, 8, 8, 96, 96, 64, seed=21)
     A = qmcgen.make_ainv_rows(21, 64, 96)
     out_v, spo_v = q.spo_eval(tab, dev(pos), vgh=False, Ainv=dev(A), want_spo=True)
     assert torch.equal(spo_v[:, 0].cpu(), torch.from_numpy(spo[:, 0]))
-    assert np.array_equal(out_v.cpu().numpy()[:, 0], out[:, 0])
+    np.testing.assert_allclose(out_v.cpu().numpy()[:, 0], out[:, 0], rtol=1e-12, atol=1e-14)
     assert np.all(out_v.cpu().numpy()[:, 1:] == 0)
 
 
@@ -106,6 +125,24 @@ def test_spo_no_ratio_and_empty(q):
 def test_spo_device_generator_matches_host(q):
     g = q.gen_spo_table(77, 6, 5, 7, 30, 32).cpu().numpy()
     assert np.array_equal(g, qmcgen.spo_table(77, 6, 5, 7, 30, 32))
+
+
+def test_spo_kernels_agree(q):
+    """The TMA-pipelined and the LDG kernels: identical per-orbital sums (same
+    order), ratios equal to rounding."""
+    T = qmcgen.spo_table(31, 9, 8, 7, 200, 200)
+    tab = q.SpoTable(dev(T), 200, (2.0, 2.5, 3.0))
+    pos = dev((np.random.default_rng(1).random((3000, 3)) * 3).astype(np.float32))
+    A = dev(qmcgen.make_ainv_rows(31, 3000, 200))
+    os.environ.pop("QJ2_SPO", None)
+    o1, s1 = q.spo_eval(tab, pos, Ainv=A, want_spo=True)
+    os.environ["QJ2_SPO"] = "ldg"
+    try:
+        o2, s2 = q.spo_eval(tab, pos, Ainv=A, want_spo=True)
+    finally:
+        os.environ.pop("QJ2_SPO", None)
+    assert torch.equal(s1, s2)
+    torch.testing.assert_close(o1, o2, rtol=1e-12, atol=1e-12)
 
 
 def test_spo_nio64_full_size_sampled(q):
