@@ -12,7 +12,7 @@ static cudaError_t launch_tma(const SpoParams &p, int nc, cudaStream_t s, bool *
     *done = false;
     const size_t stage = (size_t)16 * p.ld * 4;
     const size_t per_stage = stage + SPO_HDR * 4 + 16;
-    const size_t fixed = 2 * 8 * 5 * sizeof(double) + 128;
+    const size_t fixed = 2 * SPO_MAXC * 5 * sizeof(double) + 4 * 8 + 128;
     const size_t budget = 220 * 1024;
     int nst = (int)std::min<size_t>(16, (budget - fixed) / per_stage);
     if (nst < 4) return cudaSuccess;                 // rows too long for a deep ring: LDG kernel
@@ -35,8 +35,8 @@ static cudaError_t launch_tma(const SpoParams &p, int nc, cudaStream_t s, bool *
 cudaError_t launch_spo(const SpoParams &p, bool vgh, cudaStream_t s) {
     const char *env = getenv("QJ2_SPO");                    // A/B: "ldg" forces the LDG kernel
     const bool force_ldg = env && strcmp(env, "ldg") == 0;
-    const int64_t nc = (p.nvec + 31) / 32;
-    if (!force_ldg && nc <= 8) {
+    const int64_t nc = (p.ld / (vgh ? spo_tma_nv<true>() : spo_tma_nv<false>()) + 31) / 32;
+    if (!force_ldg && nc <= SPO_MAXC) {
         bool done = false;
         cudaError_t e = vgh ? launch_tma<true>(p, (int)nc, s, &done) : launch_tma<false>(p, (int)nc, s, &done);
         if (e != cudaSuccess || done) return e;

@@ -249,14 +249,41 @@ __global__ void __launch_bounds__(256, 2) spo_kernel(const __grid_constant__ Spo
 // (~190 KB) of gathers are in flight instead of ~50 KB of LDGs.
 // ===========================================================================
 constexpr int SPO_HDR = 48;                   // floats per stage header (36 weights, padded to 192 B)
+constexpr int SPO_MAXC = 16;                  // consumer warps per CTA, at most
+// Orbitals per consumer thread: 1 for vgh (10 accumulators; more warps to
+// hide the FMA and shared-memory latency), 2 for v.
+template <bool VGH> __host__ __device__ constexpr int spo_tma_nv() { return VGH ? 1 : 2; }
+
+template <bool VGH, int NR>
+__device__ __forceinline__ void spo_finalize(const SpoParams &p, const double *red, uint32_t rbar, int NC,
+                                             int64_t i, int64_t w) {
+    const uint32_t slot = (uint32_t)(i & 1), use = (uint32_t)(i >> 1);
+    mbar_wait(rbar + 8 * slot, use & 1);
+    const double *rb = red + slot * SPO_MAXC * NR;
+    double s[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        s[r] = 0.0;
+        for (int k = 0; k < NC; ++k) s[r] += rb[k * NR + r];
+    }
+    mbar_arrive(rbar + 8 * (2 + slot));
+    double *o = p.out + w * 5;
+    o[0] = s[0];
+    if constexpr (VGH) {
+        const double inv = 1.0 / s[0];
+        o[1] = s[1] * inv; o[2] = s[2] * inv; o[3] = s[3] * inv; o[4] = s[4] * inv;
+    } else {
+        o[1] = o[2] = o[3] = o[4] = 0.0;
+    }
+}
 
 template <bool VGH>
 __global__ void spo_tma_kernel(const __grid_constant__ SpoParams p, int nst) {
-    constexpr int NV = VGH ? 2 : 4;
+    constexpr int NV = spo_tma_nv<VGH>();    // orbitals per consumer thread
     using Vt = FV<NV>;
     constexpr int NQ = VGH ? 10 : 1;
     constexpr int NR = VGH ? 5 : 1;
-    const int NC = blockDim.x / 32 - 1;       // consumer warps
+    const int NC = blockDim.x / 32 - 1;       // consumer warps (<= SPO_MAXC)
     const int64_t ld = p.ld;
     const uint32_t stage_bytes = (uint32_t)(16 * ld * 4);
 
@@ -264,7 +291,8 @@ __global__ void spo_tma_kernel(const __grid_constant__ SpoParams p, int nst) {
     float *ring = reinterpret_cast<float *>(smem);                                        // [nst][16][ld]
     float *hdr = reinterpret_cast<float *>(smem + (size_t)nst * stage_bytes);             // [nst][SPO_HDR]
     uint64_t *bars = reinterpret_cast<uint64_t *>(hdr + (size_t)nst * SPO_HDR);          // full[nst], empty[nst]
-    double *red = reinterpret_cast<double *>(bars + 2 * nst);                             // [2][8][NR]
+    double *red = reinterpret_cast<double *>(bars + 2 * nst);                             // [2][SPO_MAXC][NR]
+    const uint32_t rbar = (uint32_t)__cvta_generic_to_shared(red + 2 * SPO_MAXC * NR);    // full[2], empty[2]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(bars);
     const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(ring);
@@ -272,6 +300,10 @@ __global__ void spo_tma_kernel(const __grid_constant__ SpoParams p, int nst) {
         for (int st = 0; st < nst; ++st) {
             mbar_init(bar0 + 8 * st, 1);                  // full: the producer's expect_tx arrival
             mbar_init(bar0 + 8 * (nst + st), NC);         // empty: one arrival per consumer warp
+        }
+        for (int sl = 0; sl < 2; ++sl) {
+            mbar_init(rbar + 8 * sl, NC);                 // ratio partials published by every consumer warp
+            mbar_init(rbar + 8 * (2 + sl), 1);            // ... and read by the finalizer
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -356,10 +388,11 @@ __global__ void spo_tma_kernel(const __grid_constant__ SpoParams p, int nst) {
     // =====================  consumer warps  =====================
     const int t = threadIdx.x;                  // consumer thread: orbital vector j = t
     const int NCT = NC * 32;
-    const bool has = t < p.nvec;
+    const int64_t nvec = ld / NV;
+    const bool has = t < nvec;
     uint32_t n = 0;
-    int par = 0;
-    for (int64_t w = blockIdx.x; w < p.W; w += G, par ^= 1) {
+    int64_t it = 0, w_prev = -1;
+    for (int64_t w = blockIdx.x; w < p.W; w += G, ++it) {
         // A^{-1} row entries of this thread's orbitals (used after the gather)
         float av[NV];
         const float *arow = p.Ainv ? p.Ainv + w * p.ainv_stride + (p.krow ? (int64_t)p.krow[w] * p.ainv_ld : 0)
@@ -419,7 +452,7 @@ __global__ void spo_tma_kernel(const __grid_constant__ SpoParams p, int nst) {
         if (has && p.spo_out) {
             Vt *o = reinterpret_cast<Vt *>(p.spo_out + w * NQ * ld) + t;
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) o[q * p.nvec] = acc[q];
+            for (int q = 0; q < NQ; ++q) o[q * nvec] = acc[q];
         }
         if (!p.out || !p.Ainv) continue;
         double part[NR];
@@ -434,30 +467,23 @@ __global__ void spo_tma_kernel(const __grid_constant__ SpoParams p, int nst) {
             part[1] = dot(acc[1]); part[2] = dot(acc[2]); part[3] = dot(acc[3]);
             part[4] = dot(acc[4]) + dot(acc[7]) + dot(acc[9]);
         }
-        double *rb = red + par * 8 * NR;
+        // partials -> 2-slot ring in shared memory (full: NC warp arrivals,
+        // empty: the finalizer's arrival); thread 0 finalizes walker i - 1
+        // after publishing walker i, so no warp waits for the others here.
+        const uint32_t slot = (uint32_t)(it & 1), use = (uint32_t)(it >> 1);
+        double *rb = red + slot * SPO_MAXC * NR;
+        if (lane == 0) mbar_wait(rbar + 8 * (2 + slot), (use & 1) ^ 1);
+        __syncwarp();
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
             const double v = warp_sum_d(part[r]);
             if (lane == 0) rb[warp * NR + r] = v;
         }
-        named_bar(1, NCT);                          // consumers only (red is double-buffered by walker parity)
-        if (t == 0) {
-            double s[NR];
-#pragma unroll
-            for (int r = 0; r < NR; ++r) {
-                s[r] = 0.0;
-                for (int k = 0; k < NC; ++k) s[r] += rb[k * NR + r];
-            }
-            double *o = p.out + w * 5;
-            o[0] = s[0];
-            if constexpr (VGH) {
-                const double inv = 1.0 / s[0];
-                o[1] = s[1] * inv; o[2] = s[2] * inv; o[3] = s[3] * inv; o[4] = s[4] * inv;
-            } else {
-                o[1] = o[2] = o[3] = o[4] = 0.0;
-            }
-        }
+        if (lane == 0) mbar_arrive(rbar + 8 * slot);
+        if (t == 0 && it > 0) spo_finalize<VGH, NR>(p, red, rbar, NC, it - 1, w_prev);
+        w_prev = w;
     }
+    if (t == 0 && it > 0 && p.out && p.Ainv) spo_finalize<VGH, NR>(p, red, rbar, NC, it - 1, w_prev);
 }
 
 cudaError_t launch_spo(const SpoParams &p, bool vgh, cudaStream_t s);
