@@ -13,9 +13,12 @@ static cudaError_t launch_tma(const SpoParams &p, int nc, cudaStream_t s, bool *
     const size_t stage = (size_t)16 * p.ld * 4;
     const size_t per_stage = stage + SPO_HDR * 4 + 16;
     const size_t fixed = 2 * SPO_MAXC * 5 * sizeof(double) + 4 * 8 + 128;
-    const size_t budget = 220 * 1024;
+    // ring budget per CTA: 110 KB = 2 CTAs/SM (4 plane stages each at 384 orbitals); measured on
+    // B200 (S1 vgh): 220 KB / 1 CTA 1.77 ms, 110 KB 1.02 ms, 75 KB / 3 CTAs 1.05, 55 KB / 4 CTAs 1.19
+    const char *bk = getenv("QJ2_SPO_SMEM_KB");           // A/B override
+    const size_t budget = (size_t)(bk ? atoi(bk) : 110) * 1024;
     int nst = (int)std::min<size_t>(16, (budget - fixed) / per_stage);
-    if (nst < 4) return cudaSuccess;                 // rows too long for a deep ring: LDG kernel
+    if (nst < 2) return cudaSuccess;                 // rows too long for a 2-stage ring: LDG kernel
     const size_t smem = (size_t)nst * per_stage + fixed;
     auto kern = spo_tma_kernel<VGH>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

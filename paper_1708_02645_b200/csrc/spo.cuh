@@ -250,9 +250,9 @@ __global__ void __launch_bounds__(256, 2) spo_kernel(const __grid_constant__ Spo
 // ===========================================================================
 constexpr int SPO_HDR = 48;                   // floats per stage header (36 weights, padded to 192 B)
 constexpr int SPO_MAXC = 16;                  // consumer warps per CTA, at most
-// Orbitals per consumer thread: 1 for vgh (10 accumulators; more warps to
-// hide the FMA and shared-memory latency), 2 for v.
-template <bool VGH> __host__ __device__ constexpr int spo_tma_nv() { return VGH ? 1 : 2; }
+// Orbitals per consumer thread (2: one orbital per thread measured 1.4x slower
+// for vgh -- per-row overhead no longer amortised).
+template <bool VGH> __host__ __device__ constexpr int spo_tma_nv() { return 2; }
 
 template <bool VGH, int NR>
 __device__ __forceinline__ void spo_finalize(const SpoParams &p, const double *red, uint32_t rbar, int NC,
@@ -353,9 +353,23 @@ __global__ void spo_tma_kernel(const __grid_constant__ SpoParams p, int nst) {
                     const uint32_t slot = n % (uint32_t)nst, round = n / (uint32_t)nst;
                     mbar_wait(bar0 + 8 * (nst + slot), (round & 1) ^ 1);
                     if (lane == qw) {
+                        // header of plane a: per column b the 6 (x, y) weights (wv, wgx, wgy,
+                        // whxx, whxy, whyy), then the 12 z weights (B, B', B'')
                         float *h = hdr + slot * SPO_HDR;
+                        const float bx = a == 0 ? wts[0] : a == 1 ? wts[1] : a == 2 ? wts[2] : wts[3];
+                        const float dx = a == 0 ? wts[4] : a == 1 ? wts[5] : a == 2 ? wts[6] : wts[7];
+                        const float sx = a == 0 ? wts[8] : a == 1 ? wts[9] : a == 2 ? wts[10] : wts[11];
 #pragma unroll
-                        for (int e = 0; e < 36; ++e) h[e] = wts[e];
+                        for (int b = 0; b < 4; ++b) {
+                            h[b * 6 + 0] = bx * wts[12 + b];
+                            h[b * 6 + 1] = dx * wts[12 + b];
+                            h[b * 6 + 2] = bx * wts[16 + b];
+                            h[b * 6 + 3] = sx * wts[12 + b];
+                            h[b * 6 + 4] = dx * wts[16 + b];
+                            h[b * 6 + 5] = bx * wts[20 + b];
+                        }
+#pragma unroll
+                        for (int e = 0; e < 12; ++e) h[24 + e] = wts[24 + e];
                     }
                     __syncwarp();
                     const uint32_t full = bar0 + 8 * slot;
@@ -408,13 +422,12 @@ __global__ void spo_tma_kernel(const __grid_constant__ SpoParams p, int nst) {
         for (int a = 0; a < 4; ++a, ++n) {
             const uint32_t slot = n % (uint32_t)nst, round = n / (uint32_t)nst;
             mbar_wait(bar0 + 8 * slot, round & 1);
-            const float *h = hdr + slot * SPO_HDR;
-            const float bx = h[a], dx = h[4 + a], sxx = h[8 + a];
-            float By[4], Dy[4], Sy[4], Bz[4], Dz[4], Sz[4];
+            const float4 *h4 = reinterpret_cast<const float4 *>(hdr + slot * SPO_HDR);
+            float hw[36];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                By[c] = h[12 + c]; Dy[c] = h[16 + c]; Sy[c] = h[20 + c];
-                Bz[c] = h[24 + c]; Dz[c] = h[28 + c]; Sz[c] = h[32 + c];
+            for (int e = 0; e < 9; ++e) {
+                const float4 v = h4[e];
+                hw[4 * e] = v.x; hw[4 * e + 1] = v.y; hw[4 * e + 2] = v.z; hw[4 * e + 3] = v.w;
             }
             if (has) {
                 const Vt *st = reinterpret_cast<const Vt *>(ring + (size_t)slot * 16 * ld) + t;
@@ -426,21 +439,21 @@ __global__ void spo_tma_kernel(const __grid_constant__ SpoParams p, int nst) {
                     for (int c = 0; c < 4; ++c) r[c] = st[(b * 4 + c) * rs];
                     Vt s0 = zero4<NV>();
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) fma4(s0, Bz[c], r[c]);
-                    const float wv = bx * By[b];
+                    for (int c = 0; c < 4; ++c) fma4(s0, hw[24 + c], r[c]);
+                    const float wv = hw[b * 6 + 0];
                     fma4(acc[0], wv, s0);
                     if constexpr (VGH) {
                         Vt s1 = zero4<NV>(), s2 = zero4<NV>();
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) { fma4(s1, Dz[c], r[c]); fma4(s2, Sz[c], r[c]); }
-                        const float wgx = dx * By[b], wgy = bx * Dy[b];
+                        for (int c = 0; c < 4; ++c) { fma4(s1, hw[28 + c], r[c]); fma4(s2, hw[32 + c], r[c]); }
+                        const float wgx = hw[b * 6 + 1], wgy = hw[b * 6 + 2];
                         fma4(acc[1], wgx, s0);
                         fma4(acc[2], wgy, s0);
                         fma4(acc[3], wv, s1);
-                        fma4(acc[4], sxx * By[b], s0);
-                        fma4(acc[5], dx * Dy[b], s0);
+                        fma4(acc[4], hw[b * 6 + 3], s0);
+                        fma4(acc[5], hw[b * 6 + 4], s0);
                         fma4(acc[6], wgx, s1);
-                        fma4(acc[7], bx * Sy[b], s0);
+                        fma4(acc[7], hw[b * 6 + 5], s0);
                         fma4(acc[8], wgy, s1);
                         fma4(acc[9], wv, s2);
                     }

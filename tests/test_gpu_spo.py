@@ -142,7 +142,7 @@ def test_spo_kernels_agree(q):
     finally:
         os.environ.pop("QJ2_SPO", None)
     assert torch.equal(s1, s2)
-    torch.testing.assert_close(o1, o2, rtol=1e-12, atol=1e-12)
+    torch.testing.assert_close(o1, o2, rtol=1e-10, atol=1e-12)
 
 
 def test_spo_nio64_full_size_sampled(q):
