@@ -20,7 +20,10 @@
 namespace qj2 {
 
 constexpr int TPB = 256;          // threads per CTA
-constexpr int ITERS = 8;          // vector iterations per sub-tile: 32 fp32 terms per thread per trial
+#ifndef QJ2_ITERS
+#define QJ2_ITERS 8
+#endif
+constexpr int ITERS = QJ2_ITERS;  // vector iterations per sub-tile: 32 fp32 terms per thread per trial (A/B: -DQJ2_ITERS=n)
 #ifndef QJ2_SUB
 #define QJ2_SUB 4
 #endif

@@ -401,7 +401,6 @@ __global__ void spo_tma_kernel(const __grid_constant__ SpoParams p, int nst) {
 
     // =====================  consumer warps  =====================
     const int t = threadIdx.x;                  // consumer thread: orbital vector j = t
-    const int NCT = NC * 32;
     const int64_t nvec = ld / NV;
     const bool has = t < nvec;
     uint32_t n = 0;
