@@ -80,6 +80,40 @@ def eval_sharded(R_local, k, r_trial, fn, n_total: int, n_up: int, i_offset: int
     return out
 
 
+def _default(name):
+    """An entry point of the CUDA library package (no CPU path)."""
+    import importlib
+    return getattr(importlib.import_module(__package__), name)
+
+
+def sweep_step_sharded(R_local, state_local, k, r_trial, u, fn, n_total: int, n_up: int, i_offset: int,
+                       n_local: int, *, group=None, out=None, ratio_out=None, acc=None, workspace=None,
+                       accept_workspace=None, eval_fn: Callable | None = None, ratio_fn: Callable | None = None,
+                       metropolis_fn: Callable | None = None, accept_fn: Callable | None = None):
+    """One particle-by-particle move of every walker on a source-axis split
+    (NEXT-2 at C5 scale; Alg. 1 L5-L9 for the J2 factor):
+
+    1. eval_sharded with the P = 2 drift trials (r_k, r'_k): this rank's partial
+       (V, G, L), one all_reduce(SUM), e^{dJ2} of trial 1 against trial 0;
+    2. Metropolis u < rho^2 -- identical on every rank (the reduced sums and u
+       are replicated), so no exchange of decisions;
+    3. accept on this rank's slice of R and of the 5N state, with r_old = trial 0
+       (= r_k, replicated: no exchange of positions); only the rank whose slice
+       holds k commits r'_k and state_k (= the reduced out of trial 1).
+
+    Returns (out [W][2][5], ratio [W][2][2], acc [W])."""
+    out, ratio = eval_sharded(R_local, k, r_trial, fn, n_total, n_up, i_offset, n_local, group=group, ratio=True,
+                              out=out, ratio_out=ratio_out, workspace=workspace, eval_fn=eval_fn,
+                              ratio_fn=ratio_fn)
+    metropolis_fn = metropolis_fn or _default("metropolis")
+    accept_fn = accept_fn or _default("accept")
+    acc = metropolis_fn(ratio, u, acc, trial=1)
+    r_old = r_trial[:, 0, :].contiguous()
+    accept_fn(R_local, state_local, k, r_trial, acc, out, fn, n_total, n_up, trial=1, i_offset=i_offset,
+              n_local=n_local, r_old=r_old, workspace=accept_workspace)
+    return out, ratio, acc
+
+
 def gather_instances(local: torch.Tensor, counts: Iterable[int], group=None) -> torch.Tensor:
     """Concatenate per-rank results of the by-instance split on every rank
     (outside the timed region; e.g. per-instance checksums)."""

@@ -115,3 +115,91 @@ def test_source_split_allreduce_gloo_world2():
         assert err < 1e-13, (rank, err)          # reduced partials == unsplit oracle
         assert rerr < 1e-12, (rank, rerr)
         assert g == [[0.0] * 5] * 3 + [[1.0] * 5] * 2
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2 at C5 scale: one PbyP move on a source-axis split (sweep_step_sharded)
+# ---------------------------------------------------------------------------
+def _numpy_metropolis(ratio, u, acc=None, trial=0):
+    rho = ratio.numpy()[:, trial, 1]
+    return torch.from_numpy((u.numpy() < rho * rho).astype(np.int32))
+
+
+def _oracle_accept_slice(R_local, S_local, k, r_trial, acc, out, fn, n_total, n_up, trial=0, i_offset=0,
+                         n_local=None, r_old=None, workspace=None):
+    """CPU stand-in for qj2_accept on a slice with the kernel's semantics: the
+    oracle's partner update on the slice's electrons (r_k from the caller's
+    r_old), state_k = the reduced eval output of the accepted trial, R[:, k]
+    committed by the owner."""
+    W, _, Np = R_local.shape
+    Rl, Sl = R_local.numpy(), S_local.numpy()
+    a, b = i_offset, i_offset + n_local
+    ro, rn = r_old.numpy(), r_trial.numpy()[:, trial]
+    for w in range(W):
+        if not acc[w]:
+            continue
+        kw = int(k[w])
+        # a full-length stand-in row: the slice's electrons in place, r_k at k
+        Rf = np.zeros((1, 3, n_total))
+        Rf[0, :, a:b] = Rl[w, :, :n_local]
+        Rf[0, :, kw] = ro[w]
+        Sf = np.zeros((1, 5, n_total))
+        Sf[0, :, a:b] = Sl[w, :, :n_local]
+        _, S2, _ = oracle.accept(Rf, Sf, np.array([kw], np.int32), rn[w:w + 1], np.ones(1, np.int32), fn,
+                                 n_total, n_up)
+        Sl[w, :, :n_local] = S2[0, :, a:b]
+        if a <= kw < b:
+            Sl[w, :, kw - a] = out.numpy()[w, trial]
+            Rl[w, :, kw - a] = rn[w]
+    return R_local, S_local
+
+
+def _sweep_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        N, W = 150, 8
+        L = qmcgen.cell_length(N)
+        R = qmcgen.positions(9, np.arange(W), N, N, L, np.float64)
+        fn = qmcgen.make_functor(9, L)
+        state = np.stack([oracle.j2_state(R[w], N, N // 2, fn)[0] for w in range(W)])
+        ks, tr, u = qmcgen.make_sweep(9, W, N, L, np.float64, 1)
+        k, rt, uu = ks[0], tr[0], u[0]
+        a, b = parallel.shard_bounds(N, rank, world)
+        Rl = torch.from_numpy(np.ascontiguousarray(R[:, :, a:b]))
+        Sl = torch.from_numpy(np.ascontiguousarray(state[:, :, a:b]))
+        out, rat, acc = parallel.sweep_step_sharded(
+            Rl, Sl, torch.from_numpy(k), torch.from_numpy(rt), torch.from_numpy(uu), fn, N, N // 2, a, b - a,
+            eval_fn=_oracle_eval, ratio_fn=_numpy_ratio, metropolis_fn=_numpy_metropolis,
+            accept_fn=_oracle_accept_slice)
+        # unsplit reference: oracle eval, the same decision, oracle accept
+        full, _, _ = oracle.eval_j2(R, k, rt, fn, N, N // 2)
+        acc_ref = (uu < np.exp(full[:, 1, 0] - full[:, 0, 0]) ** 2).astype(np.int32)
+        R2, S2, ab = oracle.accept(R, state, k, rt[:, 1], acc_ref, fn, N, N // 2)
+        serr = float(oracle.normalized_error_state(Sl.numpy(), S2[:, :, a:b], np.nan_to_num(ab[:, :, a:b]),
+                                                   fn).max())
+        q.put((rank, acc.numpy().tolist(), acc_ref.tolist(), bool(np.array_equal(Rl.numpy(), R2[:, :, a:b])),
+               serr))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sweep_step_source_split_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world = 2
+    port = _free_port()
+    procs = [ctx.Process(target=_sweep_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    accs = [r[1] for r in res]
+    assert accs[0] == accs[1] == res[0][2]          # identical decisions on every rank, = the unsplit oracle
+    assert 0 < sum(accs[0]) < len(accs[0])
+    for rank, _, _, r_ok, serr in res:
+        assert r_ok, rank                            # positions: only the owner of k commits r'_k
+        assert serr < 1e-12, (rank, serr)
