@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C3S", "C3P2", "C3P12", "S1"])
+    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C3S", "C3P2", "C3P12", "S1", "J1S"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -252,12 +252,49 @@ class OracleSampleSpo:
         return time.perf_counter() - t0
 
 
+class OracleSampleJ1:
+    """NEXT-1 CPU oracle sample: oracle.eval_j1 (single-threaded as it stands)
+    on the first n trial points of the J1S sweep batch."""
+
+    def __init__(self, cfg, n, threads):
+        self.cfg, self.n = cfg, int(max(1, min(n, cfg.W)))
+        self.ions, self.start, self.rt, self.fn1 = j1_inputs(cfg, self.n)
+        self.ions = self.ions.astype(np.float64)
+        self.rt = self.rt.astype(np.float64)
+        self.items = self.n * cfg.n_ions
+
+    def run(self):
+        import oracle
+        t0 = time.perf_counter()
+        oracle.eval_j1(self.ions, self.start, self.rt, self.fn1)
+        return time.perf_counter() - t0
+
+
+def j1_inputs(cfg, n=None):
+    """ions [3][Np], species_start, trial points [n][1][3] (fp32), J1 functor of a J1 config."""
+    import qmcgen
+    n = cfg.W if n is None else n
+    ions, start = qmcgen.make_ions(cfg.seed, cfg.n_ions, qmcgen.padded_size(cfg.n_ions, 4), cfg.L, np.float32,
+                                   n_species=cfg.n_species)
+    fn1 = qmcgen.make_j1_functor(cfg.seed, cfg.L, n_species=cfg.n_species)
+    ids = np.arange(n)
+    k = (ids % cfg.N).astype(np.int32)                 # electron of each trial point
+    rt = qmcgen.make_trials(cfg.seed, ids, k, cfg.N, cfg.L, np.float32)
+    return ions, start, rt, fn1
+
+
 def make_oracle_sample(cfg, n, threads):
-    return OracleSampleSpo(cfg, n, threads) if cfg.name.startswith("S") else OracleSample(cfg, n, threads)
+    if cfg.name.startswith("S"):
+        return OracleSampleSpo(cfg, n, threads)
+    if cfg.name.startswith("J"):
+        return OracleSampleJ1(cfg, n, threads)
+    return OracleSample(cfg, n, threads)
 
 
 def _what(cfg):
     import qmcgen
+    if cfg.name.startswith("J"):
+        return f"J1 over {cfg.n_ions} ions of {cfg.n_species} species, one trial point per row"
     if cfg.name.startswith("S"):
         return f"Bspline-vgh of {cfg.n_orb} orbitals + determinant ratio, {cfg.nx}x{cfg.ny}x{cfg.nz} grid"
     if cfg.name == "C3S":
@@ -274,7 +311,7 @@ def oracle_sample_size(cfg, cores, budget_s):
     dt0 = s0.run()
     per_round = max(dt0, 1e-6)              # one walker per core
     n = int(budget_s / per_round) * cores
-    if cfg.name.startswith("S"):            # the SPO oracle runs on one thread
+    if cfg.name[0] in "SJ":                 # the SPO and J1 oracles run on one thread
         n = int(budget_s / per_round * n0)
     return max(n0, min(cfg.W, n)), s0.items / dt0
 
@@ -313,7 +350,7 @@ def run_reference(args):
     times = [smp.run() for _ in range(args.steps)]
     t = float(np.mean(times))
     value = smp.items / t
-    used = 1 if cfg.name.startswith("S") else cores
+    used = 1 if cfg.name[0] in "SJ" else cores
     sample = (f"{smp.n} of {cfg.W} walkers of {cfg.name} (N={cfg.N}, {_what(cfg)}) per step, fp32 inputs promoted "
               f"exactly to fp64, plain C oracle, {used} threads ({cpu_model()})")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -328,6 +365,12 @@ def run_reference(args):
 
 def workload_config(cfg, world):
     name = cfg.name
+    if name.startswith("J"):
+        return {"workload": f"{name} (NEXT-1): the J1 share of one PbyP sweep of {cfg.walkers} walkers of a NiO-64-"
+                            f"shaped system (N={cfg.N} electrons, {cfg.n_ions} ions of {cfg.n_species} species), "
+                            f"W={cfg.W} independent trial points per rank, fp32",
+                "N": cfg.N, "n_ions": cfg.n_ions, "W": cfg.W, "parallelism": f"walker-batch x{world}",
+                "l2": "ions shared (L2/shared-memory resident); trial points stream"}
     if name.startswith("S"):
         return {"workload": f"{name} (NEXT-4): NiO-64-shaped SPO set (Table 1: {cfg.nx}x{cfg.ny}x{cfg.nz} grid, "
                             f"{cfg.n_orb} orbitals = N/2 for N={cfg.N}, fp32 table {cfg.table_bytes / 1e6:.0f} MB), "
@@ -828,7 +871,62 @@ class SpoPlan:
                        "(the shared table stays resident)"}
 
 
+class J1Plan:
+    """NEXT-1: one qj2_eval_j1 launch over a full sweep's trial points (ions in
+    shared memory, one thread per trial point).  Issue-bound: ALU roofline."""
+    mode = "J1S"
+    launches_per_step = 1
+    OPS_PER_PAIR = 36
+
+    def __init__(self, cfg, rank, world):
+        self.cfg = cfg
+        self.items_per_step = cfg.W * cfg.n_ions
+
+    def items_total(self, world):
+        return self.items_per_step * world
+
+    @property
+    def alg_bytes_per_launch(self):
+        cfg = self.cfg
+        return cfg.W * (12 + 40 + 16) + cfg.n_ions * 12
+
+    def prepare(self, q):
+        import torch
+        cfg = self.cfg
+        ions, self.start, rt, fn1 = j1_inputs(cfg)
+        self.fn1 = q.J1Functor.of(fn1)
+        self.ions = torch.from_numpy(ions).cuda()
+        self.rt = torch.from_numpy(rt).cuda()
+        self.out = torch.empty((cfg.W, 1, 5), dtype=torch.float64, device="cuda")
+        self.ratio = torch.empty((cfg.W, 1, 2), dtype=torch.float64, device="cuda")
+        self.V_cur = torch.zeros((cfg.W,), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+
+    def step(self, q, dist_mod):
+        q.eval_j1(self.ions, self.start, self.rt, self.fn1, V_cur=self.V_cur, ratio=True, out=self.out,
+                  ratio_out=self.ratio)
+
+    def kernel_ms(self, q, stream, reps):
+        return _event_ms(lambda: self.step(q, None), stream, reps)
+
+    def roofline(self, kms, peak_hbm):
+        cfg = self.cfg
+        ops = cfg.W * cfg.n_ions * self.OPS_PER_PAIR
+        peak = 148 * 128 * 1.965e9 / 1e12
+        achieved = ops / (kms / 1e3) / 1e12
+        return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": committed_traffic(self.mode), "kernel": "j1_thread_kernel<float>", "kernel_ms": kms,
+                "alg_ops_per_launch": ops, "ops_per_pair": self.OPS_PER_PAIR,
+                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1.965 GHz, one op per lane per clock "
+                               "(DESIGN.md section 7)"}
+
+    def e2e(self, q, steps, dist_mod):
+        return None
+
+
 def make_plan(cfg, rank, world):
+    if cfg.name.startswith("J"):
+        return J1Plan(cfg, rank, world)
     if cfg.name.startswith("S"):
         return SpoPlan(cfg, rank, world)
     if cfg.name in ("C3P2", "C3P12"):
@@ -912,7 +1010,7 @@ def run_ours(args):
         nw = args.cpu_sample_walkers or oracle_sample_size(cfg, cores, 15.0)[0]
         smp = make_oracle_sample(cfg, nw, cores)
         dt = smp.run()
-        used = 1 if cfg.name.startswith("S") else cores
+        used = 1 if cfg.name[0] in "SJ" else cores
         cpu = {"value": smp.items / dt, "unit": UNIT, "cores": used, "kind": "oracle",
                "sample": f"{smp.n} of {cfg.W} walkers of {cfg.name} (N={cfg.N}, {_what(cfg)}), one pass, fp32 inputs "
                          f"promoted exactly to fp64, plain C oracle, {used} threads ({cpu_model()}), "
@@ -922,7 +1020,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "weak" if plan.mode in ("C3", "C3S", "C3P2", "C3P12", "S1") else "strong",
+            "scaling": "weak" if plan.mode in ("C3", "C3S", "C3P2", "C3P12", "S1", "J1S") else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(cfg, world),
             "roofline": (plan.roofline(kms, peak) if hasattr(plan, "roofline") else

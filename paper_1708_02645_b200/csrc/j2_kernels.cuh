@@ -641,4 +641,72 @@ j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
     }
 }
 
+
+// ===========================================================================
+// J1 with a small ion set (NEXT-1; NiO-64 has 64 ions): one thread per
+// (walker, trial).  The ions (x|y|z, padded to 16 B per ion) and the
+// species' functor rows are staged in shared memory once per CTA; every
+// thread walks all ions species by species (a uniform loop: all lanes read
+// the same ion, a shared-memory broadcast) with the species' constants, fp32
+// partials of <= 32 terms flushed to fp64 in physical units.  No cross-thread
+// reduction at all.  The ions are fixed and shared by every walker
+// (PAPER:1306-1308).
+// ===========================================================================
+constexpr int J1_MAX_IONS = 4096;
+
+template <typename T>
+__global__ void __launch_bounds__(TPB) j1_thread_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
+    using Tr = Traits<T>;
+    __shared__ Coef4<T> tab[MAXTAB];
+    extern __shared__ __align__(16) unsigned char j1_smem[];
+    T *ion = reinterpret_cast<T *>(j1_smem);          // [n][4]: x, y, z, 0
+    load_table<T>(p, tab);
+    const T *src = static_cast<const T *>(p.R);
+    for (int64_t i = threadIdx.x; i < p.N_local; i += blockDim.x) {
+        ion[i * 4 + 0] = src[i];
+        ion[i * 4 + 1] = src[p.Np + i];
+        ion[i * 4 + 2] = src[2 * p.Np + i];
+        ion[i * 4 + 3] = T(0);
+    }
+    __syncthreads();
+    const int64_t unit = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (unit >= n_units) return;
+    const int64_t w = unit / p.P;
+    const int32_t pp = (int32_t)(unit - w * p.P);
+    const T *rt = static_cast<const T *>(p.r_trial) + unit * 3;
+    const Axis<T> ax = make_axis<T>(rt[0], T(p.L[0])), ay = make_axis<T>(rt[1], T(p.L[1])),
+                  az = make_axis<T>(rt[2], T(p.L[2]));
+    const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tab);
+    double dacc[NOUT] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int g = 0; g < p.n_src_groups; ++g) {
+        const GroupC<T> gc = group_consts<T, MODE_J1>(p, g, 0, tab_addr);
+        const int64_t i1 = p.grp_start[g + 1];
+        for (int64_t i0 = p.grp_start[g]; i0 < i1; i0 += 32) {
+            const int64_t ie = min(i0 + 32, i1);
+            T acc[NACC] = {T(0), T(0), T(0), T(0), T(0), T(0)};
+#pragma unroll 4
+            for (int64_t i = i0; i < ie; ++i) {
+                const T x = ion[i * 4 + 0], y = ion[i * 4 + 1], z = ion[i * 4 + 2];
+                const T dx = min_image(x, ax), dy = min_image(y, ay), dz = min_image(z, az);
+                const T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                accumulate<T>(dx, dy, dz, r2, gc.invd, gc.base, gc.clamp, acc);
+            }
+            dacc[0] += (double)acc[0];
+            dacc[1] += gc.sg * (double)acc[1];
+            dacc[2] += gc.sg * (double)acc[2];
+            dacc[3] += gc.sg * (double)acc[3];
+            dacc[4] += gc.sh * (double)acc[4] + gc.ss * (double)acc[5];
+        }
+    }
+    double *o = p.out + unit * 5;
+#pragma unroll
+    for (int a = 0; a < NOUT; ++a) o[a] = dacc[a];
+    if (p.ratio_out) {     // V_cur, or (P == 1) the fused reference is this unit itself
+        const double dj = dacc[0] - (p.V_cur ? p.V_cur[w] : dacc[0]);
+        p.ratio_out[unit * 2 + 0] = dj;
+        p.ratio_out[unit * 2 + 1] = exp(dj);
+    }
+    (void)pp;
+}
+
 }  // namespace qj2

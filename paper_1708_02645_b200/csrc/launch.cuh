@@ -59,6 +59,20 @@ inline bool use_warp_mapping(const EvalParams &p) {
 
 template <typename T, int PB, int MODE>
 cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStream_t s) {
+    if constexpr (MODE == MODE_J1) {
+        // small ion sets: one thread per (walker, trial), ions in shared memory
+        if (!row && p.N_local <= J1_MAX_IONS && !getenv("QJ2_J1_WARP")) {
+            const int64_t units = p.W * p.P;
+            const size_t smem = (size_t)p.N_local * 4 * sizeof(T);
+            auto kern = j1_thread_kernel<T>;
+            if (smem > 48 * 1024) {
+                cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e != cudaSuccess) return e;
+            }
+            kern<<<(unsigned)((units + TPB - 1) / TPB), TPB, smem, s>>>(p, units);
+            return cudaGetLastError();
+        }
+    }
     if (use_warp_mapping(p)) {
         const int64_t units = p.W * p.n_groups;
         const unsigned nbw = (unsigned)((units + TPB / 32 - 1) / (TPB / 32));

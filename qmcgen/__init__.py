@@ -307,6 +307,34 @@ SPO_CONFIGS = {
 }
 
 
+@dataclasses.dataclass(frozen=True)
+class J1Config:
+    """NEXT-1 workload: the J1 share of one full PbyP sweep of a walker
+    population, batched (DeltaJ1 of a move depends only on r_k and r'_k, so
+    all proposals of a sweep are independent): W walkers x N electrons trial
+    points against N_ion ions of S species (Table 1)."""
+    name: str
+    N: int
+    n_ions: int
+    n_species: int
+    walkers: int
+    seed: int
+
+    @property
+    def W(self) -> int:
+        return self.walkers * self.N            # trial points (one per electron move)
+
+    @property
+    def L(self) -> float:
+        return cell_length(self.N)
+
+
+J1_CONFIGS = {
+    # NiO-64 (Table 1): N = 768 electrons, 64 ions (Ni, O), the paper's 1024-walker population
+    "J1S": J1Config("J1S", N=768, n_ions=64, n_species=2, walkers=1024, seed=13),
+}
+
+
 def spo_positions(seed: int, W: int, L: float) -> np.ndarray:
     """W positions uniform in the cell (fp32), the r'_k of one move per walker."""
     rng = np.random.default_rng([int(seed), 8])
@@ -413,6 +441,8 @@ def config(name: str):
         return dataclasses.replace(CONFIGS["C3"], name=name)
     if name in SPO_CONFIGS:
         return SPO_CONFIGS[name]
+    if name in J1_CONFIGS:
+        return J1_CONFIGS[name]
     return CONFIGS[name]
 
 

@@ -96,3 +96,48 @@ def test_j1_validation(q):
         q.eval_j1(dev(ions), [0, 60, 50], dev(rt), fn1)          # not nondecreasing
     with pytest.raises(q.QJ2Error):
         q.eval_j1(dev(ions), [1, 50, 100], dev(rt), fn1)         # must start at 0
+
+
+# ---------------------------------------------------------------------------
+# Small ion sets: the thread-per-(walker, trial) kernel (ions in shared memory)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("n_ions,S", [(64, 2), (33, 3), (4096, 4)])
+def test_j1_thread_kernel_many_walkers(q, dtype, n_ions, S):
+    """NiO-64-sized ion sets (64 ions, Ni and O) and the largest staged set,
+    many walkers; sampled walkers vs the oracle."""
+    ions, start, rt, fn1 = j1_case(n_ions, 20000, seed=900 + n_ions, dtype=dtype, S=S)
+    check(q, ions, start, rt, fn1, dtype, sample=np.r_[0:40, 19990:20000])
+
+
+def test_j1_thread_kernel_nlpp_and_ratio(q):
+    """P = 12 quadrature points per walker through the thread kernel; ratios
+    against V_cur and against trial 0 (second launch)."""
+    import qmcgen as g
+    ions, start, _, fn1 = j1_case(64, 300, seed=31, dtype=np.float32)
+    N = 768
+    k = g.make_k(31, 300, N)
+    rt = g.make_trials(31, np.arange(300), k, N, g.cell_length(N), np.float32, P=12, mode="nlpp")
+    rt = np.mod(rt, np.float32(fn1.L[0])).astype(np.float32)
+    res, orc = check(q, ions, start, rt, fn1, np.float32)
+    vcur = dev(orc[:, 0, 0].copy())
+    _, r1 = q.eval_j1(dev(ions), start, dev(rt), fn1, V_cur=vcur, ratio=True)
+    _, r0 = q.eval_j1(dev(ions), start, dev(rt), fn1, ratio=True)
+    out = res.cpu().numpy()
+    np.testing.assert_allclose(r1.cpu().numpy()[:, :, 0], out[:, :, 0] - orc[:, :1, 0], atol=1e-9)
+    assert np.all(r0.cpu().numpy()[:, 0, 0] == 0.0)
+
+
+def test_j1_thread_and_warp_kernels_agree(q):
+    import os
+    ions, start, rt, fn1 = j1_case(64, 5000, seed=41, dtype=np.float32)
+    a = q.eval_j1(dev(ions), start, dev(rt), fn1).cpu().numpy()
+    os.environ["QJ2_J1_WARP"] = "1"
+    try:
+        b = q.eval_j1(dev(ions), start, dev(rt), fn1).cpu().numpy()
+    finally:
+        os.environ.pop("QJ2_J1_WARP", None)
+    orc, absout = oracle.eval_j1(ions.astype(np.float64), start, rt[:50].astype(np.float64), fn1)
+    assert oracle.normalized_error_j1(a[:50], orc, absout, fn1).max() <= 1e-5
+    assert oracle.normalized_error_j1(b[:50], orc, absout, fn1).max() <= 1e-5
+    assert np.max(np.abs(a - b)) <= 1e-4 * np.abs(a).max()
