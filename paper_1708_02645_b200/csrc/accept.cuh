@@ -25,6 +25,7 @@
 namespace qj2 {
 
 constexpr int ATPB = 256;     // threads per CTA
+constexpr int ACCEPT_FAST_MAX_M = 16;   // fp32 geometry up to m = 16 intervals (see accept_terms_fast)
 constexpr int AITER = 4;      // iterations per tile
 // vectors per thread per iteration: fp32 2 (each 8 x 16-byte loads in
 // flight), fp64 1 (fits 128 registers without spilling)
@@ -78,12 +79,83 @@ __global__ void gather_rk_kernel(const __grid_constant__ AcceptParams p, T *__re
     for (int d = 0; d < 3; ++d) r_old[w * 3 + d] = Rw[d * p.Np + kl];
 }
 
+// Functor argument in fp64 (the accept path compares single pair terms, not
+// N-term sums).  With t = r/delta up to m, any relative error in r becomes
+// an absolute error ~ m * eps in the interval fraction f and from there in
+// U' and U'' -- the fp32 displacement's own rounding (2^-24) alone gives
+// ~1e-5 of the functor scale at m = 64.  So the displacement is formed
+// exactly in fp64 (the difference of two fp32 values and the +-L shift are
+// exact), r and t follow in fp64, and only f is rounded to T for the fp32
+// Horner; the fp32 displacement (one rounding) and 1/r feed the gradient
+// factors, whose errors are relative and not amplified by t.
+struct AxisD { double c, half, L; };
+
+__device__ __forceinline__ double min_image_d(double x, const AxisD &a) {
+    double d = x - a.c;                        // exact for fp32 (or fp64 in range) inputs
+    if (d > a.half) d -= a.L;
+    else if (d <= -a.half) d += a.L;
+    return d;
+}
+
+template <typename T>
+__device__ __forceinline__ FunctorEval<T> accept_functor(double r2, double invd64, uint32_t base, int m, T &ir) {
+    const double ird = rsqrt(r2);
+    const double t = r2 * ird * invd64;
+    const double fl = floor(t);
+    const int j = fl < (double)m ? (int)fl : m;    // r >= r_cut (and dead partners) -> the zero row
+    const T f = T(t - fl);
+    ir = T(ird);
+    T a0, a1, a2, a3;
+    ld_shared_c4(base + (uint32_t)j * (uint32_t)sizeof(Coef4<T>), a0, a1, a2, a3);
+    FunctorEval<T> e;
+    const T pp = fma(a3, f, a2);
+    const T q = fma(pp, f, a1);
+    e.u = fma(q, f, a0);
+    const T r1 = fma(a3, f, pp);
+    e.du = fma(r1, f, q);
+    e.h = fma(a3, f, r1);
+    return e;
+}
+
 // Old/new functor terms of one partner; returns the (dV, dGx, dGy, dGz, dL)
 // update in physical units (dead partners: exactly zero).
 template <typename T>
-__device__ __forceinline__ void accept_terms(T x, T y, T z, bool dead, const Axis<T> (&ao)[3],
-                                             const Axis<T> (&an)[3], uint32_t base,
-                                             typename Traits<T>::U clamp, T invd, T (&dl)[5]) {
+__device__ __forceinline__ void accept_terms(T x, T y, T z, bool dead, const AxisD (&ao)[3],
+                                             const AxisD (&an)[3], uint32_t base, int m, double invd64,
+                                             T invd, T (&dl)[5]) {
+    T t[2][5];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const AxisD(&a)[3] = s ? an : ao;
+        const double ddx = min_image_d((double)x, a[0]);
+        const double ddy = min_image_d((double)y, a[1]);
+        const double ddz = min_image_d((double)z, a[2]);
+        double r2 = fma(ddz, ddz, fma(ddy, ddy, ddx * ddx));
+        r2 = dead ? 1e30 : r2;                 // lands on the all-zero interval: every term 0
+        T ir;
+        const FunctorEval<T> e = accept_functor<T>(r2, invd64, base, m, ir);
+        const T g = e.du * ir;                 // U' delta / r
+        t[s][0] = e.u;
+        t[s][1] = g * T(ddx);
+        t[s][2] = g * T(ddy);
+        t[s][3] = g * T(ddz);
+        t[s][4] = fma(e.h, invd, g);           // (U'' delta^2/2)/delta + U' delta/r  -> x 2/delta = U'' + 2U'/r
+    }
+    dl[0] = t[1][0] - t[0][0];
+    dl[1] = (t[1][1] - t[0][1]) * invd;
+    dl[2] = (t[1][2] - t[0][2]) * invd;
+    dl[3] = (t[1][3] - t[0][3]) * invd;
+    dl[4] = (t[1][4] - t[0][4]) * (T(2) * invd);
+}
+
+// Fast path (fp32 geometry, the same arithmetic as the eval kernel): per
+// pair-term error ~ (m + 4) * 2^-23 of the functor scale -- within the 1e-5
+// per-entry bar for m <= 16 (measured 4e-6 at m = 8 and 16, 3e-5 at m = 64);
+// finer functor grids take accept_terms above (the host picks by m).
+template <typename T>
+__device__ __forceinline__ void accept_terms_fast(T x, T y, T z, bool dead, const Axis<T> (&ao)[3],
+                                                  const Axis<T> (&an)[3], uint32_t base,
+                                                  typename Traits<T>::U clamp, T invd, T (&dl)[5]) {
     using Tr = Traits<T>;
     T t[2][5];
 #pragma unroll
@@ -101,7 +173,7 @@ __device__ __forceinline__ void accept_terms(T x, T y, T z, bool dead, const Axi
         t[s][1] = g * dx;
         t[s][2] = g * dy;
         t[s][3] = g * dz;
-        t[s][4] = fma(e.h, invd, g);           // (U'' delta^2/2)/delta + U' delta/r  -> x 2/delta = U'' + 2U'/r
+        t[s][4] = fma(e.h, invd, g);
     }
     dl[0] = t[1][0] - t[0][0];
     dl[1] = (t[1][1] - t[0][1]) * invd;
@@ -110,7 +182,8 @@ __device__ __forceinline__ void accept_terms(T x, T y, T z, bool dead, const Axi
     dl[4] = (t[1][4] - t[0][4]) * (T(2) * invd);
 }
 
-template <typename T>
+// PREC: fp64 geometry (accept_terms) instead of the fp32 fast path.
+template <typename T, bool PREC>
 __global__ void __launch_bounds__(ATPB, sizeof(T) == 4 ? 2 : 1)
 j2_accept_kernel(const __grid_constant__ AcceptParams p) {
     using Tr = Traits<T>;
@@ -131,18 +204,23 @@ j2_accept_kernel(const __grid_constant__ AcceptParams p) {
     const int64_t kg = p.k[w];
     const T *rn = static_cast<const T *>(p.r_new) + w * p.r_stride;
     const T *ro = static_cast<const T *>(p.r_old) + w * 3;
-    Axis<T> an[3], ao[3];
+    AxisD an[3], ao[3];
+    Axis<T> fan[3], fao[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-        an[d] = make_axis<T>(rn[d], T(p.L[d]));
-        ao[d] = make_axis<T>(ro[d], T(p.L[d]));
+        // the cell as the kernel's type sees it (fp32 L for fp32 positions)
+        const double Ld = (double)T(p.L[d]);
+        an[d].c = (double)rn[d]; an[d].L = Ld; an[d].half = 0.5 * Ld;
+        ao[d].c = (double)ro[d]; ao[d].L = Ld; ao[d].half = 0.5 * Ld;
+        fan[d] = make_axis<T>(rn[d], T(p.L[d]));
+        fao[d] = make_axis<T>(ro[d], T(p.L[d]));
     }
+    const typename Tr::U clamp = (typename Tr::U)p.m;
     const bool k_up = kg < p.N_up;
     const uint32_t tab0 = (uint32_t)__cvta_generic_to_shared(tab);
     const uint32_t base_same = tab0, base_opp = tab0 + (uint32_t)((p.m + 1) * (int)sizeof(Coef4<T>));
     const uint32_t base_up = k_up ? base_same : base_opp;      // partners i < N_up
     const uint32_t base_dn = k_up ? base_opp : base_same;      // partners i >= N_up
-    const typename Tr::U clamp = (typename Tr::U)p.m;
     const T invd = T(p.inv_delta);
     const int64_t t0 = tile * TILE;                            // local index of the tile's first source
     const int64_t kl = kg - p.i_offset;                        // k's local index (may be outside the slice)
@@ -188,8 +266,12 @@ j2_accept_kernel(const __grid_constant__ AcceptParams p) {
                 const bool dead = is_k || li >= nl;
                 const uint32_t base = (li + g_off < p.N_up) ? base_up : base_dn;
                 T dl[5];
-                accept_terms<T>(Tr::comp(bx[u], e), Tr::comp(by[u], e), Tr::comp(bz[u], e), dead, ao, an, base,
-                                clamp, invd, dl);
+                if constexpr (PREC)
+                    accept_terms<T>(Tr::comp(bx[u], e), Tr::comp(by[u], e), Tr::comp(bz[u], e), dead, ao, an, base,
+                                    p.m, p.inv_delta, invd, dl);
+                else
+                    accept_terms_fast<T>(Tr::comp(bx[u], e), Tr::comp(by[u], e), Tr::comp(bz[u], e), dead, fao, fan,
+                                         base, clamp, invd, dl);
 #pragma unroll
                 for (int c = 0; c < 5; ++c) {
                     T s = Tr::comp(bs[u][c], e) + dl[c];

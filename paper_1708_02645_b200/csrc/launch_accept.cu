@@ -13,7 +13,11 @@ static cudaError_t launch_accept(const AcceptParams &p0, void *r_old_ws, cudaStr
         p.r_old = r_old_ws;
     }
     const int64_t nb = p.W * p.tiles_per_walker;
-    j2_accept_kernel<T><<<(unsigned)nb, ATPB, 0, s>>>(p);
+    // fp64 geometry when the functor grid is fine enough for fp32's relative
+    // error in r to matter per entry (t = r/delta up to m; accept.cuh); fp64
+    // positions are exact either way
+    if (sizeof(T) == 4 && p.m > ACCEPT_FAST_MAX_M) j2_accept_kernel<T, true><<<(unsigned)nb, ATPB, 0, s>>>(p);
+    else                                           j2_accept_kernel<T, false><<<(unsigned)nb, ATPB, 0, s>>>(p);
     return cudaGetLastError();
 }
 

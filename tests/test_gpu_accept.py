@@ -34,14 +34,14 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-def setup(N, W, seed, dtype, n_up=None, pad_fill=7.0):
+def setup(N, W, seed, dtype, n_up=None, pad_fill=7.0, m=8):
     L = qmcgen.cell_length(N)
     vw = 4 if dtype == np.float32 else 2
     Np = qmcgen.padded_size(N, vw)
     R = qmcgen.positions(seed, np.arange(W), N, Np, L, dtype)
     k = qmcgen.make_k(seed, W, N)
     rt = qmcgen.make_trials(seed, np.arange(W), k, N, L, dtype)
-    fn = qmcgen.make_functor(seed, L)
+    fn = qmcgen.make_functor(seed, L, m)
     rng = np.random.default_rng(seed)
     state = rng.normal(size=(W, 5, Np)).astype(dtype)        # the update is additive: any state works
     state[:, :, N:] = pad_fill
@@ -78,6 +78,17 @@ def test_accept_parity(q, dtype, N):
     Rg, Sg, _ = run_gpu(q, R, k, rt, fn, state, acc, N, n_up)
     R2, S2, ab = oracle.accept(R, state, k, rt[:, 0], acc, fn, N, n_up)
     compare(R, state, acc, N, fn, dtype, Rg, Sg, R2, S2, ab)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("m", [4, 13, 64])
+def test_accept_functor_resolution(q, dtype, m):
+    """Per-entry parity for fine functor grids (t = r/delta up to m = 64): the
+    accept path forms r and t in fp64."""
+    R, k, rt, fn, state, acc, n_up = setup(1400, 64, 700 + m, dtype, m=m)
+    Rg, Sg, _ = run_gpu(q, R, k, rt, fn, state, acc, 1400, n_up)
+    R2, S2, ab = oracle.accept(R, state, k, rt[:, 0], acc, fn, 1400, n_up)
+    compare(R, state, acc, 1400, fn, dtype, Rg, Sg, R2, S2, ab)
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
