@@ -25,7 +25,7 @@ constexpr int TPB = 256;          // threads per CTA
 #endif
 constexpr int ITERS = QJ2_ITERS;  // vector iterations per sub-tile: 32 fp32 terms per thread per trial (A/B: -DQJ2_ITERS=n)
 #ifndef QJ2_SUB
-#define QJ2_SUB 4
+#define QJ2_SUB 8
 #endif
 constexpr int SUB = QJ2_SUB;      // sub-tiles per CTA tile (A/B builds: -DQJ2_SUB=n)
 constexpr int NACC = 6;           // fp32 accumulators per trial: V, Gx, Gy, Gz, sum h, sum du/r
@@ -506,6 +506,50 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
 #pragma unroll
         for (int a = 0; a < ND; ++a) dacc[q][a] = 0.0;
 
+    if constexpr (MODE == MODE_J2) {
+        // J2: classify sub-tiles with 32-bit offsets relative to the tile, from
+        // three per-CTA values (length, k, first spin-down source), and the two
+        // per-CTA functor constant sets (same / opposite spin as k)
+        const int32_t tlen = (int32_t)(end - start);
+        const int32_t k_t = (k_local >= start && k_local < end) ? (int32_t)(k_local - start) : -1;
+        const int64_t up64 = p.N_up - p.i_offset - start;
+        const int32_t up_t = up64 <= 0 ? 0 : (up64 >= tlen ? tlen : (int32_t)up64);
+        const GroupC<T> g_up = group_consts<T, MODE>(p, 0, kg, tab_addr);
+        const GroupC<T> g_dn = group_consts<T, MODE>(p, 1, kg, tab_addr);
+#pragma unroll 1
+        for (int sidx = 0; sidx < SUB; ++sidx) {
+            const int32_t s0 = sidx * SCH;
+            if (s0 >= tlen) break;
+            const int32_t len = min(SCH, tlen - s0);
+            const int32_t k_rel = k_t - s0;
+            const bool k_in = k_t >= 0 && (uint32_t)k_rel < (uint32_t)len;
+            const int32_t up_rel = up_t - s0;                 // sources [0, up_rel) of the sub-tile are spin-up
+            const bool straddle = up_rel > 0 && up_rel < len;
+            const GroupC<T> &gc = up_rel > 0 ? g_up : g_dn;   // the group of the sub-tile's first source
+            const int64_t vs = (int64_t)sidx * (SCH / VW);
+            V *rp[PB];
+#pragma unroll
+            for (int q = 0; q < PB; ++q) rp[q] = ROW ? rowp[q] + vs : nullptr;
+            T acc[PB][NACC];
+#pragma unroll
+            for (int q = 0; q < PB; ++q)
+#pragma unroll
+                for (int a = 0; a < NACC; ++a) acc[q][a] = T(0);
+            SubMask mk;
+            mk.len = len;
+            mk.k_rel = k_in ? k_rel : -1;
+            mk.g0 = 0;                                         // (J1 only)
+            mk.up_rel = straddle ? up_rel : len;
+            mk.base_hi = straddle ? g_dn.base : gc.base;
+            if (len == SCH && !k_in && !straddle)
+                tile_run<T, PB, ROW, PF, false, TPB, MODE>(threadIdx.x, p, kg, tab_addr, px + vs, py + vs, pz + vs, tr,
+                                                           np, gc, mk, acc, rp, row_stride);
+            else
+                tile_run<T, PB, ROW, PF, true, TPB, MODE>(threadIdx.x, p, kg, tab_addr, px + vs, py + vs, pz + vs, tr,
+                                                          np, gc, mk, acc, rp, row_stride);
+            flush<T, PB, MODE>(acc, dacc, gc.sg, gc.sh, gc.ss);      // J2: raw sums (one delta for both groups)
+        }
+    } else {
 #pragma unroll 1
     for (int sidx = 0; sidx < SUB; ++sidx) {
         const int64_t sstart = start + (int64_t)sidx * SCH;
@@ -517,6 +561,7 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
         for (int q = 0; q < PB; ++q) rp[q] = ROW ? rowp[q] + vs : nullptr;
         sub_tile<T, PB, ROW, PF, TPB, MODE>(threadIdx.x, p, kg, tab_addr, sstart, send, k_local, px + vs, py + vs,
                                             pz + vs, tr, np, dacc, rp, row_stride);
+    }
     }
 
     // ---- CTA reduction in fp64 (fixed order: deterministic) ----
