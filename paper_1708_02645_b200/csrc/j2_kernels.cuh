@@ -410,6 +410,43 @@ __device__ __forceinline__ void sub_tile(int tid, const EvalParams &p, int kg, u
     }
 }
 
+// J2 sub-tile with 32-bit classification relative to the walker's tile
+// (tile length tlen, k at k_t or -1, sources [0, up_t) of the tile spin-up)
+// and the two per-walker functor constant sets.  s0: the sub-tile's offset.
+template <typename T, int PB, bool ROW, int PF, int NT>
+__device__ __forceinline__ void j2_sub_tile32(int tid, const EvalParams &p, int kg, uint32_t tab_addr, int32_t s0,
+                                              int32_t tlen, int32_t k_t, int32_t up_t, const GroupC<T> &g_up,
+                                              const GroupC<T> &g_dn, const typename Traits<T>::V *px,
+                                              const typename Traits<T>::V *py, const typename Traits<T>::V *pz,
+                                              const Trial<T> (&tr)[PB], int np, double (&dacc)[PB][NACC],
+                                              typename Traits<T>::V *const (&rp)[PB], int64_t row_stride) {
+    constexpr int SCH = NT * Traits<T>::VW * ITERS;
+    const int32_t len = min(SCH, tlen - s0);
+    const int32_t k_rel = k_t - s0;
+    const bool k_in = k_t >= 0 && (uint32_t)k_rel < (uint32_t)len;
+    const int32_t up_rel = up_t - s0;                 // sources [0, up_rel) of the sub-tile are spin-up
+    const bool straddle = up_rel > 0 && up_rel < len;
+    const GroupC<T> &gc = up_rel > 0 ? g_up : g_dn;   // the group of the sub-tile's first source
+    T acc[PB][NACC];
+#pragma unroll
+    for (int q = 0; q < PB; ++q)
+#pragma unroll
+        for (int a = 0; a < NACC; ++a) acc[q][a] = T(0);
+    SubMask mk;
+    mk.len = len;
+    mk.k_rel = k_in ? k_rel : -1;
+    mk.g0 = 0;                                         // (J1 only)
+    mk.up_rel = straddle ? up_rel : len;
+    mk.base_hi = straddle ? g_dn.base : gc.base;
+    if (len == SCH && !k_in && !straddle)
+        tile_run<T, PB, ROW, PF, false, NT, MODE_J2>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp,
+                                                     row_stride);
+    else
+        tile_run<T, PB, ROW, PF, true, NT, MODE_J2>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp,
+                                                    row_stride);
+    flush<T, PB, MODE_J2>(acc, dacc, gc.sg, gc.sh, gc.ss);      // J2: raw sums (one delta for both groups)
+}
+
 // Per-walker setup shared by the CTA and warp kernels.
 template <typename T, int PB, int MODE>
 __device__ __forceinline__ void walker_setup(const EvalParams &p, int64_t w, int32_t p0, int np,
@@ -520,34 +557,12 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
         for (int sidx = 0; sidx < SUB; ++sidx) {
             const int32_t s0 = sidx * SCH;
             if (s0 >= tlen) break;
-            const int32_t len = min(SCH, tlen - s0);
-            const int32_t k_rel = k_t - s0;
-            const bool k_in = k_t >= 0 && (uint32_t)k_rel < (uint32_t)len;
-            const int32_t up_rel = up_t - s0;                 // sources [0, up_rel) of the sub-tile are spin-up
-            const bool straddle = up_rel > 0 && up_rel < len;
-            const GroupC<T> &gc = up_rel > 0 ? g_up : g_dn;   // the group of the sub-tile's first source
             const int64_t vs = (int64_t)sidx * (SCH / VW);
             V *rp[PB];
 #pragma unroll
             for (int q = 0; q < PB; ++q) rp[q] = ROW ? rowp[q] + vs : nullptr;
-            T acc[PB][NACC];
-#pragma unroll
-            for (int q = 0; q < PB; ++q)
-#pragma unroll
-                for (int a = 0; a < NACC; ++a) acc[q][a] = T(0);
-            SubMask mk;
-            mk.len = len;
-            mk.k_rel = k_in ? k_rel : -1;
-            mk.g0 = 0;                                         // (J1 only)
-            mk.up_rel = straddle ? up_rel : len;
-            mk.base_hi = straddle ? g_dn.base : gc.base;
-            if (len == SCH && !k_in && !straddle)
-                tile_run<T, PB, ROW, PF, false, TPB, MODE>(threadIdx.x, p, kg, tab_addr, px + vs, py + vs, pz + vs, tr,
-                                                           np, gc, mk, acc, rp, row_stride);
-            else
-                tile_run<T, PB, ROW, PF, true, TPB, MODE>(threadIdx.x, p, kg, tab_addr, px + vs, py + vs, pz + vs, tr,
-                                                          np, gc, mk, acc, rp, row_stride);
-            flush<T, PB, MODE>(acc, dacc, gc.sg, gc.sh, gc.ss);      // J2: raw sums (one delta for both groups)
+            j2_sub_tile32<T, PB, ROW, PF, TPB>(threadIdx.x, p, kg, tab_addr, s0, tlen, k_t, up_t, g_up, g_dn, px + vs,
+                                               py + vs, pz + vs, tr, np, dacc, rp, row_stride);
         }
     } else {
 #pragma unroll 1
@@ -660,6 +675,16 @@ j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
 #pragma unroll
         for (int a = 0; a < ND; ++a) dacc[q][a] = 0.0;
 
+    // J2: per-walker 32-bit classification state (the slice is one tile)
+    const int32_t tlen = (int32_t)p.N_local;
+    const int32_t k_t = (MODE == MODE_J2 && k_local >= 0 && k_local < p.N_local) ? (int32_t)k_local : -1;
+    const int64_t up64 = p.N_up - p.i_offset;
+    const int32_t up_t = up64 <= 0 ? 0 : (up64 >= tlen ? tlen : (int32_t)up64);
+    GroupC<T> g_up, g_dn;
+    if constexpr (MODE == MODE_J2) {
+        g_up = group_consts<T, MODE>(p, 0, kg, tab_addr);
+        g_dn = group_consts<T, MODE>(p, 1, kg, tab_addr);
+    }
     for (int64_t sstart = 0; sstart < p.N_local; sstart += SCH) {
         const int64_t send = min(sstart + (int64_t)SCH, p.N_local);
         const int64_t voff = (sstart / VW) + lane;
@@ -671,8 +696,12 @@ j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
         for (int q = 0; q < PB; ++q)
             rp[q] = ROW ? reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + p0 + (q < np ? q : 0)) * 4) * p.Np) + voff
                         : nullptr;
-        sub_tile<T, PB, ROW, PF, 32, MODE>(lane, p, kg, tab_addr, sstart, send, k_local, px, py, pz, tr, np, dacc, rp,
-                                           row_stride);
+        if constexpr (MODE == MODE_J2)
+            j2_sub_tile32<T, PB, ROW, PF, 32>(lane, p, kg, tab_addr, (int32_t)sstart, tlen, k_t, up_t, g_up, g_dn, px,
+                                              py, pz, tr, np, dacc, rp, row_stride);
+        else
+            sub_tile<T, PB, ROW, PF, 32, MODE>(lane, p, kg, tab_addr, sstart, send, k_local, px, py, pz, tr, np, dacc,
+                                               rp, row_stride);
     }
 
     double V0 = 0.0;
