@@ -77,7 +77,13 @@ cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStre
         const int64_t units = p.W * p.n_groups;
         const unsigned nbw = (unsigned)((units + TPB / 32 - 1) / (TPB / 32));
         constexpr int MB = (sizeof(T) == 4 && PB == 1) ? 3 : 2;
+        // fp32: three vector groups in flight per lane at 2 CTAs/SM (128 registers, no spills): on a
+        // C4 wave 5.89 TB/s vs 5.31 for two groups at 3 CTAs/SM (80 registers, spilling), 5.51 for
+        // four groups, 5.52 for one group at 4 CTAs/SM (profiles/r01_ab_sweep_s3.md).
+        const char *wv = (MODE == MODE_J2 && sizeof(T) == 4) ? getenv("QJ2_WARP") : nullptr;   // A/B variants
         if (row) j2_eval_warp_kernel<T, PB, true, 1, 2, MODE><<<nbw, TPB, 0, s>>>(p, units);
+        else if (wv && strcmp(wv, "p2m3") == 0) j2_eval_warp_kernel<T, PB, false, 2, 3, MODE><<<nbw, TPB, 0, s>>>(p, units);
+        else if (sizeof(T) == 4) j2_eval_warp_kernel<T, PB, false, 3, 2, MODE><<<nbw, TPB, 0, s>>>(p, units);
         else     j2_eval_warp_kernel<T, PB, false, 2, MB, MODE><<<nbw, TPB, 0, s>>>(p, units);
         return cudaGetLastError();
     }
