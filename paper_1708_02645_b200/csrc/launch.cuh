@@ -98,6 +98,8 @@ cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStre
         const char *e = getenv("QJ2_KERNEL");
         if (MODE == MODE_J2 && e && strcmp(e, "ldg1") == 0)   // A/B: prefetch distance 1, 4 CTAs/SM
             j2_eval_kernel<T, PB, false, 1, 4, MODE><<<nb, TPB, 0, s>>>(p);
+        else if (MODE == MODE_J2 && e && strcmp(e, "p3m2") == 0)   // A/B: prefetch distance 3, 2 CTAs/SM
+            j2_eval_kernel<T, PB, false, 3, 2, MODE><<<nb, TPB, 0, s>>>(p);
         else    // default: two vector groups in flight per thread, 3 CTAs/SM (80 registers);
                 // measured best on B200
             j2_eval_kernel<T, PB, false, 2, 3, MODE><<<nb, TPB, 0, s>>>(p);

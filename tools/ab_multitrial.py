@@ -1,6 +1,6 @@
 """A/B timing of the multi-trial (P > 1) eval kernel variants on the C3
-instance (N = 614,400, W = 1024, fp32): QJ2_PBN selects prefetch distance /
-CTAs per SM of the PB > 1 kernel (launch.cuh).  CUDA events, best of reps.
+instance (N = 614,400, W = 1024, fp32): QJ2_KERNEL selects the CTA kernel
+variant (launch.cuh: ldg1, p3m2, tma323).  CUDA events, best of reps.
 Usage: python tools/ab_multitrial.py [P ...]"""
 import json
 import os
@@ -15,7 +15,7 @@ import qmcgen  # noqa: E402
 
 cfg = qmcgen.CONFIGS["C3"]
 Ps = [int(a) for a in sys.argv[1:]] or [2, 4, 12]
-variants = os.environ.get("AB_VARIANTS", "default,22,pb1").split(",")
+variants = os.environ.get("AB_VARIANTS", "default,p3m2,ldg1").split(",")
 R = q.gen_positions(cfg.seed, cfg.W, cfg.N, cfg.Np, cfg.L, torch.float32)
 k = qmcgen.make_k(cfg.seed, cfg.W, cfg.N)
 fn = q.Functor.of(qmcgen.make_functor(cfg.seed, cfg.L, cfg.m))
@@ -28,12 +28,9 @@ for P in Ps:
     out = torch.empty((cfg.W, P, 5), dtype=torch.float64, device="cuda")
     ref = None
     for v in variants:
-        os.environ.pop("QJ2_PBN", None)
-        os.environ.pop("QJ2_PB1", None)
-        if v == "pb1":
-            os.environ["QJ2_PB1"] = "1"
-        elif v != "default":
-            os.environ["QJ2_PBN"] = v
+        os.environ.pop("QJ2_KERNEL", None)
+        if v != "default":
+            os.environ["QJ2_KERNEL"] = v
         for _ in range(3):
             q.eval(R, kd, rt, fn, cfg.N, cfg.n_up, out=out, workspace=ws)
         torch.cuda.synchronize()
