@@ -752,18 +752,30 @@ __global__ void __launch_bounds__(TPB) j1_thread_kernel(const __grid_constant__ 
                   az = make_axis<T>(rt[2], T(p.L[2]));
     const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tab);
     double dacc[NOUT] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    auto term = [&](int32_t i, const GroupC<T> &gc, T (&acc)[NACC]) {
+        T x, y, z;
+        if constexpr (sizeof(T) == 4) {
+            const float4 v = reinterpret_cast<const float4 *>(ion)[i];    // one LDS.128 (broadcast)
+            x = v.x; y = v.y; z = v.z;
+        } else {
+            const double2 v = reinterpret_cast<const double2 *>(ion)[2 * i];
+            x = v.x; y = v.y; z = ion[i * 4 + 2];
+        }
+        const T dx = min_image(x, ax), dy = min_image(y, ay), dz = min_image(z, az);
+        const T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        accumulate<T>(dx, dy, dz, r2, gc.invd, gc.base, gc.clamp, acc);
+    };
     for (int g = 0; g < p.n_src_groups; ++g) {
         const GroupC<T> gc = group_consts<T, MODE_J1>(p, g, 0, tab_addr);
-        const int64_t i1 = p.grp_start[g + 1];
-        for (int64_t i0 = p.grp_start[g]; i0 < i1; i0 += 32) {
-            const int64_t ie = min(i0 + 32, i1);
+        const int32_t i1 = (int32_t)p.grp_start[g + 1];
+        for (int32_t i0 = (int32_t)p.grp_start[g]; i0 < i1; i0 += 32) {
             T acc[NACC] = {T(0), T(0), T(0), T(0), T(0), T(0)};
-#pragma unroll 4
-            for (int64_t i = i0; i < ie; ++i) {
-                const T x = ion[i * 4 + 0], y = ion[i * 4 + 1], z = ion[i * 4 + 2];
-                const T dx = min_image(x, ax), dy = min_image(y, ay), dz = min_image(z, az);
-                const T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-                accumulate<T>(dx, dy, dz, r2, gc.invd, gc.base, gc.clamp, acc);
+            if (i1 - i0 >= 32) {                 // full chunk: fixed trip count, fully pipelined
+#pragma unroll 8
+                for (int32_t i = 0; i < 32; ++i) term(i0 + i, gc, acc);
+            } else {
+#pragma unroll 1
+                for (int32_t i = i0; i < i1; ++i) term(i, gc, acc);
             }
             dacc[0] += (double)acc[0];
             dacc[1] += gc.sg * (double)acc[1];
