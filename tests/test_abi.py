@@ -121,3 +121,70 @@ def test_package_has_no_cpu_fallback():
                 txt = open(os.path.join(dirpath, fn)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, fn
                 assert "liboracle" not in txt, fn
+
+
+def _call_accept(q, f, **over):
+    P = ctypes.c_void_p(4096)
+    args = dict(dtype=0, W=4, N_total=100, N_up=50, i_offset=0, N_local=100, Np=128, R=P, S=P, k=P, rn=P,
+                rs=3, ro=None, acc=P, out=P, os=5, ws=P, wsb=1 << 20)
+    args.update(over)
+    st = q._lib.qj2_accept(f.ptr, args["dtype"], args["W"], args["N_total"], args["N_up"], args["i_offset"],
+                           args["N_local"], args["Np"], args["R"], args["S"], args["k"], args["rn"], args["rs"],
+                           args["ro"], args["acc"], args["out"], args["os"], args["ws"], args["wsb"], None)
+    return st, q._lib.qj2_last_error().decode()
+
+
+def test_accept_host_validation(q):
+    """qj2_accept (NEXT-2): argument checks that return before any CUDA call."""
+    f = _functor(q)
+    assert _call_accept(q, f, N_total=1)[0] == 1
+    assert _call_accept(q, f, N_up=101)[0] == 2
+    assert _call_accept(q, f, i_offset=50, N_local=60)[0] == 2
+    assert _call_accept(q, f, Np=99)[0] == 1
+    assert _call_accept(q, f, os=4)[0] == 1                   # out_stride < 5
+    assert _call_accept(q, f, rs=2)[0] == 1                   # r_stride < 3
+    assert _call_accept(q, f, S=None)[0] == 1
+    assert _call_accept(q, f, acc=None)[0] == 1
+    assert _call_accept(q, f, S=ctypes.c_void_p(4104))[0] == 1     # misaligned state
+    st, msg = _call_accept(q, f, ws=None, wsb=0)
+    assert st == 1 and "workspace" in msg                     # r_old NULL needs the gather workspace
+    assert _call_accept(q, f, W=0)[0] == 0
+    assert _call_accept(q, _functor(q, m=3))[0] == 1
+    b = ctypes.c_size_t()
+    assert q._lib.qj2_accept_workspace_size(1024, 0, ctypes.byref(b)) == 0 and b.value >= 1024 * 12
+
+
+def test_metropolis_and_spo_host_validation(q):
+    P = ctypes.c_void_p(4096)
+    lib = q._lib
+    assert lib.qj2_metropolis(-1, P, 2, P, P, None) == 1
+    assert lib.qj2_metropolis(4, P, 1, P, P, None) == 1         # ratio_stride < 2
+    assert lib.qj2_metropolis(4, None, 2, P, P, None) == 1
+    assert lib.qj2_metropolis(0, None, 2, None, None, None) == 0
+
+    def tab(**kw):
+        t = q._SpoTable()
+        for d in range(3):
+            t.L[d] = 3.0
+        t.nx = t.ny = t.nz = 8
+        t.n_orb, t.ld, t.coef = 10, 12, 4096
+        for a, v in kw.items():
+            setattr(t, a, v)
+        return t
+
+    def spo(t, what=1, dt=0, W=5, pos=P, ps=3, ainv=P, out=P, spo_out=None):
+        return lib.qj2_spo_eval(ctypes.byref(t), what, dt, W, pos, ps, ainv, 12, 12, None, out, spo_out, None)
+
+    assert spo(tab(), what=2) == 1
+    assert spo(tab(), dt=5) == 1
+    assert spo(tab(nx=3)) == 1                                  # grid >= 4
+    assert spo(tab(ld=10)) == 1                                 # ld % 4
+    assert spo(tab(ld=8)) == 1                                  # ld < n_orb
+    assert spo(tab(nx=1024, ny=1024, nz=1024)) == 1             # >= 2^31 floats
+    assert spo(tab(), ps=2) == 1
+    assert spo(tab(coef=4100)) == 1                             # misaligned table
+    assert spo(tab(), pos=None) == 1
+    assert spo(tab(), W=0) == 0
+    L = tab()
+    L.L[1] = 0.0
+    assert spo(L) == 1
