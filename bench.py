@@ -270,8 +270,9 @@ class OracleSampleJ1:
         return time.perf_counter() - t0
 
 
-def j1_inputs(cfg, n=None):
-    """ions [3][Np], species_start, trial points [n][1][3] (fp32), J1 functor of a J1 config."""
+def j1_inputs(cfg, n=None, rank=0):
+    """ions [3][Np], species_start, trial points [n][1][3] (fp32), J1 functor of a J1 config
+    (the ions and functor are the system's; the trial points are rank-specific)."""
     import qmcgen
     n = cfg.W if n is None else n
     ions, start = qmcgen.make_ions(cfg.seed, cfg.n_ions, qmcgen.padded_size(cfg.n_ions, 4), cfg.L, np.float32,
@@ -279,7 +280,7 @@ def j1_inputs(cfg, n=None):
     fn1 = qmcgen.make_j1_functor(cfg.seed, cfg.L, n_species=cfg.n_species)
     ids = np.arange(n)
     k = (ids % cfg.N).astype(np.int32)                 # electron of each trial point
-    rt = qmcgen.make_trials(cfg.seed, ids, k, cfg.N, cfg.L, np.float32)
+    rt = qmcgen.make_trials(cfg.seed + rank, ids, k, cfg.N, cfg.L, np.float32)
     return ions, start, rt, fn1
 
 
@@ -886,6 +887,7 @@ class J1Plan:
 
     def __init__(self, cfg, rank, world):
         self.cfg = cfg
+        self.rank = rank
         self.items_per_step = cfg.W * cfg.n_ions
 
     def items_total(self, world):
@@ -899,7 +901,7 @@ class J1Plan:
     def prepare(self, q):
         import torch
         cfg = self.cfg
-        ions, self.start, rt, fn1 = j1_inputs(cfg)
+        ions, self.start, rt, fn1 = j1_inputs(cfg, rank=self.rank)
         self.fn1 = q.J1Functor.of(fn1)
         self.ions = torch.from_numpy(ions).cuda()
         self.rt = torch.from_numpy(rt).cuda()
