@@ -44,7 +44,9 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        _lib = ctypes.CDLL(build())
+        # ORACLE_LIB: a deliberately mutated build, loaded by tests/test_oracle_mutations.py
+        # to show that the pins catch plausible mistakes (test infrastructure only)
+        _lib = ctypes.CDLL(os.environ.get("ORACLE_LIB") or build())
         dp = ctypes.POINTER(ctypes.c_double)
         i32p = ctypes.POINTER(ctypes.c_int32)
         i64 = ctypes.c_int64
