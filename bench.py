@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C3S", "C3P2", "C3P12", "S1", "J1S"])
+    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C3S", "C3P2", "C3P12", "S1", "S1V", "J1S"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -240,9 +240,15 @@ class OracleSampleSpo:
             _SPO_TABLE_CACHE[cfg.name] = oracle.gen_spo_table(cfg.seed, cfg.nx, cfg.ny, cfg.nz, cfg.n_orb, cfg.ld,
                                                               threads=threads)
         self.T = _SPO_TABLE_CACHE[cfg.name]
-        self.pos = qmcgen.spo_positions(cfg.seed, cfg.W, cfg.L)[:self.n].astype(np.float64)
         self.A = qmcgen.make_ainv_rows(cfg.seed, cfg.W, cfg.n_orb)[:self.n]
-        self.items = self.n * cfg.n_orb
+        if cfg.name == "S1V":          # 12 NLPP points per walker, each with its walker's A^-1 row
+            k = qmcgen.make_k(cfg.seed, cfg.W, cfg.N)[:self.n]
+            pts = qmcgen.make_trials(cfg.seed, np.arange(self.n), k, cfg.N, cfg.L, np.float32, P=12, mode="nlpp")
+            self.pos = pts.reshape(-1, 3).astype(np.float64)
+            self.A = np.repeat(self.A, 12, axis=0)
+        else:
+            self.pos = qmcgen.spo_positions(cfg.seed, cfg.W, cfg.L)[:self.n].astype(np.float64)
+        self.items = self.pos.shape[0] * cfg.n_orb
 
     def run(self):
         import oracle
@@ -296,6 +302,8 @@ def _what(cfg):
     import qmcgen
     if cfg.name.startswith("J"):
         return f"J1 over {cfg.n_ions} ions of {cfg.n_species} species, one trial point per row"
+    if cfg.name == "S1V":
+        return f"Bspline-v of {cfg.n_orb} orbitals at 12 NLPP points per walker + determinant ratios"
     if cfg.name.startswith("S"):
         return f"Bspline-vgh of {cfg.n_orb} orbitals + determinant ratio, {cfg.nx}x{cfg.ny}x{cfg.nz} grid"
     if cfg.name == "C3S":
@@ -373,9 +381,11 @@ def workload_config(cfg, world):
                 "N": cfg.N, "n_ions": cfg.n_ions, "W": cfg.W, "parallelism": f"walker-batch x{world}",
                 "l2": "ions shared (L2/shared-memory resident); trial points stream"}
     if name.startswith("S"):
+        what = ("12 NLPP quadrature points each (Bspline-v + determinant ratio, one A^-1 row per walker)"
+                if name == "S1V" else "one Bspline-vgh + determinant ratio each")
         return {"workload": f"{name} (NEXT-4): NiO-64-shaped SPO set (Table 1: {cfg.nx}x{cfg.ny}x{cfg.nz} grid, "
                             f"{cfg.n_orb} orbitals = N/2 for N={cfg.N}, fp32 table {cfg.table_bytes / 1e6:.0f} MB), "
-                            f"W={cfg.W} walkers per rank, one Bspline-vgh + determinant ratio each",
+                            f"W={cfg.W} walkers per rank, {what}",
                 "nx": cfg.nx, "n_orb": cfg.n_orb, "ld": cfg.ld, "W": cfg.W, "N": cfg.N,
                 "parallelism": f"walker-batch x{world}",
                 "l2": "table 786 MB > 126 MB L2; random gathers (no flush needed)"}
@@ -816,8 +826,11 @@ class SpoPlan:
 
     def __init__(self, cfg, rank, world):
         self.cfg = cfg
+        self.mode = cfg.name
         self.seed = cfg.seed + rank
-        self.items_per_step = cfg.W * cfg.n_orb
+        self.nlpp = cfg.name == "S1V"                 # Bspline-v at 12 quadrature points per walker
+        self.ppw = 12 if self.nlpp else 1
+        self.items_per_step = cfg.W * self.ppw * cfg.n_orb
 
     def items_total(self, world):
         return self.items_per_step * world
@@ -825,9 +838,9 @@ class SpoPlan:
     @property
     def alg_bytes_per_launch(self):
         cfg = self.cfg
-        # per walker: 64 coefficient rows of n_orb fp32 (the method's gather), the A^{-1} row,
-        # the position and the 5 fp64 outputs
-        return cfg.W * (64 * cfg.n_orb * 4 + cfg.n_orb * 4 + 12 + 40)
+        # per evaluation: 64 coefficient rows of n_orb fp32 (the method's gather), the position and
+        # the 5 fp64 outputs; per walker the A^{-1} row
+        return cfg.W * self.ppw * (64 * cfg.n_orb * 4 + 12 + 40) + cfg.W * cfg.n_orb * 4
 
     def prepare(self, q):
         import torch
@@ -835,13 +848,21 @@ class SpoPlan:
         cfg = self.cfg
         self.coef = q.gen_spo_table(cfg.seed, cfg.nx, cfg.ny, cfg.nz, cfg.n_orb, cfg.ld)
         self.tab = q.SpoTable(self.coef, cfg.n_orb, cfg.L)
-        self.pos = torch.from_numpy(qmcgen.spo_positions(self.seed, cfg.W, cfg.L)).cuda()
+        if self.nlpp:
+            k = qmcgen.make_k(self.seed, cfg.W, cfg.N)
+            pts = qmcgen.make_trials(self.seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32, P=12, mode="nlpp")
+            self.pos = torch.from_numpy(np.ascontiguousarray(pts)).cuda()
+        else:
+            self.pos = torch.from_numpy(qmcgen.spo_positions(self.seed, cfg.W, cfg.L)).cuda()
         self.A = torch.from_numpy(qmcgen.make_ainv_rows(self.seed, cfg.W, cfg.n_orb)).cuda()
-        self.out = torch.empty((cfg.W, 5), dtype=torch.float64, device="cuda")
+        self.out = torch.empty((cfg.W * self.ppw, 5), dtype=torch.float64, device="cuda")
         torch.cuda.synchronize()
 
     def step(self, q, dist_mod):
-        q.spo_eval(self.tab, self.pos, Ainv=self.A, out=self.out)
+        if self.nlpp:
+            q.spo_eval(self.tab, self.pos, vgh=False, Ainv=self.A, all_trials=True, out=self.out)
+        else:
+            q.spo_eval(self.tab, self.pos, Ainv=self.A, out=self.out)
 
     def kernel_ms(self, q, stream, reps):
         return _event_ms(lambda: self.step(q, None), stream, reps)
@@ -854,13 +875,16 @@ class SpoPlan:
         cfg = self.cfg
         ph = self.pos.cpu().pin_memory()
         ah = self.A.cpu().pin_memory()
-        oh = torch.empty((cfg.W, 5), dtype=torch.float64, pin_memory=True)
+        oh = torch.empty((cfg.W * self.ppw, 5), dtype=torch.float64, pin_memory=True)
         pd, ad = torch.empty_like(self.pos), torch.empty_like(self.A)
 
         def run():
             pd.copy_(ph, non_blocking=True)
             ad.copy_(ah, non_blocking=True)
-            q.spo_eval(self.tab, pd, Ainv=ad, out=self.out)
+            if self.nlpp:
+                q.spo_eval(self.tab, pd, vgh=False, Ainv=ad, all_trials=True, out=self.out)
+            else:
+                q.spo_eval(self.tab, pd, Ainv=ad, out=self.out)
             oh.copy_(self.out, non_blocking=True)
             torch.cuda.current_stream().synchronize()
         run()
@@ -951,7 +975,8 @@ def make_plan(cfg, rank, world):
 
 
 def plan_kernel_name(plan):
-    return {"C3S": "j2_accept_kernel<float>", "S1": "spo_kernel<vgh>"}.get(plan.mode, "j2_eval_kernel<float,1,false>")
+    return {"C3S": "j2_accept_kernel<float>", "S1": "spo_tma_kernel<vgh>",
+            "S1V": "spo_tma_kernel<v>"}.get(plan.mode, "j2_eval_kernel<float,1,false>")
 
 
 def run_ours(args):
@@ -1028,7 +1053,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "weak" if plan.mode in ("C3", "C3S", "C3P2", "C3P12", "S1", "J1S") else "strong",
+            "scaling": "weak" if plan.mode in ("C3", "C3S", "C3P2", "C3P12", "S1", "S1V", "J1S") else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(cfg, world),
             "roofline": (plan.roofline(kms, peak) if hasattr(plan, "roofline") else

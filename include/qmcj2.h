@@ -298,9 +298,12 @@ enum { QJ2_SPO_V = 0, QJ2_SPO_VGH = 1 };
 /*   W          evaluations (>= 0).                                          */
 /*   pos        device, row w at pos + w*pos_stride elements (x, y, z), any  */
 /*              real value (wrapped into the cell); pos_stride >= 3.         */
-/*   Ainv       device fp32 or NULL (no ratio): row of walker w at           */
-/*              Ainv + w*ainv_stride + krow[w]*ainv_ld (krow == NULL: row 0),*/
+/*   Ainv       device fp32 or NULL (no ratio): for evaluation w the row of  */
+/*              walker a = w / points_per_walker at                          */
+/*              Ainv + a*ainv_stride + krow[a]*ainv_ld (krow == NULL: row 0),*/
 /*              n_orb entries.                                               */
+/*   points_per_walker >= 1: consecutive evaluations sharing one walker's    */
+/*              A^{-1} row (12 for the NLPP quadrature).      */
 /*   out        device fp64 [W][5] (rho, Gx, Gy, Gz, L) or NULL; with        */
 /*              QJ2_SPO_V only rho is computed (G, L written as 0).          */
 /*   spo_out    device fp32 [W][10][ld] (v, gx, gy, gz, hxx, hxy, hxz, hyy,  */
@@ -309,7 +312,7 @@ enum { QJ2_SPO_V = 0, QJ2_SPO_VGH = 1 };
 qj2_status qj2_spo_eval(const qj2_spo_table *tab, int32_t what, qj2_dtype pos_dtype, int64_t W,
                         const void *pos, int64_t pos_stride,
                         const float *Ainv, int64_t ainv_stride, int64_t ainv_ld, const int32_t *krow,
-                        double *out, float *spo_out, void *stream);
+                        int64_t points_per_walker, double *out, float *spo_out, void *stream);
 
 /* Synthetic SPO coefficient table (test/bench harness, NOT the method):     */
 /* coef[ix][iy][iz][o] = 2u - 1, u = top 24 bits of mix64(key' ^ flat index) */

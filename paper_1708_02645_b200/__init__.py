@@ -97,7 +97,7 @@ def _load():
                                       vp, vp, i64, vp, sz, vp]),
         "qj2_metropolis": (ctypes.c_int, [i64, vp, i64, vp, vp, vp]),
         "qj2_spo_eval": (ctypes.c_int, [ctypes.POINTER(_SpoTable), i32, ctypes.c_int, i64, vp, i64, vp, i64, i64,
-                                        vp, vp, vp, vp]),
+                                        vp, i64, vp, vp, vp]),
         "qj2gen_spo_table": (ctypes.c_int, [ctypes.c_uint64, i64, i64, i64, i64, i64, vp, vp]),
         "qj2_eval_j1": (ctypes.c_int, [ctypes.POINTER(_J1Functor), ctypes.c_int, i64, ctypes.POINTER(i64), i64,
                                        vp, i32, vp, vp, vp, vp, vp, vp, sz, vp]),
@@ -440,16 +440,22 @@ class SpoTable:
         return ctypes.byref(self._c)
 
 
-def spo_eval(tab: SpoTable, pos, *, vgh: bool = True, Ainv=None, krow=None, trial: int = 0, out=None,
-             spo_out=None, want_spo: bool = False, stream=None):
+def spo_eval(tab: SpoTable, pos, *, vgh: bool = True, Ainv=None, krow=None, trial: int = 0, all_trials: bool = False,
+             out=None, spo_out=None, want_spo: bool = False, stream=None):
     """qj2_spo_eval (NEXT-4): Bspline-vgh (vgh=True) or Bspline-v at pos
-    ([W][3] or [W][P][3], trial `trial`, f32/f64) fused with the determinant
-    ratio against Ainv (fp32, [W][n][lda] with krow [W] int32, or [W][lda]
-    rows).  Returns out [W][5] fp64 (rho, G, L) (None without Ainv) and, if
-    want_spo, spo [W][10 or 1][ld] fp32."""
+    ([W][3], or [W][P][3]: trial `trial`, or every trial with all_trials=True --
+    then the P points of a walker share its A^{-1} row, e.g. the NLPP
+    quadrature), fused with the determinant ratio against Ainv (fp32,
+    [W][n][lda] with krow [W] int32, or [W][lda] rows).  Returns out
+    [W*P or W][5] fp64 (rho, G, L) (None without Ainv) and, if want_spo, spo
+    [evaluations][10 or 1][ld] fp32."""
     _req(pos, "pos")
+    ppw = 1
+    if all_trials and pos.dim() == 3:
+        ppw = pos.shape[1]
+        pos = pos.reshape(-1, 3)
     W = pos.shape[0]
-    pp, ps = _row_ptr(pos, trial, 3)
+    pp, ps = _row_ptr(pos, trial if not all_trials else 0, 3)
     ldv = tab.coef.shape[3]
     dev = pos.device
     a_ptr, a_stride, a_ld = None, 0, 0
@@ -469,7 +475,7 @@ def spo_eval(tab: SpoTable, pos, *, vgh: bool = True, Ainv=None, krow=None, tria
     if want_spo and spo_out is None:
         spo_out = torch.empty((W, 10 if vgh else 1, ldv), dtype=torch.float32, device=dev)
     _check(_lib.qj2_spo_eval(tab.ptr, QJ2_SPO_VGH if vgh else QJ2_SPO_V, _dtype_code(pos.dtype), W, pp, ps,
-                             a_ptr, a_stride, a_ld, _ptr(krow), _ptr(out) if Ainv is not None else None,
+                             a_ptr, a_stride, a_ld, _ptr(krow), ppw, _ptr(out) if Ainv is not None else None,
                              _ptr(spo_out), ctypes.c_void_p(_stream_ptr(stream))), "qj2_spo_eval")
     if want_spo:
         return out, spo_out

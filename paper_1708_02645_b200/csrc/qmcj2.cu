@@ -579,8 +579,9 @@ qj2_status qj2_metropolis(int64_t W, const double *ratio, int64_t ratio_stride,
 qj2_status qj2_spo_eval(const qj2_spo_table *tab, int32_t what, qj2_dtype pos_dtype, int64_t W,
                         const void *pos, int64_t pos_stride,
                         const float *Ainv, int64_t ainv_stride, int64_t ainv_ld, const int32_t *krow,
-                        double *out, float *spo_out, void *stream) {
+                        int64_t points_per_walker, double *out, float *spo_out, void *stream) {
     if (!tab) return fail(QJ2_EINVAL, "tab is NULL");
+    if (points_per_walker < 1) return fail(QJ2_EINVAL, "points_per_walker must be >= 1");
     if (what != QJ2_SPO_V && what != QJ2_SPO_VGH) return fail(QJ2_EINVAL, "what must be QJ2_SPO_V or QJ2_SPO_VGH");
     if (pos_dtype != QJ2_FP32 && pos_dtype != QJ2_FP64) return fail(QJ2_EINVAL, "bad pos_dtype");
     for (int d = 0; d < 3; ++d)
@@ -607,7 +608,7 @@ qj2_status qj2_spo_eval(const qj2_spo_table *tab, int32_t what, qj2_dtype pos_dt
     p.coef = tab->coef;
     for (int d = 0; d < 3; ++d) p.L[d] = tab->L[d];
     p.pos_f64 = pos_dtype == QJ2_FP64; p.pos = pos; p.pos_stride = pos_stride;
-    p.Ainv = Ainv; p.ainv_stride = ainv_stride; p.ainv_ld = ainv_ld; p.krow = krow;
+    p.Ainv = Ainv; p.ainv_stride = ainv_stride; p.ainv_ld = ainv_ld; p.krow = krow; p.ppw = points_per_walker;
     p.out = out; p.spo_out = spo_out;
     const int64_t lanes = ((p.nvec + 31) / 32) * 32;
     p.tpw = (int32_t)(lanes < 256 ? lanes : 256);

@@ -30,6 +30,7 @@ struct SpoParams {
     const float *Ainv;                          // row of walker w at Ainv + w*ainv_stride + krow[w]*ainv_ld
     int64_t ainv_stride, ainv_ld;
     const int32_t *krow;                        // or NULL (Ainv rows pre-gathered)
+    int64_t ppw;                                // evaluations per walker (A^{-1} row of walker w / ppw)
     double *out;                                // [W][5] (rho, Gx, Gy, Gz, L) or NULL
     float *spo_out;                             // [W][NQ][ld] or NULL
     int32_t tpw, wpc;                           // threads per walker, walkers per CTA
@@ -138,7 +139,10 @@ __global__ void __launch_bounds__(256, 2) spo_kernel(const __grid_constant__ Spo
         axis_weights(x[2], p.L[2], p.nz, (int32_t)p.nvec, az);
         const Vt *coef = reinterpret_cast<const Vt *>(p.coef);
         const float *arow = nullptr;
-        if (p.Ainv) arow = p.Ainv + w * p.ainv_stride + (p.krow ? (int64_t)p.krow[w] * p.ainv_ld : 0);
+        if (p.Ainv) {
+            const int64_t wa = w / p.ppw;
+            arow = p.Ainv + wa * p.ainv_stride + (p.krow ? (int64_t)p.krow[wa] * p.ainv_ld : 0);
+        }
 
         for (int64_t j = lane; j < p.nvec; j += p.tpw) {
             Vt acc[NQ];
@@ -408,7 +412,8 @@ __global__ void spo_tma_kernel(const __grid_constant__ SpoParams p, int nst) {
     for (int64_t w = blockIdx.x; w < p.W; w += G, ++it) {
         // A^{-1} row entries of this thread's orbitals (used after the gather)
         float av[NV];
-        const float *arow = p.Ainv ? p.Ainv + w * p.ainv_stride + (p.krow ? (int64_t)p.krow[w] * p.ainv_ld : 0)
+        const int64_t wa = w / p.ppw;
+        const float *arow = p.Ainv ? p.Ainv + wa * p.ainv_stride + (p.krow ? (int64_t)p.krow[wa] * p.ainv_ld : 0)
                                    : nullptr;
 #pragma unroll
         for (int e = 0; e < NV; ++e) {

@@ -304,6 +304,8 @@ class SpoConfig:
 SPO_CONFIGS = {
     # NiO-64 (Table 1): N = 768, FFT grid 80^3; the determinant needs N/2 = 384 orbitals per spin
     "S1": SpoConfig("S1", 80, 80, 80, 384, 384, 65536, 768, seed=11),
+    # NLPP ratios (Bspline-v): 8192 (walker, electron near an ion) pairs x 12 quadrature points
+    "S1V": SpoConfig("S1V", 80, 80, 80, 384, 384, 8192, 768, seed=11),
 }
 
 

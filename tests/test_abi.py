@@ -172,8 +172,8 @@ def test_metropolis_and_spo_host_validation(q):
             setattr(t, a, v)
         return t
 
-    def spo(t, what=1, dt=0, W=5, pos=P, ps=3, ainv=P, out=P, spo_out=None):
-        return lib.qj2_spo_eval(ctypes.byref(t), what, dt, W, pos, ps, ainv, 12, 12, None, out, spo_out, None)
+    def spo(t, what=1, dt=0, W=5, pos=P, ps=3, ainv=P, out=P, spo_out=None, ppw=1):
+        return lib.qj2_spo_eval(ctypes.byref(t), what, dt, W, pos, ps, ainv, 12, 12, None, ppw, out, spo_out, None)
 
     assert spo(tab(), what=2) == 1
     assert spo(tab(), dt=5) == 1
@@ -185,6 +185,7 @@ def test_metropolis_and_spo_host_validation(q):
     assert spo(tab(coef=4100)) == 1                             # misaligned table
     assert spo(tab(), pos=None) == 1
     assert spo(tab(), W=0) == 0
+    assert spo(tab(), ppw=0) == 1
     L = tab()
     L.L[1] = 0.0
     assert spo(L) == 1

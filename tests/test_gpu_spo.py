@@ -164,3 +164,23 @@ def test_spo_nio64_full_size_sampled(q):
     orc, aab = oracle.det_ratio(A[ws], v, g, h)
     assert np.max(np.abs(out[ws, 0] - orc[:, 0]) / aab[:, 0]) <= TOL
     assert np.max(np.abs(out[ws, 1:] * out[ws, :1] - orc[:, 1:] * orc[:, :1]) / aab[:, 1:]) <= TOL
+
+
+def test_spo_v_nlpp_points_share_the_walkers_row(q, kernel):
+    """Bspline-v at the 12 NLPP quadrature points of each walker (all_trials,
+    points_per_walker = 12): every point's ratio uses its walker's A^{-1} row."""
+    n_orb, W = 48, 40
+    L = (3.0, 3.0, 3.0)
+    T = qmcgen.spo_table(51, 6, 6, 6, n_orb)
+    tab = q.SpoTable(dev(T), n_orb, L)
+    k = qmcgen.make_k(51, W, 200)
+    pts = qmcgen.make_trials(51, np.arange(W), k, 200, 3.0, np.float32, P=12, mode="nlpp")     # [W][12][3]
+    A = qmcgen.make_ainv_rows(51, W, n_orb)
+    out, spo = q.spo_eval(tab, dev(pts), vgh=False, Ainv=dev(A), all_trials=True, want_spo=True)
+    out, spo = out.cpu().numpy(), spo.cpu().numpy()
+    assert out.shape == (W * 12, 5)
+    v, g, h, ab = oracle.spo_vgh(T, n_orb, L, pts.reshape(-1, 3).astype(np.float64))
+    err = np.abs(spo[:, 0, :n_orb] - v) / np.maximum(ab[:, 0], np.abs(T).max())
+    assert err.max() <= TOL
+    orc, aab = oracle.det_ratio(np.repeat(A, 12, axis=0), v, g, h)
+    assert np.max(np.abs(out[:, 0] - orc[:, 0]) / aab[:, 0]) <= TOL
