@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C3S", "C3P2", "C3P12", "S1", "S1V", "J1S"])
+    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C3S", "C3P2", "C3P12", "S1", "S1V", "J1S", "N64S"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -195,11 +195,13 @@ class OracleSample:
         import oracle
         import qmcgen
         self.cfg, self.n, self.threads = cfg, int(n_walkers), threads
-        self.sweep = cfg.name == "C3S"
+        self.sweep = cfg.name in ("C3S", "N64S")
+        self.moves = cfg.N if cfg.name == "N64S" else 1       # N64S: one full sweep per step
         if self.sweep:
             self.n = min(self.n, self.MAX_SWEEP_WALKERS)
-            ks, tr, u = qmcgen.make_sweep(cfg.seed, cfg.W, cfg.N, cfg.L, cfg.np_dtype, 1)
-            self.k, self.rt, self.u = ks[0][:self.n], tr[0][:self.n], u[0][:self.n]
+            ks, tr, u = qmcgen.make_sweep(cfg.seed, cfg.W, cfg.N, cfg.L, cfg.np_dtype, self.moves)
+            self.ks, self.trs, self.us = ks[:, :self.n], tr[:, :self.n], u[:, :self.n]
+            self.k, self.rt = self.ks[0], self.trs[0]
             self.S = np.zeros((self.n, 5, cfg.Np))
         else:
             P, mode = qmcgen.trial_spec(cfg.name)
@@ -210,16 +212,21 @@ class OracleSample:
         self.P = self.rt.shape[1]
         self.fn = qmcgen.make_functor(cfg.seed, cfg.L, cfg.m)
         self.R = oracle.gen_positions(cfg.seed, 0, self.n, cfg.N, cfg.Np, cfg.L, cfg.np_dtype, threads)
-        self.items = self.n * self.P * (cfg.N - 1)
+        # items in the bench's unit: (walker, trial, partner) terms; the sweep configs count one per
+        # (move, partner) like their GPU lines
+        self.items = self.n * (self.moves if self.sweep else self.P) * (cfg.N - 1)
 
     def run(self):
         import oracle
         t0 = time.perf_counter()
-        out, _, _ = oracle.eval_j2(self.R, self.k, self.rt, self.fn, self.cfg.N, self.cfg.n_up,
-                                   threads=self.threads)
-        if self.sweep:
-            acc = (self.u < np.exp(out[:, 1, 0] - out[:, 0, 0]) ** 2).astype(np.int32)
-            oracle.accept(self.R, self.S, self.k, self.rt[:, 1], acc, self.fn, self.cfg.N, self.cfg.n_up)
+        if not self.sweep:
+            oracle.eval_j2(self.R, self.k, self.rt, self.fn, self.cfg.N, self.cfg.n_up, threads=self.threads)
+            return time.perf_counter() - t0
+        for m in range(self.moves):
+            k, rt, u = self.ks[m], self.trs[m], self.us[m]
+            out, _, _ = oracle.eval_j2(self.R, k, rt, self.fn, self.cfg.N, self.cfg.n_up, threads=self.threads)
+            acc = (u < np.exp(out[:, 1, 0] - out[:, 0, 0]) ** 2).astype(np.int32)
+            self.R, self.S, _ = oracle.accept(self.R, self.S, k, rt[:, 1], acc, self.fn, self.cfg.N, self.cfg.n_up)
         return time.perf_counter() - t0
 
 
@@ -308,6 +315,8 @@ def _what(cfg):
         return f"Bspline-vgh of {cfg.n_orb} orbitals + determinant ratio, {cfg.nx}x{cfg.ny}x{cfg.nz} grid"
     if cfg.name == "C3S":
         return "eval P=2 + Metropolis + accept update"
+    if cfg.name == "N64S":
+        return f"one sweep of {cfg.N} moves: eval P=2 + Metropolis + accept update"
     P, mode = qmcgen.trial_spec(cfg.name)
     return f"P={P} {mode}" if P > 1 else "P=1"
 
@@ -397,11 +406,14 @@ def workload_config(cfg, world):
                 f"variant (U^2_k at r_k and r'_k in one step, ratio fused)",
         "C3P12": f"C3P12 (NEXT-3): C3 instance per rank (N={cfg.N} x W={cfg.W}, fp32, seed 2(+rank)), P=12 NLPP "
                  f"virtual moves (icosahedral quadrature sphere about a nearby ion point), ratios vs V_cur",
+        "N64S": f"N64S: the paper's NiO-64 size (N={cfg.N} electrons, Table 1) x W={cfg.W} walkers, fp32: one full "
+                f"particle-by-particle sweep per step ({cfg.N} moves: eval at (r_k, r'_k) -> Metropolis -> accept "
+                f"of R and the 5N state), replayed as one CUDA graph",
         "C3S": f"C3S (NEXT-2 sweep step): C3 instance per rank (N={cfg.N} x W={cfg.W}, fp32, seed 2(+rank)), "
                f"one PbyP move per walker: eval at (r_k, r'_k) -> Metropolis -> accept-side update of R and "
                f"the 5N fp32 J2 state",
     }[name]
-    return {"workload": desc, "N": cfg.N, "W": cfg.W, "P": {"C3S": 2, "C3P2": 2, "C3P12": 12}.get(name, 1), "m": cfg.m, "Np": cfg.Np,
+    return {"workload": desc, "N": cfg.N, "W": cfg.W, "P": {"C3S": 2, "C3P2": 2, "C3P12": 12, "N64S": 2}.get(name, 1), "m": cfg.m, "Np": cfg.Np,
             "parallelism": f"{'walker-instance' if name != 'C5' else 'source-axis'} x{world}",
             "l2": "inputs > 126 MB L2 (no flush needed)"}
 
@@ -753,7 +765,7 @@ class SweepPlan:
     qj2_accept (R[:, k] and the 5N fp32 state of every partner).  Electron
     k = (k0 + s) mod N at step s (ordered sweep), inputs pre-drawn by qmcgen."""
     mode = "C3S"
-    launches_per_step = 5      # eval kernel + counter memset + metropolis + r_k gather + accept kernel
+    launches_per_step = 6      # eval kernel + counter memset + ratio + metropolis + r_k gather + accept kernel
 
     def __init__(self, cfg, rank, world):
         self.cfg = cfg
@@ -770,7 +782,7 @@ class SweepPlan:
         cfg = self.cfg
         self.fn = q.Functor.of(qmcgen.make_functor(cfg.seed, cfg.L, cfg.m))
         self.R = q.gen_positions(self.seed, cfg.W, cfg.N, cfg.Np, cfg.L, torch.float32)
-        self.S = torch.zeros((cfg.W, 5, cfg.Np), dtype=torch.float32, device="cuda")   # 5N state
+        self.S_ = torch.zeros((cfg.W, 5, cfg.Np), dtype=torch.float32, device="cuda")   # 5N state
         ks, tr, u = qmcgen.make_sweep(self.seed, cfg.W, cfg.N, cfg.L, np.float32, n_steps)
         self.ks, self.tr, self.u = (torch.from_numpy(ks).cuda(), torch.from_numpy(tr).cuda(),
                                     torch.from_numpy(u).cuda())
@@ -790,7 +802,7 @@ class SweepPlan:
         q.eval(self.R, k, self.tr[s], self.fn, cfg.N, cfg.n_up, ratio=True, out=self.out,
                ratio_out=self.ratio, workspace=self.ws)
         q.metropolis(self.ratio, self.u[s], self.acc, trial=1)
-        q.accept(self.R, self.S, k, self.tr[s], self.acc, self.out, self.fn, cfg.N, cfg.n_up, trial=1,
+        q.accept(self.R, self.S_, k, self.tr[s], self.acc, self.out, self.fn, cfg.N, cfg.n_up, trial=1,
                  workspace=self.wsa)
 
     def kernel_ms(self, q, stream, reps):
@@ -803,7 +815,7 @@ class SweepPlan:
         r_old = self.tr[s][:, 0, :].contiguous()
         self.n_acc = int(self.acc.sum().item())
         torch.cuda.synchronize()
-        return _event_ms(lambda: q.accept(self.R, self.S, k, self.tr[s], self.acc, self.out, self.fn, cfg.N,
+        return _event_ms(lambda: q.accept(self.R, self.S_, k, self.tr[s], self.acc, self.out, self.fn, cfg.N,
                                           cfg.n_up, trial=1, r_old=r_old), stream, reps)
 
     @property
@@ -816,6 +828,81 @@ class SweepPlan:
 
     def e2e(self, q, steps, dist_mod):
         return None   # see DESIGN.md: the host-buffer path is measured on C3
+
+
+class GraphSweepPlan(SweepPlan):
+    """A full particle-by-particle sweep of the paper's NiO-64 size (N = 768,
+    1024 walkers): N moves per walker, each eval P = 2 -> ratio -> Metropolis
+    -> accept (5 launches, the rows L2-resident: 9.4 MB of positions, 15.7 MB of
+    state), captured once as a CUDA graph and replayed per step -- the per-move
+    work is a few microseconds, so eager launches would dominate.  Replays
+    re-run the same pre-drawn moves on the evolving configuration (the timing
+    is unaffected)."""
+    mode = "N64S"
+    OPS_PER_PAIR = 36 * 2 + 36 * 2      # eval at (r_k, r'_k) + accept's old/new functor terms, per partner
+
+    def __init__(self, cfg, rank, world):
+        super().__init__(cfg, rank, world)
+        self.S = cfg.N
+        self.launches_per_step = 5 * self.S
+        self.items_per_step = self.S * cfg.W * (cfg.N - 1)
+
+    def prepare(self, q, n_steps=None):
+        import torch
+        super().prepare(q, self.S)
+        cfg = self.cfg
+        self.q = q
+        # eager reference timing of one sweep (launch-bound), then capture the sweep
+        for _ in range(2):
+            self._sweep(q)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        self._sweep(q)
+        e1.record()
+        torch.cuda.synchronize()
+        self.eager_ms = e0.elapsed_time(e1)
+        self.graph = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            self._sweep(q)                   # warm-up on the capture stream
+        torch.cuda.current_stream().wait_stream(cs)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(self.graph):
+            self._sweep(q)
+        torch.cuda.synchronize()
+        log(f"[bench] N64S: eager sweep {self.eager_ms:.3f} ms; captured {self.S} moves x 5 launches in one graph")
+
+    def _sweep(self, q):
+        cfg = self.cfg
+        for s in range(self.S):
+            k = self.ks[s]
+            q.eval(self.R, k, self.tr[s], self.fn, cfg.N, cfg.n_up, ratio=True, out=self.out,
+                   ratio_out=self.ratio, workspace=self.ws)
+            q.metropolis(self.ratio, self.u[s], self.acc, trial=1)
+            q.accept(self.R, self.S_, k, self.tr[s], self.acc, self.out, self.fn, cfg.N, cfg.n_up, trial=1,
+                     workspace=self.wsa)
+
+    def step(self, q, dist_mod):
+        self.graph.replay()
+
+    def kernel_ms(self, q, stream, reps):
+        return _event_ms(lambda: self.graph.replay(), stream, max(1, reps // 10))
+
+    def roofline(self, kms, peak_hbm):
+        cfg = self.cfg
+        ops = self.S * cfg.W * (cfg.N - 1) * self.OPS_PER_PAIR
+        peak = 148 * 128 * 1.965e9 / 1e12
+        achieved = ops / (kms / 1e3) / 1e12
+        return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": None, "kernel": "one sweep: 768 x (j2_eval_warp_kernel, ratio, metropolis, gather, "
+                                             "j2_accept_kernel) in one CUDA graph",
+                "kernel_ms": kms, "alg_ops_per_launch": ops, "ops_per_pair": self.OPS_PER_PAIR,
+                "eager_ms_per_sweep": self.eager_ms,
+                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1.965 GHz (DESIGN.md section 7); the "
+                               "working set (25 MB) is L2-resident and each launch is a few microseconds, so "
+                               "this sweep is latency-bound, which the graph addresses"}
 
 
 class SpoPlan:
@@ -957,6 +1044,8 @@ class J1Plan:
 
 
 def make_plan(cfg, rank, world):
+    if cfg.name == "N64S":
+        return GraphSweepPlan(cfg, rank, world)
     if cfg.name.startswith("J"):
         return J1Plan(cfg, rank, world)
     if cfg.name.startswith("S"):
@@ -992,7 +1081,9 @@ def run_ours(args):
     cfg = qmcgen.config(args.config)
 
     plan = make_plan(cfg, rank, world)
-    if plan.mode == "C3S":                            # pre-drawn sweep inputs for every step
+    if plan.mode == "N64S":
+        plan.prepare(q)                               # one sweep's moves, captured as a CUDA graph
+    elif plan.mode == "C3S":                          # pre-drawn sweep inputs for every step
         plan.prepare(q, args.warmup + 2 * args.steps + 2)
     else:
         plan.prepare(q)                               # device-resident inputs (generation untimed)
@@ -1053,7 +1144,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "weak" if plan.mode in ("C3", "C3S", "C3P2", "C3P12", "S1", "S1V", "J1S") else "strong",
+            "scaling": "weak" if plan.mode in ("C3", "C3S", "C3P2", "C3P12", "S1", "S1V", "J1S", "N64S") else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(cfg, world),
             "roofline": (plan.roofline(kms, peak) if hasattr(plan, "roofline") else

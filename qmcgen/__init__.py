@@ -432,6 +432,9 @@ CONFIGS = {
     "C3": Config("C3", N=614400, W=1024, dtype="f32", seed=2),
     "C4": Config("C4", N=6144, W=1024, dtype="f32", seed=3, instances=4096),
     "C5": Config("C5", N=4915200, W=1024, dtype="f32", seed=5),
+    # the paper's own NiO-64 size (Table 1: N = 768) and population (1024 walkers): one full
+    # particle-by-particle sweep (768 moves per walker) as one CUDA graph
+    "N64S": Config("N64S", N=768, W=1024, dtype="f32", seed=14),
 }
 
 

@@ -233,3 +233,53 @@ def test_accept_C3_full_size_sampled(q):
                 S[w:w + 1].cpu().numpy(), R2, S2, ab)
     del R, S
     torch.cuda.empty_cache()
+
+
+def test_sweep_captured_as_cuda_graph_equals_eager(q):
+    """A full particle-by-particle sweep (N moves: eval P = 2 -> Metropolis ->
+    accept) captured once in a CUDA graph and replayed gives bitwise the same
+    positions, state and decisions as the same calls launched eagerly (the
+    bench's N64S path)."""
+    N, W = 96, 64
+    L = qmcgen.cell_length(N)
+    Np = qmcgen.padded_size(N, 32)
+    fn = q.Functor.of(qmcgen.make_functor(3, L))
+    ks, tr, u = qmcgen.make_sweep(3, W, N, L, np.float32, N)
+    ks, tr, u = dev(ks), dev(tr), dev(u)
+    R0 = dev(qmcgen.positions(3, np.arange(W), N, Np, L, np.float32))
+    ws = q.Workspace(q.workspace_size(W, 2, N, torch.float32))
+    wsa = q.Workspace(1 << 16)
+
+    def run(R, S, out, ratio, acc, accs):
+        for s in range(N):
+            q.eval(R, ks[s], tr[s], fn, N, N // 2, ratio=True, out=out, ratio_out=ratio, workspace=ws)
+            q.metropolis(ratio, u[s], acc, trial=1)
+            q.accept(R, S, ks[s], tr[s], acc, out, fn, N, N // 2, trial=1, workspace=wsa)
+            accs[s].copy_(acc)
+
+    def buffers():
+        return (R0.clone(), torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda"),
+                torch.empty((W, 2, 5), dtype=torch.float64, device="cuda"),
+                torch.empty((W, 2, 2), dtype=torch.float64, device="cuda"),
+                torch.empty(W, dtype=torch.int32, device="cuda"),
+                torch.empty((N, W), dtype=torch.int32, device="cuda"))
+
+    e = buffers()
+    run(*e)
+    g_bufs = buffers()
+    warm = buffers()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cs):
+        run(*warm)
+    torch.cuda.current_stream().wait_stream(cs)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        run(*g_bufs)
+    g_bufs[0].copy_(R0)
+    g_bufs[1].zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(e[0], g_bufs[0]) and torch.equal(e[1], g_bufs[1]) and torch.equal(e[5], g_bufs[5])
+    a = e[5].cpu().numpy()
+    assert 0 < a.sum() < a.size
