@@ -832,19 +832,19 @@ class SweepPlan:
 
 class GraphSweepPlan(SweepPlan):
     """A full particle-by-particle sweep of the paper's NiO-64 size (N = 768,
-    1024 walkers): N moves per walker, each eval P = 2 -> ratio -> Metropolis
-    -> accept (5 launches, the rows L2-resident: 9.4 MB of positions, 15.7 MB of
-    state), captured once as a CUDA graph and replayed per step -- the per-move
-    work is a few microseconds, so eager launches would dominate.  Replays
-    re-run the same pre-drawn moves on the evolving configuration (the timing
-    is unaffected)."""
+    1024 walkers): N moves per walker, each eval P = 2 -> Metropolis fused
+    into accept (2 launches; the rows are L2-resident: 9.4 MB of positions,
+    15.7 MB of state), captured once as a CUDA graph and replayed per step --
+    the per-move work is a few microseconds, so eager launches would dominate.
+    Replays re-run the same pre-drawn moves on the evolving configuration (the
+    timing is unaffected)."""
     mode = "N64S"
     OPS_PER_PAIR = 36 * 2 + 36 * 2      # eval at (r_k, r'_k) + accept's old/new functor terms, per partner
 
     def __init__(self, cfg, rank, world):
         super().__init__(cfg, rank, world)
         self.S = cfg.N
-        self.launches_per_step = 5 * self.S
+        self.launches_per_step = 2 * self.S
         self.items_per_step = self.S * cfg.W * (cfg.N - 1)
 
     def prepare(self, q, n_steps=None):
@@ -872,20 +872,26 @@ class GraphSweepPlan(SweepPlan):
         with torch.cuda.graph(self.graph):
             self._sweep(q)
         torch.cuda.synchronize()
-        log(f"[bench] N64S: eager sweep {self.eager_ms:.3f} ms; captured {self.S} moves x 5 launches in one graph")
+        log(f"[bench] N64S: eager sweep {self.eager_ms:.3f} ms; captured {self.S} moves x 2 launches in one graph")
 
     def _sweep(self, q):
+        # per move two launches: qj2_eval at (r_k, r'_k), then the Metropolis test fused into the
+        # accept-side update (qj2_metropolis_accept, r_k = trial 0, V_ref = V(r_k))
         cfg = self.cfg
         for s in range(self.S):
             k = self.ks[s]
-            q.eval(self.R, k, self.tr[s], self.fn, cfg.N, cfg.n_up, ratio=True, out=self.out,
-                   ratio_out=self.ratio, workspace=self.ws)
-            q.metropolis(self.ratio, self.u[s], self.acc, trial=1)
-            q.accept(self.R, self.S_, k, self.tr[s], self.acc, self.out, self.fn, cfg.N, cfg.n_up, trial=1,
-                     workspace=self.wsa)
+            q.eval(self.R, k, self.tr[s], self.fn, cfg.N, cfg.n_up, out=self.out, workspace=self.ws)
+            q.metropolis_accept(self.R, self.S_, k, self.tr[s], self.out, self.u[s], self.fn, cfg.N, cfg.n_up,
+                                acc=self.acc)
 
     def step(self, q, dist_mod):
         self.graph.replay()
+
+    @property
+    def alg_bytes_per_launch(self):
+        # the sweep's rows stay in L2 (25 MB working set); reported against the ALU ceiling instead
+        cfg = self.cfg
+        return self.S * cfg.W * (cfg.N - 1) * 12
 
     def kernel_ms(self, q, stream, reps):
         return _event_ms(lambda: self.graph.replay(), stream, max(1, reps // 10))
@@ -896,8 +902,8 @@ class GraphSweepPlan(SweepPlan):
         peak = 148 * 128 * 1.965e9 / 1e12
         achieved = ops / (kms / 1e3) / 1e12
         return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "one sweep: 768 x (j2_eval_warp_kernel, ratio, metropolis, gather, "
-                                             "j2_accept_kernel) in one CUDA graph",
+                "traffic": None, "kernel": "one sweep: 768 x (j2_eval_warp_kernel, j2_accept_kernel with the "
+                                             "fused Metropolis test) in one CUDA graph",
                 "kernel_ms": kms, "alg_ops_per_launch": ops, "ops_per_pair": self.OPS_PER_PAIR,
                 "eager_ms_per_sweep": self.eager_ms,
                 "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1.965 GHz (DESIGN.md section 7); the "

@@ -260,6 +260,25 @@ qj2_status qj2_accept(const qj2_functor *fn, qj2_dtype dtype,
 qj2_status qj2_metropolis(int64_t W, const double *ratio, int64_t ratio_stride,
                           const double *u, int32_t *accept, void *stream);
 
+/* qj2_metropolis_accept -- qj2_metropolis fused into qj2_accept (one launch */
+/* per move instead of three: the paper-sized sweeps are launch-bound).      */
+/* Every CTA of walker w takes the same decision                             */
+/*   accept[w] = u[w] < rho^2,  rho = exp(V_new - V_ref),                    */
+/*   V_new = out_new[w*out_stride], V_ref = v_ref[w*v_ref_stride]            */
+/* (v_ref = qj2_eval's out at r_k of the P = 2 drift variant, stride 5P, or  */
+/* the caller's V_cur, stride 1), writes it to accept (device [W] int32,     */
+/* OUTPUT), and applies the update of qj2_accept to accepted walkers.        */
+/* r_old is REQUIRED here (row w at r_old + w*r_stride, e.g. trial 0 of the  */
+/* drift variant); r_new likewise with the same stride.  Other arguments and */
+/* errors as qj2_accept; no workspace.                                       */
+qj2_status qj2_metropolis_accept(const qj2_functor *fn, qj2_dtype dtype,
+                                 int64_t W, int64_t N_total, int64_t N_up,
+                                 int64_t i_offset, int64_t N_local, int64_t Np,
+                                 void *R, void *state, const int32_t *k,
+                                 const void *r_new, const void *r_old, int64_t r_stride,
+                                 const double *out_new, const double *v_ref, int64_t out_stride,
+                                 int64_t v_ref_stride, const double *u, int32_t *accept, void *stream);
+
 /* ------------------------------------------------------------------------ */
 /* NEXT-4: tricubic B-spline single-particle orbitals (SPOs) and the         */
 /* determinant ratio.                                                        */

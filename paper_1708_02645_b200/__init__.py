@@ -28,7 +28,8 @@ import torch
 
 from . import _build
 
-__all__ = ["QJ2Error", "Functor", "J1Functor", "Workspace", "eval", "eval_j1", "accept", "metropolis", "SpoTable",
+__all__ = ["QJ2Error", "Functor", "J1Functor", "Workspace", "eval", "eval_j1", "accept", "metropolis",
+           "metropolis_accept", "SpoTable",
            "spo_eval", "gen_spo_table", "eval_host", "ratio", "functor_eval_vgl",
            "min_image_disp", "check_inputs", "padded_size", "gen_positions", "lib_path",
            "workspace_size", "host_workspace_size", "version", "device_check"]
@@ -96,6 +97,8 @@ def _load():
         "qj2_accept": (ctypes.c_int, [F, ctypes.c_int, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp, i64, vp,
                                       vp, vp, i64, vp, sz, vp]),
         "qj2_metropolis": (ctypes.c_int, [i64, vp, i64, vp, vp, vp]),
+        "qj2_metropolis_accept": (ctypes.c_int, [F, ctypes.c_int, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, i64,
+                                                 vp, vp, i64, i64, vp, vp, vp]),
         "qj2_spo_eval": (ctypes.c_int, [ctypes.POINTER(_SpoTable), i32, ctypes.c_int, i64, vp, i64, vp, i64, i64,
                                         vp, i64, vp, vp, vp]),
         "qj2gen_spo_table": (ctypes.c_int, [ctypes.c_uint64, i64, i64, i64, i64, i64, vp, vp]),
@@ -122,7 +125,7 @@ def _load():
 _lib = _load()
 EXPORTS = ("qj2_version", "qj2_status_string", "qj2_last_error", "qj2_device_check", "qj2_padded_size",
            "qj2_eval_workspace_size", "qj2_eval", "qj2_ratio", "qj2_eval_j1", "qj2_accept_workspace_size",
-           "qj2_accept", "qj2_metropolis", "qj2_spo_eval", "qj2gen_spo_table", "qj2_eval_host_workspace_size",
+           "qj2_accept", "qj2_metropolis", "qj2_metropolis_accept", "qj2_spo_eval", "qj2gen_spo_table", "qj2_eval_host_workspace_size",
            "qj2_eval_host", "qj2_functor_eval_vgl", "qj2_min_image_disp", "qj2_check_inputs",
            "qj2gen_positions")
 
@@ -399,6 +402,37 @@ def accept(R, state, k, r_new, acc, out_new, fn, n_total: int, n_up: int, *, tri
                            op, os_, _ptr(ws.buf), ws.nbytes,
                            ctypes.c_void_p(_stream_ptr(stream))), "qj2_accept")
     return R, state
+
+
+def metropolis_accept(R, state, k, r_trial, out, u, fn, n_total: int, n_up: int, *, acc=None, trial_new: int = 1,
+                      trial_old: int = 0, V_cur=None, i_offset: int = 0, n_local: int | None = None, stream=None):
+    """qj2_metropolis_accept: the Metropolis test (u < exp(2 (V_new - V_ref)))
+    fused into the accept-side update, one launch.  r_trial [W][P][3] holds
+    r_k (trial_old) and r'_k (trial_new), out is qj2_eval's [W][P][5];
+    V_ref = V_cur [W] if given, else out[:, trial_old, 0].  Returns acc [W]."""
+    _req(R, "R", ndim=3)
+    W, _, Np = R.shape
+    _req(state, "state", R.dtype, 3)
+    _req(k, "k", torch.int32, 1)
+    _req(r_trial, "r_trial", R.dtype, 3)
+    _req(out, "out", torch.float64, 3)
+    _req(u, "u", torch.float64, 1)
+    rn, rs = _row_ptr(r_trial, trial_new, 3)
+    ro, _ = _row_ptr(r_trial, trial_old, 3)
+    on, os_ = _row_ptr(out, trial_new, 5)
+    if V_cur is not None:
+        _req(V_cur, "V_cur", torch.float64, 1)
+        vr, vrs = _ptr(V_cur), 1
+    else:
+        vr, vrs = _row_ptr(out, trial_old, 5)
+    if acc is None:
+        acc = torch.empty(W, dtype=torch.int32, device=R.device)
+    n_local = min(Np, n_total - i_offset) if n_local is None else int(n_local)
+    f = Functor.of(fn)
+    _check(_lib.qj2_metropolis_accept(f.ptr, _dtype_code(R.dtype), W, n_total, n_up, i_offset, n_local, Np,
+                                      _ptr(R), _ptr(state), _ptr(k), rn, ro, rs, on, vr, os_, vrs, _ptr(u),
+                                      _ptr(acc), ctypes.c_void_p(_stream_ptr(stream))), "qj2_metropolis_accept")
+    return acc
 
 
 def metropolis(ratio_out, u, acc=None, *, trial: int = 0, stream=None):

@@ -41,10 +41,17 @@ struct AcceptParams {
     const int32_t *k;             // [W] global
     const void *r_new;            // row w at r_new + w * r_stride
     int64_t r_stride;
-    const void *r_old;            // [W][3] (caller's, or gathered into the workspace)
+    const void *r_old;            // row w at r_old + w * r_old_stride (caller's, or gathered into the workspace)
+    int64_t r_old_stride;
     const int32_t *accept;        // [W]
     const double *out_new;        // row w at out_new + w * out_stride: (V, Gx, Gy, Gz, L) at r'_k
     int64_t out_stride;
+    // fused Metropolis (qj2_metropolis_accept): u != NULL -> accept iff u[w] < exp(2 (V_new - V_ref)),
+    // V_ref = v_ref[w * v_ref_stride]; the decision is written to acc_out
+    const double *u;
+    const double *v_ref;
+    int64_t v_ref_stride;
+    int32_t *acc_out;
     double L[3];
     double pcoef[2 * (QJ2_MAX_M + 1)][4];   // power basis: [0, m] same spin, [m+1, 2m+1] opposite
 };
@@ -193,7 +200,14 @@ j2_accept_kernel(const __grid_constant__ AcceptParams p) {
     constexpr int TILE = ATPB * AVPT * AITER * VW;
     const int64_t w = (int64_t)blockIdx.x / p.tiles_per_walker;
     const int64_t tile = (int64_t)blockIdx.x - w * p.tiles_per_walker;
-    if (!p.accept[w]) return;                  // rejected: nothing to do (Alg. 1 L9 "or reject")
+    if (p.u) {                                 // fused Metropolis (the same decision in every CTA of w)
+        const double rho = exp(p.out_new[w * p.out_stride] - p.v_ref[w * p.v_ref_stride]);
+        const bool acc = p.u[w] < rho * rho;
+        if (tile == 0 && threadIdx.x == 0) p.acc_out[w] = acc ? 1 : 0;
+        if (!acc) return;
+    } else if (!p.accept[w]) {
+        return;                                // rejected: nothing to do (Alg. 1 L9 "or reject")
+    }
 
     __shared__ Coef4<T> tab[2 * (QJ2_MAX_M + 1)];
     for (int e = threadIdx.x; e < 2 * (p.m + 1); e += blockDim.x) {
@@ -203,7 +217,7 @@ j2_accept_kernel(const __grid_constant__ AcceptParams p) {
     }
     const int64_t kg = p.k[w];
     const T *rn = static_cast<const T *>(p.r_new) + w * p.r_stride;
-    const T *ro = static_cast<const T *>(p.r_old) + w * 3;
+    const T *ro = static_cast<const T *>(p.r_old) + w * p.r_old_stride;
     AxisD an[3], ao[3];
     Axis<T> fan[3], fao[3];
 #pragma unroll

@@ -11,6 +11,7 @@ static cudaError_t launch_accept(const AcceptParams &p0, void *r_old_ws, cudaStr
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         p.r_old = r_old_ws;
+        p.r_old_stride = 3;
     }
     const int64_t nb = p.W * p.tiles_per_walker;
     // fp64 geometry when the functor grid is fine enough for fp32's relative

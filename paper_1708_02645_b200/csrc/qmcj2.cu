@@ -549,13 +549,60 @@ qj2_status qj2_accept(const qj2_functor *fn, qj2_dtype dtype,
     p.tiles_per_walker = tpw;
     p.m = fn->m;
     p.inv_delta = (double)fn->m / fn->r_cut;
-    p.R = R; p.state = state; p.k = k; p.r_new = r_new; p.r_stride = r_stride; p.r_old = r_old; p.accept = accept;
+    p.R = R; p.state = state; p.k = k; p.r_new = r_new; p.r_stride = r_stride; p.r_old = r_old; p.r_old_stride = 3;
+    p.accept = accept;
     p.out_new = out_new; p.out_stride = out_stride;
     for (int d = 0; d < 3; ++d) p.L[d] = fn->L[d];
     power_basis(fn->coef[0], fn->m, p.pcoef);
     power_basis(fn->coef[1], fn->m, p.pcoef + (fn->m + 1));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e = dtype == QJ2_FP32 ? launch_accept_f32(p, workspace, s) : launch_accept_f64(p, workspace, s);
+    return e == cudaSuccess ? QJ2_OK : cuda_fail(e, "j2_accept_kernel launch");
+}
+
+qj2_status qj2_metropolis_accept(const qj2_functor *fn, qj2_dtype dtype,
+                                 int64_t W, int64_t N_total, int64_t N_up,
+                                 int64_t i_offset, int64_t N_local, int64_t Np,
+                                 void *R, void *state, const int32_t *k,
+                                 const void *r_new, const void *r_old, int64_t r_stride,
+                                 const double *out_new, const double *v_ref, int64_t out_stride,
+                                 int64_t v_ref_stride, const double *u, int32_t *accept, void *stream) {
+    qj2_status st = validate_functor(fn);
+    if (st) return st;
+    if (dtype != QJ2_FP32 && dtype != QJ2_FP64) return fail(QJ2_EINVAL, "bad dtype %d", (int)dtype);
+    if (W < 0) return fail(QJ2_EINVAL, "W < 0");
+    if (N_total < 2) return fail(QJ2_EINVAL, "N_total must be >= 2");
+    if (N_up < 0 || N_up > N_total) return fail(QJ2_ERANGE, "N_up out of [0, N_total]");
+    if (i_offset < 0 || N_local < 1) return fail(QJ2_EINVAL, "need i_offset >= 0 and N_local >= 1");
+    if (i_offset + N_local > N_total) return fail(QJ2_ERANGE, "i_offset + N_local > N_total");
+    if (Np < N_local || Np % vw_of(dtype) != 0)
+        return fail(QJ2_EINVAL, "Np must be >= N_local and a multiple of %d", vw_of(dtype));
+    if (r_stride < 3 || out_stride < 5 || v_ref_stride < 1)
+        return fail(QJ2_EINVAL, "need r_stride >= 3, out_stride >= 5, v_ref_stride >= 1");
+    if (W == 0) return QJ2_OK;
+    if (!R || !state || !k || !r_new || !r_old || !out_new || !v_ref || !u || !accept)
+        return fail(QJ2_EINVAL, "R, state, k, r_new, r_old, out_new, v_ref, u and accept must be non-NULL");
+    if (((uintptr_t)R & 15) || ((uintptr_t)state & 15)) return fail(QJ2_EINVAL, "R and state must be 16-byte aligned");
+    const int64_t tile = dtype == QJ2_FP32 ? accept_tile<float>() : accept_tile<double>();
+    const int64_t tpw = (N_local + tile - 1) / tile;
+    if (W * tpw > 0x7fffffffLL) return fail(QJ2_EINVAL, "problem too large for one launch");
+    st = check_device();
+    if (st) return st;
+    AcceptParams p;
+    memset(&p, 0, sizeof p);
+    p.W = W; p.N_total = N_total; p.N_up = N_up; p.i_offset = i_offset; p.N_local = N_local; p.Np = Np;
+    p.tiles_per_walker = tpw;
+    p.m = fn->m;
+    p.inv_delta = (double)fn->m / fn->r_cut;
+    p.R = R; p.state = state; p.k = k; p.r_new = r_new; p.r_stride = r_stride; p.r_old = r_old;
+    p.r_old_stride = r_stride; p.accept = accept;
+    p.out_new = out_new; p.out_stride = out_stride;
+    p.u = u; p.v_ref = v_ref; p.v_ref_stride = v_ref_stride; p.acc_out = accept;
+    for (int d = 0; d < 3; ++d) p.L[d] = fn->L[d];
+    power_basis(fn->coef[0], fn->m, p.pcoef);
+    power_basis(fn->coef[1], fn->m, p.pcoef + (fn->m + 1));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = dtype == QJ2_FP32 ? launch_accept_f32(p, nullptr, s) : launch_accept_f64(p, nullptr, s);
     return e == cudaSuccess ? QJ2_OK : cuda_fail(e, "j2_accept_kernel launch");
 }
 

@@ -154,6 +154,25 @@ def test_accept_host_validation(q):
     assert q._lib.qj2_accept_workspace_size(1024, 0, ctypes.byref(b)) == 0 and b.value >= 1024 * 12
 
 
+def test_metropolis_accept_host_validation(q):
+    f = _functor(q)
+    P = ctypes.c_void_p(4096)
+
+    def call(**over):
+        a = dict(W=4, N_total=100, N_up=50, i_offset=0, N_local=100, Np=128, R=P, S=P, k=P, rn=P, ro=P, rs=6,
+                 on=P, vr=P, os=10, vrs=10, u=P, acc=P)
+        a.update(over)
+        return q._lib.qj2_metropolis_accept(f.ptr, 0, a["W"], a["N_total"], a["N_up"], a["i_offset"], a["N_local"],
+                                            a["Np"], a["R"], a["S"], a["k"], a["rn"], a["ro"], a["rs"], a["on"],
+                                            a["vr"], a["os"], a["vrs"], a["u"], a["acc"], None)
+    assert call(ro=None) == 1                     # r_old is required (no gather in the fused path)
+    assert call(u=None) == 1
+    assert call(rs=2) == 1
+    assert call(vrs=0) == 1
+    assert call(N_up=101) == 2
+    assert call(W=0) == 0
+
+
 def test_metropolis_and_spo_host_validation(q):
     P = ctypes.c_void_p(4096)
     lib = q._lib

@@ -252,9 +252,13 @@ def test_sweep_captured_as_cuda_graph_equals_eager(q):
 
     def run(R, S, out, ratio, acc, accs):
         for s in range(N):
-            q.eval(R, ks[s], tr[s], fn, N, N // 2, ratio=True, out=out, ratio_out=ratio, workspace=ws)
-            q.metropolis(ratio, u[s], acc, trial=1)
-            q.accept(R, S, ks[s], tr[s], acc, out, fn, N, N // 2, trial=1, workspace=wsa)
+            if s % 2:      # both move forms: separate ratio/Metropolis/accept launches and the fused one
+                q.eval(R, ks[s], tr[s], fn, N, N // 2, ratio=True, out=out, ratio_out=ratio, workspace=ws)
+                q.metropolis(ratio, u[s], acc, trial=1)
+                q.accept(R, S, ks[s], tr[s], acc, out, fn, N, N // 2, trial=1, workspace=wsa)
+            else:
+                q.eval(R, ks[s], tr[s], fn, N, N // 2, out=out, workspace=ws)
+                q.metropolis_accept(R, S, ks[s], tr[s], out, u[s], fn, N, N // 2, acc=acc)
             accs[s].copy_(acc)
 
     def buffers():
@@ -283,3 +287,32 @@ def test_sweep_captured_as_cuda_graph_equals_eager(q):
     assert torch.equal(e[0], g_bufs[0]) and torch.equal(e[1], g_bufs[1]) and torch.equal(e[5], g_bufs[5])
     a = e[5].cpu().numpy()
     assert 0 < a.sum() < a.size
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_fused_metropolis_accept_equals_separate_calls(q, dtype):
+    """qj2_metropolis_accept (decision inside the accept kernel) == qj2_eval's
+    ratio -> qj2_metropolis -> qj2_accept, bitwise (same fp64 decision), over a
+    few sweep moves; and the fused decisions equal the oracle's where clear."""
+    N, W = 3000, 96
+    L = qmcgen.cell_length(N)
+    Np = qmcgen.padded_size(N, 4 if dtype == np.float32 else 2)
+    fn = q.Functor.of(qmcgen.make_functor(5, L))
+    ks, tr, u = qmcgen.make_sweep(5, W, N, L, dtype, 4)
+    R = qmcgen.positions(5, np.arange(W), N, Np, L, dtype)
+    Ra, Rb = dev(R), dev(R)
+    Sa = torch.zeros((W, 5, Np), dtype=Ra.dtype, device="cuda")
+    Sb = torch.zeros_like(Sa)
+    for s in range(4):
+        kd, td, ud = dev(ks[s]), dev(tr[s]), dev(u[s])
+        out_a, rat = q.eval(Ra, kd, td, fn, N, N // 2, ratio=True)
+        acc_a = q.metropolis(rat, ud, trial=1)
+        q.accept(Ra, Sa, kd, td, acc_a, out_a, fn, N, N // 2, trial=1)
+        out_b = q.eval(Rb, kd, td, fn, N, N // 2)
+        acc_b = q.metropolis_accept(Rb, Sb, kd, td, out_b, ud, fn, N, N // 2)
+        assert torch.equal(acc_a, acc_b)
+        o = out_b.cpu().numpy()
+        rho2 = np.exp(o[:, 1, 0] - o[:, 0, 0]) ** 2
+        clear = np.abs(u[s] - rho2) > 1e-9 * rho2
+        assert np.array_equal(acc_b.cpu().numpy()[clear], (u[s] < rho2)[clear].astype(np.int32))
+    assert torch.equal(Ra, Rb) and torch.equal(Sa, Sb)
