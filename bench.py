@@ -408,7 +408,7 @@ def workload_config(cfg, world):
                  f"virtual moves (icosahedral quadrature sphere about a nearby ion point), ratios vs V_cur",
         "N64S": f"N64S: the paper's NiO-64 size (N={cfg.N} electrons, Table 1) x W={cfg.W} walkers, fp32: one full "
                 f"particle-by-particle sweep per step ({cfg.N} moves: eval at (r_k, r'_k) -> Metropolis -> accept "
-                f"of R and the 5N state), replayed as one CUDA graph",
+                f"of R and the 5N state) in one qj2_sweep launch",
         "C3S": f"C3S (NEXT-2 sweep step): C3 instance per rank (N={cfg.N} x W={cfg.W}, fp32, seed 2(+rank)), "
                f"one PbyP move per walker: eval at (r_k, r'_k) -> Metropolis -> accept-side update of R and "
                f"the 5N fp32 J2 state",
@@ -832,51 +832,51 @@ class SweepPlan:
 
 class GraphSweepPlan(SweepPlan):
     """A full particle-by-particle sweep of the paper's NiO-64 size (N = 768,
-    1024 walkers): N moves per walker, each eval P = 2 -> Metropolis fused
-    into accept (2 launches; the rows are L2-resident: 9.4 MB of positions,
-    15.7 MB of state), captured once as a CUDA graph and replayed per step --
-    the per-move work is a few microseconds, so eager launches would dominate.
-    Replays re-run the same pre-drawn moves on the evolving configuration (the
-    timing is unaffected)."""
+    1024 walkers): N moves per walker, each eval at (r_k, r'_k) -> Metropolis ->
+    accept.  The timed step is ONE qj2_sweep launch (walkers resident in shared
+    memory, pair terms kept in registers between the ratio and the update);
+    for context prepare() also times the same sweep as per-move launches
+    (qj2_eval + qj2_metropolis_accept, 2 per move), eagerly and captured in a
+    CUDA graph.  Replays re-run the same pre-drawn moves on the evolving
+    configuration (the work per step is unaffected)."""
     mode = "N64S"
-    OPS_PER_PAIR = 36 * 2 + 36 * 2      # eval at (r_k, r'_k) + accept's old/new functor terms, per partner
+    OPS_PER_PAIR = 36 * 2               # functor terms at r_k and r'_k per partner (reused by the update)
 
     def __init__(self, cfg, rank, world):
         super().__init__(cfg, rank, world)
         self.S = cfg.N
-        self.launches_per_step = 2 * self.S
+        self.launches_per_step = 1
         self.items_per_step = self.S * cfg.W * (cfg.N - 1)
 
     def prepare(self, q, n_steps=None):
         import torch
         super().prepare(q, self.S)
-        cfg = self.cfg
         self.q = q
-        # eager reference timing of one sweep (launch-bound), then capture the sweep
+        self.acc_all = torch.empty((self.S, self.cfg.W), dtype=torch.int32, device="cuda")
+        self.dj_all = torch.empty((self.S, self.cfg.W), dtype=torch.float64, device="cuda")
+        # context: the same sweep as per-move launches, eager and as one CUDA graph
         for _ in range(2):
-            self._sweep(q)
+            self._per_move(q)
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        self._sweep(q)
-        e1.record()
-        torch.cuda.synchronize()
-        self.eager_ms = e0.elapsed_time(e1)
-        self.graph = torch.cuda.CUDAGraph()
+        self.eager_ms = _event_ms(lambda: self._per_move(q), torch.cuda.current_stream(), 1)
+        graph = torch.cuda.CUDAGraph()
         cs = torch.cuda.Stream()
         cs.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(cs):
-            self._sweep(q)                   # warm-up on the capture stream
+            self._per_move(q)
         torch.cuda.current_stream().wait_stream(cs)
         torch.cuda.synchronize()
-        with torch.cuda.graph(self.graph):
-            self._sweep(q)
+        with torch.cuda.graph(graph):
+            self._per_move(q)
         torch.cuda.synchronize()
-        log(f"[bench] N64S: eager sweep {self.eager_ms:.3f} ms; captured {self.S} moves x 2 launches in one graph")
+        graph.replay()
+        torch.cuda.synchronize()
+        self.graph_ms = _event_ms(lambda: graph.replay(), torch.cuda.current_stream(), 3)
+        del graph
+        log(f"[bench] N64S: per-move launches {self.eager_ms:.3f} ms eager, {self.graph_ms:.3f} ms as one CUDA "
+            f"graph ({self.S} moves x 2 launches); the timed step is one qj2_sweep launch")
 
-    def _sweep(self, q):
-        # per move two launches: qj2_eval at (r_k, r'_k), then the Metropolis test fused into the
-        # accept-side update (qj2_metropolis_accept, r_k = trial 0, V_ref = V(r_k))
+    def _per_move(self, q):
         cfg = self.cfg
         for s in range(self.S):
             k = self.ks[s]
@@ -885,16 +885,16 @@ class GraphSweepPlan(SweepPlan):
                                 acc=self.acc)
 
     def step(self, q, dist_mod):
-        self.graph.replay()
+        q.sweep(self.R, self.S_, self.ks, self.tr, self.u, self.fn, self.cfg.N, self.cfg.n_up, acc=self.acc_all,
+                dj=self.dj_all)
 
     @property
     def alg_bytes_per_launch(self):
-        # the sweep's rows stay in L2 (25 MB working set); reported against the ALU ceiling instead
         cfg = self.cfg
-        return self.S * cfg.W * (cfg.N - 1) * 12
+        return cfg.W * cfg.Np * 8 * 4 * 2 + self.S * cfg.W * (4 + 24 + 8 + 4 + 8)   # R + state in/out, inputs
 
     def kernel_ms(self, q, stream, reps):
-        return _event_ms(lambda: self.graph.replay(), stream, max(1, reps // 10))
+        return _event_ms(lambda: self.step(q, None), stream, max(1, reps // 5))
 
     def roofline(self, kms, peak_hbm):
         cfg = self.cfg
@@ -902,13 +902,11 @@ class GraphSweepPlan(SweepPlan):
         peak = 148 * 128 * 1.965e9 / 1e12
         achieved = ops / (kms / 1e3) / 1e12
         return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "one sweep: 768 x (j2_eval_warp_kernel, j2_accept_kernel with the "
-                                             "fused Metropolis test) in one CUDA graph",
+                "traffic": committed_traffic(self.mode),
+                "kernel": "j2_sweep_kernel (one launch per sweep, walkers resident in shared memory)",
                 "kernel_ms": kms, "alg_ops_per_launch": ops, "ops_per_pair": self.OPS_PER_PAIR,
-                "eager_ms_per_sweep": self.eager_ms,
-                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1.965 GHz (DESIGN.md section 7); the "
-                               "working set (25 MB) is L2-resident and each launch is a few microseconds, so "
-                               "this sweep is latency-bound, which the graph addresses"}
+                "per_move_launches_eager_ms": self.eager_ms, "per_move_launches_graph_ms": self.graph_ms,
+                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1.965 GHz (DESIGN.md section 7)"}
 
 
 class SpoPlan:
@@ -1088,7 +1086,7 @@ def run_ours(args):
 
     plan = make_plan(cfg, rank, world)
     if plan.mode == "N64S":
-        plan.prepare(q)                               # one sweep's moves, captured as a CUDA graph
+        plan.prepare(q)                               # one sweep's pre-drawn moves
     elif plan.mode == "C3S":                          # pre-drawn sweep inputs for every step
         plan.prepare(q, args.warmup + 2 * args.steps + 2)
     else:

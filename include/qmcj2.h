@@ -279,6 +279,24 @@ qj2_status qj2_metropolis_accept(const qj2_functor *fn, qj2_dtype dtype,
                                  const double *out_new, const double *v_ref, int64_t out_stride,
                                  int64_t v_ref_stride, const double *u, int32_t *accept, void *stream);
 
+/* qj2_sweep -- S particle-by-particle moves of every walker in ONE launch,  */
+/* the walker resident in shared memory (the paper's system sizes: Table 1   */
+/* N = 256..768).  For s = 0..S-1 and walker w, with k = ks[s*W + w],        */
+/* r_k = trials[((s*W + w)*2 + 0)*3 ..], r'_k = trials[((s*W + w)*2 + 1)*3..]*/
+/* (the P = 2 drift pair): V, G, L at r_k and r'_k (as qj2_eval), the        */
+/* Metropolis decision accept[s*W + w] = u[s*W + w] < exp(2 dJ2) with dJ2 =  */
+/* V(r'_k) - V(r_k) (written to dj[s*W + w] if dj != NULL), and on           */
+/* acceptance the update of qj2_accept (state_i += T_i(r'_k) - T_i(r_k),     */
+/* state_k = the values at r'_k, R[:, k] = r'_k).  fp32 only: R [W][3][Np],  */
+/* state [W][5][Np] (in/out), trials fp32, u fp64, accept int32 (out).       */
+/* Requirements (else QJ2_EINVAL): 2 <= N <= 1024, Np >= N, functor m <= 16  */
+/* (pair terms are kept in fp32; finer functors use qj2_eval +               */
+/* qj2_metropolis_accept).  Moves within a call are sequential per walker;   */
+/* walkers are independent.                                                  */
+qj2_status qj2_sweep(const qj2_functor *fn, int64_t W, int64_t N, int64_t N_up, int64_t Np,
+                     float *R, float *state, int64_t S, const int32_t *ks, const float *trials,
+                     const double *u, int32_t *accept, double *dj, void *stream);
+
 /* ------------------------------------------------------------------------ */
 /* NEXT-4: tricubic B-spline single-particle orbitals (SPOs) and the         */
 /* determinant ratio.                                                        */

@@ -29,7 +29,7 @@ import torch
 from . import _build
 
 __all__ = ["QJ2Error", "Functor", "J1Functor", "Workspace", "eval", "eval_j1", "accept", "metropolis",
-           "metropolis_accept", "SpoTable",
+           "metropolis_accept", "sweep", "SpoTable",
            "spo_eval", "gen_spo_table", "eval_host", "ratio", "functor_eval_vgl",
            "min_image_disp", "check_inputs", "padded_size", "gen_positions", "lib_path",
            "workspace_size", "host_workspace_size", "version", "device_check"]
@@ -97,6 +97,7 @@ def _load():
         "qj2_accept": (ctypes.c_int, [F, ctypes.c_int, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp, i64, vp,
                                       vp, vp, i64, vp, sz, vp]),
         "qj2_metropolis": (ctypes.c_int, [i64, vp, i64, vp, vp, vp]),
+        "qj2_sweep": (ctypes.c_int, [F, i64, i64, i64, i64, vp, vp, i64, vp, vp, vp, vp, vp, vp]),
         "qj2_metropolis_accept": (ctypes.c_int, [F, ctypes.c_int, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, i64,
                                                  vp, vp, i64, i64, vp, vp, vp]),
         "qj2_spo_eval": (ctypes.c_int, [ctypes.POINTER(_SpoTable), i32, ctypes.c_int, i64, vp, i64, vp, i64, i64,
@@ -125,7 +126,7 @@ def _load():
 _lib = _load()
 EXPORTS = ("qj2_version", "qj2_status_string", "qj2_last_error", "qj2_device_check", "qj2_padded_size",
            "qj2_eval_workspace_size", "qj2_eval", "qj2_ratio", "qj2_eval_j1", "qj2_accept_workspace_size",
-           "qj2_accept", "qj2_metropolis", "qj2_metropolis_accept", "qj2_spo_eval", "qj2gen_spo_table", "qj2_eval_host_workspace_size",
+           "qj2_accept", "qj2_metropolis", "qj2_metropolis_accept", "qj2_sweep", "qj2_spo_eval", "qj2gen_spo_table", "qj2_eval_host_workspace_size",
            "qj2_eval_host", "qj2_functor_eval_vgl", "qj2_min_image_disp", "qj2_check_inputs",
            "qj2gen_positions")
 
@@ -433,6 +434,29 @@ def metropolis_accept(R, state, k, r_trial, out, u, fn, n_total: int, n_up: int,
                                       _ptr(R), _ptr(state), _ptr(k), rn, ro, rs, on, vr, os_, vrs, _ptr(u),
                                       _ptr(acc), ctypes.c_void_p(_stream_ptr(stream))), "qj2_metropolis_accept")
     return acc
+
+
+def sweep(R, state, ks, trials, u, fn, n: int, n_up: int, *, acc=None, dj=None, stream=None):
+    """qj2_sweep: S particle-by-particle moves of every walker in one launch,
+    walkers resident in shared memory (N <= 1024, fp32, functor m <= 16).
+    R [W][3][Np], state [W][5][Np] fp32 (in place); ks [S][W] int32, trials
+    [S][W][2][3] fp32 (r_k, r'_k), u [S][W] fp64.  Returns (acc [S][W] int32,
+    dj [S][W] fp64)."""
+    _req(R, "R", torch.float32, 3)
+    W, _, Np = R.shape
+    _req(state, "state", torch.float32, 3)
+    _req(ks, "ks", torch.int32, 2)
+    _req(trials, "trials", torch.float32, 4)
+    _req(u, "u", torch.float64, 2)
+    S = ks.shape[0]
+    if acc is None:
+        acc = torch.empty((S, W), dtype=torch.int32, device=R.device)
+    if dj is None:
+        dj = torch.empty((S, W), dtype=torch.float64, device=R.device)
+    f = Functor.of(fn)
+    _check(_lib.qj2_sweep(f.ptr, W, n, n_up, Np, _ptr(R), _ptr(state), S, _ptr(ks), _ptr(trials), _ptr(u),
+                          _ptr(acc), _ptr(dj), ctypes.c_void_p(_stream_ptr(stream))), "qj2_sweep")
+    return acc, dj
 
 
 def metropolis(ratio_out, u, acc=None, *, trial: int = 0, stream=None):

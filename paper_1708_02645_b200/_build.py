@@ -15,9 +15,9 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libqmcj2.so")
 OBJDIR = os.path.join(PKG, "build_obj")
 SOURCES = [os.path.join(CSRC, f) for f in
-           ["qmcj2.cu", "gen.cu", "launch_accept.cu", "spo.cu"] + [f"launch_{d}_{b}_{m}.cu" for d in ("f32", "f64") for b in ("pb1",)
+           ["qmcj2.cu", "gen.cu", "launch_accept.cu", "spo.cu", "sweep.cu"] + [f"launch_{d}_{b}_{m}.cu" for d in ("f32", "f64") for b in ("pb1",)
                                      for m in ("j2", "j1")]]
-HEADERS = [os.path.join(CSRC, f) for f in ("j2_device.cuh", "j2_kernels.cuh", "j2_tma.cuh", "launch.cuh", "accept.cuh", "spo.cuh")] + \
+HEADERS = [os.path.join(CSRC, f) for f in ("j2_device.cuh", "j2_kernels.cuh", "j2_tma.cuh", "launch.cuh", "accept.cuh", "spo.cuh", "sweep.cuh", "bulk.cuh")] + \
           [os.path.join(ROOT, "include", "qmcj2.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

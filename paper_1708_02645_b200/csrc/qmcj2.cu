@@ -24,6 +24,7 @@
 #include "launch.cuh"
 #include "accept.cuh"
 #include "spo.cuh"
+#include "sweep.cuh"
 
 // ===========================================================================
 // Small kernels
@@ -604,6 +605,39 @@ qj2_status qj2_metropolis_accept(const qj2_functor *fn, qj2_dtype dtype,
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e = dtype == QJ2_FP32 ? launch_accept_f32(p, nullptr, s) : launch_accept_f64(p, nullptr, s);
     return e == cudaSuccess ? QJ2_OK : cuda_fail(e, "j2_accept_kernel launch");
+}
+
+qj2_status qj2_sweep(const qj2_functor *fn, int64_t W, int64_t N, int64_t N_up, int64_t Np,
+                     float *R, float *state, int64_t S, const int32_t *ks, const float *trials,
+                     const double *u, int32_t *accept, double *dj, void *stream) {
+    qj2_status st = validate_functor(fn);
+    if (st) return st;
+    if (fn->m > ACCEPT_FAST_MAX_M)
+        return fail(QJ2_EINVAL, "qj2_sweep keeps fp32 pair terms: m must be <= %d (use qj2_eval + "
+                    "qj2_metropolis_accept per move for finer functors)", ACCEPT_FAST_MAX_M);
+    if (W < 0 || S < 0) return fail(QJ2_EINVAL, "W and S must be >= 0");
+    if (N < 2 || N > SW_MAXN) return fail(QJ2_EINVAL, "qj2_sweep needs 2 <= N <= %d (walker resident in "
+                                          "shared memory)", SW_MAXN);
+    if (N_up < 0 || N_up > N) return fail(QJ2_ERANGE, "N_up out of [0, N]");
+    if (Np < N) return fail(QJ2_EINVAL, "Np must be >= N");
+    if (W > 0x7fffffffLL) return fail(QJ2_EINVAL, "W too large for one launch");
+    if (W == 0 || S == 0) return QJ2_OK;
+    if (!R || !state || !ks || !trials || !u || !accept)
+        return fail(QJ2_EINVAL, "R, state, ks, trials, u and accept must be non-NULL");
+    st = check_device();
+    if (st) return st;
+    SweepParams p;
+    memset(&p, 0, sizeof p);
+    p.W = W; p.N = N; p.N_up = N_up; p.Np = Np; p.S = S;
+    p.m = fn->m;
+    p.inv_delta = (double)fn->m / fn->r_cut;
+    p.invd = (float)p.inv_delta;
+    p.R = R; p.state = state; p.ks = ks; p.trials = trials; p.u = u; p.acc = accept; p.dj = dj;
+    for (int d = 0; d < 3; ++d) p.L[d] = (float)fn->L[d];
+    power_basis(fn->coef[0], fn->m, p.pcoef);
+    power_basis(fn->coef[1], fn->m, p.pcoef + (fn->m + 1));
+    cudaError_t e = launch_sweep(p, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? QJ2_OK : cuda_fail(e, "j2_sweep_kernel launch");
 }
 
 qj2_status qj2_metropolis(int64_t W, const double *ratio, int64_t ratio_stride,

@@ -1,0 +1,151 @@
+// sweep.cu -- the resident-walker sweep kernel's launch (own translation unit).
+#include "sweep.cuh"
+
+namespace qj2 {
+
+__device__ __forceinline__ double sw_warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(SW_TPB, 2) j2_sweep_kernel(const __grid_constant__ SweepParams p) {
+    extern __shared__ __align__(16) float sw_smem[];
+    const int64_t w = blockIdx.x;
+    const int N = (int)p.N;
+    float *rx = sw_smem, *ry = rx + N, *rz = ry + N;                  // R (SoA)
+    float *st = rz + N;                                              // state [5][N]
+    __shared__ Coef4<float> tab[2 * (QJ2_MAX_M + 1)];
+    __shared__ double red[SW_TPB / 32][10];
+    __shared__ double fin[10];
+    __shared__ int s_acc;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < 2 * (p.m + 1); e += SW_TPB) {
+        Coef4<float> c;
+        c.a0 = (float)p.pcoef[e][0]; c.a1 = (float)p.pcoef[e][1];
+        c.a2 = (float)p.pcoef[e][2]; c.a3 = (float)p.pcoef[e][3];
+        tab[e] = c;
+    }
+    const float *Rg = p.R + w * 3 * p.Np;
+    const float *Sg = p.state + w * 5 * p.Np;
+    for (int i = tid; i < N; i += SW_TPB) {
+        rx[i] = Rg[i]; ry[i] = Rg[p.Np + i]; rz[i] = Rg[2 * p.Np + i];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) st[c * N + i] = Sg[c * p.Np + i];
+    }
+    __syncthreads();
+    const uint32_t tab0 = (uint32_t)__cvta_generic_to_shared(tab);
+    const uint32_t tab_opp = tab0 + (uint32_t)((p.m + 1) * (int)sizeof(Coef4<float>));
+    const unsigned clamp = (unsigned)p.m;
+    const float invd = p.invd;
+
+    for (int64_t s = 0; s < p.S; ++s) {
+        const int k = p.ks[s * p.W + w];
+        const float *tr = p.trials + (s * p.W + w) * 6;
+        Axis<float> a0[3], a1[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            a0[d] = make_axis<float>(tr[d], p.L[d]);
+            a1[d] = make_axis<float>(tr[3 + d], p.L[d]);
+        }
+        const bool k_up = k < p.N_up;
+        // 1. pair terms at r_k (q = 0) and r'_k (q = 1), kept per partner
+        float t[SW_SPT][2][5];
+        float acc[2][5];
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int c = 0; c < 5; ++c) acc[q][c] = 0.f;
+#pragma unroll
+        for (int j = 0; j < SW_SPT; ++j) {
+            const int i = tid + j * SW_TPB;
+            const bool live = i < N && i != k;
+            const int ii = i < N ? i : 0;
+            const float x = rx[ii], y = ry[ii], z = rz[ii];
+            const uint32_t base = ((ii < p.N_up) == k_up) ? tab0 : tab_opp;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const Axis<float>(&a)[3] = q ? a1 : a0;
+                const float dx = min_image(x, a[0]), dy = min_image(y, a[1]), dz = min_image(z, a[2]);
+                float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                r2 = live ? r2 : 1e30f;            // the zero row: every term exactly 0
+                const float ir = Traits<float>::rsqrt(r2);
+                const FunctorEval<float> e = functor_from_t<float>(r2 * ir * invd, base, clamp);
+                const float g = e.du * ir;         // U' delta / r
+                t[j][q][0] = e.u;
+                t[j][q][1] = g * dx;
+                t[j][q][2] = g * dy;
+                t[j][q][3] = g * dz;
+                t[j][q][4] = fmaf(e.h, invd, g);   // (U'' + 2U'/r) * delta / 2
+#pragma unroll
+                for (int c = 0; c < 5; ++c) acc[q][c] += t[j][q][c];
+            }
+        }
+        // 2. block reduction (fp64, fixed order)
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+                const double v = sw_warp_sum((double)acc[q][c]);
+                if (lane == 0) red[warp][q * 5 + c] = v;
+            }
+        __syncthreads();
+        if (tid < 10) {
+            double v = 0.0;
+#pragma unroll
+            for (int wi = 0; wi < SW_TPB / 32; ++wi) v += red[wi][tid];
+            fin[tid] = v;
+        }
+        __syncthreads();
+        // 3. Metropolis, decided once
+        if (tid == 0) {
+            const double dj = fin[5] - fin[0];
+            const double rho = exp(dj);
+            const int a = p.u[s * p.W + w] < rho * rho ? 1 : 0;
+            s_acc = a;
+            p.acc[s * p.W + w] = a;
+            if (p.dj) p.dj[s * p.W + w] = dj;
+        }
+        __syncthreads();
+        // 4. accept: partners from the kept terms, then electron k and its position
+        if (s_acc) {
+            const float sg = invd, sl = 2.f * invd;
+#pragma unroll
+            for (int j = 0; j < SW_SPT; ++j) {
+                const int i = tid + j * SW_TPB;
+                if (i < N && i != k) {
+                    st[0 * N + i] += t[j][1][0] - t[j][0][0];
+                    st[1 * N + i] += (t[j][1][1] - t[j][0][1]) * sg;
+                    st[2 * N + i] += (t[j][1][2] - t[j][0][2]) * sg;
+                    st[3 * N + i] += (t[j][1][3] - t[j][0][3]) * sg;
+                    st[4 * N + i] += (t[j][1][4] - t[j][0][4]) * sl;
+                }
+            }
+            if (tid == 0) {
+                // state_k = (V, G, L) at r'_k: G = -invd * sum g d, L = 2 invd * sum (h invd + g)
+                st[0 * N + k] = (float)fin[5];
+                st[1 * N + k] = (float)(-p.inv_delta * fin[6]);
+                st[2 * N + k] = (float)(-p.inv_delta * fin[7]);
+                st[3 * N + k] = (float)(-p.inv_delta * fin[8]);
+                st[4 * N + k] = (float)(2.0 * p.inv_delta * fin[9]);
+                rx[k] = tr[3]; ry[k] = tr[4]; rz[k] = tr[5];
+            }
+        }
+        __syncthreads();
+    }
+    float *Rw = p.R + w * 3 * p.Np;
+    float *Sw = p.state + w * 5 * p.Np;
+    for (int i = tid; i < N; i += SW_TPB) {
+        Rw[i] = rx[i]; Rw[p.Np + i] = ry[i]; Rw[2 * p.Np + i] = rz[i];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) Sw[c * p.Np + i] = st[c * N + i];
+    }
+}
+
+cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s) {
+    const size_t smem = (size_t)8 * p.N * sizeof(float);          // R (3) + state (5) per electron
+    j2_sweep_kernel<<<(unsigned)p.W, SW_TPB, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace qj2

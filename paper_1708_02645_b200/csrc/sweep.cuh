@@ -1,0 +1,50 @@
+// sweep.cuh -- NEXT-2 at the paper's system sizes: a whole particle-by-particle
+// sweep of the J2 factor in one persistent kernel, the walker resident in
+// shared memory (sm_100a).
+//
+// For every walker (one CTA) and every move s < S (Alg. 1 L4-L9 for the J2
+// factor, electron k = ks[s][w], trial positions r_k = trials[s][w][0] and
+// r'_k = trials[s][w][1]):
+//   1. each thread forms, for its partners i != k (i = tid, tid + 256, ...),
+//      the pair terms T_i(r_k) and T_i(r'_k) -- the same fp32 arithmetic as
+//      the eval kernel (single-rounding minimum image, power-basis Horner) --
+//      and keeps them in registers;
+//   2. a block reduction in fp64 gives U^2_k at r_k and r'_k with their
+//      gradient and Laplacian (Eq. 5 / PAPER:1382, Alg. 1 L7-L8);
+//   3. the Metropolis test u < exp(2 dJ2) (reading R19), decided once;
+//   4. if accepted: state_i += T_i(r'_k) - T_i(r_k) from the kept terms (no
+//      recomputation), state_k = the reduced values at r'_k, R[:, k] = r'_k
+//      (PAPER:1305-1306, 1389-1393).
+// R and the 5N state stay in shared memory for all S moves (32 B per
+// electron: N <= 1024 in 32 KB); global memory is touched only to load and
+// store them once and to read the move inputs -- no launch per move.
+#pragma once
+
+#include "qmcj2.h"
+#include "j2_device.cuh"
+
+namespace qj2 {
+
+constexpr int SW_TPB = 256;       // threads per walker (CTA)
+constexpr int SW_SPT = 4;         // partners per thread: N <= SW_TPB * SW_SPT
+constexpr int SW_MAXN = SW_TPB * SW_SPT;
+
+struct SweepParams {
+    int64_t W, N, N_up, Np, S;
+    int32_t m;
+    float invd;                   // 1/delta in fp32 (the eval kernel's)
+    double inv_delta;
+    float *R;                     // [W][3][Np] in/out
+    float *state;                 // [W][5][Np] in/out
+    const int32_t *ks;            // [S][W]
+    const float *trials;          // [S][W][2][3]
+    const double *u;              // [S][W]
+    int32_t *acc;                 // [S][W] out
+    double *dj;                   // [S][W] out (dJ2 of each move) or NULL
+    float L[3];
+    double pcoef[2 * (QJ2_MAX_M + 1)][4];
+};
+
+cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s);
+
+}  // namespace qj2

@@ -173,6 +173,20 @@ def test_metropolis_accept_host_validation(q):
     assert call(W=0) == 0
 
 
+def test_sweep_host_validation(q):
+    f = _functor(q)
+    P = ctypes.c_void_p(4096)
+
+    def call(fn=f, W=4, N=100, N_up=50, Np=128, S=3):
+        return q._lib.qj2_sweep(fn.ptr, W, N, N_up, Np, P, P, S, P, P, P, P, None, None)
+    assert call(N=1025, Np=1056) == 1            # walker must fit shared memory
+    assert call(N=1) == 1
+    assert call(Np=64) == 1
+    assert call(N_up=101) == 2
+    assert call(fn=_functor(q, m=17)) == 1       # fp32 pair terms: m <= 16
+    assert call(S=0) == 0 and call(W=0) == 0
+
+
 def test_metropolis_and_spo_host_validation(q):
     P = ctypes.c_void_p(4096)
     lib = q._lib

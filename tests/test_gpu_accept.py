@@ -316,3 +316,66 @@ def test_fused_metropolis_accept_equals_separate_calls(q, dtype):
         clear = np.abs(u[s] - rho2) > 1e-9 * rho2
         assert np.array_equal(acc_b.cpu().numpy()[clear], (u[s] < rho2)[clear].astype(np.int32))
     assert torch.equal(Ra, Rb) and torch.equal(Sa, Sb)
+
+
+# ---------------------------------------------------------------------------
+# qj2_sweep: a whole sweep in one launch, walkers resident in shared memory
+# ---------------------------------------------------------------------------
+def _sweep_inputs(N, W, seed, n_up=None):
+    L = qmcgen.cell_length(N)
+    Np = qmcgen.padded_size(N, 32)
+    R = qmcgen.positions(seed, np.arange(W), N, Np, L, np.float32)
+    fn = qmcgen.make_functor(seed, L)
+    ks, tr, u = qmcgen.make_sweep(seed, W, N, L, np.float32, N)
+    return R, fn, ks, tr, u, Np, (N // 2 if n_up is None else n_up)
+
+
+@pytest.mark.parametrize("N", [2, 33, 256, 768, 1024])
+def test_sweep_kernel_vs_oracle_sequence(q, N):
+    """One full sweep (N moves) in one qj2_sweep launch vs the oracle running
+    the same moves (its own eval -> decision -> accept); the state starts from
+    the oracle's from-scratch state."""
+    W = 12
+    R, fn, ks, tr, u, Np, n_up = _sweep_inputs(N, W, 60 + N)
+    state = np.stack([oracle.j2_state(R[w], N, n_up, fn)[0] for w in range(W)]).astype(np.float32)
+    Rd, Sd = dev(R), dev(state)
+    acc, dj = q.sweep(Rd, Sd, dev(ks), dev(tr), dev(u), fn, N, n_up)
+    acc, dj = acc.cpu().numpy(), dj.cpu().numpy()
+    Rh, Sh = R.astype(np.float64), state.astype(np.float64)
+    for s in range(N):
+        orc, _, _ = oracle.eval_j2(Rh, ks[s], tr[s], fn, N, n_up)
+        d = orc[:, 1, 0] - orc[:, 0, 0]
+        rho2 = np.exp(d) ** 2
+        a = (u[s] < rho2).astype(np.int32)
+        clear = np.abs(u[s] - rho2) > 1e-6 * rho2
+        assert np.array_equal(acc[s][clear], a[clear]), s
+        assert np.max(np.abs(dj[s] - d) / np.maximum(np.abs(orc[:, :, 0]).max(1), 1.0)) < 1e-5
+        Rh, Sh, _ = oracle.accept(Rh, Sh, ks[s], tr[s][:, 1], acc[s], fn, N, n_up)   # the GPU's decisions
+    assert np.array_equal(Rd.cpu().numpy().astype(np.float64), Rh)
+    Sg = Sd.cpu().numpy()
+    for w in range(W):
+        fresh, ab = oracle.j2_state(Rh[w], N, n_up, fn)
+        # accumulated over N updates in fp32: normalized by the from-scratch absolute sums
+        err = oracle.normalized_error_state(Sg[w][:, :N], Sh[w][:, :N], ab[:, :N], fn)
+        assert err.max() <= 1e-5, (w, err.max())
+
+
+def test_sweep_kernel_equals_per_move_kernels(q):
+    """qj2_sweep vs the per-move launches (qj2_eval + qj2_metropolis_accept):
+    the same decisions and positions, states equal to fp32 rounding."""
+    N, W = 768, 64
+    R, fn, ks, tr, u, Np, n_up = _sweep_inputs(N, W, 71)
+    Ra, Sa = dev(R), torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
+    Rb, Sb = dev(R), torch.zeros_like(Sa)
+    acc_a, _ = q.sweep(Ra, Sa, dev(ks), dev(tr), dev(u), fn, N, n_up)
+    kd, td, ud = dev(ks), dev(tr), dev(u)
+    accs = []
+    for s in range(N):
+        out = q.eval(Rb, kd[s], td[s], fn, N, n_up)
+        accs.append(q.metropolis_accept(Rb, Sb, kd[s], td[s], out, ud[s], fn, N, n_up))
+    acc_b = torch.stack(accs)
+    assert (acc_a != acc_b).sum().item() <= 2          # decisions at the rounding edge may differ
+    if torch.equal(acc_a, acc_b):
+        assert torch.equal(Ra, Rb)
+        fresh_scale = Sa.abs().max().item() + 1.0
+        assert (Sa - Sb).abs().max().item() <= 1e-5 * fresh_scale
