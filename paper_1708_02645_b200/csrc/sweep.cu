@@ -3,13 +3,11 @@
 
 namespace qj2 {
 
-__device__ __forceinline__ double sw_warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
 
-__global__ void __launch_bounds__(SW_TPB, 2) j2_sweep_kernel(const __grid_constant__ SweepParams p) {
+// SPT partners per thread (the host picks ceil(N / SW_TPB)): no wasted slots
+// at N = 768 and fewer registers for the kept terms (3 CTAs/SM up to SPT = 3).
+template <int SPT>
+__global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? 3 : 2) j2_sweep_kernel(const __grid_constant__ SweepParams p) {
     extern __shared__ __align__(16) float sw_smem[];
     const int64_t w = blockIdx.x;
     const int N = (int)p.N;
@@ -17,8 +15,6 @@ __global__ void __launch_bounds__(SW_TPB, 2) j2_sweep_kernel(const __grid_consta
     float *st = rz + N;                                              // state [5][N]
     __shared__ Coef4<float> tab[2 * (QJ2_MAX_M + 1)];
     __shared__ double red[SW_TPB / 32][10];
-    __shared__ double fin[10];
-    __shared__ int s_acc;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int e = tid; e < 2 * (p.m + 1); e += SW_TPB) {
         Coef4<float> c;
@@ -50,14 +46,14 @@ __global__ void __launch_bounds__(SW_TPB, 2) j2_sweep_kernel(const __grid_consta
         }
         const bool k_up = k < p.N_up;
         // 1. pair terms at r_k (q = 0) and r'_k (q = 1), kept per partner
-        float t[SW_SPT][2][5];
+        float t[SPT][2][5];
         float acc[2][5];
 #pragma unroll
         for (int q = 0; q < 2; ++q)
 #pragma unroll
             for (int c = 0; c < 5; ++c) acc[q][c] = 0.f;
 #pragma unroll
-        for (int j = 0; j < SW_SPT; ++j) {
+        for (int j = 0; j < SPT; ++j) {
             const int i = tid + j * SW_TPB;
             const bool live = i < N && i != k;
             const int ii = i < N ? i : 0;
@@ -81,37 +77,60 @@ __global__ void __launch_bounds__(SW_TPB, 2) j2_sweep_kernel(const __grid_consta
                 for (int c = 0; c < 5; ++c) acc[q][c] += t[j][q][c];
             }
         }
-        // 2. block reduction (fp64, fixed order)
+        // 2. block reduction in fp64, fixed order: a reduce-scatter across the
+        //    warp (16 slots, 10 used: 16 double shuffles instead of 50), one
+        //    partial per value and warp in shared memory
+        {
+            double v[16];
 #pragma unroll
-        for (int q = 0; q < 2; ++q)
+            for (int q = 0; q < 2; ++q)
 #pragma unroll
-            for (int c = 0; c < 5; ++c) {
-                const double v = sw_warp_sum((double)acc[q][c]);
-                if (lane == 0) red[warp][q * 5 + c] = v;
+                for (int c = 0; c < 5; ++c) v[q * 5 + c] = (double)acc[q][c];
+#pragma unroll
+            for (int c = 10; c < 16; ++c) v[c] = 0.0;
+#pragma unroll
+            for (int h = 8, o = 16; h >= 1; h >>= 1, o >>= 1) {
+                const bool up = lane & o;           // this lane keeps the upper half of the slots
+#pragma unroll
+                for (int j = 0; j < h; ++j) {
+                    const double send = up ? v[j] : v[j + h];
+                    const double keep = up ? v[j + h] : v[j];
+                    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
             }
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+            // lane holds slot ((lane>>4)&1)*8 + ((lane>>3)&1)*4 + ((lane>>2)&1)*2 + ((lane>>1)&1)
+            const int slot = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+            if ((lane & 1) == 0 && slot < 10) red[warp][slot] = v[0];
+        }
         __syncthreads();
-        if (tid < 10) {
-            double v = 0.0;
+        // 3. Metropolis: every thread sums V at r_k and r'_k and takes the same
+        //    decision (no second barrier); thread 0 records it
+        double V0 = 0.0, V1 = 0.0;
 #pragma unroll
-            for (int wi = 0; wi < SW_TPB / 32; ++wi) v += red[wi][tid];
-            fin[tid] = v;
+        for (int wi = 0; wi < SW_TPB / 32; ++wi) { V0 += red[wi][0]; V1 += red[wi][5]; }
+        const double djs = V1 - V0;
+        // u < exp(2 dJ2): an fp32 exp settles it unless u is within 1e-4 of the threshold (its
+        // relative error is < 2e-5 for |dJ2| < 100) or the fp32 value over/underflows; then fp64.
+        // Either way the decision equals the fp64 test.
+        const double uu = p.u[s * p.W + w];
+        const float e32 = __expf(2.f * (float)djs);
+        bool accepted;
+        if (isfinite(e32) && e32 > 1e-30f && fabs((float)uu - e32) > 1e-4f * e32 && fabs(djs) < 100.0) {
+            accepted = (float)uu < e32;
+        } else {
+            const double rho = exp(djs);
+            accepted = uu < rho * rho;
         }
-        __syncthreads();
-        // 3. Metropolis, decided once
         if (tid == 0) {
-            const double dj = fin[5] - fin[0];
-            const double rho = exp(dj);
-            const int a = p.u[s * p.W + w] < rho * rho ? 1 : 0;
-            s_acc = a;
-            p.acc[s * p.W + w] = a;
-            if (p.dj) p.dj[s * p.W + w] = dj;
+            p.acc[s * p.W + w] = accepted ? 1 : 0;
+            if (p.dj) p.dj[s * p.W + w] = djs;
         }
-        __syncthreads();
         // 4. accept: partners from the kept terms, then electron k and its position
-        if (s_acc) {
+        if (accepted) {
             const float sg = invd, sl = 2.f * invd;
 #pragma unroll
-            for (int j = 0; j < SW_SPT; ++j) {
+            for (int j = 0; j < SPT; ++j) {
                 const int i = tid + j * SW_TPB;
                 if (i < N && i != k) {
                     st[0 * N + i] += t[j][1][0] - t[j][0][0];
@@ -123,11 +142,16 @@ __global__ void __launch_bounds__(SW_TPB, 2) j2_sweep_kernel(const __grid_consta
             }
             if (tid == 0) {
                 // state_k = (V, G, L) at r'_k: G = -invd * sum g d, L = 2 invd * sum (h invd + g)
-                st[0 * N + k] = (float)fin[5];
-                st[1 * N + k] = (float)(-p.inv_delta * fin[6]);
-                st[2 * N + k] = (float)(-p.inv_delta * fin[7]);
-                st[3 * N + k] = (float)(-p.inv_delta * fin[8]);
-                st[4 * N + k] = (float)(2.0 * p.inv_delta * fin[9]);
+                double f[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int wi = 0; wi < SW_TPB / 32; ++wi)
+#pragma unroll
+                    for (int c = 0; c < 5; ++c) f[c] += red[wi][5 + c];
+                st[0 * N + k] = (float)f[0];
+                st[1 * N + k] = (float)(-p.inv_delta * f[1]);
+                st[2 * N + k] = (float)(-p.inv_delta * f[2]);
+                st[3 * N + k] = (float)(-p.inv_delta * f[3]);
+                st[4 * N + k] = (float)(2.0 * p.inv_delta * f[4]);
                 rx[k] = tr[3]; ry[k] = tr[4]; rz[k] = tr[5];
             }
         }
@@ -144,7 +168,13 @@ __global__ void __launch_bounds__(SW_TPB, 2) j2_sweep_kernel(const __grid_consta
 
 cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s) {
     const size_t smem = (size_t)8 * p.N * sizeof(float);          // R (3) + state (5) per electron
-    j2_sweep_kernel<<<(unsigned)p.W, SW_TPB, smem, s>>>(p);
+    const int spt = (int)((p.N + SW_TPB - 1) / SW_TPB);
+    switch (spt) {
+        case 1: j2_sweep_kernel<1><<<(unsigned)p.W, SW_TPB, smem, s>>>(p); break;
+        case 2: j2_sweep_kernel<2><<<(unsigned)p.W, SW_TPB, smem, s>>>(p); break;
+        case 3: j2_sweep_kernel<3><<<(unsigned)p.W, SW_TPB, smem, s>>>(p); break;
+        default: j2_sweep_kernel<4><<<(unsigned)p.W, SW_TPB, smem, s>>>(p); break;
+    }
     return cudaGetLastError();
 }
 
