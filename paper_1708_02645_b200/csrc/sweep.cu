@@ -6,15 +6,18 @@ namespace qj2 {
 
 // SPT partners per thread (the host picks ceil(N / SW_TPB)): no wasted slots
 // at N = 768 and fewer registers for the kept terms (3 CTAs/SM up to SPT = 3).
+#ifndef QJ2_SWEEP_MINB
+#define QJ2_SWEEP_MINB 4
+#endif
 template <int SPT>
-__global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? 3 : 2) j2_sweep_kernel(const __grid_constant__ SweepParams p) {
+__global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? QJ2_SWEEP_MINB : 2) j2_sweep_kernel(const __grid_constant__ SweepParams p) {
     extern __shared__ __align__(16) float sw_smem[];
     const int64_t w = blockIdx.x;
     const int N = (int)p.N;
     float *rx = sw_smem, *ry = rx + N, *rz = ry + N;                  // R (SoA)
     float *st = rz + N;                                              // state [5][N]
     __shared__ Coef4<float> tab[2 * (QJ2_MAX_M + 1)];
-    __shared__ double red[SW_TPB / 32][10];
+    __shared__ double red2[2][SW_TPB / 32][10];      // double-buffered by move parity
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int e = tid; e < 2 * (p.m + 1); e += SW_TPB) {
         Coef4<float> c;
@@ -101,11 +104,12 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? 3 : 2) j2_sweep_kernel(cons
             v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
             // lane holds slot ((lane>>4)&1)*8 + ((lane>>3)&1)*4 + ((lane>>2)&1)*2 + ((lane>>1)&1)
             const int slot = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-            if ((lane & 1) == 0 && slot < 10) red[warp][slot] = v[0];
+            if ((lane & 1) == 0 && slot < 10) red2[s & 1][warp][slot] = v[0];
         }
         __syncthreads();
         // 3. Metropolis: every thread sums V at r_k and r'_k and takes the same
         //    decision (no second barrier); thread 0 records it
+        double (*red)[10] = red2[s & 1];
         double V0 = 0.0, V1 = 0.0;
 #pragma unroll
         for (int wi = 0; wi < SW_TPB / 32; ++wi) { V0 += red[wi][0]; V1 += red[wi][5]; }
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? 3 : 2) j2_sweep_kernel(cons
                     st[4 * N + i] += (t[j][1][4] - t[j][0][4]) * sl;
                 }
             }
-            if (tid == 0) {
+            if (tid == (k & (SW_TPB - 1))) {     // the thread that owns slot k (no cross-thread writes)
                 // state_k = (V, G, L) at r'_k: G = -invd * sum g d, L = 2 invd * sum (h invd + g)
                 double f[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -155,7 +159,9 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? 3 : 2) j2_sweep_kernel(cons
                 rx[k] = tr[3]; ry[k] = tr[4]; rz[k] = tr[5];
             }
         }
-        __syncthreads();
+        // no barrier: every thread only touches its own slots of R and the state,
+        // and the partials are double-buffered (a warp writes red2[s & 1] again at
+        // move s + 2, after every thread has passed the barrier of move s + 1)
     }
     float *Rw = p.R + w * 3 * p.Np;
     float *Sw = p.state + w * 5 * p.Np;
