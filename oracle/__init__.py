@@ -7,8 +7,9 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline and
 ``--impl reference`` legs may import this package.  It shares no code with
 paper_1708_02645_b200/ and never imports it.
 
-Parity status: pinned (tests/test_oracle_pins.py); nothing is
-"parity unpinned".
+Parity status: pinned (tests/test_oracle_pins.py, test_oracle_accept.py,
+test_oracle_spo.py, test_inputs.py; mutation check in
+test_oracle_mutations.py); nothing is "parity unpinned".
 """
 from __future__ import annotations
 

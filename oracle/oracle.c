@@ -5,7 +5,10 @@
  * Mathuriya et al., "Embracing a new era of highly efficient and productive
  * quantum Monte Carlo simulations" (SC'17, arXiv 1708.02645): the on-the-fly
  * electron-electron distance row and the two-body Jastrow (J2) value,
- * gradient and Laplacian of a particle-by-particle move.
+ * gradient and Laplacian of a particle-by-particle move; and, for the NEXT
+ * rows, the one-body Jastrow over the electron-ion row, the per-electron 5N
+ * J2 state with its accept-side update, and the tricubic B-spline orbitals
+ * with the determinant ratio.
  *
  * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
  * --impl reference leg may load this library.  The product path
@@ -20,9 +23,15 @@
  * Neumaier-compensated.  Positions given in fp32 are promoted to fp64 exactly
  * by the caller.
  *
- * Parity status: every function here is pinned by tests/test_oracle_pins.py
- * (closed forms, brute force, finite differences, library B-spline, worked
- * examples).  Nothing is "parity unpinned".
+ * Parity status: every function here is pinned -- tests/test_oracle_pins.py
+ * (J2/J1 eval, functor, minimum image: closed forms, brute force, finite
+ * differences, library B-spline, worked examples), tests/test_oracle_accept.py
+ * (5N state and accept: pair-sum brute force, finite differences, state from
+ * scratch after many accepted moves), tests/test_oracle_spo.py (tricubic SPOs
+ * and determinant ratio: scipy separable splines, Marsden, LU determinants),
+ * tests/test_inputs.py (the generator twins, bitwise); and
+ * tests/test_oracle_mutations.py shows 18 plausible one-line mistakes each
+ * fail a pin.  Nothing is "parity unpinned".
  */
 #include <math.h>
 #include <stdint.h>
