@@ -17,7 +17,7 @@
  * Citations: PAPER:n is a line of /root/reference/PAPER.md, SPEC:n a line of
  * /root/reference/SPEC.md (a spec written from the paper; used for
  * interfaces and test ideas only).  Readings of the paper where it is silent
- * are numbered R1..R15 as in DESIGN.md.
+ * are numbered R1..R23 as in DESIGN.md.
  *
  * Everything is scalar fp64, IEEE round-to-nearest, no SIMD pragmas, sums are
  * Neumaier-compensated.  Positions given in fp32 are promoted to fp64 exactly
