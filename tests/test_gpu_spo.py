@@ -184,3 +184,23 @@ def test_spo_v_nlpp_points_share_the_walkers_row(q, kernel):
     assert err.max() <= TOL
     orc, aab = oracle.det_ratio(np.repeat(A, 12, axis=0), v, g, h)
     assert np.max(np.abs(out[:, 0] - orc[:, 0]) / aab[:, 0]) <= TOL
+
+
+def test_spo_S1V_full_size_sampled(q):
+    """The S1V bench workload at full size (NiO-64 table, 8192 walkers x 12 NLPP
+    points, Bspline-v + ratio) in the bench launch configuration; sampled
+    walkers' 12 points vs the oracle on its own C-generated table."""
+    cfg = qmcgen.SPO_CONFIGS["S1V"]
+    coef = q.gen_spo_table(cfg.seed, cfg.nx, cfg.ny, cfg.nz, cfg.n_orb, cfg.ld)
+    tab = q.SpoTable(coef, cfg.n_orb, cfg.L)
+    k = qmcgen.make_k(cfg.seed, cfg.W, cfg.N)
+    pts = qmcgen.make_trials(cfg.seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32, P=12, mode="nlpp")
+    A = qmcgen.make_ainv_rows(cfg.seed, cfg.W, cfg.n_orb)
+    out = q.spo_eval(tab, dev(pts), vgh=False, Ainv=dev(A), all_trials=True).cpu().numpy()
+    del coef
+    torch.cuda.empty_cache()
+    T = oracle.gen_spo_table(cfg.seed, cfg.nx, cfg.ny, cfg.nz, cfg.n_orb, cfg.ld, threads=os.cpu_count() or 1)
+    for w in (0, 4095, 8191):
+        v, g, h, _ = oracle.spo_vgh(T, cfg.n_orb, cfg.L, pts[w].astype(np.float64))
+        orc, aab = oracle.det_ratio(np.repeat(A[w:w + 1], 12, axis=0), v, g, h)
+        assert np.max(np.abs(out[w * 12:(w + 1) * 12, 0] - orc[:, 0]) / aab[:, 0]) <= TOL
