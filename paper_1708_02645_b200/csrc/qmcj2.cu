@@ -1,16 +1,22 @@
-// qmcj2.cu -- sm_100a kernels and C-ABI entry points of the J2 / distance-row
-// hot path of arXiv 1708.02645 (declared and documented in include/qmcj2.h).
+// qmcj2.cu -- C-ABI entry points (declared and documented in include/qmcj2.h)
+// and the small kernels of the J2 / distance-row hot path of arXiv 1708.02645
+// and its NEXT rows, for sm_100a.
 //
-// Kernel map:
-//   j2_eval_kernel<T, PB>   the hot path: one CTA per (walker, trial group,
-//                           source tile); SoA lanes streamed with coalesced
-//                           128-bit loads, per-term math in T, fp32 partials of
-//                           32 terms flushed to fp64, warp-shuffle + smem CTA
-//                           reduction, deterministic cross-CTA reduction by the
-//                           last CTA of each (walker, group).
-//   ratio_kernel            dJ2 and exp(dJ2) after a sharded reduction.
-//   vgl_kernel / minimg_kernel   batched building blocks.
-//   check_kernel            optional precondition scan.
+// Kernel map (one translation unit each where noted):
+//   j2_eval_kernel           the hot path (j2_kernels.cuh, launch_*.cu): one CTA
+//                            per (walker, trial, tile of 8 sub-tiles); SoA lanes
+//                            streamed with 128-bit loads, per-term math in T,
+//                            fp32 partials of 32 terms flushed to fp64, warp
+//                            shuffle + smem CTA reduction, deterministic
+//                            cross-CTA reduction by the last CTA of (walker, trial)
+//   j2_eval_warp_kernel      short rows, many walkers: one warp per (walker, trial)
+//   j1_thread_kernel         J1 over small ion sets: one thread per (walker, trial)
+//   j2_accept_kernel         NEXT-2 accept-side update (accept.cuh, launch_accept.cu),
+//                            optionally with the Metropolis test fused
+//   j2_sweep_kernel          NEXT-2 whole sweeps, walkers resident in smem (sweep.cu)
+//   spo_tma_kernel / spo_kernel   NEXT-4 Bspline-v/vgh + determinant ratio (spo.cu)
+//   ratio_kernel, metropolis_kernel, vgl_kernel, minimg_kernel, check_kernel  (here)
+//   gen_kernel, gen_spo_table kernels  synthetic inputs (gen.cu; harness)
 #include "qmcj2.h"
 #include "j2_device.cuh"
 
