@@ -409,3 +409,49 @@ def test_sweep_N64S_full_size_sampled(q):
         _, ab = oracle.j2_state(Rh[j], N, n_up, fn)
         err = oracle.normalized_error_state(Sg[j][:, :N], Sh[j][:, :N], ab[:, :N], fn)
         assert err.max() <= 1e-5, (j, err.max())
+
+
+@pytest.mark.parametrize("n_up_case", ["zero", "all", "odd"])
+def test_sweep_kernel_spin_boundaries(q, n_up_case):
+    """qj2_sweep with N_up = 0, N_up = N and an odd split: every move's ratio
+    vs the oracle replaying the sweep."""
+    N, W = 130, 6
+    n_up = {"zero": 0, "all": N, "odd": 47}[n_up_case]
+    R, fn, ks, tr, u, Np, _ = _sweep_inputs(N, W, 90 + n_up)
+    Rd, Sd = dev(R), torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
+    acc, dj = q.sweep(Rd, Sd, dev(ks), dev(tr), dev(u), fn, N, n_up)
+    acc, dj = acc.cpu().numpy(), dj.cpu().numpy()
+    Rh, Sh = R.astype(np.float64), np.zeros((W, 5, Np))
+    for s in range(N):
+        orc, _, _ = oracle.eval_j2(Rh, ks[s], tr[s], fn, N, n_up)
+        d = orc[:, 1, 0] - orc[:, 0, 0]
+        assert np.max(np.abs(dj[s] - d) / np.maximum(np.abs(orc[:, :, 0]).max(1), 1.0)) < 1e-5
+        Rh, Sh, _ = oracle.accept(Rh, Sh, ks[s], tr[s][:, 1], acc[s], fn, N, n_up)
+    assert np.array_equal(Rd.cpu().numpy().astype(np.float64), Rh)
+
+
+def test_fused_metropolis_accept_sharded_slices(q):
+    """qj2_metropolis_accept on source-axis slices (each rank's call with
+    i_offset; r_k = trial 0 replicated) equals the unsharded call."""
+    N, W = 20000, 24
+    L = qmcgen.cell_length(N)
+    fn = q.Functor.of(qmcgen.make_functor(19, L))
+    ks, tr, u = qmcgen.make_sweep(19, W, N, L, np.float32, 1)
+    R = qmcgen.positions(19, np.arange(W), N, qmcgen.padded_size(N, 4), L, np.float32)
+    Rd = dev(R)
+    S0 = torch.zeros((W, 5, R.shape[2]), dtype=torch.float32, device="cuda")
+    out = q.eval(Rd, dev(ks[0]), dev(tr[0]), fn, N, N // 2)
+    Ru, Su = Rd.clone(), S0.clone()
+    acc_u = q.metropolis_accept(Ru, Su, dev(ks[0]), dev(tr[0]), out, dev(u[0]), fn, N, N // 2)
+    bounds = [0, 7001, 13333, N]
+    Rs, Ss = [], []
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        Np = qmcgen.padded_size(b - a, 4)
+        Rl = torch.zeros((W, 3, Np), dtype=torch.float32, device="cuda")
+        Rl[:, :, :b - a] = Rd[:, :, a:b]
+        Sl = torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
+        acc = q.metropolis_accept(Rl, Sl, dev(ks[0]), dev(tr[0]), out, dev(u[0]), fn, N, N // 2, i_offset=a,
+                                  n_local=b - a)
+        assert torch.equal(acc, acc_u)
+        Rs.append(Rl[:, :, :b - a]); Ss.append(Sl[:, :, :b - a])
+    assert torch.equal(torch.cat(Rs, 2), Ru[:, :, :N]) and torch.equal(torch.cat(Ss, 2), Su[:, :, :N])
