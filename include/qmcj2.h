@@ -293,9 +293,25 @@ qj2_status qj2_metropolis_accept(const qj2_functor *fn, qj2_dtype dtype,
 /* (pair terms are kept in fp32; finer functors use qj2_eval +               */
 /* qj2_metropolis_accept).  Moves within a call are sequential per walker;   */
 /* walkers are independent.                                                  */
+/*                                                                           */
+/* Optional one-body Jastrow (j1 != NULL; NEXT-1 joined to the move): the   */
+/* ratio becomes exp(dJ1 + dJ2) (Eq. 4-5), dj holds dJ1 +   */
+/* dJ2, and on acceptance electron k's J1 state row (U^1_k, grad, lap at    */
+/* r'_k, as qj2_eval_j1 computes them) is written to j1->state.  Ions fixed */
+/* (PAPER:1306-1308), <= 256 of them, sorted by species; the J1 functor's   */
+/* cell must equal fn's.                                                     */
+typedef struct {
+    const qj2_j1_functor *fn;       /* host: per-species functors and cell   */
+    const int64_t *species_start;   /* host [n_species + 1], as qj2_eval_j1  */
+    const float *ions;              /* device [3][Np_ion] fp32               */
+    int64_t Np_ion;                 /* >= number of ions                     */
+    float *state;                   /* device [W][5][Np] fp32 (rows of accepted k written) */
+} qj2_sweep_j1;
+
 qj2_status qj2_sweep(const qj2_functor *fn, int64_t W, int64_t N, int64_t N_up, int64_t Np,
                      float *R, float *state, int64_t S, const int32_t *ks, const float *trials,
-                     const double *u, int32_t *accept, double *dj, void *stream);
+                     const double *u, int32_t *accept, double *dj, const qj2_sweep_j1 *j1,
+                     void *stream);
 
 /* ------------------------------------------------------------------------ */
 /* NEXT-4: tricubic B-spline single-particle orbitals (SPOs) and the         */

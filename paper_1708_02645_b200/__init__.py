@@ -61,6 +61,11 @@ class _SpoTable(ctypes.Structure):
                 ("coef", ctypes.c_void_p)]
 
 
+class _SweepJ1(ctypes.Structure):
+    _fields_ = [("fn", ctypes.c_void_p), ("species_start", ctypes.POINTER(ctypes.c_int64)),
+                ("ions", ctypes.c_void_p), ("Np_ion", ctypes.c_int64), ("state", ctypes.c_void_p)]
+
+
 class _J1Functor(ctypes.Structure):
     _fields_ = [("L", ctypes.c_double * 3),
                 ("n_species", ctypes.c_int32),
@@ -97,7 +102,8 @@ def _load():
         "qj2_accept": (ctypes.c_int, [F, ctypes.c_int, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp, i64, vp,
                                       vp, vp, i64, vp, sz, vp]),
         "qj2_metropolis": (ctypes.c_int, [i64, vp, i64, vp, vp, vp]),
-        "qj2_sweep": (ctypes.c_int, [F, i64, i64, i64, i64, vp, vp, i64, vp, vp, vp, vp, vp, vp]),
+        "qj2_sweep": (ctypes.c_int, [F, i64, i64, i64, i64, vp, vp, i64, vp, vp, vp, vp, vp,
+                                     ctypes.POINTER(_SweepJ1), vp]),
         "qj2_metropolis_accept": (ctypes.c_int, [F, ctypes.c_int, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, i64,
                                                  vp, vp, i64, i64, vp, vp, vp]),
         "qj2_spo_eval": (ctypes.c_int, [ctypes.POINTER(_SpoTable), i32, ctypes.c_int, i64, vp, i64, vp, i64, i64,
@@ -436,12 +442,13 @@ def metropolis_accept(R, state, k, r_trial, out, u, fn, n_total: int, n_up: int,
     return acc
 
 
-def sweep(R, state, ks, trials, u, fn, n: int, n_up: int, *, acc=None, dj=None, stream=None):
+def sweep(R, state, ks, trials, u, fn, n: int, n_up: int, *, acc=None, dj=None, j1=None, stream=None):
     """qj2_sweep: S particle-by-particle moves of every walker in one launch,
     walkers resident in shared memory (N <= 1024, fp32, functor m <= 16).
     R [W][3][Np], state [W][5][Np] fp32 (in place); ks [S][W] int32, trials
-    [S][W][2][3] fp32 (r_k, r'_k), u [S][W] fp64.  Returns (acc [S][W] int32,
-    dj [S][W] fp64)."""
+    [S][W][2][3] fp32 (r_k, r'_k), u [S][W] fp64.  j1 = (ions [3][Np_ion] fp32,
+    species_start, fn1, state_j1 [W][5][Np] fp32) adds the one-body Jastrow to
+    every move's ratio.  Returns (acc [S][W] int32, dj [S][W] fp64)."""
     _req(R, "R", torch.float32, 3)
     W, _, Np = R.shape
     _req(state, "state", torch.float32, 3)
@@ -454,8 +461,20 @@ def sweep(R, state, ks, trials, u, fn, n: int, n_up: int, *, acc=None, dj=None, 
     if dj is None:
         dj = torch.empty((S, W), dtype=torch.float64, device=R.device)
     f = Functor.of(fn)
+    j1p = None
+    keep = []
+    if j1 is not None:
+        ions, start, fn1, state_j1 = j1
+        _req(ions, "ions", torch.float32, 2)
+        _req(state_j1, "state_j1", torch.float32, 3)
+        f1 = J1Functor.of(fn1)
+        st = (ctypes.c_int64 * (len(f1.m) + 1))(*[int(x) for x in start])
+        s1 = _SweepJ1(ctypes.addressof(f1._c), st, ions.data_ptr(), ions.shape[1], state_j1.data_ptr())
+        keep = [f1, st, s1]
+        j1p = ctypes.byref(s1)
     _check(_lib.qj2_sweep(f.ptr, W, n, n_up, Np, _ptr(R), _ptr(state), S, _ptr(ks), _ptr(trials), _ptr(u),
-                          _ptr(acc), _ptr(dj), ctypes.c_void_p(_stream_ptr(stream))), "qj2_sweep")
+                          _ptr(acc), _ptr(dj), j1p, ctypes.c_void_p(_stream_ptr(stream))), "qj2_sweep")
+    del keep
     return acc, dj
 
 

@@ -615,7 +615,8 @@ qj2_status qj2_metropolis_accept(const qj2_functor *fn, qj2_dtype dtype,
 
 qj2_status qj2_sweep(const qj2_functor *fn, int64_t W, int64_t N, int64_t N_up, int64_t Np,
                      float *R, float *state, int64_t S, const int32_t *ks, const float *trials,
-                     const double *u, int32_t *accept, double *dj, void *stream) {
+                     const double *u, int32_t *accept, double *dj, const qj2_sweep_j1 *j1,
+                     void *stream) {
     qj2_status st = validate_functor(fn);
     if (st) return st;
     if (fn->m > ACCEPT_FAST_MAX_M)
@@ -627,9 +628,25 @@ qj2_status qj2_sweep(const qj2_functor *fn, int64_t W, int64_t N, int64_t N_up, 
     if (N_up < 0 || N_up > N) return fail(QJ2_ERANGE, "N_up out of [0, N]");
     if (Np < N) return fail(QJ2_EINVAL, "Np must be >= N");
     if (W > 0x7fffffffLL) return fail(QJ2_EINVAL, "W too large for one launch");
+    int64_t n_ions = 0;
+    if (j1) {
+        st = validate_j1_functor(j1->fn);
+        if (st) return st;
+        for (int d = 0; d < 3; ++d)
+            if (j1->fn->L[d] != fn->L[d]) return fail(QJ2_EINVAL, "the J1 and J2 functors must share the cell");
+        if (!j1->species_start || j1->species_start[0] != 0)
+            return fail(QJ2_EINVAL, "j1->species_start must be non-NULL with species_start[0] == 0");
+        for (int sp = 0; sp < j1->fn->n_species; ++sp)
+            if (j1->species_start[sp + 1] < j1->species_start[sp])
+                return fail(QJ2_EINVAL, "j1->species_start must be nondecreasing");
+        n_ions = j1->species_start[j1->fn->n_species];
+        if (n_ions < 1 || n_ions > SW_MAX_IONS) return fail(QJ2_EINVAL, "qj2_sweep takes 1..%d ions", SW_MAX_IONS);
+        if (j1->Np_ion < n_ions) return fail(QJ2_EINVAL, "j1->Np_ion must be >= the number of ions");
+    }
     if (W == 0 || S == 0) return QJ2_OK;
     if (!R || !state || !ks || !trials || !u || !accept)
         return fail(QJ2_EINVAL, "R, state, ks, trials, u and accept must be non-NULL");
+    if (j1 && (!j1->ions || !j1->state)) return fail(QJ2_EINVAL, "j1->ions and j1->state must be non-NULL");
     st = check_device();
     if (st) return st;
     SweepParams p;
@@ -642,6 +659,21 @@ qj2_status qj2_sweep(const qj2_functor *fn, int64_t W, int64_t N, int64_t N_up, 
     for (int d = 0; d < 3; ++d) p.L[d] = (float)fn->L[d];
     power_basis(fn->coef[0], fn->m, p.pcoef);
     power_basis(fn->coef[1], fn->m, p.pcoef + (fn->m + 1));
+    if (j1) {
+        p.n_ions = (int32_t)n_ions;
+        p.n_species = j1->fn->n_species;
+        int row = 0;
+        for (int sp = 0; sp <= QJ2_MAX_SPECIES; ++sp)
+            p.sp_start[sp] = (int32_t)(sp <= p.n_species ? j1->species_start[sp] : n_ions);
+        for (int sp = 0; sp < p.n_species; ++sp) {
+            p.sp_tab[sp] = row;
+            p.sp_m[sp] = j1->fn->m[sp];
+            p.sp_invd[sp] = (float)((double)j1->fn->m[sp] / j1->fn->r_cut[sp]);
+            power_basis(j1->fn->coef[sp], j1->fn->m[sp], p.pcoef1 + row);
+            row += j1->fn->m[sp] + 1;
+        }
+        p.ions = j1->ions; p.Np_ion = j1->Np_ion; p.state_j1 = j1->state;
+    }
     cudaError_t e = launch_sweep(p, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? QJ2_OK : cuda_fail(e, "j2_sweep_kernel launch");
 }

@@ -9,21 +9,38 @@ namespace qj2 {
 #ifndef QJ2_SWEEP_MINB
 #define QJ2_SWEEP_MINB 4
 #endif
-template <int SPT>
-__global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? QJ2_SWEEP_MINB : 2) j2_sweep_kernel(const __grid_constant__ SweepParams p) {
+// J1: the one-body Jastrow over the (<= 256) ions joins each move's ratio.
+template <int SPT, bool J1>
+__global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? (J1 ? 3 : QJ2_SWEEP_MINB) : 2) j2_sweep_kernel(const __grid_constant__ SweepParams p) {
+    constexpr int NV = J1 ? 20 : 10;          // reduced values per move: J2 (and J1) at r_k, r'_k
     extern __shared__ __align__(16) float sw_smem[];
     const int64_t w = blockIdx.x;
     const int N = (int)p.N;
     float *rx = sw_smem, *ry = rx + N, *rz = ry + N;                  // R (SoA)
     float *st = rz + N;                                              // state [5][N]
     __shared__ Coef4<float> tab[2 * (QJ2_MAX_M + 1)];
-    __shared__ double red2[2][SW_TPB / 32][10];      // double-buffered by move parity
+    __shared__ double red2[2][SW_TPB / 32][NV];      // double-buffered by move parity
+    __shared__ Coef4<float> tab1[J1 ? QJ2_MAX_SPECIES * (QJ2_MAX_M + 1) : 1];
+    __shared__ float ion_s[J1 ? 3 : 1][J1 ? SW_MAX_IONS : 1];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int e = tid; e < 2 * (p.m + 1); e += SW_TPB) {
         Coef4<float> c;
         c.a0 = (float)p.pcoef[e][0]; c.a1 = (float)p.pcoef[e][1];
         c.a2 = (float)p.pcoef[e][2]; c.a3 = (float)p.pcoef[e][3];
         tab[e] = c;
+    }
+    if constexpr (J1) {
+        for (int e = tid; e < QJ2_MAX_SPECIES * (QJ2_MAX_M + 1); e += SW_TPB) {
+            Coef4<float> c;
+            c.a0 = (float)p.pcoef1[e][0]; c.a1 = (float)p.pcoef1[e][1];
+            c.a2 = (float)p.pcoef1[e][2]; c.a3 = (float)p.pcoef1[e][3];
+            tab1[e] = c;
+        }
+        if (tid < p.n_ions) {
+            ion_s[0][tid] = p.ions[tid];
+            ion_s[1][tid] = p.ions[p.Np_ion + tid];
+            ion_s[2][tid] = p.ions[2 * p.Np_ion + tid];
+        }
     }
     const float *Rg = p.R + w * 3 * p.Np;
     const float *Sg = p.state + w * 5 * p.Np;
@@ -80,19 +97,56 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? QJ2_SWEEP_MINB : 2) j2_swee
                 for (int c = 0; c < 5; ++c) acc[q][c] += t[j][q][c];
             }
         }
+        // 1b. J1: thread tid takes ion tid at both positions, in physical units
+        //     (species differ in delta): V, G = -U' d/r, L = U'' + 2U'/r
+        float a1c[2][5];
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int c = 0; c < 5; ++c) a1c[q][c] = 0.f;
+        if constexpr (J1) {
+            if (tid < p.n_ions) {
+                int sp = 0;
+#pragma unroll
+                for (int b = 1; b < QJ2_MAX_SPECIES; ++b) sp += (b < p.n_species && tid >= p.sp_start[b]) ? 1 : 0;
+                const uint32_t base1 = (uint32_t)__cvta_generic_to_shared(tab1) +
+                                       (uint32_t)(p.sp_tab[sp] * (int)sizeof(Coef4<float>));
+                const float iv = p.sp_invd[sp];
+                const float x = ion_s[0][tid], y = ion_s[1][tid], z = ion_s[2][tid];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const Axis<float>(&a)[3] = q ? a1 : a0;
+                    const float dx = min_image(x, a[0]), dy = min_image(y, a[1]), dz = min_image(z, a[2]);
+                    const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                    const float ir = Traits<float>::rsqrt(r2);
+                    const FunctorEval<float> e = functor_from_t<float>(r2 * ir * iv, base1, (unsigned)p.sp_m[sp]);
+                    const float g = e.du * ir * iv;           // U'/r
+                    a1c[q][0] = e.u;
+                    a1c[q][1] = -g * dx;
+                    a1c[q][2] = -g * dy;
+                    a1c[q][3] = -g * dz;
+                    a1c[q][4] = 2.f * (e.h * iv * iv + g);    // U'' + 2U'/r
+                }
+            }
+        }
         // 2. block reduction in fp64, fixed order: a reduce-scatter across the
-        //    warp (16 slots, 10 used: 16 double shuffles instead of 50), one
-        //    partial per value and warp in shared memory
+        //    warp (16 or 32 slots for 10 or 20 values: one double shuffle per
+        //    slot instead of five per value), one partial per value and warp in
+        //    shared memory
         {
-            double v[16];
+            constexpr int NS = J1 ? 32 : 16;
+            double v[NS];
 #pragma unroll
             for (int q = 0; q < 2; ++q)
 #pragma unroll
-                for (int c = 0; c < 5; ++c) v[q * 5 + c] = (double)acc[q][c];
+                for (int c = 0; c < 5; ++c) {
+                    v[q * 5 + c] = (double)acc[q][c];
+                    if (J1) v[10 + q * 5 + c] = (double)a1c[q][c];
+                }
 #pragma unroll
-            for (int c = 10; c < 16; ++c) v[c] = 0.0;
+            for (int c = NV; c < NS; ++c) v[c] = 0.0;
 #pragma unroll
-            for (int h = 8, o = 16; h >= 1; h >>= 1, o >>= 1) {
+            for (int h = NS / 2, o = 16; h >= 1 && o >= 1; h >>= 1, o >>= 1) {
                 const bool up = lane & o;           // this lane keeps the upper half of the slots
 #pragma unroll
                 for (int j = 0; j < h; ++j) {
@@ -101,18 +155,28 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? QJ2_SWEEP_MINB : 2) j2_swee
                     v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                 }
             }
-            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-            // lane holds slot ((lane>>4)&1)*8 + ((lane>>3)&1)*4 + ((lane>>2)&1)*2 + ((lane>>1)&1)
-            const int slot = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-            if ((lane & 1) == 0 && slot < 10) red2[s & 1][warp][slot] = v[0];
+            int slot;
+            if constexpr (J1) {
+                slot = lane;                        // 32 slots: five levels leave one slot per lane
+            } else {
+                v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+                // lane holds slot ((lane>>4)&1)*8 + ((lane>>3)&1)*4 + ((lane>>2)&1)*2 + ((lane>>1)&1)
+                slot = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+                if (lane & 1) slot = NV;            // the pair partner holds the same sum
+            }
+            if (slot < NV) red2[s & 1][warp][slot] = v[0];
         }
         __syncthreads();
         // 3. Metropolis: every thread sums V at r_k and r'_k and takes the same
         //    decision (no second barrier); thread 0 records it
-        double (*red)[10] = red2[s & 1];
+        double (*red)[NV] = red2[s & 1];
         double V0 = 0.0, V1 = 0.0;
 #pragma unroll
-        for (int wi = 0; wi < SW_TPB / 32; ++wi) { V0 += red[wi][0]; V1 += red[wi][5]; }
+        for (int wi = 0; wi < SW_TPB / 32; ++wi) {
+            V0 += red[wi][0];
+            V1 += red[wi][5];
+            if (J1) { V0 += red[wi][10]; V1 += red[wi][15]; }      // dJ = dJ2 + dJ1 (Eq. 4-5)
+        }
         const double djs = V1 - V0;
         // u < exp(2 dJ2): an fp32 exp settles it unless u is within 1e-4 of the threshold (its
         // relative error is < 2e-5 for |dJ2| < 100) or the fp32 value over/underflows; then fp64.
@@ -157,6 +221,16 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? QJ2_SWEEP_MINB : 2) j2_swee
                 st[3 * N + k] = (float)(-p.inv_delta * f[3]);
                 st[4 * N + k] = (float)(2.0 * p.inv_delta * f[4]);
                 rx[k] = tr[3]; ry[k] = tr[4]; rz[k] = tr[5];
+                if constexpr (J1) {                  // electron k's J1 state: U^1_k and derivatives at r'_k
+                    double f1[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                    for (int wi = 0; wi < SW_TPB / 32; ++wi)
+#pragma unroll
+                        for (int c = 0; c < 5; ++c) f1[c] += red[wi][15 + c];
+                    float *S1 = p.state_j1 + w * 5 * p.Np;
+#pragma unroll
+                    for (int c = 0; c < 5; ++c) S1[c * p.Np + k] = (float)f1[c];
+                }
             }
         }
         // no barrier: every thread only touches its own slots of R and the state,
@@ -175,12 +249,17 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? QJ2_SWEEP_MINB : 2) j2_swee
 cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s) {
     const size_t smem = (size_t)8 * p.N * sizeof(float);          // R (3) + state (5) per electron
     const int spt = (int)((p.N + SW_TPB - 1) / SW_TPB);
+    const bool j1 = p.n_ions > 0;
+#define QJ2_SWEEP_LAUNCH(S_)                                                            \
+    (j1 ? (j2_sweep_kernel<S_, true><<<(unsigned)p.W, SW_TPB, smem, s>>>(p), 0)          \
+        : (j2_sweep_kernel<S_, false><<<(unsigned)p.W, SW_TPB, smem, s>>>(p), 0))
     switch (spt) {
-        case 1: j2_sweep_kernel<1><<<(unsigned)p.W, SW_TPB, smem, s>>>(p); break;
-        case 2: j2_sweep_kernel<2><<<(unsigned)p.W, SW_TPB, smem, s>>>(p); break;
-        case 3: j2_sweep_kernel<3><<<(unsigned)p.W, SW_TPB, smem, s>>>(p); break;
-        default: j2_sweep_kernel<4><<<(unsigned)p.W, SW_TPB, smem, s>>>(p); break;
+        case 1: QJ2_SWEEP_LAUNCH(1); break;
+        case 2: QJ2_SWEEP_LAUNCH(2); break;
+        case 3: QJ2_SWEEP_LAUNCH(3); break;
+        default: QJ2_SWEEP_LAUNCH(4); break;
     }
+#undef QJ2_SWEEP_LAUNCH
     return cudaGetLastError();
 }
 

@@ -43,7 +43,20 @@ struct SweepParams {
     double *dj;                   // [S][W] out (dJ2 of each move) or NULL
     float L[3];
     double pcoef[2 * (QJ2_MAX_M + 1)][4];
+    // optional one-body Jastrow over the electron-ion row (NEXT-1): the move's
+    // ratio becomes exp(dJ1 + dJ2); the ions are fixed (one per thread)
+    int32_t n_ions, n_species;
+    int32_t sp_start[QJ2_MAX_SPECIES + 1];   // ions sorted by species
+    int32_t sp_tab[QJ2_MAX_SPECIES];         // first row of species s in pcoef1
+    int32_t sp_m[QJ2_MAX_SPECIES];
+    float sp_invd[QJ2_MAX_SPECIES];
+    const float *ions;                       // [3][Np_ion]
+    int64_t Np_ion;
+    float *state_j1;                         // [W][5][Np]: electron e's U^1_e, grad, lap (k's row on acceptance)
+    double pcoef1[QJ2_MAX_SPECIES * (QJ2_MAX_M + 1)][4];
 };
+
+constexpr int SW_MAX_IONS = SW_TPB;      // one ion per thread in the J1 part of a move
 
 cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s);
 

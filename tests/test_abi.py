@@ -178,7 +178,7 @@ def test_sweep_host_validation(q):
     P = ctypes.c_void_p(4096)
 
     def call(fn=f, W=4, N=100, N_up=50, Np=128, S=3):
-        return q._lib.qj2_sweep(fn.ptr, W, N, N_up, Np, P, P, S, P, P, P, P, None, None)
+        return q._lib.qj2_sweep(fn.ptr, W, N, N_up, Np, P, P, S, P, P, P, P, None, None, None)
     assert call(N=1025, Np=1056) == 1            # walker must fit shared memory
     assert call(N=1) == 1
     assert call(Np=64) == 1

@@ -455,3 +455,39 @@ def test_fused_metropolis_accept_sharded_slices(q):
         assert torch.equal(acc, acc_u)
         Rs.append(Rl[:, :, :b - a]); Ss.append(Sl[:, :, :b - a])
     assert torch.equal(torch.cat(Rs, 2), Ru[:, :, :N]) and torch.equal(torch.cat(Ss, 2), Su[:, :, :N])
+
+
+@pytest.mark.parametrize("n_ions,S", [(64, 2), (37, 3), (256, 1)])
+def test_sweep_kernel_with_j1_vs_oracle(q, n_ions, S):
+    """qj2_sweep with the one-body Jastrow joined to every move: dJ = dJ2 + dJ1
+    per move vs the oracle (eval_j2 + eval_j1 at r_k and r'_k), the decisions,
+    positions, J2 state, and the J1 state rows of accepted electrons (= the J1
+    values at their new positions)."""
+    N, W = 200, 8
+    R, fn, ks, tr, u, Np, n_up = _sweep_inputs(N, W, 300 + n_ions)
+    L = fn.L[0]
+    ions, start = qmcgen.make_ions(300 + n_ions, n_ions, qmcgen.padded_size(n_ions, 4), L, np.float32,
+                                   n_species=S)
+    fn1 = qmcgen.make_j1_functor(300 + n_ions, L, n_species=S, m=(8, 10, 6), rcut_frac=(0.5, 0.4, 0.3))
+    Rd, Sd = dev(R), torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
+    S1 = torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
+    acc, dj = q.sweep(Rd, Sd, dev(ks), dev(tr), dev(u), fn, N, n_up, j1=(dev(ions), start, fn1, S1))
+    acc, dj = acc.cpu().numpy(), dj.cpu().numpy()
+    Rh, Sh = R.astype(np.float64), np.zeros((W, 5, Np))
+    S1h = np.zeros((W, 5, Np))
+    for s in range(N):
+        o2, a2, _ = oracle.eval_j2(Rh, ks[s], tr[s], fn, N, n_up)
+        o1, a1 = oracle.eval_j1(ions.astype(np.float64), start, tr[s].astype(np.float64), fn1)
+        d = (o2[:, 1, 0] - o2[:, 0, 0]) + (o1[:, 1, 0] - o1[:, 0, 0])
+        scale = np.maximum(np.maximum(a2[:, :, 0].max(1), a1[:, :, 0].max(1)), 1.0)
+        assert np.max(np.abs(dj[s] - d) / scale) < 1e-5, s
+        rho2 = np.exp(d) ** 2
+        clear = np.abs(u[s] - rho2) > 1e-6 * rho2
+        assert np.array_equal(acc[s][clear], (u[s] < rho2)[clear].astype(np.int32)), s
+        Rh, Sh, _ = oracle.accept(Rh, Sh, ks[s], tr[s][:, 1], acc[s], fn, N, n_up)
+        for w in np.nonzero(acc[s])[0]:
+            S1h[w, :, ks[s][w]] = o1[w, 1]
+    assert np.array_equal(Rd.cpu().numpy().astype(np.float64), Rh)
+    err1 = oracle.normalized_error_j1(np.moveaxis(S1.cpu().numpy()[:, :, :N], 1, 2),
+                                      np.moveaxis(S1h[:, :, :N], 1, 2), np.zeros((W, N, 5)), fn1)
+    assert err1.max() <= 1e-5
