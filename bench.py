@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C3S", "C3P2", "C3P12", "S1", "S1V", "J1S", "N64S"])
+    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C3S", "C3P2", "C3P12", "S1", "S1V", "J1S", "N64S", "N64SJ"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -195,8 +195,12 @@ class OracleSample:
         import oracle
         import qmcgen
         self.cfg, self.n, self.threads = cfg, int(n_walkers), threads
-        self.sweep = cfg.name in ("C3S", "N64S")
-        self.moves = cfg.N if cfg.name == "N64S" else 1       # N64S: one full sweep per step
+        self.sweep = cfg.name in ("C3S", "N64S", "N64SJ")
+        self.moves = cfg.N if cfg.name in ("N64S", "N64SJ") else 1   # N64S(J): one full sweep per step
+        self.j1 = None
+        if cfg.name == "N64SJ":
+            ions, start = qmcgen.make_ions(cfg.seed, 64, 64, cfg.L, np.float32, n_species=2)
+            self.j1 = (ions.astype(np.float64), start, qmcgen.make_j1_functor(cfg.seed, cfg.L, n_species=2))
         if self.sweep:
             self.n = min(self.n, self.MAX_SWEEP_WALKERS)
             ks, tr, u = qmcgen.make_sweep(cfg.seed, cfg.W, cfg.N, cfg.L, cfg.np_dtype, self.moves)
@@ -214,7 +218,7 @@ class OracleSample:
         self.R = oracle.gen_positions(cfg.seed, 0, self.n, cfg.N, cfg.Np, cfg.L, cfg.np_dtype, threads)
         # items in the bench's unit: (walker, trial, partner) terms; the sweep configs count one per
         # (move, partner) like their GPU lines
-        self.items = self.n * (self.moves if self.sweep else self.P) * (cfg.N - 1)
+        self.items = self.n * (self.moves if self.sweep else self.P) * (cfg.N - 1 + (64 if self.j1 else 0))
 
     def run(self):
         import oracle
@@ -225,7 +229,11 @@ class OracleSample:
         for m in range(self.moves):
             k, rt, u = self.ks[m], self.trs[m], self.us[m]
             out, _, _ = oracle.eval_j2(self.R, k, rt, self.fn, self.cfg.N, self.cfg.n_up, threads=self.threads)
-            acc = (u < np.exp(out[:, 1, 0] - out[:, 0, 0]) ** 2).astype(np.int32)
+            d = out[:, 1, 0] - out[:, 0, 0]
+            if self.j1 is not None:
+                o1, _ = oracle.eval_j1(self.j1[0], self.j1[1], rt.astype(np.float64), self.j1[2])
+                d = d + (o1[:, 1, 0] - o1[:, 0, 0])
+            acc = (u < np.exp(d) ** 2).astype(np.int32)
             self.R, self.S, _ = oracle.accept(self.R, self.S, k, rt[:, 1], acc, self.fn, self.cfg.N, self.cfg.n_up)
         return time.perf_counter() - t0
 
@@ -315,8 +323,9 @@ def _what(cfg):
         return f"Bspline-vgh of {cfg.n_orb} orbitals + determinant ratio, {cfg.nx}x{cfg.ny}x{cfg.nz} grid"
     if cfg.name == "C3S":
         return "eval P=2 + Metropolis + accept update"
-    if cfg.name == "N64S":
-        return f"one sweep of {cfg.N} moves: eval P=2 + Metropolis + accept update"
+    if cfg.name in ("N64S", "N64SJ"):
+        return (f"one sweep of {cfg.N} moves: eval P=2 + Metropolis + accept update"
+                + (" + J1 over 64 ions" if cfg.name == "N64SJ" else ""))
     P, mode = qmcgen.trial_spec(cfg.name)
     return f"P={P} {mode}" if P > 1 else "P=1"
 
@@ -406,6 +415,8 @@ def workload_config(cfg, world):
                 f"variant (U^2_k at r_k and r'_k in one step, ratio fused)",
         "C3P12": f"C3P12 (NEXT-3): C3 instance per rank (N={cfg.N} x W={cfg.W}, fp32, seed 2(+rank)), P=12 NLPP "
                  f"virtual moves (icosahedral quadrature sphere about a nearby ion point), ratios vs V_cur",
+        "N64SJ": f"N64SJ: as N64S with the one-body Jastrow over NiO-64's 64 ions (Ni, O) joined to every move's "
+                 f"ratio (dJ1 + dJ2) and state, one qj2_sweep launch per sweep",
         "N64S": f"N64S: the paper's NiO-64 size (N={cfg.N} electrons, Table 1) x W={cfg.W} walkers, fp32: one full "
                 f"particle-by-particle sweep per step ({cfg.N} moves: eval at (r_k, r'_k) -> Metropolis -> accept "
                 f"of R and the 5N state) in one qj2_sweep launch",
@@ -413,7 +424,7 @@ def workload_config(cfg, world):
                f"one PbyP move per walker: eval at (r_k, r'_k) -> Metropolis -> accept-side update of R and "
                f"the 5N fp32 J2 state",
     }[name]
-    return {"workload": desc, "N": cfg.N, "W": cfg.W, "P": {"C3S": 2, "C3P2": 2, "C3P12": 12, "N64S": 2}.get(name, 1), "m": cfg.m, "Np": cfg.Np,
+    return {"workload": desc, "N": cfg.N, "W": cfg.W, "P": {"C3S": 2, "C3P2": 2, "C3P12": 12, "N64S": 2, "N64SJ": 2}.get(name, 1), "m": cfg.m, "Np": cfg.Np,
             "parallelism": f"{'walker-instance' if name != 'C5' else 'source-axis'} x{world}",
             "l2": "inputs > 126 MB L2 (no flush needed)"}
 
@@ -842,11 +853,15 @@ class GraphSweepPlan(SweepPlan):
     mode = "N64S"
     OPS_PER_PAIR = 36 * 2               # functor terms at r_k and r'_k per partner (reused by the update)
 
+    N_IONS = 64                         # NiO-64 (Table 1): 64 ions of 2 species
+
     def __init__(self, cfg, rank, world):
         super().__init__(cfg, rank, world)
+        self.mode = cfg.name
+        self.with_j1 = cfg.name == "N64SJ"
         self.S = cfg.N
         self.launches_per_step = 1
-        self.items_per_step = self.S * cfg.W * (cfg.N - 1)
+        self.items_per_step = self.S * cfg.W * (cfg.N - 1 + (self.N_IONS if self.with_j1 else 0))
 
     def prepare(self, q, n_steps=None):
         import torch
@@ -854,6 +869,14 @@ class GraphSweepPlan(SweepPlan):
         self.q = q
         self.acc_all = torch.empty((self.S, self.cfg.W), dtype=torch.int32, device="cuda")
         self.dj_all = torch.empty((self.S, self.cfg.W), dtype=torch.float64, device="cuda")
+        self.j1 = None
+        if self.with_j1:
+            import qmcgen
+            cfg = self.cfg
+            ions, start = qmcgen.make_ions(cfg.seed, self.N_IONS, self.N_IONS, cfg.L, np.float32, n_species=2)
+            fn1 = q.J1Functor.of(qmcgen.make_j1_functor(cfg.seed, cfg.L, n_species=2))
+            self.j1 = (torch.from_numpy(ions).cuda(), start, fn1,
+                       torch.zeros((cfg.W, 5, cfg.Np), dtype=torch.float32, device="cuda"))
         # context: the same sweep as per-move launches, eager and as one CUDA graph
         for _ in range(2):
             self._per_move(q)
@@ -886,7 +909,7 @@ class GraphSweepPlan(SweepPlan):
 
     def step(self, q, dist_mod):
         q.sweep(self.R, self.S_, self.ks, self.tr, self.u, self.fn, self.cfg.N, self.cfg.n_up, acc=self.acc_all,
-                dj=self.dj_all)
+                dj=self.dj_all, j1=self.j1)
 
     @property
     def alg_bytes_per_launch(self):
@@ -898,12 +921,13 @@ class GraphSweepPlan(SweepPlan):
 
     def roofline(self, kms, peak_hbm):
         cfg = self.cfg
-        ops = self.S * cfg.W * (cfg.N - 1) * self.OPS_PER_PAIR
+        ops = self.S * cfg.W * (cfg.N - 1 + (self.N_IONS if self.with_j1 else 0)) * self.OPS_PER_PAIR
         peak = 148 * 128 * 1.965e9 / 1e12
         achieved = ops / (kms / 1e3) / 1e12
         return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": committed_traffic(self.mode),
-                "kernel": "j2_sweep_kernel (one launch per sweep, walkers resident in shared memory)",
+                "kernel": "j2_sweep_kernel (one launch per sweep, walkers resident in shared memory"
+                          + (", J1 over 64 ions in every move)" if self.with_j1 else ")"),
                 "kernel_ms": kms, "alg_ops_per_launch": ops, "ops_per_pair": self.OPS_PER_PAIR,
                 "per_move_launches_eager_ms": self.eager_ms, "per_move_launches_graph_ms": self.graph_ms,
                 "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1.965 GHz (DESIGN.md section 7)"}
@@ -1048,7 +1072,7 @@ class J1Plan:
 
 
 def make_plan(cfg, rank, world):
-    if cfg.name == "N64S":
+    if cfg.name in ("N64S", "N64SJ"):
         return GraphSweepPlan(cfg, rank, world)
     if cfg.name.startswith("J"):
         return J1Plan(cfg, rank, world)
@@ -1085,7 +1109,7 @@ def run_ours(args):
     cfg = qmcgen.config(args.config)
 
     plan = make_plan(cfg, rank, world)
-    if plan.mode == "N64S":
+    if plan.mode in ("N64S", "N64SJ"):
         plan.prepare(q)                               # one sweep's pre-drawn moves
     elif plan.mode == "C3S":                          # pre-drawn sweep inputs for every step
         plan.prepare(q, args.warmup + 2 * args.steps + 2)
@@ -1148,7 +1172,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "weak" if plan.mode in ("C3", "C3S", "C3P2", "C3P12", "S1", "S1V", "J1S", "N64S") else "strong",
+            "scaling": "weak" if plan.mode in ("C3", "C3S", "C3P2", "C3P12", "S1", "S1V", "J1S", "N64S", "N64SJ") else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(cfg, world),
             "roofline": (plan.roofline(kms, peak) if hasattr(plan, "roofline") else

@@ -435,6 +435,8 @@ CONFIGS = {
     # the paper's own NiO-64 size (Table 1: N = 768) and population (1024 walkers): one full
     # particle-by-particle sweep (768 moves per walker) as one CUDA graph
     "N64S": Config("N64S", N=768, W=1024, dtype="f32", seed=14),
+    # the same sweep with the one-body Jastrow over NiO-64's 64 ions (Ni, O) in every move's ratio
+    "N64SJ": Config("N64SJ", N=768, W=1024, dtype="f32", seed=14),
 }
 
 
