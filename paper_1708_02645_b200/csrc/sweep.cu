@@ -1,50 +1,57 @@
 // sweep.cu -- the resident-walker sweep kernel's launch (own translation unit).
+#include <cstdlib>
+
 #include "sweep.cuh"
 
 namespace qj2 {
 
 
-// SPT partners per thread (the host picks ceil(N / SW_TPB)): no wasted slots
-// at N = 768 and fewer registers for the kept terms (3 CTAs/SM up to SPT = 3).
-#ifndef QJ2_SWEEP_MINB
-#define QJ2_SWEEP_MINB 4
-#endif
+// TPB threads per walker, SPT partners per thread (the host picks
+// ceil(N / TPB)). Only the differences T_i(r'_k) - T_i(r_k) are kept (5 floats
+// per partner), so 128 threads x 6 partners fit 64 registers: 8 CTAs/SM, every
+// NiO-64 walker of a 1024-walker population resident in one wave.
 // J1: the one-body Jastrow over the (<= 256) ions joins each move's ratio.
-template <int SPT, bool J1>
-__global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? (J1 ? 3 : QJ2_SWEEP_MINB) : 2) j2_sweep_kernel(const __grid_constant__ SweepParams p) {
+template <int TPB, int SPT, bool J1>
+constexpr int sweep_minb() {
+    return TPB == 128 ? (SPT <= 6 ? 8 : 4) : (SPT <= 3 ? (J1 ? 3 : 4) : 2);
+}
+
+template <int TPB, int SPT, bool J1>
+__global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kernel(const __grid_constant__ SweepParams p) {
     constexpr int NV = J1 ? 20 : 10;          // reduced values per move: J2 (and J1) at r_k, r'_k
+    constexpr int NW = TPB / 32;
     extern __shared__ __align__(16) float sw_smem[];
     const int64_t w = blockIdx.x;
     const int N = (int)p.N;
     float *rx = sw_smem, *ry = rx + N, *rz = ry + N;                  // R (SoA)
     float *st = rz + N;                                              // state [5][N]
     __shared__ Coef4<float> tab[2 * (QJ2_MAX_M + 1)];
-    __shared__ double red2[2][SW_TPB / 32][NV];      // double-buffered by move parity
+    __shared__ double red2[2][NW][NV];               // double-buffered by move parity
     __shared__ Coef4<float> tab1[J1 ? QJ2_MAX_SPECIES * (QJ2_MAX_M + 1) : 1];
     __shared__ float ion_s[J1 ? 3 : 1][J1 ? SW_MAX_IONS : 1];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int e = tid; e < 2 * (p.m + 1); e += SW_TPB) {
+    for (int e = tid; e < 2 * (p.m + 1); e += TPB) {
         Coef4<float> c;
         c.a0 = (float)p.pcoef[e][0]; c.a1 = (float)p.pcoef[e][1];
         c.a2 = (float)p.pcoef[e][2]; c.a3 = (float)p.pcoef[e][3];
         tab[e] = c;
     }
     if constexpr (J1) {
-        for (int e = tid; e < QJ2_MAX_SPECIES * (QJ2_MAX_M + 1); e += SW_TPB) {
+        for (int e = tid; e < QJ2_MAX_SPECIES * (QJ2_MAX_M + 1); e += TPB) {
             Coef4<float> c;
             c.a0 = (float)p.pcoef1[e][0]; c.a1 = (float)p.pcoef1[e][1];
             c.a2 = (float)p.pcoef1[e][2]; c.a3 = (float)p.pcoef1[e][3];
             tab1[e] = c;
         }
-        if (tid < p.n_ions) {
-            ion_s[0][tid] = p.ions[tid];
-            ion_s[1][tid] = p.ions[p.Np_ion + tid];
-            ion_s[2][tid] = p.ions[2 * p.Np_ion + tid];
+        for (int j = tid; j < p.n_ions; j += TPB) {
+            ion_s[0][j] = p.ions[j];
+            ion_s[1][j] = p.ions[p.Np_ion + j];
+            ion_s[2][j] = p.ions[2 * p.Np_ion + j];
         }
     }
     const float *Rg = p.R + w * 3 * p.Np;
     const float *Sg = p.state + w * 5 * p.Np;
-    for (int i = tid; i < N; i += SW_TPB) {
+    for (int i = tid; i < N; i += TPB) {
         rx[i] = Rg[i]; ry[i] = Rg[p.Np + i]; rz[i] = Rg[2 * p.Np + i];
 #pragma unroll
         for (int c = 0; c < 5; ++c) st[c * N + i] = Sg[c * p.Np + i];
@@ -65,8 +72,8 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? (J1 ? 3 : QJ2_SWEEP_MINB) :
             a1[d] = make_axis<float>(tr[3 + d], p.L[d]);
         }
         const bool k_up = k < p.N_up;
-        // 1. pair terms at r_k (q = 0) and r'_k (q = 1), kept per partner
-        float t[SPT][2][5];
+        // 1. pair terms at r_k (q = 0) and r'_k (q = 1); their difference is kept per partner
+        float d[SPT][5];
         float acc[2][5];
 #pragma unroll
         for (int q = 0; q < 2; ++q)
@@ -74,11 +81,12 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? (J1 ? 3 : QJ2_SWEEP_MINB) :
             for (int c = 0; c < 5; ++c) acc[q][c] = 0.f;
 #pragma unroll
         for (int j = 0; j < SPT; ++j) {
-            const int i = tid + j * SW_TPB;
+            const int i = tid + j * TPB;
             const bool live = i < N && i != k;
             const int ii = i < N ? i : 0;
             const float x = rx[ii], y = ry[ii], z = rz[ii];
             const uint32_t base = ((ii < p.N_up) == k_up) ? tab0 : tab_opp;
+            float t[2][5];
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 const Axis<float>(&a)[3] = q ? a1 : a0;
@@ -88,16 +96,18 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? (J1 ? 3 : QJ2_SWEEP_MINB) :
                 const float ir = Traits<float>::rsqrt(r2);
                 const FunctorEval<float> e = functor_from_t<float>(r2 * ir * invd, base, clamp);
                 const float g = e.du * ir;         // U' delta / r
-                t[j][q][0] = e.u;
-                t[j][q][1] = g * dx;
-                t[j][q][2] = g * dy;
-                t[j][q][3] = g * dz;
-                t[j][q][4] = fmaf(e.h, invd, g);   // (U'' + 2U'/r) * delta / 2
+                t[q][0] = e.u;
+                t[q][1] = g * dx;
+                t[q][2] = g * dy;
+                t[q][3] = g * dz;
+                t[q][4] = fmaf(e.h, invd, g);   // (U'' + 2U'/r) * delta / 2
 #pragma unroll
-                for (int c = 0; c < 5; ++c) acc[q][c] += t[j][q][c];
+                for (int c = 0; c < 5; ++c) acc[q][c] += t[q][c];
             }
+#pragma unroll
+            for (int c = 0; c < 5; ++c) d[j][c] = t[1][c] - t[0][c];
         }
-        // 1b. J1: thread tid takes ion tid at both positions, in physical units
+        // 1b. J1: thread tid takes ions tid, tid + TPB at both positions, in physical units
         //     (species differ in delta): V, G = -U' d/r, L = U'' + 2U'/r
         float a1c[2][5];
 #pragma unroll
@@ -105,14 +115,16 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? (J1 ? 3 : QJ2_SWEEP_MINB) :
 #pragma unroll
             for (int c = 0; c < 5; ++c) a1c[q][c] = 0.f;
         if constexpr (J1) {
-            if (tid < p.n_ions) {
+#pragma unroll
+            for (int ion = tid; ion < SW_MAX_IONS; ion += TPB) {
+                if (ion >= p.n_ions) break;
                 int sp = 0;
 #pragma unroll
-                for (int b = 1; b < QJ2_MAX_SPECIES; ++b) sp += (b < p.n_species && tid >= p.sp_start[b]) ? 1 : 0;
+                for (int b = 1; b < QJ2_MAX_SPECIES; ++b) sp += (b < p.n_species && ion >= p.sp_start[b]) ? 1 : 0;
                 const uint32_t base1 = (uint32_t)__cvta_generic_to_shared(tab1) +
                                        (uint32_t)(p.sp_tab[sp] * (int)sizeof(Coef4<float>));
                 const float iv = p.sp_invd[sp];
-                const float x = ion_s[0][tid], y = ion_s[1][tid], z = ion_s[2][tid];
+                const float x = ion_s[0][ion], y = ion_s[1][ion], z = ion_s[2][ion];
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
                     const Axis<float>(&a)[3] = q ? a1 : a0;
@@ -121,11 +133,11 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? (J1 ? 3 : QJ2_SWEEP_MINB) :
                     const float ir = Traits<float>::rsqrt(r2);
                     const FunctorEval<float> e = functor_from_t<float>(r2 * ir * iv, base1, (unsigned)p.sp_m[sp]);
                     const float g = e.du * ir * iv;           // U'/r
-                    a1c[q][0] = e.u;
-                    a1c[q][1] = -g * dx;
-                    a1c[q][2] = -g * dy;
-                    a1c[q][3] = -g * dz;
-                    a1c[q][4] = 2.f * (e.h * iv * iv + g);    // U'' + 2U'/r
+                    a1c[q][0] += e.u;
+                    a1c[q][1] += -g * dx;
+                    a1c[q][2] += -g * dy;
+                    a1c[q][3] += -g * dz;
+                    a1c[q][4] += 2.f * (e.h * iv * iv + g);    // U'' + 2U'/r
                 }
             }
         }
@@ -172,7 +184,7 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? (J1 ? 3 : QJ2_SWEEP_MINB) :
         double (*red)[NV] = red2[s & 1];
         double V0 = 0.0, V1 = 0.0;
 #pragma unroll
-        for (int wi = 0; wi < SW_TPB / 32; ++wi) {
+        for (int wi = 0; wi < NW; ++wi) {
             V0 += red[wi][0];
             V1 += red[wi][5];
             if (J1) { V0 += red[wi][10]; V1 += red[wi][15]; }      // dJ = dJ2 + dJ1 (Eq. 4-5)
@@ -199,20 +211,20 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? (J1 ? 3 : QJ2_SWEEP_MINB) :
             const float sg = invd, sl = 2.f * invd;
 #pragma unroll
             for (int j = 0; j < SPT; ++j) {
-                const int i = tid + j * SW_TPB;
+                const int i = tid + j * TPB;
                 if (i < N && i != k) {
-                    st[0 * N + i] += t[j][1][0] - t[j][0][0];
-                    st[1 * N + i] += (t[j][1][1] - t[j][0][1]) * sg;
-                    st[2 * N + i] += (t[j][1][2] - t[j][0][2]) * sg;
-                    st[3 * N + i] += (t[j][1][3] - t[j][0][3]) * sg;
-                    st[4 * N + i] += (t[j][1][4] - t[j][0][4]) * sl;
+                    st[0 * N + i] += d[j][0];
+                    st[1 * N + i] += d[j][1] * sg;
+                    st[2 * N + i] += d[j][2] * sg;
+                    st[3 * N + i] += d[j][3] * sg;
+                    st[4 * N + i] += d[j][4] * sl;
                 }
             }
-            if (tid == (k & (SW_TPB - 1))) {     // the thread that owns slot k (no cross-thread writes)
+            if (tid == (k & (TPB - 1))) {     // the thread that owns slot k (no cross-thread writes)
                 // state_k = (V, G, L) at r'_k: G = -invd * sum g d, L = 2 invd * sum (h invd + g)
                 double f[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-                for (int wi = 0; wi < SW_TPB / 32; ++wi)
+                for (int wi = 0; wi < NW; ++wi)
 #pragma unroll
                     for (int c = 0; c < 5; ++c) f[c] += red[wi][5 + c];
                 st[0 * N + k] = (float)f[0];
@@ -224,7 +236,7 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? (J1 ? 3 : QJ2_SWEEP_MINB) :
                 if constexpr (J1) {                  // electron k's J1 state: U^1_k and derivatives at r'_k
                     double f1[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-                    for (int wi = 0; wi < SW_TPB / 32; ++wi)
+                    for (int wi = 0; wi < NW; ++wi)
 #pragma unroll
                         for (int c = 0; c < 5; ++c) f1[c] += red[wi][15 + c];
                     float *S1 = p.state_j1 + w * 5 * p.Np;
@@ -239,7 +251,7 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? (J1 ? 3 : QJ2_SWEEP_MINB) :
     }
     float *Rw = p.R + w * 3 * p.Np;
     float *Sw = p.state + w * 5 * p.Np;
-    for (int i = tid; i < N; i += SW_TPB) {
+    for (int i = tid; i < N; i += TPB) {
         Rw[i] = rx[i]; Rw[p.Np + i] = ry[i]; Rw[2 * p.Np + i] = rz[i];
 #pragma unroll
         for (int c = 0; c < 5; ++c) Sw[c * p.Np + i] = st[c * N + i];
@@ -248,16 +260,27 @@ __global__ void __launch_bounds__(SW_TPB, SPT <= 3 ? (J1 ? 3 : QJ2_SWEEP_MINB) :
 
 cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s) {
     const size_t smem = (size_t)8 * p.N * sizeof(float);          // R (3) + state (5) per electron
-    const int spt = (int)((p.N + SW_TPB - 1) / SW_TPB);
     const bool j1 = p.n_ions > 0;
-#define QJ2_SWEEP_LAUNCH(S_)                                                            \
-    (j1 ? (j2_sweep_kernel<S_, true><<<(unsigned)p.W, SW_TPB, smem, s>>>(p), 0)          \
-        : (j2_sweep_kernel<S_, false><<<(unsigned)p.W, SW_TPB, smem, s>>>(p), 0))
-    switch (spt) {
-        case 1: QJ2_SWEEP_LAUNCH(1); break;
-        case 2: QJ2_SWEEP_LAUNCH(2); break;
-        case 3: QJ2_SWEEP_LAUNCH(3); break;
-        default: QJ2_SWEEP_LAUNCH(4); break;
+    // 128 threads per walker for 384 < N <= 768 (8 CTAs/SM), else 256
+    int tpb = (p.N > 384 && p.N <= 768) ? 128 : SW_TPB;
+    if (const char *e = getenv("QJ2_SWEEP_TPB")) tpb = atoi(e) == 128 && p.N <= 768 ? 128 : SW_TPB;   // A/B
+    const int spt = (int)((p.N + tpb - 1) / tpb);
+#define QJ2_SWEEP_LAUNCH(T_, S_)                                                            \
+    (j1 ? (j2_sweep_kernel<T_, S_, true><<<(unsigned)p.W, T_, smem, s>>>(p), 0)              \
+        : (j2_sweep_kernel<T_, S_, false><<<(unsigned)p.W, T_, smem, s>>>(p), 0))
+    if (tpb == 128) {
+        switch (spt) {
+            case 1: case 2: case 3: case 4: QJ2_SWEEP_LAUNCH(128, 4); break;
+            case 5: QJ2_SWEEP_LAUNCH(128, 5); break;
+            default: QJ2_SWEEP_LAUNCH(128, 6); break;
+        }
+    } else {
+        switch (spt) {
+            case 1: QJ2_SWEEP_LAUNCH(256, 1); break;
+            case 2: QJ2_SWEEP_LAUNCH(256, 2); break;
+            case 3: QJ2_SWEEP_LAUNCH(256, 3); break;
+            default: QJ2_SWEEP_LAUNCH(256, 4); break;
+        }
     }
 #undef QJ2_SWEEP_LAUNCH
     return cudaGetLastError();
