@@ -141,25 +141,40 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
                 }
             }
         }
-        // 2. block reduction in fp64, fixed order: a reduce-scatter across the
+        // 2. block reduction, fixed order: a reduce-scatter across the
         //    warp (16 or 32 slots for 10 or 20 values: one double shuffle per
         //    slot instead of five per value), one partial per value and warp in
         //    shared memory
         {
             constexpr int NS = J1 ? 32 : 16;
-            double v[NS];
+            // levels 1-2 (lanes 16 and 8 apart) in fp32: partials of <= 4 lanes x 6
+            // terms (the eval kernel's fp32 partials of <= 32 terms), then fp64
+            float vf[NS];
 #pragma unroll
             for (int q = 0; q < 2; ++q)
 #pragma unroll
                 for (int c = 0; c < 5; ++c) {
-                    v[q * 5 + c] = (double)acc[q][c];
-                    if (J1) v[10 + q * 5 + c] = (double)a1c[q][c];
+                    vf[q * 5 + c] = acc[q][c];
+                    if (J1) vf[10 + q * 5 + c] = a1c[q][c];
                 }
 #pragma unroll
-            for (int c = NV; c < NS; ++c) v[c] = 0.0;
+            for (int c = NV; c < NS; ++c) vf[c] = 0.f;
 #pragma unroll
-            for (int h = NS / 2, o = 16; h >= 1 && o >= 1; h >>= 1, o >>= 1) {
+            for (int h = NS / 2, o = 16; o >= 8; h >>= 1, o >>= 1) {
                 const bool up = lane & o;           // this lane keeps the upper half of the slots
+#pragma unroll
+                for (int j = 0; j < h; ++j) {
+                    const float send = up ? vf[j] : vf[j + h];
+                    const float keep = up ? vf[j + h] : vf[j];
+                    vf[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+            }
+            double v[NS / 4];
+#pragma unroll
+            for (int j = 0; j < NS / 4; ++j) v[j] = (double)vf[j];
+#pragma unroll
+            for (int h = NS / 8, o = 4; h >= 1 && o >= 1; h >>= 1, o >>= 1) {
+                const bool up = lane & o;
 #pragma unroll
                 for (int j = 0; j < h; ++j) {
                     const double send = up ? v[j] : v[j + h];
