@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
                     st[4 * N + i] += d[j][4] * sl;
                 }
             }
-            if (tid == (k & (TPB - 1))) {     // the thread that owns slot k (no cross-thread writes)
+            if (tid == k % TPB) {     // the thread that owns slot k (no cross-thread writes)
                 // state_k = (V, G, L) at r'_k: G = -invd * sum g d, L = 2 invd * sum (h invd + g)
                 double f[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -276,7 +276,8 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
 cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s) {
     const size_t smem = (size_t)8 * p.N * sizeof(float);          // R (3) + state (5) per electron
     const bool j1 = p.n_ions > 0;
-    // 128 threads per walker for 384 < N <= 768 (8 CTAs/SM), else 256
+    // 128 threads per walker for 384 < N <= 768 (8 CTAs/SM), else 256 (64 and 96
+    // threads per walker were measured too: profiles/r01_s4/ab_tpb.log)
     int tpb = (p.N > 384 && p.N <= 768) ? 128 : SW_TPB;
     if (const char *e = getenv("QJ2_SWEEP_TPB")) tpb = atoi(e) == 128 && p.N <= 768 ? 128 : SW_TPB;   // A/B
     const int spt = (int)((p.N + tpb - 1) / tpb);
