@@ -18,7 +18,7 @@ constexpr int sweep_minb() {
 
 template <int TPB, int SPT, bool J1>
 __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kernel(const __grid_constant__ SweepParams p) {
-    constexpr int NV = J1 ? 20 : 10;          // reduced values per move: J2 (and J1) at r_k, r'_k
+    constexpr int NV = J1 ? 12 : 6;           // reduced values per move: dJ and the terms at r'_k (J2, J1)
     constexpr int NW = TPB / 32;
     extern __shared__ __align__(16) float sw_smem[];
     const int64_t w = blockIdx.x;
@@ -72,13 +72,13 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
             a1[d] = make_axis<float>(tr[3 + d], p.L[d]);
         }
         const bool k_up = k < p.N_up;
-        // 1. pair terms at r_k (q = 0) and r'_k (q = 1); their difference is kept per partner
+        // 1. pair terms at r_k (q = 0) and r'_k (q = 1): their differences are kept per
+        //    partner (the update), summed over partners only where a move needs the sum:
+        //    dv = sum_i U(r'_k) - U(r_k) (dJ2) and acc = the terms at r'_k (state_k)
         float d[SPT][5];
-        float acc[2][5];
+        float dv = 0.f, acc[5];
 #pragma unroll
-        for (int q = 0; q < 2; ++q)
-#pragma unroll
-            for (int c = 0; c < 5; ++c) acc[q][c] = 0.f;
+        for (int c = 0; c < 5; ++c) acc[c] = 0.f;
 #pragma unroll
         for (int j = 0; j < SPT; ++j) {
             const int i = tid + j * TPB;
@@ -101,19 +101,20 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
                 t[q][2] = g * dy;
                 t[q][3] = g * dz;
                 t[q][4] = fmaf(e.h, invd, g);   // (U'' + 2U'/r) * delta / 2
-#pragma unroll
-                for (int c = 0; c < 5; ++c) acc[q][c] += t[q][c];
             }
 #pragma unroll
-            for (int c = 0; c < 5; ++c) d[j][c] = t[1][c] - t[0][c];
+            for (int c = 0; c < 5; ++c) {
+                d[j][c] = t[1][c] - t[0][c];
+                acc[c] += t[1][c];
+            }
+            dv += d[j][0];
         }
         // 1b. J1: thread tid takes ions tid, tid + TPB at both positions, in physical units
-        //     (species differ in delta): V, G = -U' d/r, L = U'' + 2U'/r
-        float a1c[2][5];
+        //     (species differ in delta): dv1 = sum U(r'_k) - U(r_k); at r'_k V, G = -U' d/r,
+        //     L = U'' + 2U'/r (electron k's J1 state on acceptance)
+        float dv1 = 0.f, a1c[5];
 #pragma unroll
-        for (int q = 0; q < 2; ++q)
-#pragma unroll
-            for (int c = 0; c < 5; ++c) a1c[q][c] = 0.f;
+        for (int c = 0; c < 5; ++c) a1c[c] = 0.f;
         if constexpr (J1) {
 #pragma unroll
             for (int ion = tid; ion < SW_MAX_IONS; ion += TPB) {
@@ -125,6 +126,7 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
                                        (uint32_t)(p.sp_tab[sp] * (int)sizeof(Coef4<float>));
                 const float iv = p.sp_invd[sp];
                 const float x = ion_s[0][ion], y = ion_s[1][ion], z = ion_s[2][ion];
+                float u0 = 0.f;
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
                     const Axis<float>(&a)[3] = q ? a1 : a0;
@@ -132,33 +134,39 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
                     const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
                     const float ir = Traits<float>::rsqrt(r2);
                     const FunctorEval<float> e = functor_from_t<float>(r2 * ir * iv, base1, (unsigned)p.sp_m[sp]);
-                    const float g = e.du * ir * iv;           // U'/r
-                    a1c[q][0] += e.u;
-                    a1c[q][1] += -g * dx;
-                    a1c[q][2] += -g * dy;
-                    a1c[q][3] += -g * dz;
-                    a1c[q][4] += 2.f * (e.h * iv * iv + g);    // U'' + 2U'/r
+                    if (q == 0) {
+                        u0 = e.u;
+                    } else {
+                        const float g = e.du * ir * iv;           // U'/r
+                        dv1 += e.u - u0;
+                        a1c[0] += e.u;
+                        a1c[1] += -g * dx;
+                        a1c[2] += -g * dy;
+                        a1c[3] += -g * dz;
+                        a1c[4] += 2.f * (e.h * iv * iv + g);    // U'' + 2U'/r
+                    }
                 }
             }
         }
-        // 2. block reduction, fixed order: a reduce-scatter across the
-        //    warp (16 or 32 slots for 10 or 20 values: one double shuffle per
-        //    slot instead of five per value), one partial per value and warp in
-        //    shared memory
+        // 2. block reduction, fixed order: a reduce-scatter across the warp (8 or 16
+        //    slots for 6 or 12 values: one shuffle per slot and level instead of five
+        //    per value), one partial per value and warp in shared memory. Levels 1-2
+        //    (lanes 16 and 8 apart) add in fp32 -- partials of <= 4 lanes x 6 terms, the
+        //    eval kernel's fp32 partials of <= 32 terms -- the rest in fp64.
         {
-            constexpr int NS = J1 ? 32 : 16;
-            // levels 1-2 (lanes 16 and 8 apart) in fp32: partials of <= 4 lanes x 6
-            // terms (the eval kernel's fp32 partials of <= 32 terms), then fp64
+            constexpr int NS = J1 ? 16 : 8;
+            constexpr int OREM = J1 ? 1 : 2;        // lanes below this distance hold copies of one slot
             float vf[NS];
+            vf[0] = dv;
 #pragma unroll
-            for (int q = 0; q < 2; ++q)
-#pragma unroll
-                for (int c = 0; c < 5; ++c) {
-                    vf[q * 5 + c] = acc[q][c];
-                    if (J1) vf[10 + q * 5 + c] = a1c[q][c];
-                }
+            for (int c = 0; c < 5; ++c) {
+                vf[1 + c] = acc[c];
+                if (J1) vf[7 + c] = a1c[c];
+            }
+            if (J1) vf[6] = dv1;
 #pragma unroll
             for (int c = NV; c < NS; ++c) vf[c] = 0.f;
+            int slot = 0;
 #pragma unroll
             for (int h = NS / 2, o = 16; o >= 8; h >>= 1, o >>= 1) {
                 const bool up = lane & o;           // this lane keeps the upper half of the slots
@@ -168,12 +176,13 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
                     const float keep = up ? vf[j + h] : vf[j];
                     vf[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                 }
+                slot += up ? h : 0;
             }
             double v[NS / 4];
 #pragma unroll
             for (int j = 0; j < NS / 4; ++j) v[j] = (double)vf[j];
 #pragma unroll
-            for (int h = NS / 8, o = 4; h >= 1 && o >= 1; h >>= 1, o >>= 1) {
+            for (int h = NS / 8, o = 4; h >= 1; h >>= 1, o >>= 1) {
                 const bool up = lane & o;
 #pragma unroll
                 for (int j = 0; j < h; ++j) {
@@ -181,30 +190,22 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
                     const double keep = up ? v[j + h] : v[j];
                     v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                 }
+                slot += up ? h : 0;
             }
-            int slot;
-            if constexpr (J1) {
-                slot = lane;                        // 32 slots: five levels leave one slot per lane
-            } else {
-                v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-                // lane holds slot ((lane>>4)&1)*8 + ((lane>>3)&1)*4 + ((lane>>2)&1)*2 + ((lane>>1)&1)
-                slot = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-                if (lane & 1) slot = NV;            // the pair partner holds the same sum
-            }
-            if (slot < NV) red2[s & 1][warp][slot] = v[0];
+#pragma unroll
+            for (int o = OREM; o >= 1; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+            if ((lane & (2 * OREM - 1)) == 0 && slot < NV) red2[s & 1][warp][slot] = v[0];
         }
         __syncthreads();
-        // 3. Metropolis: every thread sums V at r_k and r'_k and takes the same
-        //    decision (no second barrier); thread 0 records it
+        // 3. Metropolis: every thread sums dJ and takes the same decision (no second
+        //    barrier); thread 0 records it
         double (*red)[NV] = red2[s & 1];
-        double V0 = 0.0, V1 = 0.0;
+        double djs = 0.0;
 #pragma unroll
         for (int wi = 0; wi < NW; ++wi) {
-            V0 += red[wi][0];
-            V1 += red[wi][5];
-            if (J1) { V0 += red[wi][10]; V1 += red[wi][15]; }      // dJ = dJ2 + dJ1 (Eq. 4-5)
+            djs += red[wi][0];
+            if (J1) djs += red[wi][6];              // dJ = dJ2 + dJ1 (Eq. 4-5)
         }
-        const double djs = V1 - V0;
         // u < exp(2 dJ2): an fp32 exp settles it unless u is within 1e-4 of the threshold (its
         // relative error is < 2e-5 for |dJ2| < 100) or the fp32 value over/underflows; then fp64.
         // Either way the decision equals the fp64 test.
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
 #pragma unroll
                 for (int wi = 0; wi < NW; ++wi)
 #pragma unroll
-                    for (int c = 0; c < 5; ++c) f[c] += red[wi][5 + c];
+                    for (int c = 0; c < 5; ++c) f[c] += red[wi][1 + c];
                 st[0 * N + k] = (float)f[0];
                 st[1 * N + k] = (float)(-p.inv_delta * f[1]);
                 st[2 * N + k] = (float)(-p.inv_delta * f[2]);
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
 #pragma unroll
                     for (int wi = 0; wi < NW; ++wi)
 #pragma unroll
-                        for (int c = 0; c < 5; ++c) f1[c] += red[wi][15 + c];
+                        for (int c = 0; c < 5; ++c) f1[c] += red[wi][7 + c];
                     float *S1 = p.state_j1 + w * 5 * p.Np;
 #pragma unroll
                     for (int c = 0; c < 5; ++c) S1[c * p.Np + k] = (float)f1[c];
