@@ -75,39 +75,45 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
         // 1. pair terms at r_k (q = 0) and r'_k (q = 1): their differences are kept per
         //    partner (the update), summed over partners only where a move needs the sum:
         //    dv = sum_i U(r'_k) - U(r_k) (dJ2) and acc = the terms at r'_k (state_k)
+        // position-outer: only one position's axes are live (64 registers, no spills)
         float d[SPT][5];
         float dv = 0.f, acc[5];
 #pragma unroll
         for (int c = 0; c < 5; ++c) acc[c] = 0.f;
 #pragma unroll
-        for (int j = 0; j < SPT; ++j) {
-            const int i = tid + j * TPB;
-            const bool live = i < N && i != k;
-            const int ii = i < N ? i : 0;
-            const float x = rx[ii], y = ry[ii], z = rz[ii];
-            const uint32_t base = ((ii < p.N_up) == k_up) ? tab0 : tab_opp;
-            float t[2][5];
+        for (int q = 0; q < 2; ++q) {
+            const Axis<float>(&a)[3] = q ? a1 : a0;
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const Axis<float>(&a)[3] = q ? a1 : a0;
+            for (int j = 0; j < SPT; ++j) {
+                const int i = tid + j * TPB;
+                const bool live = i < N && i != k;
+                const int ii = i < N ? i : 0;
+                const float x = rx[ii], y = ry[ii], z = rz[ii];
+                const uint32_t base = ((ii < p.N_up) == k_up) ? tab0 : tab_opp;
                 const float dx = min_image(x, a[0]), dy = min_image(y, a[1]), dz = min_image(z, a[2]);
                 float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
                 r2 = live ? r2 : 1e30f;            // the zero row: every term exactly 0
                 const float ir = Traits<float>::rsqrt(r2);
                 const FunctorEval<float> e = functor_from_t<float>(r2 * ir * invd, base, clamp);
                 const float g = e.du * ir;         // U' delta / r
-                t[q][0] = e.u;
-                t[q][1] = g * dx;
-                t[q][2] = g * dy;
-                t[q][3] = g * dz;
-                t[q][4] = fmaf(e.h, invd, g);   // (U'' + 2U'/r) * delta / 2
-            }
+                float t[5];
+                t[0] = e.u;
+                t[1] = g * dx;
+                t[2] = g * dy;
+                t[3] = g * dz;
+                t[4] = fmaf(e.h, invd, g);      // (U'' + 2U'/r) * delta / 2
+                if (q == 0) {
 #pragma unroll
-            for (int c = 0; c < 5; ++c) {
-                d[j][c] = t[1][c] - t[0][c];
-                acc[c] += t[1][c];
+                    for (int c = 0; c < 5; ++c) d[j][c] = t[c];
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 5; ++c) {
+                        d[j][c] = t[c] - d[j][c];
+                        acc[c] += t[c];
+                    }
+                    dv += d[j][0];
+                }
             }
-            dv += d[j][0];
         }
         // 1b. J1: thread tid takes ions tid, tid + TPB at both positions, in physical units
         //     (species differ in delta): dv1 = sum U(r'_k) - U(r_k); at r'_k V, G = -U' d/r,
