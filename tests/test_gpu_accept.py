@@ -330,7 +330,7 @@ def _sweep_inputs(N, W, seed, n_up=None):
     return R, fn, ks, tr, u, Np, (N // 2 if n_up is None else n_up)
 
 
-@pytest.mark.parametrize("N", [2, 33, 256, 768, 1024])
+@pytest.mark.parametrize("N", [2, 33, 256, 385, 600, 768, 1024])      # 128 threads x 4, 5, 6 partners at 385-768
 def test_sweep_kernel_vs_oracle_sequence(q, N):
     """One full sweep (N moves) in one qj2_sweep launch vs the oracle running
     the same moves (its own eval -> decision -> accept); the state starts from
@@ -457,13 +457,14 @@ def test_fused_metropolis_accept_sharded_slices(q):
     assert torch.equal(torch.cat(Rs, 2), Ru[:, :, :N]) and torch.equal(torch.cat(Ss, 2), Su[:, :, :N])
 
 
-@pytest.mark.parametrize("n_ions,S", [(64, 2), (37, 3), (256, 1)])
-def test_sweep_kernel_with_j1_vs_oracle(q, n_ions, S):
+@pytest.mark.parametrize("n_ions,S,N", [(64, 2, 200), (37, 3, 200), (256, 1, 200), (256, 2, 520), (64, 2, 768)])
+def test_sweep_kernel_with_j1_vs_oracle(q, n_ions, S, N):
     """qj2_sweep with the one-body Jastrow joined to every move: dJ = dJ2 + dJ1
     per move vs the oracle (eval_j2 + eval_j1 at r_k and r'_k), the decisions,
     positions, J2 state, and the J1 state rows of accepted electrons (= the J1
-    values at their new positions)."""
-    N, W = 200, 8
+    values at their new positions). N = 520 and 768 run 128 threads per walker
+    (256 ions: two per thread)."""
+    W = 8
     R, fn, ks, tr, u, Np, n_up = _sweep_inputs(N, W, 300 + n_ions)
     L = fn.L[0]
     ions, start = qmcgen.make_ions(300 + n_ions, n_ions, qmcgen.padded_size(n_ions, 4), L, np.float32,
