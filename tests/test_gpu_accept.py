@@ -475,7 +475,7 @@ def test_sweep_kernel_with_j1_vs_oracle(q, n_ions, S, N):
     acc, dj = q.sweep(Rd, Sd, dev(ks), dev(tr), dev(u), fn, N, n_up, j1=(dev(ions), start, fn1, S1))
     acc, dj = acc.cpu().numpy(), dj.cpu().numpy()
     Rh, Sh = R.astype(np.float64), np.zeros((W, 5, Np))
-    S1h = np.zeros((W, 5, Np))
+    S1h, A1h = np.zeros((W, 5, Np)), np.zeros((W, 5, Np))
     for s in range(N):
         o2, a2, _ = oracle.eval_j2(Rh, ks[s], tr[s], fn, N, n_up)
         o1, a1 = oracle.eval_j1(ions.astype(np.float64), start, tr[s].astype(np.float64), fn1)
@@ -488,7 +488,9 @@ def test_sweep_kernel_with_j1_vs_oracle(q, n_ions, S, N):
         Rh, Sh, _ = oracle.accept(Rh, Sh, ks[s], tr[s][:, 1], acc[s], fn, N, n_up)
         for w in np.nonzero(acc[s])[0]:
             S1h[w, :, ks[s][w]] = o1[w, 1]
+            A1h[w, :, ks[s][w]] = a1[w, 1]
     assert np.array_equal(Rd.cpu().numpy().astype(np.float64), Rh)
+    # normalised like every J1 parity check: by the oracle's absolute sums over the ions
     err1 = oracle.normalized_error_j1(np.moveaxis(S1.cpu().numpy()[:, :, :N], 1, 2),
-                                      np.moveaxis(S1h[:, :, :N], 1, 2), np.zeros((W, N, 5)), fn1)
+                                      np.moveaxis(S1h[:, :, :N], 1, 2), np.moveaxis(A1h[:, :, :N], 1, 2), fn1)
     assert err1.max() <= 1e-5
