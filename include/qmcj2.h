@@ -292,7 +292,9 @@ qj2_status qj2_metropolis_accept(const qj2_functor *fn, qj2_dtype dtype,
 /* Requirements (else QJ2_EINVAL): 2 <= N <= 1024, Np >= N, functor m <= 16  */
 /* (pair terms are kept in fp32; finer functors use qj2_eval +               */
 /* qj2_metropolis_accept).  Moves within a call are sequential per walker;   */
-/* walkers are independent.                                                  */
+/* walkers are independent.  Preconditions (not scanned): trial coordinates  */
+/* in [0, L_d) (else the values are unspecified); a move whose k is outside  */
+/* [0, N) is never accepted (nothing is written) and its accept entry is -1. */
 /*                                                                           */
 /* Optional one-body Jastrow (j1 != NULL; NEXT-1 joined to the move): the   */
 /* ratio becomes exp(dJ1 + dJ2) (Eq. 4-5), dj holds dJ1 +   */

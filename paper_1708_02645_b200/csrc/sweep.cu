@@ -63,6 +63,8 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
     const float invd = p.invd;
 
     for (int64_t s = 0; s < p.S; ++s) {
+        // k outside [0, N) (a precondition): no partner is excluded, the move is never
+        // accepted (nothing is written) and its accept entry is -1
         const int k = p.ks[s * p.W + w];
         const float *tr = p.trials + (s * p.W + w) * 6;
         Axis<float> a0[3], a1[3];
@@ -224,8 +226,10 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
             const double rho = exp(djs);
             accepted = uu < rho * rho;
         }
+        const bool k_ok = (unsigned)k < (unsigned)N;
+        accepted = accepted && k_ok;
         if (tid == 0) {
-            p.acc[s * p.W + w] = accepted ? 1 : 0;
+            p.acc[s * p.W + w] = k_ok ? (accepted ? 1 : 0) : -1;
             if (p.dj) p.dj[s * p.W + w] = djs;
         }
         // 4. accept: partners from the kept terms, then electron k and its position

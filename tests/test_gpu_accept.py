@@ -411,6 +411,38 @@ def test_sweep_N64S_full_size_sampled(q):
         assert err.max() <= 1e-5, (j, err.max())
 
 
+def test_sweep_kernel_out_of_range_k(q):
+    """A move whose k is outside [0, N) (a precondition violation) is never
+    accepted and flagged -1; the other moves and the walker's state go on as
+    the oracle replay with those moves rejected says (memory stays intact)."""
+    for N in (130, 600):          # 256 and 128 threads per walker
+        W = 6
+        R, fn, ks, tr, u, Np, n_up = _sweep_inputs(N, W, 120 + N)
+        ks0, ks = ks, ks.copy()
+        bad = [(3, 2, -5), (7, 4, N), (11, 0, N + 1000), (12, 5, -(1 << 30))]
+        for s_, w_, k_ in bad:
+            ks[s_, w_] = k_
+        Rd, Sd = dev(R), torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
+        acc, _ = q.sweep(Rd, Sd, dev(ks), dev(tr), dev(u), fn, N, n_up)
+        acc = acc.cpu().numpy()
+        for s_, w_, _ in bad:
+            assert acc[s_, w_] == -1
+        assert set(np.unique(acc)) <= {-1, 0, 1}
+        Rh, Sh = R.astype(np.float64), np.zeros((W, 5, Np))
+        for s in range(N):
+            a = np.maximum(acc[s], 0)
+            kk = ks0[s]                  # the drawn k (its move is rejected either way)
+            orc, _, _ = oracle.eval_j2(Rh, kk, tr[s], fn, N, n_up)
+            d = orc[:, 1, 0] - orc[:, 0, 0]
+            rho2 = np.exp(d) ** 2
+            ok = acc[s] >= 0
+            clear = ok & (np.abs(u[s] - rho2) > 1e-6 * rho2)
+            assert np.array_equal(acc[s][clear], (u[s] < rho2)[clear].astype(np.int32)), s
+            Rh, Sh, _ = oracle.accept(Rh, Sh, kk, tr[s][:, 1], a, fn, N, n_up)
+        assert np.array_equal(Rd.cpu().numpy().astype(np.float64), Rh)
+        assert np.array_equal(Rd.cpu().numpy()[:, :, N:], R[:, :, N:])     # padding untouched
+
+
 @pytest.mark.parametrize("n_up_case", ["zero", "all", "odd"])
 def test_sweep_kernel_spin_boundaries(q, n_up_case):
     """qj2_sweep with N_up = 0, N_up = N and an odd split: every move's ratio
