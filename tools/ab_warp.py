@@ -19,7 +19,7 @@ fn = q.Functor.of(qmcgen.make_functor(cfg.seed, cfg.L, cfg.m))
 out = torch.empty((n_inst * cfg.W, 1, 5), dtype=torch.float64, device="cuda")
 ws = q.Workspace(0)
 gb = n_inst * cfg.W * (cfg.N - 1) * 12 / 1e9
-for v in ["default", "p3m2", "p4m2", "p3m3", "p1m4"]:
+for v in (sys.argv[1:] or ["default", "p2m3"]):
     os.environ.pop("QJ2_WARP", None)
     if v != "default":
         os.environ["QJ2_WARP"] = v
