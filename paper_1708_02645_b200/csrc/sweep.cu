@@ -11,18 +11,20 @@ namespace qj2 {
 // per partner), so 128 threads x 6 partners fit 64 registers: 8 CTAs/SM, every
 // NiO-64 walker of a 1024-walker population resident in one wave.
 // J1: the one-body Jastrow over the (<= 256) ions joins each move's ratio.
+// FULL (with J1): N == TPB * SPT (NiO-64's 768 = 128 x 6, 1024 = 256 x 4), the
+// shared-memory layout and the partner bounds are compile-time constants.
 template <int TPB, int SPT, bool J1>
 constexpr int sweep_minb() {
     return TPB == 128 ? (SPT <= 6 ? 8 : 4) : (SPT <= 3 ? (J1 ? 3 : 4) : 2);
 }
 
-template <int TPB, int SPT, bool J1>
+template <int TPB, int SPT, bool J1, bool FULL>
 __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kernel(const __grid_constant__ SweepParams p) {
     constexpr int NV = J1 ? 12 : 6;           // reduced values per move: dJ and the terms at r'_k (J2, J1)
     constexpr int NW = TPB / 32;
     extern __shared__ __align__(16) float sw_smem[];
     const int64_t w = blockIdx.x;
-    const int N = (int)p.N;
+    const int N = FULL ? TPB * SPT : (int)p.N;
     float *rx = sw_smem, *ry = rx + N, *rz = ry + N;                  // R (SoA)
     float *st = rz + N;                                              // state [5][N]
     __shared__ Coef4<float> tab[2 * (QJ2_MAX_M + 1)];
@@ -88,8 +90,8 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
 #pragma unroll
             for (int j = 0; j < SPT; ++j) {
                 const int i = tid + j * TPB;
-                const bool live = i < N && i != k;
-                const int ii = i < N ? i : 0;
+                const bool live = (FULL || i < N) && i != k;
+                const int ii = (FULL || i < N) ? i : 0;
                 const float x = rx[ii], y = ry[ii], z = rz[ii];
                 const uint32_t base = ((ii < p.N_up) == k_up) ? tab0 : tab_opp;
                 const float dx = min_image(x, a[0]), dy = min_image(y, a[1]), dz = min_image(z, a[2]);
@@ -238,7 +240,7 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
 #pragma unroll
             for (int j = 0; j < SPT; ++j) {
                 const int i = tid + j * TPB;
-                if (i < N && i != k) {
+                if ((FULL || i < N) && i != k) {
                     st[0 * N + i] += d[j][0];
                     st[1 * N + i] += d[j][1] * sg;
                     st[2 * N + i] += d[j][2] * sg;
@@ -292,24 +294,35 @@ cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s) {
     int tpb = (p.N > 384 && p.N <= 768) ? 128 : SW_TPB;
     if (const char *e = getenv("QJ2_SWEEP_TPB")) tpb = atoi(e) == 128 && p.N <= 768 ? 128 : SW_TPB;   // A/B
     const int spt = (int)((p.N + tpb - 1) / tpb);
+    // compile-time layout where N fills the threads exactly: measured with J1 (N64SJ 4.39 ->
+    // 3.98 ms); without J1 it spills (104 B) and gains nothing (N64S 3.51 vs 3.52 ms)
+    const bool full = j1 && p.N == (int64_t)tpb * spt && !getenv("QJ2_SWEEP_NOFULL");
 #define QJ2_SWEEP_LAUNCH(T_, S_)                                                            \
-    (j1 ? (j2_sweep_kernel<T_, S_, true><<<(unsigned)p.W, T_, smem, s>>>(p), 0)              \
-        : (j2_sweep_kernel<T_, S_, false><<<(unsigned)p.W, T_, smem, s>>>(p), 0))
+    (j1 ? (j2_sweep_kernel<T_, S_, true, false><<<(unsigned)p.W, T_, smem, s>>>(p), 0)       \
+        : (j2_sweep_kernel<T_, S_, false, false><<<(unsigned)p.W, T_, smem, s>>>(p), 0))
+#define QJ2_SWEEP_LAUNCH_FULL(T_, S_) (j2_sweep_kernel<T_, S_, true, true><<<(unsigned)p.W, T_, smem, s>>>(p), 0)
     if (tpb == 128) {
         switch (spt) {
             case 1: case 2: case 3: case 4: QJ2_SWEEP_LAUNCH(128, 4); break;
             case 5: QJ2_SWEEP_LAUNCH(128, 5); break;
-            default: QJ2_SWEEP_LAUNCH(128, 6); break;
+            default:
+                if (full) QJ2_SWEEP_LAUNCH_FULL(128, 6);
+                else QJ2_SWEEP_LAUNCH(128, 6);
+                break;
         }
     } else {
         switch (spt) {
             case 1: QJ2_SWEEP_LAUNCH(256, 1); break;
             case 2: QJ2_SWEEP_LAUNCH(256, 2); break;
             case 3: QJ2_SWEEP_LAUNCH(256, 3); break;
-            default: QJ2_SWEEP_LAUNCH(256, 4); break;
+            default:
+                if (full) QJ2_SWEEP_LAUNCH_FULL(256, 4);
+                else QJ2_SWEEP_LAUNCH(256, 4);
+                break;
         }
     }
 #undef QJ2_SWEEP_LAUNCH
+#undef QJ2_SWEEP_LAUNCH_FULL
     return cudaGetLastError();
 }
 

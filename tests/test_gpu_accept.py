@@ -489,13 +489,15 @@ def test_fused_metropolis_accept_sharded_slices(q):
     assert torch.equal(torch.cat(Rs, 2), Ru[:, :, :N]) and torch.equal(torch.cat(Ss, 2), Su[:, :, :N])
 
 
-@pytest.mark.parametrize("n_ions,S,N", [(64, 2, 200), (37, 3, 200), (256, 1, 200), (256, 2, 520), (64, 2, 768)])
+@pytest.mark.parametrize("n_ions,S,N", [(64, 2, 200), (37, 3, 200), (256, 1, 200), (256, 2, 520), (64, 2, 768),
+                                         (100, 2, 1024)])
 def test_sweep_kernel_with_j1_vs_oracle(q, n_ions, S, N):
     """qj2_sweep with the one-body Jastrow joined to every move: dJ = dJ2 + dJ1
     per move vs the oracle (eval_j2 + eval_j1 at r_k and r'_k), the decisions,
     positions, J2 state, and the J1 state rows of accepted electrons (= the J1
     values at their new positions). N = 520 and 768 run 128 threads per walker
-    (256 ions: two per thread)."""
+    (256 ions: two per thread); 768 and 1024 fill the threads exactly (the
+    compile-time-layout kernels)."""
     W = 8
     R, fn, ks, tr, u, Np, n_up = _sweep_inputs(N, W, 300 + n_ions)
     L = fn.L[0]
