@@ -22,6 +22,8 @@ HEADERS = [os.path.join(CSRC, f) for f in ("j2_device.cuh", "j2_kernels.cuh", "j
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
+# A/B builds only (e.g. QJ2_EXTRA_FLAGS="-DQJ2_SWEEP_MINB128=7" with build(force=True))
+NVCC_FLAGS += os.environ.get("QJ2_EXTRA_FLAGS", "").split()
 
 
 def nvcc() -> str:

@@ -11,11 +11,14 @@ namespace qj2 {
 // per partner), so 128 threads x 6 partners fit 64 registers: 8 CTAs/SM, every
 // NiO-64 walker of a 1024-walker population resident in one wave.
 // J1: the one-body Jastrow over the (<= 256) ions joins each move's ratio.
-// FULL (with J1): N == TPB * SPT (NiO-64's 768 = 128 x 6, 1024 = 256 x 4), the
-// shared-memory layout and the partner bounds are compile-time constants.
+// FULL: N == TPB * SPT (NiO-64's 768 = 128 x 6, 1024 = 256 x 4), the shared-memory
+// layout and the partner bounds are compile-time constants.
+// 128 threads per walker: 7 CTAs/SM without J1 (72 registers, no spills; 148 x 7 = 1036 walkers
+// in one wave), 8 with J1 (64 registers) -- measured: N64S 3.28 ms at 7 vs 3.52 at 8, N64SJ 3.98
+// at 8 vs 4.10 at 7 (profiles/r01_s4/ab_minb.log)
 template <int TPB, int SPT, bool J1>
 constexpr int sweep_minb() {
-    return TPB == 128 ? (SPT <= 6 ? 8 : 4) : (SPT <= 3 ? (J1 ? 3 : 4) : 2);
+    return TPB == 128 ? (SPT <= 6 ? (J1 ? 8 : 7) : 4) : (SPT <= 3 ? (J1 ? 3 : 4) : 2);
 }
 
 template <int TPB, int SPT, bool J1, bool FULL>
@@ -294,13 +297,15 @@ cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s) {
     int tpb = (p.N > 384 && p.N <= 768) ? 128 : SW_TPB;
     if (const char *e = getenv("QJ2_SWEEP_TPB")) tpb = atoi(e) == 128 && p.N <= 768 ? 128 : SW_TPB;   // A/B
     const int spt = (int)((p.N + tpb - 1) / tpb);
-    // compile-time layout where N fills the threads exactly: measured with J1 (N64SJ 4.39 ->
-    // 3.98 ms); without J1 it spills (104 B) and gains nothing (N64S 3.51 vs 3.52 ms)
-    const bool full = j1 && p.N == (int64_t)tpb * spt && !getenv("QJ2_SWEEP_NOFULL");
+    // compile-time layout where N fills the threads exactly (N64SJ 4.39 -> 3.98 ms, N64S at 7
+    // CTAs/SM 3.40 -> 3.28 ms)
+    const bool full = p.N == (int64_t)tpb * spt && !getenv("QJ2_SWEEP_NOFULL");
 #define QJ2_SWEEP_LAUNCH(T_, S_)                                                            \
     (j1 ? (j2_sweep_kernel<T_, S_, true, false><<<(unsigned)p.W, T_, smem, s>>>(p), 0)       \
         : (j2_sweep_kernel<T_, S_, false, false><<<(unsigned)p.W, T_, smem, s>>>(p), 0))
-#define QJ2_SWEEP_LAUNCH_FULL(T_, S_) (j2_sweep_kernel<T_, S_, true, true><<<(unsigned)p.W, T_, smem, s>>>(p), 0)
+#define QJ2_SWEEP_LAUNCH_FULL(T_, S_)                                                       \
+    (j1 ? (j2_sweep_kernel<T_, S_, true, true><<<(unsigned)p.W, T_, smem, s>>>(p), 0)        \
+        : (j2_sweep_kernel<T_, S_, false, true><<<(unsigned)p.W, T_, smem, s>>>(p), 0))
     if (tpb == 128) {
         switch (spt) {
             case 1: case 2: case 3: case 4: QJ2_SWEEP_LAUNCH(128, 4); break;
