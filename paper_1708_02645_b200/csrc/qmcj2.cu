@@ -672,6 +672,7 @@ qj2_status qj2_sweep(const qj2_functor *fn, int64_t W, int64_t N, int64_t N_up, 
             power_basis(j1->fn->coef[sp], j1->fn->m[sp], p.pcoef1 + row);
             row += j1->fn->m[sp] + 1;
         }
+        p.n_rows1 = row;
         p.ions = j1->ions; p.Np_ion = j1->Np_ion; p.state_j1 = j1->state;
     }
     cudaError_t e = launch_sweep(p, static_cast<cudaStream_t>(stream));

@@ -16,9 +16,12 @@ namespace qj2 {
 // 128 threads per walker: 7 CTAs/SM without J1 (72 registers, no spills; 148 x 7 = 1036 walkers
 // in one wave), 8 with J1 (64 registers) -- measured: N64S 3.28 ms at 7 vs 3.52 at 8, N64SJ 3.98
 // at 8 vs 4.10 at 7 (profiles/r01_s4/ab_minb.log)
+#ifndef QJ2_SWEEP_MINB_J1
+#define QJ2_SWEEP_MINB_J1 8
+#endif
 template <int TPB, int SPT, bool J1>
 constexpr int sweep_minb() {
-    return TPB == 128 ? (SPT <= 6 ? (J1 ? 8 : 7) : 4) : (SPT <= 3 ? (J1 ? 3 : 4) : 2);
+    return TPB == 128 ? (SPT <= 6 ? (J1 ? QJ2_SWEEP_MINB_J1 : 7) : 4) : (SPT <= 3 ? (J1 ? 3 : 4) : 2);
 }
 
 template <int TPB, int SPT, bool J1, bool FULL>
@@ -28,12 +31,14 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
     extern __shared__ __align__(16) float sw_smem[];
     const int64_t w = blockIdx.x;
     const int N = FULL ? TPB * SPT : (int)p.N;
-    float *rx = sw_smem, *ry = rx + N, *rz = ry + N;                  // R (SoA)
-    float *st = rz + N;                                              // state [5][N]
-    __shared__ Coef4<float> tab[2 * (QJ2_MAX_M + 1)];
+    // dynamic shared memory, sized by the call (every byte counts at 7-8 CTAs/SM):
+    // R (SoA) [3][N] | state [5][N] | J2 table [2(m+1)] | J1 table [n_rows1] | ions [3][n_ions]
+    float *rx = sw_smem, *ry = rx + N, *rz = ry + N;
+    float *st = rz + N;
+    Coef4<float> *tab = reinterpret_cast<Coef4<float> *>(sw_smem + 8 * N);
+    Coef4<float> *tab1 = tab + 2 * (p.m + 1);
+    float *ion_s = reinterpret_cast<float *>(tab1 + (J1 ? p.n_rows1 : 0));
     __shared__ double red2[2][NW][NV];               // double-buffered by move parity
-    __shared__ Coef4<float> tab1[J1 ? QJ2_MAX_SPECIES * (QJ2_MAX_M + 1) : 1];
-    __shared__ float ion_s[J1 ? 3 : 1][J1 ? SW_MAX_IONS : 1];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int e = tid; e < 2 * (p.m + 1); e += TPB) {
         Coef4<float> c;
@@ -42,16 +47,16 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
         tab[e] = c;
     }
     if constexpr (J1) {
-        for (int e = tid; e < QJ2_MAX_SPECIES * (QJ2_MAX_M + 1); e += TPB) {
+        for (int e = tid; e < p.n_rows1; e += TPB) {
             Coef4<float> c;
             c.a0 = (float)p.pcoef1[e][0]; c.a1 = (float)p.pcoef1[e][1];
             c.a2 = (float)p.pcoef1[e][2]; c.a3 = (float)p.pcoef1[e][3];
             tab1[e] = c;
         }
         for (int j = tid; j < p.n_ions; j += TPB) {
-            ion_s[0][j] = p.ions[j];
-            ion_s[1][j] = p.ions[p.Np_ion + j];
-            ion_s[2][j] = p.ions[2 * p.Np_ion + j];
+            ion_s[j] = p.ions[j];
+            ion_s[p.n_ions + j] = p.ions[p.Np_ion + j];
+            ion_s[2 * p.n_ions + j] = p.ions[2 * p.Np_ion + j];
         }
     }
     const float *Rg = p.R + w * 3 * p.Np;
@@ -138,7 +143,7 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
                 const uint32_t base1 = (uint32_t)__cvta_generic_to_shared(tab1) +
                                        (uint32_t)(p.sp_tab[sp] * (int)sizeof(Coef4<float>));
                 const float iv = p.sp_invd[sp];
-                const float x = ion_s[0][ion], y = ion_s[1][ion], z = ion_s[2][ion];
+                const float x = ion_s[ion], y = ion_s[p.n_ions + ion], z = ion_s[2 * p.n_ions + ion];
                 float u0 = 0.f;
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
@@ -290,8 +295,10 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
 }
 
 cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s) {
-    const size_t smem = (size_t)8 * p.N * sizeof(float);          // R (3) + state (5) per electron
     const bool j1 = p.n_ions > 0;
+    const size_t smem = (size_t)8 * p.N * sizeof(float)                       // R (3) + state (5) per electron
+                      + (size_t)(2 * (p.m + 1) + (j1 ? p.n_rows1 : 0)) * sizeof(Coef4<float>)
+                      + (j1 ? (size_t)3 * p.n_ions * sizeof(float) : 0);
     // 128 threads per walker for 384 < N <= 768 (8 CTAs/SM), else 256 (64 and 96
     // threads per walker were measured too: profiles/r01_s4/ab_tpb.log)
     int tpb = (p.N > 384 && p.N <= 768) ? 128 : SW_TPB;

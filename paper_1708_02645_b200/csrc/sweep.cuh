@@ -49,6 +49,7 @@ struct SweepParams {
     int32_t sp_start[QJ2_MAX_SPECIES + 1];   // ions sorted by species
     int32_t sp_tab[QJ2_MAX_SPECIES];         // first row of species s in pcoef1
     int32_t sp_m[QJ2_MAX_SPECIES];
+    int32_t n_rows1;                         // J1 table rows: sum over species of m_s + 1
     float sp_invd[QJ2_MAX_SPECIES];
     const float *ions;                       // [3][Np_ion]
     int64_t Np_ion;
