@@ -942,6 +942,40 @@ class GraphSweepPlan(SweepPlan):
         q.sweep(self.R, self.S_, self.ks, self.tr, self.u, self.fn, self.cfg.N, self.cfg.n_up, acc=self.acc_all,
                 dj=self.dj_all, j1=self.j1)
 
+    def e2e(self, q, steps, dist_mod):
+        """Through the public API with host buffers: each step uploads the walkers'
+        positions and 5N state (and J1 state), the sweep's moves (k, r_k, r'_k, u)
+        from pinned memory, runs qj2_sweep and reads the accept flags back (the
+        functor tables and the ions are model data, resident on the device)."""
+        import torch
+        cfg = self.cfg
+        dev = [self.R, self.S_, self.ks, self.tr, self.u] + ([self.j1[3]] if self.j1 else [])
+        host = [t.cpu().pin_memory() for t in dev]
+        dbuf = [torch.empty_like(t) for t in dev]
+        acc_h = torch.empty(tuple(self.acc_all.shape), dtype=torch.int32, pin_memory=True)
+        j1 = (self.j1[0], self.j1[1], self.j1[2], dbuf[5]) if self.j1 else None
+
+        def run():
+            for d, h in zip(dbuf, host):
+                d.copy_(h, non_blocking=True)
+            q.sweep(dbuf[0], dbuf[1], dbuf[2], dbuf[3], dbuf[4], self.fn, cfg.N, cfg.n_up, acc=self.acc_all,
+                    dj=self.dj_all, j1=j1)
+            acc_h.copy_(self.acc_all, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        run()
+        if dist_mod:
+            dist_mod.barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            run()
+        dt = allreduce_max((time.perf_counter() - t0) / steps, dist_mod)
+        world = dist_mod.get_world_size() if dist_mod else 1
+        return {"value": self.items_per_step * world / dt, "unit": UNIT,
+                "h2d_bytes_per_step": sum(h.numel() * h.element_size() for h in host),
+                "d2h_bytes_per_step": acc_h.numel() * 4, "ms_per_step": dt * 1e3, "steps": steps,
+                "api": "qj2_sweep with R, the 5N state and the sweep's moves copied from pinned host memory "
+                       "every step, accept flags read back"}
+
     @property
     def alg_bytes_per_launch(self):
         cfg = self.cfg
