@@ -1134,7 +1134,36 @@ class J1Plan:
                                "(DESIGN.md section 7)"}
 
     def e2e(self, q, steps, dist_mod):
-        return None
+        """Through the public API with host buffers: each step uploads the sweep's
+        trial points from pinned memory, runs qj2_eval_j1 (ratio fused) and reads
+        the (V, G, L) rows and ratios back (the ions are model data, resident)."""
+        import torch
+        cfg = self.cfg
+        rh = self.rt.cpu().pin_memory()
+        rd = torch.empty_like(self.rt)
+        oh = torch.empty(tuple(self.out.shape), dtype=torch.float64, pin_memory=True)
+        qh = torch.empty(tuple(self.ratio.shape), dtype=torch.float64, pin_memory=True)
+
+        def run():
+            rd.copy_(rh, non_blocking=True)
+            q.eval_j1(self.ions, self.start, rd, self.fn1, V_cur=self.V_cur, ratio=True, out=self.out,
+                      ratio_out=self.ratio)
+            oh.copy_(self.out, non_blocking=True)
+            qh.copy_(self.ratio, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        run()
+        if dist_mod:
+            dist_mod.barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            run()
+        dt = allreduce_max((time.perf_counter() - t0) / steps, dist_mod)
+        world = dist_mod.get_world_size() if dist_mod else 1
+        return {"value": self.items_per_step * world / dt, "unit": UNIT,
+                "h2d_bytes_per_step": rh.numel() * 4, "d2h_bytes_per_step": (oh.numel() + qh.numel()) * 8,
+                "ms_per_step": dt * 1e3, "steps": steps,
+                "api": "qj2_eval_j1 with the trial points copied from pinned host memory every step, (V, G, L) "
+                       "and the ratios read back"}
 
 
 def make_plan(cfg, rank, world):
