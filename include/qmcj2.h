@@ -23,6 +23,12 @@
  *   different workspaces are independent and may run concurrently.
  * - Device entry points require an sm_100 device (else QJ2_ENOTSUP).
  * - All sizes are int64; all flat offsets inside kernels are 64-bit.
+ * - Kernel variants are chosen from the arguments alone.  The QJ2_KERNEL,
+ *   QJ2_WARP, QJ2_J1_WARP, QJ2_SPO, QJ2_SPO_SMEM_KB, QJ2_SWEEP_TPB and
+ *   QJ2_SWEEP_NOFULL environment variables are A/B measurement switches
+ *   (read at each call, so a measuring process can flip them); leave them
+ *   unset in production.  Every variant they select computes the same
+ *   results within the parity bar (the GPU suite passes with each).
  */
 #ifndef QMCJ2_H
 #define QMCJ2_H
