@@ -25,9 +25,9 @@ constexpr int TPB = 256;          // threads per CTA
 #endif
 constexpr int ITERS = QJ2_ITERS;  // vector iterations per sub-tile: 32 fp32 terms per thread per trial (A/B: -DQJ2_ITERS=n)
 #ifndef QJ2_SUB
-#define QJ2_SUB 8
+#define QJ2_SUB 25
 #endif
-constexpr int SUB = QJ2_SUB;      // sub-tiles per CTA tile (A/B builds: -DQJ2_SUB=n)
+constexpr int SUB = QJ2_SUB;      // sub-tiles per CTA tile: 25 x 8192 fp32 sources (A/B builds: -DQJ2_SUB=n)
 constexpr int NACC = 6;           // fp32 accumulators per trial: V, Gx, Gy, Gz, sum h, sum du/r
 constexpr int NOUT = 5;           // fp64 physical outputs per trial: V, Gx, Gy, Gz, L
 constexpr int MAXPB = 4;

@@ -108,8 +108,9 @@ def test_workspace_size(q):
     import torch
     assert q.workspace_size(1024, 1, 1400, torch.float32) == 0            # one tile per walker
     b = q.workspace_size(1024, 1, 614400, torch.float32)
-    assert b >= 1024 * 10 * 6 * 8 + 1024 * 4                           # 10 tiles of 65536 sources, 6 fp64 partials
-    assert q.workspace_size(8, 3, 40000, torch.float64) > 0             # fp64 tiles hold 32768 sources
+    assert b >= 1024 * 3 * 6 * 8 + 1024 * 4                            # 3 tiles of 204800 sources, 6 fp64 partials
+    assert q.workspace_size(8, 3, 40000, torch.float64) == 0            # fp64 tiles hold 102400 sources
+    assert q.workspace_size(8, 3, 102401, torch.float64) > 0
 
 
 def test_package_has_no_cpu_fallback():

@@ -82,15 +82,15 @@ def test_ragged_sizes(q, dtype, N):
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 def test_k_at_tile_and_spin_boundaries(q, dtype):
-    # sub-tiles of 8192 (fp32) / 4096 (fp64) sources, CTA tiles of 4 sub-tiles
-    N = 2 * 32768 + 77
-    ks = np.array([0, 1, 4095, 4096, 8191, 8192, 8193, 16383, 32767, 32768, 32769, 65535, 65536,
-                   N - 2, N - 1, N // 2], np.int32)
+    # sub-tiles of 8192 (fp32) / 4096 (fp64) sources, CTA tiles of 25 sub-tiles (204800 / 102400)
+    N = 2 * 204800 + 77
+    ks = np.array([0, 1, 4095, 4096, 8191, 8192, 8193, 16383, 102399, 102400, 102401, 204799, 204800,
+                   204801, 307199, 307200, 409599, 409600, N - 2, N - 1, N // 2], np.int32)
     W = ks.size
     R, k, rt, fn, _ = instance(N, W, seed=7, dtype=dtype)
     L = qmcgen.cell_length(N)
     rt = qmcgen.make_trials(7, np.arange(W), ks, N, L, dtype)
-    for n_up in (N // 2, 32768, 8192, 8190, 0, N, 1):   # spin boundary inside / on a tile edge / degenerate
+    for n_up in (N // 2, 204800, 102400, 8192, 8190, 0, N, 1):   # spin boundary inside / on a tile edge / degenerate
         check(q, R, ks, rt, fn, N, n_up, dtype)
 
 
