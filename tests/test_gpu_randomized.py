@@ -1,0 +1,162 @@
+"""Randomized GPU parity (-m gpu; needs a B200): a seeded generator draws the
+shapes and arguments -- N (log-uniform over every kernel regime), W, P,
+functor grid m, spin split N_up, trial mode, a source-axis slice, dtype,
+accept mask -- and every drawn case is checked against the CPU oracle with the
+parity bar of DESIGN.md section 4 (normalized error <= 1e-5 fp32 / 1e-12 fp64;
+positions bit-exact).  The draws are fixed (seeded), so a failure names a
+reproducible case id; they complement the hand-picked edge cases of
+test_gpu_parity.py / test_gpu_accept.py (tile edges, k and N_up at
+boundaries), they do not replace them.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import qmcgen
+
+pytestmark = pytest.mark.gpu
+
+TOL = {np.float32: 1e-5, np.float64: 1e-12}
+THREADS = os.cpu_count() or 1
+
+
+def _log_uniform(rng, lo, hi):
+    return int(np.exp(rng.uniform(np.log(lo), np.log(hi + 1))))
+
+
+def _eval_cases(n=40, seed=2024):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for _ in range(n):
+        N = max(2, _log_uniform(rng, 2, 450000))
+        c = dict(N=N, W=int(rng.integers(1, 7)), P=int(rng.integers(1, 6)), m=int(rng.integers(4, 25)),
+                 f64=bool(rng.random() < 0.4), drift=bool(rng.random() < 0.5), seed=int(rng.integers(2**31)),
+                 up_frac=float(rng.choice([0.0, 1.0, rng.random(), 0.5])),
+                 slice_frac=(float(rng.random()), float(rng.random())), sharded=bool(rng.random() < 0.3))
+        cases.append(c)
+    return cases
+
+
+def _accept_cases(n=25, seed=2025):
+    rng = np.random.default_rng(seed)
+    return [dict(N=max(2, _log_uniform(rng, 2, 30000)), W=int(rng.integers(1, 9)), m=int(rng.integers(4, 65)),
+                 f64=bool(rng.random() < 0.4), seed=int(rng.integers(2**31)),
+                 up_frac=float(rng.choice([0.0, 1.0, rng.random(), 0.5])), p_acc=float(rng.random()))
+            for _ in range(n)]
+
+
+def _sweep_cases(n=12, seed=2026):
+    rng = np.random.default_rng(seed)
+    return [dict(N=max(2, _log_uniform(rng, 2, 1024)), W=int(rng.integers(1, 6)), m=int(rng.integers(4, 17)),
+                 seed=int(rng.integers(2**31)), up_frac=float(rng.choice([0.0, 1.0, rng.random(), 0.5])),
+                 moves=int(rng.integers(1, 65)))
+            for _ in range(n)]
+
+
+@pytest.fixture(scope="module")
+def q():
+    import paper_1708_02645_b200 as q
+    assert torch.cuda.is_available()
+    q.device_check()
+    return q
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+# N log-uniform over the kernels' regimes: one warp's sub-tile, several sub-tiles,
+# several CTA tiles (204800 fp32 / 102400 fp64 sources)
+@pytest.mark.parametrize("c", _eval_cases(), ids=lambda c: f"N{c['N']}-W{c['W']}-P{c['P']}-m{c['m']}"
+                         f"-{'f64' if c['f64'] else 'f32'}{'-drift' if c['drift'] else ''}{'-shard' if c['sharded'] else ''}")
+def test_eval_random(q, c):
+    N, W, P, m, f64, drift, seed = c["N"], c["W"], c["P"], c["m"], c["f64"], c["drift"], c["seed"]
+    up_frac, slice_frac, sharded = c["up_frac"], c["slice_frac"], c["sharded"]
+    dtype = np.float64 if f64 else np.float32
+    if drift and P < 2:
+        P = 2
+    L = qmcgen.cell_length(N)
+    Np = qmcgen.padded_size(N, 2 if f64 else 4)
+    R = qmcgen.positions(seed, np.arange(W), N, Np, L, dtype)
+    k = qmcgen.make_k(seed, W, N)
+    rt = qmcgen.make_trials(seed, np.arange(W), k, N, L, dtype, P=P, mode="drift" if drift else "move")
+    fn = qmcgen.make_functor(seed, L, m)
+    n_up = int(round(up_frac * N))
+    i_offset, n_local = 0, None
+    if sharded and N > 2:
+        a, b = sorted(int(f * N) for f in slice_frac)
+        a = min(a, N - 1)
+        b = max(b, a + 1)
+        i_offset, n_local = a, min(b, N) - a
+        Rs = np.zeros((W, 3, qmcgen.padded_size(n_local, 2 if f64 else 4)), dtype)
+        Rs[:, :, :n_local] = R[:, :, a:a + n_local]
+        R = Rs
+    out = q.eval(dev(R), dev(k), dev(rt), fn, N, n_up, i_offset=i_offset, n_local=n_local).cpu().numpy()
+    orc, absout, _ = oracle.eval_j2(R, k, rt, fn, N, n_up, i_offset=i_offset, n_local=n_local, threads=THREADS)
+    assert np.all(np.isfinite(out))
+    err = oracle.normalized_error(out, orc, absout, fn).max()
+    assert err <= TOL[dtype], (N, W, P, m, dtype, n_up, i_offset, n_local, err)
+
+
+@pytest.mark.parametrize("c", _accept_cases(), ids=lambda c: f"N{c['N']}-W{c['W']}-m{c['m']}-"
+                         f"{'f64' if c['f64'] else 'f32'}")
+def test_accept_random(q, c):
+    N, W, m, f64, seed, up_frac, p_acc = c["N"], c["W"], c["m"], c["f64"], c["seed"], c["up_frac"], c["p_acc"]
+    dtype = np.float64 if f64 else np.float32
+    L = qmcgen.cell_length(N)
+    Np = qmcgen.padded_size(N, 2 if f64 else 4)
+    R = qmcgen.positions(seed, np.arange(W), N, Np, L, dtype)
+    k = qmcgen.make_k(seed, W, N)
+    rt = qmcgen.make_trials(seed, np.arange(W), k, N, L, dtype)
+    fn = qmcgen.make_functor(seed, L, m)
+    rng = np.random.default_rng(seed)
+    state = rng.normal(size=(W, 5, Np)).astype(dtype)
+    state[:, :, N:] = 7.0
+    acc = (rng.random(W) < p_acc).astype(np.int32)
+    n_up = int(round(up_frac * N))
+    Rd, Sd = dev(R), dev(state)
+    out = q.eval(Rd, dev(k), dev(rt), fn, N, n_up)
+    q.accept(Rd, Sd, dev(k), dev(rt), dev(acc), out, fn, N, n_up)
+    Rg, Sg = Rd.cpu().numpy(), Sd.cpu().numpy()
+    R2, S2, ab = oracle.accept(R, state, k, rt[:, 0], acc, fn, N, n_up)
+    assert np.array_equal(Rg.astype(np.float64), R2)
+    rej = acc == 0
+    assert np.array_equal(Sg[rej], state[rej]) and np.array_equal(Sg[:, :, N:], state[:, :, N:])
+    a = ~rej
+    if a.any():
+        err = oracle.normalized_error_state(Sg[a][:, :, :N], S2[a][:, :, :N], ab[a][:, :, :N], fn).max()
+        assert err <= TOL[dtype], (N, W, m, dtype, n_up, err)
+
+
+@pytest.mark.parametrize("c", _sweep_cases(), ids=lambda c: f"N{c['N']}-W{c['W']}-m{c['m']}-S{c['moves']}")
+def test_sweep_random(q, c):
+    """qj2_sweep over a drawn number of moves vs the oracle replaying them."""
+    N, W, m, seed, up_frac, moves = c["N"], c["W"], c["m"], c["seed"], c["up_frac"], c["moves"]
+    S = min(moves, N)
+    L = qmcgen.cell_length(N)
+    Np = qmcgen.padded_size(N, 32)
+    R = qmcgen.positions(seed, np.arange(W), N, Np, L, np.float32)
+    fn = qmcgen.make_functor(seed, L, m)
+    ks, tr, u = qmcgen.make_sweep(seed, W, N, L, np.float32, S)
+    n_up = int(round(up_frac * N))
+    Rd, Sd = dev(R), torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
+    acc, dj = q.sweep(Rd, Sd, dev(ks), dev(tr), dev(u), fn, N, n_up)
+    acc, dj = acc.cpu().numpy(), dj.cpu().numpy()
+    Rh, Sh = R.astype(np.float64), np.zeros((W, 5, Np))
+    for s in range(S):
+        o, _, _ = oracle.eval_j2(Rh, ks[s], tr[s], fn, N, n_up)
+        d = o[:, 1, 0] - o[:, 0, 0]
+        assert np.max(np.abs(dj[s] - d) / np.maximum(np.abs(o[:, :, 0]).max(1), 1.0)) < 1e-5, s
+        rho2 = np.exp(d) ** 2
+        clear = np.abs(u[s] - rho2) > 1e-6 * rho2
+        assert np.array_equal(acc[s][clear], (u[s] < rho2)[clear].astype(np.int32)), s
+        Rh, Sh, _ = oracle.accept(Rh, Sh, ks[s], tr[s][:, 1], acc[s], fn, N, n_up)
+    assert np.array_equal(Rd.cpu().numpy().astype(np.float64), Rh)
+    Sg = Sd.cpu().numpy()
+    for w in range(W):
+        _, ab = oracle.j2_state(Rh[w], N, n_up, fn)
+        err = oracle.normalized_error_state(Sg[w][:, :N], Sh[w][:, :N], ab[:, :N], fn)
+        assert err.max() <= 1e-5, (N, W, m, n_up, S, w, err.max())
