@@ -314,6 +314,22 @@ def det_ratio(Ainv_rows, v, g, h):
     return out, ab
 
 
+def det_ratio_scale(Ainv_rows, ab_vgh, F):
+    """Parity scale of the determinant-ratio numerators (rho, rho G, rho L) in the
+    form of DESIGN.md section 4, max(A_s, F_s) per term: sum_o |a_o| max(ab_o, F)
+    with ab_vgh [M][10][n] the SPO absolute-term sums (spo_vgh) and F [10] the
+    table scale per component (value, 3 gradient, 6 Hessian lanes).  Without the
+    F floor a near-zero sum of |a . grad phi| (few orbitals) would leave no room
+    for the fp32 rounding of grad phi itself."""
+    A = np.abs(_f64(np.atleast_2d(Ainv_rows)))
+    m = np.maximum(_f64(ab_vgh), np.asarray(F, dtype=np.float64)[None, :, None])
+    out = np.empty((A.shape[0], 5))
+    out[:, 0] = (A * m[:, 0]).sum(-1)
+    out[:, 1:4] = (A[:, None, :] * m[:, 1:4]).sum(-1)
+    out[:, 4] = (A * (m[:, 4] + m[:, 7] + m[:, 9])).sum(-1)
+    return out
+
+
 def gen_spo_table(seed: int, nx: int, ny: int, nz: int, n_orb: int, ld: int | None = None,
                   threads: int = 1) -> np.ndarray:
     """Oracle-side C twin of qmcgen.spo_table (input generation only)."""

@@ -160,3 +160,83 @@ def test_sweep_random(q, c):
         _, ab = oracle.j2_state(Rh[w], N, n_up, fn)
         err = oracle.normalized_error_state(Sg[w][:, :N], Sh[w][:, :N], ab[:, :N], fn)
         assert err.max() <= 1e-5, (N, W, m, n_up, S, w, err.max())
+
+
+def _j1_cases(n=20, seed=2027):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        S = int(rng.integers(1, 5))
+        out.append(dict(n_ions=max(S, _log_uniform(rng, 1, 60000)), S=S, W=int(rng.integers(1, 9)),
+                        P=int(rng.integers(1, 4)), m=tuple(int(x) for x in rng.integers(4, 21, 4)),
+                        rcut=tuple(float(x) for x in rng.uniform(0.2, 0.5, 4)), f64=bool(rng.random() < 0.4),
+                        seed=int(rng.integers(2**31))))
+    return out
+
+
+@pytest.mark.parametrize("c", _j1_cases(), ids=lambda c: f"ions{c['n_ions']}-S{c['S']}-W{c['W']}-P{c['P']}-"
+                         f"{'f64' if c['f64'] else 'f32'}")
+def test_j1_random(q, c):
+    """qj2_eval_j1 (thread kernel for <= 4096 ions, the CTA/warp kernels above)."""
+    dtype = np.float64 if c["f64"] else np.float32
+    n_ions, S, W, P, seed = c["n_ions"], c["S"], c["W"], c["P"], c["seed"]
+    N = max(12 * n_ions, 64)
+    L = qmcgen.cell_length(N)
+    ions, start = qmcgen.make_ions(seed, n_ions, qmcgen.padded_size(n_ions, 2 if c["f64"] else 4), L, dtype,
+                                   n_species=S)
+    fn1 = qmcgen.make_j1_functor(seed, L, n_species=S, m=c["m"], rcut_frac=c["rcut"])
+    k = qmcgen.make_k(seed, W, N)
+    rt = qmcgen.make_trials(seed, np.arange(W), k, N, L, dtype, P=P)
+    out = q.eval_j1(dev(ions), start, dev(rt), fn1).cpu().numpy()
+    orc, absout = oracle.eval_j1(ions.astype(np.float64), start, rt.astype(np.float64), fn1)
+    assert np.all(np.isfinite(out))
+    err = oracle.normalized_error_j1(out, orc, absout, fn1).max()
+    assert err <= TOL[dtype], (n_ions, S, W, P, dtype, err)
+
+
+def _spo_cases(n=16, seed=2028):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        n_orb = max(1, _log_uniform(rng, 1, 640))
+        out.append(dict(nx=int(rng.integers(4, 25)), ny=int(rng.integers(4, 25)), nz=int(rng.integers(4, 25)),
+                        n_orb=n_orb, ld=n_orb + int(rng.integers(0, 3)) * 4 + (-n_orb) % 4,
+                        W=int(rng.integers(1, 300)), f64=bool(rng.random() < 0.3),
+                        L=tuple(float(x) for x in rng.uniform(2.0, 6.0, 3)), ldg=bool(rng.random() < 0.3),
+                        shift=float(rng.choice([0.0, rng.uniform(-6, 6)])), seed=int(rng.integers(2**31))))
+    return out
+
+
+@pytest.mark.parametrize("c", _spo_cases(), ids=lambda c: f"{c['nx']}x{c['ny']}x{c['nz']}-orb{c['n_orb']}-"
+                         f"W{c['W']}{'-ldg' if c['ldg'] else ''}{'-f64pos' if c['f64'] else ''}")
+def test_spo_random(q, c):
+    """qj2_spo_eval (vgh + determinant ratio) on a drawn grid, orbital count, row
+    pitch, cell, position precision and offset (positions outside the cell wrap)."""
+    old = os.environ.pop("QJ2_SPO", None)
+    if c["ldg"]:
+        os.environ["QJ2_SPO"] = "ldg"
+    try:
+        nx, ny, nz, n_orb, ld, W, L = c["nx"], c["ny"], c["nz"], c["n_orb"], c["ld"], c["W"], c["L"]
+        T = qmcgen.spo_table(c["seed"], nx, ny, nz, n_orb, ld)
+        tab = q.SpoTable(dev(T), n_orb, L)
+        rng = np.random.default_rng(c["seed"])
+        pos = (rng.random((W, 3)) * np.asarray(L) + c["shift"]).astype(np.float64 if c["f64"] else np.float32)
+        A = qmcgen.make_ainv_rows(c["seed"], W, n_orb)
+        out, spo = q.spo_eval(tab, dev(pos), Ainv=dev(A), want_spo=True)
+        out, spo = out.cpu().numpy(), spo.cpu().numpy()
+    finally:
+        os.environ.pop("QJ2_SPO", None)
+        if old is not None:
+            os.environ["QJ2_SPO"] = old
+    v, g, h, ab = oracle.spo_vgh(T, n_orb, L, pos.astype(np.float64))
+    ref = np.concatenate([v[:, None, :], g, h], axis=1)
+    s = np.array((nx, ny, nz), dtype=np.float64) / np.array(L)
+    Fs = np.array([1, s[0], s[1], s[2], s[0] ** 2, s[0] * s[1], s[0] * s[2], s[1] ** 2, s[1] * s[2], s[2] ** 2])
+    F = np.abs(T).max() * Fs[None, :, None]
+    assert np.all(np.isfinite(spo[:, :, :n_orb]))
+    err = (np.abs(spo[:, :, :n_orb] - ref) / np.maximum(ab, F)).max()
+    assert err <= 1e-5, err
+    orc, aab = oracle.det_ratio(A, v, g, h)
+    scale = np.maximum(aab, oracle.det_ratio_scale(A, ab, Fs * np.abs(T).max()))
+    assert np.max(np.abs(out[:, 0] - orc[:, 0]) / scale[:, 0]) <= 1e-5
+    assert np.max(np.abs(out[:, 1:] * out[:, :1] - orc[:, 1:] * orc[:, :1]) / scale[:, 1:]) <= 1e-5

@@ -74,11 +74,12 @@ def check_spo(q, nx, ny, nz, n_orb, ld, W, seed, pos_dtype=np.float32, L=(3.0, 3
     assert np.all(np.isfinite(spo[:, :, :n_orb]))
     assert err.max() <= TOL, f"spo max normalized error {err.max():.3e}"
     orc, aab = oracle.det_ratio(A, v, g, h)
+    scale = np.maximum(aab, oracle.det_ratio_scale(A, ab, np.abs(T).max() * _F(L, (nx, ny, nz))))
     rho_g, rho_o = out[:, 0], orc[:, 0]
-    assert np.max(np.abs(rho_g - rho_o) / aab[:, 0]) <= TOL
+    assert np.max(np.abs(rho_g - rho_o) / scale[:, 0]) <= TOL
     num_g = out[:, 1:] * rho_g[:, None]
     num_o = orc[:, 1:] * rho_o[:, None]
-    assert np.max(np.abs(num_g - num_o) / aab[:, 1:]) <= TOL
+    assert np.max(np.abs(num_g - num_o) / scale[:, 1:]) <= TOL
     return T, tab, pos, out, spo
 
 
