@@ -240,3 +240,53 @@ def test_spo_random(q, c):
     scale = np.maximum(aab, oracle.det_ratio_scale(A, ab, Fs * np.abs(T).max()))
     assert np.max(np.abs(out[:, 0] - orc[:, 0]) / scale[:, 0]) <= 1e-5
     assert np.max(np.abs(out[:, 1:] * out[:, :1] - orc[:, 1:] * orc[:, :1]) / scale[:, 1:]) <= 1e-5
+
+
+def _sweep_j1_cases(n=8, seed=2029):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        S = int(rng.integers(1, 5))
+        out.append(dict(N=max(2, _log_uniform(rng, 2, 1024)), W=int(rng.integers(1, 5)), n_ions=int(rng.integers(S, 257)),
+                        S=S, m=tuple(int(x) for x in rng.integers(4, 17, 4)),
+                        rcut=tuple(float(x) for x in rng.uniform(0.2, 0.5, 4)), seed=int(rng.integers(2**31)),
+                        up_frac=float(rng.choice([0.0, 1.0, rng.random(), 0.5])), moves=int(rng.integers(1, 48))))
+    return out
+
+
+@pytest.mark.parametrize("c", _sweep_j1_cases(), ids=lambda c: f"N{c['N']}-W{c['W']}-ions{c['n_ions']}-S{c['S']}")
+def test_sweep_j1_random(q, c):
+    """qj2_sweep with J1 joined to every move, vs the oracle (eval_j2 + eval_j1)."""
+    N, W, n_ions, S_, seed = c["N"], c["W"], c["n_ions"], c["S"], c["seed"]
+    S = min(c["moves"], N)
+    L = qmcgen.cell_length(N)
+    Np = qmcgen.padded_size(N, 32)
+    R = qmcgen.positions(seed, np.arange(W), N, Np, L, np.float32)
+    fn = qmcgen.make_functor(seed, L, 8)
+    ks, tr, u = qmcgen.make_sweep(seed, W, N, L, np.float32, S)
+    n_up = int(round(c["up_frac"] * N))
+    ions, start = qmcgen.make_ions(seed, n_ions, qmcgen.padded_size(n_ions, 4), L, np.float32, n_species=S_)
+    fn1 = qmcgen.make_j1_functor(seed, L, n_species=S_, m=c["m"], rcut_frac=c["rcut"])
+    Rd, Sd = dev(R), torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
+    S1 = torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
+    acc, dj = q.sweep(Rd, Sd, dev(ks), dev(tr), dev(u), fn, N, n_up, j1=(dev(ions), start, fn1, S1))
+    acc, dj = acc.cpu().numpy(), dj.cpu().numpy()
+    Rh, Sh = R.astype(np.float64), np.zeros((W, 5, Np))
+    S1h, A1h = np.zeros((W, 5, Np)), np.zeros((W, 5, Np))
+    for s in range(S):
+        o2, a2, _ = oracle.eval_j2(Rh, ks[s], tr[s], fn, N, n_up)
+        o1, a1 = oracle.eval_j1(ions.astype(np.float64), start, tr[s].astype(np.float64), fn1)
+        d = (o2[:, 1, 0] - o2[:, 0, 0]) + (o1[:, 1, 0] - o1[:, 0, 0])
+        scale = np.maximum(np.maximum(a2[:, :, 0].max(1), a1[:, :, 0].max(1)), 1.0)
+        assert np.max(np.abs(dj[s] - d) / scale) < 1e-5, s
+        rho2 = np.exp(d) ** 2
+        clear = np.abs(u[s] - rho2) > 1e-6 * rho2
+        assert np.array_equal(acc[s][clear], (u[s] < rho2)[clear].astype(np.int32)), s
+        Rh, Sh, _ = oracle.accept(Rh, Sh, ks[s], tr[s][:, 1], acc[s], fn, N, n_up)
+        for w in np.nonzero(acc[s])[0]:
+            S1h[w, :, ks[s][w]] = o1[w, 1]
+            A1h[w, :, ks[s][w]] = a1[w, 1]
+    assert np.array_equal(Rd.cpu().numpy().astype(np.float64), Rh)
+    err1 = oracle.normalized_error_j1(np.moveaxis(S1.cpu().numpy()[:, :, :N], 1, 2),
+                                      np.moveaxis(S1h[:, :, :N], 1, 2), np.moveaxis(A1h[:, :, :N], 1, 2), fn1)
+    assert err1.max() <= 1e-5
