@@ -766,7 +766,10 @@ __global__ void __launch_bounds__(TPB) j1_thread_kernel(const __grid_constant__ 
         accumulate<T>(dx, dy, dz, r2, gc.invd, gc.base, gc.clamp, acc);
     };
     for (int g = 0; g < p.n_src_groups; ++g) {
-        const GroupC<T> gc = group_consts<T, MODE_J1>(p, g, 0, tab_addr);
+        GroupC<T> gc = group_consts<T, MODE_J1>(p, g, 0, tab_addr);
+        // keep the species' row base as one value: otherwise the compiler re-associates
+        // row offset and table base into every term's address (one more add per term)
+        asm volatile("" : "+r"(gc.base));
         const int32_t i1 = (int32_t)p.grp_start[g + 1];
         for (int32_t i0 = (int32_t)p.grp_start[g]; i0 < i1; i0 += 32) {
             T acc[NACC] = {T(0), T(0), T(0), T(0), T(0), T(0)};
