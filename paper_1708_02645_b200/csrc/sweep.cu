@@ -32,12 +32,14 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
     const int64_t w = blockIdx.x;
     const int N = FULL ? TPB * SPT : (int)p.N;
     // dynamic shared memory, sized by the call (every byte counts at 7-8 CTAs/SM):
-    // R (SoA) [3][N] | state [5][N] | J2 table [2(m+1)] | J1 table [n_rows1] | ions [3][n_ions]
+    // R (SoA) [3][N] | state [5][N] | J2 table [2(m+1)] | J1 table [n_rows1] | ions [n_ions] (2 arrays)
     float *rx = sw_smem, *ry = rx + N, *rz = ry + N;
     float *st = rz + N;
     Coef4<float> *tab = reinterpret_cast<Coef4<float> *>(sw_smem + 8 * N);
     Coef4<float> *tab1 = tab + 2 * (p.m + 1);
-    float *ion_s = reinterpret_cast<float *>(tab1 + (J1 ? p.n_rows1 : 0));
+    // per ion, resolved once: (x, y, z, 1/delta_s) and (table row base, m_s) of its species
+    float4 *ion_p = reinterpret_cast<float4 *>(tab1 + (J1 ? p.n_rows1 : 0));
+    uint2 *ion_c = reinterpret_cast<uint2 *>(ion_p + (J1 ? p.n_ions : 0));
     __shared__ double red2[2][NW][NV];               // double-buffered by move parity
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int e = tid; e < 2 * (p.m + 1); e += TPB) {
@@ -54,9 +56,13 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
             tab1[e] = c;
         }
         for (int j = tid; j < p.n_ions; j += TPB) {
-            ion_s[j] = p.ions[j];
-            ion_s[p.n_ions + j] = p.ions[p.Np_ion + j];
-            ion_s[2 * p.n_ions + j] = p.ions[2 * p.Np_ion + j];
+            int sp = 0;
+#pragma unroll
+            for (int b = 1; b < QJ2_MAX_SPECIES; ++b) sp += (b < p.n_species && j >= p.sp_start[b]) ? 1 : 0;
+            ion_p[j] = make_float4(p.ions[j], p.ions[p.Np_ion + j], p.ions[2 * p.Np_ion + j], p.sp_invd[sp]);
+            ion_c[j] = make_uint2((uint32_t)__cvta_generic_to_shared(tab1) +
+                                      (uint32_t)(p.sp_tab[sp] * (int)sizeof(Coef4<float>)),
+                                  (uint32_t)p.sp_m[sp]);
         }
     }
     const float *Rg = p.R + w * 3 * p.Np;
@@ -137,13 +143,11 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
 #pragma unroll
             for (int ion = tid; ion < SW_MAX_IONS; ion += TPB) {
                 if (ion >= p.n_ions) break;
-                int sp = 0;
-#pragma unroll
-                for (int b = 1; b < QJ2_MAX_SPECIES; ++b) sp += (b < p.n_species && ion >= p.sp_start[b]) ? 1 : 0;
-                const uint32_t base1 = (uint32_t)__cvta_generic_to_shared(tab1) +
-                                       (uint32_t)(p.sp_tab[sp] * (int)sizeof(Coef4<float>));
-                const float iv = p.sp_invd[sp];
-                const float x = ion_s[ion], y = ion_s[p.n_ions + ion], z = ion_s[2 * p.n_ions + ion];
+                const float4 ip = ion_p[ion];
+                const uint2 ic = ion_c[ion];
+                const uint32_t base1 = ic.x;
+                const float iv = ip.w;
+                const float x = ip.x, y = ip.y, z = ip.z;
                 float u0 = 0.f;
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
@@ -151,7 +155,7 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
                     const float dx = min_image(x, a[0]), dy = min_image(y, a[1]), dz = min_image(z, a[2]);
                     const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
                     const float ir = Traits<float>::rsqrt(r2);
-                    const FunctorEval<float> e = functor_from_t<float>(r2 * ir * iv, base1, (unsigned)p.sp_m[sp]);
+                    const FunctorEval<float> e = functor_from_t<float>(r2 * ir * iv, base1, ic.y);
                     if (q == 0) {
                         u0 = e.u;
                     } else {
@@ -298,7 +302,7 @@ cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s) {
     const bool j1 = p.n_ions > 0;
     const size_t smem = (size_t)8 * p.N * sizeof(float)                       // R (3) + state (5) per electron
                       + (size_t)(2 * (p.m + 1) + (j1 ? p.n_rows1 : 0)) * sizeof(Coef4<float>)
-                      + (j1 ? (size_t)3 * p.n_ions * sizeof(float) : 0);
+                      + (j1 ? (size_t)p.n_ions * (sizeof(float4) + sizeof(uint2)) : 0);
     // 128 threads per walker for 384 < N <= 768 (8 CTAs/SM), else 256 (64 and 96
     // threads per walker were measured too: profiles/r01_s4/ab_tpb.log)
     int tpb = (p.N > 384 && p.N <= 768) ? 128 : SW_TPB;
