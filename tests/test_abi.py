@@ -124,6 +124,25 @@ def test_package_has_no_cpu_fallback():
                 assert "liboracle" not in txt, fn
 
 
+def test_oracle_is_independent_of_the_product():
+    """The oracle imports nothing from the product package, includes none of its
+    headers, and the product's binding, kernels and bench timing path never
+    load it (bench.py only in its cpu_baseline / --impl reference legs)."""
+    import re
+    odir = os.path.join(ROOT, "oracle")
+    for fn in os.listdir(odir):
+        txt = open(os.path.join(odir, fn)).read() if fn.endswith((".py", ".c", ".h")) else ""
+        if fn.endswith(".py"):      # its imports: stdlib and numpy only
+            mods = re.findall(r"^\s*(?:from|import)\s+([\w.]+)", txt, re.M)
+            assert set(mods) <= {"__future__", "ctypes", "os", "subprocess", "numpy"}, (fn, mods)
+        elif txt:                   # its includes: the C library only
+            incs = re.findall(r'#include\s*[<"]([^>"]+)[>"]', txt)
+            assert set(incs) <= {"math.h", "stdint.h", "stdlib.h", "string.h", "pthread.h"}, (fn, incs)
+    txt = open(os.path.join(ROOT, "qmcgen", "__init__.py")).read()   # the shared input generator
+    mods = re.findall(r"^\s*(?:from|import)\s+([\w.]+)", txt, re.M)
+    assert not any(m.startswith(("oracle", "paper_1708_02645_b200")) for m in mods), mods
+
+
 def _call_accept(q, f, **over):
     P = ctypes.c_void_p(4096)
     args = dict(dtype=0, W=4, N_total=100, N_up=50, i_offset=0, N_local=100, Np=128, R=P, S=P, k=P, rn=P,
