@@ -1,21 +1,22 @@
-// sweep.cu -- the resident-walker sweep kernel's launch (own translation unit).
+// sweep.cu -- the resident-walker sweep kernel (qj2_sweep) and its launch.
+// The design, in order of the per-move steps, is in sweep.cuh and DESIGN.md section 7.
 #include <cstdlib>
 
 #include "sweep.cuh"
 
 namespace qj2 {
 
-
-// TPB threads per walker, SPT partners per thread (the host picks
-// ceil(N / TPB)). Only the differences T_i(r'_k) - T_i(r_k) are kept (5 floats
-// per partner), so 128 threads x 6 partners fit 64 registers: 8 CTAs/SM, every
-// NiO-64 walker of a 1024-walker population resident in one wave.
-// J1: the one-body Jastrow over the (<= 256) ions joins each move's ratio.
-// FULL: N == TPB * SPT (NiO-64's 768 = 128 x 6, 1024 = 256 x 4), the shared-memory
-// layout and the partner bounds are compile-time constants.
-// 128 threads per walker: 7 CTAs/SM without J1 (72 registers, no spills; 148 x 7 = 1036 walkers
-// in one wave), 8 with J1 (64 registers) -- measured: N64S 3.28 ms at 7 vs 3.52 at 8, N64SJ 3.98
-// at 8 vs 4.10 at 7 (profiles/r01_s4/ab_minb.log)
+// Template parameters:
+//   TPB  threads per walker (one CTA per walker): 128 for 384 < N <= 768, else 256;
+//   SPT  partners per thread, ceil(N / TPB); only the five differences
+//        T_i(r'_k) - T_i(r_k) are kept per partner;
+//   J1   the one-body Jastrow over the (<= 256) ions joins each move's ratio;
+//   FULL N == TPB * SPT (NiO-64's 768 = 128 x 6, 1024 = 256 x 4): the shared-memory
+//        layout and the partner bounds are compile-time constants.
+// CTAs per SM at 128 threads: 7 without J1 (72 registers, no spills; 148 x 7 = 1036
+// walkers in one wave), 8 with J1 (64 registers) -- measured: N64S 3.28 ms at 7 vs 3.52
+// at 8, N64SJ 3.82 at 8 vs 3.87 at 7 (profiles/r01_s4/ab_minb.log).  QJ2_SWEEP_MINB_J1:
+// A/B builds only.
 #ifndef QJ2_SWEEP_MINB_J1
 #define QJ2_SWEEP_MINB_J1 8
 #endif
@@ -303,7 +304,7 @@ cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s) {
     const size_t smem = (size_t)8 * p.N * sizeof(float)                       // R (3) + state (5) per electron
                       + (size_t)(2 * (p.m + 1) + (j1 ? p.n_rows1 : 0)) * sizeof(Coef4<float>)
                       + (j1 ? (size_t)p.n_ions * (sizeof(float4) + sizeof(uint2)) : 0);
-    // 128 threads per walker for 384 < N <= 768 (8 CTAs/SM), else 256 (64 and 96
+    // 128 threads per walker for 384 < N <= 768 (7-8 CTAs/SM), else 256 (64 and 96
     // threads per walker were measured too: profiles/r01_s4/ab_tpb.log)
     int tpb = (p.N > 384 && p.N <= 768) ? 128 : SW_TPB;
     if (const char *e = getenv("QJ2_SWEEP_TPB")) tpb = atoi(e) == 128 && p.N <= 768 ? 128 : SW_TPB;   // A/B

@@ -1,23 +1,22 @@
 // sweep.cuh -- NEXT-2 at the paper's system sizes: a whole particle-by-particle
-// sweep of the J2 factor in one persistent kernel, the walker resident in
-// shared memory (sm_100a).
+// sweep of the J2 factor (optionally with J1) in one persistent kernel, the walker
+// resident in shared memory (sm_100a).
 //
-// For every walker (one CTA) and every move s < S (Alg. 1 L4-L9 for the J2
-// factor, electron k = ks[s][w], trial positions r_k = trials[s][w][0] and
-// r'_k = trials[s][w][1]):
-//   1. each thread forms, for its partners i != k (i = tid, tid + 256, ...),
-//      the pair terms T_i(r_k) and T_i(r'_k) -- the same fp32 arithmetic as
-//      the eval kernel (single-rounding minimum image, power-basis Horner) --
-//      and keeps them in registers;
-//   2. a block reduction in fp64 gives U^2_k at r_k and r'_k with their
-//      gradient and Laplacian (Eq. 5 / PAPER:1382, Alg. 1 L7-L8);
-//   3. the Metropolis test u < exp(2 dJ2) (reading R19), decided once;
-//   4. if accepted: state_i += T_i(r'_k) - T_i(r_k) from the kept terms (no
-//      recomputation), state_k = the reduced values at r'_k, R[:, k] = r'_k
-//      (PAPER:1305-1306, 1389-1393).
-// R and the 5N state stay in shared memory for all S moves (32 B per
-// electron: N <= 1024 in 32 KB); global memory is touched only to load and
-// store them once and to read the move inputs -- no launch per move.
+// One CTA per walker.  For every move s < S (Alg. 1 L4-L9; electron
+// k = ks[s][w], r_k = trials[s][w][0], r'_k = trials[s][w][1]):
+//   1. each thread forms, for its partners i != k (i = tid, tid + TPB, ...), the
+//      pair terms T_i at r_k and then at r'_k with the eval kernel's fp32
+//      arithmetic (single-rounding minimum image, power-basis Horner) and keeps
+//      only the differences T_i(r'_k) - T_i(r_k) in registers;
+//   2. a reduce-scatter (fp32 for lanes 16 and 8 apart, then fp64) and ONE barrier
+//      give dJ2 = sum_i (U(r'_k) - U(r_k)) and the sums at r'_k (electron k's new
+//      state, Eq. 5 / PAPER:1382, Alg. 1 L7-L8); with J1 also dJ1 and k's J1 row;
+//   3. every thread takes the same Metropolis decision u < exp(2 dJ) (reading R19);
+//   4. if accepted: state_i += the kept differences (no recomputation), state_k =
+//      the sums at r'_k, R[:, k] = r'_k.
+// R and the 5N state stay in shared memory for all S moves (32 B per electron:
+// N <= 1024 in 32 KB); global memory is touched only to load and store them once
+// and to read the moves -- no launch per move.
 #pragma once
 
 #include "qmcj2.h"
