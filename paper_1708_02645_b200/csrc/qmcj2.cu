@@ -4,7 +4,7 @@
 //
 // Kernel map (one translation unit each where noted):
 //   j2_eval_kernel           the hot path (j2_kernels.cuh, launch_*.cu): one CTA
-//                            per (walker, trial, tile of 8 sub-tiles); SoA lanes
+//                            per (walker, trial, tile of 25 sub-tiles); SoA lanes
 //                            streamed with 128-bit loads, per-term math in T,
 //                            fp32 partials of 32 terms flushed to fp64, warp
 //                            shuffle + smem CTA reduction, deterministic
@@ -13,7 +13,8 @@
 //   j1_thread_kernel         J1 over small ion sets: one thread per (walker, trial)
 //   j2_accept_kernel         NEXT-2 accept-side update (accept.cuh, launch_accept.cu),
 //                            optionally with the Metropolis test fused
-//   j2_sweep_kernel          NEXT-2 whole sweeps, walkers resident in smem (sweep.cu)
+//   j2_sweep_kernel          NEXT-2 whole sweeps (optionally with J1), walkers resident
+//                            in smem, one barrier per move (sweep.cu)
 //   spo_tma_kernel / spo_kernel   NEXT-4 Bspline-v/vgh + determinant ratio (spo.cu)
 //   ratio_kernel, metropolis_kernel, vgl_kernel, minimg_kernel, check_kernel  (here)
 //   gen_kernel, gen_spo_table kernels  synthetic inputs (gen.cu; harness)
