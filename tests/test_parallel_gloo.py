@@ -83,7 +83,7 @@ def _worker(rank, world, port, q):
         dj = full[:, 1, 0] - full[:, 0, 0]
         rerr = float(np.max(np.abs(rat.numpy()[:, 1, 0] - dj)))
         # instance gather with unequal counts
-        counts = [3, 2][:world] if world == 2 else [3]
+        counts = [3, 2, 4][:world]
         local = torch.full((counts[rank], 5), float(rank))
         g = parallel.gather_instances(local, counts)
         q.put((rank, err, rerr, g.numpy().tolist()))
@@ -99,10 +99,11 @@ def _free_port():
     return p
 
 
-def test_source_split_allreduce_gloo_world2():
+@pytest.mark.parametrize("world", [2, 3])
+def test_source_split_allreduce_gloo(world):
+    """C5's source-axis split at world 2 and 3 (unequal shards of N = 203)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    world = 2
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
@@ -114,7 +115,8 @@ def test_source_split_allreduce_gloo_world2():
     for rank, err, rerr, g in res:
         assert err < 1e-13, (rank, err)          # reduced partials == unsplit oracle
         assert rerr < 1e-12, (rank, rerr)
-        assert g == [[0.0] * 5] * 3 + [[1.0] * 5] * 2
+        counts = [3, 2, 4][:world]
+        assert g == sum(([[float(r)] * 5] * counts[r] for r in range(world)), [])
 
 
 # ---------------------------------------------------------------------------
