@@ -528,3 +528,32 @@ def test_sweep_kernel_with_j1_vs_oracle(q, n_ions, S, N):
     err1 = oracle.normalized_error_j1(np.moveaxis(S1.cpu().numpy()[:, :, :N], 1, 2),
                                       np.moveaxis(S1h[:, :, :N], 1, 2), np.moveaxis(A1h[:, :, :N], 1, 2), fn1)
     assert err1.max() <= 1e-5
+
+
+@pytest.mark.parametrize("with_j1", [False, True])
+def test_sweep_kernel_deterministic(q, with_j1):
+    """The sweep kernel's one-barrier-per-move design (double-buffered partials, every
+    thread writing only its own slots) leaves no shared-memory race: five runs of a
+    full NiO-64-sized sweep from the same inputs are bitwise identical (positions,
+    state, J1 state, decisions, dJ)."""
+    cfg = qmcgen.config("N64S")
+    N, W, n_up = cfg.N, cfg.W, cfg.n_up
+    fn = q.Functor.of(qmcgen.make_functor(cfg.seed, cfg.L, cfg.m))
+    R0 = q.gen_positions(cfg.seed, W, N, cfg.Np, cfg.L, torch.float32)
+    ks, tr, u = qmcgen.make_sweep(cfg.seed, W, N, cfg.L, np.float32, N)
+    kd, td, ud = dev(ks), dev(tr), dev(u)
+    j1 = None
+    if with_j1:
+        ions, start = qmcgen.make_ions(cfg.seed, 64, 64, cfg.L, np.float32, n_species=2)
+        fn1 = q.J1Functor.of(qmcgen.make_j1_functor(cfg.seed, cfg.L, n_species=2))
+    results = []
+    for _ in range(5):
+        R, S = R0.clone(), torch.zeros((W, 5, cfg.Np), dtype=torch.float32, device="cuda")
+        if with_j1:
+            j1 = (dev(ions), start, fn1, torch.zeros((W, 5, cfg.Np), dtype=torch.float32, device="cuda"))
+        acc, dj = q.sweep(R, S, kd, td, ud, fn, N, n_up, j1=j1)
+        results.append((R, S, acc, dj) + ((j1[3],) if with_j1 else ()))
+    torch.cuda.synchronize()
+    for other in results[1:]:
+        for a, b in zip(results[0], other):
+            assert torch.equal(a, b)
