@@ -205,3 +205,17 @@ def test_spo_S1V_full_size_sampled(q):
         v, g, h, _ = oracle.spo_vgh(T, cfg.n_orb, cfg.L, pts[w].astype(np.float64))
         orc, aab = oracle.det_ratio(np.repeat(A[w:w + 1], 12, axis=0), v, g, h)
         assert np.max(np.abs(out[w * 12:(w + 1) * 12, 0] - orc[:, 0]) / aab[:, 0]) <= TOL
+
+
+def test_spo_tma_kernel_deterministic(q, kernel):
+    """The bulk-copy ring (full/empty mbarriers) and the deferred ratio finalize leave
+    no race: repeated evaluations over many walkers are bitwise identical."""
+    T = qmcgen.spo_table(77, 20, 20, 20, 384, 384)
+    tab = q.SpoTable(dev(T), 384, (4.0, 4.0, 4.0))
+    rng = np.random.default_rng(77)
+    pos = dev((rng.random((20000, 3)) * 4.0).astype(np.float32))
+    A = dev(qmcgen.make_ainv_rows(77, 20000, 384))
+    ref = q.spo_eval(tab, pos, Ainv=A, want_spo=True)
+    for _ in range(4):
+        out = q.spo_eval(tab, pos, Ainv=A, want_spo=True)
+        assert torch.equal(out[0], ref[0]) and torch.equal(out[1], ref[1])
