@@ -2,6 +2,9 @@
 // streaming read (the C3 kernel's access pattern without its arithmetic):
 // grid-stride or tiled LDG.128 (L1::no_allocate, L2::256B) over a buffer of
 // the C3 size, a few unroll depths.  Context for DESIGN.md section 7 only.
+// Build and run (GPU box):
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/probe/read_probe tools/probe/read_probe.cu
+//   ./tools/probe/read_probe
 #include <cstdio>
 #include <cuda_runtime.h>
 
