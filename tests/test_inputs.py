@@ -90,3 +90,20 @@ def test_spo_table_generators_agree():
     r = qmcgen.spo_table_rows(9, 5, 6, 7, 12, 10, [[4, 5, 6], [0, 0, 0]])
     assert np.array_equal(r[0], a[4, 5, 6]) and np.array_equal(r[1], a[0, 0, 0])
     assert np.all(a[..., 10:] == 0) and a.min() >= -1 and a.max() < 1
+
+
+def test_sweep_inputs_are_an_ordered_sweep():
+    """qmcgen.make_sweep (reading R20): k[s][w] = (k0_w + s) mod N, trial 0 is the
+    electron's generated position (no electron moves twice while S <= N), trial 1 is
+    inside the cell, u in [0, 1)."""
+    N, W, S = 50, 7, 50
+    L = qmcgen.cell_length(N)
+    Np = qmcgen.padded_size(N, 32)
+    R = qmcgen.positions(3, np.arange(W), N, Np, L, np.float32)
+    ks, tr, u = qmcgen.make_sweep(3, W, N, L, np.float32, S)
+    assert ks.shape == (S, W) and tr.shape == (S, W, 2, 3) and u.shape == (S, W)
+    assert np.array_equal(ks, (ks[0][None, :] + np.arange(S)[:, None]) % N)
+    for s in range(S):
+        assert np.array_equal(tr[s, :, 0, :], R[np.arange(W), :, ks[s]])
+    assert np.all((tr[:, :, 1] >= 0) & (tr[:, :, 1] < L))
+    assert np.all((u >= 0) & (u < 1)) and u.dtype == np.float64
