@@ -295,6 +295,26 @@ def test_C3_full_size_sampled(q):
     torch.cuda.empty_cache()
 
 
+def test_C3_full_size_every_walker(q):
+    """The default bench workload in its launch configuration, every one of the 1024
+    walkers against the oracle (the oracle's own C twin of the position generator
+    builds the 7.55 GB host copy; ~2 s of oracle time on the box's cores)."""
+    cfg = qmcgen.CONFIGS["C3"]
+    R = q.gen_positions(cfg.seed, cfg.W, cfg.N, cfg.Np, cfg.L, torch.float32)
+    k = qmcgen.make_k(cfg.seed, cfg.W, cfg.N)
+    rt = qmcgen.make_trials(cfg.seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32)
+    fn = qmcgen.make_functor(cfg.seed, cfg.L, cfg.m)
+    out = q.eval(R, dev(k), dev(rt), fn, cfg.N, cfg.n_up).cpu().numpy()
+    del R
+    torch.cuda.empty_cache()
+    Rh = oracle.gen_positions(cfg.seed, 0, cfg.W, cfg.N, cfg.Np, cfg.L, np.float32, threads=THREADS)
+    orc, absout, _ = oracle.eval_j2(Rh, k, rt, fn, cfg.N, cfg.n_up, threads=THREADS)
+    del Rh
+    assert np.all(np.isfinite(out))
+    err = oracle.normalized_error(out, orc, absout, fn)
+    assert err.max() <= TOL[np.float32], err.max()
+
+
 def test_C4_instances_sampled(q):
     cfg = qmcgen.CONFIGS["C4"]
     for inst in (0, 1, 4095):
@@ -412,9 +432,9 @@ def test_nlpp_P12(q, dtype):
 
 
 @pytest.mark.parametrize("name", ["C3P2", "C3P12"])
-def test_multi_trial_full_size_sampled(q, name):
+def test_multi_trial_full_size_every_walker(q, name):
     """The NEXT-3 bench workloads at full C3 size (N = 614,400, W = 1024, fp32)
-    in the bench launch configuration; sampled walkers vs the oracle."""
+    in the bench launch configuration; every walker vs the oracle."""
     cfg = qmcgen.config(name)
     P, mode = qmcgen.trial_spec(name)
     R = q.gen_positions(cfg.seed, cfg.W, cfg.N, cfg.Np, cfg.L, torch.float32)
@@ -424,10 +444,9 @@ def test_multi_trial_full_size_sampled(q, name):
     out = q.eval(R, dev(k), dev(rt), fn, cfg.N, cfg.n_up).cpu().numpy()
     del R
     torch.cuda.empty_cache()
-    ws = np.array([0, 600, 1023])
-    Rs = oracle.gen_positions(cfg.seed, 0, 1, cfg.N, cfg.Np, cfg.L, np.float32)
-    for w in ws:
-        Rs = oracle.gen_positions(cfg.seed, int(w), 1, cfg.N, cfg.Np, cfg.L, np.float32)
-        orc, absout, _ = oracle.eval_j2(Rs, k[w:w + 1], rt[w:w + 1], fn, cfg.N, cfg.n_up, threads=THREADS)
-        err = oracle.normalized_error(out[w:w + 1], orc, absout, fn)
-        assert err.max() <= TOL[np.float32], err.max()
+    Rh = oracle.gen_positions(cfg.seed, 0, cfg.W, cfg.N, cfg.Np, cfg.L, np.float32, threads=THREADS)
+    orc, absout, _ = oracle.eval_j2(Rh, k, rt, fn, cfg.N, cfg.n_up, threads=THREADS)
+    del Rh
+    assert np.all(np.isfinite(out))
+    err = oracle.normalized_error(out, orc, absout, fn)
+    assert err.max() <= TOL[np.float32], err.max()
