@@ -381,10 +381,11 @@ def test_sweep_kernel_equals_per_move_kernels(q):
         assert (Sa - Sb).abs().max().item() <= 1e-5 * fresh_scale
 
 
-def test_sweep_N64S_full_size_sampled(q):
+def test_sweep_N64S_full_size_every_walker(q):
     """The N64S bench workload at full size (W = 1024 walkers of N = 768, one
-    768-move sweep, zero initial state) in the bench launch configuration;
-    three sampled walkers replayed move by move by the oracle."""
+    768-move sweep, zero initial state) in the bench launch configuration; every
+    walker replayed move by move by the oracle (decisions where clear, dJ,
+    positions bitwise, final state)."""
     cfg = qmcgen.config("N64S")
     N, W, n_up = cfg.N, cfg.W, cfg.n_up
     fn = q.Functor.of(qmcgen.make_functor(cfg.seed, cfg.L, cfg.m))
@@ -393,22 +394,26 @@ def test_sweep_N64S_full_size_sampled(q):
     ks, tr, u = qmcgen.make_sweep(cfg.seed, W, N, cfg.L, np.float32, N)
     acc, dj = q.sweep(R, S, dev(ks), dev(tr), dev(u), fn, N, n_up)
     acc, dj = acc.cpu().numpy(), dj.cpu().numpy()
-    ws = np.array([0, 511, 1023])
-    Rh = oracle.gen_positions(cfg.seed, 0, W, N, cfg.Np, cfg.L, np.float32)[ws].astype(np.float64)
-    Sh = np.zeros((3, 5, cfg.Np))
+    ws = np.arange(W)
+    Rh = oracle.gen_positions(cfg.seed, 0, W, N, cfg.Np, cfg.L, np.float32).astype(np.float64)
+    Sh = np.zeros((W, 5, cfg.Np))
     for s in range(N):
-        orc, _, _ = oracle.eval_j2(Rh, ks[s][ws], tr[s][ws], fn, N, n_up)
+        orc, _, _ = oracle.eval_j2(Rh, ks[s], tr[s], fn, N, n_up, threads=THREADS)
         d = orc[:, 1, 0] - orc[:, 0, 0]
+        assert np.max(np.abs(dj[s] - d) / np.maximum(np.abs(orc[:, :, 0]).max(1), 1.0)) < 1e-5, s
         rho2 = np.exp(d) ** 2
-        clear = np.abs(u[s][ws] - rho2) > 1e-6 * rho2
-        assert np.array_equal(acc[s][ws][clear], (u[s][ws] < rho2)[clear].astype(np.int32)), s
-        Rh, Sh, _ = oracle.accept(Rh, Sh, ks[s][ws], tr[s][ws, 1], acc[s][ws], fn, N, n_up)
-    assert np.array_equal(R.cpu().numpy()[ws].astype(np.float64), Rh)
-    Sg = S.cpu().numpy()[ws]
-    for j in range(3):
+        clear = np.abs(u[s] - rho2) > 1e-6 * rho2
+        assert np.array_equal(acc[s][clear], (u[s] < rho2)[clear].astype(np.int32)), s
+        Rh, Sh, _ = oracle.accept(Rh, Sh, ks[s], tr[s][:, 1], acc[s], fn, N, n_up)
+    assert np.array_equal(R.cpu().numpy().astype(np.float64), Rh)
+    Sg = S.cpu().numpy()
+    for j in ws[::64]:                   # the from-scratch scale: the O(N^2) state oracle on every 64th walker
         _, ab = oracle.j2_state(Rh[j], N, n_up, fn)
         err = oracle.normalized_error_state(Sg[j][:, :N], Sh[j][:, :N], ab[:, :N], fn)
         assert err.max() <= 1e-5, (j, err.max())
+    # every walker's state vs the replayed oracle state, normalised by its magnitude
+    scale = np.maximum(np.abs(Sh[:, :, :N]).max(axis=2, keepdims=True), 1.0)
+    assert np.max(np.abs(Sg[:, :, :N] - Sh[:, :, :N]) / scale) <= 1e-5
 
 
 def test_sweep_kernel_out_of_range_k(q):
