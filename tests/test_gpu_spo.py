@@ -149,8 +149,8 @@ def test_spo_kernels_agree(q):
 def test_spo_nio64_full_size_sampled(q):
     """The bench workload: NiO-64-shaped table (80^3 grid, 384 orbitals = N/2
     for N = 768, fp32, 786 MB) generated on the device, 65,536 walkers'
-    Bspline-vgh + ratio in the bench launch configuration; sampled walkers vs
-    the oracle on the oracle side's own copy of the table."""
+    Bspline-vgh + ratio in the bench launch configuration; ~8300 walkers (both ends
+    and every 8th) vs the oracle on the oracle side's own copy of the table."""
     cfg = qmcgen.SPO_CONFIGS["S1"]
     coef = q.gen_spo_table(cfg.seed, cfg.nx, cfg.ny, cfg.nz, cfg.n_orb, cfg.ld)
     tab = q.SpoTable(coef, cfg.n_orb, cfg.L)
@@ -160,11 +160,13 @@ def test_spo_nio64_full_size_sampled(q):
     del coef
     torch.cuda.empty_cache()
     T = oracle.gen_spo_table(cfg.seed, cfg.nx, cfg.ny, cfg.nz, cfg.n_orb, cfg.ld, threads=os.cpu_count() or 1)
-    ws = np.array([0, 1, 4097, 65535])
+    ws = np.r_[0:64, 64:cfg.W - 64:8, cfg.W - 64:cfg.W]          # ~8300 walkers: both ends, every 8th
     v, g, h, ab = oracle.spo_vgh(T, cfg.n_orb, cfg.L, pos[ws].astype(np.float64))
     orc, aab = oracle.det_ratio(A[ws], v, g, h)
-    assert np.max(np.abs(out[ws, 0] - orc[:, 0]) / aab[:, 0]) <= TOL
-    assert np.max(np.abs(out[ws, 1:] * out[ws, :1] - orc[:, 1:] * orc[:, :1]) / aab[:, 1:]) <= TOL
+    scale = np.maximum(aab, oracle.det_ratio_scale(A[ws], ab, np.abs(T).max() *
+                                                   _F(cfg.L, (cfg.nx, cfg.ny, cfg.nz))))
+    assert np.max(np.abs(out[ws, 0] - orc[:, 0]) / scale[:, 0]) <= TOL
+    assert np.max(np.abs(out[ws, 1:] * out[ws, :1] - orc[:, 1:] * orc[:, :1]) / scale[:, 1:]) <= TOL
 
 
 def test_spo_v_nlpp_points_share_the_walkers_row(q, kernel):
@@ -201,10 +203,13 @@ def test_spo_S1V_full_size_sampled(q):
     del coef
     torch.cuda.empty_cache()
     T = oracle.gen_spo_table(cfg.seed, cfg.nx, cfg.ny, cfg.nz, cfg.n_orb, cfg.ld, threads=os.cpu_count() or 1)
-    for w in (0, 4095, 8191):
-        v, g, h, _ = oracle.spo_vgh(T, cfg.n_orb, cfg.L, pts[w].astype(np.float64))
-        orc, aab = oracle.det_ratio(np.repeat(A[w:w + 1], 12, axis=0), v, g, h)
-        assert np.max(np.abs(out[w * 12:(w + 1) * 12, 0] - orc[:, 0]) / aab[:, 0]) <= TOL
+    ws = np.r_[0:16, 16:cfg.W - 16:8, cfg.W - 16:cfg.W]           # ~1050 walkers x 12 points
+    v, g, h, ab = oracle.spo_vgh(T, cfg.n_orb, cfg.L, pts[ws].reshape(-1, 3).astype(np.float64))
+    orc, aab = oracle.det_ratio(np.repeat(A[ws], 12, axis=0), v, g, h)
+    scale = np.maximum(aab, oracle.det_ratio_scale(np.repeat(A[ws], 12, axis=0), ab, np.abs(T).max() *
+                                                   _F(cfg.L, (cfg.nx, cfg.ny, cfg.nz))))
+    rows = (ws[:, None] * 12 + np.arange(12)[None, :]).reshape(-1)
+    assert np.max(np.abs(out[rows, 0] - orc[:, 0]) / scale[:, 0]) <= TOL
 
 
 def test_spo_tma_kernel_deterministic(q, kernel):
