@@ -211,9 +211,9 @@ def test_sweep_matches_state_from_scratch(q):
 
 def test_accept_C3_full_size_sampled(q):
     """The bench's sweep step at full C3 size (N = 614,400, W = 1024, fp32):
-    eval -> accept with every walker accepted, zero initial state; sampled
-    walkers checked in full against the oracle (which regenerates their
-    positions with its own C generator)."""
+    eval -> accept (every 7th walker rejected), zero initial state; 96 walkers
+    (both ends, the middle) checked in full against the oracle (which
+    regenerates their positions with its own C generator)."""
     cfg = qmcgen.CONFIGS["C3"]
     R = q.gen_positions(cfg.seed, cfg.W, cfg.N, cfg.Np, cfg.L, torch.float32)
     k = qmcgen.make_k(cfg.seed, cfg.W, cfg.N)
@@ -225,12 +225,13 @@ def test_accept_C3_full_size_sampled(q):
     out = q.eval(R, dev(k), dev(rt), fn, cfg.N, cfg.n_up)
     q.accept(R, S, dev(k), dev(rt), dev(acc), out, fn, cfg.N, cfg.n_up)
     torch.cuda.synchronize()
-    for w in (0, 1, 511, 1023):
-        Rw = oracle.gen_positions(cfg.seed, w, 1, cfg.N, cfg.Np, cfg.L, np.float32)
-        Sw = np.zeros((1, 5, cfg.Np), np.float32)
-        R2, S2, ab = oracle.accept(Rw, Sw, k[w:w + 1], rt[w:w + 1, 0], acc[w:w + 1], fn, cfg.N, cfg.n_up)
-        compare(Rw, Sw, acc[w:w + 1], cfg.N, fn, np.float32, R[w:w + 1].cpu().numpy(),
-                S[w:w + 1].cpu().numpy(), R2, S2, ab)
+    for w0 in list(range(0, 32, 8)) + list(range(480, 544, 16)) + [992, 1000, 1008, 1016]:   # 96 walkers
+        n = 8
+        Rw = oracle.gen_positions(cfg.seed, w0, n, cfg.N, cfg.Np, cfg.L, np.float32, threads=THREADS)
+        Sw = np.zeros((n, 5, cfg.Np), np.float32)
+        sl = slice(w0, w0 + n)
+        R2, S2, ab = oracle.accept(Rw, Sw, k[sl], rt[sl, 0], acc[sl], fn, cfg.N, cfg.n_up)
+        compare(Rw, Sw, acc[sl], cfg.N, fn, np.float32, R[sl].cpu().numpy(), S[sl].cpu().numpy(), R2, S2, ab)
     del R, S
     torch.cuda.empty_cache()
 
