@@ -315,12 +315,21 @@ def test_C3_full_size_every_walker(q):
     assert err.max() <= TOL[np.float32], err.max()
 
 
-def test_C4_instances_sampled(q):
+def test_C4_instances_every_walker(q):
+    """Three of C4's 4096 instances (first, second, last) in the bench's launch
+    configuration (warp-per-walker kernel), every walker vs the oracle."""
     cfg = qmcgen.CONFIGS["C4"]
+    fn = qmcgen.make_functor(cfg.seed, cfg.L, cfg.m)
     for inst in (0, 1, 4095):
         seed = cfg.seed + inst
         R = q.gen_positions(seed, cfg.W, cfg.N, cfg.Np, cfg.L, torch.float32)
-        _sampled_check(q, cfg, seed, R, np.array([0, 5, 1023]))
+        k = qmcgen.make_k(seed, cfg.W, cfg.N)
+        rt = qmcgen.make_trials(seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32)
+        out = q.eval(R, dev(k), dev(rt), fn, cfg.N, cfg.n_up).cpu().numpy()
+        Rh = oracle.gen_positions(seed, 0, cfg.W, cfg.N, cfg.Np, cfg.L, np.float32, threads=THREADS)
+        orc, absout, _ = oracle.eval_j2(Rh, k, rt, fn, cfg.N, cfg.n_up, threads=THREADS)
+        assert np.all(np.isfinite(out))
+        assert oracle.normalized_error(out, orc, absout, fn).max() <= TOL[np.float32], inst
 
 
 def test_C5_sliced_single_gpu_sampled(q):
@@ -339,7 +348,12 @@ def test_C5_sliced_single_gpu_sampled(q):
         tot += q.eval(R, kd, td, fn, cfg.N, cfg.n_up, i_offset=a, n_local=b - a).cpu().numpy()
         del R
     torch.cuda.empty_cache()
-    _sampled_check(q, cfg, cfg.seed, None, np.array([0, 333, 1023]), out=tot)
+    ws = np.r_[0:1024:8, 1023]                                          # 129 walkers, 59 MB of positions each
+    Rh = np.concatenate([oracle.gen_positions(cfg.seed, int(w), 1, cfg.N, cfg.Np, cfg.L, np.float32, threads=THREADS)
+                         for w in ws])
+    orc, absout, _ = oracle.eval_j2(Rh, k[ws], rt[ws], fn, cfg.N, cfg.n_up, threads=THREADS)
+    assert np.all(np.isfinite(tot))
+    assert oracle.normalized_error(tot[ws], orc, absout, fn).max() <= TOL[np.float32]
 
 
 # ---------------------------------------------------------------------------
