@@ -26,7 +26,6 @@ inputs stand in for them with the paper's shape parameters (N, W).
 from __future__ import annotations
 
 import dataclasses
-import math
 
 import numpy as np
 

@@ -5,7 +5,6 @@ polynomial reproduction, finite differences, periodicity, and numpy's LU
 determinant for the matrix determinant lemma (Eq. 6).
 """
 import numpy as np
-import pytest
 from scipy.interpolate import BSpline
 
 import oracle
