@@ -201,7 +201,11 @@ class OracleSample:
         if cfg.name == "N64SJ":
             ions, start = qmcgen.make_ions(cfg.seed, 64, 64, cfg.L, np.float32, n_species=2)
             self.j1 = (ions.astype(np.float64), start, qmcgen.make_j1_functor(cfg.seed, cfg.L, n_species=2))
-        if self.sweep:
+        if self.sweep and cfg.name in ("N64S", "N64SJ"):
+            self.n = min(self.n, self.MAX_SWEEP_WALKERS)
+            self.ks, self.delta, self.us = [a[:, :self.n] for a in qmcgen.make_sweep_moves(cfg.seed, cfg.W, cfg.N, self.moves)]
+            self.rt = np.zeros((self.n, 1, 3), np.float32)
+        elif self.sweep:
             self.n = min(self.n, self.MAX_SWEEP_WALKERS)
             ks, tr, u = qmcgen.make_sweep(cfg.seed, cfg.W, cfg.N, cfg.L, cfg.np_dtype, self.moves)
             self.ks, self.trs, self.us = ks[:, :self.n], tr[:, :self.n], u[:, :self.n]
@@ -216,6 +220,16 @@ class OracleSample:
         self.P = self.rt.shape[1]
         self.fn = qmcgen.make_functor(cfg.seed, cfg.L, cfg.m)
         self.R = oracle.gen_positions(cfg.seed, 0, self.n, cfg.N, cfg.Np, cfg.L, cfg.np_dtype, threads)
+        if self.sweep and cfg.name in ("N64S", "N64SJ"):      # the state of the start configuration (untimed)
+            self.S = np.stack([oracle.j2_state(self.R[w].astype(np.float64), cfg.N, cfg.n_up, self.fn)[0]
+                               for w in range(self.n)])
+            self.S1 = None
+            if self.j1 is not None:
+                ions, start, fn1 = self.j1
+                self.S1 = np.zeros((self.n, 5, cfg.Np))
+                for w in range(self.n):
+                    o1, _ = oracle.eval_j1(ions, start, self.R[w][:, :cfg.N].T.reshape(-1, 1, 3).astype(np.float64), fn1)
+                    self.S1[w][:, :cfg.N] = o1[:, 0].T
         # items in the bench's unit: (walker, trial, partner) terms; the sweep configs count one per
         # (move, partner) like their GPU lines
         self.items = self.n * (self.moves if self.sweep else self.P) * (cfg.N - 1 + (64 if self.j1 else 0))
@@ -226,13 +240,15 @@ class OracleSample:
         if not self.sweep:
             oracle.eval_j2(self.R, self.k, self.rt, self.fn, self.cfg.N, self.cfg.n_up, threads=self.threads)
             return time.perf_counter() - t0
+        if self.cfg.name in ("N64S", "N64SJ"):           # oracle.sweep: the whole sweep, as it stands
+            j1 = None if self.j1 is None else (self.j1[0], self.j1[1], self.j1[2], self.S1)
+            oracle.sweep(self.R, self.S, self.ks, self.delta, self.us, self.fn, self.cfg.N, self.cfg.n_up, j1=j1,
+                         threads=self.threads)
+            return time.perf_counter() - t0
         for m in range(self.moves):
             k, rt, u = self.ks[m], self.trs[m], self.us[m]
             out, _, _ = oracle.eval_j2(self.R, k, rt, self.fn, self.cfg.N, self.cfg.n_up, threads=self.threads)
             d = out[:, 1, 0] - out[:, 0, 0]
-            if self.j1 is not None:
-                o1, _ = oracle.eval_j1(self.j1[0], self.j1[1], rt.astype(np.float64), self.j1[2])
-                d = d + (o1[:, 1, 0] - o1[:, 0, 0])
             acc = (u < np.exp(d) ** 2).astype(np.int32)
             self.R, self.S, _ = oracle.accept(self.R, self.S, k, rt[:, 1], acc, self.fn, self.cfg.N, self.cfg.n_up)
         return time.perf_counter() - t0
@@ -546,6 +562,7 @@ def _event_ms(fn, stream, reps=1):
 
 
 L2_FLUSH_BYTES = 256 << 20     # > the 126 MB L2
+SPIN_CYCLES = 400_000          # ~0.2 ms of device spin before each separately timed step
 
 
 class L2Flusher:
@@ -565,6 +582,9 @@ class L2Flusher:
         evs = []
         for _ in range(reps):
             self.flush()
+            # keep the GPU busy (untimed) while the host prepares the launch, so that the
+            # events time the kernel and not the host's launch latency
+            torch.cuda._sleep(SPIN_CYCLES)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             fn()
@@ -873,16 +893,19 @@ class SweepPlan:
 
 class GraphSweepPlan(SweepPlan):
     """A full particle-by-particle sweep of the paper's NiO-64 size (N = 768,
-    1024 walkers): N moves per walker, each eval at (r_k, r'_k) -> Metropolis ->
-    accept.  The timed step is ONE qj2_sweep launch (walkers resident in shared
-    memory, pair terms kept in registers between the ratio and the update);
-    for context prepare() also times the same sweep as per-move launches
-    (qj2_eval + qj2_metropolis_accept, 2 per move), eagerly and captured in a
-    CUDA graph.  Replays re-run the same pre-drawn moves on the evolving
-    configuration (the work per step is unaffected)."""
+    1024 walkers): N moves per walker (Alg. 1 L4-L9), each r'_k = wrap(r_k +
+    delta) from the walker's current r_k -> U^2_k(R') on the fly -> ratio with
+    the stored U^2_k(R) -> Metropolis -> on acceptance the update of R and the 5N
+    state.  The timed step is ONE qj2_sweep launch (walkers resident in shared
+    memory); consecutive steps continue the Markov chain from the evolved
+    configuration (the state starts from qj2_state_init), with the moves of
+    step i drawn from a pool of POOL pre-drawn sweeps.  For context prepare()
+    also times one sweep's moves as per-move launches (qj2_eval + qj2_metropolis_
+    accept, 2 per move), eagerly and captured in a CUDA graph."""
     mode = "N64S"
-    OPS_PER_PAIR = 36 * 2               # functor terms at r_k and r'_k per partner (reused by the update)
+    OPS_PER_PAIR = 36                   # algorithmic flops per functor term (SURVEY 8(d))
     flush_l2 = True                     # R, state and the moves (~53 MB) fit in L2
+    POOL = 4
 
     N_IONS = 64                         # NiO-64 (Table 1): 64 ions of 2 species
 
@@ -893,22 +916,37 @@ class GraphSweepPlan(SweepPlan):
         self.S = cfg.N
         self.launches_per_step = 1
         self.items_per_step = self.S * cfg.W * (cfg.N - 1 + (self.N_IONS if self.with_j1 else 0))
+        self.i = 0
 
     def prepare(self, q, n_steps=None):
         import torch
-        super().prepare(q, self.S)
+        import qmcgen
+        cfg = self.cfg
         self.q = q
-        self.acc_all = torch.empty((self.S, self.cfg.W), dtype=torch.int32, device="cuda")
-        self.dj_all = torch.empty((self.S, self.cfg.W), dtype=torch.float64, device="cuda")
+        self.fn = q.Functor.of(qmcgen.make_functor(cfg.seed, cfg.L, cfg.m))
+        self.R = q.gen_positions(self.seed, cfg.W, cfg.N, cfg.Np, cfg.L, torch.float32)
+        self.S_ = torch.zeros((cfg.W, 5, cfg.Np), dtype=torch.float32, device="cuda")
         self.j1 = None
         if self.with_j1:
-            import qmcgen
-            cfg = self.cfg
             ions, start = qmcgen.make_ions(cfg.seed, self.N_IONS, self.N_IONS, cfg.L, np.float32, n_species=2)
             fn1 = q.J1Functor.of(qmcgen.make_j1_functor(cfg.seed, cfg.L, n_species=2))
             self.j1 = (torch.from_numpy(ions).cuda(), start, fn1,
                        torch.zeros((cfg.W, 5, cfg.Np), dtype=torch.float32, device="cuda"))
-        # context: the same sweep as per-move launches, eager and as one CUDA graph
+        q.state_init(self.R, self.S_, self.fn, cfg.N, cfg.n_up, j1=self.j1)       # untimed
+        ks, dl, u = qmcgen.make_sweep_moves(self.seed, cfg.W, cfg.N, self.POOL * self.S)
+        self.moves = [(torch.from_numpy(ks[i * self.S:(i + 1) * self.S]).cuda(),
+                       torch.from_numpy(dl[i * self.S:(i + 1) * self.S]).cuda(),
+                       torch.from_numpy(u[i * self.S:(i + 1) * self.S]).cuda()) for i in range(self.POOL)]
+        self.acc_all = torch.empty((self.S, cfg.W), dtype=torch.int32, device="cuda")
+        self.dj_all = torch.empty((self.S, cfg.W), dtype=torch.float64, device="cuda")
+        # context: one sweep's moves as per-move launches on copies (pre-drawn (r_k, r'_k) pairs of an
+        # ordered sweep from the start configuration), eager and as one CUDA graph
+        pks, ptr, pu = qmcgen.make_sweep(self.seed, cfg.W, cfg.N, cfg.L, np.float32, self.S)
+        self.pks, self.ptr, self.pu = torch.from_numpy(pks).cuda(), torch.from_numpy(ptr).cuda(), torch.from_numpy(pu).cuda()
+        self.Rc, self.Sc = self.R.clone(), self.S_.clone()
+        self.ws = q.Workspace(q.workspace_size(cfg.W, 2, cfg.N, torch.float32))
+        self.out = torch.empty((cfg.W, 2, 5), dtype=torch.float64, device="cuda")
+        self.acc = torch.empty((cfg.W,), dtype=torch.int32, device="cuda")
         for _ in range(2):
             self._per_move(q)
         torch.cuda.synchronize()
@@ -926,20 +964,23 @@ class GraphSweepPlan(SweepPlan):
         graph.replay()
         torch.cuda.synchronize()
         self.graph_ms = _event_ms(lambda: graph.replay(), torch.cuda.current_stream(), 3)
-        del graph
-        log(f"[bench] N64S: per-move launches {self.eager_ms:.3f} ms eager, {self.graph_ms:.3f} ms as one CUDA "
+        del graph, self.Rc, self.Sc
+        log(f"[bench] {self.mode}: per-move launches {self.eager_ms:.3f} ms eager, {self.graph_ms:.3f} ms as one CUDA "
             f"graph ({self.S} moves x 2 launches); the timed step is one qj2_sweep launch")
+        torch.cuda.synchronize()
 
     def _per_move(self, q):
         cfg = self.cfg
         for s in range(self.S):
-            k = self.ks[s]
-            q.eval(self.R, k, self.tr[s], self.fn, cfg.N, cfg.n_up, out=self.out, workspace=self.ws)
-            q.metropolis_accept(self.R, self.S_, k, self.tr[s], self.out, self.u[s], self.fn, cfg.N, cfg.n_up,
+            k = self.pks[s]
+            q.eval(self.Rc, k, self.ptr[s], self.fn, cfg.N, cfg.n_up, out=self.out, workspace=self.ws)
+            q.metropolis_accept(self.Rc, self.Sc, k, self.ptr[s], self.out, self.pu[s], self.fn, cfg.N, cfg.n_up,
                                 acc=self.acc)
 
     def step(self, q, dist_mod):
-        q.sweep(self.R, self.S_, self.ks, self.tr, self.u, self.fn, self.cfg.N, self.cfg.n_up, acc=self.acc_all,
+        ks, dl, u = self.moves[self.i % self.POOL]
+        self.i += 1
+        q.sweep(self.R, self.S_, ks, dl, u, self.fn, self.cfg.N, self.cfg.n_up, acc=self.acc_all,
                 dj=self.dj_all, j1=self.j1)
 
     def e2e(self, q, steps, dist_mod):
@@ -949,7 +990,8 @@ class GraphSweepPlan(SweepPlan):
         functor tables and the ions are model data, resident on the device)."""
         import torch
         cfg = self.cfg
-        dev = [self.R, self.S_, self.ks, self.tr, self.u] + ([self.j1[3]] if self.j1 else [])
+        ks, dl, u = self.moves[0]
+        dev = [self.R, self.S_, ks, dl, u] + ([self.j1[3]] if self.j1 else [])
         host = [t.cpu().pin_memory() for t in dev]
         dbuf = [torch.empty_like(t) for t in dev]
         acc_h = torch.empty(tuple(self.acc_all.shape), dtype=torch.int32, pin_memory=True)
@@ -973,20 +1015,23 @@ class GraphSweepPlan(SweepPlan):
         return {"value": self.items_per_step * world / dt, "unit": UNIT,
                 "h2d_bytes_per_step": sum(h.numel() * h.element_size() for h in host),
                 "d2h_bytes_per_step": acc_h.numel() * 4, "ms_per_step": dt * 1e3, "steps": steps,
-                "api": "qj2_sweep with R, the 5N state and the sweep's moves copied from pinned host memory "
-                       "every step, accept flags read back"}
+                "api": "qj2_sweep with R, the 5N state and the sweep's moves (k, delta, u) copied from pinned "
+                       "host memory every step, accept flags read back"}
 
     @property
     def alg_bytes_per_launch(self):
         cfg = self.cfg
-        return cfg.W * cfg.Np * 8 * 4 * 2 + self.S * cfg.W * (4 + 24 + 8 + 4 + 8)   # R + state in/out, inputs
+        return cfg.W * cfg.Np * 8 * 4 * 2 + self.S * cfg.W * (4 + 12 + 8 + 4 + 8)   # R + state in/out, moves
 
     def kernel_ms(self, q, stream, reps):
         return self.flusher.event_ms(lambda: self.step(q, None), stream, max(1, reps // 5))
 
     def roofline(self, kms, peak_hbm):
         cfg = self.cfg
-        ops = self.S * cfg.W * (cfg.N - 1 + (self.N_IONS if self.with_j1 else 0)) * self.OPS_PER_PAIR
+        acc = (self.acc_all == 1).float().mean().item()    # acceptance of the last timed sweep
+        # functor terms per move: N - 1 at r'_k, N - 1 more at r_k when accepted; J1: 2 per ion
+        terms = self.S * cfg.W * ((cfg.N - 1) * (1.0 + acc) + (2 * self.N_IONS if self.with_j1 else 0))
+        ops = terms * self.OPS_PER_PAIR
         peak = 148 * 128 * 1.965e9 / 1e12
         achieved = ops / (kms / 1e3) / 1e12
         return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,

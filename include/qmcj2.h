@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define QJ2_VERSION 10000 /* major*10000 + minor*100 + patch */
+#define QJ2_VERSION 20000 /* major*10000 + minor*100 + patch */
 
 typedef enum {
     QJ2_OK = 0,
@@ -287,27 +287,37 @@ qj2_status qj2_metropolis_accept(const qj2_functor *fn, qj2_dtype dtype,
 
 /* qj2_sweep -- S particle-by-particle moves of every walker in ONE launch,  */
 /* the walker resident in shared memory (the paper's system sizes: Table 1   */
-/* N = 256..768).  For s = 0..S-1 and walker w, with k = ks[s*W + w],        */
-/* r_k = trials[((s*W + w)*2 + 0)*3 ..], r'_k = trials[((s*W + w)*2 + 1)*3..]*/
-/* (the P = 2 drift pair): V, G, L at r_k and r'_k (as qj2_eval), the        */
-/* Metropolis decision accept[s*W + w] = u[s*W + w] < exp(2 dJ2) with dJ2 =  */
-/* V(r'_k) - V(r_k) (written to dj[s*W + w] if dj != NULL), and on           */
-/* acceptance the update of qj2_accept (state_i += T_i(r'_k) - T_i(r_k),     */
-/* state_k = the values at r'_k, R[:, k] = r'_k).  fp32 only: R [W][3][Np],  */
-/* state [W][5][Np] (in/out), trials fp32, u fp64, accept int32 (out).       */
-/* Requirements (else QJ2_EINVAL): 2 <= N <= 1024, Np >= N, functor m <= 16  */
-/* (pair terms are kept in fp32; finer functors use qj2_eval +               */
-/* qj2_metropolis_accept).  Moves within a call are sequential per walker;   */
-/* walkers are independent.  Preconditions (not scanned): trial coordinates  */
-/* in [0, L_d) (else the values are unspecified); a move whose k is outside  */
-/* [0, N) is never accepted (nothing is written) and its accept entry is -1. */
+/* N = 256..768).  Alg. 1 L4-L9 for a Jastrow-only trial     */
+/* function.  For s = 0..S-1 and walker w, k = ks[s*W + w]:                  */
+/*   r_k  = the walker's CURRENT position of electron k (R as updated by the */
+/*          earlier accepted moves of this call);                            */
+/*   r'_k = wrap(r_k + delta[(s*W + w)*3 ..]): fp32 x = r + d, then x += L_d */
+/*          if x < 0, then x -= L_d if x >= L_d (Alg. 1 L5 without the drift */
+/*          term, reading R24; precondition |d| < L_d);                      */
+/*   dJ2  = U^2_k(R') - U^2_k(R): U^2_k(R') = sum_{i != k} U(|r_i - r'_k|)   */
+/*          computed on the fly, U^2_k(R) = state[w][0][k], the stored 5N    */
+/*          state (PAPER:1382-1393 -- the caller keeps the state consistent  */
+/*          with R: qj2_state_init, qj2_accept, earlier sweeps);             */
+/*   accept[s*W + w] = u[s*W + w] < exp(2 dJ) (reading R19), dj[s*W + w] =   */
+/*          dJ if dj != NULL;                                                */
+/*   on acceptance the update of qj2_accept: state_i += T_i(r'_k) - T_i(r_k) */
+/*          for i != k, state_k = (V, G, L) at r'_k, R[:, k] = r'_k.         */
+/* Any k sequence is valid (an electron may move any number of times).       */
+/* fp32 only: R [W][3][Np], state [W][5][Np] (in/out), delta fp32, u fp64,   */
+/* accept int32 (out).  Requirements (else QJ2_EINVAL): 2 <= N <= 1024,      */
+/* Np >= N, functor m <= 16 (pair terms are kept in fp32; finer functors use */
+/* qj2_eval + qj2_metropolis_accept).  Moves within a call are sequential    */
+/* per walker; walkers are independent.  Preconditions (not scanned): a move */
+/* whose k is outside [0, N) is never accepted (nothing is written), its     */
+/* accept entry is -1 and its dj entry 0.                                    */
 /*                                                                           */
 /* Optional one-body Jastrow (j1 != NULL; NEXT-1 joined to the move): the   */
-/* ratio becomes exp(dJ1 + dJ2) (Eq. 4-5), dj holds dJ1 +   */
-/* dJ2, and on acceptance electron k's J1 state row (U^1_k, grad, lap at    */
-/* r'_k, as qj2_eval_j1 computes them) is written to j1->state.  Ions fixed */
-/* (PAPER:1306-1308), <= 256 of them, sorted by species; the J1 functor's   */
-/* cell must equal fn's.                                                     */
+/* ratio becomes exp(dJ1 + dJ2) (Eq. 4-5) with dJ1 =         */
+/* U^1_k(r'_k) - U^1_k(r_k) over the ions (both computed on the fly), dj     */
+/* holds dJ1 + dJ2, and on acceptance electron k's J1 row (U^1_k, grad, lap */
+/* at r'_k, as qj2_eval_j1 computes them) is written to j1->state.  Ions    */
+/* fixed, <= 256 of them, sorted by species, species m <=  */
+/* 16; the J1 functor's cell must equal fn's.                                */
 typedef struct {
     const qj2_j1_functor *fn;       /* host: per-species functors and cell   */
     const int64_t *species_start;   /* host [n_species + 1], as qj2_eval_j1  */
@@ -317,9 +327,19 @@ typedef struct {
 } qj2_sweep_j1;
 
 qj2_status qj2_sweep(const qj2_functor *fn, int64_t W, int64_t N, int64_t N_up, int64_t Np,
-                     float *R, float *state, int64_t S, const int32_t *ks, const float *trials,
+                     float *R, float *state, int64_t S, const int32_t *ks, const float *delta,
                      const double *u, int32_t *accept, double *dj, const qj2_sweep_j1 *j1,
                      void *stream);
+
+/* qj2_state_init -- the 5N J2 state of every electron from scratch (the     */
+/* "new states are periodically computed from scratch" of PAPER:764-765):    */
+/* state[w][:, e] = (V_e, G_e, L_e) as defined for qj2_accept, over all      */
+/* partners j != e, fp32 pair terms with fp64 sums of <= 32-term partials.   */
+/* With j1 != NULL also every electron's J1 row into j1->state.  Sizes and   */
+/* requirements as qj2_sweep (2 <= N <= 1024, m <= 16).  R [W][3][Np] fp32   */
+/* (read), state [W][5][Np] fp32 (written; padding untouched).               */
+qj2_status qj2_state_init(const qj2_functor *fn, int64_t W, int64_t N, int64_t N_up, int64_t Np,
+                          const float *R, float *state, const qj2_sweep_j1 *j1, void *stream);
 
 /* ------------------------------------------------------------------------ */
 /* NEXT-4: tricubic B-spline single-particle orbitals (SPOs) and the         */

@@ -257,6 +257,76 @@ def accept(R, state, k, r_new, acc, fn, n: int, n_up: int):
     return R2, S2, ab
 
 
+def propose_f32(L, r, delta) -> np.ndarray:
+    """Oracle of the in-kernel proposal r' = wrap(r + delta) in fp32
+    (orc_propose_f32; Alg. 1 L5 without drift, reading R24).  r, delta [n][3]."""
+    r = np.ascontiguousarray(np.asarray(r, dtype=np.float32).reshape(-1, 3))
+    d = np.ascontiguousarray(np.asarray(delta, dtype=np.float32).reshape(-1, 3))
+    out = np.empty_like(r)
+    Lb = lib()
+    Lb.orc_propose_f32.restype = None
+    Lb.orc_propose_f32.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.c_void_p,
+                                   ctypes.c_void_p, ctypes.c_void_p]
+    Lb.orc_propose_f32(_dp(_f64(np.broadcast_to(np.asarray(L, dtype=np.float64), (3,)))), r.shape[0],
+                       r.ctypes.data_as(ctypes.c_void_p), d.ctypes.data_as(ctypes.c_void_p),
+                       out.ctypes.data_as(ctypes.c_void_p))
+    return out
+
+
+def sweep(R, state, ks, delta, u, fn, n: int, n_up: int, *, forced=None, j1=None, threads: int = 1):
+    """Oracle of qj2_sweep (orc_sweep): S ordered particle-by-particle moves per
+    walker with the ratio from the stored state.
+
+    R [W][3][Np] fp32 (copied), state [W][5][Np] (promoted to fp64, copied),
+    ks [S][W], delta [S][W][3] fp32, u [S][W] fp64, forced [S][W] int (decisions
+    to apply; None = the oracle's own), j1 = (ions [3][Np_ion], species_start,
+    fn1, state_j1 [W][5][Np]) or None.
+    Returns (R', state', acc [S][W] (the oracle's own decisions, -1 for an
+    invalid k), dj [S][W], state_j1' or None)."""
+    R2 = np.ascontiguousarray(np.asarray(R, dtype=np.float32)).copy()
+    S2 = _f64(state).copy()
+    W, _, Np = R2.shape
+    ks = np.ascontiguousarray(np.asarray(ks, dtype=np.int32))
+    S = ks.shape[0]
+    dl = np.ascontiguousarray(np.asarray(delta, dtype=np.float32).reshape(S, W, 3))
+    uu = _f64(np.asarray(u).reshape(S, W))
+    fc = None if forced is None else np.ascontiguousarray(np.asarray(forced, dtype=np.int32).reshape(S, W))
+    acc = np.zeros((S, W), dtype=np.int32)
+    dj = np.zeros((S, W))
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    dp = ctypes.POINTER(ctypes.c_double)
+    Lb = lib()
+    Lb.orc_sweep.restype = ctypes.c_int64
+    Lb.orc_sweep.argtypes = [dp, ctypes.c_double, ctypes.c_int, dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                             ctypes.c_int64, ctypes.c_void_p, dp, ctypes.c_int64, i32p, ctypes.c_void_p, dp, i32p,
+                             i32p, dp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), dp, ctypes.POINTER(ctypes.c_int),
+                             dp, ctypes.c_int, ctypes.c_int64, dp, dp, ctypes.c_int]
+    keep = []
+    if j1 is not None:
+        ions, start, fn1, sj1 = j1
+        ions = _f64(ions)
+        st = np.ascontiguousarray(np.asarray(start, dtype=np.int64))
+        rc = _f64(fn1.r_cut)
+        mm = np.ascontiguousarray(np.asarray(fn1.m, dtype=np.int32))
+        c1 = _f64(fn1.coef)
+        S1 = _f64(sj1).copy()
+        keep = [ions, st, rc, mm, c1, S1]
+        j1args = (len(fn1.m), st.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _dp(rc),
+                  mm.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), _dp(c1), c1.shape[1], ions.shape[1], _dp(ions),
+                  _dp(S1))
+    else:
+        S1 = None
+        j1args = (0, None, None, None, None, 0, 0, None, None)
+    r = Lb.orc_sweep(_dp(_f64(fn.L)), float(fn.r_cut), int(fn.m), _dp(_f64(fn.coef)), W, n, n_up, Np,
+                     R2.ctypes.data_as(ctypes.c_void_p), _dp(S2), S, ks.ctypes.data_as(i32p),
+                     dl.ctypes.data_as(ctypes.c_void_p), _dp(uu), None if fc is None else fc.ctypes.data_as(i32p),
+                     acc.ctypes.data_as(i32p), _dp(dj), *j1args, int(threads))
+    del keep
+    if r:
+        raise CoincidentError(f"walker {r - 1} has a coincident pair")
+    return R2, S2, acc, dj, S1
+
+
 def normalized_error_state(gpu, orc, absst, fn) -> np.ndarray:
     """Parity metric for the 5N state (NEXT-2): per entry
     |s_gpu - s_orc| / max(A, F) with A the oracle's absolute-term bound and F

@@ -734,3 +734,184 @@ void orc_gen_spo_table(uint64_t seed, int64_t nx, int64_t ny, int64_t nz, int64_
     for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
     free(jobs); free(th);
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-2 at the paper's system sizes: whole particle-by-particle sweeps      */
+/* (Alg. 1 L4-L9) of the Jastrow-only trial function.          */
+/*                                                                            */
+/* orc_propose_f32: Alg. 1 L5 "r'_k <- r_k + ... + delta" without the drift   */
+/* term (reading R24: the drift needs grad ln Psi_T including the           */
+/* determinant, out of scope), in fp32 -- the sweep's position type -- and    */
+/* wrapped into the periodic cell [0, L_d) (SPEC:138 cell convention):        */
+/*   x = r + delta (one fp32 rounding); if x < 0: x += L; if x >= L: x -= L.  */
+/* Precondition |delta| < L_d.  The second test also catches x + L rounding   */
+/* up to L exactly (the result is then 0, the same point of the torus).       */
+/* ------------------------------------------------------------------------ */
+void orc_propose_f32(const double L[3], int64_t n, const float *r, const float *delta, float *out)
+{
+    for (int64_t i = 0; i < n; ++i)
+        for (int c = 0; c < 3; ++c) {
+            const float Lf = (float)L[c];
+            float x = r[3 * i + c] + delta[3 * i + c];
+            if (x < 0.0f) x = x + Lf;
+            if (x >= Lf) x = x - Lf;
+            out[3 * i + c] = x;
+        }
+}
+
+/* One-body row of electron position r over the ions (the J1 values of        */
+/* orc_eval_j1 for one position, no absolute sums): o = (V, G, L).            */
+static int j1_row(const double L[3], int n_species, const int64_t *sp_start, const double *r_cut,
+                  const int *m, const double *coef, int coef_stride, int64_t Np, const double *ions,
+                  const double r[3], double o[5])
+{
+    nsum S[5];
+    for (int c = 0; c < 5; ++c) S[c].s = S[c].c = 0.0;
+    for (int s = 0; s < n_species; ++s)
+        for (int64_t I = sp_start[s]; I < sp_start[s + 1]; ++I) {
+            double src[3] = { ions[I], ions[Np + I], ions[2 * Np + I] };
+            double d[3], rho, u[3];
+            orc_min_image(L, r, src, d, &rho);
+            if (!(rho < r_cut[s])) continue;
+            if (rho == 0.0) return 1;
+            orc_bspline(coef + s * coef_stride, m[s], r_cut[s], rho, u);
+            nsum_add(&S[0], u[0]);
+            for (int c = 0; c < 3; ++c) nsum_add(&S[1 + c], -u[1] * d[c] / rho);
+            nsum_add(&S[4], u[2] + 2.0 * u[1] / rho);
+        }
+    for (int c = 0; c < 5; ++c) o[c] = nsum_get(&S[c]);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* orc_sweep: S particle-by-particle moves of every walker, in order, as the  */
+/* paper's compute-on-the-fly J2 does them (the 5N state     */
+/* holds U^2_e(R) of every electron so the ratio reuses it; only the row of   */
+/* the moved electron at R' is computed):                                     */
+/*   for s = 0..S-1, walker w, k = ks[s][w]:                                  */
+/*     r_k = R[w][:, k] (the walker's CURRENT position of k), r'_k =          */
+/*       orc_propose_f32(r_k, delta[s][w]);                                   */
+/*     T' = sum_{i != k} T_k(r'_k) (pair_terms with d = r'_k - r_i: V, G, L   */
+/*       of electron k at R');                                                */
+/*     dJ2 = T'_V - state[w][V][k]     (Eq. 5, with            */
+/*       U^2_k(R) = the stored state);                            */
+/*     with ions (n_species > 0): dJ1 = U^1_k(r'_k) - U^1_k(r_k) over the     */
+/*       ions, dJ = dJ1 + dJ2 (Eq. 4);                      */
+/*     own decision (Alg. 1 L9, reading R19): accept iff u[s][w] < rho^2,    */
+/*       rho = exp(dJ);                                                       */
+/*     the decision applied is forced[s][w] when forced != NULL (to replay a  */
+/*       trajectory whose decisions were taken elsewhere), else the own one;  */
+/*     on acceptance: the update of orc_accept (partners += T_i(r'_k) -       */
+/*       T_i(r_k), state_k = T', R[:, k] = r'_k) and, with ions, electron k's */
+/*       J1 row state_j1[w][:, k] = (V, G, L) of U^1 at r'_k.                 */
+/*   A move whose k is outside [0, N) changes nothing: acc_out = -1, dj = 0.  */
+/* R is fp32 (positions stay fp32 numbers: the proposal is fp32), states fp64.*/
+/* Outputs acc_out[s][w] (own decision 0/1, or -1), dj_out[s][w] (dJ).       */
+/* Walkers are independent (threads over walkers).  Returns 0, or 1 + w of    */
+/* the first walker with a coincident pair.                                   */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    const double *L; double r_cut; int m; const double *coef;
+    int64_t W, N, N_up, Np;
+    float *R; double *state;
+    int64_t S; const int32_t *ks; const float *delta; const double *u; const int32_t *forced;
+    int32_t *acc_out; double *dj_out;
+    int n_species; const int64_t *sp_start; const double *r_cut1; const int *m1; const double *coef1;
+    int coef1_stride; int64_t Np_ion; const double *ions; double *state_j1;
+    int64_t w0, w1, status;
+} sweep_job;
+
+static int64_t sweep_walker(sweep_job *J, int64_t w)
+{
+    const int mc = J->m + 3;
+    const int64_t Np = J->Np;
+    float *Rw = J->R + w * 3 * Np;
+    double *Sw = J->state + w * 5 * Np;
+    for (int64_t s = 0; s < J->S; ++s) {
+        const int64_t sw = s * J->W + w;
+        const int64_t k = J->ks[sw];
+        if (k < 0 || k >= J->N) { J->acc_out[sw] = -1; J->dj_out[sw] = 0.0; continue; }
+        float rkf[3] = { Rw[k], Rw[Np + k], Rw[2 * Np + k] }, rnf[3];
+        orc_propose_f32(J->L, 1, rkf, J->delta + 3 * sw, rnf);
+        const double rk[3] = { rkf[0], rkf[1], rkf[2] }, rn[3] = { rnf[0], rnf[1], rnf[2] };
+        nsum Tk[5];
+        for (int c = 0; c < 5; ++c) Tk[c].s = Tk[c].c = 0.0;
+        for (int64_t i = 0; i < J->N; ++i) {
+            if (i == k) continue;
+            const double ri[3] = { Rw[i], Rw[Np + i], Rw[2 * Np + i] };
+            double t[5], a[5];
+            if (pair_terms(J->L, J->r_cut, J->m, J->coef + spin_channel(i, k, J->N_up) * mc, rn, ri, t, a))
+                return 1;
+            for (int c = 0; c < 5; ++c) nsum_add(&Tk[c], t[c]);
+        }
+        double dj = nsum_get(&Tk[0]) - Sw[k];
+        double o1n[5] = {0, 0, 0, 0, 0};
+        if (J->n_species > 0) {
+            double o1o[5];
+            if (j1_row(J->L, J->n_species, J->sp_start, J->r_cut1, J->m1, J->coef1, J->coef1_stride, J->Np_ion,
+                       J->ions, rn, o1n) ||
+                j1_row(J->L, J->n_species, J->sp_start, J->r_cut1, J->m1, J->coef1, J->coef1_stride, J->Np_ion,
+                       J->ions, rk, o1o))
+                return 1;
+            dj += o1n[0] - o1o[0];
+        }
+        const double rho = exp(dj);
+        const int own = J->u[sw] < rho * rho ? 1 : 0;
+        J->acc_out[sw] = own;
+        J->dj_out[sw] = dj;
+        const int a = J->forced ? (J->forced[sw] > 0) : own;
+        if (!a) continue;
+        for (int64_t i = 0; i < J->N; ++i) {
+            if (i == k) continue;
+            const double *cs = J->coef + spin_channel(i, k, J->N_up) * mc;
+            const double ri[3] = { Rw[i], Rw[Np + i], Rw[2 * Np + i] };
+            double tn[5], to[5], an[5], ao[5];
+            if (pair_terms(J->L, J->r_cut, J->m, cs, ri, rn, tn, an)) return 1;   /* d = r_i - r'_k */
+            if (pair_terms(J->L, J->r_cut, J->m, cs, ri, rk, to, ao)) return 1;   /* d = r_i - r_k  */
+            for (int c = 0; c < 5; ++c) Sw[c * Np + i] += tn[c] - to[c];
+        }
+        for (int c = 0; c < 5; ++c) Sw[c * Np + k] = nsum_get(&Tk[c]);
+        for (int c = 0; c < 3; ++c) Rw[c * Np + k] = rnf[c];
+        if (J->n_species > 0)
+            for (int c = 0; c < 5; ++c) J->state_j1[(w * 5 + c) * Np + k] = o1n[c];
+    }
+    return 0;
+}
+
+static void *sweep_thread(void *arg)
+{
+    sweep_job *J = (sweep_job *)arg;
+    J->status = 0;
+    for (int64_t w = J->w0; w < J->w1 && !J->status; ++w)
+        if (sweep_walker(J, w)) J->status = 1 + w;
+    return NULL;
+}
+
+int64_t orc_sweep(const double L[3], double r_cut, int m, const double *coef,
+                  int64_t W, int64_t N, int64_t N_up, int64_t Np, float *R, double *state,
+                  int64_t S, const int32_t *ks, const float *delta, const double *u, const int32_t *forced,
+                  int32_t *acc_out, double *dj_out,
+                  int n_species, const int64_t *sp_start, const double *r_cut1, const int *m1,
+                  const double *coef1, int coef1_stride, int64_t Np_ion, const double *ions,
+                  double *state_j1, int nthreads)
+{
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > W) nthreads = (int)(W > 0 ? W : 1);
+    sweep_job *jobs = (sweep_job *)calloc((size_t)nthreads, sizeof(sweep_job));
+    pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+    int64_t per = (W + nthreads - 1) / nthreads;
+    for (int t = 0; t < nthreads; ++t) {
+        sweep_job J = { L, r_cut, m, coef, W, N, N_up, Np, R, state, S, ks, delta, u, forced, acc_out, dj_out,
+                        n_species, sp_start, r_cut1, m1, coef1, coef1_stride, Np_ion, ions, state_j1, 0, 0, 0 };
+        J.w0 = t * per < W ? t * per : W;
+        J.w1 = (t + 1) * per < W ? (t + 1) * per : W;
+        jobs[t] = J;
+    }
+    for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, sweep_thread, &jobs[t]);
+    sweep_thread(&jobs[0]);
+    for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+    int64_t st = 0;
+    for (int t = 0; t < nthreads && !st; ++t) st = jobs[t].status;
+    free(jobs); free(th);
+    return st;
+}

@@ -29,7 +29,7 @@ import torch
 from . import _build
 
 __all__ = ["QJ2Error", "Functor", "J1Functor", "Workspace", "eval", "eval_j1", "accept", "metropolis",
-           "metropolis_accept", "sweep", "SpoTable",
+           "metropolis_accept", "sweep", "state_init", "SpoTable",
            "spo_eval", "gen_spo_table", "eval_host", "ratio", "functor_eval_vgl",
            "min_image_disp", "check_inputs", "padded_size", "gen_positions", "lib_path",
            "workspace_size", "host_workspace_size", "version", "device_check"]
@@ -104,6 +104,7 @@ def _load():
         "qj2_metropolis": (ctypes.c_int, [i64, vp, i64, vp, vp, vp]),
         "qj2_sweep": (ctypes.c_int, [F, i64, i64, i64, i64, vp, vp, i64, vp, vp, vp, vp, vp,
                                      ctypes.POINTER(_SweepJ1), vp]),
+        "qj2_state_init": (ctypes.c_int, [F, i64, i64, i64, i64, vp, vp, ctypes.POINTER(_SweepJ1), vp]),
         "qj2_metropolis_accept": (ctypes.c_int, [F, ctypes.c_int, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, i64,
                                                  vp, vp, i64, i64, vp, vp, vp]),
         "qj2_spo_eval": (ctypes.c_int, [ctypes.POINTER(_SpoTable), i32, ctypes.c_int, i64, vp, i64, vp, i64, i64,
@@ -132,7 +133,7 @@ def _load():
 _lib = _load()
 EXPORTS = ("qj2_version", "qj2_status_string", "qj2_last_error", "qj2_device_check", "qj2_padded_size",
            "qj2_eval_workspace_size", "qj2_eval", "qj2_ratio", "qj2_eval_j1", "qj2_accept_workspace_size",
-           "qj2_accept", "qj2_metropolis", "qj2_metropolis_accept", "qj2_sweep", "qj2_spo_eval", "qj2gen_spo_table", "qj2_eval_host_workspace_size",
+           "qj2_accept", "qj2_metropolis", "qj2_metropolis_accept", "qj2_sweep", "qj2_state_init", "qj2_spo_eval", "qj2gen_spo_table", "qj2_eval_host_workspace_size",
            "qj2_eval_host", "qj2_functor_eval_vgl", "qj2_min_image_disp", "qj2_check_inputs",
            "qj2gen_positions")
 
@@ -204,6 +205,11 @@ def _req(t: torch.Tensor, name: str, dtype=None, ndim=None):
         raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
     if ndim is not None and t.dim() != ndim:
         raise ValueError(f"{name} must have {ndim} dims, got {t.dim()}")
+
+
+def _shape(t: torch.Tensor, name: str, shape):
+    if tuple(t.shape) != tuple(int(x) for x in shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
 
 
 def padded_size(n: int, block: int) -> int:
@@ -442,40 +448,78 @@ def metropolis_accept(R, state, k, r_trial, out, u, fn, n_total: int, n_up: int,
     return acc
 
 
-def sweep(R, state, ks, trials, u, fn, n: int, n_up: int, *, acc=None, dj=None, j1=None, stream=None):
+def _sweep_j1(j1, W, Np):
+    """(ctypes qj2_sweep_j1, objects to keep alive) for j1 = (ions [3][Np_ion] fp32,
+    species_start, fn1, state_j1 [W][5][Np] fp32) or None."""
+    if j1 is None:
+        return None, []
+    ions, start, fn1, state_j1 = j1
+    _req(ions, "ions", torch.float32, 2)
+    if ions.shape[0] != 3:
+        raise ValueError("ions must be [3][Np_ion]")
+    _req(state_j1, "state_j1", torch.float32, 3)
+    _shape(state_j1, "state_j1", (W, 5, Np))
+    f1 = J1Functor.of(fn1)
+    if len(start) != len(f1.m) + 1 or int(start[-1]) > ions.shape[1]:
+        raise ValueError("species_start must have n_species + 1 entries and end <= Np_ion")
+    st = (ctypes.c_int64 * (len(f1.m) + 1))(*[int(x) for x in start])
+    s1 = _SweepJ1(ctypes.addressof(f1._c), st, ions.data_ptr(), ions.shape[1], state_j1.data_ptr())
+    return ctypes.byref(s1), [f1, st, s1]
+
+
+def sweep(R, state, ks, delta, u, fn, n: int, n_up: int, *, acc=None, dj=None, j1=None, stream=None):
     """qj2_sweep: S particle-by-particle moves of every walker in one launch,
     walkers resident in shared memory (N <= 1024, fp32, functor m <= 16).
-    R [W][3][Np], state [W][5][Np] fp32 (in place); ks [S][W] int32, trials
-    [S][W][2][3] fp32 (r_k, r'_k), u [S][W] fp64.  j1 = (ions [3][Np_ion] fp32,
+    R [W][3][Np], state [W][5][Np] fp32 (in place, consistent with R: see
+    state_init); ks [S][W] int32, delta [S][W][3] fp32 (r'_k = wrap(r_k + delta)
+    from the walker's current r_k), u [S][W] fp64.  j1 = (ions [3][Np_ion] fp32,
     species_start, fn1, state_j1 [W][5][Np] fp32) adds the one-body Jastrow to
     every move's ratio.  Returns (acc [S][W] int32, dj [S][W] fp64)."""
     _req(R, "R", torch.float32, 3)
-    W, _, Np = R.shape
+    W, three, Np = R.shape
+    if three != 3:
+        raise ValueError("R must be [W][3][Np]")
     _req(state, "state", torch.float32, 3)
+    _shape(state, "state", (W, 5, Np))
     _req(ks, "ks", torch.int32, 2)
-    _req(trials, "trials", torch.float32, 4)
-    _req(u, "u", torch.float64, 2)
     S = ks.shape[0]
+    _shape(ks, "ks", (S, W))
+    _req(delta, "delta", torch.float32, 3)
+    _shape(delta, "delta", (S, W, 3))
+    _req(u, "u", torch.float64, 2)
+    _shape(u, "u", (S, W))
     if acc is None:
         acc = torch.empty((S, W), dtype=torch.int32, device=R.device)
+    _req(acc, "acc", torch.int32, 2)
+    _shape(acc, "acc", (S, W))
     if dj is None:
         dj = torch.empty((S, W), dtype=torch.float64, device=R.device)
+    _req(dj, "dj", torch.float64, 2)
+    _shape(dj, "dj", (S, W))
     f = Functor.of(fn)
-    j1p = None
-    keep = []
-    if j1 is not None:
-        ions, start, fn1, state_j1 = j1
-        _req(ions, "ions", torch.float32, 2)
-        _req(state_j1, "state_j1", torch.float32, 3)
-        f1 = J1Functor.of(fn1)
-        st = (ctypes.c_int64 * (len(f1.m) + 1))(*[int(x) for x in start])
-        s1 = _SweepJ1(ctypes.addressof(f1._c), st, ions.data_ptr(), ions.shape[1], state_j1.data_ptr())
-        keep = [f1, st, s1]
-        j1p = ctypes.byref(s1)
-    _check(_lib.qj2_sweep(f.ptr, W, n, n_up, Np, _ptr(R), _ptr(state), S, _ptr(ks), _ptr(trials), _ptr(u),
+    j1p, keep = _sweep_j1(j1, W, Np)
+    _check(_lib.qj2_sweep(f.ptr, W, n, n_up, Np, _ptr(R), _ptr(state), S, _ptr(ks), _ptr(delta), _ptr(u),
                           _ptr(acc), _ptr(dj), j1p, ctypes.c_void_p(_stream_ptr(stream))), "qj2_sweep")
     del keep
     return acc, dj
+
+
+def state_init(R, state, fn, n: int, n_up: int, *, j1=None, stream=None):
+    """qj2_state_init: the 5N J2 state of every electron from scratch into
+    state [W][5][Np] fp32 (and, with j1 as for sweep(), every electron's J1 row
+    into state_j1).  R [W][3][Np] fp32.  Returns state."""
+    _req(R, "R", torch.float32, 3)
+    W, three, Np = R.shape
+    if three != 3:
+        raise ValueError("R must be [W][3][Np]")
+    _req(state, "state", torch.float32, 3)
+    _shape(state, "state", (W, 5, Np))
+    f = Functor.of(fn)
+    j1p, keep = _sweep_j1(j1, W, Np)
+    _check(_lib.qj2_state_init(f.ptr, W, n, n_up, Np, _ptr(R), _ptr(state), j1p,
+                               ctypes.c_void_p(_stream_ptr(stream))), "qj2_state_init")
+    del keep
+    return state
 
 
 def metropolis(ratio_out, u, acc=None, *, trial: int = 0, stream=None):

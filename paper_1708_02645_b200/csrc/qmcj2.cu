@@ -614,18 +614,16 @@ qj2_status qj2_metropolis_accept(const qj2_functor *fn, qj2_dtype dtype,
     return e == cudaSuccess ? QJ2_OK : cuda_fail(e, "j2_accept_kernel launch");
 }
 
-qj2_status qj2_sweep(const qj2_functor *fn, int64_t W, int64_t N, int64_t N_up, int64_t Np,
-                     float *R, float *state, int64_t S, const int32_t *ks, const float *trials,
-                     const double *u, int32_t *accept, double *dj, const qj2_sweep_j1 *j1,
-                     void *stream) {
+// Shared validation and parameter set-up of qj2_sweep / qj2_state_init.
+static qj2_status sweep_params(const qj2_functor *fn, int64_t W, int64_t N, int64_t N_up, int64_t Np,
+                               const qj2_sweep_j1 *j1, SweepParams &p) {
     qj2_status st = validate_functor(fn);
     if (st) return st;
     if (fn->m > ACCEPT_FAST_MAX_M)
-        return fail(QJ2_EINVAL, "qj2_sweep keeps fp32 pair terms: m must be <= %d (use qj2_eval + "
+        return fail(QJ2_EINVAL, "the resident-walker kernels keep fp32 pair terms: m must be <= %d (use qj2_eval + "
                     "qj2_metropolis_accept per move for finer functors)", ACCEPT_FAST_MAX_M);
-    if (W < 0 || S < 0) return fail(QJ2_EINVAL, "W and S must be >= 0");
-    if (N < 2 || N > SW_MAXN) return fail(QJ2_EINVAL, "qj2_sweep needs 2 <= N <= %d (walker resident in "
-                                          "shared memory)", SW_MAXN);
+    if (W < 0) return fail(QJ2_EINVAL, "W must be >= 0");
+    if (N < 2 || N > SW_MAXN) return fail(QJ2_EINVAL, "need 2 <= N <= %d (walker resident in shared memory)", SW_MAXN);
     if (N_up < 0 || N_up > N) return fail(QJ2_ERANGE, "N_up out of [0, N]");
     if (Np < N) return fail(QJ2_EINVAL, "Np must be >= N");
     if (W > 0x7fffffffLL) return fail(QJ2_EINVAL, "W too large for one launch");
@@ -635,28 +633,25 @@ qj2_status qj2_sweep(const qj2_functor *fn, int64_t W, int64_t N, int64_t N_up, 
         if (st) return st;
         for (int d = 0; d < 3; ++d)
             if (j1->fn->L[d] != fn->L[d]) return fail(QJ2_EINVAL, "the J1 and J2 functors must share the cell");
+        for (int sp = 0; sp < j1->fn->n_species; ++sp)
+            if (j1->fn->m[sp] > ACCEPT_FAST_MAX_M)
+                return fail(QJ2_EINVAL, "the resident-walker kernels keep fp32 J1 terms: m[%d] must be <= %d", sp,
+                            ACCEPT_FAST_MAX_M);
         if (!j1->species_start || j1->species_start[0] != 0)
             return fail(QJ2_EINVAL, "j1->species_start must be non-NULL with species_start[0] == 0");
         for (int sp = 0; sp < j1->fn->n_species; ++sp)
             if (j1->species_start[sp + 1] < j1->species_start[sp])
                 return fail(QJ2_EINVAL, "j1->species_start must be nondecreasing");
         n_ions = j1->species_start[j1->fn->n_species];
-        if (n_ions < 1 || n_ions > SW_MAX_IONS) return fail(QJ2_EINVAL, "qj2_sweep takes 1..%d ions", SW_MAX_IONS);
+        if (n_ions < 1 || n_ions > SW_MAX_IONS) return fail(QJ2_EINVAL, "the resident-walker kernels take 1..%d ions",
+                                                            SW_MAX_IONS);
         if (j1->Np_ion < n_ions) return fail(QJ2_EINVAL, "j1->Np_ion must be >= the number of ions");
     }
-    if (W == 0 || S == 0) return QJ2_OK;
-    if (!R || !state || !ks || !trials || !u || !accept)
-        return fail(QJ2_EINVAL, "R, state, ks, trials, u and accept must be non-NULL");
-    if (j1 && (!j1->ions || !j1->state)) return fail(QJ2_EINVAL, "j1->ions and j1->state must be non-NULL");
-    st = check_device();
-    if (st) return st;
-    SweepParams p;
     memset(&p, 0, sizeof p);
-    p.W = W; p.N = N; p.N_up = N_up; p.Np = Np; p.S = S;
+    p.W = (int32_t)W; p.N = (int32_t)N; p.N_up = (int32_t)N_up; p.Np = Np;
     p.m = fn->m;
     p.inv_delta = (double)fn->m / fn->r_cut;
     p.invd = (float)p.inv_delta;
-    p.R = R; p.state = state; p.ks = ks; p.trials = trials; p.u = u; p.acc = accept; p.dj = dj;
     for (int d = 0; d < 3; ++d) p.L[d] = (float)fn->L[d];
     power_basis(fn->coef[0], fn->m, p.pcoef);
     power_basis(fn->coef[1], fn->m, p.pcoef + (fn->m + 1));
@@ -676,8 +671,42 @@ qj2_status qj2_sweep(const qj2_functor *fn, int64_t W, int64_t N, int64_t N_up, 
         p.n_rows1 = row;
         p.ions = j1->ions; p.Np_ion = j1->Np_ion; p.state_j1 = j1->state;
     }
+    return QJ2_OK;
+}
+
+qj2_status qj2_sweep(const qj2_functor *fn, int64_t W, int64_t N, int64_t N_up, int64_t Np,
+                     float *R, float *state, int64_t S, const int32_t *ks, const float *delta,
+                     const double *u, int32_t *accept, double *dj, const qj2_sweep_j1 *j1,
+                     void *stream) {
+    SweepParams p;
+    qj2_status st = sweep_params(fn, W, N, N_up, Np, j1, p);
+    if (st) return st;
+    if (S < 0 || S > 0x7fffffffLL) return fail(QJ2_EINVAL, "S must be in [0, 2^31)");
+    if (W == 0 || S == 0) return QJ2_OK;
+    if (!R || !state || !ks || !delta || !u || !accept)
+        return fail(QJ2_EINVAL, "R, state, ks, delta, u and accept must be non-NULL");
+    if (j1 && (!j1->ions || !j1->state)) return fail(QJ2_EINVAL, "j1->ions and j1->state must be non-NULL");
+    st = check_device();
+    if (st) return st;
+    p.S = S;
+    p.R = R; p.state = state; p.ks = ks; p.delta = delta; p.u = u; p.acc = accept; p.dj = dj;
     cudaError_t e = launch_sweep(p, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? QJ2_OK : cuda_fail(e, "j2_sweep_kernel launch");
+}
+
+qj2_status qj2_state_init(const qj2_functor *fn, int64_t W, int64_t N, int64_t N_up, int64_t Np,
+                          const float *R, float *state, const qj2_sweep_j1 *j1, void *stream) {
+    SweepParams p;
+    qj2_status st = sweep_params(fn, W, N, N_up, Np, j1, p);
+    if (st) return st;
+    if (W == 0) return QJ2_OK;
+    if (!R || !state) return fail(QJ2_EINVAL, "R and state must be non-NULL");
+    if (j1 && (!j1->ions || !j1->state)) return fail(QJ2_EINVAL, "j1->ions and j1->state must be non-NULL");
+    st = check_device();
+    if (st) return st;
+    p.R = const_cast<float *>(R); p.state = state;
+    cudaError_t e = launch_state_init(p, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? QJ2_OK : cuda_fail(e, "state_init_kernel launch");
 }
 
 qj2_status qj2_metropolis(int64_t W, const double *ratio, int64_t ratio_stride,

@@ -1,62 +1,72 @@
-// sweep.cu -- the resident-walker sweep kernel (qj2_sweep) and its launch.
-// The design, in order of the per-move steps, is in sweep.cuh and DESIGN.md section 7.
-#include <cstdlib>
-
+// sweep.cu -- the resident-walker sweep kernel (qj2_sweep), the from-scratch
+// state kernel (qj2_state_init) and their launches.  The design, in order of
+// the per-move steps, is in sweep.cuh and DESIGN.md section 7.
 #include "sweep.cuh"
 
 namespace qj2 {
 
-// Template parameters:
+// Template parameters of the sweep kernel:
 //   TPB  threads per walker (one CTA per walker): 128 for 384 < N <= 768, else 256;
-//   SPT  partners per thread, ceil(N / TPB); only the five differences
-//        T_i(r'_k) - T_i(r_k) are kept per partner;
+//   SPT  partners per thread, ceil(N / TPB); the five pair terms at r'_k are kept
+//        per partner between the ratio and the update;
 //   J1   the one-body Jastrow over the (<= 256) ions joins each move's ratio;
-//   FULL N == TPB * SPT (NiO-64's 768 = 128 x 6, 1024 = 256 x 4): the shared-memory
-//        layout and the partner bounds are compile-time constants.
-// CTAs per SM at 128 threads: 7 without J1 (72 registers, no spills; 148 x 7 = 1036
-// walkers in one wave), 8 with J1 (64 registers) -- measured: N64S 3.28 ms at 7 vs 3.52
-// at 8, N64SJ 3.82 at 8 vs 3.87 at 7 (profiles/r01_s4/ab_minb.log).  QJ2_SWEEP_MINB_J1:
-// A/B builds only.
-#ifndef QJ2_SWEEP_MINB_J1
-#define QJ2_SWEEP_MINB_J1 8
-#endif
+//   FULL N == TPB * SPT with N_up = N / 2 and SPT even (NiO-64's 768 = 128 x 6, 1024 =
+//        256 x 4): the shared-memory layout, the partner bounds and every partner's spin
+//        half (j < SPT/2: up) are compile-time constants.
+// 128 threads at <= 72 registers: 7 CTAs per SM, 148 x 7 = 1036 walkers in one wave.
 template <int TPB, int SPT, bool J1>
 constexpr int sweep_minb() {
-    return TPB == 128 ? (SPT <= 6 ? (J1 ? QJ2_SWEEP_MINB_J1 : 7) : 4) : (SPT <= 3 ? (J1 ? 3 : 4) : 2);
+    return TPB == 128 ? (SPT <= 6 ? 7 : 4) : (SPT <= 3 ? (J1 ? 3 : 4) : 2);
 }
 
-template <int TPB, int SPT, bool J1, bool FULL>
-__global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kernel(const __grid_constant__ SweepParams p) {
-    constexpr int NV = J1 ? 12 : 6;           // reduced values per move: dJ and the terms at r'_k (J2, J1)
-    constexpr int NW = TPB / 32;
-    extern __shared__ __align__(16) float sw_smem[];
-    const int64_t w = blockIdx.x;
-    const int N = FULL ? TPB * SPT : (int)p.N;
-    // dynamic shared memory, sized by the call (every byte counts at 7-8 CTAs/SM):
-    // R (SoA) [3][N] | state [5][N] | J2 table [2(m+1)] | J1 table [n_rows1] | ions [n_ions] (2 arrays)
-    float *rx = sw_smem, *ry = rx + N, *rz = ry + N;
-    float *st = rz + N;
-    Coef4<float> *tab = reinterpret_cast<Coef4<float> *>(sw_smem + 8 * N);
-    Coef4<float> *tab1 = tab + 2 * (p.m + 1);
-    // per ion, resolved once: (x, y, z, 1/delta_s) and (table row base, m_s) of its species
-    float4 *ion_p = reinterpret_cast<float4 *>(tab1 + (J1 ? p.n_rows1 : 0));
-    uint2 *ion_c = reinterpret_cast<uint2 *>(ion_p + (J1 ? p.n_ions : 0));
-    __shared__ double red2[2][NW][NV];               // double-buffered by move parity
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int e = tid; e < 2 * (p.m + 1); e += TPB) {
+// The proposal of Alg. 1 L5 without drift (reading R24): r + delta in fp32, wrapped
+// into [0, L) (|delta| < L): the oracle's orc_propose_f32, operation for operation.
+__device__ __forceinline__ float propose(float r, float d, float L) {
+    float x = __fadd_rn(r, d);
+    if (x < 0.0f) x = __fadd_rn(x, L);
+    if (x >= L) x = __fadd_rn(x, -L);
+    return x;
+}
+
+// Pair terms of one partner at (x, y, z) against a position's axes, with the eval
+// kernel's fp32 arithmetic, in raw units: t = (U, g dx, g dy, g dz, h invd + g),
+// g = U' delta / r, h = U'' delta^2 / 2, d = partner - position.  A dead partner
+// (r^2 forced to 1e30, i.e. onto the all-zero interval) gives exactly 0.
+__device__ __forceinline__ void pair_raw(float x, float y, float z, const Axis<float> (&a)[3], bool live,
+                                         uint32_t base, unsigned clamp, float invd, float (&t)[5]) {
+    const float dx = min_image(x, a[0]), dy = min_image(y, a[1]), dz = min_image(z, a[2]);
+    float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+    r2 = live ? r2 : 1e30f;
+    const float ir = Traits<float>::rsqrt(r2);
+    const FunctorEval<float> e = functor_from_t<float>(r2 * ir * invd, base, clamp);
+    const float g = e.du * ir;
+    t[0] = e.u;
+    t[1] = g * dx;
+    t[2] = g * dy;
+    t[3] = g * dz;
+    t[4] = fmaf(e.h, invd, g);
+}
+
+// Shared-memory staging common to both kernels: the J2 power-basis table (same-spin
+// rows [0, m], opposite-spin rows [m+1, 2m+1]) and, with J1, the species tables and
+// per ion (x, y, z, 1/delta_s) and (table row address, m_s) of its species.
+template <bool J1>
+__device__ __forceinline__ void stage_tables(const SweepParams &p, Coef4<float> *tab, Coef4<float> *tab1,
+                                             float4 *ion_p, uint2 *ion_c, int tid, int nthr) {
+    for (int e = tid; e < 2 * (p.m + 1); e += nthr) {
         Coef4<float> c;
         c.a0 = (float)p.pcoef[e][0]; c.a1 = (float)p.pcoef[e][1];
         c.a2 = (float)p.pcoef[e][2]; c.a3 = (float)p.pcoef[e][3];
         tab[e] = c;
     }
     if constexpr (J1) {
-        for (int e = tid; e < p.n_rows1; e += TPB) {
+        for (int e = tid; e < p.n_rows1; e += nthr) {
             Coef4<float> c;
             c.a0 = (float)p.pcoef1[e][0]; c.a1 = (float)p.pcoef1[e][1];
             c.a2 = (float)p.pcoef1[e][2]; c.a3 = (float)p.pcoef1[e][3];
             tab1[e] = c;
         }
-        for (int j = tid; j < p.n_ions; j += TPB) {
+        for (int j = tid; j < p.n_ions; j += nthr) {
             int sp = 0;
 #pragma unroll
             for (int b = 1; b < QJ2_MAX_SPECIES; ++b) sp += (b < p.n_species && j >= p.sp_start[b]) ? 1 : 0;
@@ -66,97 +76,129 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
                                   (uint32_t)p.sp_m[sp]);
         }
     }
-    const float *Rg = p.R + w * 3 * p.Np;
-    const float *Sg = p.state + w * 5 * p.Np;
-    for (int i = tid; i < N; i += TPB) {
-        rx[i] = Rg[i]; ry[i] = Rg[p.Np + i]; rz[i] = Rg[2 * p.Np + i];
-#pragma unroll
-        for (int c = 0; c < 5; ++c) st[c * N + i] = Sg[c * p.Np + i];
-    }
-    __syncthreads();
-    const uint32_t tab0 = (uint32_t)__cvta_generic_to_shared(tab);
-    const uint32_t tab_opp = tab0 + (uint32_t)((p.m + 1) * (int)sizeof(Coef4<float>));
-    const unsigned clamp = (unsigned)p.m;
-    const float invd = p.invd;
+}
 
-    for (int64_t s = 0; s < p.S; ++s) {
-        // k outside [0, N) (a precondition): no partner is excluded, the move is never
-        // accepted (nothing is written) and its accept entry is -1
-        const int k = p.ks[s * p.W + w];
-        const float *tr = p.trials + (s * p.W + w) * 6;
-        Axis<float> a0[3], a1[3];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            a0[d] = make_axis<float>(tr[d], p.L[d]);
-            a1[d] = make_axis<float>(tr[3 + d], p.L[d]);
-        }
-        const bool k_up = k < p.N_up;
-        // 1. pair terms at r_k (q = 0) and r'_k (q = 1): their differences are kept per
-        //    partner (the update), summed over partners only where a move needs the sum:
-        //    dv = sum_i U(r'_k) - U(r_k) (dJ2) and acc = the terms at r'_k (state_k)
-        // position-outer: only one position's axes are live (64 registers, no spills)
-        float d[SPT][5];
-        float dv = 0.f, acc[5];
-#pragma unroll
-        for (int c = 0; c < 5; ++c) acc[c] = 0.f;
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const Axis<float>(&a)[3] = q ? a1 : a0;
+// Moves s0 .. s0 + SW_MCH - 1 (those < S) of walker w into shared memory: k, delta, u.
+constexpr int SW_MCH = 32;
+__device__ __forceinline__ void stage_moves(const SweepParams &p, int w, int64_t s0, int *mk, float (*md)[3],
+                                            double *mu, int tid, int nthr) {
+    for (int e = tid; e < 5 * SW_MCH; e += nthr) {
+        const int j = e < SW_MCH ? e : (e < 4 * SW_MCH ? (e - SW_MCH) / 3 : e - 4 * SW_MCH);
+        const int64_t s = s0 + j;
+        if (s >= p.S) continue;
+        const int64_t sw = s * p.W + w;
+        if (e < SW_MCH) mk[j] = p.ks[sw];
+        else if (e < 4 * SW_MCH) { const int c = (e - SW_MCH) % 3; md[j][c] = p.delta[sw * 3 + c]; }
+        else mu[j] = p.u[sw];
+    }
+}
+
+template <int TPB, int SPT, bool J1, bool FULL>
+__global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kernel(const __grid_constant__ SweepParams p) {
+    constexpr int NV = J1 ? 11 : 5;           // reduced values: sums at r'_k (J2: V, Gx, Gy, Gz, L); J1: dJ1 + 5
+    constexpr int NW = TPB / 32;
+    extern __shared__ __align__(16) float sw_smem[];
+    const int w = blockIdx.x;
+    const int N = FULL ? TPB * SPT : p.N;
+    // dynamic shared memory, sized by the call (every byte counts at 7 CTAs/SM), one 16-byte
+    // vector per electron and array, so a partner is one LDS.128 (and its state one more):
+    // P4 [N] = (x, y, z, L) | S4 [N] = (V, Gx, Gy, Gz) (state in physical units) |
+    // J2 table [2(m+1)] | J1 table | ions (2 arrays)
+    float4 *P4 = reinterpret_cast<float4 *>(sw_smem);
+    float4 *S4 = P4 + N;
+    Coef4<float> *tab = reinterpret_cast<Coef4<float> *>(sw_smem + 8 * N);
+    Coef4<float> *tab1 = tab + 2 * (p.m + 1);
+    float4 *ion_p = reinterpret_cast<float4 *>(tab1 + (J1 ? p.n_rows1 : 0));
+    uint2 *ion_c = reinterpret_cast<uint2 *>(ion_p + (J1 ? p.n_ions : 0));
+    __shared__ double red2[2][NW][NV];               // double-buffered by move parity
+    __shared__ float vk2[2];                         // U^2_k(R) published by the owner of slot k
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    stage_tables<J1>(p, tab, tab1, ion_p, ion_c, tid, TPB);
+    const float *Rg = p.R + (int64_t)w * 3 * p.Np;
+    const float *Sg = p.state + (int64_t)w * 5 * p.Np;
+    for (int i = tid; i < N; i += TPB) {
+        P4[i] = make_float4(Rg[i], Rg[p.Np + i], Rg[2 * p.Np + i], Sg[4 * p.Np + i]);
+        S4[i] = make_float4(Sg[i], Sg[p.Np + i], Sg[2 * p.Np + i], Sg[3 * p.Np + i]);
+    }
+    __shared__ int mv_k[2][SW_MCH];
+    __shared__ float mv_d[2][SW_MCH][3];
+    __shared__ double mv_u[2][SW_MCH];
+    stage_moves(p, w, 0, mv_k[0], mv_d[0], mv_u[0], tid, TPB);
+    __syncthreads();
+    const uint32_t tab_s = (uint32_t)__cvta_generic_to_shared(tab);
+    const uint32_t tab_o = tab_s + (uint32_t)((p.m + 1) * (int)sizeof(Coef4<float>));
+    const unsigned clamp = (unsigned)p.m;
+    const float invd = p.invd, sl = 2.f * p.invd;
+    const int n_up = p.N_up;
+    const float L0 = p.L[0], L1 = p.L[1], L2 = p.L[2];
+
+    int prev_k = -1;
+    bool prev_acc = false;
+    const int S = (int)p.S;
+    for (int s = 0; s < S; ++s) {
+        const int b = (s / SW_MCH) & 1, jm = s % SW_MCH;
+        // the moves are staged SW_MCH at a time: chunk c + 1 is loaded during the second
+        // move of chunk c, into the buffer of chunk c - 1 (whose last reads, u after the
+        // barrier of move SW_MCH*c - 1, precede the barrier of move SW_MCH*c); it is
+        // visible after that move's barrier
+        if (jm == 1 && s - 1 + SW_MCH < S)
+            stage_moves(p, w, s - 1 + SW_MCH, mv_k[b ^ 1], mv_d[b ^ 1], mv_u[b ^ 1], tid, TPB);
+        const int k = mv_k[b][jm];
+        const float dlx = mv_d[b][jm][0], dly = mv_d[b][jm][1], dlz = mv_d[b][jm][2];
+        // k outside [0, N) (a precondition): the move is never accepted and flagged -1
+        const bool k_ok = (unsigned)k < (unsigned)N;
+        const int kk = k_ok ? k : 0;
+        // r_k was written by its owner in the previous move (the same electron moved
+        // twice in a row): make the write visible before everyone reads it
+        if (kk == prev_k && prev_acc) __syncthreads();
+        const float4 pk = P4[kk];
+        const float xk = pk.x, yk = pk.y, zk = pk.z;
+        const float xn = propose(xk, dlx, L0), yn = propose(yk, dly, L1), zn = propose(zk, dlz, L2);
+        const bool k_up = kk < n_up;
+        const uint32_t bu = k_up ? tab_s : tab_o, bd = k_up ? tab_o : tab_s;   // partner spin up / down
+        if (tid == (kk & (TPB - 1))) vk2[s & 1] = S4[kk].x;                   // U^2_k(R), the stored state
+        // 1. pair terms at r'_k, kept per partner; their sums are electron k's values at R'
+        float t1[SPT][5];
+        float acc[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+        {
+            Axis<float> a1[3];
+            a1[0] = make_axis<float>(xn, L0);
+            a1[1] = make_axis<float>(yn, L1);
+            a1[2] = make_axis<float>(zn, L2);
 #pragma unroll
             for (int j = 0; j < SPT; ++j) {
                 const int i = tid + j * TPB;
-                const bool live = (FULL || i < N) && i != k;
-                const int ii = (FULL || i < N) ? i : 0;
-                const float x = rx[ii], y = ry[ii], z = rz[ii];
-                const uint32_t base = ((ii < p.N_up) == k_up) ? tab0 : tab_opp;
-                const float dx = min_image(x, a[0]), dy = min_image(y, a[1]), dz = min_image(z, a[2]);
-                float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-                r2 = live ? r2 : 1e30f;            // the zero row: every term exactly 0
-                const float ir = Traits<float>::rsqrt(r2);
-                const FunctorEval<float> e = functor_from_t<float>(r2 * ir * invd, base, clamp);
-                const float g = e.du * ir;         // U' delta / r
-                float t[5];
-                t[0] = e.u;
-                t[1] = g * dx;
-                t[2] = g * dy;
-                t[3] = g * dz;
-                t[4] = fmaf(e.h, invd, g);      // (U'' + 2U'/r) * delta / 2
-                if (q == 0) {
+                const bool inb = FULL || i < N;
+                const int ii = inb ? i : 0;
+                const float4 pi = P4[ii];
+                const bool dn = FULL ? (j >= SPT / 2) : (ii >= n_up);        // partner's spin half
+                pair_raw(pi.x, pi.y, pi.z, a1, inb && i != kk, dn ? bd : bu, clamp, invd, t1[j]);
 #pragma unroll
-                    for (int c = 0; c < 5; ++c) d[j][c] = t[c];
-                } else {
-#pragma unroll
-                    for (int c = 0; c < 5; ++c) {
-                        d[j][c] = t[c] - d[j][c];
-                        acc[c] += t[c];
-                    }
-                    dv += d[j][0];
-                }
+                for (int c = 0; c < 5; ++c) acc[c] += t1[j][c];
             }
         }
         // 1b. J1: thread tid takes ions tid, tid + TPB at both positions, in physical units
         //     (species differ in delta): dv1 = sum U(r'_k) - U(r_k); at r'_k V, G = -U' d/r,
-        //     L = U'' + 2U'/r (electron k's J1 state on acceptance)
-        float dv1 = 0.f, a1c[5];
-#pragma unroll
-        for (int c = 0; c < 5; ++c) a1c[c] = 0.f;
+        //     L = U'' + 2U'/r (electron k's J1 row on acceptance)
+        float dv1 = 0.f, a1c[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
         if constexpr (J1) {
+            Axis<float> a0[3], a1[3];
+            a0[0] = make_axis<float>(xk, L0); a0[1] = make_axis<float>(yk, L1); a0[2] = make_axis<float>(zk, L2);
+            a1[0] = make_axis<float>(xn, L0); a1[1] = make_axis<float>(yn, L1); a1[2] = make_axis<float>(zn, L2);
 #pragma unroll
             for (int ion = tid; ion < SW_MAX_IONS; ion += TPB) {
                 if (ion >= p.n_ions) break;
                 const float4 ip = ion_p[ion];
                 const uint2 ic = ion_c[ion];
-                const uint32_t base1 = ic.x;
                 const float iv = ip.w;
-                const float x = ip.x, y = ip.y, z = ip.z;
                 float u0 = 0.f;
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
                     const Axis<float>(&a)[3] = q ? a1 : a0;
-                    const float dx = min_image(x, a[0]), dy = min_image(y, a[1]), dz = min_image(z, a[2]);
+                    const float dx = min_image(ip.x, a[0]), dy = min_image(ip.y, a[1]), dz = min_image(ip.z, a[2]);
                     const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
                     const float ir = Traits<float>::rsqrt(r2);
-                    const FunctorEval<float> e = functor_from_t<float>(r2 * ir * iv, base1, ic.y);
+                    const FunctorEval<float> e = functor_from_t<float>(r2 * ir * iv, ic.x, ic.y);
                     if (q == 0) {
                         u0 = e.u;
                     } else {
@@ -172,21 +214,20 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
             }
         }
         // 2. block reduction, fixed order: a reduce-scatter across the warp (8 or 16
-        //    slots for 6 or 12 values: one shuffle per slot and level instead of five
-        //    per value), one partial per value and warp in shared memory. Levels 1-2
-        //    (lanes 16 and 8 apart) add in fp32 -- partials of <= 4 lanes x 6 terms, the
-        //    eval kernel's fp32 partials of <= 32 terms -- the rest in fp64.
+        //    slots for 5 or 11 values: one shuffle per slot and level instead of one
+        //    per value), one partial per value and warp in shared memory.  Levels 1-2
+        //    (lanes 16 and 8 apart) add in fp32 -- partials of <= 4 lanes x SPT terms,
+        //    the eval kernel's fp32 partials of <= 32 terms -- the rest in fp64.
         {
             constexpr int NS = J1 ? 16 : 8;
             constexpr int OREM = J1 ? 1 : 2;        // lanes below this distance hold copies of one slot
             float vf[NS];
-            vf[0] = dv;
 #pragma unroll
             for (int c = 0; c < 5; ++c) {
-                vf[1 + c] = acc[c];
-                if (J1) vf[7 + c] = a1c[c];
+                vf[c] = acc[c];
+                if (J1) vf[6 + c] = a1c[c];
             }
-            if (J1) vf[6] = dv1;
+            if (J1) vf[5] = dv1;
 #pragma unroll
             for (int c = NV; c < NS; ++c) vf[c] = 0.f;
             int slot = 0;
@@ -220,19 +261,20 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
             if ((lane & (2 * OREM - 1)) == 0 && slot < NV) red2[s & 1][warp][slot] = v[0];
         }
         __syncthreads();
-        // 3. Metropolis: every thread sums dJ and takes the same decision (no second
-        //    barrier); thread 0 records it
-        double (*red)[NV] = red2[s & 1];
-        double djs = 0.0;
+        // 3. ratio and Metropolis: every thread sums the partials and takes the same
+        //    decision (no second barrier); thread 0 records it
+        const double (*red)[NV] = red2[s & 1];
+        double vnew = 0.0, dj1 = 0.0;
 #pragma unroll
         for (int wi = 0; wi < NW; ++wi) {
-            djs += red[wi][0];
-            if (J1) djs += red[wi][6];              // dJ = dJ2 + dJ1 (Eq. 4-5)
+            vnew += red[wi][0];
+            if (J1) dj1 += red[wi][5];
         }
-        // u < exp(2 dJ2): an fp32 exp settles it unless u is within 1e-4 of the threshold (its
-        // relative error is < 2e-5 for |dJ2| < 100) or the fp32 value over/underflows; then fp64.
+        const double djs = (vnew - (double)vk2[s & 1]) + dj1;      // dJ2 + dJ1 (Eq. 4-5)
+        const double uu = mv_u[b][jm];
+        // u < exp(2 dJ): an fp32 exp settles it unless u is within 1e-4 of the threshold (its
+        // relative error is < 2e-5 for |dJ| < 100) or the fp32 value over/underflows; then fp64.
         // Either way the decision equals the fp64 test.
-        const double uu = p.u[s * p.W + w];
         const float e32 = __expf(2.f * (float)djs);
         bool accepted;
         if (isfinite(e32) && e32 > 1e-30f && fabs((float)uu - e32) > 1e-4f * e32 && fabs(djs) < 100.0) {
@@ -241,105 +283,211 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
             const double rho = exp(djs);
             accepted = uu < rho * rho;
         }
-        const bool k_ok = (unsigned)k < (unsigned)N;
         accepted = accepted && k_ok;
         if (tid == 0) {
-            p.acc[s * p.W + w] = k_ok ? (accepted ? 1 : 0) : -1;
-            if (p.dj) p.dj[s * p.W + w] = djs;
+            const int64_t sw = (int64_t)s * p.W + w;
+            p.acc[sw] = k_ok ? (accepted ? 1 : 0) : -1;
+            if (p.dj) p.dj[sw] = k_ok ? djs : 0.0;
         }
-        // 4. accept: partners from the kept terms, then electron k and its position
+        // 4. accept: pair terms at r_k, partners += T(r'_k) - T(r_k); the owner of slot k
+        //    writes state_k = the sums at r'_k and r_k <- r'_k
         if (accepted) {
-            const float sg = invd, sl = 2.f * invd;
+            Axis<float> a0[3];
+            a0[0] = make_axis<float>(xk, L0);
+            a0[1] = make_axis<float>(yk, L1);
+            a0[2] = make_axis<float>(zk, L2);
 #pragma unroll
             for (int j = 0; j < SPT; ++j) {
                 const int i = tid + j * TPB;
-                if ((FULL || i < N) && i != k) {
-                    st[0 * N + i] += d[j][0];
-                    st[1 * N + i] += d[j][1] * sg;
-                    st[2 * N + i] += d[j][2] * sg;
-                    st[3 * N + i] += d[j][3] * sg;
-                    st[4 * N + i] += d[j][4] * sl;
+                const bool inb = FULL || i < N;
+                const int ii = inb ? i : 0;
+                float t0[5];
+                const float4 pi = P4[ii];
+                const bool dn = FULL ? (j >= SPT / 2) : (ii >= n_up);
+                pair_raw(pi.x, pi.y, pi.z, a0, inb && i != kk, dn ? bd : bu, clamp, invd, t0);
+                // the self slot adds T - T = 0 (both terms masked) and is then overwritten by its owner
+                if (inb) {
+                    float4 si = S4[i];
+                    si.x += t1[j][0] - t0[0];
+                    si.y = fmaf(t1[j][1] - t0[1], invd, si.y);
+                    si.z = fmaf(t1[j][2] - t0[2], invd, si.z);
+                    si.w = fmaf(t1[j][3] - t0[3], invd, si.w);
+                    S4[i] = si;
+                    reinterpret_cast<float *>(P4 + i)[3] = fmaf(t1[j][4] - t0[4], sl, pi.w);
                 }
             }
-            if (tid == k % TPB) {     // the thread that owns slot k (no cross-thread writes)
+            if (tid == (kk & (TPB - 1))) {     // the thread that owns slot k (no cross-thread writes)
                 // state_k = (V, G, L) at r'_k: G = -invd * sum g d, L = 2 invd * sum (h invd + g)
-                double f[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+                double f[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
                 for (int wi = 0; wi < NW; ++wi)
 #pragma unroll
-                    for (int c = 0; c < 5; ++c) f[c] += red[wi][1 + c];
-                st[0 * N + k] = (float)f[0];
-                st[1 * N + k] = (float)(-p.inv_delta * f[1]);
-                st[2 * N + k] = (float)(-p.inv_delta * f[2]);
-                st[3 * N + k] = (float)(-p.inv_delta * f[3]);
-                st[4 * N + k] = (float)(2.0 * p.inv_delta * f[4]);
-                rx[k] = tr[3]; ry[k] = tr[4]; rz[k] = tr[5];
-                if constexpr (J1) {                  // electron k's J1 state: U^1_k and derivatives at r'_k
+                    for (int c = 0; c < 4; ++c) f[c] += red[wi][1 + c];
+                S4[kk] = make_float4((float)vnew, (float)(-p.inv_delta * f[0]), (float)(-p.inv_delta * f[1]),
+                                     (float)(-p.inv_delta * f[2]));
+                P4[kk] = make_float4(propose(xk, mv_d[b][jm][0], L0), propose(yk, mv_d[b][jm][1], L1),
+                                     propose(zk, mv_d[b][jm][2], L2), (float)(2.0 * p.inv_delta * f[3]));
+                if constexpr (J1) {                  // electron k's J1 row: U^1_k and derivatives at r'_k
                     double f1[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
                     for (int wi = 0; wi < NW; ++wi)
 #pragma unroll
-                        for (int c = 0; c < 5; ++c) f1[c] += red[wi][7 + c];
-                    float *S1 = p.state_j1 + w * 5 * p.Np;
+                        for (int c = 0; c < 5; ++c) f1[c] += red[wi][6 + c];
+                    float *S1 = p.state_j1 + (int64_t)w * 5 * p.Np;
 #pragma unroll
-                    for (int c = 0; c < 5; ++c) S1[c * p.Np + k] = (float)f1[c];
+                    for (int c = 0; c < 5; ++c) S1[c * p.Np + kk] = (float)f1[c];
                 }
             }
         }
-        // no barrier: every thread only touches its own slots of R and the state,
-        // and the partials are double-buffered (a warp writes red2[s & 1] again at
-        // move s + 2, after every thread has passed the barrier of move s + 1)
+        prev_k = kk;
+        prev_acc = accepted;
+        // no barrier: every thread only touches its own slots of R and the state, the
+        // partials and U^2_k are double-buffered (a warp writes red2[s & 1] again at move
+        // s + 2, after every thread has passed the barrier of move s + 1), and r_k of the
+        // next move is re-synchronised above when its owner has just written it
     }
-    float *Rw = p.R + w * 3 * p.Np;
-    float *Sw = p.state + w * 5 * p.Np;
-    for (int i = tid; i < N; i += TPB) {
-        Rw[i] = rx[i]; Rw[p.Np + i] = ry[i]; Rw[2 * p.Np + i] = rz[i];
+    float *Rw = p.R + (int64_t)w * 3 * p.Np;
+    float *Sw = p.state + (int64_t)w * 5 * p.Np;
+    for (int i = tid; i < N; i += TPB) {         // own slots only: no barrier needed
+        const float4 pi = P4[i], si = S4[i];
+        Rw[i] = pi.x; Rw[p.Np + i] = pi.y; Rw[2 * p.Np + i] = pi.z;
+        Sw[i] = si.x; Sw[p.Np + i] = si.y; Sw[2 * p.Np + i] = si.z; Sw[3 * p.Np + i] = si.w; Sw[4 * p.Np + i] = pi.w;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// qj2_state_init: the state of every electron from scratch (the "new states
+// periodically computed from scratch" of PAPER:764-765), one CTA per walker,
+// positions in shared memory, one electron per thread at a time, its partners
+// walked in a uniform loop (every partner read is a shared-memory broadcast);
+// fp32 partials of <= 32 terms flushed to fp64, as in the eval kernel.
+// ---------------------------------------------------------------------------
+constexpr int SI_TPB = 256;
+
+template <bool J1>
+__global__ void __launch_bounds__(SI_TPB) state_init_kernel(const __grid_constant__ SweepParams p) {
+    extern __shared__ __align__(16) float si_smem[];
+    const int w = blockIdx.x, N = p.N, tid = threadIdx.x;
+    float *rx = si_smem, *ry = rx + N, *rz = ry + N;
+    const int N4 = (3 * N + 3) & ~3;
+    Coef4<float> *tab = reinterpret_cast<Coef4<float> *>(si_smem + N4);
+    Coef4<float> *tab1 = tab + 2 * (p.m + 1);
+    float4 *ion_p = reinterpret_cast<float4 *>(tab1 + (J1 ? p.n_rows1 : 0));
+    uint2 *ion_c = reinterpret_cast<uint2 *>(ion_p + (J1 ? p.n_ions : 0));
+    stage_tables<J1>(p, tab, tab1, ion_p, ion_c, tid, SI_TPB);
+    const float *Rg = p.R + (int64_t)w * 3 * p.Np;
+    for (int i = tid; i < N; i += SI_TPB) { rx[i] = Rg[i]; ry[i] = Rg[p.Np + i]; rz[i] = Rg[2 * p.Np + i]; }
+    __syncthreads();
+    const uint32_t tab_s = (uint32_t)__cvta_generic_to_shared(tab);
+    const uint32_t tab_o = tab_s + (uint32_t)((p.m + 1) * (int)sizeof(Coef4<float>));
+    const float invd = p.invd;
+    float *Sw = p.state + (int64_t)w * 5 * p.Np;
+    for (int e = tid; e < ((N + SI_TPB - 1) / SI_TPB) * SI_TPB; e += SI_TPB) {
+        const bool ok = e < N;
+        const int ee = ok ? e : 0;
+        Axis<float> a[3];
+        a[0] = make_axis<float>(rx[ee], p.L[0]);
+        a[1] = make_axis<float>(ry[ee], p.L[1]);
+        a[2] = make_axis<float>(rz[ee], p.L[2]);
+        const bool e_up = ee < p.N_up;
+        const uint32_t bu = e_up ? tab_s : tab_o, bd = e_up ? tab_o : tab_s;
+        double d[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        for (int i0 = 0; i0 < N; i0 += 32) {
+            float acc[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            const int i1 = min(i0 + 32, N);
+            for (int i = i0; i < i1; ++i) {
+                float t[5];
+                pair_raw(rx[i], ry[i], rz[i], a, i != ee, i >= p.N_up ? bd : bu, (unsigned)p.m, invd, t);
+                acc[0] += t[0]; acc[1] += t[1]; acc[2] += t[2]; acc[3] += t[3]; acc[4] += t[4];
+            }
 #pragma unroll
-        for (int c = 0; c < 5; ++c) Sw[c * p.Np + i] = st[c * N + i];
+            for (int c = 0; c < 5; ++c) d[c] += (double)acc[c];
+        }
+        if (ok) {
+            // partner-minus-electron displacements: G_e = -invd * sum g d, L_e = 2 invd * sum (h invd + g)
+            Sw[ee] = (float)d[0];
+            Sw[p.Np + ee] = (float)(-p.inv_delta * d[1]);
+            Sw[2 * p.Np + ee] = (float)(-p.inv_delta * d[2]);
+            Sw[3 * p.Np + ee] = (float)(-p.inv_delta * d[3]);
+            Sw[4 * p.Np + ee] = (float)(2.0 * p.inv_delta * d[4]);
+        }
+        if constexpr (J1) {                     // electron e's J1 row over the ions, physical units
+            double f[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+            for (int i0 = 0; i0 < p.n_ions; i0 += 32) {
+                float acc[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+                const int i1 = min(i0 + 32, p.n_ions);
+                for (int ion = i0; ion < i1; ++ion) {
+                    const float4 ip = ion_p[ion];
+                    const uint2 ic = ion_c[ion];
+                    const float dx = min_image(ip.x, a[0]), dy = min_image(ip.y, a[1]), dz = min_image(ip.z, a[2]);
+                    const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                    const float ir = Traits<float>::rsqrt(r2);
+                    const FunctorEval<float> fe = functor_from_t<float>(r2 * ir * ip.w, ic.x, ic.y);
+                    const float g = fe.du * ir * ip.w;                  // U'/r
+                    acc[0] += fe.u;
+                    acc[1] += -g * dx;
+                    acc[2] += -g * dy;
+                    acc[3] += -g * dz;
+                    acc[4] += 2.f * (fe.h * ip.w * ip.w + g);        // U'' + 2U'/r
+                }
+#pragma unroll
+                for (int c = 0; c < 5; ++c) f[c] += (double)acc[c];
+            }
+            if (ok) {
+                float *S1 = p.state_j1 + (int64_t)w * 5 * p.Np;
+#pragma unroll
+                for (int c = 0; c < 5; ++c) S1[c * p.Np + ee] = (float)f[c];
+            }
+        }
     }
+}
+
+static size_t table_smem(const SweepParams &p, bool j1) {
+    return (size_t)(2 * (p.m + 1) + (j1 ? p.n_rows1 : 0)) * sizeof(Coef4<float>) +
+           (j1 ? (size_t)p.n_ions * (sizeof(float4) + sizeof(uint2)) : 0);
 }
 
 cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s) {
     const bool j1 = p.n_ions > 0;
-    const size_t smem = (size_t)8 * p.N * sizeof(float)                       // R (3) + state (5) per electron
-                      + (size_t)(2 * (p.m + 1) + (j1 ? p.n_rows1 : 0)) * sizeof(Coef4<float>)
-                      + (j1 ? (size_t)p.n_ions * (sizeof(float4) + sizeof(uint2)) : 0);
-    // 128 threads per walker for 384 < N <= 768 (7-8 CTAs/SM), else 256 (64 and 96
-    // threads per walker were measured too: profiles/r01_s4/ab_tpb.log)
-    int tpb = (p.N > 384 && p.N <= 768) ? 128 : SW_TPB;
-    if (const char *e = getenv("QJ2_SWEEP_TPB")) tpb = atoi(e) == 128 && p.N <= 768 ? 128 : SW_TPB;   // A/B
-    const int spt = (int)((p.N + tpb - 1) / tpb);
-    // compile-time layout where N fills the threads exactly (N64SJ 4.39 -> 3.98 ms, N64S at 7
-    // CTAs/SM 3.40 -> 3.28 ms)
-    const bool full = p.N == (int64_t)tpb * spt && !getenv("QJ2_SWEEP_NOFULL");
-#define QJ2_SWEEP_LAUNCH(T_, S_)                                                            \
-    (j1 ? (j2_sweep_kernel<T_, S_, true, false><<<(unsigned)p.W, T_, smem, s>>>(p), 0)       \
-        : (j2_sweep_kernel<T_, S_, false, false><<<(unsigned)p.W, T_, smem, s>>>(p), 0))
-#define QJ2_SWEEP_LAUNCH_FULL(T_, S_)                                                       \
-    (j1 ? (j2_sweep_kernel<T_, S_, true, true><<<(unsigned)p.W, T_, smem, s>>>(p), 0)        \
-        : (j2_sweep_kernel<T_, S_, false, true><<<(unsigned)p.W, T_, smem, s>>>(p), 0))
+    const size_t smem = (size_t)8 * p.N * sizeof(float) + table_smem(p, j1);   // R (3) + state (5) per electron
+    // 128 threads per walker for 384 < N <= 768 (7 CTAs/SM), else 256 (64 and 96 threads
+    // per walker were measured too: profiles/r01_s4/ab_tpb.log)
+    const int tpb = (p.N > 384 && p.N <= 768) ? 128 : SW_TPB;
+    const int spt = (p.N + tpb - 1) / tpb;
+    // compile-time layout where N fills the threads exactly and splits evenly into spin halves
+    const bool full = p.N == tpb * spt && 2 * p.N_up == p.N && spt % 2 == 0;
+#define QJ2_SWEEP_LAUNCH(T_, S_, F_)                                                         \
+    (j1 ? (j2_sweep_kernel<T_, S_, true, F_><<<(unsigned)p.W, T_, smem, s>>>(p), 0)           \
+        : (j2_sweep_kernel<T_, S_, false, F_><<<(unsigned)p.W, T_, smem, s>>>(p), 0))
     if (tpb == 128) {
         switch (spt) {
-            case 1: case 2: case 3: case 4: QJ2_SWEEP_LAUNCH(128, 4); break;
-            case 5: QJ2_SWEEP_LAUNCH(128, 5); break;
+            case 1: case 2: case 3: case 4: QJ2_SWEEP_LAUNCH(128, 4, false); break;
+            case 5: QJ2_SWEEP_LAUNCH(128, 5, false); break;
             default:
-                if (full) QJ2_SWEEP_LAUNCH_FULL(128, 6);
-                else QJ2_SWEEP_LAUNCH(128, 6);
+                if (full) QJ2_SWEEP_LAUNCH(128, 6, true);
+                else QJ2_SWEEP_LAUNCH(128, 6, false);
                 break;
         }
     } else {
         switch (spt) {
-            case 1: QJ2_SWEEP_LAUNCH(256, 1); break;
-            case 2: QJ2_SWEEP_LAUNCH(256, 2); break;
-            case 3: QJ2_SWEEP_LAUNCH(256, 3); break;
+            case 1: QJ2_SWEEP_LAUNCH(256, 1, false); break;
+            case 2: QJ2_SWEEP_LAUNCH(256, 2, false); break;
+            case 3: QJ2_SWEEP_LAUNCH(256, 3, false); break;
             default:
-                if (full) QJ2_SWEEP_LAUNCH_FULL(256, 4);
-                else QJ2_SWEEP_LAUNCH(256, 4);
+                if (full) QJ2_SWEEP_LAUNCH(256, 4, true);
+                else QJ2_SWEEP_LAUNCH(256, 4, false);
                 break;
         }
     }
 #undef QJ2_SWEEP_LAUNCH
-#undef QJ2_SWEEP_LAUNCH_FULL
+    return cudaGetLastError();
+}
+
+cudaError_t launch_state_init(const SweepParams &p, cudaStream_t s) {
+    const bool j1 = p.n_ions > 0;
+    const size_t smem = (size_t)((3 * p.N + 3) & ~3) * sizeof(float) + table_smem(p, j1);
+    if (j1) state_init_kernel<true><<<(unsigned)p.W, SI_TPB, smem, s>>>(p);
+    else state_init_kernel<false><<<(unsigned)p.W, SI_TPB, smem, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -1,22 +1,29 @@
-// sweep.cuh -- NEXT-2 at the paper's system sizes: a whole particle-by-particle
-// sweep of the J2 factor (optionally with J1) in one persistent kernel, the walker
-// resident in shared memory (sm_100a).
+// sweep.cuh -- NEXT-2 at the paper's system sizes: whole particle-by-particle
+// sweeps of the Jastrow factor (J2, optionally with J1) in one persistent
+// kernel, the walker resident in shared memory (sm_100a).
 //
 // One CTA per walker.  For every move s < S (Alg. 1 L4-L9; electron
-// k = ks[s][w], r_k = trials[s][w][0], r'_k = trials[s][w][1]):
-//   1. each thread forms, for its partners i != k (i = tid, tid + TPB, ...), the
-//      pair terms T_i at r_k and then at r'_k with the eval kernel's fp32
-//      arithmetic (single-rounding minimum image, power-basis Horner) and keeps
-//      only the differences T_i(r'_k) - T_i(r_k) in registers;
-//   2. a reduce-scatter (fp32 for lanes 16 and 8 apart, then fp64) and ONE barrier
-//      give dJ2 = sum_i (U(r'_k) - U(r_k)) and the sums at r'_k (electron k's new
-//      state, Eq. 5 / PAPER:1382, Alg. 1 L7-L8); with J1 also dJ1 and k's J1 row;
-//   3. every thread takes the same Metropolis decision u < exp(2 dJ) (reading R19);
-//   4. if accepted: state_i += the kept differences (no recomputation), state_k =
-//      the sums at r'_k, R[:, k] = r'_k.
-// R and the 5N state stay in shared memory for all S moves (32 B per electron:
-// N <= 1024 in 32 KB); global memory is touched only to load and store them once
-// and to read the moves -- no launch per move.
+// k = ks[s][w], proposal displacement delta[s][w]):
+//   0. r_k is the walker's CURRENT position of k (shared memory) and
+//      r'_k = wrap(r_k + delta) is formed in fp32 (Alg. 1 L5 without drift,
+//      reading R24);
+//   1. each thread forms, for its partners i != k (i = tid + j*TPB), the pair
+//      terms T_i(r'_k) with the eval kernel's fp32 arithmetic (single-rounding
+//      minimum image, power-basis Horner), keeps them in registers and sums
+//      them: the sums are U^2_k(R') and its gradient / Laplacian (Alg. 1 L7-L8);
+//   2. a fixed-order reduce-scatter (fp32 for lanes 16 and 8 apart, then fp64)
+//      and ONE barrier;
+//   3. dJ2 = U^2_k(R') - U^2_k(R), with U^2_k(R) the electron's entry of the 5N
+//      state (the state is kept so the ratio reuses it; the
+//      owner of slot k publishes it before the barrier); every thread takes
+//      the same Metropolis decision u < exp(2 dJ) (reading R19);
+//   4. if accepted: each thread forms T_i(r_k) for its partners and adds
+//      T_i(r'_k) - T_i(r_k) to their state; the owner of slot k writes
+//      state_k = the sums at r'_k and r_k <- r'_k.
+// Rejected moves cost one pass of pair terms, accepted ones two.  R and the
+// 5N state stay in shared memory for all S moves (32 B per electron: N <= 1024
+// in 32 KB); global memory is touched to load and store them once and to read
+// the moves -- no launch per move.
 #pragma once
 
 #include "qmcj2.h"
@@ -24,26 +31,26 @@
 
 namespace qj2 {
 
-constexpr int SW_TPB = 256;       // threads per walker (CTA)
+constexpr int SW_TPB = 256;       // threads per walker (CTA) outside 384 < N <= 768
 constexpr int SW_SPT = 4;         // partners per thread: N <= SW_TPB * SW_SPT
 constexpr int SW_MAXN = SW_TPB * SW_SPT;
 
 struct SweepParams {
-    int64_t W, N, N_up, Np, S;
-    int32_t m;
+    int32_t W, N, N_up, m;
+    int64_t Np, S;
     float invd;                   // 1/delta in fp32 (the eval kernel's)
     double inv_delta;
     float *R;                     // [W][3][Np] in/out
     float *state;                 // [W][5][Np] in/out
     const int32_t *ks;            // [S][W]
-    const float *trials;          // [S][W][2][3]
+    const float *delta;           // [S][W][3]
     const double *u;              // [S][W]
     int32_t *acc;                 // [S][W] out
-    double *dj;                   // [S][W] out (dJ2 of each move) or NULL
+    double *dj;                   // [S][W] out (dJ of each move) or NULL
     float L[3];
     double pcoef[2 * (QJ2_MAX_M + 1)][4];
     // optional one-body Jastrow over the electron-ion row (NEXT-1): the move's
-    // ratio becomes exp(dJ1 + dJ2); the ions are fixed (one per thread)
+    // ratio becomes exp(dJ1 + dJ2); the ions are fixed
     int32_t n_ions, n_species;
     int32_t sp_start[QJ2_MAX_SPECIES + 1];   // ions sorted by species
     int32_t sp_tab[QJ2_MAX_SPECIES];         // first row of species s in pcoef1
@@ -56,8 +63,11 @@ struct SweepParams {
     double pcoef1[QJ2_MAX_SPECIES * (QJ2_MAX_M + 1)][4];
 };
 
-constexpr int SW_MAX_IONS = SW_TPB;      // one ion per thread in the J1 part of a move
+constexpr int SW_MAX_IONS = SW_TPB;      // at most two ions per thread in the J1 part of a move
 
 cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s);
+// The 5N state (and, with ions, the J1 rows) of every electron from scratch
+// (qj2_state_init): same SweepParams (S, ks, delta, u, acc, dj unused).
+cudaError_t launch_state_init(const SweepParams &p, cudaStream_t s);
 
 }  // namespace qj2

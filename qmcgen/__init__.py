@@ -240,6 +240,30 @@ def make_sweep(seed: int, W: int, N: int, L: float, dtype, steps: int):
     return ks, np.ascontiguousarray(trials), u
 
 
+def make_sweep_moves(seed: int, W: int, N: int, steps: int, order: str = "ordered", sigma: float = 0.1):
+    """Inputs of qj2_sweep (harness draws, no method arithmetic): for move s <
+    steps of walker w, the electron ks[s][w] and the proposal displacement
+    delta[s][w] ~ N(0, sigma^2 I) (reading R13: sigma^2 = 0.01), fp32; u[s][w]
+    fp64 uniforms in [0, 1) for the Metropolis test.  The kernel forms r'_k =
+    wrap(r_k + delta) from the walker's CURRENT r_k, so any number of moves
+    and any k sequence is valid.
+    order="ordered": k = (k0_w + s) mod N (particle-by-particle sweeps, Alg. 1
+    L4; steps = n*N is n full sweeps); order="random": k ~ U{0..N-1}
+    independently per move (repeats included)."""
+    rng = np.random.default_rng([int(seed), 9])
+    if order == "ordered":
+        k0 = make_k(seed, W, N).astype(np.int64)
+        s = np.arange(steps, dtype=np.int64)[:, None]
+        ks = ((k0[None, :] + s) % N).astype(np.int32)
+    elif order == "random":
+        ks = rng.integers(0, N, size=(steps, W)).astype(np.int32)
+    else:
+        raise ValueError(order)
+    delta = rng.normal(0.0, sigma, size=(steps, W, 3)).astype(np.float32)
+    u = rng.random((steps, W))
+    return ks, np.ascontiguousarray(delta), u
+
+
 # ---------------------------------------------------------------------------
 # NEXT-4 inputs: a synthetic 3D B-spline SPO coefficient table (Table 1 grid
 # and orbital counts, PAPER:936-958; the real DFT orbitals are not available)

@@ -35,7 +35,7 @@ def test_header_symbols_exported(q):
 
 
 def test_version_and_status_strings(q):
-    assert q.version() == 10000
+    assert q.version() == 20000
     lib = q._lib
     assert lib.qj2_status_string(0) == b"ok"
     assert lib.qj2_status_string(1) == b"invalid-argument"
@@ -204,6 +204,21 @@ def test_sweep_host_validation(q):
     assert call(N_up=101) == 2
     assert call(fn=_functor(q, m=17)) == 1       # fp32 pair terms: m <= 16
     assert call(S=0) == 0 and call(W=0) == 0
+    assert call(S=-1) == 1
+
+
+def test_state_init_host_validation(q):
+    f = _functor(q)
+    P = ctypes.c_void_p(4096)
+
+    def call(fn=f, W=4, N=100, N_up=50, Np=128):
+        return q._lib.qj2_state_init(fn.ptr, W, N, N_up, Np, P, P, None, None)
+    assert call(N=1025, Np=1056) == 1
+    assert call(N=1) == 1
+    assert call(Np=64) == 1
+    assert call(N_up=-1) == 2
+    assert call(fn=_functor(q, m=17)) == 1
+    assert call(W=0) == 0
 
 
 def test_metropolis_and_spo_host_validation(q):

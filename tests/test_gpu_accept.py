@@ -319,155 +319,6 @@ def test_fused_metropolis_accept_equals_separate_calls(q, dtype):
     assert torch.equal(Ra, Rb) and torch.equal(Sa, Sb)
 
 
-# ---------------------------------------------------------------------------
-# qj2_sweep: a whole sweep in one launch, walkers resident in shared memory
-# ---------------------------------------------------------------------------
-def _sweep_inputs(N, W, seed, n_up=None):
-    L = qmcgen.cell_length(N)
-    Np = qmcgen.padded_size(N, 32)
-    R = qmcgen.positions(seed, np.arange(W), N, Np, L, np.float32)
-    fn = qmcgen.make_functor(seed, L)
-    ks, tr, u = qmcgen.make_sweep(seed, W, N, L, np.float32, N)
-    return R, fn, ks, tr, u, Np, (N // 2 if n_up is None else n_up)
-
-
-@pytest.mark.parametrize("N", [2, 33, 256, 385, 600, 768, 1024])      # 128 threads x 4, 5, 6 partners at 385-768
-def test_sweep_kernel_vs_oracle_sequence(q, N):
-    """One full sweep (N moves) in one qj2_sweep launch vs the oracle running
-    the same moves (its own eval -> decision -> accept); the state starts from
-    the oracle's from-scratch state."""
-    W = 12
-    R, fn, ks, tr, u, Np, n_up = _sweep_inputs(N, W, 60 + N)
-    state = np.stack([oracle.j2_state(R[w], N, n_up, fn)[0] for w in range(W)]).astype(np.float32)
-    Rd, Sd = dev(R), dev(state)
-    acc, dj = q.sweep(Rd, Sd, dev(ks), dev(tr), dev(u), fn, N, n_up)
-    acc, dj = acc.cpu().numpy(), dj.cpu().numpy()
-    Rh, Sh = R.astype(np.float64), state.astype(np.float64)
-    for s in range(N):
-        orc, _, _ = oracle.eval_j2(Rh, ks[s], tr[s], fn, N, n_up)
-        d = orc[:, 1, 0] - orc[:, 0, 0]
-        rho2 = np.exp(d) ** 2
-        a = (u[s] < rho2).astype(np.int32)
-        clear = np.abs(u[s] - rho2) > 1e-6 * rho2
-        assert np.array_equal(acc[s][clear], a[clear]), s
-        assert np.max(np.abs(dj[s] - d) / np.maximum(np.abs(orc[:, :, 0]).max(1), 1.0)) < 1e-5
-        Rh, Sh, _ = oracle.accept(Rh, Sh, ks[s], tr[s][:, 1], acc[s], fn, N, n_up)   # the GPU's decisions
-    assert np.array_equal(Rd.cpu().numpy().astype(np.float64), Rh)
-    Sg = Sd.cpu().numpy()
-    for w in range(W):
-        fresh, ab = oracle.j2_state(Rh[w], N, n_up, fn)
-        # accumulated over N updates in fp32: normalized by the from-scratch absolute sums
-        err = oracle.normalized_error_state(Sg[w][:, :N], Sh[w][:, :N], ab[:, :N], fn)
-        assert err.max() <= 1e-5, (w, err.max())
-
-
-def test_sweep_kernel_equals_per_move_kernels(q):
-    """qj2_sweep vs the per-move launches (qj2_eval + qj2_metropolis_accept):
-    the same decisions and positions, states equal to fp32 rounding."""
-    N, W = 768, 64
-    R, fn, ks, tr, u, Np, n_up = _sweep_inputs(N, W, 71)
-    Ra, Sa = dev(R), torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
-    Rb, Sb = dev(R), torch.zeros_like(Sa)
-    acc_a, _ = q.sweep(Ra, Sa, dev(ks), dev(tr), dev(u), fn, N, n_up)
-    kd, td, ud = dev(ks), dev(tr), dev(u)
-    accs = []
-    for s in range(N):
-        out = q.eval(Rb, kd[s], td[s], fn, N, n_up)
-        accs.append(q.metropolis_accept(Rb, Sb, kd[s], td[s], out, ud[s], fn, N, n_up))
-    acc_b = torch.stack(accs)
-    assert (acc_a != acc_b).sum().item() <= 2          # decisions at the rounding edge may differ
-    if torch.equal(acc_a, acc_b):
-        assert torch.equal(Ra, Rb)
-        fresh_scale = Sa.abs().max().item() + 1.0
-        assert (Sa - Sb).abs().max().item() <= 1e-5 * fresh_scale
-
-
-def test_sweep_N64S_full_size_every_walker(q):
-    """The N64S bench workload at full size (W = 1024 walkers of N = 768, one
-    768-move sweep, zero initial state) in the bench launch configuration; every
-    walker replayed move by move by the oracle (decisions where clear, dJ,
-    positions bitwise, final state)."""
-    cfg = qmcgen.config("N64S")
-    N, W, n_up = cfg.N, cfg.W, cfg.n_up
-    fn = q.Functor.of(qmcgen.make_functor(cfg.seed, cfg.L, cfg.m))
-    R = q.gen_positions(cfg.seed, W, N, cfg.Np, cfg.L, torch.float32)
-    S = torch.zeros((W, 5, cfg.Np), dtype=torch.float32, device="cuda")
-    ks, tr, u = qmcgen.make_sweep(cfg.seed, W, N, cfg.L, np.float32, N)
-    acc, dj = q.sweep(R, S, dev(ks), dev(tr), dev(u), fn, N, n_up)
-    acc, dj = acc.cpu().numpy(), dj.cpu().numpy()
-    ws = np.arange(W)
-    Rh = oracle.gen_positions(cfg.seed, 0, W, N, cfg.Np, cfg.L, np.float32).astype(np.float64)
-    Sh = np.zeros((W, 5, cfg.Np))
-    for s in range(N):
-        orc, _, _ = oracle.eval_j2(Rh, ks[s], tr[s], fn, N, n_up, threads=THREADS)
-        d = orc[:, 1, 0] - orc[:, 0, 0]
-        assert np.max(np.abs(dj[s] - d) / np.maximum(np.abs(orc[:, :, 0]).max(1), 1.0)) < 1e-5, s
-        rho2 = np.exp(d) ** 2
-        clear = np.abs(u[s] - rho2) > 1e-6 * rho2
-        assert np.array_equal(acc[s][clear], (u[s] < rho2)[clear].astype(np.int32)), s
-        Rh, Sh, _ = oracle.accept(Rh, Sh, ks[s], tr[s][:, 1], acc[s], fn, N, n_up)
-    assert np.array_equal(R.cpu().numpy().astype(np.float64), Rh)
-    Sg = S.cpu().numpy()
-    for j in ws[::64]:                   # the from-scratch scale: the O(N^2) state oracle on every 64th walker
-        _, ab = oracle.j2_state(Rh[j], N, n_up, fn)
-        err = oracle.normalized_error_state(Sg[j][:, :N], Sh[j][:, :N], ab[:, :N], fn)
-        assert err.max() <= 1e-5, (j, err.max())
-    # every walker's state vs the replayed oracle state, normalised by its magnitude
-    scale = np.maximum(np.abs(Sh[:, :, :N]).max(axis=2, keepdims=True), 1.0)
-    assert np.max(np.abs(Sg[:, :, :N] - Sh[:, :, :N]) / scale) <= 1e-5
-
-
-def test_sweep_kernel_out_of_range_k(q):
-    """A move whose k is outside [0, N) (a precondition violation) is never
-    accepted and flagged -1; the other moves and the walker's state go on as
-    the oracle replay with those moves rejected says (memory stays intact)."""
-    for N in (130, 600):          # 256 and 128 threads per walker
-        W = 6
-        R, fn, ks, tr, u, Np, n_up = _sweep_inputs(N, W, 120 + N)
-        ks0, ks = ks, ks.copy()
-        bad = [(3, 2, -5), (7, 4, N), (11, 0, N + 1000), (12, 5, -(1 << 30))]
-        for s_, w_, k_ in bad:
-            ks[s_, w_] = k_
-        Rd, Sd = dev(R), torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
-        acc, _ = q.sweep(Rd, Sd, dev(ks), dev(tr), dev(u), fn, N, n_up)
-        acc = acc.cpu().numpy()
-        for s_, w_, _ in bad:
-            assert acc[s_, w_] == -1
-        assert set(np.unique(acc)) <= {-1, 0, 1}
-        Rh, Sh = R.astype(np.float64), np.zeros((W, 5, Np))
-        for s in range(N):
-            a = np.maximum(acc[s], 0)
-            kk = ks0[s]                  # the drawn k (its move is rejected either way)
-            orc, _, _ = oracle.eval_j2(Rh, kk, tr[s], fn, N, n_up)
-            d = orc[:, 1, 0] - orc[:, 0, 0]
-            rho2 = np.exp(d) ** 2
-            ok = acc[s] >= 0
-            clear = ok & (np.abs(u[s] - rho2) > 1e-6 * rho2)
-            assert np.array_equal(acc[s][clear], (u[s] < rho2)[clear].astype(np.int32)), s
-            Rh, Sh, _ = oracle.accept(Rh, Sh, kk, tr[s][:, 1], a, fn, N, n_up)
-        assert np.array_equal(Rd.cpu().numpy().astype(np.float64), Rh)
-        assert np.array_equal(Rd.cpu().numpy()[:, :, N:], R[:, :, N:])     # padding untouched
-
-
-@pytest.mark.parametrize("n_up_case", ["zero", "all", "odd"])
-def test_sweep_kernel_spin_boundaries(q, n_up_case):
-    """qj2_sweep with N_up = 0, N_up = N and an odd split: every move's ratio
-    vs the oracle replaying the sweep."""
-    N, W = 130, 6
-    n_up = {"zero": 0, "all": N, "odd": 47}[n_up_case]
-    R, fn, ks, tr, u, Np, _ = _sweep_inputs(N, W, 90 + n_up)
-    Rd, Sd = dev(R), torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
-    acc, dj = q.sweep(Rd, Sd, dev(ks), dev(tr), dev(u), fn, N, n_up)
-    acc, dj = acc.cpu().numpy(), dj.cpu().numpy()
-    Rh, Sh = R.astype(np.float64), np.zeros((W, 5, Np))
-    for s in range(N):
-        orc, _, _ = oracle.eval_j2(Rh, ks[s], tr[s], fn, N, n_up)
-        d = orc[:, 1, 0] - orc[:, 0, 0]
-        assert np.max(np.abs(dj[s] - d) / np.maximum(np.abs(orc[:, :, 0]).max(1), 1.0)) < 1e-5
-        Rh, Sh, _ = oracle.accept(Rh, Sh, ks[s], tr[s][:, 1], acc[s], fn, N, n_up)
-    assert np.array_equal(Rd.cpu().numpy().astype(np.float64), Rh)
-
-
 def test_fused_metropolis_accept_sharded_slices(q):
     """qj2_metropolis_accept on source-axis slices (each rank's call with
     i_offset; r_k = trial 0 replicated) equals the unsharded call."""
@@ -493,73 +344,3 @@ def test_fused_metropolis_accept_sharded_slices(q):
         assert torch.equal(acc, acc_u)
         Rs.append(Rl[:, :, :b - a]); Ss.append(Sl[:, :, :b - a])
     assert torch.equal(torch.cat(Rs, 2), Ru[:, :, :N]) and torch.equal(torch.cat(Ss, 2), Su[:, :, :N])
-
-
-@pytest.mark.parametrize("n_ions,S,N", [(64, 2, 200), (37, 3, 200), (256, 1, 200), (256, 2, 520), (64, 2, 768),
-                                         (100, 2, 1024)])
-def test_sweep_kernel_with_j1_vs_oracle(q, n_ions, S, N):
-    """qj2_sweep with the one-body Jastrow joined to every move: dJ = dJ2 + dJ1
-    per move vs the oracle (eval_j2 + eval_j1 at r_k and r'_k), the decisions,
-    positions, J2 state, and the J1 state rows of accepted electrons (= the J1
-    values at their new positions). N = 520 and 768 run 128 threads per walker
-    (256 ions: two per thread); 768 and 1024 fill the threads exactly (the
-    compile-time-layout kernels)."""
-    W = 8
-    R, fn, ks, tr, u, Np, n_up = _sweep_inputs(N, W, 300 + n_ions)
-    L = fn.L[0]
-    ions, start = qmcgen.make_ions(300 + n_ions, n_ions, qmcgen.padded_size(n_ions, 4), L, np.float32,
-                                   n_species=S)
-    fn1 = qmcgen.make_j1_functor(300 + n_ions, L, n_species=S, m=(8, 10, 6), rcut_frac=(0.5, 0.4, 0.3))
-    Rd, Sd = dev(R), torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
-    S1 = torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
-    acc, dj = q.sweep(Rd, Sd, dev(ks), dev(tr), dev(u), fn, N, n_up, j1=(dev(ions), start, fn1, S1))
-    acc, dj = acc.cpu().numpy(), dj.cpu().numpy()
-    Rh, Sh = R.astype(np.float64), np.zeros((W, 5, Np))
-    S1h, A1h = np.zeros((W, 5, Np)), np.zeros((W, 5, Np))
-    for s in range(N):
-        o2, a2, _ = oracle.eval_j2(Rh, ks[s], tr[s], fn, N, n_up)
-        o1, a1 = oracle.eval_j1(ions.astype(np.float64), start, tr[s].astype(np.float64), fn1)
-        d = (o2[:, 1, 0] - o2[:, 0, 0]) + (o1[:, 1, 0] - o1[:, 0, 0])
-        scale = np.maximum(np.maximum(a2[:, :, 0].max(1), a1[:, :, 0].max(1)), 1.0)
-        assert np.max(np.abs(dj[s] - d) / scale) < 1e-5, s
-        rho2 = np.exp(d) ** 2
-        clear = np.abs(u[s] - rho2) > 1e-6 * rho2
-        assert np.array_equal(acc[s][clear], (u[s] < rho2)[clear].astype(np.int32)), s
-        Rh, Sh, _ = oracle.accept(Rh, Sh, ks[s], tr[s][:, 1], acc[s], fn, N, n_up)
-        for w in np.nonzero(acc[s])[0]:
-            S1h[w, :, ks[s][w]] = o1[w, 1]
-            A1h[w, :, ks[s][w]] = a1[w, 1]
-    assert np.array_equal(Rd.cpu().numpy().astype(np.float64), Rh)
-    # normalised like every J1 parity check: by the oracle's absolute sums over the ions
-    err1 = oracle.normalized_error_j1(np.moveaxis(S1.cpu().numpy()[:, :, :N], 1, 2),
-                                      np.moveaxis(S1h[:, :, :N], 1, 2), np.moveaxis(A1h[:, :, :N], 1, 2), fn1)
-    assert err1.max() <= 1e-5
-
-
-@pytest.mark.parametrize("with_j1", [False, True])
-def test_sweep_kernel_deterministic(q, with_j1):
-    """The sweep kernel's one-barrier-per-move design (double-buffered partials, every
-    thread writing only its own slots) leaves no shared-memory race: five runs of a
-    full NiO-64-sized sweep from the same inputs are bitwise identical (positions,
-    state, J1 state, decisions, dJ)."""
-    cfg = qmcgen.config("N64S")
-    N, W, n_up = cfg.N, cfg.W, cfg.n_up
-    fn = q.Functor.of(qmcgen.make_functor(cfg.seed, cfg.L, cfg.m))
-    R0 = q.gen_positions(cfg.seed, W, N, cfg.Np, cfg.L, torch.float32)
-    ks, tr, u = qmcgen.make_sweep(cfg.seed, W, N, cfg.L, np.float32, N)
-    kd, td, ud = dev(ks), dev(tr), dev(u)
-    j1 = None
-    if with_j1:
-        ions, start = qmcgen.make_ions(cfg.seed, 64, 64, cfg.L, np.float32, n_species=2)
-        fn1 = q.J1Functor.of(qmcgen.make_j1_functor(cfg.seed, cfg.L, n_species=2))
-    results = []
-    for _ in range(5):
-        R, S = R0.clone(), torch.zeros((W, 5, cfg.Np), dtype=torch.float32, device="cuda")
-        if with_j1:
-            j1 = (dev(ions), start, fn1, torch.zeros((W, 5, cfg.Np), dtype=torch.float32, device="cuda"))
-        acc, dj = q.sweep(R, S, kd, td, ud, fn, N, n_up, j1=j1)
-        results.append((R, S, acc, dj) + ((j1[3],) if with_j1 else ()))
-    torch.cuda.synchronize()
-    for other in results[1:]:
-        for a, b in zip(results[0], other):
-            assert torch.equal(a, b)

@@ -16,6 +16,7 @@ import torch
 
 import oracle
 import qmcgen
+from sweep_check import check_sweep
 
 pytestmark = pytest.mark.gpu
 
@@ -52,7 +53,7 @@ def _sweep_cases(n=12, seed=2026):
     rng = np.random.default_rng(seed)
     return [dict(N=max(2, _log_uniform(rng, 2, 1024)), W=int(rng.integers(1, 6)), m=int(rng.integers(4, 17)),
                  seed=int(rng.integers(2**31)), up_frac=float(rng.choice([0.0, 1.0, rng.random(), 0.5])),
-                 moves=int(rng.integers(1, 65)))
+                 moves=int(rng.integers(1, 257)))
             for _ in range(n)]
 
 
@@ -133,33 +134,18 @@ def test_accept_random(q, c):
 
 @pytest.mark.parametrize("c", _sweep_cases(), ids=lambda c: f"N{c['N']}-W{c['W']}-m{c['m']}-S{c['moves']}")
 def test_sweep_random(q, c):
-    """qj2_sweep over a drawn number of moves vs the oracle replaying them."""
-    N, W, m, seed, up_frac, moves = c["N"], c["W"], c["m"], c["seed"], c["up_frac"], c["moves"]
-    S = min(moves, N)
+    """qj2_sweep over a drawn number of moves (random k, repeats included) from the
+    qj2_state_init state vs the oracle replaying them (tests/sweep_check.py)."""
+    N, W, m, seed, up_frac, S = c["N"], c["W"], c["m"], c["seed"], c["up_frac"], c["moves"]
     L = qmcgen.cell_length(N)
     Np = qmcgen.padded_size(N, 32)
     R = qmcgen.positions(seed, np.arange(W), N, Np, L, np.float32)
     fn = qmcgen.make_functor(seed, L, m)
-    ks, tr, u = qmcgen.make_sweep(seed, W, N, L, np.float32, S)
+    ks, delta, u = qmcgen.make_sweep_moves(seed, W, N, S, order="random")
     n_up = int(round(up_frac * N))
-    Rd, Sd = dev(R), torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
-    acc, dj = q.sweep(Rd, Sd, dev(ks), dev(tr), dev(u), fn, N, n_up)
-    acc, dj = acc.cpu().numpy(), dj.cpu().numpy()
-    Rh, Sh = R.astype(np.float64), np.zeros((W, 5, Np))
-    for s in range(S):
-        o, _, _ = oracle.eval_j2(Rh, ks[s], tr[s], fn, N, n_up)
-        d = o[:, 1, 0] - o[:, 0, 0]
-        assert np.max(np.abs(dj[s] - d) / np.maximum(np.abs(o[:, :, 0]).max(1), 1.0)) < 1e-5, s
-        rho2 = np.exp(d) ** 2
-        clear = np.abs(u[s] - rho2) > 1e-6 * rho2
-        assert np.array_equal(acc[s][clear], (u[s] < rho2)[clear].astype(np.int32)), s
-        Rh, Sh, _ = oracle.accept(Rh, Sh, ks[s], tr[s][:, 1], acc[s], fn, N, n_up)
-    assert np.array_equal(Rd.cpu().numpy().astype(np.float64), Rh)
-    Sg = Sd.cpu().numpy()
-    for w in range(W):
-        _, ab = oracle.j2_state(Rh[w], N, n_up, fn)
-        err = oracle.normalized_error_state(Sg[w][:, :N], Sh[w][:, :N], ab[:, :N], fn)
-        assert err.max() <= 1e-5, (N, W, m, n_up, S, w, err.max())
+    Sd = torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
+    q.state_init(dev(R), Sd, fn, N, n_up)
+    check_sweep(q, R, Sd.cpu().numpy(), ks, delta, u, fn, N, n_up)
 
 
 def _j1_cases(n=20, seed=2027):
@@ -250,43 +236,24 @@ def _sweep_j1_cases(n=8, seed=2029):
         out.append(dict(N=max(2, _log_uniform(rng, 2, 1024)), W=int(rng.integers(1, 5)), n_ions=int(rng.integers(S, 257)),
                         S=S, m=tuple(int(x) for x in rng.integers(4, 17, 4)),
                         rcut=tuple(float(x) for x in rng.uniform(0.2, 0.5, 4)), seed=int(rng.integers(2**31)),
-                        up_frac=float(rng.choice([0.0, 1.0, rng.random(), 0.5])), moves=int(rng.integers(1, 48))))
+                        up_frac=float(rng.choice([0.0, 1.0, rng.random(), 0.5])), moves=int(rng.integers(1, 129))))
     return out
 
 
 @pytest.mark.parametrize("c", _sweep_j1_cases(), ids=lambda c: f"N{c['N']}-W{c['W']}-ions{c['n_ions']}-S{c['S']}")
 def test_sweep_j1_random(q, c):
-    """qj2_sweep with J1 joined to every move, vs the oracle (eval_j2 + eval_j1)."""
-    N, W, n_ions, S_, seed = c["N"], c["W"], c["n_ions"], c["S"], c["seed"]
-    S = min(c["moves"], N)
+    """qj2_sweep with J1 joined to every move vs the oracle (tests/sweep_check.py)."""
+    N, W, n_ions, S_, seed, S = c["N"], c["W"], c["n_ions"], c["S"], c["seed"], c["moves"]
     L = qmcgen.cell_length(N)
     Np = qmcgen.padded_size(N, 32)
     R = qmcgen.positions(seed, np.arange(W), N, Np, L, np.float32)
     fn = qmcgen.make_functor(seed, L, 8)
-    ks, tr, u = qmcgen.make_sweep(seed, W, N, L, np.float32, S)
+    ks, delta, u = qmcgen.make_sweep_moves(seed, W, N, S, order="random")
     n_up = int(round(c["up_frac"] * N))
     ions, start = qmcgen.make_ions(seed, n_ions, qmcgen.padded_size(n_ions, 4), L, np.float32, n_species=S_)
     fn1 = qmcgen.make_j1_functor(seed, L, n_species=S_, m=c["m"], rcut_frac=c["rcut"])
-    Rd, Sd = dev(R), torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
+    Sd = torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
     S1 = torch.zeros((W, 5, Np), dtype=torch.float32, device="cuda")
-    acc, dj = q.sweep(Rd, Sd, dev(ks), dev(tr), dev(u), fn, N, n_up, j1=(dev(ions), start, fn1, S1))
-    acc, dj = acc.cpu().numpy(), dj.cpu().numpy()
-    Rh, Sh = R.astype(np.float64), np.zeros((W, 5, Np))
-    S1h, A1h = np.zeros((W, 5, Np)), np.zeros((W, 5, Np))
-    for s in range(S):
-        o2, a2, _ = oracle.eval_j2(Rh, ks[s], tr[s], fn, N, n_up)
-        o1, a1 = oracle.eval_j1(ions.astype(np.float64), start, tr[s].astype(np.float64), fn1)
-        d = (o2[:, 1, 0] - o2[:, 0, 0]) + (o1[:, 1, 0] - o1[:, 0, 0])
-        scale = np.maximum(np.maximum(a2[:, :, 0].max(1), a1[:, :, 0].max(1)), 1.0)
-        assert np.max(np.abs(dj[s] - d) / scale) < 1e-5, s
-        rho2 = np.exp(d) ** 2
-        clear = np.abs(u[s] - rho2) > 1e-6 * rho2
-        assert np.array_equal(acc[s][clear], (u[s] < rho2)[clear].astype(np.int32)), s
-        Rh, Sh, _ = oracle.accept(Rh, Sh, ks[s], tr[s][:, 1], acc[s], fn, N, n_up)
-        for w in np.nonzero(acc[s])[0]:
-            S1h[w, :, ks[s][w]] = o1[w, 1]
-            A1h[w, :, ks[s][w]] = a1[w, 1]
-    assert np.array_equal(Rd.cpu().numpy().astype(np.float64), Rh)
-    err1 = oracle.normalized_error_j1(np.moveaxis(S1.cpu().numpy()[:, :, :N], 1, 2),
-                                      np.moveaxis(S1h[:, :, :N], 1, 2), np.moveaxis(A1h[:, :, :N], 1, 2), fn1)
-    assert err1.max() <= 1e-5
+    q.state_init(dev(R), Sd, fn, N, n_up, j1=(dev(ions), start, fn1, S1))
+    check_sweep(q, R, Sd.cpu().numpy(), ks, delta, u, fn, N, n_up, j1=(ions, start, fn1),
+                state_j1=S1.cpu().numpy())

@@ -14,7 +14,8 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "oracle", "oracle.c")
-PINS = ["tests/test_oracle_pins.py", "tests/test_oracle_accept.py", "tests/test_oracle_spo.py"]
+PINS = ["tests/test_oracle_pins.py", "tests/test_oracle_accept.py", "tests/test_oracle_spo.py",
+        "tests/test_oracle_sweep.py"]
 
 MUTANTS = {
     "eval_G_sign": ("nsum_add(&G[c], -g);", "nsum_add(&G[c], g);", 0),
@@ -42,6 +43,11 @@ MUTANTS = {
     "det_ratio_laplacian_not_divided": ("out[4] = nsum_get(&Lp) / rho;", "out[4] = nsum_get(&Lp);"),
     "j1_species_functor": ("orc_bspline(coef + s * coef_stride, m[s], r_cut[s], rho, u);",
                            "orc_bspline(coef, m[s], r_cut[s], rho, u);"),
+    "sweep_ratio_sign": ("double dj = nsum_get(&Tk[0]) - Sw[k];", "double dj = Sw[k] - nsum_get(&Tk[0]);"),
+    "sweep_decision_not_squared": ("J->u[sw] < rho * rho ? 1 : 0;", "J->u[sw] < rho ? 1 : 0;"),
+    "sweep_commit_position": ("for (int c = 0; c < 3; ++c) Rw[c * Np + k] = rnf[c];", ""),
+    "sweep_j1_sign": ("dj += o1n[0] - o1o[0];", "dj -= o1n[0] - o1o[0];"),
+    "propose_wrap_direction": ("if (x < 0.0f) x = x + Lf;", "if (x < 0.0f) x = x - Lf;"),
 }
 
 
