@@ -3,7 +3,7 @@
 CPU oracle (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C3|C4|C5]
+                    [--config NAME] [--dist-backend nccl|gloo] [--same-device]
 
 One step = one pass of the whole hot path (staged
 SoA rows -> on-the-fly distance row -> functor -> fp64 reduction -> out and
@@ -13,10 +13,12 @@ Workload (N=1 default): C3 = one instance of N = 614,400 electrons x W = 1024
 walkers, P = 1, fp32 (7.55 GB of positions: larger than the 126 MB L2, so no
 L2 flush is needed between steps).  BASELINE.json names C3 the "single-GPU
 roofline measurement"; C2 (17 MB) is L2-resident and is a parity case.
-N>1 (torchrun): --config C3 (default) runs one distinct C3 instance per rank
-(weak scaling, no collective on the data path); C4 shards 4096 independent
-instances by rank; C5 splits one N = 4,915,200 instance along the electron
-axis and combines the partial sums with an NCCL all-reduce.
+N>1 (torchrun): the default is C5 -- one N = 4,915,200 instance split along
+the electron axis, the partial sums combined with an NCCL all-reduce (strong
+scaling; at N = 1 C5's per-GPU rate equals C3's, both streaming one pass of
+positions at the HBM roofline).  --config C4 shards 4096 independent instances
+by rank (strong); --config C3 runs one distinct C3 instance per rank (weak
+scaling, no collective on the data path).
 
 Prints ONE JSON line on rank 0.
 """
@@ -49,7 +51,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "C3S", "C3P2", "C3P12", "S1", "S1V", "J1S", "N64S", "N64SJ"])
+    ap.add_argument("--config", default=None,
+                    choices=["C1", "C2", "C2f64", "C3", "C3f64", "C4", "C5", "C3S", "C3P2", "C3P12", "S1", "S1V", "J1S",
+                             "N64S", "N64SJ"],
+                    help="default: C3 at N = 1, C5 (source split + all-reduce) at N > 1")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend at N > 1 (gloo: functional runs of several ranks on one GPU)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="every rank on cuda:0 (functional multi-rank runs on a one-GPU box; not a measurement)")
+    ap.add_argument("--c4-instances", type=int, default=0, help="C4 instance count override (functional runs)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -67,24 +77,25 @@ def dist_env():
     return rank, world, local
 
 
-def dist_init(world, local, backend="nccl"):
+def dist_init(world, device, backend="nccl"):
     import torch
     import torch.distributed as dist
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if backend == "nccl":
-            torch.cuda.set_device(local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
         else:
             dist.init_process_group(backend)
     return dist if world > 1 else None
 
 
 def allreduce_max(x: float, dist_mod) -> float:
+    """max over ranks of a host number (per-rank device-timed spans, e2e times)."""
     if dist_mod is None:
         return x
     import torch
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist_mod.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist_mod.all_reduce(t, op=dist_mod.ReduceOp.MAX)
     return float(t.item())
 
@@ -168,16 +179,67 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+ALU_PEAKS = os.path.join(ROOT, "profiles", "r02_alu_peaks.json")
+
+
+def alu_peaks():
+    """The measured ALU ceilings (tools/probe/alu_peaks.cu, committed as
+    profiles/r02_alu_peaks.json): FP32 / FP64 TFLOP/s (FMA = 2 flops) and the
+    thread-instruction issue rate, or None."""
+    if os.path.exists(ALU_PEAKS):
+        return json.load(open(ALU_PEAKS))
+    return None
+
+
+def kernel_record(config_name: str):
+    """The committed ncu record of a configuration's dominant kernel
+    (profiles/r02_kernels.json, else round 1's profiles/ncu_traffic.json): DRAM
+    bytes and thread instructions per launch."""
+    for name in ("r02_kernels.json", "ncu_traffic.json"):
+        p = os.path.join(ROOT, "profiles", name)
+        if os.path.exists(p):
+            e = json.load(open(p)).get(config_name)
+            if e:
+                return e
+    return {}
+
+
 def committed_traffic(config_name: str):
     """dram read+write bytes per launch of the dominant kernel from the committed
     ncu --set full capture (profiles/), or None."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(p):
-        d = json.load(open(p))
-        e = d.get(config_name)
-        if e:
-            return e.get("dram_bytes_per_launch")
-    return None
+    return kernel_record(config_name).get("dram_bytes_per_launch")
+
+
+FLOPS_PER_TERM = 36       # SURVEY 8(d): algorithmic flops of one functor term (FMA = 2 flops)
+
+
+def alu_roofline(cfg_name, kernel, kms, terms, fp64=False, extra=None):
+    """Roofline of an issue/ALU-bound kernel: algorithmic flops (36 per functor term,
+    FMA = 2) per launch / launch time against the measured FP32 (or FP64) FMA peak;
+    beside it the issue fraction: the kernel's thread instructions per launch (the
+    committed ncu record) / launch time against the measured issue rate."""
+    pk = alu_peaks()
+    flops = terms * FLOPS_PER_TERM
+    achieved = flops / (kms / 1e3) / 1e12
+    if pk:
+        peak = pk["fp64_tflops" if fp64 else "fp32_tflops"]
+        src = (f"measured: {'DFMA' if fp64 else 'FFMA'} throughput, FMA = 2 flops (profiles/r02_alu_peaks.json, "
+               f"{pk['sm_clock_mhz_median']:.0f} MHz)")
+    else:
+        peak = 148 * 128 * 2 * 1.965e9 / 1e12 / (2 if fp64 else 1)
+        src = "derived: 148 SMs x 128 FP32 lanes x 2 flops x 1.965 GHz (no committed measurement)"
+    r = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+         "traffic": committed_traffic(cfg_name), "kernel": kernel, "kernel_ms": kms, "alg_flops_per_launch": flops,
+         "flops_per_term": FLOPS_PER_TERM, "terms_per_launch": terms, "peak_source": src}
+    rec = kernel_record(cfg_name)
+    if pk and rec.get("thread_inst_per_launch"):
+        ti = rec["thread_inst_per_launch"]
+        r["issue"] = {"thread_inst_per_launch": ti, "sass_per_term": ti / terms,
+                      "achieved_tinst_per_s": ti / (kms / 1e3) / 1e12, "peak_tinst_per_s": pk["issue_tinst_per_s"],
+                      "frac": ti / (kms / 1e3) / 1e12 / pk["issue_tinst_per_s"], "source": rec.get("source")}
+    if extra:
+        r.update(extra)
+    return r
 
 
 # ---------------------------------------------------------------------------
@@ -376,12 +438,19 @@ def cpu_model():
     return "unknown"
 
 
+def config_name(args, world):
+    """--config, else the default workload: C3 (BASELINE.json's single-GPU roofline
+    configuration) at N = 1 and C5 (the source-axis split whose partial sums meet
+    in an all-reduce) at N > 1."""
+    return args.config or ("C3" if world == 1 else "C5")
+
+
 def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return 0
     import qmcgen
-    cfg = qmcgen.config(args.config)
+    cfg = qmcgen.config(config_name(args, world))
     cores = cpu_cores()
     budget_total = 120.0
     per_step = max(0.2, min(10.0, budget_total / max(1, args.steps + args.warmup)))
@@ -423,9 +492,15 @@ def workload_config(cfg, world):
                 "nx": cfg.nx, "n_orb": cfg.n_orb, "ld": cfg.ld, "W": cfg.W, "N": cfg.N,
                 "parallelism": f"walker-batch x{world}",
                 "l2": "table 786 MB > 126 MB L2; random gathers (no flush needed)"}
+    sz = 8 if cfg.dtype == "f64" else 4
+    rbytes = cfg.W * 3 * cfg.Np * sz
     desc = {
+        "C1": f"C1: SPEC's tiny instance, N={cfg.N} electrons x W={cfg.W} walkers, P=1, fp64, seed 0(+rank)",
+        "C2": f"C2: N={cfg.N} x W={cfg.W} (100 x C1's N), P=1, fp32, seed 1(+rank)",
+        "C2f64": f"C2f64: N={cfg.N} x W={cfg.W} (100 x C1's N), P=1, fp64, seed 1(+rank)",
         "C3": f"C3: one instance per rank, N={cfg.N} electrons x W={cfg.W} walkers, P=1, fp32, seed 2(+rank)",
-        "C4": f"C4: 4096 instances of N={cfg.N} x W={cfg.W}, P=1, fp32, seeds 3..4098, sharded by instance",
+        "C3f64": f"C3f64: C3's instance in fp64 (N={cfg.N} x W={cfg.W}, P=1, seed 2(+rank)): the fp64 path",
+        "C4": f"C4: {cfg.instances} instances of N={cfg.N} x W={cfg.W}, P=1, fp32, seeds 3.., sharded by instance",
         "C5": f"C5: one instance N={cfg.N} x W={cfg.W}, P=1, fp32, seed 5, split along N + NCCL all-reduce",
         "C3P2": f"C3P2 (NEXT-3): C3 instance per rank (N={cfg.N} x W={cfg.W}, fp32, seed 2(+rank)), P=2 drift "
                 f"variant (U^2_k at r_k and r'_k in one step, ratio fused)",
@@ -434,40 +509,57 @@ def workload_config(cfg, world):
         "N64SJ": f"N64SJ: as N64S with the one-body Jastrow over NiO-64's 64 ions (Ni, O) joined to every move's "
                  f"ratio (dJ1 + dJ2) and state, one qj2_sweep launch per sweep",
         "N64S": f"N64S: the paper's NiO-64 size (N={cfg.N} electrons, Table 1) x W={cfg.W} walkers, fp32: one full "
-                f"particle-by-particle sweep per step ({cfg.N} moves: eval at (r_k, r'_k) -> Metropolis -> accept "
-                f"of R and the 5N state) in one qj2_sweep launch",
+                f"particle-by-particle sweep per step ({cfg.N} moves: r'_k = wrap(r_k + delta) -> U^2_k(R') on the "
+                f"fly -> ratio against the stored U^2_k(R) -> Metropolis -> on acceptance the update of R and the "
+                f"5N state) in one qj2_sweep launch, continuing the Markov chain from step to step",
         "C3S": f"C3S (NEXT-2 sweep step): C3 instance per rank (N={cfg.N} x W={cfg.W}, fp32, seed 2(+rank)), "
                f"one PbyP move per walker: eval at (r_k, r'_k) -> Metropolis -> accept-side update of R and "
                f"the 5N fp32 J2 state",
     }[name]
-    return {"workload": desc, "N": cfg.N, "W": cfg.W, "P": {"C3S": 2, "C3P2": 2, "C3P12": 12, "N64S": 2, "N64SJ": 2}.get(name, 1), "m": cfg.m, "Np": cfg.Np,
-            "parallelism": f"{'walker-instance' if name != 'C5' else 'source-axis'} x{world}",
-            "l2": ("R, state and moves (~53 MB) < 126 MB L2: 256 MB L2 flush before every timed step"
-                   if name in ("N64S", "N64SJ") else "inputs > 126 MB L2 (no flush needed)")}
+    if name in ("N64S", "N64SJ"):
+        l2 = "R, state and moves (~53 MB) < 126 MB L2: 256 MB L2 flush before every timed step"
+    elif rbytes < (126 << 20):
+        l2 = f"positions {rbytes / 1e6:.1f} MB < 126 MB L2: 256 MB L2 flush before every timed step"
+    else:
+        l2 = f"inputs ({rbytes / 1e9:.2f} GB of positions per instance) > 126 MB L2 (no flush needed)"
+    return {"workload": desc, "N": cfg.N, "W": cfg.W,
+            "P": {"C3S": 2, "C3P2": 2, "C3P12": 12}.get(name, 1), "m": cfg.m, "Np": cfg.Np, "dtype": cfg.dtype,
+            "parallelism": f"{'source-axis' if name == 'C5' else ('instance' if name == 'C4' else 'walker-instance')} x{world}",
+            "l2": l2}
 
 
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-class C3Plan:
-    """One C3-shaped instance per rank (weak scaling; no collective on the data path)."""
-    mode = "C3"
-    launches_per_step = 2      # j2_eval_kernel + the 4 KB counter memset issued by qj2_eval
+class EvalPlan:
+    """The hot path on one instance per rank (C1, C2, C2f64, C3, C3f64; weak
+    scaling, no collective on the data path): one qj2_eval launch over all W
+    walkers, P = 1, ratio fused against the caller's 5N-state value V_cur."""
+    launches_per_step = 2      # j2_eval kernel + the counter memset (multi-tile rows; 1 for one-tile rows)
 
     def __init__(self, cfg, rank, world):
+        import torch
         self.cfg = cfg
+        self.mode = cfg.name
         self.seed = cfg.seed + rank
         self.items_per_step = cfg.W * (cfg.N - 1)
+        self.f64 = cfg.dtype == "f64"
+        self.tdt = torch.float64 if self.f64 else torch.float32
+        self.sz = 8 if self.f64 else 4
+        # inputs that fit in the 126 MB L2 (C1, C2, C2f64) are flushed before every timed step
+        self.flush_l2 = cfg.W * 3 * cfg.Np * self.sz < (126 << 20)
+        self.ch = 204800 if not self.f64 else 102400          # tile of the CTA kernel (sources)
+        if cfg.N <= 2048 or (cfg.N <= self.ch and cfg.W >= 4096):
+            self.launches_per_step = 1
 
     def items_total(self, world):
         return self.items_per_step * world
 
     def _alg(self):
         cfg = self.cfg
-        sz = 4
-        # algorithmic bytes (DESIGN.md "Roofline"): x, y, z of every source i != k once per walker,
-        # plus per walker k (4 B), r_trial (12 B), V_cur (8 B), out (40 B), ratio (16 B)
-        return cfg.W * (cfg.N - 1) * 3 * sz + cfg.W * (4 + 12 + 8 + 40 + 16)
+        # algorithmic bytes (DESIGN.md section 7): x, y, z of every source i != k once per walker, plus per
+        # walker k (4 B), r_trial (3 sz), V_cur (8 B), out (40 B), ratio (16 B)
+        return cfg.W * (cfg.N - 1) * 3 * self.sz + cfg.W * (4 + 3 * self.sz + 8 + 40 + 16)
 
     @property
     def alg_bytes_per_launch(self):
@@ -478,13 +570,13 @@ class C3Plan:
         import qmcgen
         cfg = self.cfg
         self.fn = q.Functor.of(qmcgen.make_functor(cfg.seed, cfg.L, cfg.m))
-        self.R = q.gen_positions(self.seed, cfg.W, cfg.N, cfg.Np, cfg.L, torch.float32)
+        self.R = q.gen_positions(self.seed, cfg.W, cfg.N, cfg.Np, cfg.L, self.tdt)
         k = qmcgen.make_k(self.seed, cfg.W, cfg.N)
-        rt = qmcgen.make_trials(self.seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32)
-        rk = qmcgen.make_trials(self.seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32, mode="noop")
+        rt = qmcgen.make_trials(self.seed, np.arange(cfg.W), k, cfg.N, cfg.L, cfg.np_dtype)
+        rk = qmcgen.make_trials(self.seed, np.arange(cfg.W), k, cfg.N, cfg.L, cfg.np_dtype, mode="noop")
         self.k = torch.from_numpy(k).cuda()
         self.rt = torch.from_numpy(rt).cuda()
-        self.ws = q.Workspace(q.workspace_size(cfg.W, 1, cfg.N, torch.float32))
+        self.ws = q.Workspace(q.workspace_size(cfg.W, 1, cfg.N, self.tdt))
         # the caller's 5N state: U^2_k(R) at the current positions (untimed)
         v0 = q.eval(self.R, self.k, torch.from_numpy(rk).cuda(), self.fn, cfg.N, cfg.n_up, workspace=self.ws)
         self.V_cur = v0[:, 0, 0].contiguous()
@@ -498,15 +590,32 @@ class C3Plan:
                out=self.out, ratio_out=self.ratio, workspace=self.ws)
 
     def kernel_ms(self, q, stream, reps):
-        import torch
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(reps):
-            self.step(q, None)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / reps
+        if self.flush_l2:
+            return self.flusher.event_ms(lambda: self.step(q, None), stream, reps)
+        return _event_ms(lambda: self.step(q, None), stream, reps)
+
+    def gpu_sample(self, n):
+        """(out [n][P][5]) of walkers [0, n) from the last step, for the parity field."""
+        return self.out[:n].cpu().numpy()
+
+    def roofline(self, kms, peak_hbm):
+        cfg = self.cfg
+        achieved = self._alg() / (kms / 1e3) / 1e9
+        kern = ("j2_eval_warp_kernel" if self.launches_per_step == 1 else "j2_eval_kernel") + \
+            f"<{'double' if self.f64 else 'float'}>"
+        r = {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s", "frac": achieved / peak_hbm,
+             "traffic": committed_traffic(self.mode), "kernel": kern, "kernel_ms": kms,
+             "alg_bytes_per_launch": self._alg(), "bytes_per_item": 3 * self.sz}
+        if self.flush_l2:
+            r["regime"] = (f"launch/latency-bound: {cfg.W * 3 * cfg.Np * self.sz / 1e6:.1f} MB of positions per step "
+                           f"(L2 flushed before every step); not an HBM measurement (SURVEY 8(d))")
+        if self.f64:      # the fp64 path also against the measured DFMA peak (36 flops per term)
+            pk = alu_peaks()
+            if pk:
+                fl = cfg.W * (cfg.N - 1) * FLOPS_PER_TERM / (kms / 1e3) / 1e12
+                r["fp64_alu"] = {"achieved": fl, "peak": pk["fp64_tflops"], "unit": "TFLOP/s",
+                                 "frac": fl / pk["fp64_tflops"], "source": "profiles/r02_alu_peaks.json (DFMA)"}
+        return r
 
     def e2e(self, q, steps, dist_mod):
         """Same metric through the public host-buffer API (qj2_eval_host): every step copies the
@@ -516,18 +625,19 @@ class C3Plan:
         try:
             Rh = torch.empty(self.R.shape, dtype=self.R.dtype, pin_memory=True)
             pinned = True
-        except RuntimeError as e:       # host without room to pin 7.55 GB per rank: pageable copies
+        except RuntimeError as e:       # host without room to pin the positions: pageable copies
             log(f"[bench] pinned host buffer unavailable ({e}); e2e uses pageable memory")
             Rh = torch.empty(self.R.shape, dtype=self.R.dtype)
             pinned = False
         Rh.copy_(self.R)
         kh = self.k.cpu().pin_memory()
         th = self.rt.cpu().pin_memory()
-        vh = self.V_cur.cpu().pin_memory()
-        outh = torch.empty((cfg.W, 1, 5), dtype=torch.float64, pin_memory=True)
-        rath = torch.empty((cfg.W, 1, 2), dtype=torch.float64, pin_memory=True)
-        chunk = 32
-        ws = q.Workspace(q.host_workspace_size(cfg.W, 1, cfg.Np, torch.float32, chunk))
+        vh = self.V_cur.cpu().pin_memory() if self.V_cur is not None else None
+        P = th.shape[1]
+        outh = torch.empty((cfg.W, P, 5), dtype=torch.float64, pin_memory=True)
+        rath = torch.empty((cfg.W, P, 2), dtype=torch.float64, pin_memory=True)
+        chunk = 32 if cfg.N > 100000 else max(32, min(cfg.W, 256))
+        ws = q.Workspace(q.host_workspace_size(cfg.W, P, cfg.Np, self.tdt, chunk))
         run = lambda: q.eval_host(Rh, kh, th, self.fn, cfg.N, cfg.n_up, V_cur=vh, ratio=True,  # noqa: E731
                                   chunk_walkers=chunk, out=outh, ratio_out=rath, workspace=ws)
         run()
@@ -541,7 +651,7 @@ class C3Plan:
         dt = allreduce_max(dt, dist_mod)
         same = bool(torch.equal(outh, self.out.cpu()))
         world = dist_mod.get_world_size() if dist_mod else 1
-        h2d = Rh.numel() * 4 + kh.numel() * 4 + th.numel() * 4 + vh.numel() * 8
+        h2d = Rh.numel() * self.sz + kh.numel() * 4 + th.numel() * self.sz + (vh.numel() * 8 if vh is not None else 0)
         d2h = outh.numel() * 8 + rath.numel() * 8
         del Rh
         return {"value": self.items_per_step * world / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
@@ -757,7 +867,7 @@ class C4Plan:
         return None   # see DESIGN.md: the host-buffer path is measured on C3
 
 
-class MultiTrialPlan(C3Plan):
+class MultiTrialPlan(EvalPlan):
     """NEXT-3: the hot path with P trial positions per walker (P = 2 drift
     variant, P = 12 NLPP quadrature), one eval launch per step; the P trials
     of a tile run on consecutive CTAs (one HBM read, L2 hits for the rest).
@@ -797,26 +907,13 @@ class MultiTrialPlan(C3Plan):
         self.ratio = torch.empty((cfg.W, self.P, 2), dtype=torch.float64, device="cuda")
         torch.cuda.synchronize()
 
-    def e2e(self, q, steps, dist_mod):
-        return None   # see DESIGN.md: the host-buffer path is measured on C3
-
-    OPS_PER_PAIR = 36          # algorithmic operations per (walker, trial, source) pair
-
     def roofline(self, kms, peak_hbm):
         cfg = self.cfg
-        pairs = cfg.W * self.P * (cfg.N - 1)
-        ops = pairs * self.OPS_PER_PAIR
-        clk = 1.965e9
-        peak = 148 * 128 * clk / 1e12           # one FP32/ALU op per lane per clock (the issue ceiling), T/s
-        achieved = ops / (kms / 1e3) / 1e12
         hbm = self._alg() / (kms / 1e3) / 1e9
-        return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": committed_traffic(self.mode), "kernel": "j2_eval_kernel<float,1,false>", "kernel_ms": kms,
-                "alg_ops_per_launch": ops, "ops_per_pair": self.OPS_PER_PAIR,
-                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1.965 GHz, one op per lane per clock "
-                               "(B200_PROFILING.md unit counts; DESIGN.md section 7)",
-                "hbm": {"achieved": hbm, "peak": peak_hbm, "unit": "GB/s", "frac": hbm / peak_hbm,
-                        "alg_bytes_per_launch": self._alg()}}
+        return alu_roofline(self.mode, "j2_eval_kernel<float,false,2,3> (one trial per CTA, the P trials of a tile "
+                            "on consecutive CTAs)", kms, cfg.W * self.P * (cfg.N - 1),
+                            extra={"hbm": {"achieved": hbm, "peak": peak_hbm, "unit": "GB/s", "frac": hbm / peak_hbm,
+                                           "alg_bytes_per_launch": self._alg()}})
 
 
 class SweepPlan:
@@ -903,7 +1000,6 @@ class GraphSweepPlan(SweepPlan):
     also times one sweep's moves as per-move launches (qj2_eval + qj2_metropolis_
     accept, 2 per move), eagerly and captured in a CUDA graph."""
     mode = "N64S"
-    OPS_PER_PAIR = 36                   # algorithmic flops per functor term (SURVEY 8(d))
     flush_l2 = True                     # R, state and the moves (~53 MB) fit in L2
     POOL = 4
 
@@ -933,10 +1029,9 @@ class GraphSweepPlan(SweepPlan):
             self.j1 = (torch.from_numpy(ions).cuda(), start, fn1,
                        torch.zeros((cfg.W, 5, cfg.Np), dtype=torch.float32, device="cuda"))
         q.state_init(self.R, self.S_, self.fn, cfg.N, cfg.n_up, j1=self.j1)       # untimed
-        ks, dl, u = qmcgen.make_sweep_moves(self.seed, cfg.W, cfg.N, self.POOL * self.S)
-        self.moves = [(torch.from_numpy(ks[i * self.S:(i + 1) * self.S]).cuda(),
-                       torch.from_numpy(dl[i * self.S:(i + 1) * self.S]).cuda(),
-                       torch.from_numpy(u[i * self.S:(i + 1) * self.S]).cuda()) for i in range(self.POOL)]
+        self.moves = [tuple(torch.from_numpy(a).cuda()
+                            for a in qmcgen.make_sweep_moves(self.seed, cfg.W, cfg.N, self.S, stream=i))
+                      for i in range(self.POOL)]
         self.acc_all = torch.empty((self.S, cfg.W), dtype=torch.int32, device="cuda")
         self.dj_all = torch.empty((self.S, cfg.W), dtype=torch.float64, device="cuda")
         # context: one sweep's moves as per-move launches on copies (pre-drawn (r_k, r'_k) pairs of an
@@ -1031,16 +1126,10 @@ class GraphSweepPlan(SweepPlan):
         acc = (self.acc_all == 1).float().mean().item()    # acceptance of the last timed sweep
         # functor terms per move: N - 1 at r'_k, N - 1 more at r_k when accepted; J1: 2 per ion
         terms = self.S * cfg.W * ((cfg.N - 1) * (1.0 + acc) + (2 * self.N_IONS if self.with_j1 else 0))
-        ops = terms * self.OPS_PER_PAIR
-        peak = 148 * 128 * 1.965e9 / 1e12
-        achieved = ops / (kms / 1e3) / 1e12
-        return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": committed_traffic(self.mode),
-                "kernel": "j2_sweep_kernel (one launch per sweep, walkers resident in shared memory"
-                          + (", J1 over 64 ions in every move)" if self.with_j1 else ")"),
-                "kernel_ms": kms, "alg_ops_per_launch": ops, "ops_per_pair": self.OPS_PER_PAIR,
-                "per_move_launches_eager_ms": self.eager_ms, "per_move_launches_graph_ms": self.graph_ms,
-                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1.965 GHz (DESIGN.md section 7)"}
+        return alu_roofline(self.mode, "j2_sweep_kernel (one launch per sweep, walkers resident in shared memory"
+                            + (", J1 over 64 ions in every move)" if self.with_j1 else ")"), kms, terms,
+                            extra={"acceptance": acc, "per_move_launches_eager_ms": self.eager_ms,
+                                   "per_move_launches_graph_ms": self.graph_ms})
 
 
 class SpoPlan:
@@ -1132,7 +1221,6 @@ class J1Plan:
     shared memory, one thread per trial point).  Issue-bound: ALU roofline."""
     mode = "J1S"
     launches_per_step = 1
-    OPS_PER_PAIR = 36
     flush_l2 = True                     # trial points + outputs (~41 MB) fit in L2
 
     def __init__(self, cfg, rank, world):
@@ -1169,14 +1257,7 @@ class J1Plan:
 
     def roofline(self, kms, peak_hbm):
         cfg = self.cfg
-        ops = cfg.W * cfg.n_ions * self.OPS_PER_PAIR
-        peak = 148 * 128 * 1.965e9 / 1e12
-        achieved = ops / (kms / 1e3) / 1e12
-        return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": committed_traffic(self.mode), "kernel": "j1_thread_kernel<float>", "kernel_ms": kms,
-                "alg_ops_per_launch": ops, "ops_per_pair": self.OPS_PER_PAIR,
-                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1.965 GHz, one op per lane per clock "
-                               "(DESIGN.md section 7)"}
+        return alu_roofline("J1S", "j1_thread_kernel<float>", kms, cfg.W * cfg.n_ions)
 
     def e2e(self, q, steps, dist_mod):
         """Through the public API with host buffers: each step uploads the sweep's
@@ -1222,8 +1303,8 @@ def make_plan(cfg, rank, world):
         return MultiTrialPlan(cfg, rank, world)
     if cfg.name == "C3S":
         return SweepPlan(cfg, rank, world)
-    if cfg.name == "C3":
-        return C3Plan(cfg, rank, world)
+    if cfg.name in ("C1", "C2", "C2f64", "C3", "C3f64"):
+        return EvalPlan(cfg, rank, world)
     if cfg.name == "C4":
         return C4Plan(cfg, rank, world)
     if cfg.name == "C5":
@@ -1241,12 +1322,16 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world != args.gpus:
         log(f"[bench] warning: --gpus {args.gpus} but WORLD_SIZE {world}")
-    torch.cuda.set_device(local)
-    dist_mod = dist_init(world, local)
+    device = 0 if args.same_device else local
+    torch.cuda.set_device(device)
+    dist_mod = dist_init(world, device, args.dist_backend)
     import qmcgen
     import paper_1708_02645_b200 as q
     q.device_check()
-    cfg = qmcgen.config(args.config)
+    cfg = qmcgen.config(config_name(args, world))
+    if cfg.name == "C4" and args.c4_instances:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, instances=args.c4_instances)
 
     plan = make_plan(cfg, rank, world)
     if plan.mode in ("N64S", "N64SJ"):
@@ -1319,7 +1404,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "weak" if plan.mode in ("C3", "C3S", "C3P2", "C3P12", "S1", "S1V", "J1S", "N64S", "N64SJ") else "strong",
+            "scaling": "strong" if plan.mode in ("C4", "C5") else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(cfg, world),
             "roofline": (plan.roofline(kms, peak) if hasattr(plan, "roofline") else

@@ -23,12 +23,9 @@
  *   different workspaces are independent and may run concurrently.
  * - Device entry points require an sm_100 device (else QJ2_ENOTSUP).
  * - All sizes are int64; all flat offsets inside kernels are 64-bit.
- * - Kernel variants are chosen from the arguments alone.  The QJ2_KERNEL,
- *   QJ2_WARP, QJ2_J1_WARP, QJ2_SPO, QJ2_SPO_SMEM_KB, QJ2_SWEEP_TPB and
- *   QJ2_SWEEP_NOFULL environment variables are A/B measurement switches
- *   (read at each call, so a measuring process can flip them); leave them
- *   unset in production.  Every variant they select computes the same
- *   results within the parity bar (the GPU suite passes with each).
+ * - Kernel variants are chosen from the arguments alone (one variant per
+ *   argument shape; no environment variable is read).  The alternatives
+ *   measured against them are compile-time builds (tools/ab).
  */
 #ifndef QMCJ2_H
 #define QMCJ2_H
@@ -364,7 +361,7 @@ typedef struct {
                                 /* nx*ny*nz*ld < 2^31; lanes [n_orb, ld) ignored  */
 } qj2_spo_table;
 
-enum { QJ2_SPO_V = 0, QJ2_SPO_VGH = 1 };
+enum { QJ2_SPO_V = 0, QJ2_SPO_VGH = 1, QJ2_SPO_GATHER = 0x10 };
 
 /* qj2_spo_eval -- "Bspline-v" (what = QJ2_SPO_V) or "Bspline-vgh"          */
 /* (QJ2_SPO_VGH) at one position per walker, fused with the determinant     */
@@ -375,6 +372,10 @@ enum { QJ2_SPO_V = 0, QJ2_SPO_VGH = 1 };
 /*   and lap D / D at R'; same lemma).                        */
 /* Arguments                                                                 */
 /*   tab        host struct (the table itself is device memory).             */
+/*   what       QJ2_SPO_V or QJ2_SPO_VGH, optionally | QJ2_SPO_GATHER: use    */
+/*              the per-thread-gather kernel (the one taken for rows too long */
+/*              for the TMA ring) regardless of the row length -- the same    */
+/*              sums in the same order, for validation of that kernel.        */
 /*   pos_dtype  QJ2_FP32 / QJ2_FP64 of pos.                                  */
 /*   W          evaluations (>= 0).                                          */
 /*   pos        device, row w at pos + w*pos_stride elements (x, y, z), any  */

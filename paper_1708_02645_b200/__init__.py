@@ -269,12 +269,20 @@ def eval(R, k, r_trial, fn, n_total: int, n_up: int, *, i_offset: int = 0, n_loc
     if out is None:
         out = torch.empty((W, P, 5), dtype=torch.float64, device=dev)
     _req(out, "out", torch.float64)
+    _shape(out, "out", (W, P, 5))
     if row and row_out is None:
         row_out = torch.empty((W, P, 4, Np), dtype=R.dtype, device=dev)
+    if row:
+        _req(row_out, "row_out", R.dtype)
+        _shape(row_out, "row_out", (W, P, 4, Np))
     if ratio and ratio_out is None:
         ratio_out = torch.empty((W, P, 2), dtype=torch.float64, device=dev)
+    if ratio:
+        _req(ratio_out, "ratio_out", torch.float64)
+        _shape(ratio_out, "ratio_out", (W, P, 2))
     if V_cur is not None:
         _req(V_cur, "V_cur", torch.float64, 1)
+        _shape(V_cur, "V_cur", (W,))
     need = workspace_size(max(W, 0), P, max(n_local, 1), R.dtype) if W > 0 and n_local >= 1 else 0
     ws = workspace if workspace is not None else Workspace(device=dev)
     ws.reserve(need)
@@ -333,17 +341,32 @@ def eval_j1(ions, species_start, r_trial, fn1, *, row: bool = False, V_cur=None,
     _req(ions, "ions", ndim=2)
     _req(r_trial, "r_trial", ions.dtype, 3)
     W, P = r_trial.shape[0], r_trial.shape[1]
+    if ions.shape[0] != 3 or r_trial.shape[2] != 3:
+        raise ValueError("ions must be [3][Np] and r_trial [W][P][3]")
     Np = ions.shape[1]
     f = J1Functor.of(fn1)
+    if len(species_start) != len(f.m) + 1 or int(species_start[-1]) > Np:
+        raise ValueError("species_start must have n_species + 1 entries and end <= Np")
     st = (ctypes.c_int64 * (len(f.m) + 1))(*[int(x) for x in species_start])
     n_ions = int(species_start[-1])
     dev = ions.device
     if out is None:
         out = torch.empty((W, P, 5), dtype=torch.float64, device=dev)
+    _req(out, "out", torch.float64)
+    _shape(out, "out", (W, P, 5))
     if row and row_out is None:
         row_out = torch.empty((W, P, 4, Np), dtype=ions.dtype, device=dev)
+    if row:
+        _req(row_out, "row_out", ions.dtype)
+        _shape(row_out, "row_out", (W, P, 4, Np))
     if ratio and ratio_out is None:
         ratio_out = torch.empty((W, P, 2), dtype=torch.float64, device=dev)
+    if ratio:
+        _req(ratio_out, "ratio_out", torch.float64)
+        _shape(ratio_out, "ratio_out", (W, P, 2))
+    if V_cur is not None:
+        _req(V_cur, "V_cur", torch.float64, 1)
+        _shape(V_cur, "V_cur", (W,))
     need = workspace_size(W, P, max(n_ions, 1), ions.dtype) if W > 0 else 0
     ws = workspace if workspace is not None else Workspace(device=dev)
     ws.reserve(need)
@@ -364,16 +387,21 @@ def ratio(out, V_cur=None, ratio_out=None, stream=None):
     W, P, _ = out.shape
     if ratio_out is None:
         ratio_out = torch.empty((W, P, 2), dtype=torch.float64, device=out.device)
+    _req(ratio_out, "ratio_out", torch.float64)
+    _shape(ratio_out, "ratio_out", (W, P, 2))
     if V_cur is not None:
         _req(V_cur, "V_cur", torch.float64, 1)
+        _shape(V_cur, "V_cur", (W,))
     _check(_lib.qj2_ratio(W, P, _ptr(out), _ptr(V_cur), _ptr(ratio_out), ctypes.c_void_p(_stream_ptr(stream))),
            "qj2_ratio")
     return ratio_out
 
 
-def _row_ptr(t: torch.Tensor, trial: int, width: int):
+def _row_ptr(t: torch.Tensor, trial: int, width: int, W: int | None = None):
     """(pointer, stride in elements) of trial `trial` of a [W][P][width]
-    (or [W][width]) contiguous tensor."""
+    (or [W][width]) contiguous tensor (W checked when given)."""
+    if t.dim() not in (2, 3) or t.shape[-1] != width or (W is not None and t.shape[0] != W):
+        raise ValueError(f"expected a [W={W}][P][{width}] or [W][{width}] tensor, got {tuple(t.shape)}")
     if t.dim() == 2:
         if trial != 0:
             raise ValueError("trial index on a [W][width] tensor")
@@ -396,13 +424,16 @@ def accept(R, state, k, r_new, acc, out_new, fn, n_total: int, n_up: int, *, tri
     if tuple(state.shape) != (W, 5, Np):
         raise ValueError("state must be [W][5][Np]")
     _req(k, "k", torch.int32, 1)
+    _shape(k, "k", (W,))
     _req(acc, "acc", torch.int32, 1)
+    _shape(acc, "acc", (W,))
     _req(r_new, "r_new", R.dtype)
     if r_old is not None:
         _req(r_old, "r_old", R.dtype, 2)
+        _shape(r_old, "r_old", (W, 3))
     _req(out_new, "out_new", torch.float64)
-    rp, rs = _row_ptr(r_new, trial, 3)
-    op, os_ = _row_ptr(out_new, trial, 5)
+    rp, rs = _row_ptr(r_new, trial, 3, W)
+    op, os_ = _row_ptr(out_new, trial, 5, W)
     n_local = min(Np, n_total - i_offset) if n_local is None else int(n_local)
     f = Functor.of(fn)
     b = ctypes.c_size_t()
@@ -426,20 +457,28 @@ def metropolis_accept(R, state, k, r_trial, out, u, fn, n_total: int, n_up: int,
     _req(R, "R", ndim=3)
     W, _, Np = R.shape
     _req(state, "state", R.dtype, 3)
+    _shape(state, "state", (W, 5, Np))
     _req(k, "k", torch.int32, 1)
+    _shape(k, "k", (W,))
     _req(r_trial, "r_trial", R.dtype, 3)
     _req(out, "out", torch.float64, 3)
+    if out.shape[1] != r_trial.shape[1]:
+        raise ValueError("out and r_trial must have the same number of trials")
     _req(u, "u", torch.float64, 1)
-    rn, rs = _row_ptr(r_trial, trial_new, 3)
-    ro, _ = _row_ptr(r_trial, trial_old, 3)
-    on, os_ = _row_ptr(out, trial_new, 5)
+    _shape(u, "u", (W,))
+    rn, rs = _row_ptr(r_trial, trial_new, 3, W)
+    ro, _ = _row_ptr(r_trial, trial_old, 3, W)
+    on, os_ = _row_ptr(out, trial_new, 5, W)
     if V_cur is not None:
         _req(V_cur, "V_cur", torch.float64, 1)
+        _shape(V_cur, "V_cur", (W,))
         vr, vrs = _ptr(V_cur), 1
     else:
-        vr, vrs = _row_ptr(out, trial_old, 5)
+        vr, vrs = _row_ptr(out, trial_old, 5, W)
     if acc is None:
         acc = torch.empty(W, dtype=torch.int32, device=R.device)
+    _req(acc, "acc", torch.int32, 1)
+    _shape(acc, "acc", (W,))
     n_local = min(Np, n_total - i_offset) if n_local is None else int(n_local)
     f = Functor.of(fn)
     _check(_lib.qj2_metropolis_accept(f.ptr, _dtype_code(R.dtype), W, n_total, n_up, i_offset, n_local, Np,
@@ -528,15 +567,17 @@ def metropolis(ratio_out, u, acc=None, *, trial: int = 0, stream=None):
     _req(ratio_out, "ratio_out", torch.float64)
     _req(u, "u", torch.float64, 1)
     W = u.shape[0]
-    rp, rs = _row_ptr(ratio_out, trial, 2)
+    rp, rs = _row_ptr(ratio_out, trial, 2, W)
     if acc is None:
         acc = torch.empty(W, dtype=torch.int32, device=u.device)
+    _req(acc, "acc", torch.int32, 1)
+    _shape(acc, "acc", (W,))
     _check(_lib.qj2_metropolis(W, rp, rs, _ptr(u), _ptr(acc), ctypes.c_void_p(_stream_ptr(stream))),
            "qj2_metropolis")
     return acc
 
 
-QJ2_SPO_V, QJ2_SPO_VGH = 0, 1
+QJ2_SPO_V, QJ2_SPO_VGH, QJ2_SPO_GATHER = 0, 1, 0x10
 
 
 class SpoTable:
@@ -562,14 +603,17 @@ class SpoTable:
 
 
 def spo_eval(tab: SpoTable, pos, *, vgh: bool = True, Ainv=None, krow=None, trial: int = 0, all_trials: bool = False,
-             out=None, spo_out=None, want_spo: bool = False, stream=None):
+             out=None, spo_out=None, want_spo: bool = False, kernel: str = "auto", stream=None):
     """qj2_spo_eval (NEXT-4): Bspline-vgh (vgh=True) or Bspline-v at pos
     ([W][3], or [W][P][3]: trial `trial`, or every trial with all_trials=True --
     then the P points of a walker share its A^{-1} row, e.g. the NLPP
     quadrature), fused with the determinant ratio against Ainv (fp32,
     [W][n][lda] with krow [W] int32, or [W][lda] rows).  Returns out
     [W*P or W][5] fp64 (rho, G, L) (None without Ainv) and, if want_spo, spo
-    [evaluations][10 or 1][ld] fp32."""
+    [evaluations][10 or 1][ld] fp32.  kernel="gather" selects the per-thread-gather
+    kernel (QJ2_SPO_GATHER) instead of the automatic choice."""
+    if kernel not in ("auto", "gather"):
+        raise ValueError("kernel must be 'auto' or 'gather'")
     _req(pos, "pos")
     ppw = 1
     if all_trials and pos.dim() == 3:
@@ -582,20 +626,36 @@ def spo_eval(tab: SpoTable, pos, *, vgh: bool = True, Ainv=None, krow=None, tria
     a_ptr, a_stride, a_ld = None, 0, 0
     if Ainv is not None:
         _req(Ainv, "Ainv", torch.float32)
+        n_walk = W // ppw                # walkers owning an A^{-1} row (points_per_walker points each)
+        if W % ppw:
+            raise ValueError("the evaluation count must be a multiple of points_per_walker")
         if Ainv.dim() == 3:
             if krow is None:
                 raise ValueError("krow is required with a [W][n][lda] Ainv")
             _req(krow, "krow", torch.int32, 1)
+            _shape(krow, "krow", (n_walk,))
+            if Ainv.shape[0] != n_walk or Ainv.shape[2] < tab.n_orb:
+                raise ValueError(f"Ainv must be [{n_walk}][n][>= {tab.n_orb}], got {tuple(Ainv.shape)}")
             a_stride, a_ld = Ainv.shape[1] * Ainv.shape[2], Ainv.shape[2]
-        else:
+        elif Ainv.dim() == 2:
+            if Ainv.shape[0] != n_walk or Ainv.shape[1] < tab.n_orb:
+                raise ValueError(f"Ainv must be [{n_walk}][>= {tab.n_orb}], got {tuple(Ainv.shape)}")
             a_stride, a_ld = Ainv.shape[1], Ainv.shape[1]
             krow = None
+        else:
+            raise ValueError("Ainv must be [W][n][lda] (with krow) or [W][lda]")
         a_ptr = _ptr(Ainv)
         if out is None:
             out = torch.empty((W, 5), dtype=torch.float64, device=dev)
+        _req(out, "out", torch.float64)
+        _shape(out, "out", (W, 5))
     if want_spo and spo_out is None:
         spo_out = torch.empty((W, 10 if vgh else 1, ldv), dtype=torch.float32, device=dev)
-    _check(_lib.qj2_spo_eval(tab.ptr, QJ2_SPO_VGH if vgh else QJ2_SPO_V, _dtype_code(pos.dtype), W, pp, ps,
+    if spo_out is not None:
+        _req(spo_out, "spo_out", torch.float32)
+        _shape(spo_out, "spo_out", (W, 10 if vgh else 1, ldv))
+    what = (QJ2_SPO_VGH if vgh else QJ2_SPO_V) | (QJ2_SPO_GATHER if kernel == "gather" else 0)
+    _check(_lib.qj2_spo_eval(tab.ptr, what, _dtype_code(pos.dtype), W, pp, ps,
                              a_ptr, a_stride, a_ld, _ptr(krow), ppw, _ptr(out) if Ainv is not None else None,
                              _ptr(spo_out), ctypes.c_void_p(_stream_ptr(stream))), "qj2_spo_eval")
     if want_spo:
@@ -630,13 +690,23 @@ def eval_host(R, k, r_trial, fn, n_total: int, n_up: int, *, i_offset: int = 0, 
     for t, nm in ((R, "R"), (k, "k"), (r_trial, "r_trial")):
         if t.is_cuda or not t.is_contiguous():
             raise ValueError(f"{nm} must be a contiguous host tensor")
+    if R.dim() != 3 or R.shape[1] != 3:
+        raise ValueError("R must be [W][3][Np]")
     W, _, Np = R.shape
+    if r_trial.dim() != 3 or r_trial.shape[0] != W or r_trial.shape[2] != 3 or r_trial.dtype != R.dtype:
+        raise ValueError("r_trial must be [W][P][3] of R's dtype")
+    if tuple(k.shape) != (W,) or k.dtype != torch.int32:
+        raise ValueError("k must be [W] int32")
     P = r_trial.shape[1]
     n_local = min(Np, n_total - i_offset) if n_local is None else int(n_local)
     if out is None:
         out = torch.empty((W, P, 5), dtype=torch.float64, pin_memory=R.is_pinned())
     if ratio and ratio_out is None:
         ratio_out = torch.empty((W, P, 2), dtype=torch.float64, pin_memory=R.is_pinned())
+    for t, nm, shp in ((out, "out", (W, P, 5)), (ratio_out if ratio else None, "ratio_out", (W, P, 2)),
+                       (V_cur, "V_cur", (W,))):
+        if t is not None and (t.is_cuda or not t.is_contiguous() or t.dtype != torch.float64 or tuple(t.shape) != shp):
+            raise ValueError(f"{nm} must be a contiguous fp64 host tensor of shape {shp}")
     f = Functor.of(fn)
     need = host_workspace_size(W, P, Np, R.dtype, chunk_walkers)
     ws = workspace if workspace is not None else Workspace(device=torch.cuda.current_device())

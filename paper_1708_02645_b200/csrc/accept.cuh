@@ -200,6 +200,7 @@ j2_accept_kernel(const __grid_constant__ AcceptParams p) {
     constexpr int TILE = ATPB * AVPT * AITER * VW;
     const int64_t w = (int64_t)blockIdx.x / p.tiles_per_walker;
     const int64_t tile = (int64_t)blockIdx.x - w * p.tiles_per_walker;
+    QJ2_DCHECK(w < p.W && p.N_local <= p.Np && 2 * (p.m + 1) <= 2 * (QJ2_MAX_M + 1));
     if (p.u) {                                 // fused Metropolis (the same decision in every CTA of w)
         const double rho = exp(p.out_new[w * p.out_stride] - p.v_ref[w * p.v_ref_stride]);
         const bool acc = p.u[w] < rho * rho;
@@ -259,6 +260,7 @@ j2_accept_kernel(const __grid_constant__ AcceptParams p) {
             const int64_t li = t0 + ((int64_t)(it * AVPT + u) * ATPB + threadIdx.x) * VW;
             live[u] = li < nl;
             vi[u] = li / VW;
+            QJ2_DCHECK(!live[u] || (vi[u] + 1) * VW <= p.Np);
             if (live[u]) {
                 bx[u] = AVec<T>::ld(vx + vi[u]);
                 by[u] = AVec<T>::ld(vy + vi[u]);
@@ -297,6 +299,7 @@ j2_accept_kernel(const __grid_constant__ AcceptParams p) {
             for (int c = 0; c < 5; ++c) __stcs(vs[c] + vi[u], bs[u][c]);
             if (has_k) {                                   // commit r'_k into Rsoa
                 const int e = (int)(kl - li0);
+                QJ2_DCHECK(e >= 0 && e < VW);
                 V nx = bx[u], ny = by[u], nz = bz[u];
                 Tr::set(nx, e, rn[0]); Tr::set(ny, e, rn[1]); Tr::set(nz, e, rn[2]);
                 vx[vi[u]] = nx; vy[vi[u]] = ny; vz[vi[u]] = nz;

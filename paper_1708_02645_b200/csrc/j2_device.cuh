@@ -13,9 +13,36 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
+// Debug build (-DQJ2_CHECK; tools/ab/build_check.sh): device-side checks of every
+// index computed from the arguments before it addresses global or shared memory
+// (the substitute for compute-sanitizer, which this pool does not offer).  A failed
+// check prints its location and traps, so the launch fails with a sticky error.
+#ifdef QJ2_CHECK
+#define QJ2_DCHECK(cond)                                                                        \
+    do {                                                                                        \
+        if (!(cond)) {                                                                          \
+            printf("QJ2_CHECK failed at %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__,  \
+                   #cond, (int)blockIdx.x, (int)threadIdx.x);                                   \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define QJ2_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 namespace qj2 {
+
+// Dynamic shared memory of the launch, in bytes (for QJ2_DCHECK of layouts).
+__device__ __forceinline__ uint32_t dyn_smem_bytes() {
+    uint32_t x;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(x));
+    return x;
+}
 
 // ---------------------------------------------------------------------------
 // Type traits

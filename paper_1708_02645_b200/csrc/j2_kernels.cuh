@@ -30,7 +30,6 @@ constexpr int ITERS = QJ2_ITERS;  // vector iterations per sub-tile: 32 fp32 ter
 constexpr int SUB = QJ2_SUB;      // sub-tiles per CTA tile: 25 x 8192 fp32 sources (A/B builds: -DQJ2_SUB=n)
 constexpr int NACC = 6;           // fp32 accumulators per trial: V, Gx, Gy, Gz, sum h, sum du/r
 constexpr int NOUT = 5;           // fp64 physical outputs per trial: V, Gx, Gy, Gz, L
-constexpr int MAXPB = 4;
 constexpr int MAXG = 4;           // source groups (J2: 2 spin halves; J1: up to 4 species)
 constexpr int MAXTAB = MAXG * (QJ2_MAX_M + 1);
 
@@ -47,7 +46,6 @@ template <int MODE> __host__ __device__ constexpr int ndacc() { return MODE == M
 struct EvalParams {
     int64_t W, N_total, N_up, i_offset, N_local, Np;
     int64_t tiles_per_walker;     // ceil(N_local / CH)
-    int64_t n_groups;             // trial groups: ceil(P / PB)
     int32_t P, m;                 // m: J2 interval count
     int32_t mode;                 // MODE_J2 | MODE_J1 (the kernels are also templated on it)
     int32_t n_src_groups;         // J2: 2; J1: species
@@ -64,8 +62,8 @@ struct EvalParams {
     void *row_out;
     const double *V_cur;
     double *ratio_out;
-    double *partials;             // [W][n_groups][tiles][PB][ndacc]
-    unsigned int *counters;       // [W][n_groups]
+    double *partials;             // [W][P][tiles][ndacc]
+    unsigned int *counters;       // [W][P]
     double L[3];
     double inv_delta;             // J2: 1/delta
     float inv_delta_f;            // J2: 1/delta rounded to fp32
@@ -83,6 +81,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 template <typename T>
 __device__ __forceinline__ void load_table(const EvalParams &p, Coef4<T> *tab) {
+    QJ2_DCHECK(p.n_tab <= MAXTAB);
     for (int e = threadIdx.x; e < p.n_tab; e += blockDim.x) {
         Coef4<T> c;
         c.a0 = T(p.pcoef[e][0]);
@@ -164,23 +163,6 @@ __device__ __forceinline__ T accumulate(T dx, T dy, T dz, T r2, T inv_delta, uin
     return r;
 }
 
-// Minimum image for one axis, optionally specialised on the trial
-// coordinate's case (SPEC = 1: case A, c < L/2; 0: case B; -1: unified,
-// see make_axis).  Specialised forms take 3 instructions instead of 4, but the
-// 8 per-walker bodies measured slower on B200 (instruction-cache pressure,
-// DESIGN.md section 7); the kernels use the unified form.
-template <typename T, int SPEC>
-__device__ __forceinline__ T min_image_k(T x, const Axis<T> &a) {
-    if constexpr (SPEC < 0) {
-        return min_image(x, a);
-    } else if constexpr (SPEC == 1) {           // case A: wrap shifts the source (x - L exact)
-        const T xs = x > a.thr ? x - a.a1 : x;
-        return xs - a.b0;
-    } else {                                    // case B: wrap shifts the trial (c - L exact)
-        return x - (x > a.thr ? a.b1 : a.b0);
-    }
-}
-
 // A sub-tile that is not "clean": ragged length, holds the self source k, or
 // straddles a group boundary.  Offsets relative to the sub-tile start.
 struct SubMask {
@@ -202,14 +184,14 @@ struct SubMask {
 // the source's group picks the functor.  J2 groups share delta, so only the
 // table row changes (raw accumulation); J1 groups differ in delta, so GEN
 // sub-tiles accumulate physical units (PHYS).
-template <typename T, int PB, bool ROW, int PF, bool GEN, int NT, int MODE>
+template <typename T, bool ROW, int PF, bool GEN, int NT, int MODE>
 __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, uint32_t tab_addr,
                                          const typename Traits<T>::V *__restrict__ px,
                                          const typename Traits<T>::V *__restrict__ py,
                                          const typename Traits<T>::V *__restrict__ pz,
-                                         const Trial<T> (&tr)[PB], int np, const GroupC<T> &gc,
-                                         const SubMask &mk, T (&acc)[PB][NACC],
-                                         typename Traits<T>::V *const (&rowp)[PB], int64_t row_stride) {
+                                         const Trial<T> &tr, const GroupC<T> &gc,
+                                         const SubMask &mk, T (&acc)[NACC],
+                                         typename Traits<T>::V *rowp, int64_t row_stride) {
     using Tr = Traits<T>;
     using V = typename Tr::V;
     constexpr int VW = Tr::VW;
@@ -233,7 +215,7 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
         }
         const int rel = (it * NT + tid) * VW;
         if (!GEN || rel < mk.len) {
-            V ro[PB][4];
+            V ro[4];
 #pragma unroll
             for (int e = 0; e < VW; ++e) {
                 bool dead = false;
@@ -244,25 +226,17 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
                     if (MODE == MODE_J2) base = li < mk.up_rel ? gc.base : mk.base_hi;   // spin halves
                 }
                 const T x = Tr::comp(bx[it], e), y = Tr::comp(by[it], e), z = Tr::comp(bz[it], e);
-#pragma unroll
-                for (int q = 0; q < PB; ++q) {
-                    if (PB == 1 || q < np) {
-                        const T dx = min_image_k<T, -1>(x, tr[q].ax);
-                        const T dy = min_image_k<T, -1>(y, tr[q].ay);
-                        const T dz = min_image_k<T, -1>(z, tr[q].az);
-                        T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-                        if (GEN) r2 = dead ? T(1e30) : r2;
-                        const T r = accumulate<T>(dx, dy, dz, r2, gc.invd, base, gc.clamp, acc[q]);
-                        if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
-                    }
-                }
+                const T dx = min_image(x, tr.ax);
+                const T dy = min_image(y, tr.ay);
+                const T dz = min_image(z, tr.az);
+                T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                if (GEN) r2 = dead ? T(1e30) : r2;
+                const T r = accumulate<T>(dx, dy, dz, r2, gc.invd, base, gc.clamp, acc);
+                if (ROW) { Tr::set(ro[0], e, r); Tr::set(ro[1], e, dx); Tr::set(ro[2], e, dy); Tr::set(ro[3], e, dz); }
             }
             if (ROW) {
 #pragma unroll
-                for (int q = 0; q < PB; ++q)
-                    if (PB == 1 || q < np)
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) __stcs(rowp[q] + c * row_stride + it * NT, ro[q][c]);
+                for (int c = 0; c < 4; ++c) __stcs(rowp + c * row_stride + it * NT, ro[c]);
             }
         }
     }
@@ -273,14 +247,13 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
 // footprint small.  The species is looked up per source and the terms are
 // accumulated in physical units because species differ in delta.  (J2's spin
 // straddle stays in the pipelined loop: both halves share delta.)
-template <typename T, int PB, bool ROW, int NT, int MODE>
+template <typename T, bool ROW, int NT, int MODE>
 __device__ __forceinline__ void tile_multi(int tid, const EvalParams &p, int kg, uint32_t tab_addr,
                                            const typename Traits<T>::V *__restrict__ px,
                                            const typename Traits<T>::V *__restrict__ py,
                                            const typename Traits<T>::V *__restrict__ pz,
-                                           const Trial<T> (&tr)[PB], int np, const SubMask &mk,
-                                           T (&acc)[PB][NACC],
-                                           typename Traits<T>::V *const (&rowp)[PB], int64_t row_stride) {
+                                           const Trial<T> &tr, const SubMask &mk, T (&acc)[NACC],
+                                           typename Traits<T>::V *rowp, int64_t row_stride) {
     using Tr = Traits<T>;
     using V = typename Tr::V;
     constexpr int VW = Tr::VW;
@@ -289,7 +262,7 @@ __device__ __forceinline__ void tile_multi(int tid, const EvalParams &p, int kg,
         const int rel = (it * NT + tid) * VW;
         if (rel >= mk.len) break;
         const V vx = Tr::ld_stream(px + it * NT), vy = Tr::ld_stream(py + it * NT), vz = Tr::ld_stream(pz + it * NT);
-        V ro[PB][4];
+        V ro[4];
 #pragma unroll
         for (int e = 0; e < VW; ++e) {
             const int li = rel + e;
@@ -297,46 +270,34 @@ __device__ __forceinline__ void tile_multi(int tid, const EvalParams &p, int kg,
             const int gsrc = MODE == MODE_J2 ? (mk.g0 + li >= p.N_up ? 1 : 0) : src_group(p, mk.g0 + li);
             const GroupC<T> ge = group_consts<T, MODE>(p, gsrc, kg, tab_addr);
             const T x = Tr::comp(vx, e), y = Tr::comp(vy, e), z = Tr::comp(vz, e);
-#pragma unroll
-            for (int q = 0; q < PB; ++q) {
-                if (PB == 1 || q < np) {
-                    const T dx = min_image(x, tr[q].ax);
-                    const T dy = min_image(y, tr[q].ay);
-                    const T dz = min_image(z, tr[q].az);
-                    T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-                    r2 = dead ? T(1e30) : r2;
-                    const T r = accumulate<T, MODE == MODE_J1>(dx, dy, dz, r2, ge.invd, ge.base, ge.clamp, acc[q]);
-                    if (ROW) { Tr::set(ro[q][0], e, r); Tr::set(ro[q][1], e, dx); Tr::set(ro[q][2], e, dy); Tr::set(ro[q][3], e, dz); }
-                }
-            }
+            const T dx = min_image(x, tr.ax);
+            const T dy = min_image(y, tr.ay);
+            const T dz = min_image(z, tr.az);
+            T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+            r2 = dead ? T(1e30) : r2;
+            const T r = accumulate<T, MODE == MODE_J1>(dx, dy, dz, r2, ge.invd, ge.base, ge.clamp, acc);
+            if (ROW) { Tr::set(ro[0], e, r); Tr::set(ro[1], e, dx); Tr::set(ro[2], e, dy); Tr::set(ro[3], e, dz); }
         }
         if (ROW) {
 #pragma unroll
-            for (int q = 0; q < PB; ++q)
-                if (PB == 1 || q < np)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) __stcs(rowp[q] + c * row_stride + it * NT, ro[q][c]);
+            for (int c = 0; c < 4; ++c) __stcs(rowp + c * row_stride + it * NT, ro[c]);
         }
     }
 }
 
 // Flush a sub-tile's T partials into the fp64 accumulators: raw for J2,
 // physical (scaled by the sub-tile group's delta factors) for J1.
-template <typename T, int PB, int MODE>
-__device__ __forceinline__ void flush(T (&acc)[PB][NACC], double (&dacc)[PB][ndacc<MODE>()], double sg, double sh,
-                                      double ss) {
+template <typename T, int MODE>
+__device__ __forceinline__ void flush(T (&acc)[NACC], double (&dacc)[ndacc<MODE>()], double sg, double sh, double ss) {
+    if constexpr (MODE == MODE_J2) {
 #pragma unroll
-    for (int q = 0; q < PB; ++q) {
-        if constexpr (MODE == MODE_J2) {
-#pragma unroll
-            for (int a = 0; a < NACC; ++a) dacc[q][a] += (double)acc[q][a];
-        } else {
-            dacc[q][0] += (double)acc[q][0];
-            dacc[q][1] += sg * (double)acc[q][1];
-            dacc[q][2] += sg * (double)acc[q][2];
-            dacc[q][3] += sg * (double)acc[q][3];
-            dacc[q][4] += sh * (double)acc[q][4] + ss * (double)acc[q][5];
-        }
+        for (int a = 0; a < NACC; ++a) dacc[a] += (double)acc[a];
+    } else {
+        dacc[0] += (double)acc[0];
+        dacc[1] += sg * (double)acc[1];
+        dacc[2] += sg * (double)acc[2];
+        dacc[3] += sg * (double)acc[3];
+        dacc[4] += sh * (double)acc[4] + ss * (double)acc[5];
     }
 }
 
@@ -358,19 +319,17 @@ __device__ __forceinline__ void to_physical(const EvalParams &p, const double *s
 
 // Process the sub-tile [sstart, send) (local indices) of one walker for a team
 // of NT threads: classify, run the clean or the masked loop, flush to fp64.
-template <typename T, int PB, bool ROW, int PF, int NT, int MODE>
+template <typename T, bool ROW, int PF, int NT, int MODE>
 __device__ __forceinline__ void sub_tile(int tid, const EvalParams &p, int kg, uint32_t tab_addr,
                                          int64_t sstart, int64_t send, int64_t k_local,
                                          const typename Traits<T>::V *px, const typename Traits<T>::V *py,
-                                         const typename Traits<T>::V *pz, const Trial<T> (&tr)[PB], int np,
-                                         double (&dacc)[PB][ndacc<MODE>()],
-                                         typename Traits<T>::V *const (&rp)[PB], int64_t row_stride) {
+                                         const typename Traits<T>::V *pz, const Trial<T> &tr,
+                                         double (&dacc)[ndacc<MODE>()], typename Traits<T>::V *rp,
+                                         int64_t row_stride) {
     constexpr int SCH = NT * Traits<T>::VW * ITERS;
-    T acc[PB][NACC];
+    T acc[NACC];
 #pragma unroll
-    for (int q = 0; q < PB; ++q)
-#pragma unroll
-        for (int a = 0; a < NACC; ++a) acc[q][a] = T(0);
+    for (int a = 0; a < NACC; ++a) acc[a] = T(0);
     const int64_t g0 = sstart + p.i_offset;                 // global index of the first source
     int grp;
     bool one_group;
@@ -396,30 +355,28 @@ __device__ __forceinline__ void sub_tile(int tid, const EvalParams &p, int kg, u
         }
     }
     if (mk.len == SCH && !k_in && one_group) {                 // clean
-        tile_run<T, PB, ROW, PF, false, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp,
-                                                  row_stride);
-        flush<T, PB, MODE>(acc, dacc, gc.sg, gc.sh, gc.ss);
+        tile_run<T, ROW, PF, false, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, gc, mk, acc, rp, row_stride);
+        flush<T, MODE>(acc, dacc, gc.sg, gc.sh, gc.ss);
     } else if (one_group || MODE == MODE_J2) {                // ragged, holds k, or straddles N_up (J2)
-        tile_run<T, PB, ROW, PF, true, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp,
-                                                 row_stride);
-        flush<T, PB, MODE>(acc, dacc, gc.sg, gc.sh, gc.ss);
+        tile_run<T, ROW, PF, true, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, gc, mk, acc, rp, row_stride);
+        flush<T, MODE>(acc, dacc, gc.sg, gc.sh, gc.ss);
     } else {                                                   // J1: straddles a species boundary
-        tile_multi<T, PB, ROW, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, np, mk, acc, rp, row_stride);
-        if constexpr (MODE == MODE_J2) flush<T, PB, MODE>(acc, dacc, gc.sg, gc.sh, gc.ss);   // shared delta: raw
-        else flush<T, PB, MODE>(acc, dacc, -1.0, 1.0, 2.0);                                  // already physical
+        tile_multi<T, ROW, NT, MODE>(tid, p, kg, tab_addr, px, py, pz, tr, mk, acc, rp, row_stride);
+        if constexpr (MODE == MODE_J2) flush<T, MODE>(acc, dacc, gc.sg, gc.sh, gc.ss);   // shared delta: raw
+        else flush<T, MODE>(acc, dacc, -1.0, 1.0, 2.0);                                  // already physical
     }
 }
 
 // J2 sub-tile with 32-bit classification relative to the walker's tile
 // (tile length tlen, k at k_t or -1, sources [0, up_t) of the tile spin-up)
 // and the two per-walker functor constant sets.  s0: the sub-tile's offset.
-template <typename T, int PB, bool ROW, int PF, int NT>
+template <typename T, bool ROW, int PF, int NT>
 __device__ __forceinline__ void j2_sub_tile32(int tid, const EvalParams &p, int kg, uint32_t tab_addr, int32_t s0,
                                               int32_t tlen, int32_t k_t, int32_t up_t, const GroupC<T> &g_up,
                                               const GroupC<T> &g_dn, const typename Traits<T>::V *px,
                                               const typename Traits<T>::V *py, const typename Traits<T>::V *pz,
-                                              const Trial<T> (&tr)[PB], int np, double (&dacc)[PB][NACC],
-                                              typename Traits<T>::V *const (&rp)[PB], int64_t row_stride) {
+                                              const Trial<T> &tr, double (&dacc)[NACC], typename Traits<T>::V *rp,
+                                              int64_t row_stride) {
     constexpr int SCH = NT * Traits<T>::VW * ITERS;
     const int32_t len = min(SCH, tlen - s0);
     const int32_t k_rel = k_t - s0;
@@ -427,11 +384,9 @@ __device__ __forceinline__ void j2_sub_tile32(int tid, const EvalParams &p, int 
     const int32_t up_rel = up_t - s0;                 // sources [0, up_rel) of the sub-tile are spin-up
     const bool straddle = up_rel > 0 && up_rel < len;
     const GroupC<T> &gc = up_rel > 0 ? g_up : g_dn;   // the group of the sub-tile's first source
-    T acc[PB][NACC];
+    T acc[NACC];
 #pragma unroll
-    for (int q = 0; q < PB; ++q)
-#pragma unroll
-        for (int a = 0; a < NACC; ++a) acc[q][a] = T(0);
+    for (int a = 0; a < NACC; ++a) acc[a] = T(0);
     SubMask mk;
     mk.len = len;
     mk.k_rel = k_in ? k_rel : -1;
@@ -439,55 +394,47 @@ __device__ __forceinline__ void j2_sub_tile32(int tid, const EvalParams &p, int 
     mk.up_rel = straddle ? up_rel : len;
     mk.base_hi = straddle ? g_dn.base : gc.base;
     if (len == SCH && !k_in && !straddle)
-        tile_run<T, PB, ROW, PF, false, NT, MODE_J2>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp,
-                                                     row_stride);
+        tile_run<T, ROW, PF, false, NT, MODE_J2>(tid, p, kg, tab_addr, px, py, pz, tr, gc, mk, acc, rp, row_stride);
     else
-        tile_run<T, PB, ROW, PF, true, NT, MODE_J2>(tid, p, kg, tab_addr, px, py, pz, tr, np, gc, mk, acc, rp,
-                                                    row_stride);
-    flush<T, PB, MODE_J2>(acc, dacc, gc.sg, gc.sh, gc.ss);      // J2: raw sums (one delta for both groups)
+        tile_run<T, ROW, PF, true, NT, MODE_J2>(tid, p, kg, tab_addr, px, py, pz, tr, gc, mk, acc, rp, row_stride);
+    flush<T, MODE_J2>(acc, dacc, gc.sg, gc.sh, gc.ss);      // J2: raw sums (one delta for both groups)
 }
 
 // Per-walker setup shared by the CTA and warp kernels.
-template <typename T, int PB, int MODE>
-__device__ __forceinline__ void walker_setup(const EvalParams &p, int64_t w, int32_t p0, int np,
-                                             Trial<T> (&tr)[PB], int &kg, int64_t &k_local) {
+template <typename T, int MODE>
+__device__ __forceinline__ void walker_setup(const EvalParams &p, int64_t w, int32_t g, Trial<T> &tr, int &kg,
+                                             int64_t &k_local) {
     const int64_t kw = MODE == MODE_J2 ? (int64_t)p.k[w] : -1;
     kg = (MODE == MODE_J2 && kw >= p.N_up) ? 1 : 0;
     k_local = MODE == MODE_J2 ? kw - p.i_offset : -1;
-    const T L0 = T(p.L[0]), L1 = T(p.L[1]), L2 = T(p.L[2]);
-#pragma unroll
-    for (int q = 0; q < PB; ++q) {
-        const int qq = q < np ? q : 0;
-        const T *rt = static_cast<const T *>(p.r_trial) + ((w * p.P + p0 + qq) * 3);
-        tr[q].ax = make_axis<T>(rt[0], L0);
-        tr[q].ay = make_axis<T>(rt[1], L1);
-        tr[q].az = make_axis<T>(rt[2], L2);
-    }
+    const T *rt = static_cast<const T *>(p.r_trial) + ((w * p.P + g) * 3);
+    tr.ax = make_axis<T>(rt[0], T(p.L[0]));
+    tr.ay = make_axis<T>(rt[1], T(p.L[1]));
+    tr.az = make_axis<T>(rt[2], T(p.L[2]));
 }
 
-// Write the physical totals (lane 0 holds them) and the fused ratio.
-template <int PB, int MODE>
-__device__ __forceinline__ void write_out(const EvalParams &p, int64_t w, int32_t p0, int np, int q,
-                                          const double *sraw, double V0) {
-    if (q >= np) return;
+// Write the physical totals of trial g of walker w and the fused ratio (against V_cur,
+// or, for P = 1 without V_cur, against this trial itself: the host launches a separate
+// ratio kernel when P > 1 and V_cur == NULL).
+template <int MODE>
+__device__ __forceinline__ void write_out(const EvalParams &p, int64_t w, int32_t g, const double *sraw) {
     double s[NOUT];
     to_physical<MODE>(p, sraw, s);
-    const int64_t o = w * p.P + p0 + q;
+    const int64_t o = w * p.P + g;
 #pragma unroll
     for (int a = 0; a < NOUT; ++a) p.out[o * 5 + a] = s[a];
     if (p.ratio_out) {   // e^{dJ} factor of Eq. 4 (host guarantees a valid reference)
-        const double dj = s[0] - (p.V_cur ? p.V_cur[w] : V0);
+        const double dj = s[0] - (p.V_cur ? p.V_cur[w] : s[0]);
         p.ratio_out[o * 2 + 0] = dj;
         p.ratio_out[o * 2 + 1] = exp(dj);
     }
 }
 
 // ===========================================================================
-// Long rows: one CTA per (walker, trial group, tile of SUB sub-tiles).
+// Long rows: one CTA per (walker, trial, tile of SUB sub-tiles).
 // PF: prefetch distance (vector groups in flight), MINB: resident CTAs per SM.
 // ===========================================================================
-template <typename T, int PB, bool ROW, int PF = 1, int MINB = ((sizeof(T) == 4 && PB == 1) ? 4 : 2),
-          int MODE = MODE_J2>
+template <typename T, bool ROW, int PF, int MINB, int MODE = MODE_J2>
 __global__ void __launch_bounds__(TPB, MINB)
 j2_eval_kernel(const __grid_constant__ EvalParams p) {
     using Tr = Traits<T>;
@@ -497,51 +444,46 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
     constexpr int CH = SCH * SUB;                 // tile handled by one CTA
     constexpr int ND = ndacc<MODE>();
     __shared__ Coef4<T> tab[MAXTAB];
-    __shared__ double red[TPB / 32][PB * ND];
+    __shared__ double red[TPB / 32][ND];
     __shared__ int last_flag;
 
-    // tile decode: trial group fastest, then tile, then walker, so the CTAs of
-    // one tile's trial groups run together (one HBM read, L2 hits for the
-    // others) and consecutive tiles stream consecutive memory (32-bit
-    // arithmetic: the host guarantees W * n_groups * tiles < 2^31)
+    // tile decode: trial fastest, then tile, then walker, so the CTAs of one tile's
+    // trials run together (one HBM read, L2 hits for the others) and consecutive
+    // tiles stream consecutive memory (32-bit arithmetic: the host guarantees
+    // W * P * tiles < 2^31)
     const uint32_t b = blockIdx.x;
-    const uint32_t ng32 = (uint32_t)p.n_groups;
-    const uint32_t per_w = (uint32_t)p.tiles_per_walker * ng32;
+    const uint32_t P32 = (uint32_t)p.P;
+    const uint32_t per_w = (uint32_t)p.tiles_per_walker * P32;
     const uint32_t w32 = b / per_w;
     const uint32_t rem = b - w32 * per_w;
-    const uint32_t c32 = rem / ng32;
+    const uint32_t c32 = rem / P32;
     const int64_t tpw = p.tiles_per_walker;
-    const int64_t w = w32, c = c32, g = rem - c32 * ng32;
-    const int32_t p0 = (int32_t)g * PB;
-    const int np = min(PB, p.P - p0);
+    const int64_t w = w32, c = c32;
+    const int32_t g = (int32_t)(rem - c32 * P32);
 
     load_table<T>(p, tab);
-    Trial<T> tr[PB];
+    Trial<T> tr;
     int kg;
     int64_t k_local;
-    walker_setup<T, PB, MODE>(p, w, p0, np, tr, kg, k_local);
+    walker_setup<T, MODE>(p, w, g, tr, kg, k_local);
     const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tab);
 
     const int64_t start = c * CH;
     const int64_t end = min(start + (int64_t)CH, p.N_local);
+    // every vector this CTA loads (and row vector it stores) lies in [start, end) of lanes of Np
+    QJ2_DCHECK(w < p.W && g < p.P && c < tpw && start < end && end <= p.Np && p.N_local <= p.Np);
     const T *Rw = static_cast<const T *>(p.R) + w * p.src_stride;
     const int64_t voff = (start >> (VW == 4 ? 2 : 1)) + threadIdx.x;   // this thread's first vector
     const V *px = reinterpret_cast<const V *>(Rw) + voff;
     const V *py = reinterpret_cast<const V *>(Rw + p.Np) + voff;
     const V *pz = reinterpret_cast<const V *>(Rw + 2 * p.Np) + voff;
-    V *rowp[PB];
-#pragma unroll
-    for (int q = 0; q < PB; ++q)
-        rowp[q] = ROW ? reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + p0 + (q < np ? q : 0)) * 4) * p.Np) + voff
-                      : nullptr;
+    V *rowp = ROW ? reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + g) * 4) * p.Np) + voff : nullptr;
     const int64_t row_stride = p.Np / VW;
     __syncthreads();
 
-    double dacc[PB][ND];
+    double dacc[ND];
 #pragma unroll
-    for (int q = 0; q < PB; ++q)
-#pragma unroll
-        for (int a = 0; a < ND; ++a) dacc[q][a] = 0.0;
+    for (int a = 0; a < ND; ++a) dacc[a] = 0.0;
 
     if constexpr (MODE == MODE_J2) {
         // J2: classify sub-tiles with 32-bit offsets relative to the tile, from
@@ -558,49 +500,42 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
             const int32_t s0 = sidx * SCH;
             if (s0 >= tlen) break;
             const int64_t vs = (int64_t)sidx * (SCH / VW);
-            V *rp[PB];
-#pragma unroll
-            for (int q = 0; q < PB; ++q) rp[q] = ROW ? rowp[q] + vs : nullptr;
-            j2_sub_tile32<T, PB, ROW, PF, TPB>(threadIdx.x, p, kg, tab_addr, s0, tlen, k_t, up_t, g_up, g_dn, px + vs,
-                                               py + vs, pz + vs, tr, np, dacc, rp, row_stride);
+            j2_sub_tile32<T, ROW, PF, TPB>(threadIdx.x, p, kg, tab_addr, s0, tlen, k_t, up_t, g_up, g_dn, px + vs,
+                                           py + vs, pz + vs, tr, dacc, ROW ? rowp + vs : nullptr, row_stride);
         }
     } else {
 #pragma unroll 1
-    for (int sidx = 0; sidx < SUB; ++sidx) {
-        const int64_t sstart = start + (int64_t)sidx * SCH;
-        if (sstart >= end) break;
-        const int64_t send = min(sstart + (int64_t)SCH, end);
-        const int64_t vs = (int64_t)sidx * (SCH / VW);
-        V *rp[PB];
-#pragma unroll
-        for (int q = 0; q < PB; ++q) rp[q] = ROW ? rowp[q] + vs : nullptr;
-        sub_tile<T, PB, ROW, PF, TPB, MODE>(threadIdx.x, p, kg, tab_addr, sstart, send, k_local, px + vs, py + vs,
-                                            pz + vs, tr, np, dacc, rp, row_stride);
-    }
+        for (int sidx = 0; sidx < SUB; ++sidx) {
+            const int64_t sstart = start + (int64_t)sidx * SCH;
+            if (sstart >= end) break;
+            const int64_t send = min(sstart + (int64_t)SCH, end);
+            const int64_t vs = (int64_t)sidx * (SCH / VW);
+            sub_tile<T, ROW, PF, TPB, MODE>(threadIdx.x, p, kg, tab_addr, sstart, send, k_local, px + vs, py + vs,
+                                            pz + vs, tr, dacc, ROW ? rowp + vs : nullptr, row_stride);
+        }
     }
 
     // ---- CTA reduction in fp64 (fixed order: deterministic) ----
+    QJ2_DCHECK(tpw == 1 || (p.partials != nullptr && p.counters != nullptr));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int q = 0; q < PB; ++q)
-#pragma unroll
-        for (int a = 0; a < ND; ++a) {
-            const double v = warp_sum(dacc[q][a]);
-            if (lane == 0) red[warp][q * ND + a] = v;
-        }
+    for (int a = 0; a < ND; ++a) {
+        const double v = warp_sum(dacc[a]);
+        if (lane == 0) red[warp][a] = v;
+    }
     __syncthreads();
 
-    double tot = 0.0;   // thread t < PB*ND holds value t of this tile
-    if (threadIdx.x < PB * ND) {
+    double tot = 0.0;   // thread t < ND holds value t of this tile
+    if (threadIdx.x < ND) {
 #pragma unroll
         for (int wi = 0; wi < TPB / 32; ++wi) tot += red[wi][threadIdx.x];
     }
 
-    const int64_t wg = w * p.n_groups + g;
+    const int64_t wg = w * p.P + g;
     if (tpw > 1) {
         // publish this tile's partials; the last CTA of (w, g) reduces them
-        double *part = p.partials + (wg * tpw + c) * (PB * ND);
-        if (threadIdx.x < PB * ND) part[threadIdx.x] = tot;
+        double *part = p.partials + (wg * tpw + c) * ND;
+        if (threadIdx.x < ND) part[threadIdx.x] = tot;
         __threadfence();
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -612,38 +547,33 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
         __threadfence();
         // warp 0: value v summed over tiles, lane-strided then shuffle tree
         if (warp == 0) {
-            const double *base = p.partials + wg * tpw * (PB * ND);
-            for (int v = 0; v < PB * ND; ++v) {
+            const double *base = p.partials + wg * tpw * ND;
+            for (int v = 0; v < ND; ++v) {
                 double s = 0.0;
-                for (int64_t t = lane; t < tpw; t += 32) s += __ldcg(base + t * (PB * ND) + v);
+                for (int64_t t = lane; t < tpw; t += 32) s += __ldcg(base + t * ND + v);
                 s = warp_sum(s);
-                if (lane == v) tot = s;      // lane v keeps value v (PB*ND <= 24 < 32)
+                if (lane == v) tot = s;      // lane v keeps value v (ND <= 6 < 32)
             }
         }
     }
 
-    // ---- finalize: lane t < PB*ND of warp 0 holds value (q = t / ND, a = t % ND) ----
+    // ---- finalize: lane a < ND of warp 0 holds value a ----
     if (warp == 0) {
-        const double V0 = __shfl_sync(0xffffffffu, tot, 0);   // V of this group's first trial
+        double s[ND];
 #pragma unroll
-        for (int q = 0; q < PB; ++q) {
-            double s[ND];
-#pragma unroll
-            for (int a = 0; a < ND; ++a) s[a] = __shfl_sync(0xffffffffu, tot, q * ND + a);
-            if (lane == 0) write_out<PB, MODE>(p, w, p0, np, q, s, V0);
-        }
+        for (int a = 0; a < ND; ++a) s[a] = __shfl_sync(0xffffffffu, tot, a);
+        if (lane == 0) write_out<MODE>(p, w, g, s);
     }
 }
 
 // ===========================================================================
 // Short rows with many walkers (C1, C2, C4 waves): one warp per (walker,
-// trial group) walks all of the walker's sources in per-warp sub-tiles of
+// trial) walks all of the walker's sources in per-warp sub-tiles of
 // 32*VW*ITERS sources; the warp's fp64 shuffle tree is the whole
 // (deterministic) reduction: no shared-memory reduction, no cross-CTA
 // partials, no counters.
 // ===========================================================================
-template <typename T, int PB, bool ROW, int PF, int MINB = (sizeof(T) == 4 && PB == 1 && !ROW) ? 3 : 2,
-          int MODE = MODE_J2>
+template <typename T, bool ROW, int PF, int MINB, int MODE = MODE_J2>
 __global__ void __launch_bounds__(TPB, MINB)
 j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
     using Tr = Traits<T>;
@@ -657,23 +587,21 @@ j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t unit = (int64_t)blockIdx.x * (TPB / 32) + warp;
     if (unit >= n_units) return;
-    const int64_t w = unit / p.n_groups, g = unit - w * p.n_groups;
-    const int32_t p0 = (int32_t)g * PB;
-    const int np = min(PB, p.P - p0);
-    Trial<T> tr[PB];
+    const int64_t w = unit / p.P;
+    const int32_t g = (int32_t)(unit - w * p.P);
+    QJ2_DCHECK(w < p.W && p.N_local <= p.Np && p.tiles_per_walker == 1);
+    Trial<T> tr;
     int kg;
     int64_t k_local;
-    walker_setup<T, PB, MODE>(p, w, p0, np, tr, kg, k_local);
+    walker_setup<T, MODE>(p, w, g, tr, kg, k_local);
     const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tab);
     const T *Rw = static_cast<const T *>(p.R) + w * p.src_stride;
     const int64_t row_stride = p.Np / VW;
 
     constexpr int ND = ndacc<MODE>();
-    double dacc[PB][ND];
+    double dacc[ND];
 #pragma unroll
-    for (int q = 0; q < PB; ++q)
-#pragma unroll
-        for (int a = 0; a < ND; ++a) dacc[q][a] = 0.0;
+    for (int a = 0; a < ND; ++a) dacc[a] = 0.0;
 
     // J2: per-walker 32-bit classification state (the slice is one tile)
     const int32_t tlen = (int32_t)p.N_local;
@@ -691,28 +619,19 @@ j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
         const V *px = reinterpret_cast<const V *>(Rw) + voff;
         const V *py = reinterpret_cast<const V *>(Rw + p.Np) + voff;
         const V *pz = reinterpret_cast<const V *>(Rw + 2 * p.Np) + voff;
-        V *rp[PB];
-#pragma unroll
-        for (int q = 0; q < PB; ++q)
-            rp[q] = ROW ? reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + p0 + (q < np ? q : 0)) * 4) * p.Np) + voff
-                        : nullptr;
+        V *rp = ROW ? reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + g) * 4) * p.Np) + voff : nullptr;
         if constexpr (MODE == MODE_J2)
-            j2_sub_tile32<T, PB, ROW, PF, 32>(lane, p, kg, tab_addr, (int32_t)sstart, tlen, k_t, up_t, g_up, g_dn, px,
-                                              py, pz, tr, np, dacc, rp, row_stride);
+            j2_sub_tile32<T, ROW, PF, 32>(lane, p, kg, tab_addr, (int32_t)sstart, tlen, k_t, up_t, g_up, g_dn, px,
+                                          py, pz, tr, dacc, rp, row_stride);
         else
-            sub_tile<T, PB, ROW, PF, 32, MODE>(lane, p, kg, tab_addr, sstart, send, k_local, px, py, pz, tr, np, dacc,
-                                               rp, row_stride);
+            sub_tile<T, ROW, PF, 32, MODE>(lane, p, kg, tab_addr, sstart, send, k_local, px, py, pz, tr, dacc, rp,
+                                           row_stride);
     }
 
-    double V0 = 0.0;
+    double s[ND];
 #pragma unroll
-    for (int q = 0; q < PB; ++q) {
-        double s[ND];
-#pragma unroll
-        for (int a = 0; a < ND; ++a) s[a] = warp_sum(dacc[q][a]);
-        if (q == 0) V0 = s[0];
-        if (lane == 0) write_out<PB, MODE>(p, w, p0, np, q, s, V0);
-    }
+    for (int a = 0; a < ND; ++a) s[a] = warp_sum(dacc[a]);
+    if (lane == 0) write_out<MODE>(p, w, g, s);
 }
 
 
@@ -734,6 +653,7 @@ __global__ void __launch_bounds__(TPB) j1_thread_kernel(const __grid_constant__ 
     __shared__ Coef4<T> tab[MAXTAB];
     extern __shared__ __align__(16) unsigned char j1_smem[];
     T *ion = reinterpret_cast<T *>(j1_smem);          // [n][4]: x, y, z, 0
+    QJ2_DCHECK(p.N_local * 4 * (int64_t)sizeof(T) <= dyn_smem_bytes() && p.N_local <= p.Np && p.n_tab <= MAXTAB);
     load_table<T>(p, tab);
     const T *src = static_cast<const T *>(p.R);
     for (int64_t i = threadIdx.x; i < p.N_local; i += blockDim.x) {

@@ -191,28 +191,24 @@ void power_basis(const double *c, int m, double (*pc)[4]) {
 
 inline int vw_of(qj2_dtype d) { return d == QJ2_FP32 ? 4 : 2; }
 inline int64_t ch_of(qj2_dtype d) { return (int64_t)TPB * vw_of(d) * ITERS * SUB; }
-// Trials per CTA (or warp): always 1.  The P trials of a walker's tile run on
-// P consecutive CTAs, so the tile is read from HBM once and from L2 by the
-// other P - 1 (measured on B200 against 2 and 4 trials per thread, which
-// need 124-127 registers and run at 2 CTAs/SM: P = 2 1.84 vs 2.79 ms,
-// P = 12 10.3 vs 20.8 ms on C3).
-inline int pb_of(int32_t) { return 1; }
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// One trial per CTA (or warp): the P trials of a walker's tile run on P consecutive
+// CTAs, so the tile is read from HBM once and from L2 by the other P - 1 (measured on
+// B200 against 2 and 4 trials per thread, which need 124-127 registers and run at 2
+// CTAs/SM: P = 2 1.84 vs 2.79 ms, P = 12 10.3 vs 20.8 ms on C3).
 void ws_layout(int64_t W, int32_t P, int64_t N_local, qj2_dtype dtype,
                size_t *part_bytes, size_t *cnt_bytes) {
     const int64_t tpw = (N_local + ch_of(dtype) - 1) / ch_of(dtype);
-    const int pb = pb_of(P);
-    const int64_t ng = (P + pb - 1) / pb;
-    *part_bytes = tpw > 1 ? align256((size_t)W * ng * tpw * pb * NACC * sizeof(double)) : 0;
-    *cnt_bytes = tpw > 1 ? align256((size_t)W * ng * sizeof(unsigned)) : 0;
+    *part_bytes = tpw > 1 ? align256((size_t)W * P * tpw * NACC * sizeof(double)) : 0;
+    *cnt_bytes = tpw > 1 ? align256((size_t)W * P * sizeof(unsigned)) : 0;
 }
 
 // Kernel launches live in launch_*.cu (one translation unit per dtype / trial
 // batch, compiled in parallel); see launch.cuh.
 // Shared tail of qj2_eval / qj2_eval_j1: workspace, counters, dispatch.
-qj2_status launch_common(EvalParams &p, qj2_dtype dtype, int pb, int64_t ng, void *workspace,
-                         size_t workspace_bytes, cudaStream_t stream, bool check_dev) {
+qj2_status launch_common(EvalParams &p, qj2_dtype dtype, void *workspace, size_t workspace_bytes,
+                         cudaStream_t stream, bool check_dev) {
     if (((uintptr_t)p.R & 15) || (p.row_out && ((uintptr_t)p.row_out & 15)))
         return fail(QJ2_EINVAL, "source positions and row_out must be 16-byte aligned");
     size_t part_b, cnt_b;
@@ -220,37 +216,36 @@ qj2_status launch_common(EvalParams &p, qj2_dtype dtype, int pb, int64_t ng, voi
     if (part_b + cnt_b > 0 && (!workspace || workspace_bytes < part_b + cnt_b))
         return fail(QJ2_EINVAL, "workspace too small: need %zu bytes", part_b + cnt_b);
     const int64_t tpw = (p.N_local + ch_of(dtype) - 1) / ch_of(dtype);
-    const int64_t nblocks = p.W * ng * tpw;
+    const int64_t nblocks = p.W * p.P * tpw;
     if (nblocks > 0x7fffffffLL) return fail(QJ2_EINVAL, "problem too large for one launch (%lld CTAs)", (long long)nblocks);
     if (check_dev) { qj2_status st = check_device(); if (st) return st; }
     p.tiles_per_walker = tpw;
-    p.n_groups = ng;
     p.partials = part_b ? static_cast<double *>(workspace) : nullptr;
     p.counters = cnt_b ? reinterpret_cast<unsigned *>(static_cast<char *>(workspace) + part_b) : nullptr;
     const bool row = p.row_out != nullptr;
     cudaError_t e;
     if (cnt_b) {   // completion counters start at zero every call (no caller-side init needed)
-        e = cudaMemsetAsync(p.counters, 0, (size_t)p.W * ng * sizeof(unsigned), stream);
+        e = cudaMemsetAsync(p.counters, 0, (size_t)p.W * p.P * sizeof(unsigned), stream);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counters)");
     }
     const bool j1 = p.mode == MODE_J1;
     if (dtype == QJ2_FP32) {
-        e = j1 ? launch_f32_pb1_j1(p, pb, nblocks, row, stream) : launch_f32_pb1_j2(p, pb, nblocks, row, stream);
+        e = j1 ? launch_f32_j1(p, nblocks, row, stream) : launch_f32_j2(p, nblocks, row, stream);
     } else {
-        e = j1 ? launch_f64_pb1_j1(p, pb, nblocks, row, stream) : launch_f64_pb1_j2(p, pb, nblocks, row, stream);
+        e = j1 ? launch_f64_j1(p, nblocks, row, stream) : launch_f64_j2(p, nblocks, row, stream);
     }
     if (e != cudaSuccess) return cuda_fail(e, "j2_eval_kernel launch");
     return QJ2_OK;
 }
 
-// The fused ratio relative to trial 0 (V_cur == NULL) needs trial 0 in the
-// same trial group; otherwise the ratio is a second (tiny) launch.
-qj2_status launch_with_ratio(EvalParams &p, qj2_dtype dtype, int pb, int64_t ng, void *workspace,
-                             size_t workspace_bytes, cudaStream_t stream, bool check_dev) {
+// The fused ratio relative to trial 0 (V_cur == NULL) needs trial 0 in the same
+// CTA; for P > 1 it is a second (tiny) launch after the reduction.
+qj2_status launch_with_ratio(EvalParams &p, qj2_dtype dtype, void *workspace, size_t workspace_bytes,
+                             cudaStream_t stream, bool check_dev) {
     double *ratio_out = p.ratio_out;
-    const bool after = ratio_out && !p.V_cur && ng > 1;
+    const bool after = ratio_out && !p.V_cur && p.P > 1;
     if (after) p.ratio_out = nullptr;
-    qj2_status st = launch_common(p, dtype, pb, ng, workspace, workspace_bytes, stream, check_dev);
+    qj2_status st = launch_common(p, dtype, workspace, workspace_bytes, stream, check_dev);
     if (st || !after) return st;
     const int64_t n = p.W * p.P;
     ratio_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(p.W, p.P, p.out, nullptr, ratio_out);
@@ -275,8 +270,6 @@ qj2_status eval_impl(const qj2_functor *fn, qj2_dtype dtype,
     if (Np < N_local || Np % vw_of(dtype) != 0)
         return fail(QJ2_EINVAL, "Np must be >= N_local and a multiple of %d", vw_of(dtype));
     if (P < 1 || P > QJ2_MAX_P) return fail(QJ2_EINVAL, "P must be in [1, %d]", QJ2_MAX_P);
-    const int pb = pb_of(P);
-    const int64_t ng = (P + pb - 1) / pb;
     if (ratio_out) {
         if (i_offset != 0 || N_local != N_total)
             return fail(QJ2_EINVAL, "ratio_out needs an unsharded call; use qj2_ratio after reducing");
@@ -301,7 +294,7 @@ qj2_status eval_impl(const qj2_functor *fn, qj2_dtype dtype,
     power_basis(fn->coef[0], fn->m, p.pcoef);                  // rows [0, m]: same spin
     power_basis(fn->coef[1], fn->m, p.pcoef + (fn->m + 1));    // rows [m+1, 2m+1]: opposite spin
     p.n_tab = 2 * (fn->m + 1);
-    return launch_with_ratio(p, dtype, pb, ng, workspace, workspace_bytes, stream, check_dev);
+    return launch_with_ratio(p, dtype, workspace, workspace_bytes, stream, check_dev);
 }
 
 qj2_status validate_j1_functor(const qj2_j1_functor *fn) {
@@ -341,8 +334,6 @@ qj2_status eval_j1_impl(const qj2_j1_functor *fn, qj2_dtype dtype, int64_t W, co
     if (Np < n_ions || Np % vw_of(dtype) != 0)
         return fail(QJ2_EINVAL, "Np must be >= n_ions and a multiple of %d", vw_of(dtype));
     if (P < 1 || P > QJ2_MAX_P) return fail(QJ2_EINVAL, "P must be in [1, %d]", QJ2_MAX_P);
-    const int pb = pb_of(P);
-    const int64_t ng = (P + pb - 1) / pb;
     if (W == 0) return QJ2_OK;
     if (!ions || !r_trial || !out) return fail(QJ2_EINVAL, "ions, r_trial and out must be non-NULL");
 
@@ -366,7 +357,7 @@ qj2_status eval_j1_impl(const qj2_j1_functor *fn, qj2_dtype dtype, int64_t W, co
     p.R = ions; p.k = nullptr; p.r_trial = r_trial; p.out = out; p.row_out = row_out;
     p.V_cur = V_cur; p.ratio_out = ratio_out;
     for (int d = 0; d < 3; ++d) p.L[d] = fn->L[d];
-    return launch_with_ratio(p, dtype, pb, ng, workspace, workspace_bytes, stream, true);
+    return launch_with_ratio(p, dtype, workspace, workspace_bytes, stream, true);
 }
 
 }  // namespace
@@ -732,7 +723,10 @@ qj2_status qj2_spo_eval(const qj2_spo_table *tab, int32_t what, qj2_dtype pos_dt
                         int64_t points_per_walker, double *out, float *spo_out, void *stream) {
     if (!tab) return fail(QJ2_EINVAL, "tab is NULL");
     if (points_per_walker < 1) return fail(QJ2_EINVAL, "points_per_walker must be >= 1");
-    if (what != QJ2_SPO_V && what != QJ2_SPO_VGH) return fail(QJ2_EINVAL, "what must be QJ2_SPO_V or QJ2_SPO_VGH");
+    const bool force_gather = (what & QJ2_SPO_GATHER) != 0;
+    what &= ~QJ2_SPO_GATHER;
+    if (what != QJ2_SPO_V && what != QJ2_SPO_VGH)
+        return fail(QJ2_EINVAL, "what must be QJ2_SPO_V or QJ2_SPO_VGH (optionally | QJ2_SPO_GATHER)");
     if (pos_dtype != QJ2_FP32 && pos_dtype != QJ2_FP64) return fail(QJ2_EINVAL, "bad pos_dtype");
     for (int d = 0; d < 3; ++d)
         if (!(tab->L[d] > 0) || !std::isfinite(tab->L[d])) return fail(QJ2_EINVAL, "L[%d] must be finite and > 0", d);
@@ -763,7 +757,7 @@ qj2_status qj2_spo_eval(const qj2_spo_table *tab, int32_t what, qj2_dtype pos_dt
     const int64_t lanes = ((p.nvec + 31) / 32) * 32;
     p.tpw = (int32_t)(lanes < 256 ? lanes : 256);
     p.wpc = 256 / p.tpw;
-    cudaError_t e = launch_spo(p, vgh, static_cast<cudaStream_t>(stream));
+    cudaError_t e = launch_spo(p, vgh, force_gather, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? QJ2_OK : cuda_fail(e, "spo_kernel launch");
 }
 

@@ -2,8 +2,10 @@
 #include "spo.cuh"
 
 #include <algorithm>
-#include <cstdlib>
-#include <cstring>
+
+#ifndef QJ2_SPO_RING_KB
+#define QJ2_SPO_RING_KB 110
+#endif
 
 namespace qj2 {
 
@@ -15,8 +17,8 @@ static cudaError_t launch_tma(const SpoParams &p, int nc, cudaStream_t s, bool *
     const size_t fixed = 2 * SPO_MAXC * 5 * sizeof(double) + 4 * 8 + 128;
     // ring budget per CTA: 110 KB = 2 CTAs/SM (4 plane stages each at 384 orbitals); measured on
     // B200 (S1 vgh): 220 KB / 1 CTA 1.77 ms, 110 KB 1.02 ms, 75 KB / 3 CTAs 1.05, 55 KB / 4 CTAs 1.19
-    const char *bk = getenv("QJ2_SPO_SMEM_KB");           // A/B override
-    const size_t budget = (size_t)(bk ? atoi(bk) : 110) * 1024;
+    // (A/B builds: -DQJ2_SPO_RING_KB=n)
+    const size_t budget = (size_t)QJ2_SPO_RING_KB * 1024;
     int nst = (int)std::min<size_t>(16, (budget - fixed) / per_stage);
     if (nst < 2) return cudaSuccess;                 // rows too long for a 2-stage ring: LDG kernel
     const size_t smem = (size_t)nst * per_stage + fixed;
@@ -35,9 +37,7 @@ static cudaError_t launch_tma(const SpoParams &p, int nc, cudaStream_t s, bool *
     return cudaGetLastError();
 }
 
-cudaError_t launch_spo(const SpoParams &p, bool vgh, cudaStream_t s) {
-    const char *env = getenv("QJ2_SPO");                    // A/B: "ldg" forces the LDG kernel
-    const bool force_ldg = env && strcmp(env, "ldg") == 0;
+cudaError_t launch_spo(const SpoParams &p, bool vgh, bool force_ldg, cudaStream_t s) {
     const int64_t nc = (p.ld / (vgh ? spo_tma_nv<true>() : spo_tma_nv<false>()) + 31) / 32;
     if (!force_ldg && nc <= SPO_MAXC) {
         bool done = false;

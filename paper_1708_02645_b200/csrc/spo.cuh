@@ -15,6 +15,7 @@
 #pragma once
 
 #include "qmcj2.h"
+#include "j2_device.cuh"
 #include "bulk.cuh"
 #include <cstdint>
 
@@ -62,16 +63,20 @@ struct AxisW {
 };
 
 __device__ __forceinline__ void axis_weights(double x, double L, int64_t n, int32_t stride, AxisW &a) {
-    double xw = fmod(x, L);
+    // a non-finite coordinate gathers row 0 with NaN weights (NaN outputs, no stray address)
+    const bool fin = isfinite(x);
+    double xw = fin ? fmod(x, L) : 0.0;
     if (xw < 0) xw += L;
     const double u = xw / L * (double)n;
     double fi = floor(u);
-    const double t = u - fi;
+    const double t = fin ? u - fi : __longlong_as_double(0x7ff8000000000000ll);
     int64_t i = (int64_t)fi;
     if (i >= n) i -= n;
+    i = (i < 0 || i >= n) ? 0 : i;
     for (int c = 0; c < 4; ++c) {
         int64_t j = i - 1 + c;
         j = j < 0 ? j + n : (j >= n ? j - n : j);
+        QJ2_DCHECK(j >= 0 && j < n);
         a.off[c] = (int32_t)j * stride;
     }
     const double g = 1.0 - t, s = (double)n / L;
@@ -503,6 +508,6 @@ __global__ void spo_tma_kernel(const __grid_constant__ SpoParams p, int nst) {
     if (t == 0 && it > 0 && p.out && p.Ainv) spo_finalize<VGH, NR>(p, red, rbar, NC, it - 1, w_prev);
 }
 
-cudaError_t launch_spo(const SpoParams &p, bool vgh, cudaStream_t s);
+cudaError_t launch_spo(const SpoParams &p, bool vgh, bool force_ldg, cudaStream_t s);
 
 }  // namespace qj2

@@ -113,6 +113,9 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
     __shared__ double red2[2][NW][NV];               // double-buffered by move parity
     __shared__ float vk2[2];                         // U^2_k(R) published by the owner of slot k
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    QJ2_DCHECK(w < p.W && N <= p.Np && N == p.N && p.n_ions <= SW_MAX_IONS && p.S <= 0x7fffffff &&
+               (uint32_t)((8 * N) * sizeof(float) + (2 * (p.m + 1) + (J1 ? p.n_rows1 : 0)) * sizeof(Coef4<float>) +
+                          (J1 ? p.n_ions * (sizeof(float4) + sizeof(uint2)) : 0)) <= dyn_smem_bytes());
     stage_tables<J1>(p, tab, tab1, ion_p, ion_c, tid, TPB);
     const float *Rg = p.R + (int64_t)w * 3 * p.Np;
     const float *Sg = p.state + (int64_t)w * 5 * p.Np;
@@ -148,6 +151,7 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
         // k outside [0, N) (a precondition): the move is never accepted and flagged -1
         const bool k_ok = (unsigned)k < (unsigned)N;
         const int kk = k_ok ? k : 0;
+        QJ2_DCHECK(kk >= 0 && kk < N && jm < SW_MCH);
         // r_k was written by its owner in the previous move (the same electron moved
         // twice in a row): make the write visible before everyone reads it
         if (kk == prev_k && prev_acc) __syncthreads();
@@ -307,6 +311,7 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
                 pair_raw(pi.x, pi.y, pi.z, a0, inb && i != kk, dn ? bd : bu, clamp, invd, t0);
                 // the self slot adds T - T = 0 (both terms masked) and is then overwritten by its owner
                 if (inb) {
+                    QJ2_DCHECK(i < N);
                     float4 si = S4[i];
                     si.x += t1[j][0] - t0[0];
                     si.y = fmaf(t1[j][1] - t0[1], invd, si.y);
@@ -368,6 +373,9 @@ template <bool J1>
 __global__ void __launch_bounds__(SI_TPB) state_init_kernel(const __grid_constant__ SweepParams p) {
     extern __shared__ __align__(16) float si_smem[];
     const int w = blockIdx.x, N = p.N, tid = threadIdx.x;
+    QJ2_DCHECK(w < p.W && N <= p.Np && p.n_ions <= SW_MAX_IONS &&
+               (uint32_t)(((3 * N + 3) & ~3) * sizeof(float) + (2 * (p.m + 1) + (J1 ? p.n_rows1 : 0)) *
+                          sizeof(Coef4<float>) + (J1 ? p.n_ions * (sizeof(float4) + sizeof(uint2)) : 0)) <= dyn_smem_bytes());
     float *rx = si_smem, *ry = rx + N, *rz = ry + N;
     const int N4 = (3 * N + 3) & ~3;
     Coef4<float> *tab = reinterpret_cast<Coef4<float> *>(si_smem + N4);

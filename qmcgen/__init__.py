@@ -240,7 +240,8 @@ def make_sweep(seed: int, W: int, N: int, L: float, dtype, steps: int):
     return ks, np.ascontiguousarray(trials), u
 
 
-def make_sweep_moves(seed: int, W: int, N: int, steps: int, order: str = "ordered", sigma: float = 0.1):
+def make_sweep_moves(seed: int, W: int, N: int, steps: int, order: str = "ordered", sigma: float = 0.1,
+                     stream: int = 0):
     """Inputs of qj2_sweep (harness draws, no method arithmetic): for move s <
     steps of walker w, the electron ks[s][w] and the proposal displacement
     delta[s][w] ~ N(0, sigma^2 I) (reading R13: sigma^2 = 0.01), fp32; u[s][w]
@@ -249,8 +250,10 @@ def make_sweep_moves(seed: int, W: int, N: int, steps: int, order: str = "ordere
     and any k sequence is valid.
     order="ordered": k = (k0_w + s) mod N (particle-by-particle sweeps, Alg. 1
     L4; steps = n*N is n full sweeps); order="random": k ~ U{0..N-1}
-    independently per move (repeats included)."""
-    rng = np.random.default_rng([int(seed), 9])
+    independently per move (repeats included).  stream selects an independent
+    draw of the same shape (consecutive sweeps of a Markov chain); an ordered
+    sweep's k sequence is the same for every stream."""
+    rng = np.random.default_rng([int(seed), 9, int(stream)])
     if order == "ordered":
         k0 = make_k(seed, W, N).astype(np.int64)
         s = np.arange(steps, dtype=np.int64)[:, None]
@@ -453,6 +456,8 @@ CONFIGS = {
     "C2": Config("C2", N=1400, W=1024, dtype="f32", seed=1),
     "C2f64": Config("C2f64", N=1400, W=1024, dtype="f64", seed=1),
     "C3": Config("C3", N=614400, W=1024, dtype="f32", seed=2),
+    # C3's instance in fp64 (15.1 GB of positions): the fp64 path at the HBM roofline
+    "C3f64": Config("C3f64", N=614400, W=1024, dtype="f64", seed=2),
     "C4": Config("C4", N=6144, W=1024, dtype="f32", seed=3, instances=4096),
     "C5": Config("C5", N=4915200, W=1024, dtype="f32", seed=5),
     # the paper's own NiO-64 size (Table 1: N = 768) and population (1024 walkers): one full

@@ -129,14 +129,11 @@ def test_j1_thread_kernel_nlpp_and_ratio(q):
 
 
 def test_j1_thread_and_warp_kernels_agree(q):
-    import os
+    """The thread-per-trial kernel (small ion sets) and the shared warp kernel (taken
+    with row output, or for > 4096 ions) agree."""
     ions, start, rt, fn1 = j1_case(64, 5000, seed=41, dtype=np.float32)
     a = q.eval_j1(dev(ions), start, dev(rt), fn1).cpu().numpy()
-    os.environ["QJ2_J1_WARP"] = "1"
-    try:
-        b = q.eval_j1(dev(ions), start, dev(rt), fn1).cpu().numpy()
-    finally:
-        os.environ.pop("QJ2_J1_WARP", None)
+    b = q.eval_j1(dev(ions), start, dev(rt), fn1, row=True)[0].cpu().numpy()
     orc, absout = oracle.eval_j1(ions.astype(np.float64), start, rt[:50].astype(np.float64), fn1)
     assert oracle.normalized_error_j1(a[:50], orc, absout, fn1).max() <= 1e-5
     assert oracle.normalized_error_j1(b[:50], orc, absout, fn1).max() <= 1e-5

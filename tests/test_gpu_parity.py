@@ -332,28 +332,115 @@ def test_C4_instances_every_walker(q):
         assert oracle.normalized_error(out, orc, absout, fn).max() <= TOL[np.float32], inst
 
 
-def test_C5_sliced_single_gpu_sampled(q):
-    """C5 (N = 4,915,200) as 8 source slices evaluated in turn on one GPU with
-    i_offset (exactly the per-rank kernel calls), partials summed on the host."""
+@pytest.fixture(scope="module")
+def c5_reference():
+    """The oracle's C5 values for every 8th walker (and the last): the unsplit
+    source sum over all N = 4,915,200 electrons (~1.6 s of oracle time; 7.6 GB of
+    host positions from the oracle's own generator)."""
     cfg = qmcgen.CONFIGS["C5"]
-    G = 8
     k = qmcgen.make_k(cfg.seed, cfg.W, cfg.N)
     rt = qmcgen.make_trials(cfg.seed, np.arange(cfg.W), k, cfg.N, cfg.L, cfg.np_dtype)
     fn = qmcgen.make_functor(cfg.seed, cfg.L, cfg.m)
-    tot = np.zeros((cfg.W, 1, 5))
-    kd, td = dev(k), dev(rt)
-    for g in range(G):
-        a, b = cfg.N * g // G, cfg.N * (g + 1) // G
-        R = q.gen_positions(cfg.seed, cfg.W, b - a, b - a, cfg.L, torch.float32, i_offset=a)
-        tot += q.eval(R, kd, td, fn, cfg.N, cfg.n_up, i_offset=a, n_local=b - a).cpu().numpy()
-        del R
-    torch.cuda.empty_cache()
-    ws = np.r_[0:1024:8, 1023]                                          # 129 walkers, 59 MB of positions each
+    ws = np.r_[0:cfg.W:8, cfg.W - 1]
     Rh = np.concatenate([oracle.gen_positions(cfg.seed, int(w), 1, cfg.N, cfg.Np, cfg.L, np.float32, threads=THREADS)
                          for w in ws])
     orc, absout, _ = oracle.eval_j2(Rh, k[ws], rt[ws], fn, cfg.N, cfg.n_up, threads=THREADS)
-    assert np.all(np.isfinite(tot))
-    assert oracle.normalized_error(tot[ws], orc, absout, fn).max() <= TOL[np.float32]
+    # one rank's slice checked on its own as well: the oracle's partial sum over [a, b)
+    a, b = cfg.N // 4, cfg.N // 2
+    sub = ws[:17]
+    po, pa, _ = oracle.eval_j2(Rh[:17, :, a:b], k[sub], rt[sub], fn, cfg.N, cfg.n_up, i_offset=a, n_local=b - a,
+                               threads=THREADS)
+    del Rh
+    return dict(k=k, rt=rt, fn=fn, ws=ws, orc=orc, absout=absout, slice=(a, b, sub, po, pa))
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_C5_rank_slices_as_benched(q, c5_reference, G):
+    """C5 (N = 4,915,200, W = 1024) split along the electron axis into G slices,
+    each evaluated exactly as the rank of a G-GPU run calls it (qj2_eval with
+    i_offset over a device-generated slice; G = 1 is one 60 GB launch with 24
+    tiles per walker and 5e9 > 2^31 elements), partials summed on the host (the
+    all-reduce); every 8th walker and the last vs the unsplit oracle sum, and the
+    slice [N/4, N/2) of the G = 4 split vs the oracle's own partial sum."""
+    cfg = qmcgen.CONFIGS["C5"]
+    ref = c5_reference
+    fn = ref["fn"]
+    kd, td = dev(ref["k"]), dev(ref["rt"])
+    tot = np.zeros((cfg.W, 1, 5))
+    ws = q.Workspace()
+    for g in range(G):
+        a, b = cfg.N * g // G, cfg.N * (g + 1) // G
+        Np = qmcgen.padded_size(b - a, 32)
+        R = q.gen_positions(cfg.seed, cfg.W, b - a, Np, cfg.L, torch.float32, i_offset=a)
+        part = q.eval(R, kd, td, fn, cfg.N, cfg.n_up, i_offset=a, n_local=b - a, workspace=ws).cpu().numpy()
+        del R
+        assert np.all(np.isfinite(part))
+        tot += part
+        sa, sb, sub, po, pa = ref["slice"]
+        if (a, b) == (sa, sb):
+            assert oracle.normalized_error(part[sub], po, pa, fn).max() <= TOL[np.float32]
+    torch.cuda.empty_cache()
+    err = oracle.normalized_error(tot[ref["ws"]], ref["orc"], ref["absout"], fn)
+    assert err.max() <= TOL[np.float32], err.max()
+
+
+def _c4_wave(q, cfg, first, count, fn):
+    """One C4 wave as bench.py launches it: `count` instances (1024 walkers each)
+    concatenated into ONE qj2_eval (warp-per-walker kernel); returns out, k, rt."""
+    W = cfg.W
+    R = torch.empty((count * W, 3, cfg.Np), dtype=torch.float32, device="cuda")
+    ks, rts = [], []
+    for j in range(count):
+        seed = cfg.seed + first + j
+        q.gen_positions(seed, W, cfg.N, cfg.Np, cfg.L, torch.float32, out=R[j * W:(j + 1) * W])
+        k = qmcgen.make_k(seed, W, cfg.N)
+        ks.append(k)
+        rts.append(qmcgen.make_trials(seed, np.arange(W), k, cfg.N, cfg.L, np.float32))
+    k, rt = np.concatenate(ks), np.concatenate(rts)
+    out = q.eval(R, dev(k), dev(rt), fn, cfg.N, cfg.n_up).cpu().numpy()
+    del R
+    torch.cuda.empty_cache()
+    return out, k, rt
+
+
+def test_C4_full_wave_as_benched(q):
+    """One full C4 wave exactly as benched: 1024 instances = 1,048,576 walkers
+    (77 GB, 6.4e9 > 2^31 elements) in one qj2_eval; three walkers (first, last,
+    a middle one) of each of 65 instances spread over the wave (every 16th and
+    the last) vs the oracle."""
+    cfg = qmcgen.CONFIGS["C4"]
+    fn = qmcgen.make_functor(cfg.seed, cfg.L, cfg.m)
+    out, k, rt = _c4_wave(q, cfg, 0, 1024, fn)
+    assert np.all(np.isfinite(out))
+    for inst in list(range(0, 1024, 16)) + [1023]:
+        seed = cfg.seed + inst
+        for wl in (0, 1 + (inst * 37) % 1022, 1023):
+            Rs = oracle.gen_positions(seed, wl, 1, cfg.N, cfg.Np, cfg.L, np.float32)
+            g = inst * cfg.W + wl
+            orc, absout, _ = oracle.eval_j2(Rs, k[g:g + 1], rt[g:g + 1], fn, cfg.N, cfg.n_up)
+            assert oracle.normalized_error(out[g:g + 1], orc, absout, fn).max() <= TOL[np.float32], (inst, wl)
+
+
+@pytest.mark.slow
+def test_C4_all_instances_every_walker(q):
+    """All 4096 C4 instances in the bench's four waves of 1024, every walker of
+    every instance vs the oracle (SURVEY 8(d): every config checked in full;
+    ~2 min of oracle time on the box's cores)."""
+    cfg = qmcgen.CONFIGS["C4"]
+    fn = qmcgen.make_functor(cfg.seed, cfg.L, cfg.m)
+    worst = 0.0
+    for first in range(0, cfg.instances, 1024):
+        out, k, rt = _c4_wave(q, cfg, first, 1024, fn)
+        assert np.all(np.isfinite(out))
+        for j in range(1024):
+            seed = cfg.seed + first + j
+            sl = slice(j * cfg.W, (j + 1) * cfg.W)
+            Rh = oracle.gen_positions(seed, 0, cfg.W, cfg.N, cfg.Np, cfg.L, np.float32, threads=THREADS)
+            orc, absout, _ = oracle.eval_j2(Rh, k[sl], rt[sl], fn, cfg.N, cfg.n_up, threads=THREADS)
+            e = oracle.normalized_error(out[sl], orc, absout, fn).max()
+            worst = max(worst, e)
+            assert e <= TOL[np.float32], (first + j, e)
+    print(f"C4: all 4096 instances, worst normalized error {worst:.3e}")
 
 
 # ---------------------------------------------------------------------------

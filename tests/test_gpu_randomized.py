@@ -198,22 +198,14 @@ def _spo_cases(n=16, seed=2028):
 def test_spo_random(q, c):
     """qj2_spo_eval (vgh + determinant ratio) on a drawn grid, orbital count, row
     pitch, cell, position precision and offset (positions outside the cell wrap)."""
-    old = os.environ.pop("QJ2_SPO", None)
-    if c["ldg"]:
-        os.environ["QJ2_SPO"] = "ldg"
-    try:
-        nx, ny, nz, n_orb, ld, W, L = c["nx"], c["ny"], c["nz"], c["n_orb"], c["ld"], c["W"], c["L"]
-        T = qmcgen.spo_table(c["seed"], nx, ny, nz, n_orb, ld)
-        tab = q.SpoTable(dev(T), n_orb, L)
-        rng = np.random.default_rng(c["seed"])
-        pos = (rng.random((W, 3)) * np.asarray(L) + c["shift"]).astype(np.float64 if c["f64"] else np.float32)
-        A = qmcgen.make_ainv_rows(c["seed"], W, n_orb)
-        out, spo = q.spo_eval(tab, dev(pos), Ainv=dev(A), want_spo=True)
-        out, spo = out.cpu().numpy(), spo.cpu().numpy()
-    finally:
-        os.environ.pop("QJ2_SPO", None)
-        if old is not None:
-            os.environ["QJ2_SPO"] = old
+    nx, ny, nz, n_orb, ld, W, L = c["nx"], c["ny"], c["nz"], c["n_orb"], c["ld"], c["W"], c["L"]
+    T = qmcgen.spo_table(c["seed"], nx, ny, nz, n_orb, ld)
+    tab = q.SpoTable(dev(T), n_orb, L)
+    rng = np.random.default_rng(c["seed"])
+    pos = (rng.random((W, 3)) * np.asarray(L) + c["shift"]).astype(np.float64 if c["f64"] else np.float32)
+    A = qmcgen.make_ainv_rows(c["seed"], W, n_orb)
+    out, spo = q.spo_eval(tab, dev(pos), Ainv=dev(A), want_spo=True, kernel="gather" if c["ldg"] else "auto")
+    out, spo = out.cpu().numpy(), spo.cpu().numpy()
     v, g, h, ab = oracle.spo_vgh(T, n_orb, L, pos.astype(np.float64))
     ref = np.concatenate([v[:, None, :], g, h], axis=1)
     s = np.array((nx, ny, nz), dtype=np.float64) / np.array(L)

@@ -8,6 +8,7 @@ Tolerance (fp32 table, fp32 per-term arithmetic): per output
 derivative order).  The ratio's G and L are compared as rho*G and rho*L (the
 lemma's numerators) so that a small rho does not amplify the comparison.
 """
+
 import os
 
 import numpy as np
@@ -41,18 +42,13 @@ def _F(L, n):
 
 @pytest.fixture(params=["tma", "ldg"])
 def kernel(request):
-    """Both SPO kernels: the TMA-pipelined default and the LDG kernel (QJ2_SPO=ldg)."""
-    old = os.environ.pop("QJ2_SPO", None)
-    if request.param == "ldg":
-        os.environ["QJ2_SPO"] = "ldg"
-    yield request.param
-    os.environ.pop("QJ2_SPO", None)
-    if old is not None:
-        os.environ["QJ2_SPO"] = old
+    """Both SPO kernels: the TMA-pipelined default ("auto") and the per-thread LDG gather
+    kernel (QJ2_SPO_GATHER)."""
+    return "auto" if request.param == "tma" else "gather"
 
 
 def check_spo(q, nx, ny, nz, n_orb, ld, W, seed, pos_dtype=np.float32, L=(3.0, 3.5, 4.0), krow_mode=False,
-              shift=0.0):
+              shift=0.0, kernel="auto"):
     T = qmcgen.spo_table(seed, nx, ny, nz, n_orb, ld)
     tab = q.SpoTable(dev(T), n_orb, L)
     rng = np.random.default_rng(seed)
@@ -63,9 +59,9 @@ def check_spo(q, nx, ny, nz, n_orb, ld, W, seed, pos_dtype=np.float32, L=(3.0, 3
         full = np.random.default_rng(seed + 1).random((W, n_orb, lda)).astype(np.float32)
         krow = rng.integers(0, n_orb, W).astype(np.int32)
         full[np.arange(W), krow, :n_orb] = A
-        out, spo = q.spo_eval(tab, dev(pos), Ainv=dev(full), krow=dev(krow), want_spo=True)
+        out, spo = q.spo_eval(tab, dev(pos), Ainv=dev(full), krow=dev(krow), want_spo=True, kernel=kernel)
     else:
-        out, spo = q.spo_eval(tab, dev(pos), Ainv=dev(A), want_spo=True)
+        out, spo = q.spo_eval(tab, dev(pos), Ainv=dev(A), want_spo=True, kernel=kernel)
     out, spo = out.cpu().numpy(), spo.cpu().numpy()
     v, g, h, ab = oracle.spo_vgh(T, n_orb, L, pos.astype(np.float64))
     ref = np.concatenate([v[:, None, :], g, h], axis=1)               # [W][10][n_orb]
@@ -85,29 +81,29 @@ def check_spo(q, nx, ny, nz, n_orb, ld, W, seed, pos_dtype=np.float32, L=(3.0, 3
 
 @pytest.mark.parametrize("n_orb,ld", [(1, 4), (3, 4), (10, 12), (64, 64), (130, 132), (384, 384), (600, 600)])
 def test_spo_vgh_and_ratio(q, kernel, n_orb, ld):
-    check_spo(q, 6, 7, 8, n_orb, ld, 37, seed=10 + n_orb)
+    check_spo(q, 6, 7, 8, n_orb, ld, 37, seed=10 + n_orb, kernel=kernel)
 
 
 def test_spo_z_wrap_and_many_walkers(q, kernel):
     """nz = 4: every walker's z rows wrap (split bulk copies); W > 32 * SMs
     exercises several producer batches per CTA."""
-    check_spo(q, 5, 6, 4, 40, 40, 10000, seed=8)
+    check_spo(q, 5, 6, 4, 40, 40, 10000, seed=8, kernel=kernel)
 
 
 def test_spo_fp64_positions_krow_and_wrapping(q, kernel):
-    check_spo(q, 5, 9, 4, 48, 48, 29, seed=3, pos_dtype=np.float64, krow_mode=True)
+    check_spo(q, 5, 9, 4, 48, 48, 29, seed=3, pos_dtype=np.float64, krow_mode=True, kernel=kernel)
     # positions outside [0, L): wrapped into the cell (periodic table)
-    check_spo(q, 5, 9, 4, 48, 48, 29, seed=4, shift=-7.25)
-    check_spo(q, 5, 9, 4, 48, 48, 29, seed=5, shift=11.5)
+    check_spo(q, 5, 9, 4, 48, 48, 29, seed=4, shift=-7.25, kernel=kernel)
+    check_spo(q, 5, 9, 4, 48, 48, 29, seed=5, shift=11.5, kernel=kernel)
 
 
 def test_spo_v_equals_vgh_values_bitwise(q, kernel):
     """Bspline-v and the value lanes of Bspline-vgh: the same sums in the same
     order (SPEC: 'vs spo_eval_vgh value lanes: identical'); the ratio rho is
     the same dot product reduced over a different thread grouping (1e-12)."""
-    T, tab, pos, out, spo = check_spo(q, 8, 8, 8, 96, 96, 64, seed=21)
+    T, tab, pos, out, spo = check_spo(q, 8, 8, 8, 96, 96, 64, seed=21, kernel=kernel)
     A = qmcgen.make_ainv_rows(21, 64, 96)
-    out_v, spo_v = q.spo_eval(tab, dev(pos), vgh=False, Ainv=dev(A), want_spo=True)
+    out_v, spo_v = q.spo_eval(tab, dev(pos), vgh=False, Ainv=dev(A), want_spo=True, kernel=kernel)
     assert torch.equal(spo_v[:, 0].cpu(), torch.from_numpy(spo[:, 0]))
     np.testing.assert_allclose(out_v.cpu().numpy()[:, 0], out[:, 0], rtol=1e-12, atol=1e-14)
     assert np.all(out_v.cpu().numpy()[:, 1:] == 0)
@@ -135,13 +131,8 @@ def test_spo_kernels_agree(q):
     tab = q.SpoTable(dev(T), 200, (2.0, 2.5, 3.0))
     pos = dev((np.random.default_rng(1).random((3000, 3)) * 3).astype(np.float32))
     A = dev(qmcgen.make_ainv_rows(31, 3000, 200))
-    os.environ.pop("QJ2_SPO", None)
     o1, s1 = q.spo_eval(tab, pos, Ainv=A, want_spo=True)
-    os.environ["QJ2_SPO"] = "ldg"
-    try:
-        o2, s2 = q.spo_eval(tab, pos, Ainv=A, want_spo=True)
-    finally:
-        os.environ.pop("QJ2_SPO", None)
+    o2, s2 = q.spo_eval(tab, pos, Ainv=A, want_spo=True, kernel="gather")
     assert torch.equal(s1, s2)
     torch.testing.assert_close(o1, o2, rtol=1e-10, atol=1e-12)
 
@@ -179,7 +170,7 @@ def test_spo_v_nlpp_points_share_the_walkers_row(q, kernel):
     k = qmcgen.make_k(51, W, 200)
     pts = qmcgen.make_trials(51, np.arange(W), k, 200, 3.0, np.float32, P=12, mode="nlpp")     # [W][12][3]
     A = qmcgen.make_ainv_rows(51, W, n_orb)
-    out, spo = q.spo_eval(tab, dev(pts), vgh=False, Ainv=dev(A), all_trials=True, want_spo=True)
+    out, spo = q.spo_eval(tab, dev(pts), vgh=False, Ainv=dev(A), all_trials=True, want_spo=True, kernel=kernel)
     out, spo = out.cpu().numpy(), spo.cpu().numpy()
     assert out.shape == (W * 12, 5)
     v, g, h, ab = oracle.spo_vgh(T, n_orb, L, pts.reshape(-1, 3).astype(np.float64))
@@ -220,7 +211,7 @@ def test_spo_tma_kernel_deterministic(q, kernel):
     rng = np.random.default_rng(77)
     pos = dev((rng.random((20000, 3)) * 4.0).astype(np.float32))
     A = dev(qmcgen.make_ainv_rows(77, 20000, 384))
-    ref = q.spo_eval(tab, pos, Ainv=A, want_spo=True)
+    ref = q.spo_eval(tab, pos, Ainv=A, want_spo=True, kernel=kernel)
     for _ in range(4):
-        out = q.spo_eval(tab, pos, Ainv=A, want_spo=True)
+        out = q.spo_eval(tab, pos, Ainv=A, want_spo=True, kernel=kernel)
         assert torch.equal(out[0], ref[0]) and torch.equal(out[1], ref[1])
