@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--same-device", action="store_true",
                     help="every rank on cuda:0 (functional multi-rank runs on a one-GPU box; not a measurement)")
     ap.add_argument("--c4-instances", type=int, default=0, help="C4 instance count override (functional runs)")
+    ap.add_argument("--row", action="store_true",
+                    help="C1/C2/C2f64/C3/C3f64: also write the candidate row (r, dx, dy, dz) per item (row a5)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -296,23 +298,34 @@ class OracleSample:
         # (move, partner) like their GPU lines
         self.items = self.n * (self.moves if self.sweep else self.P) * (cfg.N - 1 + (64 if self.j1 else 0))
 
+    forced = None          # N64S(J): the GPU's decisions to replay (the parity field), else its own
+
     def run(self):
+        """Time one pass; its outputs stay in self.result for the parity field."""
         import oracle
         t0 = time.perf_counter()
         if not self.sweep:
-            oracle.eval_j2(self.R, self.k, self.rt, self.fn, self.cfg.N, self.cfg.n_up, threads=self.threads)
-            return time.perf_counter() - t0
+            out, ab, _ = oracle.eval_j2(self.R, self.k, self.rt, self.fn, self.cfg.N, self.cfg.n_up,
+                                        threads=self.threads)
+            dt = time.perf_counter() - t0
+            self.result = (out, ab)
+            return dt
         if self.cfg.name in ("N64S", "N64SJ"):           # oracle.sweep: the whole sweep, as it stands
             j1 = None if self.j1 is None else (self.j1[0], self.j1[1], self.j1[2], self.S1)
-            oracle.sweep(self.R, self.S, self.ks, self.delta, self.us, self.fn, self.cfg.N, self.cfg.n_up, j1=j1,
-                         threads=self.threads)
-            return time.perf_counter() - t0
+            res = oracle.sweep(self.R, self.S, self.ks, self.delta, self.us, self.fn, self.cfg.N, self.cfg.n_up,
+                               j1=j1, forced=self.forced, threads=self.threads)
+            dt = time.perf_counter() - t0
+            self.result = res
+            return dt
+        R, S = self.R, self.S
         for m in range(self.moves):
             k, rt, u = self.ks[m], self.trs[m], self.us[m]
-            out, _, _ = oracle.eval_j2(self.R, k, rt, self.fn, self.cfg.N, self.cfg.n_up, threads=self.threads)
+            out, ab, _ = oracle.eval_j2(R, k, rt, self.fn, self.cfg.N, self.cfg.n_up, threads=self.threads)
+            if m == 0:
+                self.result = (out, ab)
             d = out[:, 1, 0] - out[:, 0, 0]
             acc = (u < np.exp(d) ** 2).astype(np.int32)
-            self.R, self.S, _ = oracle.accept(self.R, self.S, k, rt[:, 1], acc, self.fn, self.cfg.N, self.cfg.n_up)
+            R, S, _ = oracle.accept(R, S, k, rt[:, 1], acc, self.fn, self.cfg.N, self.cfg.n_up)
         return time.perf_counter() - t0
 
 
@@ -346,9 +359,11 @@ class OracleSampleSpo:
     def run(self):
         import oracle
         t0 = time.perf_counter()
-        v, g, h, _ = oracle.spo_vgh(self.T, self.cfg.n_orb, self.cfg.L, self.pos)
-        oracle.det_ratio(self.A, v, g, h)
-        return time.perf_counter() - t0
+        v, g, h, ab = oracle.spo_vgh(self.T, self.cfg.n_orb, self.cfg.L, self.pos)
+        out, aab = oracle.det_ratio(self.A, v, g, h)
+        dt = time.perf_counter() - t0
+        self.result = (out, aab, ab)
+        return dt
 
 
 class OracleSampleJ1:
@@ -365,8 +380,10 @@ class OracleSampleJ1:
     def run(self):
         import oracle
         t0 = time.perf_counter()
-        oracle.eval_j1(self.ions, self.start, self.rt, self.fn1)
-        return time.perf_counter() - t0
+        out, ab = oracle.eval_j1(self.ions, self.start, self.rt, self.fn1)
+        dt = time.perf_counter() - t0
+        self.result = (out, ab)
+        return dt
 
 
 def j1_inputs(cfg, n=None, rank=0):
@@ -537,6 +554,8 @@ class EvalPlan:
     walkers, P = 1, ratio fused against the caller's 5N-state value V_cur."""
     launches_per_step = 2      # j2_eval kernel + the counter memset (multi-tile rows; 1 for one-tile rows)
 
+    row = False                # --row: the optional row output (Fig. 6's v, 16 / 32 B per item more)
+
     def __init__(self, cfg, rank, world):
         import torch
         self.cfg = cfg
@@ -559,7 +578,7 @@ class EvalPlan:
         cfg = self.cfg
         # algorithmic bytes: x, y, z of every source i != k once per walker, plus per
         # walker k (4 B), r_trial (3 sz), V_cur (8 B), out (40 B), ratio (16 B)
-        return cfg.W * (cfg.N - 1) * 3 * self.sz + cfg.W * (4 + 3 * self.sz + 8 + 40 + 16)
+        return cfg.W * (cfg.N - 1) * (3 + (4 if self.row else 0)) * self.sz + cfg.W * (4 + 3 * self.sz + 8 + 40 + 16)
 
     @property
     def alg_bytes_per_launch(self):
@@ -582,12 +601,13 @@ class EvalPlan:
         self.V_cur = v0[:, 0, 0].contiguous()
         self.out = torch.empty((cfg.W, 1, 5), dtype=torch.float64, device="cuda")
         self.ratio = torch.empty((cfg.W, 1, 2), dtype=torch.float64, device="cuda")
+        self.row_out = (torch.empty((cfg.W, 1, 4, cfg.Np), dtype=self.tdt, device="cuda") if self.row else None)
         torch.cuda.synchronize()
 
     def step(self, q, dist_mod):
         cfg = self.cfg
-        q.eval(self.R, self.k, self.rt, self.fn, cfg.N, cfg.n_up, V_cur=self.V_cur, ratio=True,
-               out=self.out, ratio_out=self.ratio, workspace=self.ws)
+        q.eval(self.R, self.k, self.rt, self.fn, cfg.N, cfg.n_up, V_cur=self.V_cur, ratio=True, row=self.row,
+               out=self.out, row_out=self.row_out, ratio_out=self.ratio, workspace=self.ws)
 
     def kernel_ms(self, q, stream, reps):
         if self.flush_l2:
@@ -755,8 +775,14 @@ class C5Plan:
         return _event_ms(lambda: q.eval(self.R, self.k, self.rt, self.fn, cfg.N, cfg.n_up, i_offset=self.a,
                                         n_local=self.n_local, out=self.out, workspace=self.ws), stream, reps)
 
+    def gpu_sample(self, n):
+        return self.out[:n].cpu().numpy()
+
     def e2e(self, q, steps, dist_mod):
-        return None   # see DESIGN.md: the host-buffer path is measured on C3
+        # 60 GB of positions per step cannot sit in pinned host memory: the host-buffer
+        # path is measured on C3 / C3f64 (same kernel, same access pattern)
+        return {"value": None, "reason": "the step's inputs (60.4 GB of positions over all ranks) exceed pinned "
+                                         "host memory; end to end is measured on C3 (same kernel)"}
 
 
 class C4Plan:
@@ -863,8 +889,18 @@ class C4Plan:
     def kernel_ms(self, q, stream, reps):
         return _event_ms(lambda: self._eval_wave(q, *self.resident), stream, reps)
 
+    def gpu_sample(self, n):
+        """instance i0's first n walkers (evaluated in the rank's first wave)."""
+        first, count = self.waves[0]
+        if self.resident != self.waves[0]:
+            self._gen_wave(self.q, first, count)
+            self.resident = self.waves[0]
+            self._eval_wave(self.q, first, count)
+        return self.out[:n].cpu().numpy()
+
     def e2e(self, q, steps, dist_mod):
-        return None   # see DESIGN.md: the host-buffer path is measured on C3
+        return {"value": None, "reason": "the step's inputs (309 GB of positions over 4096 instances) exceed pinned "
+                                         "host memory; end to end is measured on C3 (same kernel family)"}
 
 
 class MultiTrialPlan(EvalPlan):
@@ -959,6 +995,8 @@ class SweepPlan:
         k = self.ks[s]
         q.eval(self.R, k, self.tr[s], self.fn, cfg.N, cfg.n_up, ratio=True, out=self.out,
                ratio_out=self.ratio, workspace=self.ws)
+        if self.s == 1:               # the first move's values (the parity field's sample)
+            self.first_out = self.out.clone()
         q.metropolis(self.ratio, self.u[s], self.acc, trial=1)
         q.accept(self.R, self.S_, k, self.tr[s], self.acc, self.out, self.fn, cfg.N, cfg.n_up, trial=1,
                  workspace=self.wsa)
@@ -976,6 +1014,53 @@ class SweepPlan:
         return _event_ms(lambda: q.accept(self.R, self.S_, k, self.tr[s], self.acc, self.out, self.fn, cfg.N,
                                           cfg.n_up, trial=1, r_old=r_old), stream, reps)
 
+    def gpu_sample(self, n):
+        return self.first_out[:n].cpu().numpy()
+
+    def e2e(self, q, steps, dist_mod):
+        """Through the public API with host buffers: each step uploads its move (k, the
+        (r_k, r'_k) pair, u) from pinned host memory and reads the step's results back
+        (the (V, G, L) pair, the ratios and the decisions); R and the 5N state are the
+        walkers' resident Markov-chain state (7.55 + 12.6 GB), not per-step inputs."""
+        import torch
+        cfg = self.cfg
+        kh = [self.ks[s].cpu().pin_memory() for s in range(self.n)]
+        th = [self.tr[s].cpu().pin_memory() for s in range(self.n)]
+        uh = [self.u[s].cpu().pin_memory() for s in range(self.n)]
+        kd, td, ud = torch.empty_like(self.ks[0]), torch.empty_like(self.tr[0]), torch.empty_like(self.u[0])
+        oh = torch.empty(tuple(self.out.shape), dtype=torch.float64, pin_memory=True)
+        rh = torch.empty(tuple(self.ratio.shape), dtype=torch.float64, pin_memory=True)
+        ah = torch.empty(tuple(self.acc.shape), dtype=torch.int32, pin_memory=True)
+
+        def run(i):
+            s = i % self.n
+            kd.copy_(kh[s], non_blocking=True)
+            td.copy_(th[s], non_blocking=True)
+            ud.copy_(uh[s], non_blocking=True)
+            q.eval(self.R, kd, td, self.fn, cfg.N, cfg.n_up, ratio=True, out=self.out, ratio_out=self.ratio,
+                   workspace=self.ws)
+            q.metropolis(self.ratio, ud, self.acc, trial=1)
+            q.accept(self.R, self.S_, kd, td, self.acc, self.out, self.fn, cfg.N, cfg.n_up, trial=1,
+                     workspace=self.wsa)
+            oh.copy_(self.out, non_blocking=True)
+            rh.copy_(self.ratio, non_blocking=True)
+            ah.copy_(self.acc, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        run(self.s)
+        if dist_mod:
+            dist_mod.barrier()
+        t0 = time.perf_counter()
+        for i in range(steps):
+            run(self.s + 1 + i)
+        dt = allreduce_max((time.perf_counter() - t0) / steps, dist_mod)
+        world = dist_mod.get_world_size() if dist_mod else 1
+        return {"value": self.items_per_step * world / dt, "unit": UNIT,
+                "h2d_bytes_per_step": kh[0].numel() * 4 + th[0].numel() * 4 + uh[0].numel() * 8,
+                "d2h_bytes_per_step": oh.numel() * 8 + rh.numel() * 8 + ah.numel() * 4, "ms_per_step": dt * 1e3,
+                "steps": steps,
+                "api": "qj2_eval + qj2_metropolis + qj2_accept with each step's move copied from pinned host memory "
+                       "and its values, ratios and decisions read back (R and the 5N state resident)"}
+
     @property
     def alg_bytes_per_launch(self):
         # per accepted walker: x, y, z of every partner (12 B) + 5 fp32 state lanes read and written
@@ -983,10 +1068,6 @@ class SweepPlan:
         # per rejected walker
         cfg = self.cfg
         return self.n_acc * ((cfg.N - 1) * 52 + 72) + (cfg.W - self.n_acc) * 4
-
-    def e2e(self, q, steps, dist_mod):
-        return None   # see DESIGN.md: the host-buffer path is measured on C3
-
 
 class GraphSweepPlan(SweepPlan):
     """A full particle-by-particle sweep of the paper's NiO-64 size (N = 768,
@@ -1077,6 +1158,10 @@ class GraphSweepPlan(SweepPlan):
         self.i += 1
         q.sweep(self.R, self.S_, ks, dl, u, self.fn, self.cfg.N, self.cfg.n_up, acc=self.acc_all,
                 dj=self.dj_all, j1=self.j1)
+        if self.i == 1:               # the first sweep (from the start configuration): the parity sample
+            self.first_acc = self.acc_all.cpu().numpy()
+            self.first_dj = self.dj_all.cpu().numpy()
+            self.first_R = self.R[:64].cpu().numpy()
 
     def e2e(self, q, steps, dist_mod):
         """Through the public API with host buffers: each step uploads the walkers'
@@ -1152,9 +1237,28 @@ class SpoPlan:
     @property
     def alg_bytes_per_launch(self):
         cfg = self.cfg
-        # per evaluation: 64 coefficient rows of n_orb fp32 (the method's gather), the position and
-        # the 5 fp64 outputs; per walker the A^{-1} row
-        return cfg.W * self.ppw * (64 * cfg.n_orb * 4 + 12 + 40) + cfg.W * cfg.n_orb * 4
+        # per evaluation the position and the 5 fp64 outputs; per walker the A^{-1} row and the
+        # DISTINCT coefficient rows of n_orb fp32 its points need: 64 for one point (S1); for the 12
+        # NLPP points of a walker (S1V) the union of their 4x4x4 control blocks, since points of one
+        # walker that share a row need it once (counted from the positions: self.rows_per_walker)
+        rows = 64 * cfg.W if not self.nlpp else self.unique_rows
+        return rows * cfg.n_orb * 4 + cfg.W * self.ppw * (12 + 40) + cfg.W * cfg.n_orb * 4
+
+    def _count_unique_rows(self, pts):
+        """Distinct (ix, iy, iz) control rows per walker over its points [W][ppw][3] (the
+        table's uniform periodic grid, reading R22), summed over walkers."""
+        cfg = self.cfg
+        n = np.array([cfg.nx, cfg.ny, cfg.nz])
+        u = np.mod(pts.astype(np.float64), cfg.L) / cfg.L * n
+        i = np.minimum(np.floor(u).astype(np.int64), n - 1)                      # [W][ppw][3]
+        off = np.arange(-1, 3)
+        ix = np.mod(i[..., 0, None] + off, n[0])
+        iy = np.mod(i[..., 1, None] + off, n[1])
+        iz = np.mod(i[..., 2, None] + off, n[2])
+        flat = ((ix[..., :, None, None] * n[1] + iy[..., None, :, None]) * n[2] + iz[..., None, None, :])
+        flat = flat.reshape(pts.shape[0], -1)
+        flat.sort(axis=1)
+        return int((np.diff(flat, axis=1) != 0).sum() + flat.shape[0])
 
     def prepare(self, q):
         import torch
@@ -1166,6 +1270,7 @@ class SpoPlan:
             k = qmcgen.make_k(self.seed, cfg.W, cfg.N)
             pts = qmcgen.make_trials(self.seed, np.arange(cfg.W), k, cfg.N, cfg.L, np.float32, P=12, mode="nlpp")
             self.pos = torch.from_numpy(np.ascontiguousarray(pts)).cuda()
+            self.unique_rows = self._count_unique_rows(pts)
         else:
             self.pos = torch.from_numpy(qmcgen.spo_positions(self.seed, cfg.W, cfg.L)).cuda()
         self.A = torch.from_numpy(qmcgen.make_ainv_rows(self.seed, cfg.W, cfg.n_orb)).cuda()
@@ -1180,6 +1285,9 @@ class SpoPlan:
 
     def kernel_ms(self, q, stream, reps):
         return _event_ms(lambda: self.step(q, None), stream, reps)
+
+    def gpu_sample(self, n):
+        return self.out[:n].cpu().numpy()
 
     def e2e(self, q, steps, dist_mod):
         """Through the public API with host buffers: each step uploads the walkers'
@@ -1259,6 +1367,9 @@ class J1Plan:
         cfg = self.cfg
         return alu_roofline("J1S", "j1_thread_kernel<float>", kms, cfg.W * cfg.n_ions)
 
+    def gpu_sample(self, n):
+        return self.out[:n].cpu().numpy()
+
     def e2e(self, q, steps, dist_mod):
         """Through the public API with host buffers: each step uploads the sweep's
         trial points from pinned memory, runs qj2_eval_j1 (ratio fused) and reads
@@ -1317,6 +1428,61 @@ def plan_kernel_name(plan):
             "S1V": "spo_tma_kernel<v>"}.get(plan.mode, "j2_eval_kernel<float,1,false>")
 
 
+def _plain_rel(gpu, orc, absout):
+    """max |gpu - orc| / |orc| over components with |orc| >= 1e-3 A."""
+    m = np.abs(orc) >= 1e-3 * absout
+    if not m.any():
+        return None
+    return float(np.max(np.abs(np.asarray(gpu, np.float64)[m] - orc[m]) / np.abs(orc[m])))
+
+
+def parity_field(cfg, plan, smp):
+    """Sampled parity of this run's GPU outputs against the oracle sample the
+    cpu_baseline leg just ran (the same walkers [0, n) of rank 0's instance, the
+    same seeded inputs), computed outside the timed region: the max normalized
+    error of DESIGN.md section 4 and the max plain relative error."""
+    import oracle
+    n = smp.n
+    try:
+        if cfg.name in ("N64S", "N64SJ"):
+            R2, S2, own, dj, _ = smp.result
+            acc = plan.first_acc[:, :n]
+            ok = acc >= 0
+            rho2 = np.exp(2.0 * dj)
+            clear = ok & (np.abs(smp.us - rho2) > 1e-3 * rho2)
+            scale = np.maximum(np.abs(S2[:, 0, :cfg.N]).max(1), 1.0)[None, :]
+            e = np.abs(plan.first_dj[:, :n] - dj) / scale
+            return {"walkers": n, "moves": int(acc.shape[0]), "max_normalized_dj_err": float(e[ok].max()),
+                    "decisions_agree_where_clear": bool(np.array_equal(acc[clear], own[clear])),
+                    "positions_bitwise": bool(np.array_equal(plan.first_R[:n, :, :cfg.N], R2[:, :, :cfg.N])),
+                    "what": "the oracle replays the first timed-run sweep of walkers [0, n) on the GPU's decisions"}
+        if cfg.name.startswith("S"):
+            out, aab, ab = smp.result
+            g = plan.gpu_sample(out.shape[0])
+            T = smp.T
+            s = np.array((cfg.nx, cfg.ny, cfg.nz), np.float64) / cfg.L
+            F = np.abs(T).max() * np.array([1, s[0], s[1], s[2], s[0] ** 2, s[0] * s[1], s[0] * s[2], s[1] ** 2,
+                                            s[1] * s[2], s[2] ** 2])
+            scale = np.maximum(aab, oracle.det_ratio_scale(smp.A, ab, F))
+            e0 = np.abs(g[:, 0] - out[:, 0]) / scale[:, 0]
+            e1 = np.abs(g[:, 1:] * g[:, :1] - out[:, 1:] * out[:, :1]) / scale[:, 1:]
+            return {"walkers": int(out.shape[0]), "max_normalized_err": float(max(e0.max(), e1.max())),
+                    "max_plain_rel_err_rho": _plain_rel(g[:, 0], out[:, 0], aab[:, 0])}
+        out, ab = smp.result
+        g = plan.gpu_sample(out.shape[0])
+        if cfg.name.startswith("J"):
+            e = oracle.normalized_error_j1(g, out, ab, smp.fn1)
+        else:
+            e = oracle.normalized_error(g, out, ab, smp.fn)
+        pr = {"walkers": int(out.shape[0]), "max_normalized_err": float(e.max()),
+              "max_plain_rel_err": _plain_rel(g, out, ab)}
+        for c, name in enumerate(("V", "Gx", "Gy", "Gz", "L")):
+            pr[f"max_plain_rel_err_{name}"] = _plain_rel(g[..., c], out[..., c], ab[..., c])
+        return pr
+    except Exception as exc:        # the parity field must never take the bench line down
+        return {"error": repr(exc)}
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
@@ -1334,17 +1500,24 @@ def run_ours(args):
         cfg = dataclasses.replace(cfg, instances=args.c4_instances)
 
     plan = make_plan(cfg, rank, world)
-    if plan.mode in ("N64S", "N64SJ"):
-        plan.prepare(q)                               # one sweep's pre-drawn moves
-    elif plan.mode == "C3S":                          # pre-drawn sweep inputs for every step
-        plan.prepare(q, args.warmup + 2 * args.steps + 2)
-    else:
-        plan.prepare(q)                               # device-resident inputs (generation untimed)
+    if args.row:
+        if not isinstance(plan, EvalPlan) or isinstance(plan, MultiTrialPlan):
+            raise SystemExit("--row applies to C1, C2, C2f64, C3, C3f64")
+        plan.row = True
+    nvtx = torch.cuda.nvtx                            # phase ranges for nsys / ncu --nvtx
+    with nvtx.range(f"prepare {cfg.name}"):
+        if plan.mode in ("N64S", "N64SJ"):
+            plan.prepare(q)                           # state_init, pools of pre-drawn moves
+        elif plan.mode == "C3S":                      # pre-drawn sweep inputs for every step
+            plan.prepare(q, args.warmup + 2 * args.steps + 2)
+        else:
+            plan.prepare(q)                           # device-resident inputs (generation untimed)
 
     stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        plan.step(q, dist_mod)
-    torch.cuda.synchronize()
+    with nvtx.range("warmup"):
+        for _ in range(args.warmup):
+            plan.step(q, dist_mod)
+        torch.cuda.synchronize()
 
     flusher = L2Flusher() if getattr(plan, "flush_l2", False) else None
 
@@ -1353,7 +1526,7 @@ def run_ours(args):
             dist_mod.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with ClockSampler(local) as clk:
+        with ClockSampler(device) as clk:
             if flusher is not None:          # inputs < L2: flush before every step, time steps alone
                 ms = flusher.event_ms(lambda: plan.step(q, dist_mod), stream, K)
             else:
@@ -1367,8 +1540,9 @@ def run_ours(args):
             dist_mod.barrier()
         return ms, clk
 
-    run_timed = (lambda K: plan.timed(K, stream, local, dist_mod)) if hasattr(plan, "timed") else timed
-    ms, clk = run_timed(args.steps)
+    run_timed = (lambda K: plan.timed(K, stream, device, dist_mod)) if hasattr(plan, "timed") else timed
+    with nvtx.range(f"timed {args.steps} steps"):
+        ms, clk = run_timed(args.steps)
     if clk.rejected():
         log(f"[bench] clocks rejected ({clk.summary()}); re-measuring once")
         ms, clk = run_timed(args.steps)
@@ -1378,7 +1552,8 @@ def run_ours(args):
 
     # roofline of the dominant kernel (j2_eval_kernel), timed on its launching stream
     plan.flusher = flusher
-    kms = plan.kernel_ms(q, stream, reps=max(5, min(args.steps, 50)))
+    with nvtx.range("kernel_ms"):
+        kms = plan.kernel_ms(q, stream, reps=max(5, min(args.steps, 50)))
     alg_bytes = plan.alg_bytes_per_launch
     peak, peak_src = measured_peaks()
     achieved = alg_bytes / (kms / 1e3) / 1e9
@@ -1386,33 +1561,39 @@ def run_ours(args):
 
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
-        e2e = plan.e2e(q, args.e2e_steps, dist_mod)
+        with nvtx.range("e2e"):
+            e2e = plan.e2e(q, args.e2e_steps, dist_mod)
 
-    cpu = None
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = cpu_cores()
         nw = args.cpu_sample_walkers or oracle_sample_size(cfg, cores, 15.0)[0]
         smp = make_oracle_sample(cfg, nw, cores)
+        if cfg.name in ("N64S", "N64SJ"):
+            smp.forced = plan.first_acc[:, :smp.n]
         dt = smp.run()
         used = 1 if cfg.name[0] in "SJ" else cores
         cpu = {"value": smp.items / dt, "unit": UNIT, "cores": used, "kind": "oracle",
-               "sample": f"{smp.n} of {cfg.W} walkers of {cfg.name} (N={cfg.N}, {_what(cfg)}), one pass, fp32 inputs "
-                         f"promoted exactly to fp64, plain C oracle, {used} threads ({cpu_model()}), "
-                         f"{dt:.1f} s wall"}
+               "sample": f"{smp.n} of {cfg.W} walkers of {cfg.name} (N={cfg.N}, {_what(cfg)}), one pass, "
+                         f"{'fp64' if getattr(cfg, 'dtype', 'f32') == 'f64' else 'fp32'} inputs (promoted exactly to fp64), plain C "
+                         f"oracle, {used} threads ({cpu_model()}), {dt:.1f} s wall"}
+        parity = parity_field(cfg, plan, smp)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "strong" if plan.mode in ("C4", "C5") else "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": workload_config(cfg, world),
+            "vs_baseline": None, "dtype": getattr(cfg, "dtype", "f32"), "data": "synthetic",
+            "config": dict(workload_config(cfg, world), **({"row_out": "r, dx, dy, dz per item (SoA)"} if args.row
+                                                           else {})),
             "roofline": (plan.roofline(kms, peak) if hasattr(plan, "roofline") else
                          {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                           "frac": achieved / peak, "traffic": traffic,
                           "kernel": plan_kernel_name(plan), "kernel_ms": kms,
                           "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src}),
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": e2e,
             "gpu_launches": plan.launches_per_step * args.steps,
             "clocks": clk.summary(),

@@ -192,13 +192,14 @@ def _nlpp_trials(seed, walkers, k, N, L, dtype, P):
         raise ValueError("mode='nlpp' is the 12-point icosahedral rule (P = 12)")
     walkers = np.asarray(walkers, dtype=np.int64).reshape(-1)
     W = walkers.size
-    rng = np.random.default_rng([int(seed), 6])
     nmax = int(walkers.max()) + 1 if W else 0
-    q = rng.normal(size=(nmax, 4))[walkers] if W else np.zeros((0, 4))          # random rotations
+    # one stream per quantity, so a walker's draws do not depend on which walkers are requested
+    rq, rd, rr = (np.random.default_rng([int(seed), 6, j]) for j in range(3))
+    q = rq.normal(size=(nmax, 4))[walkers] if W else np.zeros((0, 4))          # random rotations
     q /= np.linalg.norm(q, axis=1, keepdims=True)
-    u_dir = rng.normal(size=(nmax, 3))[walkers] if W else np.zeros((0, 3))       # ion direction
+    u_dir = rd.normal(size=(nmax, 3))[walkers] if W else np.zeros((0, 3))       # ion direction
     u_dir /= np.linalg.norm(u_dir, axis=1, keepdims=True)
-    rad = rng.uniform(0.3, 1.0, size=nmax)[walkers] if W else np.zeros(0)
+    rad = rr.uniform(0.3, 1.0, size=nmax)[walkers] if W else np.zeros(0)
     rk = np.stack([position_at(seed, walkers, d, k.astype(np.int64), L, dtype) for d in range(3)],
                   axis=-1).astype(np.float64)
     rI = rk + rad[:, None] * u_dir

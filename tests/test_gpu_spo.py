@@ -215,3 +215,23 @@ def test_spo_tma_kernel_deterministic(q, kernel):
     for _ in range(4):
         out = q.spo_eval(tab, pos, Ainv=A, want_spo=True, kernel=kernel)
         assert torch.equal(out[0], ref[0]) and torch.equal(out[1], ref[1])
+
+
+@pytest.mark.parametrize("kernel", ["auto", "gather"])
+def test_spo_non_finite_positions_give_nan_not_faults(q, kernel):
+    """A NaN or infinite coordinate gathers an in-range row with NaN weights: that
+    walker's outputs are NaN, every other walker is unaffected, no device fault."""
+    T = qmcgen.spo_table(91, 8, 8, 8, 64, 64)
+    tab = q.SpoTable(dev(T), 64, (3.0, 3.0, 3.0))
+    pos = (np.random.default_rng(5).random((40, 3)) * 3).astype(np.float32)
+    bad = [3, 17, 31]
+    pos[3, 0], pos[17, 1], pos[31, 2] = np.nan, np.inf, -np.inf
+    A = qmcgen.make_ainv_rows(91, 40, 64)
+    out, spo = q.spo_eval(tab, dev(pos), Ainv=dev(A), want_spo=True, kernel=kernel)
+    torch.cuda.synchronize()
+    out, spo = out.cpu().numpy(), spo.cpu().numpy()
+    good = np.setdiff1d(np.arange(40), bad)
+    assert np.all(np.isnan(out[bad, 0])) and np.all(np.isnan(spo[bad, 0, :64]))
+    assert np.all(np.isfinite(out[good])) and np.all(np.isfinite(spo[good, :, :64]))
+    ref, _ = q.spo_eval(tab, dev(pos[good]), Ainv=dev(A[good]), want_spo=True, kernel=kernel)
+    assert np.array_equal(ref.cpu().numpy(), out[good])

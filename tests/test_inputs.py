@@ -107,3 +107,23 @@ def test_sweep_inputs_are_an_ordered_sweep():
         assert np.array_equal(tr[s, :, 0, :], R[np.arange(W), :, ks[s]])
     assert np.all((tr[:, :, 1] >= 0) & (tr[:, :, 1] < L))
     assert np.all((u >= 0) & (u < 1)) and u.dtype == np.float64
+
+
+def test_trial_draws_do_not_depend_on_the_walker_subset():
+    """Every make_trials mode gives a walker the same trial points whichever walkers
+    are requested (the bench's oracle sample of walkers [0, n) and the GPU run of all
+    W must see the same inputs), and make_sweep_moves' streams are independent draws
+    of one shape (stream 0 = the default)."""
+    N, L = 768, qmcgen.cell_length(768)
+    k = qmcgen.make_k(7, 64, N)
+    for mode, P in (("move", 1), ("drift", 2), ("noop", 1), ("nlpp", 12)):
+        full = qmcgen.make_trials(7, np.arange(64), k, N, L, np.float32, P=P, mode=mode)
+        part = qmcgen.make_trials(7, np.arange(10), k[:10], N, L, np.float32, P=P, mode=mode)
+        sub = qmcgen.make_trials(7, np.array([3, 40]), k[[3, 40]], N, L, np.float32, P=P, mode=mode)
+        assert np.array_equal(full[:10], part), mode
+        assert np.array_equal(full[[3, 40]], sub), mode
+    a = qmcgen.make_sweep_moves(7, 16, N, 20)
+    b = qmcgen.make_sweep_moves(7, 16, N, 20, stream=0)
+    c = qmcgen.make_sweep_moves(7, 16, N, 20, stream=1)
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    assert np.array_equal(a[0], c[0]) and not np.array_equal(a[1], c[1])     # ordered k, fresh delta

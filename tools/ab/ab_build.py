@@ -25,6 +25,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C3")
     ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--bench-args", default="", help="extra bench.py arguments, e.g. '--c4-instances 1024'")
     ap.add_argument("flags", nargs="*")
     a = ap.parse_args()
     from paper_1708_02645_b200 import _build
@@ -34,7 +35,8 @@ def main():
     for name, lib in libs.items():
         env = dict(os.environ, QJ2_LIB=lib)
         out = subprocess.run([sys.executable, "bench.py", "--config", a.config, "--steps", str(a.steps), "--warmup", "5",
-                              "--no-cpu-baseline", "--no-e2e"], cwd=ROOT, env=env, capture_output=True, text=True)
+                              "--no-cpu-baseline", "--no-e2e", *a.bench_args.split()], cwd=ROOT, env=env,
+                             capture_output=True, text=True)
         d = json.loads(out.stdout.strip().splitlines()[-1])
         print(json.dumps({"build": name, "flags": a.flags if name == "variant" else [], "config": a.config,
                           "ms_per_step": d["ms_per_step"], "kernel_ms": d["roofline"]["kernel_ms"],

@@ -15,7 +15,7 @@ KEYS = [
     "dram__throughput.avg.pct_of_peak_sustained_elapsed",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "smsp__issue_active.avg.pct_of_peak_sustained_active",
-    "smsp__inst_executed.sum",
+    "smsp__inst_executed.sum", "smsp__thread_inst_executed.sum",
     "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread", "launch__occupancy_limit_registers",
     "sm__cycles_elapsed.avg.per_second",
@@ -49,10 +49,15 @@ def main():
     for d in raw(rep):
         name = d.get("Kernel Name", ("?", ""))[0]
         m = {k: d[k][0] + (" " + d[k][1] if d[k][1] else "") for k in KEYS if k in d}
-        stalls = {k: float(d[k][0].replace(",", "")) for k in d
-                  if k.startswith("smsp__average_warp_latency_issue_stalled") or
-                  (k.startswith("smsp__warp_issue_stalled_") and k.endswith("_per_warp_active.pct"))}
-        top = dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:8])
+        stalls = {}
+        for k in d:
+            if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("_not_issued"):
+                try:
+                    stalls[k.replace("smsp__pcsamp_warps_issue_stalled_", "")] = float(d[k][0].replace(",", ""))
+                except ValueError:
+                    pass
+        tot = sum(stalls.values()) or 1.0
+        top = {k: round(v / tot, 4) for k, v in sorted(stalls.items(), key=lambda kv: -kv[1])[:8]}
         res.append({"kernel": name, "metrics": m, "top_stalls": top})
     txt = json.dumps(res, indent=1)
     print(txt)
