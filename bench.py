@@ -555,6 +555,7 @@ class EvalPlan:
     launches_per_step = 2      # j2_eval kernel + the counter memset (multi-tile rows; 1 for one-tile rows)
 
     row = False                # --row: the optional row output (Fig. 6's v, 16 / 32 B per item more)
+    row_out = None
 
     def __init__(self, cfg, rank, world):
         import torch
@@ -771,9 +772,21 @@ class C5Plan:
                                    workspace=self.ws)
 
     def kernel_ms(self, q, stream, reps):
+        """The eval kernel alone; spans() adds the kernel + all-reduce + ratio span."""
         cfg = self.cfg
-        return _event_ms(lambda: q.eval(self.R, self.k, self.rt, self.fn, cfg.N, cfg.n_up, i_offset=self.a,
-                                        n_local=self.n_local, out=self.out, workspace=self.ws), stream, reps)
+        kms = _event_ms(lambda: q.eval(self.R, self.k, self.rt, self.fn, cfg.N, cfg.n_up, i_offset=self.a,
+                                       n_local=self.n_local, out=self.out, workspace=self.ws), stream, reps)
+        full = _event_ms(lambda: self.step(q, None), stream, reps)
+        self.span = {"kernel_ms": kms, "kernel_allreduce_ratio_ms": full,
+                     "allreduce": "torch.distributed all_reduce(SUM) of W*5 fp64 (40 KB) on the "
+                                  + (self.parallel_backend() or "(one rank: none)")}
+        return kms
+
+    def parallel_backend(self):
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            return dist.get_backend()
+        return None
 
     def gpu_sample(self, n):
         return self.out[:n].cpu().numpy()
@@ -1465,8 +1478,10 @@ def parity_field(cfg, plan, smp):
                                             s[1] * s[2], s[2] ** 2])
             scale = np.maximum(aab, oracle.det_ratio_scale(smp.A, ab, F))
             e0 = np.abs(g[:, 0] - out[:, 0]) / scale[:, 0]
-            e1 = np.abs(g[:, 1:] * g[:, :1] - out[:, 1:] * out[:, :1]) / scale[:, 1:]
-            return {"walkers": int(out.shape[0]), "max_normalized_err": float(max(e0.max(), e1.max())),
+            e = e0.max()
+            if cfg.name != "S1V":       # Bspline-vgh: also the numerators rho G and rho L (S1V computes rho only)
+                e = max(e, (np.abs(g[:, 1:] * g[:, :1] - out[:, 1:] * out[:, :1]) / scale[:, 1:]).max())
+            return {"evaluations": int(out.shape[0]), "max_normalized_err": float(e),
                     "max_plain_rel_err_rho": _plain_rel(g[:, 0], out[:, 0], aab[:, 0])}
         out, ab = smp.result
         g = plan.gpu_sample(out.shape[0])
@@ -1578,6 +1593,13 @@ def run_ours(args):
                          f"{'fp64' if getattr(cfg, 'dtype', 'f32') == 'f64' else 'fp32'} inputs (promoted exactly to fp64), plain C "
                          f"oracle, {used} threads ({cpu_model()}), {dt:.1f} s wall"}
         parity = parity_field(cfg, plan, smp)
+        # the T = 1 oracle on a sub-sample, for the per-core rate
+        if used > 1:
+            n1 = max(1, min(smp.n, 4 if cfg.N > 100000 else 16))
+            s1 = make_oracle_sample(cfg, n1, 1)
+            dt1 = s1.run()
+            cpu["single_thread"] = {"value": s1.items / dt1, "unit": UNIT, "cores": 1,
+                                    "sample": f"{s1.n} walkers, one thread, {dt1:.2f} s wall"}
 
     if rank == 0:
         line = {
@@ -1598,6 +1620,8 @@ def run_ours(args):
             "gpu_launches": plan.launches_per_step * args.steps,
             "clocks": clk.summary(),
         }
+        if getattr(plan, "span", None):
+            line["spans"] = plan.span
         print(json.dumps(line), flush=True)
     if dist_mod:
         dist_mod.barrier()

@@ -206,6 +206,19 @@ def normalized_error(gpu, orc, absout, fn) -> np.ndarray:
     return np.abs(np.asarray(gpu, dtype=np.float64) - orc) / denom
 
 
+def plain_relative_error(gpu, orc, absout, floor: float = 1e-3):
+    """The plain relative error SURVEY 8(c) asks to report beside the normalized
+    one: max |s_gpu - s_orc| / |s_orc| over components with |s_orc| >= floor * A_s
+    (per component V, Gx, Gy, Gz, L; None where no component qualifies)."""
+    g = np.asarray(gpu, dtype=np.float64)
+    out = []
+    for c in range(orc.shape[-1]):
+        o, a, x = orc[..., c], absout[..., c], g[..., c]
+        m = np.abs(o) >= floor * a
+        out.append(float(np.max(np.abs(x[m] - o[m]) / np.abs(o[m]))) if m.any() else None)
+    return out
+
+
 def _lib_next2():
     L = lib()
     if not getattr(L, "_next2", False):

@@ -21,6 +21,12 @@
 #ifndef QJ2_WARP_MINB
 #define QJ2_WARP_MINB 2
 #endif
+#ifndef QJ2_EVAL64_PF
+#define QJ2_EVAL64_PF 2        // fp64 CTA kernel
+#endif
+#ifndef QJ2_EVAL64_MINB
+#define QJ2_EVAL64_MINB 2
+#endif
 
 namespace qj2 {
 
@@ -53,18 +59,19 @@ cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStre
         // C4 wave 5.89 TB/s vs 5.31 for two groups at 3 CTAs/SM (80 registers, spilling), 5.51 for
         // four groups, 5.52 for one group at 4 CTAs/SM (profiles/r01_ab_sweep_s3.md)
         if (row) j2_eval_warp_kernel<T, true, 1, 2, MODE><<<nbw, TPB, 0, s>>>(p, units);
-        else if (sizeof(T) == 4) j2_eval_warp_kernel<T, false, QJ2_WARP_PF, QJ2_WARP_MINB, MODE><<<nbw, TPB, 0, s>>>(p, units);
+        else if constexpr (sizeof(T) == 4)
+            j2_eval_warp_kernel<T, false, QJ2_WARP_PF, QJ2_WARP_MINB, MODE><<<nbw, TPB, 0, s>>>(p, units);
         else j2_eval_warp_kernel<T, false, 2, 2, MODE><<<nbw, TPB, 0, s>>>(p, units);
         return cudaGetLastError();
     }
     const unsigned nb = (unsigned)nblocks;
     if (row)
         j2_eval_kernel<T, true, 1, sizeof(T) == 4 ? 4 : 2, MODE><<<nb, TPB, 0, s>>>(p);
-    else if (sizeof(T) == 4)   // two vector groups in flight per thread, 3 CTAs/SM (80 registers): measured
-                               // best on B200 against distance 1 at 4 CTAs/SM and 3 at 2
+    else if constexpr (sizeof(T) == 4)   // two vector groups in flight per thread, 3 CTAs/SM (80 registers):
+                                         // measured best on B200 against distance 1 at 4 CTAs/SM and 3 at 2
         j2_eval_kernel<T, false, QJ2_EVAL_PF, QJ2_EVAL_MINB, MODE><<<nb, TPB, 0, s>>>(p);
-    else                       // fp64: two groups in flight, 2 CTAs/SM
-        j2_eval_kernel<T, false, 2, 2, MODE><<<nb, TPB, 0, s>>>(p);
+    else                                 // fp64: two groups in flight, 2 CTAs/SM
+        j2_eval_kernel<T, false, QJ2_EVAL64_PF, QJ2_EVAL64_MINB, MODE><<<nb, TPB, 0, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -55,6 +55,8 @@ def check(q, R, k, rt, fn, N, n_up, dtype, i_offset=0, n_local=None, row=False):
     err = oracle.normalized_error(out, orc, absout, fn)
     assert np.all(np.isfinite(out))
     assert err.max() <= TOL[dtype], f"max normalized error {err.max():.3e}"
+    print(f"N={N} {np.dtype(dtype).name}: normalized {err.max():.2e}, plain relative (V, Gx, Gy, Gz, L) "
+          f"{oracle.plain_relative_error(out, orc, absout)}")
     if row:
         return out, orc, res[1].cpu().numpy(), orow
     return out, orc
@@ -313,6 +315,12 @@ def test_C3_full_size_every_walker(q):
     assert np.all(np.isfinite(out))
     err = oracle.normalized_error(out, orc, absout, fn)
     assert err.max() <= TOL[np.float32], err.max()
+    # the plain relative error: fp32 per-term arithmetic (rounded functor table and 1/delta)
+    # leaves a per-interval bias of ~1e-7 of the term scale that cancelling G sums do not average away,
+    # so near |G| = 1e-3 A it reaches ~1e-4; V (all terms >= 0) stays at ~1e-7
+    rel = oracle.plain_relative_error(out, orc, absout)
+    print(f"C3 every walker: normalized {err.max():.2e}, plain relative (V, Gx, Gy, Gz, L) {rel}")
+    assert rel[0] <= 1e-6 and max(rel[1:]) <= 1e-3
 
 
 def test_C4_instances_every_walker(q):
