@@ -552,7 +552,7 @@ class EvalPlan:
     """The hot path on one instance per rank (C1, C2, C2f64, C3, C3f64; weak
     scaling, no collective on the data path): one qj2_eval launch over all W
     walkers, P = 1, ratio fused against the caller's 5N-state value V_cur."""
-    launches_per_step = 2      # j2_eval kernel + the counter memset (multi-tile rows; 1 for one-tile rows)
+    launches_per_step = 1      # one j2_eval kernel (multi-tile rows add a 4 KB cudaMemsetAsync of the counters)
 
     row = False                # --row: the optional row output (Fig. 6's v, 16 / 32 B per item more)
     row_out = None
@@ -569,8 +569,7 @@ class EvalPlan:
         # inputs that fit in the 126 MB L2 (C1, C2, C2f64) are flushed before every timed step
         self.flush_l2 = cfg.W * 3 * cfg.Np * self.sz < (126 << 20)
         self.ch = 204800 if not self.f64 else 102400          # tile of the CTA kernel (sources)
-        if cfg.N <= 2048 or (cfg.N <= self.ch and cfg.W >= 4096):
-            self.launches_per_step = 1
+        self.warp_kernel = cfg.N <= 2048 or (cfg.N <= self.ch and cfg.W >= 4096)
 
     def items_total(self, world):
         return self.items_per_step * world
@@ -622,7 +621,7 @@ class EvalPlan:
     def roofline(self, kms, peak_hbm):
         cfg = self.cfg
         achieved = self._alg() / (kms / 1e3) / 1e9
-        kern = ("j2_eval_warp_kernel" if self.launches_per_step == 1 else "j2_eval_kernel") + \
+        kern = ("j2_eval_warp_kernel" if self.warp_kernel else "j2_eval_kernel") + \
             f"<{'double' if self.f64 else 'float'}>"
         r = {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s", "frac": achieved / peak_hbm,
              "traffic": committed_traffic(self.mode), "kernel": kern, "kernel_ms": kms,
@@ -730,7 +729,7 @@ class C5Plan:
     evaluates sources [g*N/G, (g+1)*N/G) (qj2_eval with i_offset), then one NCCL
     all_reduce(SUM) of the 40 KB fp64 partials and qj2_ratio (strong scaling)."""
     mode = "C5"
-    launches_per_step = 3      # j2_eval_kernel + counter memset + ratio_kernel (+ NCCL all-reduce if G > 1)
+    launches_per_step = 2      # j2_eval_kernel + ratio_kernel (+ the counter memset and the NCCL all-reduce)
 
     def __init__(self, cfg, rank, world):
         from paper_1708_02645_b200 import parallel
@@ -805,7 +804,7 @@ class C4Plan:
     wave is outside the timed spans; the step time is the sum of the waves'
     kernel spans).  No collective on the data path."""
     mode = "C4"
-    launches_per_step = 2      # per wave: j2_eval_kernel (+ no memset: one tile per walker)
+    launches_per_step = 1      # per wave: one j2_eval_warp_kernel (one tile per walker: no memset)
     MAX_RESIDENT = 1024        # instances per wave (77 GB)
 
     def __init__(self, cfg, rank, world):
@@ -921,7 +920,7 @@ class MultiTrialPlan(EvalPlan):
     variant, P = 12 NLPP quadrature), one eval launch per step; the P trials
     of a tile run on consecutive CTAs (one HBM read, L2 hits for the rest).
     Issue-bound (FP32 ALU) rather than HBM-bound."""
-    launches_per_step = 2      # j2_eval_kernel + counter memset (+ ratio kernel when V_cur is not given)
+    launches_per_step = 1      # j2_eval_kernel (+ the ratio kernel when V_cur is not given: drift)
 
     def __init__(self, cfg, rank, world):
         import qmcgen
@@ -930,7 +929,7 @@ class MultiTrialPlan(EvalPlan):
         self.P, self.tmode = qmcgen.trial_spec(cfg.name)
         self.items_per_step = cfg.W * self.P * (cfg.N - 1)
         if self.tmode == "drift":
-            self.launches_per_step = 3
+            self.launches_per_step = 2
 
     def _alg(self):
         cfg = self.cfg
@@ -972,7 +971,7 @@ class SweepPlan:
     qj2_accept (R[:, k] and the 5N fp32 state of every partner).  Electron
     k = (k0 + s) mod N at step s (ordered sweep), inputs pre-drawn by qmcgen."""
     mode = "C3S"
-    launches_per_step = 6      # eval kernel + counter memset + ratio + metropolis + r_k gather + accept kernel
+    launches_per_step = 5      # eval kernel + ratio + metropolis + r_k gather + accept kernel (+ the counter memset)
 
     def __init__(self, cfg, rank, world):
         self.cfg = cfg

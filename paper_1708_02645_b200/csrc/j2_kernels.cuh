@@ -28,6 +28,9 @@ constexpr int ITERS = QJ2_ITERS;  // vector iterations per sub-tile: 32 fp32 ter
 #define QJ2_SUB 25
 #endif
 constexpr int SUB = QJ2_SUB;      // sub-tiles per CTA tile: 25 x 8192 fp32 sources (A/B builds: -DQJ2_SUB=n)
+#ifndef QJ2_WARP_COMPACT_GEN
+#define QJ2_WARP_COMPACT_GEN 0    // warp kernel: masked sub-tiles as a compact rolled loop (A/B builds)
+#endif
 constexpr int NACC = 6;           // fp32 accumulators per trial: V, Gx, Gy, Gz, sum h, sum du/r
 constexpr int NOUT = 5;           // fp64 physical outputs per trial: V, Gx, Gy, Gz, L
 constexpr int MAXG = 4;           // source groups (J2: 2 spin halves; J1: up to 4 species)
@@ -285,6 +288,54 @@ __device__ __forceinline__ void tile_multi(int tid, const EvalParams &p, int kg,
     }
 }
 
+// A J2 sub-tile that is not clean (holds k, straddles N_up, or is ragged), as a compact
+// rolled loop: one vector group per iteration, the next one loaded ahead.  Small code
+// (one copy of the term instead of ITERS x VW) for kernels whose warps run clean and
+// masked sub-tiles at the same time (the warp kernel: one masked sub-tile of six at C4).
+template <typename T, bool ROW, int NT>
+__device__ __forceinline__ void tile_gen_compact(int tid, const typename Traits<T>::V *__restrict__ px,
+                                                 const typename Traits<T>::V *__restrict__ py,
+                                                 const typename Traits<T>::V *__restrict__ pz, const Trial<T> &tr,
+                                                 const GroupC<T> &gc, const SubMask &mk, T (&acc)[NACC],
+                                                 typename Traits<T>::V *rowp, int64_t row_stride) {
+    using Tr = Traits<T>;
+    using V = typename Tr::V;
+    constexpr int VW = Tr::VW;
+    const int vmax = (mk.len - 1) / VW;
+    auto ld = [&](int it, V &x, V &y, V &z) {
+        const int o = min(it * NT + tid, vmax) - tid;
+        x = Tr::ld_stream(px + o); y = Tr::ld_stream(py + o); z = Tr::ld_stream(pz + o);
+    };
+    V nx, ny, nz;
+    ld(0, nx, ny, nz);
+#pragma unroll 1
+    for (int it = 0; it < ITERS; ++it) {
+        const int rel = (it * NT + tid) * VW;
+        const V bx = nx, by = ny, bz = nz;
+        if (it + 1 < ITERS) ld(it + 1, nx, ny, nz);
+        if (rel < mk.len) {
+            V ro[4];
+#pragma unroll
+            for (int e = 0; e < VW; ++e) {
+                const int li = rel + e;
+                const bool dead = (li >= mk.len) || (li == mk.k_rel);
+                const uint32_t base = li < mk.up_rel ? gc.base : mk.base_hi;
+                const T dx = min_image(Tr::comp(bx, e), tr.ax);
+                const T dy = min_image(Tr::comp(by, e), tr.ay);
+                const T dz = min_image(Tr::comp(bz, e), tr.az);
+                T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                r2 = dead ? T(1e30) : r2;
+                const T r = accumulate<T>(dx, dy, dz, r2, gc.invd, base, gc.clamp, acc);
+                if (ROW) { Tr::set(ro[0], e, r); Tr::set(ro[1], e, dx); Tr::set(ro[2], e, dy); Tr::set(ro[3], e, dz); }
+            }
+            if (ROW) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) __stcs(rowp + c * row_stride + it * NT, ro[c]);
+            }
+        }
+    }
+}
+
 // Flush a sub-tile's T partials into the fp64 accumulators: raw for J2,
 // physical (scaled by the sub-tile group's delta factors) for J1.
 template <typename T, int MODE>
@@ -370,7 +421,7 @@ __device__ __forceinline__ void sub_tile(int tid, const EvalParams &p, int kg, u
 // J2 sub-tile with 32-bit classification relative to the walker's tile
 // (tile length tlen, k at k_t or -1, sources [0, up_t) of the tile spin-up)
 // and the two per-walker functor constant sets.  s0: the sub-tile's offset.
-template <typename T, bool ROW, int PF, int NT>
+template <typename T, bool ROW, int PF, int NT, bool COMPACT_GEN = false>
 __device__ __forceinline__ void j2_sub_tile32(int tid, const EvalParams &p, int kg, uint32_t tab_addr, int32_t s0,
                                               int32_t tlen, int32_t k_t, int32_t up_t, const GroupC<T> &g_up,
                                               const GroupC<T> &g_dn, const typename Traits<T>::V *px,
@@ -395,6 +446,8 @@ __device__ __forceinline__ void j2_sub_tile32(int tid, const EvalParams &p, int 
     mk.base_hi = straddle ? g_dn.base : gc.base;
     if (len == SCH && !k_in && !straddle)
         tile_run<T, ROW, PF, false, NT, MODE_J2>(tid, p, kg, tab_addr, px, py, pz, tr, gc, mk, acc, rp, row_stride);
+    else if constexpr (COMPACT_GEN)
+        tile_gen_compact<T, ROW, NT>(tid, px, py, pz, tr, gc, mk, acc, rp, row_stride);
     else
         tile_run<T, ROW, PF, true, NT, MODE_J2>(tid, p, kg, tab_addr, px, py, pz, tr, gc, mk, acc, rp, row_stride);
     flush<T, MODE_J2>(acc, dacc, gc.sg, gc.sh, gc.ss);      // J2: raw sums (one delta for both groups)
@@ -621,8 +674,9 @@ j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
         const V *pz = reinterpret_cast<const V *>(Rw + 2 * p.Np) + voff;
         V *rp = ROW ? reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + g) * 4) * p.Np) + voff : nullptr;
         if constexpr (MODE == MODE_J2)
-            j2_sub_tile32<T, ROW, PF, 32>(lane, p, kg, tab_addr, (int32_t)sstart, tlen, k_t, up_t, g_up, g_dn, px,
-                                          py, pz, tr, dacc, rp, row_stride);
+            j2_sub_tile32<T, ROW, PF, 32, QJ2_WARP_COMPACT_GEN != 0>(lane, p, kg, tab_addr, (int32_t)sstart, tlen,
+                                                                      k_t, up_t, g_up, g_dn, px, py, pz, tr, dacc, rp,
+                                                                      row_stride);
         else
             sub_tile<T, ROW, PF, 32, MODE>(lane, p, kg, tab_addr, sstart, send, k_local, px, py, pz, tr, dacc, rp,
                                            row_stride);

@@ -11,6 +11,11 @@ cap() {  # config kernel-regex skip
     python bench.py --config $1 --steps 4 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_r02/$1.log 2>&1
   echo "ncu $1 rc $?"
   python tools/ncu_summary.py gpurun_out/ncu_r02/$1.ncu-rep --json gpurun_out/ncu_r02/$1.json > /dev/null
+  # gpurun brings back <= 64 MiB: keep the summary (and the SASS-level source page of the key kernels)
+  case " ${KEEP_SRC:-C3 N64S} " in *" $1 "*)
+    ncu -i gpurun_out/ncu_r02/$1.ncu-rep --page source --csv --print-source sass > gpurun_out/ncu_r02/$1_source.csv 2>/dev/null;;
+  esac
+  rm -f gpurun_out/ncu_r02/$1.ncu-rep
 }
 for spec in ${CAPS:-"C3 j2_eval_kernel" "C3f64 j2_eval_kernel" "C2 j2_eval_warp" "C2f64 j2_eval_warp" "C3P2 j2_eval_kernel" "C3P12 j2_eval_kernel" "C3S j2_accept" "C4 j2_eval_warp" "C5 j2_eval_kernel" "S1 spo_tma" "S1V spo_tma" "J1S j1_thread" "N64S j2_sweep" "N64SJ j2_sweep"}; do
   set -- $spec; cap $1 $2 $3
