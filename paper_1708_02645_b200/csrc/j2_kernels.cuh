@@ -28,9 +28,7 @@ constexpr int ITERS = QJ2_ITERS;  // vector iterations per sub-tile: 32 fp32 ter
 #define QJ2_SUB 25
 #endif
 constexpr int SUB = QJ2_SUB;      // sub-tiles per CTA tile: 25 x 8192 fp32 sources (A/B builds: -DQJ2_SUB=n)
-#ifndef QJ2_WARP_COMPACT_GEN
-#define QJ2_WARP_COMPACT_GEN 0    // warp kernel: masked sub-tiles as a compact rolled loop (A/B builds)
-#endif
+
 constexpr int NACC = 6;           // fp32 accumulators per trial: V, Gx, Gy, Gz, sum h, sum du/r
 constexpr int NOUT = 5;           // fp64 physical outputs per trial: V, Gx, Gy, Gz, L
 constexpr int MAXG = 4;           // source groups (J2: 2 spin halves; J1: up to 4 species)
@@ -624,9 +622,15 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
 // trial) walks all of the walker's sources in per-warp sub-tiles of
 // 32*VW*ITERS sources; the warp's fp64 shuffle tree is the whole
 // (deterministic) reduction: no shared-memory reduction, no cross-CTA
-// partials, no counters.
+// partials, no counters.  COMPACT_GEN (rows of >= 4 sub-tiles): the masked
+// sub-tile (the one holding k, a straddle, the ragged end) runs the compact
+// rolled loop, so the resident warps -- each at its own walker's clean or
+// masked sub-tile -- share a 31 KB instead of a 52 KB instruction footprint
+// (C4 wave: instruction-fetch stalls 25% of samples; 0.833 -> 0.886 of the
+// HBM peak); short rows, where most sub-tiles are masked, keep the pipelined
+// masked loop.
 // ===========================================================================
-template <typename T, bool ROW, int PF, int MINB, int MODE = MODE_J2>
+template <typename T, bool ROW, int PF, int MINB, int MODE = MODE_J2, bool COMPACT_GEN = false>
 __global__ void __launch_bounds__(TPB, MINB)
 j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
     using Tr = Traits<T>;
@@ -674,9 +678,8 @@ j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
         const V *pz = reinterpret_cast<const V *>(Rw + 2 * p.Np) + voff;
         V *rp = ROW ? reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + g) * 4) * p.Np) + voff : nullptr;
         if constexpr (MODE == MODE_J2)
-            j2_sub_tile32<T, ROW, PF, 32, QJ2_WARP_COMPACT_GEN != 0>(lane, p, kg, tab_addr, (int32_t)sstart, tlen,
-                                                                      k_t, up_t, g_up, g_dn, px, py, pz, tr, dacc, rp,
-                                                                      row_stride);
+            j2_sub_tile32<T, ROW, PF, 32, COMPACT_GEN>(lane, p, kg, tab_addr, (int32_t)sstart, tlen, k_t, up_t, g_up,
+                                                        g_dn, px, py, pz, tr, dacc, rp, row_stride);
         else
             sub_tile<T, ROW, PF, 32, MODE>(lane, p, kg, tab_addr, sstart, send, k_local, px, py, pz, tr, dacc, rp,
                                            row_stride);

@@ -59,9 +59,16 @@ cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStre
         // C4 wave 5.89 TB/s vs 5.31 for two groups at 3 CTAs/SM (80 registers, spilling), 5.51 for
         // four groups, 5.52 for one group at 4 CTAs/SM (profiles/r01_ab_sweep_s3.md)
         if (row) j2_eval_warp_kernel<T, true, 1, 2, MODE><<<nbw, TPB, 0, s>>>(p, units);
-        else if constexpr (sizeof(T) == 4)
-            j2_eval_warp_kernel<T, false, QJ2_WARP_PF, QJ2_WARP_MINB, MODE><<<nbw, TPB, 0, s>>>(p, units);
-        else j2_eval_warp_kernel<T, false, 2, 2, MODE><<<nbw, TPB, 0, s>>>(p, units);
+        else if constexpr (sizeof(T) == 4) {
+            if (p.N_local >= 4 * 32 * Traits<T>::VW * ITERS)
+                j2_eval_warp_kernel<T, false, QJ2_WARP_PF, QJ2_WARP_MINB, MODE, true><<<nbw, TPB, 0, s>>>(p, units);
+            else
+                j2_eval_warp_kernel<T, false, QJ2_WARP_PF, QJ2_WARP_MINB, MODE><<<nbw, TPB, 0, s>>>(p, units);
+        } else if (p.N_local >= 4 * 32 * Traits<T>::VW * ITERS) {
+            j2_eval_warp_kernel<T, false, 2, 2, MODE, true><<<nbw, TPB, 0, s>>>(p, units);
+        } else {
+            j2_eval_warp_kernel<T, false, 2, 2, MODE><<<nbw, TPB, 0, s>>>(p, units);
+        }
         return cudaGetLastError();
     }
     const unsigned nb = (unsigned)nblocks;
