@@ -1442,7 +1442,7 @@ def plan_kernel_name(plan):
 
 def _plain_rel(gpu, orc, absout):
     """max |gpu - orc| / |orc| over components with |orc| >= 1e-3 A."""
-    m = np.abs(orc) >= 1e-3 * absout
+    m = (np.abs(orc) >= 1e-3 * absout) & (np.abs(orc) > 0)
     if not m.any():
         return None
     return float(np.max(np.abs(np.asarray(gpu, np.float64)[m] - orc[m]) / np.abs(orc[m])))

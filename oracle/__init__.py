@@ -214,7 +214,7 @@ def plain_relative_error(gpu, orc, absout, floor: float = 1e-3):
     out = []
     for c in range(orc.shape[-1]):
         o, a, x = orc[..., c], absout[..., c], g[..., c]
-        m = np.abs(o) >= floor * a
+        m = (np.abs(o) >= floor * a) & (np.abs(o) > 0)
         out.append(float(np.max(np.abs(x[m] - o[m]) / np.abs(o[m]))) if m.any() else None)
     return out
 

@@ -30,10 +30,14 @@
 
 namespace qj2 {
 
+#ifndef QJ2_WARP_SHORT_N
+#define QJ2_WARP_SHORT_N 2048  // rows this short take the warp kernel whatever W (A/B builds)
+#endif
+
 // Warp-per-walker mapping when a walker's slice is one CTA tile and there
 // are enough (walker, trial) units to fill the GPU (or the slice is tiny).
 inline bool use_warp_mapping(const EvalParams &p) {
-    return p.tiles_per_walker == 1 && (p.W * p.P >= 4096 || p.N_local <= 2048);
+    return p.tiles_per_walker == 1 && (p.W * p.P >= 4096 || p.N_local <= QJ2_WARP_SHORT_N);
 }
 
 template <typename T, int MODE>
