@@ -42,7 +42,9 @@ MUTANTS = {
                                "Dx[a] * By[b] * Dz[c] * sx * sy,             /* hxy */"),
     "det_ratio_laplacian_not_divided": ("out[4] = nsum_get(&Lp) / rho;", "out[4] = nsum_get(&Lp);"),
     "j1_species_functor": ("orc_bspline(coef + s * coef_stride, m[s], r_cut[s], rho, u);",
-                           "orc_bspline(coef, m[s], r_cut[s], rho, u);"),
+                           "orc_bspline(coef, m[s], r_cut[s], rho, u);", 0),
+    "sweep_j1_species_functor": ("orc_bspline(coef + s * coef_stride, m[s], r_cut[s], rho, u);",
+                                 "orc_bspline(coef, m[s], r_cut[s], rho, u);", 1),
     "sweep_ratio_sign": ("double dj = nsum_get(&Tk[0]) - Sw[k];", "double dj = Sw[k] - nsum_get(&Tk[0]);"),
     "sweep_decision_not_squared": ("J->u[sw] < rho * rho ? 1 : 0;", "J->u[sw] < rho ? 1 : 0;"),
     "sweep_commit_position": ("for (int c = 0; c < 3; ++c) Rw[c * Np + k] = rnf[c];", ""),
