@@ -481,6 +481,64 @@ __device__ __forceinline__ void write_out(const EvalParams &p, int64_t w, int32_
     }
 }
 
+// CTA reduction in fp64 (fixed order: deterministic), cross-tile partials
+// (the last CTA of (w, g) reduces them) and the physical write-out.  red:
+// [TPB/32][ND] shared doubles.
+template <int MODE>
+__device__ __forceinline__ void cta_reduce_write(const EvalParams &p, const double (&dacc)[ndacc<MODE>()], int64_t w,
+                                                 int32_t g, int64_t c, double *red, int *last_flag) {
+    constexpr int ND = ndacc<MODE>();
+    const int64_t tpw = p.tiles_per_walker;
+    QJ2_DCHECK(tpw == 1 || (p.partials != nullptr && p.counters != nullptr));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int a = 0; a < ND; ++a) {
+        const double v = warp_sum(dacc[a]);
+        if (lane == 0) red[warp * ND + a] = v;
+    }
+    __syncthreads();
+
+    double tot = 0.0;   // thread t < ND holds value t of this tile
+    if (threadIdx.x < ND) {
+#pragma unroll
+        for (int wi = 0; wi < TPB / 32; ++wi) tot += red[wi * ND + threadIdx.x];
+    }
+
+    const int64_t wg = w * p.P + g;
+    if (tpw > 1) {
+        // publish this tile's partials; the last CTA of (w, g) reduces them
+        double *part = p.partials + (wg * tpw + c) * ND;
+        if (threadIdx.x < ND) part[threadIdx.x] = tot;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned prev = atomicAdd(p.counters + wg, 1u);
+            *last_flag = (prev == (unsigned)(tpw - 1));
+        }
+        __syncthreads();
+        if (!*last_flag) return;
+        __threadfence();
+        // warp 0: value v summed over tiles, lane-strided then shuffle tree
+        if (warp == 0) {
+            const double *base = p.partials + wg * tpw * ND;
+            for (int v = 0; v < ND; ++v) {
+                double s = 0.0;
+                for (int64_t t = lane; t < tpw; t += 32) s += __ldcg(base + t * ND + v);
+                s = warp_sum(s);
+                if (lane == v) tot = s;      // lane v keeps value v (ND <= 6 < 32)
+            }
+        }
+    }
+
+    // ---- finalize: lane a < ND of warp 0 holds value a ----
+    if (warp == 0) {
+        double s[ND];
+#pragma unroll
+        for (int a = 0; a < ND; ++a) s[a] = __shfl_sync(0xffffffffu, tot, a);
+        if (lane == 0) write_out<MODE>(p, w, g, s);
+    }
+}
+
 // ===========================================================================
 // Long rows: one CTA per (walker, trial, tile of SUB sub-tiles).
 // PF: prefetch distance (vector groups in flight), MINB: resident CTAs per SM.
@@ -495,7 +553,7 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
     constexpr int CH = SCH * SUB;                 // tile handled by one CTA
     constexpr int ND = ndacc<MODE>();
     __shared__ Coef4<T> tab[MAXTAB];
-    __shared__ double red[TPB / 32][ND];
+    __shared__ double red[TPB / 32 * ND];
     __shared__ int last_flag;
 
     // tile decode: trial fastest, then tile, then walker, so the CTAs of one tile's
@@ -508,8 +566,7 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
     const uint32_t w32 = b / per_w;
     const uint32_t rem = b - w32 * per_w;
     const uint32_t c32 = rem / P32;
-    const int64_t tpw = p.tiles_per_walker;
-    const int64_t w = w32, c = c32;
+        const int64_t w = w32, c = c32;
     const int32_t g = (int32_t)(rem - c32 * P32);
 
     load_table<T>(p, tab);
@@ -522,7 +579,7 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
     const int64_t start = c * CH;
     const int64_t end = min(start + (int64_t)CH, p.N_local);
     // every vector this CTA loads (and row vector it stores) lies in [start, end) of lanes of Np
-    QJ2_DCHECK(w < p.W && g < p.P && c < tpw && start < end && end <= p.Np && p.N_local <= p.Np);
+    QJ2_DCHECK(w < p.W && g < p.P && c < p.tiles_per_walker && start < end && end <= p.Np && p.N_local <= p.Np);
     const T *Rw = static_cast<const T *>(p.R) + w * p.src_stride;
     const int64_t voff = (start >> (VW == 4 ? 2 : 1)) + threadIdx.x;   // this thread's first vector
     const V *px = reinterpret_cast<const V *>(Rw) + voff;
@@ -566,55 +623,7 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
         }
     }
 
-    // ---- CTA reduction in fp64 (fixed order: deterministic) ----
-    QJ2_DCHECK(tpw == 1 || (p.partials != nullptr && p.counters != nullptr));
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int a = 0; a < ND; ++a) {
-        const double v = warp_sum(dacc[a]);
-        if (lane == 0) red[warp][a] = v;
-    }
-    __syncthreads();
-
-    double tot = 0.0;   // thread t < ND holds value t of this tile
-    if (threadIdx.x < ND) {
-#pragma unroll
-        for (int wi = 0; wi < TPB / 32; ++wi) tot += red[wi][threadIdx.x];
-    }
-
-    const int64_t wg = w * p.P + g;
-    if (tpw > 1) {
-        // publish this tile's partials; the last CTA of (w, g) reduces them
-        double *part = p.partials + (wg * tpw + c) * ND;
-        if (threadIdx.x < ND) part[threadIdx.x] = tot;
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const unsigned prev = atomicAdd(p.counters + wg, 1u);
-            last_flag = (prev == (unsigned)(tpw - 1));
-        }
-        __syncthreads();
-        if (!last_flag) return;
-        __threadfence();
-        // warp 0: value v summed over tiles, lane-strided then shuffle tree
-        if (warp == 0) {
-            const double *base = p.partials + wg * tpw * ND;
-            for (int v = 0; v < ND; ++v) {
-                double s = 0.0;
-                for (int64_t t = lane; t < tpw; t += 32) s += __ldcg(base + t * ND + v);
-                s = warp_sum(s);
-                if (lane == v) tot = s;      // lane v keeps value v (ND <= 6 < 32)
-            }
-        }
-    }
-
-    // ---- finalize: lane a < ND of warp 0 holds value a ----
-    if (warp == 0) {
-        double s[ND];
-#pragma unroll
-        for (int a = 0; a < ND; ++a) s[a] = __shfl_sync(0xffffffffu, tot, a);
-        if (lane == 0) write_out<MODE>(p, w, g, s);
-    }
+    cta_reduce_write<MODE>(p, dacc, w, g, c, red, &last_flag);
 }
 
 // ===========================================================================

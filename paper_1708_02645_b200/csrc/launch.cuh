@@ -48,7 +48,7 @@ cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStre
             const int64_t units = p.W * p.P;
             const size_t smem = (size_t)p.N_local * 4 * sizeof(T);
             auto kern = j1_thread_kernel<T>;
-            if (smem > 48 * 1024) {
+            if (smem > 40 * 1024) {   // the static functor table (<= 2.2 KB) comes on top of the 48 KB default
                 cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 if (e != cudaSuccess) return e;
             }

@@ -14,9 +14,15 @@ namespace qj2 {
 //        256 x 4): the shared-memory layout, the partner bounds and every partner's spin
 //        half (j < SPT/2: up) are compile-time constants.
 // 128 threads at <= 72 registers: 7 CTAs per SM, 148 x 7 = 1036 walkers in one wave.
+#ifndef QJ2_SWEEP_TPB64
+#define QJ2_SWEEP_TPB64 0           // A/B: 64 threads x 12 partners per walker for 384 < N <= 768
+#endif
+#ifndef QJ2_SWEEP_MINB64
+#define QJ2_SWEEP_MINB64 7
+#endif
 template <int TPB, int SPT, bool J1>
 constexpr int sweep_minb() {
-    return TPB == 128 ? (SPT <= 6 ? 7 : 4) : (SPT <= 3 ? (J1 ? 3 : 4) : 2);
+    return TPB == 64 ? QJ2_SWEEP_MINB64 : TPB == 128 ? (SPT <= 6 ? 7 : 4) : (SPT <= 3 ? (J1 ? 3 : 4) : 2);
 }
 
 // The proposal of Alg. 1 L5 without drift (reading R24): r + delta in fp32, wrapped
@@ -460,13 +466,19 @@ cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s) {
     const size_t smem = (size_t)8 * p.N * sizeof(float) + table_smem(p, j1);   // R (3) + state (5) per electron
     // 128 threads per walker for 384 < N <= 768 (7 CTAs/SM), else 256 (64 and 96 threads
     // per walker were measured too: profiles/r01_s4/ab_tpb.log)
-    const int tpb = (p.N > 384 && p.N <= 768) ? 128 : SW_TPB;
+    const int tpb = (p.N > 384 && p.N <= 768) ? (QJ2_SWEEP_TPB64 ? 64 : 128) : SW_TPB;
     const int spt = (p.N + tpb - 1) / tpb;
     // compile-time layout where N fills the threads exactly and splits evenly into spin halves
     const bool full = p.N == tpb * spt && 2 * p.N_up == p.N && spt % 2 == 0;
 #define QJ2_SWEEP_LAUNCH(T_, S_, F_)                                                         \
     (j1 ? (j2_sweep_kernel<T_, S_, true, F_><<<(unsigned)p.W, T_, smem, s>>>(p), 0)           \
         : (j2_sweep_kernel<T_, S_, false, F_><<<(unsigned)p.W, T_, smem, s>>>(p), 0))
+#if QJ2_SWEEP_TPB64
+    if (tpb == 64) {
+        if (full && spt == 12) QJ2_SWEEP_LAUNCH(64, 12, true);
+        else QJ2_SWEEP_LAUNCH(64, 12, false);
+    } else
+#endif
     if (tpb == 128) {
         switch (spt) {
             case 1: case 2: case 3: case 4: QJ2_SWEEP_LAUNCH(128, 4, false); break;

@@ -102,10 +102,11 @@ def test_j1_validation(q):
 # Small ion sets: the thread-per-(walker, trial) kernel (ions in shared memory)
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-@pytest.mark.parametrize("n_ions,S", [(64, 2), (33, 3), (4096, 4)])
+@pytest.mark.parametrize("n_ions,S", [(64, 2), (33, 3), (1500, 2), (4096, 4)])
 def test_j1_thread_kernel_many_walkers(q, dtype, n_ions, S):
-    """NiO-64-sized ion sets (64 ions, Ni and O) and the largest staged set,
-    many walkers; sampled walkers vs the oracle."""
+    """NiO-64-sized ion sets (64 ions, Ni and O), a set whose staged ions plus
+    the static functor table just pass the 48 KB default (1500 fp64 ions), and
+    the largest staged set, many walkers; sampled walkers vs the oracle."""
     ions, start, rt, fn1 = j1_case(n_ions, 20000, seed=900 + n_ions, dtype=dtype, S=S)
     check(q, ions, start, rt, fn1, dtype, sample=np.r_[0:40, 19990:20000])
 
