@@ -215,11 +215,12 @@ def committed_traffic(config_name: str):
 FLOPS_PER_TERM = 36       # algorithmic flops of one functor term (FMA = 2 flops)
 
 
-def alu_roofline(cfg_name, kernel, kms, terms, fp64=False, extra=None):
+def alu_roofline(cfg_name, kernel, kms, terms, fp64=False, extra=None, thread_inst=None):
     """Roofline of an issue/ALU-bound kernel: algorithmic flops (36 per functor term,
     FMA = 2) per launch / launch time against the measured FP32 (or FP64) FMA peak;
     beside it the issue fraction: the kernel's thread instructions per launch (the
-    committed ncu record) / launch time against the measured issue rate."""
+    committed ncu record, or thread_inst = (count, how) derived from it by the
+    caller) / launch time against the measured issue rate."""
     pk = alu_peaks()
     flops = terms * FLOPS_PER_TERM
     achieved = flops / (kms / 1e3) / 1e12
@@ -234,11 +235,11 @@ def alu_roofline(cfg_name, kernel, kms, terms, fp64=False, extra=None):
          "traffic": committed_traffic(cfg_name), "kernel": kernel, "kernel_ms": kms, "alg_flops_per_launch": flops,
          "flops_per_term": FLOPS_PER_TERM, "terms_per_launch": terms, "peak_source": src}
     rec = kernel_record(cfg_name)
-    if pk and rec.get("thread_inst_per_launch"):
-        ti = rec["thread_inst_per_launch"]
+    if pk and (thread_inst or rec.get("thread_inst_per_launch")):
+        ti, how = thread_inst or (rec["thread_inst_per_launch"], rec.get("source"))
         r["issue"] = {"thread_inst_per_launch": ti, "sass_per_term": ti / terms,
                       "achieved_tinst_per_s": ti / (kms / 1e3) / 1e12, "peak_tinst_per_s": pk["issue_tinst_per_s"],
-                      "frac": ti / (kms / 1e3) / 1e12 / pk["issue_tinst_per_s"], "source": rec.get("source")}
+                      "frac": ti / (kms / 1e3) / 1e12 / pk["issue_tinst_per_s"], "source": how}
     if extra:
         r.update(extra)
     return r
@@ -1223,10 +1224,22 @@ class GraphSweepPlan(SweepPlan):
         acc = (self.acc_all == 1).float().mean().item()    # acceptance of the last timed sweep
         # functor terms per move: N - 1 at r'_k, N - 1 more at r_k when accepted; J1: 2 per ion
         terms = self.S * cfg.W * ((cfg.N - 1) * (1.0 + acc) + (2 * self.N_IONS if self.with_j1 else 0))
+        # the ncu-captured launch sits at another point of the chain (another acceptance): its
+        # instructions split into a per-move and a per-accepted-move part (tools/sweep_model.py)
+        # give this launch's count
+        sm = kernel_record(self.mode).get("sweep_model")
+        ti = None
+        if sm:
+            per_mp = sm["per_move_partner"] + acc * sm["per_accepted_move_partner"]
+            ti = (self.S * cfg.W * cfg.N * per_mp,
+                  f"ncu SASS source page split into per-move ({sm['per_move_partner']:.1f}) and per-accepted-move "
+                  f"({sm['per_accepted_move_partner']:.1f}) thread instructions per (move, partner) "
+                  f"(tools/sweep_model.py, profiles/r02/ncu_{self.mode}.json, captured at acceptance "
+                  f"{sm['acceptance_captured']:.3f}), at this launch's acceptance: {per_mp:.1f}")
         return alu_roofline(self.mode, "j2_sweep_kernel (one launch per sweep, walkers resident in shared memory"
                             + (", J1 over 64 ions in every move)" if self.with_j1 else ")"), kms, terms,
                             extra={"acceptance": acc, "per_move_launches_eager_ms": self.eager_ms,
-                                   "per_move_launches_graph_ms": self.graph_ms})
+                                   "per_move_launches_graph_ms": self.graph_ms}, thread_inst=ti)
 
 
 class SpoPlan:

@@ -6,23 +6,23 @@
 namespace qj2 {
 
 // Template parameters of the sweep kernel:
-//   TPB  threads per walker (one CTA per walker): 128 for 384 < N <= 768, else 256;
-//   SPT  partners per thread, ceil(N / TPB); the five pair terms at r'_k are kept
-//        per partner between the ratio and the update;
+//   TPB  threads per walker (one CTA per walker): 64 for N <= 768, else 128;
+//   SPT  partners per thread (a tier >= ceil(N / TPB)); the five pair terms at r'_k are
+//        kept per partner between the ratio and the update;
 //   J1   the one-body Jastrow over the (<= 256) ions joins each move's ratio;
-//   FULL N == TPB * SPT with N_up = N / 2 and SPT even (NiO-64's 768 = 128 x 6, 1024 =
-//        256 x 4): the shared-memory layout, the partner bounds and every partner's spin
+//   FULL N == TPB * SPT with N_up = N / 2 and SPT even (NiO-64's 768 = 64 x 12, 1024 =
+//        128 x 8): the shared-memory layout, the partner bounds and every partner's spin
 //        half (j < SPT/2: up) are compile-time constants.
-// 128 threads at <= 72 registers: 7 CTAs per SM, 148 x 7 = 1036 walkers in one wave.
-#ifndef QJ2_SWEEP_TPB64
-#define QJ2_SWEEP_TPB64 0           // A/B: 64 threads x 12 partners per walker for 384 < N <= 768
-#endif
-#ifndef QJ2_SWEEP_MINB64
-#define QJ2_SWEEP_MINB64 7
-#endif
+// NiO-64: 64 threads x 12 partners at <= 128 registers, 7 CTAs per SM, 148 x 7 = 1036
+// walkers in one wave.
+// Threads x partners per walker: 64 x 4 / 6 / 8 / 10 / 12 for N <= 768 (two warps per walker:
+// the per-move work -- proposal, axes, reduction, decision -- is shared by 4-12 partners per
+// thread), 128 x 8 for 768 < N <= 1024.  Resident CTAs per SM so that the register file holds
+// the SPT x 5 pair terms kept between the ratio and the update.
 template <int TPB, int SPT, bool J1>
 constexpr int sweep_minb() {
-    return TPB == 64 ? QJ2_SWEEP_MINB64 : TPB == 128 ? (SPT <= 6 ? 7 : 4) : (SPT <= 3 ? (J1 ? 3 : 4) : 2);
+    if (TPB == 64) return SPT <= 4 ? 12 : SPT <= 8 ? 10 : SPT <= 10 ? 8 : (J1 ? 8 : 7);
+    return 5;   // 128 x 8
 }
 
 // The proposal of Alg. 1 L5 without drift (reading R24): r + delta in fp32, wrapped
@@ -225,12 +225,14 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
         }
         // 2. block reduction, fixed order: a reduce-scatter across the warp (8 or 16
         //    slots for 5 or 11 values: one shuffle per slot and level instead of one
-        //    per value), one partial per value and warp in shared memory.  Levels 1-2
-        //    (lanes 16 and 8 apart) add in fp32 -- partials of <= 4 lanes x SPT terms,
-        //    the eval kernel's fp32 partials of <= 32 terms -- the rest in fp64.
+        //    per value), one partial per value and warp in shared memory.  The first FL
+        //    levels add in fp32 -- partials of <= 2^FL lanes x SPT <= 32 terms, the eval
+        //    kernel's fp32 partial rule -- the rest in fp64.
         {
             constexpr int NS = J1 ? 16 : 8;
             constexpr int OREM = J1 ? 1 : 2;        // lanes below this distance hold copies of one slot
+            constexpr int FL = 4 * SPT <= 32 ? 2 : 1;
+            static_assert((1 << FL) * SPT <= 32, "fp32 partials of at most 32 terms");
             float vf[NS];
 #pragma unroll
             for (int c = 0; c < 5; ++c) {
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
             for (int c = NV; c < NS; ++c) vf[c] = 0.f;
             int slot = 0;
 #pragma unroll
-            for (int h = NS / 2, o = 16; o >= 8; h >>= 1, o >>= 1) {
+            for (int l = 0, h = NS / 2, o = 16; l < FL; ++l, h >>= 1, o >>= 1) {
                 const bool up = lane & o;           // this lane keeps the upper half of the slots
 #pragma unroll
                 for (int j = 0; j < h; ++j) {
@@ -252,11 +254,12 @@ __global__ void __launch_bounds__(TPB, sweep_minb<TPB, SPT, J1>()) j2_sweep_kern
                 }
                 slot += up ? h : 0;
             }
-            double v[NS / 4];
+            constexpr int NF = NS >> FL;            // slots left for the fp64 levels
+            double v[NF];
 #pragma unroll
-            for (int j = 0; j < NS / 4; ++j) v[j] = (double)vf[j];
+            for (int j = 0; j < NF; ++j) v[j] = (double)vf[j];
 #pragma unroll
-            for (int h = NS / 8, o = 4; h >= 1; h >>= 1, o >>= 1) {
+            for (int h = NF / 2, o = 16 >> FL; h >= 1; h >>= 1, o >>= 1) {
                 const bool up = lane & o;
 #pragma unroll
                 for (int j = 0; j < h; ++j) {
@@ -464,41 +467,23 @@ static size_t table_smem(const SweepParams &p, bool j1) {
 cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s) {
     const bool j1 = p.n_ions > 0;
     const size_t smem = (size_t)8 * p.N * sizeof(float) + table_smem(p, j1);   // R (3) + state (5) per electron
-    // 128 threads per walker for 384 < N <= 768 (7 CTAs/SM), else 256 (64 and 96 threads
-    // per walker were measured too: profiles/r01_s4/ab_tpb.log)
-    const int tpb = (p.N > 384 && p.N <= 768) ? (QJ2_SWEEP_TPB64 ? 64 : 128) : SW_TPB;
-    const int spt = (p.N + tpb - 1) / tpb;
-    // compile-time layout where N fills the threads exactly and splits evenly into spin halves
-    const bool full = p.N == tpb * spt && 2 * p.N_up == p.N && spt % 2 == 0;
 #define QJ2_SWEEP_LAUNCH(T_, S_, F_)                                                         \
     (j1 ? (j2_sweep_kernel<T_, S_, true, F_><<<(unsigned)p.W, T_, smem, s>>>(p), 0)           \
         : (j2_sweep_kernel<T_, S_, false, F_><<<(unsigned)p.W, T_, smem, s>>>(p), 0))
-#if QJ2_SWEEP_TPB64
-    if (tpb == 64) {
-        if (full && spt == 12) QJ2_SWEEP_LAUNCH(64, 12, true);
-        else QJ2_SWEEP_LAUNCH(64, 12, false);
-    } else
-#endif
-    if (tpb == 128) {
-        switch (spt) {
-            case 1: case 2: case 3: case 4: QJ2_SWEEP_LAUNCH(128, 4, false); break;
-            case 5: QJ2_SWEEP_LAUNCH(128, 5, false); break;
-            default:
-                if (full) QJ2_SWEEP_LAUNCH(128, 6, true);
-                else QJ2_SWEEP_LAUNCH(128, 6, false);
-                break;
-        }
-    } else {
-        switch (spt) {
-            case 1: QJ2_SWEEP_LAUNCH(256, 1, false); break;
-            case 2: QJ2_SWEEP_LAUNCH(256, 2, false); break;
-            case 3: QJ2_SWEEP_LAUNCH(256, 3, false); break;
-            default:
-                if (full) QJ2_SWEEP_LAUNCH(256, 4, true);
-                else QJ2_SWEEP_LAUNCH(256, 4, false);
-                break;
-        }
-    }
+    // the same-spin halves as compile-time partner ranges when N fills the threads exactly
+    // (NiO-64's 768 = 64 x 12, 1024 = 128 x 8, ...); a tier's unused partner slots are masked
+    // (tiers every 128 electrons: at most 1/6 of the slots idle above N = 256; the tiers against
+    // the round-1 ones (128 x 4-6, 256 x 1-4): profiles/r02/ab_results.txt)
+    auto is_full = [&](int tpb, int spt) { return p.N == tpb * spt && 2 * p.N_up == p.N && spt % 2 == 0; };
+#define QJ2_SWEEP_TIER(T_, S_) \
+    if (is_full(T_, S_)) QJ2_SWEEP_LAUNCH(T_, S_, true); else QJ2_SWEEP_LAUNCH(T_, S_, false)
+    if (p.N <= 256) { QJ2_SWEEP_TIER(64, 4); }
+    else if (p.N <= 384) { QJ2_SWEEP_TIER(64, 6); }
+    else if (p.N <= 512) { QJ2_SWEEP_TIER(64, 8); }
+    else if (p.N <= 640) { QJ2_SWEEP_TIER(64, 10); }
+    else if (p.N <= 768) { QJ2_SWEEP_TIER(64, 12); }
+    else { QJ2_SWEEP_TIER(128, 8); }
+#undef QJ2_SWEEP_TIER
 #undef QJ2_SWEEP_LAUNCH
     return cudaGetLastError();
 }

@@ -11,7 +11,7 @@
 //      terms T_i(r'_k) with the eval kernel's fp32 arithmetic (single-rounding
 //      minimum image, power-basis Horner), keeps them in registers and sums
 //      them: the sums are U^2_k(R') and its gradient / Laplacian (Alg. 1 L7-L8);
-//   2. a fixed-order reduce-scatter (fp32 for lanes 16 and 8 apart, then fp64)
+//   2. a fixed-order reduce-scatter (fp32 partials of <= 32 terms, then fp64)
 //      and ONE barrier;
 //   3. dJ2 = U^2_k(R') - U^2_k(R), with U^2_k(R) the electron's entry of the 5N
 //      state (the state is kept so the ratio reuses it; the
@@ -31,9 +31,7 @@
 
 namespace qj2 {
 
-constexpr int SW_TPB = 256;       // threads per walker (CTA) outside 384 < N <= 768
-constexpr int SW_SPT = 4;         // partners per thread: N <= SW_TPB * SW_SPT
-constexpr int SW_MAXN = SW_TPB * SW_SPT;
+constexpr int SW_MAXN = 1024;     // electrons per walker (the largest tier: 128 threads x 8 partners)
 
 struct SweepParams {
     int32_t W, N, N_up, m;
@@ -63,7 +61,7 @@ struct SweepParams {
     double pcoef1[QJ2_MAX_SPECIES * (QJ2_MAX_M + 1)][4];
 };
 
-constexpr int SW_MAX_IONS = SW_TPB;      // at most two ions per thread in the J1 part of a move
+constexpr int SW_MAX_IONS = 256;         // ions of the J1 part of a move (2-4 per thread)
 
 cudaError_t launch_sweep(const SweepParams &p, cudaStream_t s);
 // The 5N state (and, with ions, the J1 rows) of every electron from scratch

@@ -75,7 +75,7 @@ def test_state_init_j1_rows_vs_oracle(q):
         assert err <= 1e-5
 
 
-@pytest.mark.parametrize("N", [2, 33, 256, 385, 600, 768, 1024])   # 256 threads x 1-4, 128 threads x 4-6 partners
+@pytest.mark.parametrize("N", [2, 33, 256, 300, 385, 512, 600, 640, 768, 1000, 1024])   # every tier, full and ragged
 def test_sweep_one_sweep_vs_oracle(q, N):
     """One ordered sweep (N moves) in one launch from the from-scratch state."""
     W = 12

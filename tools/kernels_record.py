@@ -5,7 +5,12 @@ into profiles/r02_kernels.json, the record bench.py reads for `roofline.traffic`
 (thread-instruction slots per launch = 32 x warp instructions, the unit of the
 measured issue rate in profiles/r02_alu_peaks.json).
 
-    python tools/kernels_record.py [gpurun_out/ncu_r02] [profiles/r02_kernels.json]
+    python tools/kernels_record.py [gpurun_out/ncu_r02] [profiles/r02_kernels.json] [--only=C3,N64S]
+
+With --only the named configurations' entries are replaced and the others kept.
+The sweep configurations (N64S, N64SJ) also get their `sweep_model`
+(tools/sweep_model.py) from the trimmed SASS source page <config>_source_trim.csv
+when it is there.
 """
 import json
 import os
@@ -21,14 +26,22 @@ def num(v):
     return x * UNITS.get(m.group(2), 1)
 
 
+SWEEPS = {"N64S": (1024, 768, 768), "N64SJ": (1024, 768, 768)}   # W, S, N of the bench launch
+
+
 def main():
-    src = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/ncu_r02"
-    out = sys.argv[2] if len(sys.argv) > 2 else "profiles/r02_kernels.json"
-    rec = {}
+    args = [a for a in sys.argv[1:] if not a.startswith("--only")]
+    only = [a.split("=", 1)[1].split(",") for a in sys.argv[1:] if a.startswith("--only=")]
+    only = set(only[0]) if only else None
+    src = args[0] if len(args) > 0 else "gpurun_out/ncu_r02"
+    out = args[1] if len(args) > 1 else "profiles/r02_kernels.json"
+    rec = json.load(open(out)) if only and os.path.exists(out) else {}
     for f in sorted(os.listdir(src)):
         if not f.endswith(".json"):
             continue
         cfg = f[:-5]
+        if only is not None and cfg not in only:
+            continue
         d = json.load(open(os.path.join(src, f)))
         if not d:
             continue
@@ -51,6 +64,14 @@ def main():
             "source": f"profiles/r02/ncu_{cfg}.json (ncu --set full --clock-control none, one launch of "
                       f"bench.py --config {cfg} --steps 4 --warmup 3)",
         }
+        trim = os.path.join(src, f"{cfg}_source_trim.csv")
+        if cfg in SWEEPS and os.path.exists(trim):
+            sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+            from sweep_model import model
+            m = model(trim, *SWEEPS[cfg])
+            m.pop("kernel")
+            m["source"] = f"profiles/r02/ncu_{cfg}_source.csv"
+            rec[cfg]["sweep_model"] = m
     json.dump(rec, open(out, "w"), indent=1)
     for c, r in rec.items():
         print(f"{c:6s} {r['ncu_time_s'] * 1e3:8.3f} ms  dram {r['dram_bytes_per_launch'] / 1e9:8.3f} GB  "
