@@ -137,12 +137,13 @@ def test_sweep_out_of_range_k(q):
             assert acc[s_, w_] == -1 and dj[s_, w_] == 0.0
 
 
-@pytest.mark.parametrize("n_ions,S,N", [(64, 2, 200), (37, 3, 200), (256, 1, 200), (256, 2, 520), (64, 2, 768),
-                                         (100, 2, 1024)])
+@pytest.mark.parametrize("n_ions,S,N", [(64, 2, 200), (37, 3, 200), (256, 1, 200), (64, 2, 300), (256, 3, 450),
+                                         (256, 2, 520), (64, 2, 640), (64, 2, 768), (100, 2, 1000), (100, 2, 1024)])
 def test_sweep_with_j1_vs_oracle(q, n_ions, S, N):
     """J1 joined to every move: dJ = dJ2 + dJ1, the J1 rows of accepted electrons
-    (two sweeps, random order).  N = 520 and 768 run 128 threads per walker (256
-    ions: two per thread); 768 and 1024 fill the threads exactly."""
+    (two sweeps, random order), in every thread x partner tier (64 x 4 / 6 / 8 /
+    10 / 12, 128 x 8; 256 ions: four per thread at 64 threads); 640, 768 and 1024
+    fill the threads exactly."""
     W = 8
     R, fn, L, Np, n_up = _system(N, W, 300 + n_ions)
     ions, start = qmcgen.make_ions(300 + n_ions, n_ions, qmcgen.padded_size(n_ions, 4), L, np.float32, n_species=S)

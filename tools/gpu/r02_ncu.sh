@@ -5,7 +5,9 @@ python -c "import __graft_entry__ as g; g.build()" > gpurun_out/ncu_r02/build.lo
 if [ -z "$SKIP_LAUNCHES" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/ncu_r02/launches_C3.csv \
   python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "launches C3 rc $?"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/ncu_r02/launches_N64S.csv \
+# N64S: the timed region only (its prepare() times 1536 per-move launches for context first)
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed 3 steps/" --csv \
+  --log-file gpurun_out/ncu_r02/launches_N64S.csv \
   python bench.py --config N64S --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "launches N64S rc $?"
 fi
 cap() {  # config kernel-regex skip

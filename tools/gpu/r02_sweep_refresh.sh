@@ -10,6 +10,7 @@ done
 SKIP_LAUNCHES=1 KEEP_SRC="N64S N64SJ" CAPS="N64S:j2_sweep N64SJ:j2_sweep" bash tools/gpu/r02_ncu.sh
 python tools/kernels_record.py gpurun_out/ncu_r02 profiles/r02_kernels.json --only=N64S,N64SJ
 SKIP_ALU=1 CFGS="N64S N64SJ" bash tools/gpu/r02_bench_all.sh
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/ncu_r02/launches_N64S.csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed 3 steps/" --csv \
+  --log-file gpurun_out/ncu_r02/launches_N64S.csv \
   python bench.py --config N64S --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "launches N64S rc $?"
 rm -f gpurun_out/ncu_r02/N64S_source.csv gpurun_out/ncu_r02/N64SJ_source.csv
