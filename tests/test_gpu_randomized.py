@@ -49,9 +49,11 @@ def _accept_cases(n=25, seed=2025):
             for _ in range(n)]
 
 
-def _sweep_cases(n=12, seed=2026):
+def _sweep_cases(n=24, seed=2026):
+    # N: log-uniform (small systems) or uniform (every thread x partner tier up to 1024)
     rng = np.random.default_rng(seed)
-    return [dict(N=max(2, _log_uniform(rng, 2, 1024)), W=int(rng.integers(1, 6)), m=int(rng.integers(4, 17)),
+    return [dict(N=max(2, _log_uniform(rng, 2, 1024) if rng.random() < 0.5 else int(rng.integers(2, 1025))),
+                 W=int(rng.integers(1, 6)), m=int(rng.integers(4, 17)),
                  seed=int(rng.integers(2**31)), up_frac=float(rng.choice([0.0, 1.0, rng.random(), 0.5])),
                  moves=int(rng.integers(1, 257)))
             for _ in range(n)]
