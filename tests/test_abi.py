@@ -123,6 +123,20 @@ def test_package_has_no_cpu_fallback():
                 assert "liboracle" not in txt, fn
 
 
+def test_no_runtime_switches_in_the_product():
+    """Kernel variants are chosen from the arguments alone: no source of the
+    library reads the environment (the measured alternatives are compile-time
+    A/B builds, tools/ab), and the binding reads only QJ2_LIB (which library
+    file to load)."""
+    import re
+    csrc = os.path.join(ROOT, "paper_1708_02645_b200", "csrc")
+    for fn in os.listdir(csrc):
+        if fn.endswith((".cu", ".cuh", ".h", ".cpp")):
+            assert "getenv" not in open(os.path.join(csrc, fn)).read(), fn
+    txt = open(os.path.join(ROOT, "paper_1708_02645_b200", "__init__.py")).read()
+    assert set(re.findall(r"environ(?:\.get)?\(?\[?[\"']([A-Z0-9_]+)", txt)) <= {"QJ2_LIB"}
+
+
 def test_oracle_is_independent_of_the_product():
     """The oracle imports nothing from the product package, includes none of its
     headers, and the product's binding, kernels and bench timing path never
