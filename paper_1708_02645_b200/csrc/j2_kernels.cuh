@@ -451,6 +451,24 @@ __device__ __forceinline__ void j2_sub_tile32(int tid, const EvalParams &p, int 
     flush<T, MODE_J2>(acc, dacc, gc.sg, gc.sh, gc.ss);      // J2: raw sums (one delta for both groups)
 }
 
+// L2 prefetch of a contiguous byte range by the TMA engine (no registers, no
+// completion to wait for): the loads of a later sub-tile then hit L2.
+__device__ __forceinline__ void l2_prefetch(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// CTA kernel, J2: how many sub-tiles ahead the TMA engine prefetches into L2 (0: none).
+// fp64: one (C3f64 2.78 -> 2.51 ms per step: the register pipeline holds only two
+// vector groups per thread at 2 CTAs/SM, the prefetch turns its loads into L2 hits);
+// fp32: none (its 3 CTAs/SM already keep the HBM busy; the prefetch costs 10-20%:
+// profiles/r02/ab_results.txt).  A/B builds: -DQJ2_L2PF64=n / -DQJ2_L2PF32=n.
+#ifndef QJ2_L2PF64
+#define QJ2_L2PF64 1
+#endif
+#ifndef QJ2_L2PF32
+#define QJ2_L2PF32 0
+#endif
+
 // Per-walker setup shared by the CTA and warp kernels.
 template <typename T, int MODE>
 __device__ __forceinline__ void walker_setup(const EvalParams &p, int64_t w, int32_t g, Trial<T> &tr, int &kg,
@@ -603,10 +621,24 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
         const int32_t up_t = up64 <= 0 ? 0 : (up64 >= tlen ? tlen : (int32_t)up64);
         const GroupC<T> g_up = group_consts<T, MODE>(p, 0, kg, tab_addr);
         const GroupC<T> g_dn = group_consts<T, MODE>(p, 1, kg, tab_addr);
+        constexpr int L2PF = sizeof(T) == 8 ? QJ2_L2PF64 : QJ2_L2PF32;
+        // one thread asks the TMA engine for sub-tile s + L2PF of the three streams while
+        // sub-tile s is loaded (sizes rounded up to 16 B stay inside the Np-padded rows)
+        auto prefetch_sub = [&](int sp) {
+            const int32_t a = sp * SCH;
+            if (threadIdx.x == 0 && sp < SUB && a < tlen) {
+                const uint32_t bytes = (uint32_t)((min(SCH, tlen - a) * (int)sizeof(T) + 15) & ~15);
+#pragma unroll
+                for (int d = 0; d < 3; ++d) l2_prefetch(Rw + d * p.Np + start + a, bytes);
+            }
+        };
+#pragma unroll
+        for (int sp = 1; sp < L2PF; ++sp) prefetch_sub(sp);
 #pragma unroll 1
         for (int sidx = 0; sidx < SUB; ++sidx) {
             const int32_t s0 = sidx * SCH;
             if (s0 >= tlen) break;
+            if constexpr (L2PF > 0) prefetch_sub(sidx + L2PF);
             const int64_t vs = (int64_t)sidx * (SCH / VW);
             j2_sub_tile32<T, ROW, PF, TPB>(threadIdx.x, p, kg, tab_addr, s0, tlen, k_t, up_t, g_up, g_dn, px + vs,
                                            py + vs, pz + vs, tr, dacc, ROW ? rowp + vs : nullptr, row_stride);
