@@ -30,6 +30,19 @@
 
 namespace qj2 {
 
+// Warp kernel, rows of < 4 sub-tiles (C1, C2, C2f64): every vector group of a sub-tile is loaded
+// up front (PF = ITERS = 8, ~210 registers, 1 CTA/SM), so a walker's row costs one DRAM round
+// trip per sub-tile instead of one per three groups: C1 10.5 -> 9.5 us, C2f64 23.4 -> 20.0 us,
+// C2 unchanged (profiles/r02/ab_results.txt).  A/B builds: -DQJ2_WARP_SHORT_PF=n etc.
+#ifndef QJ2_WARP_SHORT_PF
+#define QJ2_WARP_SHORT_PF 8
+#endif
+#ifndef QJ2_WARP_SHORT_PF64
+#define QJ2_WARP_SHORT_PF64 8
+#endif
+#ifndef QJ2_WARP_SHORT_MINB
+#define QJ2_WARP_SHORT_MINB 1
+#endif
 #ifndef QJ2_WARP_SHORT_N
 #define QJ2_WARP_SHORT_N 2048  // rows this short take the warp kernel whatever W (A/B builds)
 #endif
@@ -67,11 +80,11 @@ cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStre
             if (p.N_local >= 4 * 32 * Traits<T>::VW * ITERS)
                 j2_eval_warp_kernel<T, false, QJ2_WARP_PF, QJ2_WARP_MINB, MODE, true><<<nbw, TPB, 0, s>>>(p, units);
             else
-                j2_eval_warp_kernel<T, false, QJ2_WARP_PF, QJ2_WARP_MINB, MODE><<<nbw, TPB, 0, s>>>(p, units);
+                j2_eval_warp_kernel<T, false, QJ2_WARP_SHORT_PF, QJ2_WARP_SHORT_MINB, MODE><<<nbw, TPB, 0, s>>>(p, units);
         } else if (p.N_local >= 4 * 32 * Traits<T>::VW * ITERS) {
             j2_eval_warp_kernel<T, false, 2, 2, MODE, true><<<nbw, TPB, 0, s>>>(p, units);
         } else {
-            j2_eval_warp_kernel<T, false, 2, 2, MODE><<<nbw, TPB, 0, s>>>(p, units);
+            j2_eval_warp_kernel<T, false, QJ2_WARP_SHORT_PF64, QJ2_WARP_SHORT_MINB, MODE><<<nbw, TPB, 0, s>>>(p, units);
         }
         return cudaGetLastError();
     }
