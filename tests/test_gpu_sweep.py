@@ -124,7 +124,7 @@ def test_sweep_spin_boundaries(q, n_up_case):
 def test_sweep_out_of_range_k(q):
     """A move whose k is outside [0, N) is never accepted, flagged -1, dj 0; the
     walker's other moves go on as the oracle says; padding is untouched."""
-    for N in (130, 600, 768):          # 256 threads, 128 threads, compile-time layout
+    for N in (130, 600, 768):          # 64 x 4, 64 x 10, 64 x 12 with the compile-time layout
         W = 6
         R, fn, L, Np, n_up = _system(N, W, 120 + N)
         ks, delta, u = qmcgen.make_sweep_moves(120 + N, W, N, N)
@@ -135,6 +135,22 @@ def test_sweep_out_of_range_k(q):
         acc, dj = check_sweep(q, R, state, ks, delta, u, fn, N, n_up)
         for s_, w_ in [(3, 2), (7, 4), (11, 0), (12, 5), (0, 1)]:
             assert acc[s_, w_] == -1 and dj[s_, w_] == 0.0
+
+
+def test_sweep_and_state_init_empty_calls(q):
+    """W = 0 walkers or S = 0 moves: no launch, nothing touched, status OK."""
+    N, W = 100, 3
+    R, fn, L, Np, n_up = _system(N, W, 7)
+    Rd, Sd = dev(R), torch.full((W, 5, Np), 2.5, dtype=torch.float32, device="cuda")
+    ks, delta, u = qmcgen.make_sweep_moves(7, W, N, 0)
+    q.sweep(Rd, Sd, dev(ks), dev(delta), dev(u), fn, N, n_up)                      # S = 0
+    assert torch.equal(Rd.cpu(), torch.from_numpy(R)) and bool((Sd == 2.5).all())
+    R0 = torch.zeros((0, 3, Np), dtype=torch.float32, device="cuda")
+    S0 = torch.zeros((0, 5, Np), dtype=torch.float32, device="cuda")
+    ks0, d0, u0 = qmcgen.make_sweep_moves(7, 0, N, 4)
+    q.sweep(R0, S0, dev(ks0), dev(d0), dev(u0), fn, N, n_up)                        # W = 0
+    q.state_init(R0, S0, fn, N, n_up)
+    torch.cuda.synchronize()
 
 
 @pytest.mark.parametrize("n_ions,S,N", [(64, 2, 200), (37, 3, 200), (256, 1, 200), (64, 2, 300), (256, 3, 450),
