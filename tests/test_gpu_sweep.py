@@ -13,7 +13,7 @@ import torch
 
 import oracle
 import qmcgen
-from sweep_check import THREADS, check_sweep, dev
+from sweep_check import check_sweep, dev
 
 pytestmark = pytest.mark.gpu
 
