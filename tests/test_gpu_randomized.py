@@ -21,6 +21,9 @@ from sweep_check import check_sweep
 pytestmark = pytest.mark.gpu
 
 TOL = {np.float32: 1e-5, np.float64: 1e-12}
+# QJ2_RANDOM_SHIFT=n draws another reproducible set of cases (extended campaigns,
+# tools/gpu/r02_random_campaign.sh); the suite itself runs shift 0
+SEED_SHIFT = 1000 * int(os.environ.get("QJ2_RANDOM_SHIFT", "0"))
 THREADS = os.cpu_count() or 1
 
 
@@ -29,7 +32,7 @@ def _log_uniform(rng, lo, hi):
 
 
 def _eval_cases(n=40, seed=2024):
-    rng = np.random.default_rng(seed)
+    rng = np.random.default_rng(seed + SEED_SHIFT)
     cases = []
     for _ in range(n):
         N = max(2, _log_uniform(rng, 2, 450000))
@@ -42,7 +45,7 @@ def _eval_cases(n=40, seed=2024):
 
 
 def _accept_cases(n=25, seed=2025):
-    rng = np.random.default_rng(seed)
+    rng = np.random.default_rng(seed + SEED_SHIFT)
     return [dict(N=max(2, _log_uniform(rng, 2, 30000)), W=int(rng.integers(1, 9)), m=int(rng.integers(4, 65)),
                  f64=bool(rng.random() < 0.4), seed=int(rng.integers(2**31)),
                  up_frac=float(rng.choice([0.0, 1.0, rng.random(), 0.5])), p_acc=float(rng.random()))
@@ -51,7 +54,7 @@ def _accept_cases(n=25, seed=2025):
 
 def _sweep_cases(n=24, seed=2026):
     # N: log-uniform (small systems) or uniform (every thread x partner tier up to 1024)
-    rng = np.random.default_rng(seed)
+    rng = np.random.default_rng(seed + SEED_SHIFT)
     return [dict(N=max(2, _log_uniform(rng, 2, 1024) if rng.random() < 0.5 else int(rng.integers(2, 1025))),
                  W=int(rng.integers(1, 6)), m=int(rng.integers(4, 17)),
                  seed=int(rng.integers(2**31)), up_frac=float(rng.choice([0.0, 1.0, rng.random(), 0.5])),
@@ -151,7 +154,7 @@ def test_sweep_random(q, c):
 
 
 def _j1_cases(n=20, seed=2027):
-    rng = np.random.default_rng(seed)
+    rng = np.random.default_rng(seed + SEED_SHIFT)
     out = []
     for _ in range(n):
         S = int(rng.integers(1, 5))
@@ -183,7 +186,7 @@ def test_j1_random(q, c):
 
 
 def _spo_cases(n=16, seed=2028):
-    rng = np.random.default_rng(seed)
+    rng = np.random.default_rng(seed + SEED_SHIFT)
     out = []
     for _ in range(n):
         n_orb = max(1, _log_uniform(rng, 1, 640))
@@ -223,7 +226,7 @@ def test_spo_random(q, c):
 
 
 def _sweep_j1_cases(n=8, seed=2029):
-    rng = np.random.default_rng(seed)
+    rng = np.random.default_rng(seed + SEED_SHIFT)
     out = []
     for _ in range(n):
         S = int(rng.integers(1, 5))
