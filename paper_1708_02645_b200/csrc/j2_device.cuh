@@ -193,4 +193,50 @@ __device__ __forceinline__ FunctorEval<T> functor_from_t(T t, uint32_t tab_base,
     return e;
 }
 
+// Functor argument in fp64 (the accept path compares single pair terms, not
+// N-term sums; the fp32 eval path takes it for functors finer than m = 16).  With t = r/delta up to m, any relative error in r becomes
+// an absolute error ~ m * eps in the interval fraction f and from there in
+// U' and U'' -- the fp32 displacement's own rounding (2^-24) alone gives
+// ~1e-5 of the functor scale at m = 64.  So the displacement is formed
+// exactly in fp64 (the difference of two fp32 values and the +-L shift are
+// exact), r and t follow in fp64, and only f is rounded to T for the fp32
+// Horner; the fp32 displacement (one rounding) and 1/r feed the gradient
+// factors, whose errors are relative and not amplified by t.
+struct AxisD { double c, half, L; };
+
+__device__ __forceinline__ AxisD make_axis_d(double c, double L) {
+    AxisD a;
+    a.c = c;
+    a.half = 0.5 * L;
+    a.L = L;
+    return a;
+}
+
+__device__ __forceinline__ double min_image_d(double x, const AxisD &a) {
+    double d = x - a.c;                        // exact for fp32 (or fp64 in range) inputs
+    if (d > a.half) d -= a.L;
+    else if (d <= -a.half) d += a.L;
+    return d;
+}
+
+template <typename T>
+__device__ __forceinline__ FunctorEval<T> functor_from_r2_d(double r2, double invd64, uint32_t base, int m, T &ir) {
+    const double ird = rsqrt(r2);
+    const double t = r2 * ird * invd64;
+    const double fl = floor(t);
+    const int j = fl < (double)m ? (int)fl : m;    // r >= r_cut (and dead partners) -> the zero row
+    const T f = T(t - fl);
+    ir = T(ird);
+    T a0, a1, a2, a3;
+    ld_shared_c4(base + (uint32_t)j * (uint32_t)sizeof(Coef4<T>), a0, a1, a2, a3);
+    FunctorEval<T> e;
+    const T pp = fma(a3, f, a2);
+    const T q = fma(pp, f, a1);
+    e.u = fma(q, f, a0);
+    const T r1 = fma(a3, f, pp);
+    e.du = fma(r1, f, q);
+    e.h = fma(a3, f, r1);
+    return e;
+}
+
 }  // namespace qj2

@@ -136,7 +136,38 @@ __device__ __forceinline__ GroupC<T> group_consts(const EvalParams &p, int g, in
 }
 
 // Per-trial constants: the three axes' minimum-image constants.
-template <typename T> struct Trial { Axis<T> ax, ay, az; };
+template <typename T> struct Trial {
+    Axis<T> ax, ay, az;
+    AxisD d[3];       // PREC: the same trial coordinates for the fp64 geometry
+};
+
+// One source term with the fp64 geometry (PREC: fp32 functors finer than m = 16, whose
+// fp32 t = r/delta would carry ~m 2^-23 of absolute error into the interval fraction):
+// the displacement exactly in fp64, r and t in fp64, f rounded to T for the Horner
+// (functor_from_r2_d, as the accept path); the gradient factors from the once-rounded
+// displacement and 1/r.  Returns r; d* receive the rounded displacement.
+template <typename T, bool GEN>
+__device__ __forceinline__ T term_prec(T x, T y, T z, bool dead, const Trial<T> &tr, const GroupC<T> &gc,
+                                       uint32_t base, T *acc, T &dx, T &dy, T &dz) {
+    const double ddx = min_image_d((double)x, tr.d[0]);
+    const double ddy = min_image_d((double)y, tr.d[1]);
+    const double ddz = min_image_d((double)z, tr.d[2]);
+    double r2 = fma(ddz, ddz, fma(ddy, ddy, ddx * ddx));
+    if (GEN) r2 = dead ? 1e30 : r2;
+    T ir;
+    const FunctorEval<T> e = functor_from_r2_d<T>(r2, -gc.sg, base, (int)gc.clamp, ir);
+    dx = T(ddx);
+    dy = T(ddy);
+    dz = T(ddz);
+    const T g = e.du * ir;
+    acc[0] += e.u;
+    acc[1] = fma(g, dx, acc[1]);
+    acc[2] = fma(g, dy, acc[2]);
+    acc[3] = fma(g, dz, acc[3]);
+    acc[4] += e.h;
+    acc[5] += g;
+    return T(r2) * ir;
+}
 
 // Functor + accumulation for one source at squared distance r2 (and
 // displacement d).  acc: V, Gx, Gy, Gz (sum du/r * d), H (sum h), S (sum du/r)
@@ -185,7 +216,7 @@ struct SubMask {
 // the source's group picks the functor.  J2 groups share delta, so only the
 // table row changes (raw accumulation); J1 groups differ in delta, so GEN
 // sub-tiles accumulate physical units (PHYS).
-template <typename T, bool ROW, int PF, bool GEN, int NT, int MODE>
+template <typename T, bool ROW, int PF, bool GEN, int NT, int MODE, bool PREC = false>
 __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, uint32_t tab_addr,
                                          const typename Traits<T>::V *__restrict__ px,
                                          const typename Traits<T>::V *__restrict__ py,
@@ -227,12 +258,17 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
                     if (MODE == MODE_J2) base = li < mk.up_rel ? gc.base : mk.base_hi;   // spin halves
                 }
                 const T x = Tr::comp(bx[it], e), y = Tr::comp(by[it], e), z = Tr::comp(bz[it], e);
-                const T dx = min_image(x, tr.ax);
-                const T dy = min_image(y, tr.ay);
-                const T dz = min_image(z, tr.az);
-                T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-                if (GEN) r2 = dead ? T(1e30) : r2;
-                const T r = accumulate<T>(dx, dy, dz, r2, gc.invd, base, gc.clamp, acc);
+                T dx, dy, dz, r;
+                if constexpr (PREC) {
+                    r = term_prec<T, GEN>(x, y, z, dead, tr, gc, base, acc, dx, dy, dz);
+                } else {
+                    dx = min_image(x, tr.ax);
+                    dy = min_image(y, tr.ay);
+                    dz = min_image(z, tr.az);
+                    T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                    if (GEN) r2 = dead ? T(1e30) : r2;
+                    r = accumulate<T>(dx, dy, dz, r2, gc.invd, base, gc.clamp, acc);
+                }
                 if (ROW) { Tr::set(ro[0], e, r); Tr::set(ro[1], e, dx); Tr::set(ro[2], e, dy); Tr::set(ro[3], e, dz); }
             }
             if (ROW) {
@@ -290,7 +326,7 @@ __device__ __forceinline__ void tile_multi(int tid, const EvalParams &p, int kg,
 // rolled loop: one vector group per iteration, the next one loaded ahead.  Small code
 // (one copy of the term instead of ITERS x VW) for kernels whose warps run clean and
 // masked sub-tiles at the same time (the warp kernel: one masked sub-tile of six at C4).
-template <typename T, bool ROW, int NT>
+template <typename T, bool ROW, int NT, bool PREC = false>
 __device__ __forceinline__ void tile_gen_compact(int tid, const typename Traits<T>::V *__restrict__ px,
                                                  const typename Traits<T>::V *__restrict__ py,
                                                  const typename Traits<T>::V *__restrict__ pz, const Trial<T> &tr,
@@ -318,12 +354,18 @@ __device__ __forceinline__ void tile_gen_compact(int tid, const typename Traits<
                 const int li = rel + e;
                 const bool dead = (li >= mk.len) || (li == mk.k_rel);
                 const uint32_t base = li < mk.up_rel ? gc.base : mk.base_hi;
-                const T dx = min_image(Tr::comp(bx, e), tr.ax);
-                const T dy = min_image(Tr::comp(by, e), tr.ay);
-                const T dz = min_image(Tr::comp(bz, e), tr.az);
-                T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-                r2 = dead ? T(1e30) : r2;
-                const T r = accumulate<T>(dx, dy, dz, r2, gc.invd, base, gc.clamp, acc);
+                T dx, dy, dz, r;
+                if constexpr (PREC) {
+                    r = term_prec<T, true>(Tr::comp(bx, e), Tr::comp(by, e), Tr::comp(bz, e), dead, tr, gc, base, acc,
+                                           dx, dy, dz);
+                } else {
+                    dx = min_image(Tr::comp(bx, e), tr.ax);
+                    dy = min_image(Tr::comp(by, e), tr.ay);
+                    dz = min_image(Tr::comp(bz, e), tr.az);
+                    T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                    r2 = dead ? T(1e30) : r2;
+                    r = accumulate<T>(dx, dy, dz, r2, gc.invd, base, gc.clamp, acc);
+                }
                 if (ROW) { Tr::set(ro[0], e, r); Tr::set(ro[1], e, dx); Tr::set(ro[2], e, dy); Tr::set(ro[3], e, dz); }
             }
             if (ROW) {
@@ -419,7 +461,7 @@ __device__ __forceinline__ void sub_tile(int tid, const EvalParams &p, int kg, u
 // J2 sub-tile with 32-bit classification relative to the walker's tile
 // (tile length tlen, k at k_t or -1, sources [0, up_t) of the tile spin-up)
 // and the two per-walker functor constant sets.  s0: the sub-tile's offset.
-template <typename T, bool ROW, int PF, int NT, bool COMPACT_GEN = false>
+template <typename T, bool ROW, int PF, int NT, bool COMPACT_GEN = false, bool PREC = false>
 __device__ __forceinline__ void j2_sub_tile32(int tid, const EvalParams &p, int kg, uint32_t tab_addr, int32_t s0,
                                               int32_t tlen, int32_t k_t, int32_t up_t, const GroupC<T> &g_up,
                                               const GroupC<T> &g_dn, const typename Traits<T>::V *px,
@@ -443,11 +485,11 @@ __device__ __forceinline__ void j2_sub_tile32(int tid, const EvalParams &p, int 
     mk.up_rel = straddle ? up_rel : len;
     mk.base_hi = straddle ? g_dn.base : gc.base;
     if (len == SCH && !k_in && !straddle)
-        tile_run<T, ROW, PF, false, NT, MODE_J2>(tid, p, kg, tab_addr, px, py, pz, tr, gc, mk, acc, rp, row_stride);
+        tile_run<T, ROW, PF, false, NT, MODE_J2, PREC>(tid, p, kg, tab_addr, px, py, pz, tr, gc, mk, acc, rp, row_stride);
     else if constexpr (COMPACT_GEN)
-        tile_gen_compact<T, ROW, NT>(tid, px, py, pz, tr, gc, mk, acc, rp, row_stride);
+        tile_gen_compact<T, ROW, NT, PREC>(tid, px, py, pz, tr, gc, mk, acc, rp, row_stride);
     else
-        tile_run<T, ROW, PF, true, NT, MODE_J2>(tid, p, kg, tab_addr, px, py, pz, tr, gc, mk, acc, rp, row_stride);
+        tile_run<T, ROW, PF, true, NT, MODE_J2, PREC>(tid, p, kg, tab_addr, px, py, pz, tr, gc, mk, acc, rp, row_stride);
     flush<T, MODE_J2>(acc, dacc, gc.sg, gc.sh, gc.ss);      // J2: raw sums (one delta for both groups)
 }
 
@@ -470,7 +512,7 @@ __device__ __forceinline__ void l2_prefetch(const void *src, uint32_t bytes) {
 #endif
 
 // Per-walker setup shared by the CTA and warp kernels.
-template <typename T, int MODE>
+template <typename T, int MODE, bool PREC = false>
 __device__ __forceinline__ void walker_setup(const EvalParams &p, int64_t w, int32_t g, Trial<T> &tr, int &kg,
                                              int64_t &k_local) {
     const int64_t kw = MODE == MODE_J2 ? (int64_t)p.k[w] : -1;
@@ -480,6 +522,10 @@ __device__ __forceinline__ void walker_setup(const EvalParams &p, int64_t w, int
     tr.ax = make_axis<T>(rt[0], T(p.L[0]));
     tr.ay = make_axis<T>(rt[1], T(p.L[1]));
     tr.az = make_axis<T>(rt[2], T(p.L[2]));
+    if constexpr (PREC) {     // the cell as the kernel's type sees it (fp32 L for fp32 positions)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) tr.d[d] = make_axis_d((double)rt[d], (double)T(p.L[d]));
+    }
 }
 
 // Write the physical totals of trial g of walker w and the fused ratio (against V_cur,
@@ -561,7 +607,7 @@ __device__ __forceinline__ void cta_reduce_write(const EvalParams &p, const doub
 // Long rows: one CTA per (walker, trial, tile of SUB sub-tiles).
 // PF: prefetch distance (vector groups in flight), MINB: resident CTAs per SM.
 // ===========================================================================
-template <typename T, bool ROW, int PF, int MINB, int MODE = MODE_J2>
+template <typename T, bool ROW, int PF, int MINB, int MODE = MODE_J2, bool PREC = false>
 __global__ void __launch_bounds__(TPB, MINB)
 j2_eval_kernel(const __grid_constant__ EvalParams p) {
     using Tr = Traits<T>;
@@ -591,7 +637,7 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
     Trial<T> tr;
     int kg;
     int64_t k_local;
-    walker_setup<T, MODE>(p, w, g, tr, kg, k_local);
+    walker_setup<T, MODE, PREC>(p, w, g, tr, kg, k_local);
     const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tab);
 
     const int64_t start = c * CH;
@@ -640,7 +686,7 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
             if (s0 >= tlen) break;
             if constexpr (L2PF > 0) prefetch_sub(sidx + L2PF);
             const int64_t vs = (int64_t)sidx * (SCH / VW);
-            j2_sub_tile32<T, ROW, PF, TPB>(threadIdx.x, p, kg, tab_addr, s0, tlen, k_t, up_t, g_up, g_dn, px + vs,
+            j2_sub_tile32<T, ROW, PF, TPB, false, PREC>(threadIdx.x, p, kg, tab_addr, s0, tlen, k_t, up_t, g_up, g_dn, px + vs,
                                            py + vs, pz + vs, tr, dacc, ROW ? rowp + vs : nullptr, row_stride);
         }
     } else {
@@ -671,7 +717,7 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
 // HBM peak); short rows, where most sub-tiles are masked, keep the pipelined
 // masked loop.
 // ===========================================================================
-template <typename T, bool ROW, int PF, int MINB, int MODE = MODE_J2, bool COMPACT_GEN = false>
+template <typename T, bool ROW, int PF, int MINB, int MODE = MODE_J2, bool COMPACT_GEN = false, bool PREC = false>
 __global__ void __launch_bounds__(TPB, MINB)
 j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
     using Tr = Traits<T>;
@@ -691,7 +737,7 @@ j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
     Trial<T> tr;
     int kg;
     int64_t k_local;
-    walker_setup<T, MODE>(p, w, g, tr, kg, k_local);
+    walker_setup<T, MODE, PREC>(p, w, g, tr, kg, k_local);
     const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tab);
     const T *Rw = static_cast<const T *>(p.R) + w * p.src_stride;
     const int64_t row_stride = p.Np / VW;
@@ -719,7 +765,7 @@ j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
         const V *pz = reinterpret_cast<const V *>(Rw + 2 * p.Np) + voff;
         V *rp = ROW ? reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + g) * 4) * p.Np) + voff : nullptr;
         if constexpr (MODE == MODE_J2)
-            j2_sub_tile32<T, ROW, PF, 32, COMPACT_GEN>(lane, p, kg, tab_addr, (int32_t)sstart, tlen, k_t, up_t, g_up,
+            j2_sub_tile32<T, ROW, PF, 32, COMPACT_GEN, PREC>(lane, p, kg, tab_addr, (int32_t)sstart, tlen, k_t, up_t, g_up,
                                                         g_dn, px, py, pz, tr, dacc, rp, row_stride);
         else
             sub_tile<T, ROW, PF, 32, MODE>(lane, p, kg, tab_addr, sstart, send, k_local, px, py, pz, tr, dacc, rp,
@@ -745,7 +791,7 @@ j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
 // ===========================================================================
 constexpr int J1_MAX_IONS = 4096;
 
-template <typename T>
+template <typename T, bool PREC = false>
 __global__ void __launch_bounds__(TPB) j1_thread_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
     using Tr = Traits<T>;
     __shared__ Coef4<T> tab[MAXTAB];
@@ -768,6 +814,11 @@ __global__ void __launch_bounds__(TPB) j1_thread_kernel(const __grid_constant__ 
     const T *rt = static_cast<const T *>(p.r_trial) + unit * 3;
     const Axis<T> ax = make_axis<T>(rt[0], T(p.L[0])), ay = make_axis<T>(rt[1], T(p.L[1])),
                   az = make_axis<T>(rt[2], T(p.L[2]));
+    Trial<T> trp;         // PREC (an fp32 species functor finer than m = 16): the fp64 geometry
+    if constexpr (PREC) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) trp.d[d] = make_axis_d((double)rt[d], (double)T(p.L[d]));
+    }
     const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tab);
     double dacc[NOUT] = {0.0, 0.0, 0.0, 0.0, 0.0};
     auto term = [&](int32_t i, const GroupC<T> &gc, T (&acc)[NACC]) {
@@ -779,9 +830,14 @@ __global__ void __launch_bounds__(TPB) j1_thread_kernel(const __grid_constant__ 
             const double2 v = reinterpret_cast<const double2 *>(ion)[2 * i];
             x = v.x; y = v.y; z = ion[i * 4 + 2];
         }
-        const T dx = min_image(x, ax), dy = min_image(y, ay), dz = min_image(z, az);
-        const T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-        accumulate<T>(dx, dy, dz, r2, gc.invd, gc.base, gc.clamp, acc);
+        if constexpr (PREC) {
+            T dx, dy, dz;
+            term_prec<T, false>(x, y, z, false, trp, gc, gc.base, acc, dx, dy, dz);
+        } else {
+            const T dx = min_image(x, ax), dy = min_image(y, ay), dz = min_image(z, az);
+            const T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+            accumulate<T>(dx, dy, dz, r2, gc.invd, gc.base, gc.clamp, acc);
+        }
     };
     for (int g = 0; g < p.n_src_groups; ++g) {
         GroupC<T> gc = group_consts<T, MODE_J1>(p, g, 0, tab_addr);

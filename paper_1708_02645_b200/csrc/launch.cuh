@@ -53,14 +53,37 @@ inline bool use_warp_mapping(const EvalParams &p) {
     return p.tiles_per_walker == 1 && (p.W * p.P >= 4096 || p.N_local <= QJ2_WARP_SHORT_N);
 }
 
+// fp32 J2 functors finer than this take the fp64 geometry (term_prec): with the fp32 one,
+// t = r/delta carries ~m 2^-23 of absolute error into the interval fraction, which U' and U''
+// turn into ~m 2^-23 of the functor scale -- above the 1e-5 bar on single-term-dominated sums
+// once m passes ~30 (the accept path's ACCEPT_FAST_MAX_M for the same reason).
+constexpr int EVAL_FAST_MAX_M = 16;
+
+template <typename T, int MODE, bool PREC>
+cudaError_t launch_eval_impl(const EvalParams &p, int64_t nblocks, bool row, cudaStream_t s);
+
 template <typename T, int MODE>
 cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStream_t s) {
+    if constexpr (sizeof(T) == 4 && MODE == MODE_J2) {
+        if (p.m > EVAL_FAST_MAX_M) return launch_eval_impl<T, MODE, true>(p, nblocks, row, s);
+    }
+    if constexpr (sizeof(T) == 4 && MODE == MODE_J1) {   // the small-ion kernel, a species finer than 16
+        int mmax = 0;
+        for (int g = 0; g < p.n_src_groups; ++g) mmax = p.grp_m[g] > mmax ? p.grp_m[g] : mmax;
+        if (!row && p.N_local <= J1_MAX_IONS && mmax > EVAL_FAST_MAX_M)
+            return launch_eval_impl<T, MODE, true>(p, nblocks, row, s);
+    }
+    return launch_eval_impl<T, MODE, false>(p, nblocks, row, s);
+}
+
+template <typename T, int MODE, bool PREC>
+cudaError_t launch_eval_impl(const EvalParams &p, int64_t nblocks, bool row, cudaStream_t s) {
     if constexpr (MODE == MODE_J1) {
         // small ion sets: one thread per (walker, trial), ions in shared memory
         if (!row && p.N_local <= J1_MAX_IONS) {
             const int64_t units = p.W * p.P;
             const size_t smem = (size_t)p.N_local * 4 * sizeof(T);
-            auto kern = j1_thread_kernel<T>;
+            auto kern = j1_thread_kernel<T, PREC>;
             if (smem > 40 * 1024) {   // the static functor table (<= 2.2 KB) comes on top of the 48 KB default
                 cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 if (e != cudaSuccess) return e;
@@ -75,12 +98,13 @@ cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStre
         // fp32: three vector groups in flight per lane at 2 CTAs/SM (128 registers, no spills): on a
         // C4 wave 5.89 TB/s vs 5.31 for two groups at 3 CTAs/SM (80 registers, spilling), 5.51 for
         // four groups, 5.52 for one group at 4 CTAs/SM (profiles/r01_ab_sweep_s3.md)
-        if (row) j2_eval_warp_kernel<T, true, 1, 2, MODE><<<nbw, TPB, 0, s>>>(p, units);
+        if (row) j2_eval_warp_kernel<T, true, 1, 2, MODE, false, PREC><<<nbw, TPB, 0, s>>>(p, units);
         else if constexpr (sizeof(T) == 4) {
             if (p.N_local >= 4 * 32 * Traits<T>::VW * ITERS)
-                j2_eval_warp_kernel<T, false, QJ2_WARP_PF, QJ2_WARP_MINB, MODE, true><<<nbw, TPB, 0, s>>>(p, units);
+                j2_eval_warp_kernel<T, false, QJ2_WARP_PF, QJ2_WARP_MINB, MODE, true, PREC><<<nbw, TPB, 0, s>>>(p, units);
             else
-                j2_eval_warp_kernel<T, false, QJ2_WARP_SHORT_PF, QJ2_WARP_SHORT_MINB, MODE><<<nbw, TPB, 0, s>>>(p, units);
+                j2_eval_warp_kernel<T, false, QJ2_WARP_SHORT_PF, QJ2_WARP_SHORT_MINB, MODE, false, PREC>
+                    <<<nbw, TPB, 0, s>>>(p, units);
         } else if (p.N_local >= 4 * 32 * Traits<T>::VW * ITERS) {
             j2_eval_warp_kernel<T, false, 2, 2, MODE, true><<<nbw, TPB, 0, s>>>(p, units);
         } else {
@@ -90,10 +114,10 @@ cudaError_t launch_eval(const EvalParams &p, int64_t nblocks, bool row, cudaStre
     }
     const unsigned nb = (unsigned)nblocks;
     if (row)
-        j2_eval_kernel<T, true, 1, sizeof(T) == 4 ? 4 : 2, MODE><<<nb, TPB, 0, s>>>(p);
+        j2_eval_kernel<T, true, 1, sizeof(T) == 4 ? 4 : 2, MODE, PREC><<<nb, TPB, 0, s>>>(p);
     else if constexpr (sizeof(T) == 4)   // two vector groups in flight per thread, 3 CTAs/SM (80 registers):
                                          // measured best on B200 against distance 1 at 4 CTAs/SM and 3 at 2
-        j2_eval_kernel<T, false, QJ2_EVAL_PF, QJ2_EVAL_MINB, MODE><<<nb, TPB, 0, s>>>(p);
+        j2_eval_kernel<T, false, QJ2_EVAL_PF, QJ2_EVAL_MINB, MODE, PREC><<<nb, TPB, 0, s>>>(p);
     else                                 // fp64: two groups in flight, 2 CTAs/SM
         j2_eval_kernel<T, false, QJ2_EVAL64_PF, QJ2_EVAL64_MINB, MODE><<<nb, TPB, 0, s>>>(p);
     return cudaGetLastError();

@@ -52,6 +52,17 @@ def test_j1_sizes(q, dtype, n_ions):
     check(q, ions, start, rt, fn1, dtype)
 
 
+@pytest.mark.parametrize("m", [17, 36, 64])
+def test_j1_fine_species_functors_fp32(q, m):
+    """An fp32 species functor finer than m = 16 takes the fp64 geometry in the
+    small-ion kernel: the 1e-5 bar holds where one or two ions
+    make the whole sum."""
+    for n_ions, S in ((1, 1), (2, 2), (5, 3), (64, 2)):
+        ions, start, rt, fn1 = j1_case(n_ions, 2048, seed=700 + m + n_ions, dtype=np.float32, S=S,
+                                       m=(m, 8, m, 12))
+        check(q, ions, start, rt, fn1, np.float32)
+
+
 @pytest.mark.parametrize("S", [1, 3, 4])
 def test_j1_species_counts_and_straddling(q, S):
     # species boundaries at n*s//S land inside sub-tiles (masked multi-species path)

@@ -115,6 +115,30 @@ def test_single_walker_and_larger_m(q):
         check(q, R, k, rt, fn, 4000, n_up, np.float32)
 
 
+@pytest.mark.parametrize("m", [17, 36, 64])
+def test_fine_functors_fp32(q, m):
+    """fp32 functors finer than m = 16 take the fp64 geometry:
+    the 1e-5 bar holds where one or two terms make the whole sum (tiny N: the
+    short-row warp kernel), in the compact warp kernel (long rows, many walkers),
+    in the CTA kernel (one and several tiles per walker), and the row output keeps
+    the fp32 single-rounding displacements bitwise."""
+    for N, W in ((2, 512), (4, 512), (8, 256), (4100, 4096), (5000, 64), (300000, 2)):
+        R, k, rt, fn, n_up = instance(N, W, seed=400 + m + N, dtype=np.float32, m=m)
+        check(q, R, k, rt, fn, N, n_up, np.float32)
+    N = 3000
+    R, k, rt, fn, n_up = instance(N, 8, seed=450 + m, dtype=np.float32, m=m)
+    out, orc, row, orow = check(q, R, k, rt, fn, N, n_up, np.float32, row=True)
+    L = np.float64(fn.L[0])
+    for w in range(8):
+        i = np.array([j for j in range(N) if j != k[w]])
+        d_gpu = row[w, 0, 1:, i].astype(np.float64)
+        d_orc = orow[w, 0, 1:, i]
+        tie = np.abs(np.abs(d_orc) - L / 2) <= 4 * np.spacing(np.float32(L))
+        assert ((d_gpu == d_orc.astype(np.float32)) | tie).all()
+        rg, ro = row[w, 0, 0, i], orow[w, 0, 0, i].astype(np.float32)
+        assert np.all(np.abs(rg - ro) <= 3 * np.spacing(ro))
+
+
 def test_noop_move_ratio_exactly_one(q):
     """P = 2 with r_trial[0] == r_trial[1] (no-op move): dJ2 = 0 bitwise,
     ratio 1."""

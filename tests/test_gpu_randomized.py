@@ -36,7 +36,7 @@ def _eval_cases(n=40, seed=2024):
     cases = []
     for _ in range(n):
         N = max(2, _log_uniform(rng, 2, 450000))
-        c = dict(N=N, W=int(rng.integers(1, 7)), P=int(rng.integers(1, 6)), m=int(rng.integers(4, 25)),
+        c = dict(N=N, W=int(rng.integers(1, 7)), P=int(rng.integers(1, 6)), m=int(rng.integers(4, 65)),
                  f64=bool(rng.random() < 0.4), drift=bool(rng.random() < 0.5), seed=int(rng.integers(2**31)),
                  up_frac=float(rng.choice([0.0, 1.0, rng.random(), 0.5])),
                  slice_frac=(float(rng.random()), float(rng.random())), sharded=bool(rng.random() < 0.3))
