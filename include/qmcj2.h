@@ -112,7 +112,10 @@ qj2_status qj2_eval_workspace_size(int64_t W, int32_t P, int64_t N_local,
 /* PAPER:885-887) and the J2 shares of grad_k, lap_k at R' (Alg. 1 L8,       */
 /* PAPER:849).  Arithmetic: dtype positions and per-term math, fp64          */
 /* accumulation and outputs ("quantities per walker ... in double           */
-/* precision").                                               */
+/* precision"); with fp32 positions and a functor finer than  */
+/* m = 16 the displacement, r and r/delta are formed in fp64 and only the    */
+/* interval fraction is rounded to fp32 (fp32 r/delta would leave ~m*2^-23   */
+/* of the functor scale per term).                                           */
 /*                                                                           */
 /* Arguments                                                                 */
 /*   fn        host, functor + cell (see qj2_functor).                       */
