@@ -192,6 +192,18 @@ def _stream_ptr(stream) -> int:
     return s.cuda_stream
 
 
+def _keep(stream, *tensors):
+    """A call on a stream other than the current one: tensors this call allocated
+    itself (workspaces, outputs it created) were allocated on the current stream,
+    so the caching allocator must not hand their memory to that stream again
+    before the kernels using them on `stream` have run (torch's record_stream)."""
+    if stream is None or stream == torch.cuda.current_stream():
+        return
+    for t in tensors:
+        if t is not None and t.is_cuda:
+            t.record_stream(stream)
+
+
 def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
@@ -291,6 +303,7 @@ def eval(R, k, r_trial, fn, n_total: int, n_up: int, *, i_offset: int = 0, n_loc
                        _ptr(row_out) if row else None, _ptr(V_cur), _ptr(ratio_out) if ratio else None,
                        _ptr(ws.buf), ws.nbytes, ctypes.c_void_p(_stream_ptr(stream)))
     _check(st, "qj2_eval")
+    _keep(stream, out, row_out, ratio_out, ws.buf)
     res = [out]
     if row:
         res.append(row_out)
@@ -373,6 +386,7 @@ def eval_j1(ions, species_start, r_trial, fn1, *, row: bool = False, V_cur=None,
     _check(_lib.qj2_eval_j1(f.ptr, _dtype_code(ions.dtype), W, st, Np, _ptr(ions), P, _ptr(r_trial), _ptr(out),
                             _ptr(row_out) if row else None, _ptr(V_cur), _ptr(ratio_out) if ratio else None,
                             _ptr(ws.buf), ws.nbytes, ctypes.c_void_p(_stream_ptr(stream))), "qj2_eval_j1")
+    _keep(stream, out, row_out, ratio_out, ws.buf)
     res = [out]
     if row:
         res.append(row_out)
@@ -394,6 +408,7 @@ def ratio(out, V_cur=None, ratio_out=None, stream=None):
         _shape(V_cur, "V_cur", (W,))
     _check(_lib.qj2_ratio(W, P, _ptr(out), _ptr(V_cur), _ptr(ratio_out), ctypes.c_void_p(_stream_ptr(stream))),
            "qj2_ratio")
+    _keep(stream, ratio_out)
     return ratio_out
 
 
@@ -445,6 +460,7 @@ def accept(R, state, k, r_new, acc, out_new, fn, n_total: int, n_up: int, *, tri
                            _ptr(R), _ptr(state), _ptr(k), rp, rs, _ptr(r_old), _ptr(acc),
                            op, os_, _ptr(ws.buf), ws.nbytes,
                            ctypes.c_void_p(_stream_ptr(stream))), "qj2_accept")
+    _keep(stream, ws.buf)
     return R, state
 
 
@@ -484,6 +500,7 @@ def metropolis_accept(R, state, k, r_trial, out, u, fn, n_total: int, n_up: int,
     _check(_lib.qj2_metropolis_accept(f.ptr, _dtype_code(R.dtype), W, n_total, n_up, i_offset, n_local, Np,
                                       _ptr(R), _ptr(state), _ptr(k), rn, ro, rs, on, vr, os_, vrs, _ptr(u),
                                       _ptr(acc), ctypes.c_void_p(_stream_ptr(stream))), "qj2_metropolis_accept")
+    _keep(stream, acc)
     return acc
 
 
@@ -539,6 +556,7 @@ def sweep(R, state, ks, delta, u, fn, n: int, n_up: int, *, acc=None, dj=None, j
     j1p, keep = _sweep_j1(j1, W, Np)
     _check(_lib.qj2_sweep(f.ptr, W, n, n_up, Np, _ptr(R), _ptr(state), S, _ptr(ks), _ptr(delta), _ptr(u),
                           _ptr(acc), _ptr(dj), j1p, ctypes.c_void_p(_stream_ptr(stream))), "qj2_sweep")
+    _keep(stream, acc, dj)
     del keep
     return acc, dj
 
@@ -574,6 +592,7 @@ def metropolis(ratio_out, u, acc=None, *, trial: int = 0, stream=None):
     _shape(acc, "acc", (W,))
     _check(_lib.qj2_metropolis(W, rp, rs, _ptr(u), _ptr(acc), ctypes.c_void_p(_stream_ptr(stream))),
            "qj2_metropolis")
+    _keep(stream, acc)
     return acc
 
 
@@ -658,6 +677,7 @@ def spo_eval(tab: SpoTable, pos, *, vgh: bool = True, Ainv=None, krow=None, tria
     _check(_lib.qj2_spo_eval(tab.ptr, what, _dtype_code(pos.dtype), W, pp, ps,
                              a_ptr, a_stride, a_ld, _ptr(krow), ppw, _ptr(out) if Ainv is not None else None,
                              _ptr(spo_out), ctypes.c_void_p(_stream_ptr(stream))), "qj2_spo_eval")
+    _keep(stream, out if Ainv is not None else None, spo_out)
     if want_spo:
         return out, spo_out
     return out
