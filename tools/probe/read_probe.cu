@@ -15,6 +15,48 @@ __device__ __forceinline__ float4 ld_stream(const float4 *p) {
     return v;
 }
 
+// 256-bit loads (sm_100: ld .v8.f32, one LDG.E.ENL2.256 per 8 floats)
+struct f8 { float4 a, b; };
+__device__ __forceinline__ f8 ld_stream8(const float4 *p) {
+    f8 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v.a.x), "=f"(v.a.y), "=f"(v.a.z), "=f"(v.a.w), "=f"(v.b.x), "=f"(v.b.y), "=f"(v.b.z),
+                   "=f"(v.b.w) : "l"(p));
+    return v;
+}
+
+// as read_soa3 with 32-byte loads: a thread's two consecutive float4 vectors per load
+template <int PF, int MINB>
+__global__ void __launch_bounds__(256, MINB) read_soa3_v8(const float4 *__restrict__ a, long n_vec, float *out) {
+    const long np_vec = 614400 / 4;
+    const long tiles_per_w = np_vec / (256 * 8 * 8);
+    const long w = blockIdx.x / (tiles_per_w + 1), c = blockIdx.x % (tiles_per_w + 1);
+    const float4 *px = a + w * 3 * np_vec + c * 256 * 64 + 2 * threadIdx.x;
+    const float4 *py = px + np_vec, *pz = py + np_vec;
+    const long lim = np_vec - c * 256 * 64 - 2 * threadIdx.x;
+    float acc = 0.f;
+#pragma unroll 1
+    for (int sub = 0; sub < 8; ++sub) {
+        f8 bx[4], by[4], bz[4];                      // 4 iterations of 8 floats per thread = 32 terms
+#pragma unroll
+        for (int j = 0; j < PF; ++j) {
+            const long o = (long)sub * 2048 + j * 512;
+            if (o < lim) { bx[j] = ld_stream8(px + o); by[j] = ld_stream8(py + o); bz[j] = ld_stream8(pz + o); }
+        }
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+            if (it + PF < 4) {
+                const long o = (long)sub * 2048 + (it + PF) * 512;
+                if (o < lim) {
+                    bx[it + PF] = ld_stream8(px + o); by[it + PF] = ld_stream8(py + o); bz[it + PF] = ld_stream8(pz + o);
+                }
+            }
+            acc += bx[it].a.x * by[it].a.y + bz[it].b.z + bx[it].b.w;
+        }
+    }
+    if (acc == 1234.5f) out[0] = acc;
+}
+
 template <int U>
 __global__ void __launch_bounds__(256) read_tiled(const float4 *__restrict__ a, long n_vec, float *out) {
     // each CTA reads a contiguous tile of 256 * U * 8 vectors, U vectors in flight per thread
@@ -115,5 +157,9 @@ int main() {
     run3("soa3 PF=3 MINB=3", read_soa3<3, 3>);
     run3("soa3 PF=2 MINB=4", read_soa3<2, 4>);
     run3("soa3 PF=4 MINB=2", read_soa3<4, 2>);
+    run3("soa3 v8 PF=1 MINB=3", read_soa3_v8<1, 3>);
+    run3("soa3 v8 PF=2 MINB=3", read_soa3_v8<2, 3>);
+    run3("soa3 v8 PF=1 MINB=4", read_soa3_v8<1, 4>);
+    run3("soa3 v8 PF=2 MINB=2", read_soa3_v8<2, 2>);
     return 0;
 }
