@@ -279,6 +279,57 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
     }
 }
 
+// A clean fp32 sub-tile with 256-bit loads (sm_100 `ld.v8.f32`, SASS LDG.E.ENL2.256):
+// thread tid takes the vector pairs (2 tid, 2 tid + 1) + 2 NT j, j < ITERS / 2 -- the same
+// 32 terms per thread, half the load instructions, and a streaming read that reaches 7.40
+// instead of 7.28 TB/s on this pattern (tools/probe/read_probe.cu).  px: the sub-tile's
+// vector tid (the v4 mapping's base), so px + tid is this thread's first pair; rows must be
+// 32-byte aligned (the host checks).  PFP pairs in flight ahead of the one consumed.
+struct F8 { float4 a, b; };
+__device__ __forceinline__ F8 ld_stream8(const float4 *p) {
+    F8 v;
+    asm("ld.global.nc.L1::no_allocate.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(v.a.x), "=f"(v.a.y), "=f"(v.a.z), "=f"(v.a.w), "=f"(v.b.x), "=f"(v.b.y), "=f"(v.b.z), "=f"(v.b.w)
+        : "l"(p));
+    return v;
+}
+
+template <int PFP, int NT>
+__device__ __forceinline__ void tile_run_v8(int tid, const float4 *__restrict__ px, const float4 *__restrict__ py,
+                                            const float4 *__restrict__ pz, const Trial<float> &tr,
+                                            const GroupC<float> &gc, float (&acc)[NACC]) {
+    using Tr = Traits<float>;
+    constexpr int NP = ITERS / 2;                  // vector pairs per thread
+    const float4 *qx = px + tid, *qy = py + tid, *qz = pz + tid;
+    F8 bx[NP], by[NP], bz[NP];
+#pragma unroll
+    for (int j = 0; j < PFP && j < NP; ++j) {
+        bx[j] = ld_stream8(qx + j * 2 * NT);
+        by[j] = ld_stream8(qy + j * 2 * NT);
+        bz[j] = ld_stream8(qz + j * 2 * NT);
+    }
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+        if (j + PFP < NP) {
+            bx[j + PFP] = ld_stream8(qx + (j + PFP) * 2 * NT);
+            by[j + PFP] = ld_stream8(qy + (j + PFP) * 2 * NT);
+            bz[j + PFP] = ld_stream8(qz + (j + PFP) * 2 * NT);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float4 vx = h ? bx[j].b : bx[j].a, vy = h ? by[j].b : by[j].a, vz = h ? bz[j].b : bz[j].a;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float dx = min_image(Tr::comp(vx, e), tr.ax);
+                const float dy = min_image(Tr::comp(vy, e), tr.ay);
+                const float dz = min_image(Tr::comp(vz, e), tr.az);
+                const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                accumulate<float>(dx, dy, dz, r2, gc.invd, gc.base, gc.clamp, acc);
+            }
+        }
+    }
+}
+
 // A J1 sub-tile straddling a species boundary: rare, so a compact rolled
 // loop (one vector per iteration, no prefetch) keeps the instruction
 // footprint small.  The species is looked up per source and the terms are
@@ -461,7 +512,7 @@ __device__ __forceinline__ void sub_tile(int tid, const EvalParams &p, int kg, u
 // J2 sub-tile with 32-bit classification relative to the walker's tile
 // (tile length tlen, k at k_t or -1, sources [0, up_t) of the tile spin-up)
 // and the two per-walker functor constant sets.  s0: the sub-tile's offset.
-template <typename T, bool ROW, int PF, int NT, bool COMPACT_GEN = false, bool PREC = false>
+template <typename T, bool ROW, int PF, int NT, bool COMPACT_GEN = false, bool PREC = false, bool V8 = false>
 __device__ __forceinline__ void j2_sub_tile32(int tid, const EvalParams &p, int kg, uint32_t tab_addr, int32_t s0,
                                               int32_t tlen, int32_t k_t, int32_t up_t, const GroupC<T> &g_up,
                                               const GroupC<T> &g_dn, const typename Traits<T>::V *px,
@@ -484,9 +535,13 @@ __device__ __forceinline__ void j2_sub_tile32(int tid, const EvalParams &p, int 
     mk.g0 = 0;                                         // (J1 only)
     mk.up_rel = straddle ? up_rel : len;
     mk.base_hi = straddle ? g_dn.base : gc.base;
-    if (len == SCH && !k_in && !straddle)
-        tile_run<T, ROW, PF, false, NT, MODE_J2, PREC>(tid, p, kg, tab_addr, px, py, pz, tr, gc, mk, acc, rp, row_stride);
-    else if constexpr (COMPACT_GEN)
+    if (len == SCH && !k_in && !straddle) {
+        if constexpr (V8 && sizeof(T) == 4 && !ROW && !PREC)
+            tile_run_v8<(PF + 1) / 2, NT>(tid, px, py, pz, tr, gc, acc);
+        else
+            tile_run<T, ROW, PF, false, NT, MODE_J2, PREC>(tid, p, kg, tab_addr, px, py, pz, tr, gc, mk, acc, rp,
+                                                           row_stride);
+    } else if constexpr (COMPACT_GEN)
         tile_gen_compact<T, ROW, NT, PREC>(tid, px, py, pz, tr, gc, mk, acc, rp, row_stride);
     else
         tile_run<T, ROW, PF, true, NT, MODE_J2, PREC>(tid, p, kg, tab_addr, px, py, pz, tr, gc, mk, acc, rp, row_stride);
@@ -607,7 +662,7 @@ __device__ __forceinline__ void cta_reduce_write(const EvalParams &p, const doub
 // Long rows: one CTA per (walker, trial, tile of SUB sub-tiles).
 // PF: prefetch distance (vector groups in flight), MINB: resident CTAs per SM.
 // ===========================================================================
-template <typename T, bool ROW, int PF, int MINB, int MODE = MODE_J2, bool PREC = false>
+template <typename T, bool ROW, int PF, int MINB, int MODE = MODE_J2, bool PREC = false, bool V8 = false>
 __global__ void __launch_bounds__(TPB, MINB)
 j2_eval_kernel(const __grid_constant__ EvalParams p) {
     using Tr = Traits<T>;
@@ -686,7 +741,7 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
             if (s0 >= tlen) break;
             if constexpr (L2PF > 0) prefetch_sub(sidx + L2PF);
             const int64_t vs = (int64_t)sidx * (SCH / VW);
-            j2_sub_tile32<T, ROW, PF, TPB, false, PREC>(threadIdx.x, p, kg, tab_addr, s0, tlen, k_t, up_t, g_up, g_dn, px + vs,
+            j2_sub_tile32<T, ROW, PF, TPB, false, PREC, V8>(threadIdx.x, p, kg, tab_addr, s0, tlen, k_t, up_t, g_up, g_dn, px + vs,
                                            py + vs, pz + vs, tr, dacc, ROW ? rowp + vs : nullptr, row_stride);
         }
     } else {
@@ -717,7 +772,8 @@ j2_eval_kernel(const __grid_constant__ EvalParams p) {
 // HBM peak); short rows, where most sub-tiles are masked, keep the pipelined
 // masked loop.
 // ===========================================================================
-template <typename T, bool ROW, int PF, int MINB, int MODE = MODE_J2, bool COMPACT_GEN = false, bool PREC = false>
+template <typename T, bool ROW, int PF, int MINB, int MODE = MODE_J2, bool COMPACT_GEN = false, bool PREC = false,
+          bool V8 = false>
 __global__ void __launch_bounds__(TPB, MINB)
 j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
     using Tr = Traits<T>;
@@ -765,7 +821,7 @@ j2_eval_warp_kernel(const __grid_constant__ EvalParams p, int64_t n_units) {
         const V *pz = reinterpret_cast<const V *>(Rw + 2 * p.Np) + voff;
         V *rp = ROW ? reinterpret_cast<V *>(static_cast<T *>(p.row_out) + ((w * p.P + g) * 4) * p.Np) + voff : nullptr;
         if constexpr (MODE == MODE_J2)
-            j2_sub_tile32<T, ROW, PF, 32, COMPACT_GEN, PREC>(lane, p, kg, tab_addr, (int32_t)sstart, tlen, k_t, up_t, g_up,
+            j2_sub_tile32<T, ROW, PF, 32, COMPACT_GEN, PREC, V8>(lane, p, kg, tab_addr, (int32_t)sstart, tlen, k_t, up_t, g_up,
                                                         g_dn, px, py, pz, tr, dacc, rp, row_stride);
         else
             sub_tile<T, ROW, PF, 32, MODE>(lane, p, kg, tab_addr, sstart, send, k_local, px, py, pz, tr, dacc, rp,

@@ -43,6 +43,15 @@ namespace qj2 {
 #ifndef QJ2_WARP_SHORT_MINB
 #define QJ2_WARP_SHORT_MINB 1
 #endif
+// The CTA kernel's clean fp32 sub-tiles read with 256-bit loads when the rows are 32-byte
+// aligned: C3 1.105 -> 1.083 ms, C5 8.98 -> 8.87, C3P2 1.780 -> 1.753, C3P12 9.64 -> 9.55
+// (profiles/r02/ab_results.txt).  QJ2_WARP_V8: the same in the warp kernel (A/B).
+#ifndef QJ2_EVAL_V8
+#define QJ2_EVAL_V8 1
+#endif
+#ifndef QJ2_WARP_V8
+#define QJ2_WARP_V8 0
+#endif
 #ifndef QJ2_WARP_SHORT_N
 #define QJ2_WARP_SHORT_N 2048  // rows this short take the warp kernel whatever W (A/B builds)
 #endif
@@ -100,8 +109,15 @@ cudaError_t launch_eval_impl(const EvalParams &p, int64_t nblocks, bool row, cud
         // four groups, 5.52 for one group at 4 CTAs/SM (profiles/r01_ab_sweep_s3.md)
         if (row) j2_eval_warp_kernel<T, true, 1, 2, MODE, false, PREC><<<nbw, TPB, 0, s>>>(p, units);
         else if constexpr (sizeof(T) == 4) {
-            if (p.N_local >= 4 * 32 * Traits<T>::VW * ITERS)
-                j2_eval_warp_kernel<T, false, QJ2_WARP_PF, QJ2_WARP_MINB, MODE, true, PREC><<<nbw, TPB, 0, s>>>(p, units);
+            if (p.N_local >= 4 * 32 * Traits<T>::VW * ITERS) {
+#if QJ2_WARP_V8
+                if (MODE == MODE_J2 && !PREC && p.Np % 8 == 0 && ((uintptr_t)p.R & 31) == 0)
+                    j2_eval_warp_kernel<T, false, QJ2_WARP_PF, QJ2_WARP_MINB, MODE, true, false, true>
+                        <<<nbw, TPB, 0, s>>>(p, units);
+                else
+#endif
+                    j2_eval_warp_kernel<T, false, QJ2_WARP_PF, QJ2_WARP_MINB, MODE, true, PREC><<<nbw, TPB, 0, s>>>(p, units);
+            }
             else
                 j2_eval_warp_kernel<T, false, QJ2_WARP_SHORT_PF, QJ2_WARP_SHORT_MINB, MODE, false, PREC>
                     <<<nbw, TPB, 0, s>>>(p, units);
@@ -117,7 +133,15 @@ cudaError_t launch_eval_impl(const EvalParams &p, int64_t nblocks, bool row, cud
         j2_eval_kernel<T, true, 1, sizeof(T) == 4 ? 4 : 2, MODE, PREC><<<nb, TPB, 0, s>>>(p);
     else if constexpr (sizeof(T) == 4)   // two vector groups in flight per thread, 3 CTAs/SM (80 registers):
                                          // measured best on B200 against distance 1 at 4 CTAs/SM and 3 at 2
-        j2_eval_kernel<T, false, QJ2_EVAL_PF, QJ2_EVAL_MINB, MODE, PREC><<<nb, TPB, 0, s>>>(p);
+    {
+#if QJ2_EVAL_V8
+        // 256-bit loads for the clean sub-tiles when every row starts 32-byte aligned
+        if (MODE == MODE_J2 && !PREC && p.Np % 8 == 0 && ((uintptr_t)p.R & 31) == 0)
+            j2_eval_kernel<T, false, QJ2_EVAL_PF, QJ2_EVAL_MINB, MODE, false, true><<<nb, TPB, 0, s>>>(p);
+        else
+#endif
+            j2_eval_kernel<T, false, QJ2_EVAL_PF, QJ2_EVAL_MINB, MODE, PREC><<<nb, TPB, 0, s>>>(p);
+    }
     else                                 // fp64: two groups in flight, 2 CTAs/SM
         j2_eval_kernel<T, false, QJ2_EVAL64_PF, QJ2_EVAL64_MINB, MODE><<<nb, TPB, 0, s>>>(p);
     return cudaGetLastError();
