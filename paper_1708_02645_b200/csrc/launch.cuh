@@ -43,14 +43,14 @@ namespace qj2 {
 #ifndef QJ2_WARP_SHORT_MINB
 #define QJ2_WARP_SHORT_MINB 1
 #endif
-// The CTA kernel's clean fp32 sub-tiles read with 256-bit loads when the rows are 32-byte
-// aligned: C3 1.105 -> 1.083 ms, C5 8.98 -> 8.87, C3P2 1.780 -> 1.753, C3P12 9.64 -> 9.55
-// (profiles/r02/ab_results.txt).  QJ2_WARP_V8: the same in the warp kernel (A/B).
+// The clean fp32 sub-tiles of the CTA kernel and of the compact warp kernel read with 256-bit
+// loads when the rows are 32-byte aligned: C3 1.105 -> 1.083 ms, C5 8.98 -> 8.87, C3P2 1.780 ->
+// 1.753, C3P12 9.64 -> 9.55, a C4 wave 12.57 -> 12.17 ms (profiles/r02/ab_results.txt).
 #ifndef QJ2_EVAL_V8
 #define QJ2_EVAL_V8 1
 #endif
 #ifndef QJ2_WARP_V8
-#define QJ2_WARP_V8 0
+#define QJ2_WARP_V8 1
 #endif
 #ifndef QJ2_WARP_SHORT_N
 #define QJ2_WARP_SHORT_N 2048  // rows this short take the warp kernel whatever W (A/B builds)
