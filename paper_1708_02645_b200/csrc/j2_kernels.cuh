@@ -279,29 +279,37 @@ __device__ __forceinline__ void tile_run(int tid, const EvalParams &p, int kg, u
     }
 }
 
-// A clean fp32 sub-tile with 256-bit loads (sm_100 `ld.v8.f32`, SASS LDG.E.ENL2.256):
+// A clean sub-tile with 256-bit loads (sm_100 `ld.v8.f32` / `ld.v4.f64`, SASS LDG.E.ENL2.256):
 // thread tid takes the vector pairs (2 tid, 2 tid + 1) + 2 NT j, j < ITERS / 2 -- the same
 // 32 terms per thread, half the load instructions, and a streaming read that reaches 7.40
 // instead of 7.28 TB/s on this pattern (tools/probe/read_probe.cu).  px: the sub-tile's
 // vector tid (the v4 mapping's base), so px + tid is this thread's first pair; rows must be
 // 32-byte aligned (the host checks).  PFP pairs in flight ahead of the one consumed.
-struct F8 { float4 a, b; };
-__device__ __forceinline__ F8 ld_stream8(const float4 *p) {
-    F8 v;
+template <typename T> struct Pair8 { typename Traits<T>::V a, b; };   // 32 bytes: two vectors
+__device__ __forceinline__ Pair8<float> ld_stream8(const float4 *p) {
+    Pair8<float> v;
     asm("ld.global.nc.L1::no_allocate.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
         : "=f"(v.a.x), "=f"(v.a.y), "=f"(v.a.z), "=f"(v.a.w), "=f"(v.b.x), "=f"(v.b.y), "=f"(v.b.z), "=f"(v.b.w)
         : "l"(p));
     return v;
 }
+__device__ __forceinline__ Pair8<double> ld_stream8(const double2 *p) {
+    Pair8<double> v;
+    asm("ld.global.nc.L1::no_allocate.L2::256B.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(v.a.x), "=d"(v.a.y), "=d"(v.b.x), "=d"(v.b.y) : "l"(p));
+    return v;
+}
 
-template <int PFP, int NT>
-__device__ __forceinline__ void tile_run_v8(int tid, const float4 *__restrict__ px, const float4 *__restrict__ py,
-                                            const float4 *__restrict__ pz, const Trial<float> &tr,
-                                            const GroupC<float> &gc, float (&acc)[NACC]) {
-    using Tr = Traits<float>;
+template <typename T, int PFP, int NT>
+__device__ __forceinline__ void tile_run_v8(int tid, const typename Traits<T>::V *__restrict__ px,
+                                            const typename Traits<T>::V *__restrict__ py,
+                                            const typename Traits<T>::V *__restrict__ pz, const Trial<T> &tr,
+                                            const GroupC<T> &gc, T (&acc)[NACC]) {
+    using Tr = Traits<T>;
+    using V = typename Tr::V;
     constexpr int NP = ITERS / 2;                  // vector pairs per thread
-    const float4 *qx = px + tid, *qy = py + tid, *qz = pz + tid;
-    F8 bx[NP], by[NP], bz[NP];
+    const V *qx = px + tid, *qy = py + tid, *qz = pz + tid;
+    Pair8<T> bx[NP], by[NP], bz[NP];
 #pragma unroll
     for (int j = 0; j < PFP && j < NP; ++j) {
         bx[j] = ld_stream8(qx + j * 2 * NT);
@@ -317,14 +325,14 @@ __device__ __forceinline__ void tile_run_v8(int tid, const float4 *__restrict__ 
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const float4 vx = h ? bx[j].b : bx[j].a, vy = h ? by[j].b : by[j].a, vz = h ? bz[j].b : bz[j].a;
+            const V vx = h ? bx[j].b : bx[j].a, vy = h ? by[j].b : by[j].a, vz = h ? bz[j].b : bz[j].a;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const float dx = min_image(Tr::comp(vx, e), tr.ax);
-                const float dy = min_image(Tr::comp(vy, e), tr.ay);
-                const float dz = min_image(Tr::comp(vz, e), tr.az);
-                const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-                accumulate<float>(dx, dy, dz, r2, gc.invd, gc.base, gc.clamp, acc);
+            for (int e = 0; e < Tr::VW; ++e) {
+                const T dx = min_image(Tr::comp(vx, e), tr.ax);
+                const T dy = min_image(Tr::comp(vy, e), tr.ay);
+                const T dz = min_image(Tr::comp(vz, e), tr.az);
+                const T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                accumulate<T>(dx, dy, dz, r2, gc.invd, gc.base, gc.clamp, acc);
             }
         }
     }
@@ -536,8 +544,8 @@ __device__ __forceinline__ void j2_sub_tile32(int tid, const EvalParams &p, int 
     mk.up_rel = straddle ? up_rel : len;
     mk.base_hi = straddle ? g_dn.base : gc.base;
     if (len == SCH && !k_in && !straddle) {
-        if constexpr (V8 && sizeof(T) == 4 && !ROW && !PREC)
-            tile_run_v8<(PF + 1) / 2, NT>(tid, px, py, pz, tr, gc, acc);
+        if constexpr (V8 && !ROW && !PREC)
+            tile_run_v8<T, (PF + 1) / 2, NT>(tid, px, py, pz, tr, gc, acc);
         else
             tile_run<T, ROW, PF, false, NT, MODE_J2, PREC>(tid, p, kg, tab_addr, px, py, pz, tr, gc, mk, acc, rp,
                                                            row_stride);

@@ -142,7 +142,7 @@ cudaError_t launch_eval_impl(const EvalParams &p, int64_t nblocks, bool row, cud
 #endif
             j2_eval_kernel<T, false, QJ2_EVAL_PF, QJ2_EVAL_MINB, MODE, PREC><<<nb, TPB, 0, s>>>(p);
     }
-    else                                 // fp64: two groups in flight, 2 CTAs/SM
+    else                                 // fp64: two groups in flight, 2 CTAs/SM (256-bit loads: slower, spills)
         j2_eval_kernel<T, false, QJ2_EVAL64_PF, QJ2_EVAL64_MINB, MODE><<<nb, TPB, 0, s>>>(p);
     return cudaGetLastError();
 }
