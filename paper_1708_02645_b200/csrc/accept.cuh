@@ -65,6 +65,15 @@ template <> struct AVec<float> {
         return v;
     }
 };
+// 32-byte load / streaming store of two adjacent fp32 vectors (sm_100: LDG/STG.E.ENL2.256)
+__device__ __forceinline__ void ld8(const float4 *p, float4 &a, float4 &b) {
+    asm volatile("ld.global.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w) : "l"(p));
+}
+__device__ __forceinline__ void st8cs(float4 *p, const float4 &a, const float4 &b) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "l"(p), "f"(a.x), "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w) : "memory");
+}
 template <> struct AVec<double> {
     static __device__ __forceinline__ double2 ld(const double2 *p) {
         double2 v;
@@ -153,8 +162,10 @@ __device__ __forceinline__ void accept_terms_fast(T x, T y, T z, bool dead, cons
     dl[4] = (t[1][4] - t[0][4]) * (T(2) * invd);
 }
 
-// PREC: fp64 geometry (accept_terms) instead of the fp32 fast path.
-template <typename T, bool PREC>
+// PREC: fp64 geometry (accept_terms) instead of the fp32 fast path.  V8 (fp32, rows 32-byte
+// aligned): a thread's two vectors per iteration are adjacent and move with 256-bit loads and
+// stores.
+template <typename T, bool PREC, bool V8 = false>
 __global__ void __launch_bounds__(ATPB, sizeof(T) == 4 ? 2 : 1)
 j2_accept_kernel(const __grid_constant__ AcceptParams p) {
     using Tr = Traits<T>;
@@ -221,16 +232,37 @@ j2_accept_kernel(const __grid_constant__ AcceptParams p) {
         V bx[AVPT], by[AVPT], bz[AVPT], bs[AVPT][5];
 #pragma unroll
         for (int u = 0; u < AVPT; ++u) {
-            const int64_t li = t0 + ((int64_t)(it * AVPT + u) * ATPB + threadIdx.x) * VW;
+            const int64_t li = V8 ? t0 + (((int64_t)it * ATPB + threadIdx.x) * AVPT + u) * VW
+                                  : t0 + ((int64_t)(it * AVPT + u) * ATPB + threadIdx.x) * VW;
             live[u] = li < nl;
             vi[u] = li / VW;
             QJ2_DCHECK(!live[u] || (vi[u] + 1) * VW <= p.Np);
-            if (live[u]) {
-                bx[u] = AVec<T>::ld(vx + vi[u]);
-                by[u] = AVec<T>::ld(vy + vi[u]);
-                bz[u] = AVec<T>::ld(vz + vi[u]);
+        }
+        if constexpr (V8) {
+            static_assert(sizeof(T) == 4 && AVPT == 2, "V8: two fp32 vectors per thread");
+            if (live[1]) {                                 // both vectors: one 32-byte access per lane
+                ld8(vx + vi[0], bx[0], bx[1]);
+                ld8(vy + vi[0], by[0], by[1]);
+                ld8(vz + vi[0], bz[0], bz[1]);
 #pragma unroll
-                for (int c = 0; c < 5; ++c) bs[u][c] = AVec<T>::ld(vs[c] + vi[u]);
+                for (int c = 0; c < 5; ++c) ld8(vs[c] + vi[0], bs[0][c], bs[1][c]);
+            } else if (live[0]) {
+                bx[0] = AVec<T>::ld(vx + vi[0]);
+                by[0] = AVec<T>::ld(vy + vi[0]);
+                bz[0] = AVec<T>::ld(vz + vi[0]);
+#pragma unroll
+                for (int c = 0; c < 5; ++c) bs[0][c] = AVec<T>::ld(vs[c] + vi[0]);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < AVPT; ++u) {
+                if (live[u]) {
+                    bx[u] = AVec<T>::ld(vx + vi[u]);
+                    by[u] = AVec<T>::ld(vy + vi[u]);
+                    bz[u] = AVec<T>::ld(vz + vi[u]);
+#pragma unroll
+                    for (int c = 0; c < 5; ++c) bs[u][c] = AVec<T>::ld(vs[c] + vi[u]);
+                }
             }
         }
 #pragma unroll
@@ -259,14 +291,25 @@ j2_accept_kernel(const __grid_constant__ AcceptParams p) {
                     Tr::set(bs[u][c], e, s);
                 }
             }
+            if (!V8) {
 #pragma unroll
-            for (int c = 0; c < 5; ++c) __stcs(vs[c] + vi[u], bs[u][c]);
+                for (int c = 0; c < 5; ++c) __stcs(vs[c] + vi[u], bs[u][c]);
+            }
             if (has_k) {                                   // commit r'_k into Rsoa
                 const int e = (int)(kl - li0);
                 QJ2_DCHECK(e >= 0 && e < VW);
                 V nx = bx[u], ny = by[u], nz = bz[u];
                 Tr::set(nx, e, rn[0]); Tr::set(ny, e, rn[1]); Tr::set(nz, e, rn[2]);
                 vx[vi[u]] = nx; vy[vi[u]] = ny; vz[vi[u]] = nz;
+            }
+        }
+        if constexpr (V8) {
+            if (live[1]) {
+#pragma unroll
+                for (int c = 0; c < 5; ++c) st8cs(vs[c] + vi[0], bs[0][c], bs[1][c]);
+            } else if (live[0]) {
+#pragma unroll
+                for (int c = 0; c < 5; ++c) __stcs(vs[c] + vi[0], bs[0][c]);
             }
         }
     }
