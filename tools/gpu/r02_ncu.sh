@@ -3,7 +3,8 @@
 mkdir -p gpurun_out/ncu_r02
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/ncu_r02/build.log 2>&1
 if [ -z "$SKIP_LAUNCHES" ]; then
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/ncu_r02/launches_C3.csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed 5 steps/" --csv \
+  --log-file gpurun_out/ncu_r02/launches_C3.csv \
   python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "launches C3 rc $?"
 # N64S: the timed region only (its prepare() times 1536 per-move launches for context first)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed 3 steps/" --csv \
