@@ -131,7 +131,9 @@ qj2_status qj2_eval_workspace_size(int64_t W, int32_t P, int64_t N_local,
 /*   Np        padded lane length, Np >= N_local, Np % 4 == 0 (fp32) or      */
 /*             Np % 2 == 0 (fp64).                                           */
 /*   R         device [W][3][Np] dtype, SoA lanes x|y|z (PAPER:1290-1296,    */
-/*             Rsoa[3][Np]); coordinates in [0, L_d); 16-byte aligned.       */
+/*             Rsoa[3][Np]); coordinates in [0, L_d); 16-byte aligned (fp32  */
+/*             rows that start 32-byte aligned -- R so aligned, Np % 8 == 0  */
+/*             -- are read with 256-bit loads: same results, faster).        */
 /*   k         device [W] int32, active electron, global index < N_total.    */
 /*   P         trial positions per walker, 1 <= P <= QJ2_MAX_P.             */
 /*   r_trial   device [W][P][3] dtype, coordinates in [0, L_d).              */
