@@ -108,3 +108,35 @@ def test_j1_wide_ion_padding(q):
         assert np.all(np.isfinite(out))
         orc, absout = oracle.eval_j1(ions[:, :n_ions].astype(np.float64), start, rt.astype(np.float64), fn1)
         assert oracle.normalized_error_j1(out, orc, absout, fn1).max() <= 1e-5
+
+
+@pytest.mark.parametrize("N,W", [(250000, 2), (6144, 4096)])
+def test_eval_and_accept_16_byte_aligned_rows(q, N, W):
+    """Rows that start 16- but not 32-byte aligned take the 128-bit path of the
+    kernels that otherwise read 256 bits at a time (CTA kernel, compact warp
+    kernel, accept kernel): the same results as the oracle."""
+    L = qmcgen.cell_length(N)
+    Np = qmcgen.padded_size(N, 8)
+    R = qmcgen.positions(80 + N, np.arange(W), N, Np, L, np.float32)
+    k = qmcgen.make_k(80 + N, W, N)
+    rt = qmcgen.make_trials(80 + N, np.arange(W), k, N, L, np.float32)
+    fn = qmcgen.make_functor(80 + N, L)
+    big = torch.empty(R.size + 4, dtype=torch.float32, device="cuda")
+    Rd = big[4:].view(W, 3, Np)                       # 16 bytes past a 256-byte boundary
+    assert Rd.data_ptr() % 32 == 16
+    Rd.copy_(dev(R))
+    out = q.eval(Rd, dev(k), dev(rt), fn, N, N // 2).cpu().numpy()
+    sample = np.r_[0:2, W - 2:W] if W > 16 else np.arange(W)
+    orc, absout, _ = oracle.eval_j2(R[sample], k[sample], rt[sample], fn, N, N // 2, threads=THREADS)
+    assert oracle.normalized_error(out[sample], orc, absout, fn).max() <= 1e-5
+    if W <= 16:
+        rng = np.random.default_rng(81)
+        state = rng.normal(size=(W, 5, Np)).astype(np.float32)
+        bigs = torch.empty(state.size + 4, dtype=torch.float32, device="cuda")
+        Sd = bigs[4:].view(W, 5, Np)
+        Sd.copy_(dev(state))
+        acc = np.ones(W, np.int32)
+        q.accept(Rd, Sd, dev(k), dev(rt), dev(acc), q.eval(Rd, dev(k), dev(rt), fn, N, N // 2), fn, N, N // 2)
+        R2, S2, ab = oracle.accept(R, state, k, rt[:, 0], acc, fn, N, N // 2)
+        assert np.array_equal(Rd.cpu().numpy().astype(np.float64), R2)
+        assert oracle.normalized_error_state(Sd.cpu().numpy()[:, :, :N], S2[:, :, :N], ab[:, :, :N], fn).max() <= 1e-5
