@@ -159,7 +159,7 @@ def _j1_cases(n=20, seed=2027):
     for _ in range(n):
         S = int(rng.integers(1, 5))
         out.append(dict(n_ions=max(S, _log_uniform(rng, 1, 60000)), S=S, W=int(rng.integers(1, 9)),
-                        P=int(rng.integers(1, 4)), m=tuple(int(x) for x in rng.integers(4, 21, 4)),
+                        P=int(rng.integers(1, 4)), m=tuple(int(x) for x in rng.integers(4, 65, 4)),
                         rcut=tuple(float(x) for x in rng.uniform(0.2, 0.5, 4)), f64=bool(rng.random() < 0.4),
                         seed=int(rng.integers(2**31))))
     return out
