@@ -75,7 +75,8 @@ def test_state_init_j1_rows_vs_oracle(q):
         assert err <= 1e-5
 
 
-@pytest.mark.parametrize("N", [2, 33, 256, 300, 385, 512, 600, 640, 768, 1000, 1024])   # every tier, full and ragged
+@pytest.mark.parametrize("N", [2, 33, 256, 257, 300, 384, 385, 512, 513, 600, 640, 641, 768, 769, 1000, 1024])
+# every tier, full and ragged, and both sides of each tier boundary
 def test_sweep_one_sweep_vs_oracle(q, N):
     """One ordered sweep (N moves) in one launch from the from-scratch state."""
     W = 12
