@@ -76,7 +76,8 @@ def test_config_full(q, name):
 # Edge cases: tiny / ragged / tile boundaries / spin boundary / P groups
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-@pytest.mark.parametrize("N", [2, 3, 5, 17, 1023, 8191, 8192, 8193, 20001, 32769, 70001])
+@pytest.mark.parametrize("N", [2, 3, 5, 17, 1023, 2048, 2049, 4095, 4096, 4097, 8191, 8192, 8193, 20001, 32769, 70001,
+                               102401, 204801])   # and both sides of the mapping / tile boundaries
 def test_ragged_sizes(q, dtype, N):
     R, k, rt, fn, n_up = instance(N, 37, seed=100 + N, dtype=dtype)
     check(q, R, k, rt, fn, N, n_up, dtype)
