@@ -46,6 +46,12 @@ def test_bench_line_contract(config):
     assert r["bound"] in ("hbm", "alu", "tensor") and r["unit"] in ("GB/s", "TFLOP/s")
     assert 0 < r["frac"] < 2 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     assert r["traffic"] is None or r["traffic"] > 0
+    assert r["kernel_ms"] > 0 and r["kernel_ms_back_to_back"] > 0 and r["kernel_ms_source"]
+    if config is None:                           # a C3 step is the eval launch: its roofline from the timed region
+        assert r["kernel_ms_source"].startswith("timed region")
+        assert abs(r["kernel_ms"] - d["ms_per_step"]) <= 1e-6 * d["ms_per_step"]
+    else:                                        # the sweep: its issue fraction at the timed launch's acceptance
+        assert r["bound"] == "alu" and 0 < r["acceptance"] < 1 and 0 < r["issue"]["frac"] < 1.2
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] >= 5
